@@ -1,0 +1,183 @@
+"""Pins for oracle/ckks.py: big-integer CRT identities for rescale and key-switch (O11,
+O12), keygen error identity (O7), encrypt/decrypt accuracy (O8), homomorphic ops vs
+float64, bookkeeping errors (O9)."""
+import numpy as np
+import pytest
+
+from oracle import ckks, ring
+from oracle.params import make_params, params_from_depth
+from synth import random_residues
+
+
+def _ctx(n=64, bits=(60, 40, 40, 40, 60), seed=1):
+    return ckks.Context(make_params(n, list(bits))).keygen(seed)
+
+
+def _crt(residues, qs):
+    """Plain CRT with Python ints (independent of oracle.ckks.crt_lift_centered)."""
+    Q = 1
+    for q in qs:
+        Q *= q
+    x = 0
+    for r, q in zip(residues, qs):
+        Mi = Q // q
+        x += int(r) * Mi * pow(Mi, -1, q)
+    return x % Q, Q
+
+
+def _centered(x, m):
+    x %= m
+    return x - m if x > m // 2 else x
+
+
+def test_rescale_big_int_exact():
+    ctx = _ctx()
+    lvl = ctx.L
+    data = random_residues((2, 2, lvl + 1, ctx.n), ctx.q[: lvl + 1] * 4, seed=3)
+    ct = ckks.CtArray(data, lvl, 2.0 ** 80, ctx.key_id)
+    out = ctx.rescale(ct)
+    qs, ql = ctx.q[:lvl], ctx.q[lvl]
+    for c in range(2):
+        for k in range(2):
+            coef_in = ctx.intt(ct.data[c, k].copy(), list(range(lvl + 1)))
+            coef_out = ctx.intt(out.data[c, k].copy(), list(range(lvl)))
+            for j in range(ctx.n):
+                X, _ = _crt(coef_in[:, j], ctx.q[: lvl + 1])
+                want = (X - _centered(X, ql)) // ql
+                Qo = 1
+                for q in qs:
+                    Qo *= q
+                got, _ = _crt(coef_out[:, j], qs)
+                assert got == want % Qo
+    assert out.level == lvl - 1 and out.scale == 2.0 ** 80 / float(ql)
+
+
+def test_keyswitch_mod_down_big_int_exact():
+    ctx = _ctx()
+    lvl = 2
+    d2 = random_residues((lvl + 1, ctx.n), ctx.q[: lvl + 1], seed=4)
+    acc = ctx.keyswitch_acc(d2, lvl)
+    out = ctx.mod_down(acc, lvl)
+    mods = ctx.q[: lvl + 1] + [ctx.P]
+    idx = list(range(lvl + 1)) + [ctx.L + 1]
+    Q = 1
+    for q in ctx.q[: lvl + 1]:
+        Q *= q
+    for c in range(2):
+        A = ctx.intt(acc[c].copy(), idx)
+        O = ctx.intt(out[c].copy(), list(range(lvl + 1)))
+        for j in range(ctx.n):
+            X, _ = _crt(A[:, j], mods)
+            want = ((X - _centered(X, ctx.P)) // ctx.P) % Q
+            got, _ = _crt(O[:, j], ctx.q[: lvl + 1])
+            assert got == want
+
+
+def test_keyswitch_acc_is_digit_inner_product():
+    """acc over Q*P equals sum_j [d2]_{q_j} * rlk_j exactly (the digit decomposition)."""
+    ctx = _ctx()
+    lvl = 1
+    d2 = random_residues((lvl + 1, ctx.n), ctx.q[: lvl + 1], seed=5)
+    acc = ctx.keyswitch_acc(d2, lvl)
+    idx = list(range(lvl + 1)) + [ctx.L + 1]
+    a = ctx.intt(d2.copy(), list(range(lvl + 1)))
+    for c in range(2):
+        for ti, t in enumerate(idx):
+            m = ctx.moduli[t]
+            want = np.zeros(ctx.n, dtype=np.uint64)
+            for j in range(lvl + 1):
+                x = ctx.ntt(ring.reduce(a[j].copy(), m)[None], [t])[0]
+                want = ring.add(want, ring.mul(x, ctx.rlk[j, c, t], m), m)
+            assert np.array_equal(acc[c, ti], want)
+
+
+def test_keygen_error_identity():
+    ctx = _ctx(n=256)
+    all_idx = list(range(ctx.L + 2))
+    for j in range(ctx.L + 1):
+        for i in all_idx:
+            m = ctx.moduli[i]
+            v = ring.add(ctx.rlk[j, 0, i], ring.mul(ctx.rlk[j, 1, i], ctx.s_hat[i], m), m)
+            if i == j:
+                s2 = ring.mul(ctx.s_hat[i], ctx.s_hat[i], m)
+                v = ring.sub(v, ring.mul_scalar(s2, ctx.P % m, m), m)
+            e = ctx.intt(v[None].copy(), [i])[0]
+            ec = np.array([_centered(int(x), m) for x in e])
+            assert np.abs(ec).max() <= 21
+    for i in range(ctx.L + 1):
+        q = ctx.q[i]
+        v = ring.add(ctx.pk[0, i], ring.mul(ctx.pk[1, i], ctx.s_hat[i], q), q)
+        e = ctx.intt(v[None].copy(), [i])[0]
+        assert [_centered(int(x), q) for x in e] == ctx.pk_e.tolist()
+
+
+@pytest.fixture(scope="module")
+def c0ctx():
+    return ckks.Context(params_from_depth(2)).keygen(1)
+
+
+def test_encrypt_decrypt_accuracy(c0ctx):
+    z = np.random.default_rng(0).uniform(0, 1, (3, 4096))
+    ct = c0ctx.encrypt(z, enc_seed=2)
+    assert ct.data.shape == (3, 2, 3, 8192)
+    back = c0ctx.decrypt(ct, 4096)
+    assert np.max(np.abs(back - z)) < 1e-6
+
+
+def test_homomorphic_linear_ops(c0ctx):
+    rng = np.random.default_rng(1)
+    z1, z2 = rng.uniform(-1, 1, (2, 2, 4096))
+    a = c0ctx.encrypt(z1, 2, obj0=0)
+    b = c0ctx.encrypt(z2, 2, obj0=10)
+    s = c0ctx.decrypt(c0ctx.add(a, b), 4096)
+    assert np.max(np.abs(s - (z1 + z2))) < 1e-6
+    w = [0.3, -1.7]
+    m = c0ctx.rescale(c0ctx.mul_scalar(a, w, float(c0ctx.q[2])))
+    assert np.max(np.abs(c0ctx.decrypt(m, 4096) - z1 * np.array(w)[:, None])) < 1e-6
+    p = c0ctx.add_scalar(a, [0.5, -2.0])
+    assert np.max(np.abs(c0ctx.decrypt(p, 4096) - (z1 + np.array([0.5, -2.0])[:, None]))) < 1e-6
+
+
+def test_mul_relin_rescale(c0ctx):
+    rng = np.random.default_rng(2)
+    z1, z2 = rng.uniform(-1, 1, (2, 1, 4096))
+    a = c0ctx.encrypt(z1, 2, obj0=0)
+    b = c0ctx.encrypt(z2, 2, obj0=1)
+    d, lvl, sc = c0ctx.tensor(a, b)
+    # decrypt the 3-component ciphertext with (1, s, s^2) before relinearising
+    q0 = c0ctx.q[0]
+    m3 = ring.add(ring.add(d[0, 0, 0], ring.mul(d[0, 1, 0], c0ctx.s_hat[0], q0), q0),
+                  ring.mul(d[0, 2, 0], ring.mul(c0ctx.s_hat[0], c0ctx.s_hat[0], q0), q0), q0)
+    r = c0ctx.mul_relin(a, b)
+    m2 = ring.add(r.data[0, 0, 0], ring.mul(r.data[0, 1, 0], c0ctx.s_hat[0], q0), q0)
+    diff = ring.sub(c0ctx.intt(m3[None].copy(), [0])[0], c0ctx.intt(m2[None].copy(), [0])[0], q0)
+    dc = np.array([_centered(int(x), q0) for x in diff])
+    # relinearisation noise bound: (l+1) N 21 max q / P + N, in integer units
+    bound = (lvl + 1) * c0ctx.n * 21 * max(c0ctx.q) / c0ctx.P + c0ctx.n
+    assert np.abs(dc).max() <= bound
+    out = c0ctx.decrypt(c0ctx.rescale(r), 4096)
+    assert np.max(np.abs(out - z1 * z2)) < 1e-5
+
+
+def test_bookkeeping_errors(c0ctx):
+    z = np.zeros((1, 16))
+    a = c0ctx.encrypt(z, 2)
+    x = a
+    for _ in range(c0ctx.L):            # depth sufficiency: exactly L rescales
+        x = c0ctx.rescale(c0ctx.mul_scalar(x, [1.0], float(c0ctx.q[x.level])))
+    with pytest.raises(ckks.LevelError):
+        c0ctx.rescale(x)
+    other = ckks.Context(params_from_depth(2)).keygen(7)
+    with pytest.raises(ckks.KeyMismatch):
+        other.decrypt(a, 16)
+    b = c0ctx.mul_scalar(a, [1.0], 3.0)
+    with pytest.raises(ckks.ScaleError):
+        c0ctx.add(a, b)
+    with pytest.raises(ckks.CapacityError):
+        c0ctx.encrypt(np.zeros((1, 4097)), 2)
+    with pytest.raises(ckks.ShapeMismatch):
+        c0ctx.add(a, c0ctx.encrypt(np.zeros((2, 16)), 2))
+    # auto mod-drop: adding a lower-level operand drops the higher one
+    lo = c0ctx.rescale(c0ctx.mul_scalar(a, [1.0], float(c0ctx.q[2])))
+    s = c0ctx.add(lo, a)
+    assert s.level == 1
