@@ -1,0 +1,308 @@
+"""Benchmark: encrypted images/s of the C1 CNN (BASELINE.json configs[1]) on B200.
+
+One step = server-side homomorphic inference of one 8192-image batch (784 pixel
+ciphertexts at level 4 resident in HBM -> CC 5x4x4/4 -> sigma_a -> dense 245->10), i.e.
+every row of SURVEY §8(a) a2-a10.  `value` is device-timed (CUDA events on the library's
+stream, barrier + synchronize on both sides, max over ranks); `e2e` repeats the step
+through the public API with the inputs copied from pinned host memory and the 10 output
+ciphertexts copied back inside the timed region.  N>1: each rank runs its own batch
+(weak scaling, independent batches -- the path needs no collective for them).
+
+`--impl reference` times the oracle (oracle/, the plain CPU implementation) on a bounded
+sample of the same workload on the host cores and prints the same JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "encrypted images/s (CKKS N=2^14 CNN)"
+UNIT = "images/s"
+BATCH = 8192
+WINDOWS = 49
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-windows", type=int, default=8, help="oracle sample size (windows of 49)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- oracle sample
+def oracle_sample_seconds(windows: int, seed_data: int = 2110):
+    """Oracle (CPU) server-side inference restricted to `windows` of the 49 CC windows:
+    CC for those windows (5 filters each), sigma_a on those 5*windows ciphertexts, dense
+    partial sums over them into the 10 outputs, final rescale + bias.  Work scales
+    linearly in windows (the final 10-ciphertext rescale is <0.1%)."""
+    from oracle import layers, networks
+    from oracle.ckks import CtArray
+    from synth import c1_images, c1_slots, c1_weights
+
+    K, kb, W, b = c1_weights()
+    imgs = c1_images(BATCH, seed_data)
+    slots = c1_slots(imgs)
+    ctx = networks.c1_context(1)
+    wins = list(range(windows))
+    pix = sorted({(4 * (w // 7) + u) * 28 + 4 * (w % 7) + v for w in wins for u in range(4) for v in range(4)})
+    polys = np.stack([ctx.encode(slots[p]) for p in pix])
+    xs = ctx.encrypt_poly(polys, 2, 0, ctx.p.scale)
+    full = np.zeros((784, 2, 5, ctx.n), dtype=np.uint64)
+    full[pix] = xs.data
+    x = CtArray(full, 4, xs.scale, xs.key_id)
+    t0 = time.perf_counter()
+    # CC restricted to the sampled windows
+    cc_parts = []
+    for f in range(5):
+        for w in wins:
+            r, c = divmod(w, 7)
+            idx = [(4 * r + u) * 28 + 4 * c + v for u in range(4) for v in range(4)]
+            cc_parts.append(layers.weighted_sum(ctx, x, idx, [K[f, u, v] for u in range(4) for v in range(4)],
+                                                float(ctx.q[4])))
+    acc = CtArray(np.stack(cc_parts), 4, x.scale * float(ctx.q[4]), x.key_id)
+    cc = ctx.add_scalar(ctx.rescale(acc), np.repeat(kb, len(wins)))
+    act = layers.poly_activation(ctx, cc, networks.SIGMA_A)
+    cols = [f * WINDOWS + w for f in range(5) for w in wins]
+    out = layers.dense(ctx, act, W[:, cols], b)
+    t = time.perf_counter() - t0
+    assert out.count == 10
+    return t
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    per_step = []
+    for _ in range(a.warmup if a.warmup < 1 else 0):
+        pass
+    for _ in range(a.steps):
+        t = oracle_sample_seconds(a.cpu_windows)
+        per_step.append(t * WINDOWS / a.cpu_windows)
+    t_full = float(np.mean(per_step))
+    value = BATCH / t_full
+    sample = f"{a.cpu_windows} of 49 CC windows per step (CC+sigma_a+dense partial over them), " \
+             f"extrapolated x{WINDOWS / a.cpu_windows:.3g} to one 8192-image batch"
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": t_full * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": "C1 Fashion-MNIST-shaped encrypted CNN, CKKS N=2^14 {60,40,40,40,40|60}, "
+                                   "batch 8192 in slots", "global_batch": BATCH * a.gpus},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 7]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[3 + k].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- algorithmic work
+def ks_mac_modmuls(cnt: int, l: int, n: int) -> float:
+    """Algorithmic 64-bit modular multiplications of one k_relin_ks_mac launch:
+    per ciphertext (l+1)^2 forward NTTs of (N/2) log N butterflies, (l+1) N direct d2
+    products and 2 (l+1)(l+2) N key products."""
+    logn = n.bit_length() - 1
+    w_ntt = (n // 2) * logn
+    return cnt * ((l + 1) ** 2 * w_ntt + (l + 1) * n + 2 * (l + 1) * (l + 2) * n)
+
+
+def ks_mac_bytes(cnt: int, l: int, n: int) -> float:
+    """Algorithmic HBM bytes of one k_relin_ks_mac launch: read (l+1) coefficient limbs and
+    (l+1) d2 operand limbs x2 (a1, b1), write 2 (l+2) accumulator limbs (rlk is L2-resident)."""
+    return cnt * 8 * n * ((l + 1) + 2 * (l + 1) + 2 * (l + 2))
+
+
+# ----------------------------------------------------------------------------- ours
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2110_13638_b200 import edl
+    from paper_2110_13638_b200.networks import C1Net
+    from synth import c1_images, c1_slots, c1_weights
+
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
+    ctx = edl.Context(edl.params_from_depth(4), device=local, stream=stream).keygen(1)
+    K, kb, W, b = c1_weights()
+    imgs = c1_images(BATCH, 2110 + rank)           # each rank: its own batch (weak scaling)
+    polys = torch.from_numpy(ctx.encode(c1_slots(imgs))).to(f"cuda:{local}")
+    x = ctx.encrypt_poly(polys, scale=float(2 ** 40), enc_seed=2, obj0=0)
+    del polys
+    net = C1Net(ctx, K, kb, W, b)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(max(a.warmup, 0)):
+        net.forward(x)
+    stream.synchronize()
+    barrier()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    ctx.profile(True)
+    l0 = ctx.launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stream.synchronize()
+    barrier()
+    e0.record(stream)
+    for _ in range(a.steps):
+        out = net.forward(x)["out"]
+    e1.record(stream)
+    stream.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    launches = ctx.launches - l0
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    clk = clocks.stop()
+    t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_step = ms_max / a.steps
+    value = world * BATCH * a.steps / (ms_max / 1e3)
+
+    # ---- e2e: same step through the public API with host buffers
+    e2e = None
+    if not a.no_e2e:
+        host_in = torch.empty(x.tensor.numel(), dtype=torch.int64, pin_memory=True)
+        host_in.copy_(x.tensor.cpu())
+        dev_in = edl.CtArray(torch.empty_like(x.tensor), x.count, x.level, x.scale, x.key_id)
+        out_words = out.tensor.numel()
+        host_out = torch.empty(out_words, dtype=torch.int64, pin_memory=True)
+        for _ in range(1):
+            dev_in.tensor.copy_(host_in, non_blocking=True)
+            host_out.copy_(net.forward(dev_in)["out"].tensor, non_blocking=True)
+        stream.synchronize()
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(a.e2e_steps):
+            dev_in.tensor.copy_(host_in, non_blocking=True)
+            host_out.copy_(net.forward(dev_in)["out"].tensor, non_blocking=True)
+        f1.record(stream)
+        stream.synchronize()
+        barrier()
+        te = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=f"cuda:{local}")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * BATCH * a.e2e_steps / (float(te.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(host_in.numel() * 8), "d2h_bytes_per_step": int(out_words * 8)}
+
+    # ---- roofline of the dominant kernel (largest share of the timed region)
+    n = ctx.n
+    dom = max(prof.items(), key=lambda kv: kv[1][0]) if prof else ("none", (0.0, 0))
+    roof = None
+    peak_modmul = ctx.modmul_peak()
+    if "k_relin_ks_mac" in prof:
+        ms_ks, cnt_ks = prof["k_relin_ks_mac"]
+        per_step = [(245, 3), (245, 2)]
+        work = sum(ks_mac_modmuls(c, l, n) for c, l in per_step) * a.steps
+        byts = sum(ks_mac_bytes(c, l, n) for c, l in per_step) * a.steps
+        achieved = work / (ms_ks / 1e3)
+        roof = {"kernel": "k_relin_ks_mac", "bound": "alu", "unit": "Tmodmul/s",
+                "achieved": achieved / 1e12, "peak": peak_modmul / 1e12, "frac": achieved / peak_modmul,
+                "traffic": None, "peak_kind": "measured (edl_modmul_peak register-only Shoup modmul kernel)",
+                "share_of_step": ms_ks / ms, "avg_launch_ms": ms_ks / cnt_ks,
+                "hbm_gbs": byts / (ms_ks / 1e3) / 1e9}
+    kernels = {k: {"ms_per_step": v[0] / a.steps, "launches_per_step": v[1] / a.steps} for k, v in prof.items()}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        ts = oracle_sample_seconds(a.cpu_windows)
+        v = BATCH / (ts * WINDOWS / a.cpu_windows)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{a.cpu_windows} of 49 CC windows of one 8192-image batch, extrapolated x"
+                         f"{WINDOWS / a.cpu_windows:.3g}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+                "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+                "config": {"workload": "C1 Fashion-MNIST-shaped encrypted CNN, CKKS N=2^14 {60,40,40,40,40|60}, "
+                                       "batch 8192 in slots (784 pixel ciphertexts), CC 5x4x4/4 -> sigma_a -> "
+                                       "dense 245->10", "global_batch": BATCH * world,
+                           "parallelism": f"batch-replica x{world}", "l2": "inputs 1.03 GB > L2 (no flush)"},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk, "dominant_kernel": dom[0], "kernels": kernels}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    a = _args()
+    if a.impl == "reference":
+        return run_reference(a)
+    return run_ours(a)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

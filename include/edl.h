@@ -1,0 +1,189 @@
+/*
+ * edl.h -- C-ABI of the B200-native hot path of arXiv 2110.13638 (EDLaaS: "Fully
+ * Homomorphic Encryption Over Neural Network Graphs").
+ *
+ * What crosses this boundary: homomorphic forward inference of the
+ * paper's node-centric network over RNS-CKKS ciphertexts -- cross-correlation and
+ * dense layers as ciphertext x plaintext multiply-accumulate, the
+ * polynomial sigmoid as ciphertext x ciphertext multiply with relinearisation
+ * and rescale between levels -- plus the
+ * client-side keygen / encode / encrypt / decrypt the paper delegates to MS-SEAL
+ * (PAPER.md:85).  Every step runs in the library's sm_100a kernels; there is no CPU
+ * fallback.
+ *
+ * Conventions:
+ *  - A ciphertext array (edl_cts) is `count` ciphertexts at one level `level`, stored
+ *    contiguously in DEVICE memory as uint64 [count][2][level+1][N], NTT domain (the
+ *    bit-reversed evaluation order of SURVEY O3), every residue canonical in [0, q_i).
+ *    The caller (e.g. torch) allocates it: edl_cts_bytes(count, level, log_n) bytes.
+ *  - `scale` is the CKKS scale (double), `key_id` identifies the secret key.
+ *  - The library owns keys, twiddle tables and scratch inside edl_ctx.
+ *  - All device work is enqueued on the context's stream (edl_ctx_create / set_stream)
+ *    and is asynchronous, except calls that take or return HOST buffers (edl_encode,
+ *    edl_encrypt, edl_decrypt*, edl_keygen), which synchronise the stream.
+ *  - Errors are synchronous status codes from argument validation (below); CUDA
+ *    launch/runtime errors surface as EDL_ERR_CUDA at the next call that checks.
+ *    edl_last_error() returns a message for the last failure on that context.
+ *  - `out` buffers must not alias inputs unless the function says so.
+ */
+#ifndef EDL_H
+#define EDL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t edl_status;
+
+enum {
+    EDL_OK = 0,
+    EDL_ERR_ARG = -1,         /* bad argument / unsupported configuration            */
+    EDL_ERR_LEVEL = -2,       /* LevelExhausted: no prime left to rescale by */
+    EDL_ERR_SCALE = -3,       /* operand scales differ by more than 2^-30 relative    */
+    EDL_ERR_KEY = -4,         /* KeyMismatch: operands under different keys */
+    EDL_ERR_SHAPE = -5,       /* ShapeMismatch: counts / layer shapes disagree         */
+    EDL_ERR_CAPACITY = -6,    /* more values than N/2 slots              */
+    EDL_ERR_CUDA = -7,        /* CUDA runtime error                                    */
+    EDL_ERR_NOKEY = -8        /* operation needs keys: call edl_keygen first           */
+};
+
+#define EDL_MAX_PRIMES 32
+
+/* CKKS parameter set.  bits[] is the full coefficient-modulus chain of Alg. 8
+ * INCLUDING the special prime as its last entry (reading R1);
+ * q[0..n_data-1] are the data primes, p_special the key-switching prime (rule O2:
+ * largest unused prime below 2^bits with p = 1 mod 2N), psi[k] the minimal
+ * primitive 2N-th root of unity mod q[k] (psi[n_data] is P's). */
+typedef struct {
+    int32_t log_n;
+    int32_t n_data;               /* number of data primes = L+1 */
+    int32_t n_bits;               /* entries in bits[] = n_data + 1 */
+    int32_t scale_bits;
+    int32_t bits[EDL_MAX_PRIMES + 1];
+    uint64_t q[EDL_MAX_PRIMES];
+    uint64_t p_special;
+    uint64_t psi[EDL_MAX_PRIMES + 1];
+} edl_params;
+
+typedef struct edl_ctx edl_ctx;
+
+typedef struct {
+    uint64_t* data;      /* device pointer, [count][2][level+1][N] uint64 */
+    int64_t count;
+    int32_t level;
+    int32_t reserved;
+    double scale;
+    uint64_t key_id;
+} edl_cts;
+
+/* Alg. 8 "parameterise(c, s, p)" followed by prime rule O2 and root
+ * rule O3.  depth = c >= 0, scale_bits = s (default 40), special_mult = p (default 1.5).
+ * Errors: EDL_ERR_ARG if depth < 0 or the chain exceeds EDL_MAX_PRIMES. */
+edl_status edl_params_from_depth(int32_t depth, int32_t scale_bits, double special_mult, edl_params* out);
+
+/* Explicit chain (microbench C2): bits[0..n_bits-1], last entry = special prime. */
+edl_status edl_params_from_bits(int32_t log_n, const int32_t* bits, int32_t n_bits, int32_t scale_bits,
+                                edl_params* out);
+
+/* Bytes of a ciphertext array: 2 * (level+1) * 2^log_n * 8 * count. */
+size_t edl_cts_bytes(int64_t count, int32_t level, int32_t log_n);
+
+/* Create a context on CUDA `device`, enqueueing on `cuda_stream` (a cudaStream_t; NULL =
+ * legacy default stream).  Uploads twiddle tables.  log_n must be in [10, 14]. */
+edl_status edl_ctx_create(const edl_params* params, int32_t device, void* cuda_stream, edl_ctx** out);
+void edl_ctx_destroy(edl_ctx* ctx);
+edl_status edl_ctx_set_stream(edl_ctx* ctx, void* cuda_stream);
+const char* edl_last_error(const edl_ctx* ctx);
+/* Number of kernels the library launched on this context since creation. */
+int64_t edl_launch_count(const edl_ctx* ctx);
+/* Per-launch CUDA-event timing on the context stream (enable != 0), resetting records. */
+edl_status edl_profile(edl_ctx* ctx, int32_t enable);
+/* Aggregate recorded launches by kernel name: writes up to max_entries rows of total
+ * milliseconds (ms) and launch counts (counts); names are '\n'-separated into `names`.
+ * Synchronises the stream.  Returns the number of rows (>= 0) or an error status. */
+int32_t edl_profile_read(edl_ctx* ctx, char* names, size_t names_len, double* ms, int64_t* counts,
+                         int32_t max_entries);
+
+/* O7 key generation from Philox4x32-10(seed): secret s (ternary), public key over
+ * q_0..q_L, relinearisation key over q_0..q_L, P.  key_id := seed.  Synchronises. */
+edl_status edl_keygen(edl_ctx* ctx, uint64_t seed);
+
+/* O5 encode on the host: slots [n_vec][n_slots] doubles -> int64 coefficient polys
+ * poly_out [n_vec][N] (host), m_k = rint(scale * u_k).  EDL_ERR_CAPACITY if
+ * n_slots > N/2.  Unused slots are zero. */
+edl_status edl_encode(edl_ctx* ctx, const double* slots, int64_t n_vec, int64_t n_slots, double scale,
+                      int64_t* poly_out);
+
+/* O8 public-key encryption of integer polys (DEVICE pointer int64 [n_vec][N]) at
+ * `level` with scale `scale`; ciphertext c uses Philox object id obj0 + c.  out->data
+ * must hold edl_cts_bytes(n_vec, level); out's metadata is filled in. */
+edl_status edl_encrypt_poly(edl_ctx* ctx, const int64_t* poly_dev, int64_t n_vec, int32_t level, double scale,
+                            uint64_t enc_seed, uint32_t obj0, edl_cts* out);
+
+/* Host convenience: encode (host) + copy + encrypt at the top level L, scale 2^scale_bits. */
+edl_status edl_encrypt(edl_ctx* ctx, const double* slots, int64_t n_vec, int64_t n_slots, uint64_t enc_seed,
+                       uint32_t obj0, edl_cts* out);
+
+/* Decrypt + centered CRT lift: poly_out [count][N] int64 (host).  Valid while the
+ * decrypted coefficients satisfy |m| < 2^62.  Synchronises. */
+edl_status edl_decrypt_poly(edl_ctx* ctx, const edl_cts* in, int64_t* poly_out);
+/* Decrypt + decode: slots_out [count][n_slots] doubles (host).  Synchronises. */
+edl_status edl_decrypt(edl_ctx* ctx, const edl_cts* in, double* slots_out, int64_t n_slots);
+
+/* ---- ciphertext arithmetic (meta-object rules) ---- */
+/* out = a + b; the higher-level operand is mod-dropped to the lower level first.
+ * Scales must agree within 2^-30 relative; out takes a's scale. */
+edl_status edl_ct_add(edl_ctx* ctx, const edl_cts* a, const edl_cts* b, edl_cts* out);
+/* out_c = a_c * rint(w[c] * pt_scale) (w: host doubles [count]); no rescale; scale *= pt_scale. */
+edl_status edl_ct_pt_mul(edl_ctx* ctx, const edl_cts* a, const double* w, double pt_scale, edl_cts* out);
+/* out_c = a_c + rint(c[c] * a.scale) on the constant coefficient (host doubles [count]). */
+edl_status edl_ct_pt_add(edl_ctx* ctx, const edl_cts* a, const double* c, edl_cts* out);
+/* Tensor + relinearisation (key-switch with the special prime, O11); never rescales. */
+edl_status edl_ct_ct_mul_relin(edl_ctx* ctx, const edl_cts* a, const edl_cts* b, edl_cts* out);
+/* Divide by the last prime with rounding (O12).  EDL_ERR_LEVEL at level 0. */
+edl_status edl_rescale(edl_ctx* ctx, const edl_cts* in, edl_cts* out);
+/* Keep limbs 0..level (scale unchanged).  out may alias in only if level == in->level. */
+edl_status edl_mod_drop(edl_ctx* ctx, const edl_cts* in, int32_t level, edl_cts* out);
+
+/* ---- layer nodes (O13) ---- */
+/* Biased cross-correlation (Eq. cnn) in the batch-in-slots layout:
+ * x = H*W ciphertexts (pixel-major), k = host doubles [F][kh][kw], bias [F] (or NULL).
+ * out = F*Ho*Wo ciphertexts ([f][r][c] order) at level x.level-1:
+ * Rescale(sum_taps x * const(k, q_l)) + const(b). */
+edl_status edl_cross_correlate(edl_ctx* ctx, const edl_cts* x, int32_t H, int32_t W, const double* k, int32_t F,
+                               int32_t kh, int32_t kw, int32_t stride, const double* bias, edl_cts* out);
+/* Polynomial activation: coeffs c_0..c_degree.  Supported schedules: degree 3 with
+ * c_2 = 0 (sigma_a = 0.5 + 0.197x - 0.004x^3; 2 levels) and degree 2 with
+ * (0, 0, 1) (x^2; 1 level).  Others: EDL_ERR_ARG. */
+edl_status edl_poly_activation(edl_ctx* ctx, const edl_cts* x, const double* coeffs, int32_t degree, edl_cts* out);
+/* Dense: out_o = Rescale(sum_k x_k * const(Wt[o][k], q_l)) + const(b_o).
+ * Wt host doubles [O][K] (K = x->count), b [O] or NULL.  defer_rescale != 0 returns the
+ * un-rescaled accumulators (level x.level, for the C4 NCCL combine), ignoring b. */
+edl_status edl_dense(edl_ctx* ctx, const edl_cts* x, const double* Wt, const double* b, int32_t O,
+                     int32_t defer_rescale, edl_cts* out);
+/* Finish a deferred dense after the rank partials were summed as uint64 (north_star's
+ * NCCL uint64 allreduce): in place x mod q_i (O15). */
+edl_status edl_mod_reduce(edl_ctx* ctx, edl_cts* inout);
+/* Rescale + bias of combined dense accumulators (b host doubles [count] or NULL). */
+edl_status edl_dense_finish(edl_ctx* ctx, const edl_cts* acc, const double* b, edl_cts* out);
+
+/* ---- microbench / test entry points ---- */
+/* In-place forward (inverse != 0: inverse) NTT of n_polys * (level+1) limbs laid out
+ * [n_polys][level+1][N] (device); limb j uses q_j (j == n_data means P). */
+edl_status edl_ntt(edl_ctx* ctx, uint64_t* limbs, int64_t n_polys, int32_t level, int32_t inverse);
+/* Raw Philox4x32-10 words for host counters ctr[n][4] with key (seed lo, seed hi). */
+edl_status edl_philox(edl_ctx* ctx, uint64_t seed, const uint32_t* ctr_host, int64_t n, uint32_t* out_host);
+/* Integer-pipe ceiling: lazy Shoup 64-bit modular multiplications per second measured
+ * by a register-only kernel on all SMs (the "alu" roofline peak). */
+edl_status edl_modmul_peak(edl_ctx* ctx, int32_t iters, double* modmul_per_s);
+/* Copy the secret key s_hat [L+2][N], public key [2][L+1][N] or rlk [L+1][2][L+2][N]
+ * to host (which: 0, 1, 2).  For parity tests. */
+edl_status edl_export_key(edl_ctx* ctx, int32_t which, uint64_t* host_out, size_t words);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EDL_H */

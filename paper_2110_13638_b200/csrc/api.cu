@@ -1,0 +1,807 @@
+// api.cu -- the C-ABI (include/edl.h): argument validation, CKKS level/scale
+// bookkeeping (meta-object rules), layer schedules and kernel
+// orchestration on the context's stream.  No arithmetic on ciphertexts happens here:
+// every residue is produced by the sm_100a kernels in *.cu.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/edl.h"
+#include "host_math.h"
+#include "kernels.cuh"
+
+using namespace edl;
+
+struct edl_ctx {
+    edl_params prm;
+    int logn = 0;
+    int64_t N = 0;
+    int L = 0;              // top data level
+    int device = 0;
+    cudaStream_t st = nullptr;
+    std::vector<ModInfo> h_mods;
+    ModInfo* d_mods = nullptr;
+    ChainConsts* h_cc = nullptr;
+    ChainConsts* d_cc = nullptr;
+    uint64_t* d_tw = nullptr;
+    uint64_t* d_s = nullptr;
+    uint64_t* d_pk = nullptr;
+    uint64_t* d_rlk = nullptr;
+    uint64_t* d_rlk_s = nullptr;
+    bool has_key = false;
+    uint64_t key_id = 0;
+    uint64_t* d_scratch = nullptr;
+    size_t scratch_words = 0;
+    uint8_t* h_pin = nullptr;
+    uint8_t* d_const = nullptr;
+    size_t const_cap = 0, const_off = 0;
+    std::string err;
+    mutable Prof prof;
+
+    Dev dev() const {
+        Dev d;
+        d.mods = d_mods;
+        d.cc = d_cc;
+        d.logn = logn;
+        d.L = L;
+        d.st = st;
+        d.prof = &prof;
+        return d;
+    }
+    uint64_t modulus(int idx) const { return idx <= L ? prm.q[idx] : prm.p_special; }
+};
+
+namespace edl {
+cudaEvent_t Prof::ev() {
+    if (used == pool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        pool.push_back(e);
+    }
+    return pool[used++];
+}
+void Prof::begin(const char* name, cudaStream_t st) {
+    launches++;
+    if (!on) return;
+    Rec r;
+    r.name = name;
+    r.a = ev();
+    r.b = ev();
+    cudaEventRecord(r.a, st);
+    recs.push_back(r);
+}
+void Prof::end(cudaStream_t st) {
+    if (!on || recs.empty()) return;
+    cudaEventRecord(recs.back().b, st);
+}
+void Prof::reset() {
+    recs.clear();
+    used = 0;
+}
+Prof::~Prof() {
+    for (auto e : pool) cudaEventDestroy(e);
+}
+}  // namespace edl
+
+namespace {
+
+edl_status fail(edl_ctx* c, edl_status code, const char* msg) {
+    if (c) c->err = msg;
+    return code;
+}
+
+edl_status cuda_check(edl_ctx* c, const char* where) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        if (c) c->err = std::string(where) + ": " + cudaGetErrorString(e);
+        return EDL_ERR_CUDA;
+    }
+    return EDL_OK;
+}
+
+// Grow-only scratch; growing synchronises the stream so in-flight kernels finish first.
+uint64_t* scratch(edl_ctx* c, size_t words) {
+    if (words > c->scratch_words) {
+        cudaStreamSynchronize(c->st);
+        if (c->d_scratch) cudaFree(c->d_scratch);
+        size_t w = words + words / 4;
+        if (cudaMalloc(&c->d_scratch, w * 8) != cudaSuccess) {
+            c->d_scratch = nullptr;
+            c->scratch_words = 0;
+            return nullptr;
+        }
+        c->scratch_words = w;
+    }
+    return c->d_scratch;
+}
+
+// Small constant tables (encoded weights): staged through a pinned ring, copied on
+// the stream.  Wrapping synchronises the stream, so a slot is never overwritten while
+// an earlier copy or kernel may still read it.
+template <class T>
+const T* upload(edl_ctx* c, const std::vector<T>& v) {
+    const size_t bytes = (v.size() * sizeof(T) + 255) & ~size_t(255);
+    if (bytes > c->const_cap) return nullptr;
+    if (c->const_off + bytes > c->const_cap) {
+        cudaStreamSynchronize(c->st);
+        c->const_off = 0;
+    }
+    uint8_t* h = c->h_pin + c->const_off;
+    uint8_t* d = c->d_const + c->const_off;
+    std::memcpy(h, v.data(), v.size() * sizeof(T));
+    cudaMemcpyAsync(d, h, v.size() * sizeof(T), cudaMemcpyHostToDevice, c->st);
+    c->const_off += bytes;
+    return reinterpret_cast<const T*>(d);
+}
+
+bool scales_match(double a, double b) { return std::fabs(a - b) <= std::ldexp(1.0, -30) * std::fmax(a, b); }
+
+// O10: a constant encodes to rint(value * scale) (one IEEE multiply, round-half-even).
+int64_t const_int(double value, double scale) { return (int64_t)std::nearbyint(value * scale); }
+
+uint64_t signed_mod(int64_t v, uint64_t q) {
+    __int128 r = (__int128)v % (__int128)q;
+    if (r < 0) r += q;
+    return (uint64_t)r;
+}
+
+size_t ct_words(const edl_ctx* c, int64_t cnt, int l) { return (size_t)cnt * 2 * (l + 1) * (size_t)c->N; }
+
+edl_status check_ct(edl_ctx* c, const edl_cts* a) {
+    if (!a || (!a->data && a->count > 0)) return fail(c, EDL_ERR_ARG, "null ciphertext array");
+    if (a->count < 0) return fail(c, EDL_ERR_ARG, "negative count");
+    if (a->level < 0 || a->level > c->L) return fail(c, EDL_ERR_ARG, "level out of range");
+    if (c->has_key && a->key_id != c->key_id) return fail(c, EDL_ERR_KEY, "KeyMismatch: ciphertext key differs");
+    return EDL_OK;
+}
+
+void set_meta(edl_cts* out, int64_t count, int level, double scale, uint64_t key) {
+    out->count = count;
+    out->level = level;
+    out->scale = scale;
+    out->key_id = key;
+}
+
+// Scalar constants (per ciphertext) -> Shoup pairs [cnt][l+1]
+std::vector<ulonglong2> shoup_consts(const edl_ctx* c, const std::vector<int64_t>& ints, int l) {
+    std::vector<ulonglong2> w(ints.size() * (l + 1));
+    for (size_t k = 0; k < ints.size(); k++)
+        for (int i = 0; i <= l; i++) {
+            const uint64_t q = c->prm.q[i];
+            const uint64_t r = signed_mod(ints[k], q);
+            w[k * (l + 1) + i] = make_ulonglong2(r, host::shoup_companion(r, q));
+        }
+    return w;
+}
+
+std::vector<uint64_t> residues(const edl_ctx* c, const std::vector<int64_t>& ints, int nl) {
+    std::vector<uint64_t> r(ints.size() * nl);
+    for (size_t k = 0; k < ints.size(); k++)
+        for (int i = 0; i < nl; i++) r[k * nl + i] = signed_mod(ints[k], c->prm.q[i]);
+    return r;
+}
+
+// ct x scalar at pt_scale, then rescale (fused: 2 launches).  out level l-1.
+void scalar_rescale(edl_ctx* c, const uint64_t* y, int64_t cnt, int l, const ulonglong2* w, uint64_t* r,
+                    uint64_t* out) {
+    Dev d = c->dev();
+    launch_rescale_intt(d, y, cnt, l, w, r);
+    launch_rescale_ntt(d, y, cnt, l, w, r, nullptr, out);
+}
+
+}  // namespace
+
+extern "C" {
+
+edl_status edl_params_from_bits(int32_t log_n, const int32_t* bits, int32_t n_bits, int32_t scale_bits,
+                                edl_params* out) {
+    if (!out || !bits || n_bits < 2 || n_bits > EDL_MAX_PRIMES + 1 || log_n < 1 || log_n > 17) return EDL_ERR_ARG;
+    std::memset(out, 0, sizeof(*out));
+    out->log_n = log_n;
+    out->n_bits = n_bits;
+    out->n_data = n_bits - 1;
+    out->scale_bits = scale_bits;
+    std::vector<int> b(bits, bits + n_bits);
+    std::vector<uint64_t> primes(n_bits);
+    if (!host::select_primes(b.data(), n_bits, log_n, primes.data())) return EDL_ERR_ARG;
+    for (int k = 0; k < n_bits; k++) out->bits[k] = bits[k];
+    for (int k = 0; k < n_bits - 1; k++) out->q[k] = primes[k];
+    out->p_special = primes[n_bits - 1];
+    for (int k = 0; k < n_bits; k++) out->psi[k] = host::minimal_psi(primes[k], log_n);
+    return EDL_OK;
+}
+
+edl_status edl_params_from_depth(int32_t depth, int32_t scale_bits, double special_mult, edl_params* out) {
+    if (depth < 0 || depth + 2 > EDL_MAX_PRIMES + 1 || !out) return EDL_ERR_ARG;
+    std::vector<int> bits;
+    int logn = 0;
+    host::parameterise(depth, scale_bits, special_mult, bits, logn);
+    return edl_params_from_bits(logn, bits.data(), (int32_t)bits.size(), scale_bits, out);
+}
+
+size_t edl_cts_bytes(int64_t count, int32_t level, int32_t log_n) {
+    return (size_t)count * 2 * (size_t)(level + 1) * ((size_t)1 << log_n) * 8;
+}
+
+edl_status edl_ctx_create(const edl_params* p, int32_t device, void* stream, edl_ctx** out) {
+    if (!p || !out) return EDL_ERR_ARG;
+    *out = nullptr;
+    if (p->log_n < 10 || p->log_n > 14 || p->n_data < 1 || p->n_data > EDL_MAX_PRIMES) return EDL_ERR_ARG;
+    for (int k = 0; k < p->n_data; k++)
+        if (p->q[k] >= (1ull << 61)) return EDL_ERR_ARG;
+    if (p->p_special >= (1ull << 61)) return EDL_ERR_ARG;
+    if (cudaSetDevice(device) != cudaSuccess) return EDL_ERR_CUDA;
+    edl_ctx* c = new edl_ctx();
+    c->prm = *p;
+    c->logn = p->log_n;
+    c->N = 1LL << p->log_n;
+    c->L = p->n_data - 1;
+    c->device = device;
+    c->st = (cudaStream_t)stream;
+    const int nm = c->L + 2;
+    // twiddle tables: per modulus [fwd N][inv N] of {w, w'}
+    const size_t tw_words = (size_t)nm * 4 * c->N;
+    if (cudaMalloc(&c->d_tw, tw_words * 8) != cudaSuccess) {
+        delete c;
+        return EDL_ERR_CUDA;
+    }
+    c->h_mods.resize(nm);
+    std::vector<uint64_t> tf, ti;
+    for (int k = 0; k < nm; k++) {
+        const uint64_t q = c->modulus(k);
+        const uint64_t psi = p->psi[k];
+        host::twiddle_table(q, psi, c->logn, false, tf);
+        host::twiddle_table(q, psi, c->logn, true, ti);
+        uint64_t* dfwd = c->d_tw + (size_t)k * 4 * c->N;
+        uint64_t* dinv = dfwd + 2 * c->N;
+        cudaMemcpy(dfwd, tf.data(), tf.size() * 8, cudaMemcpyHostToDevice);
+        cudaMemcpy(dinv, ti.data(), ti.size() * 8, cudaMemcpyHostToDevice);
+        ModInfo m;
+        std::memset(&m, 0, sizeof(m));
+        m.q = q;
+        const host::u128 ratio = (~(host::u128)0) / q;   // floor((2^128-1)/q) = floor(2^128/q), q odd
+        m.r_lo = (uint64_t)ratio;
+        m.r_hi = (uint64_t)(ratio >> 64);
+        m.two64 = (uint64_t)((((host::u128)1) << 64) % q);
+        m.two64_s = host::shoup_companion(m.two64, q);
+        m.tw_fwd = reinterpret_cast<const ulonglong2*>(dfwd);
+        m.tw_inv = reinterpret_cast<const ulonglong2*>(dinv);
+        m.ninv = host::invmod((uint64_t)c->N % q, q);
+        m.ninv_s = host::shoup_companion(m.ninv, q);
+        m.w1ninv = host::mulmod(ti[2 * 1], m.ninv, q);
+        m.w1ninv_s = host::shoup_companion(m.w1ninv, q);
+        c->h_mods[k] = m;
+    }
+    c->h_cc = new ChainConsts();
+    std::memset(c->h_cc, 0, sizeof(ChainConsts));
+    c->h_cc->L = c->L;
+    for (int a = 0; a < nm; a++)
+        for (int b = 0; b < nm; b++) {
+            const uint64_t qa = c->modulus(a), qb = c->modulus(b);
+            c->h_cc->qmod[a][b] = qa % qb;
+            if (a != b) {
+                const uint64_t inv = host::invmod(qa % qb, qb);
+                c->h_cc->qinv[a][b] = make_ulonglong2(inv, host::shoup_companion(inv, qb));
+            }
+        }
+    cudaMalloc(&c->d_mods, nm * sizeof(ModInfo));
+    cudaMemcpy(c->d_mods, c->h_mods.data(), nm * sizeof(ModInfo), cudaMemcpyHostToDevice);
+    cudaMalloc(&c->d_cc, sizeof(ChainConsts));
+    cudaMemcpy(c->d_cc, c->h_cc, sizeof(ChainConsts), cudaMemcpyHostToDevice);
+    c->const_cap = 16u << 20;
+    cudaMallocHost(&c->h_pin, c->const_cap);
+    cudaMalloc(&c->d_const, c->const_cap);
+    if (!set_smem_attrs(c->logn)) {
+        edl_ctx_destroy(c);
+        return EDL_ERR_CUDA;
+    }
+    if (cuda_check(c, "ctx_create") != EDL_OK) {
+        edl_ctx_destroy(c);
+        return EDL_ERR_CUDA;
+    }
+    *out = c;
+    return EDL_OK;
+}
+
+void edl_ctx_destroy(edl_ctx* c) {
+    if (!c) return;
+    cudaStreamSynchronize(c->st);
+    cudaFree(c->d_tw);
+    cudaFree(c->d_mods);
+    cudaFree(c->d_cc);
+    cudaFree(c->d_s);
+    cudaFree(c->d_pk);
+    cudaFree(c->d_rlk);
+    cudaFree(c->d_rlk_s);
+    cudaFree(c->d_scratch);
+    cudaFree(c->d_const);
+    if (c->h_pin) cudaFreeHost(c->h_pin);
+    delete c->h_cc;
+    delete c;
+}
+
+edl_status edl_ctx_set_stream(edl_ctx* c, void* stream) {
+    if (!c) return EDL_ERR_ARG;
+    cudaStreamSynchronize(c->st);
+    c->st = (cudaStream_t)stream;
+    return EDL_OK;
+}
+
+const char* edl_last_error(const edl_ctx* c) { return c ? c->err.c_str() : "null context"; }
+int64_t edl_launch_count(const edl_ctx* c) { return c ? c->prof.launches : 0; }
+
+edl_status edl_profile(edl_ctx* c, int32_t enable) {
+    if (!c) return EDL_ERR_ARG;
+    cudaStreamSynchronize(c->st);
+    c->prof.reset();
+    c->prof.on = enable != 0;
+    return EDL_OK;
+}
+
+int32_t edl_profile_read(edl_ctx* c, char* names, size_t names_len, double* ms, int64_t* counts, int32_t max_entries) {
+    if (!c) return EDL_ERR_ARG;
+    if (cudaStreamSynchronize(c->st) != cudaSuccess) return cuda_check(c, "profile_read");
+    std::vector<std::string> keys;
+    std::vector<double> tot;
+    std::vector<int64_t> cnt;
+    for (auto& r : c->prof.recs) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, r.a, r.b);
+        size_t k = 0;
+        while (k < keys.size() && keys[k] != r.name) k++;
+        if (k == keys.size()) {
+            keys.push_back(r.name);
+            tot.push_back(0.0);
+            cnt.push_back(0);
+        }
+        tot[k] += t;
+        cnt[k] += 1;
+    }
+    std::string joined;
+    int32_t n = 0;
+    for (size_t k = 0; k < keys.size() && n < max_entries; k++, n++) {
+        if (ms) ms[n] = tot[k];
+        if (counts) counts[n] = cnt[k];
+        joined += keys[k];
+        joined += "\n";
+    }
+    if (names && names_len) {
+        std::strncpy(names, joined.c_str(), names_len - 1);
+        names[names_len - 1] = 0;
+    }
+    return n;
+}
+
+edl_status edl_keygen(edl_ctx* c, uint64_t seed) {
+    if (!c) return EDL_ERR_ARG;
+    const int nm = c->L + 2;
+    const size_t N = c->N;
+    if (!c->d_s) {
+        if (cudaMalloc(&c->d_s, nm * N * 8) != cudaSuccess ||
+            cudaMalloc(&c->d_pk, 2 * (size_t)(c->L + 1) * N * 8) != cudaSuccess ||
+            cudaMalloc(&c->d_rlk, (size_t)(c->L + 1) * 2 * nm * N * 8) != cudaSuccess ||
+            cudaMalloc(&c->d_rlk_s, (size_t)(c->L + 1) * 2 * nm * N * 8) != cudaSuccess)
+            return fail(c, EDL_ERR_CUDA, "keygen: out of device memory");
+    }
+    launch_keygen(c->dev(), seed, c->d_s, c->d_pk, c->d_rlk, c->d_rlk_s, nullptr);
+    if (cudaStreamSynchronize(c->st) != cudaSuccess) return cuda_check(c, "keygen");
+    c->has_key = true;
+    c->key_id = seed;
+    return cuda_check(c, "keygen");
+}
+
+edl_status edl_encode(edl_ctx* c, const double* slots, int64_t n_vec, int64_t n_slots, double scale,
+                      int64_t* poly_out) {
+    if (!c || (!slots && n_vec > 0) || (!poly_out && n_vec > 0) || n_vec < 0 || n_slots < 0)
+        return fail(c, EDL_ERR_ARG, "encode: bad arguments");
+    if (n_slots > c->N / 2) return fail(c, EDL_ERR_CAPACITY, "CapacityError: n_slots > N/2");
+    for (int64_t v = 0; v < n_vec; v++) host::encode(slots + v * n_slots, n_slots, c->logn, scale, poly_out + v * c->N);
+    return EDL_OK;
+}
+
+edl_status edl_encrypt_poly(edl_ctx* c, const int64_t* poly, int64_t n_vec, int32_t level, double scale,
+                            uint64_t enc_seed, uint32_t obj0, edl_cts* out) {
+    if (!c || !out || (!poly && n_vec > 0) || n_vec < 0) return fail(c, EDL_ERR_ARG, "encrypt: bad arguments");
+    if (!c->has_key) return fail(c, EDL_ERR_NOKEY, "encrypt: no key");
+    if (level < 0 || level > c->L) return fail(c, EDL_ERR_LEVEL, "encrypt: level out of range");
+    if (!out->data && n_vec > 0) return fail(c, EDL_ERR_ARG, "encrypt: null output");
+    if (n_vec > 0) {
+        launch_encrypt(c->dev(), poly, n_vec, level, enc_seed, obj0, c->d_pk, out->data);
+    }
+    set_meta(out, n_vec, level, scale, c->key_id);
+    return cuda_check(c, "encrypt");
+}
+
+edl_status edl_encrypt(edl_ctx* c, const double* slots, int64_t n_vec, int64_t n_slots, uint64_t enc_seed,
+                       uint32_t obj0, edl_cts* out) {
+    if (!c) return EDL_ERR_ARG;
+    const double scale = std::ldexp(1.0, c->prm.scale_bits);
+    std::vector<int64_t> polys((size_t)n_vec * c->N);
+    edl_status s = edl_encode(c, slots, n_vec, n_slots, scale, polys.data());
+    if (s != EDL_OK) return s;
+    int64_t* d = reinterpret_cast<int64_t*>(scratch(c, polys.size()));
+    if (!d && n_vec > 0) return fail(c, EDL_ERR_CUDA, "encrypt: scratch");
+    cudaMemcpyAsync(d, polys.data(), polys.size() * 8, cudaMemcpyHostToDevice, c->st);
+    s = edl_encrypt_poly(c, d, n_vec, c->L, scale, enc_seed, obj0, out);
+    cudaStreamSynchronize(c->st);
+    return s;
+}
+
+edl_status edl_decrypt_poly(edl_ctx* c, const edl_cts* in, int64_t* poly_out) {
+    if (!c || !poly_out) return EDL_ERR_ARG;
+    if (!c->has_key) return fail(c, EDL_ERR_NOKEY, "decrypt: no key");
+    edl_status s = check_ct(c, in);
+    if (s != EDL_OK) return s;
+    const int l = in->level;
+    const size_t words = (size_t)in->count * (l + 1) * c->N;
+    uint64_t* d = scratch(c, words);
+    if (!d && words) return fail(c, EDL_ERR_CUDA, "decrypt: scratch");
+    std::vector<uint64_t> h(words);
+    if (in->count > 0) {
+        launch_decrypt(c->dev(), in->data, in->count, l, c->d_s, d);
+        cudaMemcpyAsync(h.data(), d, words * 8, cudaMemcpyDeviceToHost, c->st);
+    }
+    if (cudaStreamSynchronize(c->st) != cudaSuccess) return cuda_check(c, "decrypt");
+    for (int64_t k = 0; k < in->count; k++)
+        host::crt_lift(h.data() + (size_t)k * (l + 1) * c->N, l + 1, c->prm.q, c->logn, poly_out + k * c->N);
+    return cuda_check(c, "decrypt");
+}
+
+edl_status edl_decrypt(edl_ctx* c, const edl_cts* in, double* slots_out, int64_t n_slots) {
+    if (!c || !in || !slots_out) return EDL_ERR_ARG;
+    if (n_slots > c->N / 2) return fail(c, EDL_ERR_CAPACITY, "CapacityError: n_slots > N/2");
+    std::vector<int64_t> polys((size_t)in->count * c->N);
+    edl_status s = edl_decrypt_poly(c, in, polys.data());
+    if (s != EDL_OK) return s;
+    for (int64_t k = 0; k < in->count; k++)
+        host::decode(polys.data() + k * c->N, c->logn, in->scale, n_slots, slots_out + k * n_slots);
+    return EDL_OK;
+}
+
+edl_status edl_ct_add(edl_ctx* c, const edl_cts* a, const edl_cts* b, edl_cts* out) {
+    if (!c || !out) return EDL_ERR_ARG;
+    edl_status s;
+    if ((s = check_ct(c, a)) != EDL_OK || (s = check_ct(c, b)) != EDL_OK) return s;
+    if (a->key_id != b->key_id) return fail(c, EDL_ERR_KEY, "KeyMismatch");
+    if (a->count != b->count) return fail(c, EDL_ERR_SHAPE, "ShapeMismatch: counts differ");
+    if (!scales_match(a->scale, b->scale)) return fail(c, EDL_ERR_SCALE, "scale mismatch on add");
+    const int lo = a->level < b->level ? a->level : b->level;
+    if (a->count > 0) {
+        launch_add(c->dev(), a->data, a->level, b->data, b->level, a->count, lo, out->data);
+    }
+    set_meta(out, a->count, lo, a->scale, a->key_id);
+    return cuda_check(c, "ct_add");
+}
+
+edl_status edl_ct_pt_mul(edl_ctx* c, const edl_cts* a, const double* w, double pt_scale, edl_cts* out) {
+    if (!c || !out || (!w && a && a->count > 0)) return EDL_ERR_ARG;
+    edl_status s = check_ct(c, a);
+    if (s != EDL_OK) return s;
+    std::vector<int64_t> ints(a->count);
+    for (int64_t k = 0; k < a->count; k++) ints[k] = const_int(w[k], pt_scale);
+    if (a->count > 0) {
+        const ulonglong2* dw = upload(c, shoup_consts(c, ints, a->level));
+        launch_mul_const(c->dev(), a->data, a->count, a->level, dw, out->data);
+    }
+    set_meta(out, a->count, a->level, a->scale * pt_scale, a->key_id);
+    return cuda_check(c, "ct_pt_mul");
+}
+
+edl_status edl_ct_pt_add(edl_ctx* c, const edl_cts* a, const double* cst, edl_cts* out) {
+    if (!c || !out || (!cst && a && a->count > 0)) return EDL_ERR_ARG;
+    edl_status s = check_ct(c, a);
+    if (s != EDL_OK) return s;
+    std::vector<int64_t> ints(a->count);
+    for (int64_t k = 0; k < a->count; k++) ints[k] = const_int(cst[k], a->scale);
+    if (a->count > 0) {
+        const uint64_t* dk = upload(c, residues(c, ints, a->level + 1));
+        launch_add_const(c->dev(), a->data, a->count, a->level, dk, out->data);
+    }
+    set_meta(out, a->count, a->level, a->scale, a->key_id);
+    return cuda_check(c, "ct_pt_add");
+}
+
+edl_status edl_mod_drop(edl_ctx* c, const edl_cts* in, int32_t level, edl_cts* out) {
+    if (!c || !out) return EDL_ERR_ARG;
+    edl_status s = check_ct(c, in);
+    if (s != EDL_OK) return s;
+    if (level < 0 || level > in->level) return fail(c, EDL_ERR_LEVEL, "mod_drop: cannot raise the level");
+    if (!(out->data == in->data && level == in->level) && in->count > 0) {
+        if (out->data == in->data) return fail(c, EDL_ERR_ARG, "mod_drop: out aliases in");
+        launch_mod_drop(c->dev(), in->data, in->count, in->level, level, out->data);
+    }
+    set_meta(out, in->count, level, in->scale, in->key_id);
+    return cuda_check(c, "mod_drop");
+}
+
+edl_status edl_rescale(edl_ctx* c, const edl_cts* in, edl_cts* out) {
+    if (!c || !out) return EDL_ERR_ARG;
+    edl_status s = check_ct(c, in);
+    if (s != EDL_OK) return s;
+    const int l = in->level;
+    if (l < 1) return fail(c, EDL_ERR_LEVEL, "LevelExhausted: rescale at level 0");
+    if (out->data == in->data) return fail(c, EDL_ERR_ARG, "rescale: out aliases in");
+    if (in->count > 0) {
+        uint64_t* r = scratch(c, (size_t)in->count * 2 * c->N);
+        if (!r) return fail(c, EDL_ERR_CUDA, "rescale: scratch");
+        launch_rescale_intt(c->dev(), in->data, in->count, l, nullptr, r);
+        launch_rescale_ntt(c->dev(), in->data, in->count, l, nullptr, r, nullptr, out->data);
+    }
+    set_meta(out, in->count, l - 1, in->scale / (double)c->prm.q[l], in->key_id);
+    return cuda_check(c, "rescale");
+}
+
+edl_status edl_ct_ct_mul_relin(edl_ctx* c, const edl_cts* a, const edl_cts* b, edl_cts* out) {
+    if (!c || !out) return EDL_ERR_ARG;
+    if (!c->has_key) return fail(c, EDL_ERR_NOKEY, "mul_relin: no relinearisation key");
+    edl_status s;
+    if ((s = check_ct(c, a)) != EDL_OK || (s = check_ct(c, b)) != EDL_OK) return s;
+    if (a->key_id != b->key_id) return fail(c, EDL_ERR_KEY, "KeyMismatch");
+    if (a->count != b->count) return fail(c, EDL_ERR_SHAPE, "ShapeMismatch: counts differ");
+    if (out->data == a->data || out->data == b->data) return fail(c, EDL_ERR_ARG, "mul_relin: out aliases input");
+    const int l = a->level < b->level ? a->level : b->level;
+    const int64_t cnt = a->count;
+    if (cnt > 0) {
+        const size_t drop_a = a->level > l ? ct_words(c, cnt, l) : 0;
+        const size_t drop_b = b->level > l ? ct_words(c, cnt, l) : 0;
+        uint64_t* base = scratch(c, relin_scratch_words(cnt, l, c->logn) + drop_a + drop_b);
+        if (!base) return fail(c, EDL_ERR_CUDA, "mul_relin: scratch");
+        const uint64_t* pa = a->data;
+        const uint64_t* pb = b->data;
+        uint64_t* extra = base + relin_scratch_words(cnt, l, c->logn);
+        if (drop_a) {
+            launch_mod_drop(c->dev(), a->data, cnt, a->level, l, extra);
+            pa = extra;
+            extra += drop_a;
+        }
+        if (drop_b) {
+            launch_mod_drop(c->dev(), b->data, cnt, b->level, l, extra);
+            pb = extra;
+        }
+        launch_relin(c->dev(), pa, pb, cnt, l, false, c->d_rlk, c->d_rlk_s, base, out->data);
+    }
+    set_meta(out, cnt, l, a->scale * b->scale, a->key_id);
+    return cuda_check(c, "mul_relin");
+}
+
+edl_status edl_cross_correlate(edl_ctx* c, const edl_cts* x, int32_t H, int32_t W, const double* k, int32_t F,
+                               int32_t kh, int32_t kw, int32_t stride, const double* bias, edl_cts* out) {
+    if (!c || !out || !k) return EDL_ERR_ARG;
+    edl_status s = check_ct(c, x);
+    if (s != EDL_OK) return s;
+    if (H <= 0 || W <= 0 || F <= 0 || kh <= 0 || kw <= 0 || stride <= 0 || kh > H || kw > W)
+        return fail(c, EDL_ERR_SHAPE, "cross_correlate: bad geometry");
+    if (x->count != (int64_t)H * W) return fail(c, EDL_ERR_SHAPE, "cross_correlate: x must hold H*W ciphertexts");
+    const int l = x->level;
+    if (l < 1) return fail(c, EDL_ERR_LEVEL, "LevelExhausted");
+    const int Ho = (H - kh) / stride + 1, Wo = (W - kw) / stride + 1;
+    const int64_t cnt = (int64_t)F * Ho * Wo;
+    const int taps = kh * kw;
+    const double pt_scale = (double)c->prm.q[l];
+    std::vector<int64_t> wi((size_t)F * taps);
+    for (int f = 0; f < F; f++)
+        for (int t = 0; t < taps; t++) wi[(size_t)f * taps + t] = const_int(k[(size_t)f * taps + t], pt_scale);
+    const double s_after = (x->scale * pt_scale) / (double)c->prm.q[l];
+    uint64_t* acc = scratch(c, ct_words(c, cnt, l) + (size_t)cnt * 2 * c->N);
+    if (!acc) return fail(c, EDL_ERR_CUDA, "cross_correlate: scratch");
+    uint64_t* r = acc + ct_words(c, cnt, l);
+    const uint64_t* dw = upload(c, residues(c, wi, l + 1));
+    const uint64_t* db = nullptr;
+    if (bias) {
+        std::vector<int64_t> bi(cnt);
+        for (int64_t o = 0; o < cnt; o++) bi[o] = const_int(bias[o / (Ho * Wo)], s_after);
+        db = upload(c, residues(c, bi, l));
+    }
+    Dev d = c->dev();
+    launch_cc_mac(d, x->data, l, H, W, F, kh, kw, stride, dw, acc);
+    launch_rescale_intt(d, acc, cnt, l, nullptr, r);
+    launch_rescale_ntt(d, acc, cnt, l, nullptr, r, db, out->data);
+    set_meta(out, cnt, l - 1, s_after, x->key_id);
+    return cuda_check(c, "cross_correlate");
+}
+
+edl_status edl_dense(edl_ctx* c, const edl_cts* x, const double* Wt, const double* b, int32_t O,
+                     int32_t defer_rescale, edl_cts* out) {
+    if (!c || !out || !Wt || O <= 0) return EDL_ERR_ARG;
+    edl_status s = check_ct(c, x);
+    if (s != EDL_OK) return s;
+    const int l = x->level;
+    const int64_t K = x->count;
+    if (K <= 0) return fail(c, EDL_ERR_SHAPE, "dense: no inputs");
+    if (!defer_rescale && l < 1) return fail(c, EDL_ERR_LEVEL, "LevelExhausted");
+    if (l < 0) return fail(c, EDL_ERR_LEVEL, "dense: bad level");
+    const double pt_scale = (double)c->prm.q[l];
+    std::vector<int64_t> wi((size_t)O * K);
+    for (size_t t = 0; t < wi.size(); t++) wi[t] = const_int(Wt[t], pt_scale);
+    const uint64_t* dw = upload(c, residues(c, wi, l + 1));
+    if (!dw) return fail(c, EDL_ERR_ARG, "dense: weight table too large");
+    Dev d = c->dev();
+    if (defer_rescale) {
+        launch_dense_mac(d, x->data, K, O, l, dw, out->data);
+        set_meta(out, O, l, x->scale * pt_scale, x->key_id);
+        return cuda_check(c, "dense");
+    }
+    const double s_after = (x->scale * pt_scale) / (double)c->prm.q[l];
+    uint64_t* acc = scratch(c, ct_words(c, O, l) + (size_t)O * 2 * c->N);
+    if (!acc) return fail(c, EDL_ERR_CUDA, "dense: scratch");
+    uint64_t* r = acc + ct_words(c, O, l);
+    const uint64_t* db = nullptr;
+    if (b) {
+        std::vector<int64_t> bi(O);
+        for (int o = 0; o < O; o++) bi[o] = const_int(b[o], s_after);
+        db = upload(c, residues(c, bi, l));
+    }
+    launch_dense_mac(d, x->data, K, O, l, dw, acc);
+    launch_rescale_intt(d, acc, O, l, nullptr, r);
+    launch_rescale_ntt(d, acc, O, l, nullptr, r, db, out->data);
+    set_meta(out, O, l - 1, s_after, x->key_id);
+    return cuda_check(c, "dense");
+}
+
+edl_status edl_mod_reduce(edl_ctx* c, edl_cts* x) {
+    if (!c) return EDL_ERR_ARG;
+    edl_status s = check_ct(c, x);
+    if (s != EDL_OK) return s;
+    if (x->count > 0) {
+        launch_mod_reduce(c->dev(), x->data, x->count, x->level);
+    }
+    return cuda_check(c, "mod_reduce");
+}
+
+edl_status edl_dense_finish(edl_ctx* c, const edl_cts* acc, const double* b, edl_cts* out) {
+    if (!c || !out) return EDL_ERR_ARG;
+    edl_status s = check_ct(c, acc);
+    if (s != EDL_OK) return s;
+    const int l = acc->level;
+    if (l < 1) return fail(c, EDL_ERR_LEVEL, "LevelExhausted");
+    const int64_t O = acc->count;
+    const double s_after = acc->scale / (double)c->prm.q[l];
+    uint64_t* r = scratch(c, (size_t)O * 2 * c->N);
+    if (!r) return fail(c, EDL_ERR_CUDA, "dense_finish: scratch");
+    const uint64_t* db = nullptr;
+    if (b) {
+        std::vector<int64_t> bi(O);
+        for (int64_t o = 0; o < O; o++) bi[o] = const_int(b[o], s_after);
+        db = upload(c, residues(c, bi, l));
+    }
+    Dev d = c->dev();
+    launch_rescale_intt(d, acc->data, O, l, nullptr, r);
+    launch_rescale_ntt(d, acc->data, O, l, nullptr, r, db, out->data);
+    set_meta(out, O, l - 1, s_after, acc->key_id);
+    return cuda_check(c, "dense_finish");
+}
+
+edl_status edl_poly_activation(edl_ctx* c, const edl_cts* x, const double* coeffs, int32_t degree, edl_cts* out) {
+    if (!c || !out || !coeffs) return EDL_ERR_ARG;
+    if (!c->has_key) return fail(c, EDL_ERR_NOKEY, "poly_activation: no relinearisation key");
+    edl_status s = check_ct(c, x);
+    if (s != EDL_OK) return s;
+    if (out->data == x->data) return fail(c, EDL_ERR_ARG, "poly_activation: out aliases x");
+    const int l = x->level;
+    const int64_t cnt = x->count;
+    Dev d = c->dev();
+    if (degree == 2 && coeffs[0] == 0.0 && coeffs[1] == 0.0 && coeffs[2] == 1.0) {
+        if (l < 1) return fail(c, EDL_ERR_LEVEL, "LevelExhausted");
+        if (cnt > 0) {
+            uint64_t* base = scratch(c, relin_scratch_words(cnt, l, c->logn));
+            if (!base) return fail(c, EDL_ERR_CUDA, "poly_activation: scratch");
+            launch_relin(d, x->data, x->data, cnt, l, true, c->d_rlk, c->d_rlk_s, base, out->data);
+        }
+        set_meta(out, cnt, l - 1, (x->scale * x->scale) / (double)c->prm.q[l], x->key_id);
+        return cuda_check(c, "poly_activation");
+    }
+    if (!(degree == 3 && coeffs[2] == 0.0)) return fail(c, EDL_ERR_ARG, "poly_activation: unsupported schedule");
+    if (l < 2) return fail(c, EDL_ERR_LEVEL, "LevelExhausted");
+    const double c0 = coeffs[0], c1 = coeffs[1], c3 = coeffs[3];
+    const double ql = (double)c->prm.q[l], qlm1 = (double)c->prm.q[l - 1];
+    // O13 schedule, scale bookkeeping in the oracle's order
+    const double Sy = x->scale;
+    const double S2 = (Sy * Sy) / ql;                    // y2 = Rescale(Relin(y*y))
+    const double Su = (Sy * ql) / ql;                    // u  = Rescale(y * c3@q_l)
+    const double S3 = (Su * S2) / qlm1;                  // v  = Rescale(Relin(u*y2))
+    const double p1 = (S3 * ql) / Sy;                    // w  = Rescale(y * c1@p1)
+    const double Sw = (Sy * p1) / ql;
+    if (!scales_match(S3, Sw)) return fail(c, EDL_ERR_SCALE, "poly_activation: scale drift");
+    if (cnt > 0) {
+        const size_t wl = ct_words(c, cnt, l - 1), wv = ct_words(c, cnt, l - 2);
+        const size_t rs = relin_scratch_words(cnt, l, c->logn);
+        uint64_t* base = scratch(c, 3 * wl + wv + (size_t)cnt * 2 * c->N + rs);
+        if (!base) return fail(c, EDL_ERR_CUDA, "poly_activation: scratch");
+        uint64_t* y2 = base;
+        uint64_t* u = y2 + wl;
+        uint64_t* w = u + wl;
+        uint64_t* v = w + wl;
+        uint64_t* r = v + wv;
+        uint64_t* rsc = r + (size_t)cnt * 2 * c->N;
+        std::vector<int64_t> i3(cnt, const_int(c3, ql)), i1(cnt, const_int(c1, p1)), i0(cnt, const_int(c0, S3));
+        const ulonglong2* w3 = upload(c, shoup_consts(c, i3, l));
+        const ulonglong2* w1 = upload(c, shoup_consts(c, i1, l));
+        const uint64_t* k0 = upload(c, residues(c, i0, l - 1));
+        launch_relin(d, x->data, x->data, cnt, l, true, c->d_rlk, c->d_rlk_s, rsc, y2);   // 1.
+        scalar_rescale(c, x->data, cnt, l, w3, r, u);                                          // 2.
+        launch_relin(d, u, y2, cnt, l - 1, true, c->d_rlk, c->d_rlk_s, rsc, v);              // 3.
+        scalar_rescale(c, x->data, cnt, l, w1, r, w);                                          // 4.
+        launch_add_add_const(d, v, w, l - 1, cnt, l - 2, k0, out->data);                       // 5.
+    }
+    set_meta(out, cnt, l - 2, S3, x->key_id);
+    return cuda_check(c, "poly_activation");
+}
+
+edl_status edl_ntt(edl_ctx* c, uint64_t* limbs, int64_t n_polys, int32_t level, int32_t inverse) {
+    if (!c || (!limbs && n_polys > 0) || n_polys < 0 || level < 0 || level > c->L + 1)
+        return fail(c, EDL_ERR_ARG, "ntt: bad arguments");
+    std::vector<int> pm(level + 1);
+    for (int j = 0; j <= level; j++) pm[j] = j;
+    // grid.y limit: split very large batches
+    for (int64_t b0 = 0; b0 < n_polys; b0 += 65535) {
+        const int64_t nb = (n_polys - b0) < 65535 ? (n_polys - b0) : 65535;
+        launch_ntt_limbs(c->dev(), limbs + (size_t)b0 * (level + 1) * c->N, nb, level + 1, pm.data(), inverse != 0);
+    }
+    return cuda_check(c, "ntt");
+}
+
+edl_status edl_philox(edl_ctx* c, uint64_t seed, const uint32_t* ctr, int64_t n, uint32_t* out) {
+    if (!c || !ctr || !out || n <= 0) return EDL_ERR_ARG;
+    uint32_t* d = reinterpret_cast<uint32_t*>(scratch(c, (size_t)n * 4));
+    if (!d) return fail(c, EDL_ERR_CUDA, "philox: scratch");
+    cudaMemcpyAsync(d, ctr, (size_t)n * 16, cudaMemcpyHostToDevice, c->st);
+    launch_philox_words(c->dev(), seed, d, n, d);
+    cudaMemcpyAsync(out, d, (size_t)n * 16, cudaMemcpyDeviceToHost, c->st);
+    cudaStreamSynchronize(c->st);
+    return cuda_check(c, "philox");
+}
+
+edl_status edl_modmul_peak(edl_ctx* c, int32_t iters, double* modmul_per_s) {
+    if (!c || !modmul_per_s || iters <= 0) return EDL_ERR_ARG;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    const int blocks = sms * 8;
+    uint64_t* sink = scratch(c, 1);
+    if (!sink) return fail(c, EDL_ERR_CUDA, "modmul_peak: scratch");
+    const uint64_t q = c->prm.q[c->L];
+    const uint64_t w = q / 3 + 7, ws = host::shoup_companion(w, q);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    launch_modmul_peak(c->dev(), q, w, ws, iters, blocks, sink);   // warm-up
+    cudaEventRecord(a, c->st);
+    launch_modmul_peak(c->dev(), q, w, ws, iters, blocks, sink);
+    cudaEventRecord(b, c->st);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *modmul_per_s = (double)blocks * 256.0 * 8.0 * (double)iters / (ms * 1e-3);
+    return cuda_check(c, "modmul_peak");
+}
+
+edl_status edl_export_key(edl_ctx* c, int32_t which, uint64_t* host_out, size_t words) {
+    if (!c || !host_out) return EDL_ERR_ARG;
+    if (!c->has_key) return fail(c, EDL_ERR_NOKEY, "export_key: no key");
+    const size_t N = c->N, nm = c->L + 2;
+    const uint64_t* src = nullptr;
+    size_t need = 0;
+    if (which == 0) {
+        src = c->d_s;
+        need = nm * N;
+    } else if (which == 1) {
+        src = c->d_pk;
+        need = 2 * (size_t)(c->L + 1) * N;
+    } else if (which == 2) {
+        src = c->d_rlk;
+        need = (size_t)(c->L + 1) * 2 * nm * N;
+    } else {
+        return fail(c, EDL_ERR_ARG, "export_key: which");
+    }
+    if (words < need) return fail(c, EDL_ERR_ARG, "export_key: buffer too small");
+    cudaMemcpyAsync(host_out, src, need * 8, cudaMemcpyDeviceToHost, c->st);
+    cudaStreamSynchronize(c->st);
+    return cuda_check(c, "export_key");
+}
+
+}  // extern "C"

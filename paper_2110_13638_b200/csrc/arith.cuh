@@ -1,0 +1,110 @@
+// arith.cuh -- 64-bit modular arithmetic for sm_100a built from 32-bit IMAD.
+//
+// Residues are uint64 with q < 2^62 (Alg. 8 chains use 40- and 60-bit primes,
+// PAPER.md:222-224).  Three multiplication forms are used on the hot path:
+//   * Shoup (one operand a precomputed constant w with w' = floor(w 2^64 / q)):
+//     result in [0, 2q) -- NTT twiddles, scalar weights, rlk entries.
+//   * Barrett on a 128-bit value with ratio floor(2^128 / q): canonical result --
+//     variable x variable products and lazily accumulated 128-bit MAC sums.
+//   * 128-bit lazy accumulation of full products (MAC layers, key-switch inner product).
+#pragma once
+#include <cstdint>
+
+namespace edl {
+
+struct ModInfo {
+    uint64_t q;        // modulus
+    uint64_t r_lo;     // floor(2^128 / q), low word
+    uint64_t r_hi;     // floor(2^128 / q), high word
+    uint64_t two64;    // 2^64 mod q
+    uint64_t two64_s;  // Shoup companion of two64
+    const ulonglong2* tw_fwd;   // [N] {psi^brv(k), shoup}
+    const ulonglong2* tw_inv;   // [N] {psi^-brv(k), shoup}
+    uint64_t ninv, ninv_s;      // N^-1 mod q and Shoup companion
+    uint64_t w1ninv, w1ninv_s;  // psi^-brv(1) * N^-1 (last INTT stage), Shoup companion
+};
+
+struct U128 {
+    uint64_t lo, hi;
+};
+
+__device__ __forceinline__ U128 mul_wide(uint64_t a, uint64_t b) {
+    U128 r;
+    r.lo = a * b;
+    r.hi = __umul64hi(a, b);
+    return r;
+}
+
+__device__ __forceinline__ void add128(U128& acc, U128 v) {
+    asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;"
+        : "+l"(acc.lo), "+l"(acc.hi)
+        : "l"(v.lo), "l"(v.hi));
+}
+
+// acc += a * b (full 128-bit product), mad.lo.cc / madc.hi carry chain.
+__device__ __forceinline__ void mac128(U128& acc, uint64_t a, uint64_t b) {
+    asm("mad.lo.cc.u64 %0, %2, %3, %0;\n\tmadc.hi.u64 %1, %2, %3, %1;"
+        : "+l"(acc.lo), "+l"(acc.hi)
+        : "l"(a), "l"(b));
+}
+
+// Shoup: w*y mod q in [0, 2q) for any y < 2^64, w < q, ws = floor(w 2^64 / q).
+__device__ __forceinline__ uint64_t shoup_lazy(uint64_t y, uint64_t w, uint64_t ws, uint64_t q) {
+    uint64_t qt = __umul64hi(y, ws);
+    return y * w - qt * q;
+}
+
+__device__ __forceinline__ uint64_t csub(uint64_t x, uint64_t m) { return x >= m ? x - m : x; }
+
+__device__ __forceinline__ uint64_t shoup(uint64_t y, uint64_t w, uint64_t ws, uint64_t q) {
+    return csub(shoup_lazy(y, w, ws, q), q);
+}
+
+// Barrett reduction of a 128-bit value x < q * 2^64 ... in practice x < 2^126.
+// qest = floor(x * R / 2^128) computed without the lowest partial product; qest is at
+// most 2 below floor(x / q), so two conditional subtractions give the canonical value.
+__device__ __forceinline__ uint64_t barrett128(U128 x, const ModInfo& m) {
+    uint64_t c0 = __umul64hi(x.lo, m.r_lo);
+    uint64_t t1lo = x.lo * m.r_hi;
+    uint64_t t1hi = __umul64hi(x.lo, m.r_hi);
+    uint64_t t2lo = x.hi * m.r_lo;
+    uint64_t t2hi = __umul64hi(x.hi, m.r_lo);
+    uint64_t s, carry1, carry2;
+    // s = c0 + t1lo + t2lo, collecting carries into the quotient word
+    asm("add.cc.u64 %0, %3, %4;\n\t"
+        "addc.u64 %1, 0, 0;\n\t"
+        "add.cc.u64 %0, %0, %5;\n\t"
+        "addc.u64 %2, 0, 0;"
+        : "=l"(s), "=l"(carry1), "=l"(carry2)
+        : "l"(c0), "l"(t1lo), "l"(t2lo));
+    (void)s;
+    uint64_t qest = x.hi * m.r_hi + t1hi + t2hi + carry1 + carry2;
+    uint64_t r = x.lo - qest * m.q;
+    r = csub(r, 2 * m.q);
+    return csub(r, m.q);
+}
+
+__device__ __forceinline__ uint64_t mulmod(uint64_t a, uint64_t b, const ModInfo& m) {
+    return barrett128(mul_wide(a, b), m);
+}
+
+// Canonical reduction of an arbitrary 64-bit value.
+__device__ __forceinline__ uint64_t reduce64(uint64_t a, const ModInfo& m) {
+    U128 x;
+    x.lo = a;
+    x.hi = 0;
+    return barrett128(x, m);
+}
+
+__device__ __forceinline__ uint64_t addmod(uint64_t a, uint64_t b, uint64_t q) { return csub(a + b, q); }
+__device__ __forceinline__ uint64_t submod(uint64_t a, uint64_t b, uint64_t q) { return a >= b ? a - b : a + q - b; }
+
+// Centered lift of r in [0, qf) to (-qf/2, qf/2], reduced into [0, q) where
+// qf_mod_q = qf mod q (precomputed).  qf is odd so the half point never occurs.
+__device__ __forceinline__ uint64_t center_mod(uint64_t r, uint64_t qf, uint64_t qf_mod_q, const ModInfo& m) {
+    uint64_t rq = (r < m.q) ? r : reduce64(r, m);
+    if (r > (qf >> 1)) rq = submod(rq, qf_mod_q, m.q);
+    return rq;
+}
+
+}  // namespace edl

@@ -1,0 +1,224 @@
+// host_math.cpp -- see host_math.h.  Compiled with -ffp-contract=off so double
+// arithmetic (encode, scale bookkeeping) rounds exactly as written.
+#include "host_math.h"
+
+#include <cmath>
+#include <set>
+
+namespace edl {
+namespace host {
+
+uint64_t mulmod(uint64_t a, uint64_t b, uint64_t q) { return (uint64_t)(((u128)a * b) % q); }
+
+uint64_t powmod(uint64_t a, uint64_t e, uint64_t q) {
+    uint64_t r = 1 % q;
+    a %= q;
+    while (e) {
+        if (e & 1) r = mulmod(r, a, q);
+        a = mulmod(a, a, q);
+        e >>= 1;
+    }
+    return r;
+}
+
+uint64_t invmod(uint64_t a, uint64_t q) { return powmod(a, q - 2, q); }
+
+bool is_prime(uint64_t n) {
+    if (n < 2) return false;
+    static const uint64_t bases[] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+    for (uint64_t p : bases) {
+        if (n % p == 0) return n == p;
+    }
+    uint64_t d = n - 1;
+    int s = 0;
+    while ((d & 1) == 0) {
+        d >>= 1;
+        s++;
+    }
+    for (uint64_t a : bases) {
+        uint64_t x = powmod(a, d, n);
+        if (x == 1 || x == n - 1) continue;
+        bool comp = true;
+        for (int r = 1; r < s; r++) {
+            x = mulmod(x, x, n);
+            if (x == n - 1) {
+                comp = false;
+                break;
+            }
+        }
+        if (comp) return false;
+    }
+    return true;
+}
+
+uint64_t shoup_companion(uint64_t w, uint64_t q) { return (uint64_t)(((u128)w << 64) / q); }
+
+bool select_primes(const int* bits, int n_bits, int logn, uint64_t* out) {
+    std::set<uint64_t> used;
+    const uint64_t two_n = 2ull << logn;
+    for (int k = 0; k < n_bits; k++) {
+        const int b = bits[k];
+        if (b < 2 || b > 61) return false;
+        const uint64_t top = (b == 64) ? ~0ull : ((1ull << b) - 1);
+        uint64_t cand = top / two_n * two_n + 1;
+        while (true) {
+            if (cand < two_n) return false;
+            if (cand <= top && !used.count(cand) && is_prime(cand)) break;
+            cand -= two_n;
+        }
+        used.insert(cand);
+        out[k] = cand;
+    }
+    return true;
+}
+
+uint64_t minimal_psi(uint64_t q, int logn) {
+    const uint64_t n = 1ull << logn, two_n = 2 * n;
+    uint64_t y = 0;
+    for (uint64_t x = 2;; x++) {
+        y = powmod(x, (q - 1) / two_n, q);
+        if (powmod(y, n, q) == q - 1) break;
+    }
+    uint64_t best = q, yt = y;
+    const uint64_t y2 = mulmod(y, y, q);
+    for (uint64_t t = 0; t < n; t++) {
+        if (yt < best) best = yt;
+        yt = mulmod(yt, y2, q);
+    }
+    return best;
+}
+
+void parameterise(int c, int s, double p, std::vector<int>& bits, int& logn) {
+    bits.assign(c + 2, s);                       // m = [s for i in range(c+2)]
+    bits[0] = (int)(bits[0] * p);                // m[0] = int(m[0]*p)
+    bits[c + 1] = (int)(bits[c + 1] * p);        // m[-1] = int(m[-1]*p)
+    long b = 27, sum = 0;
+    for (int v : bits) sum += v;
+    while (b < sum) b *= 2;                      // while b < sum(m): b *= 2
+    const long n = (long)(1024.0 * ((double)b / 27.0));   // int(1024 * (b/27))
+    logn = 0;
+    while ((1L << logn) < n) logn++;
+}
+
+static uint32_t bitrev(uint32_t x, int bits) {
+    uint32_t r = 0;
+    for (int i = 0; i < bits; i++) {
+        r = (r << 1) | (x & 1);
+        x >>= 1;
+    }
+    return r;
+}
+
+void twiddle_table(uint64_t q, uint64_t psi, int logn, bool inverse, std::vector<uint64_t>& out2) {
+    const uint64_t n = 1ull << logn;
+    const uint64_t base = inverse ? invmod(psi, q) : psi;
+    out2.assign(2 * n, 0);
+    uint64_t p = 1;
+    for (uint64_t k = 0; k < n; k++) {
+        const uint32_t r = bitrev((uint32_t)k, logn);
+        out2[2 * r] = p;
+        out2[2 * r + 1] = shoup_companion(p, q);
+        p = mulmod(p, base, q);
+    }
+}
+
+// ---- canonical embedding (O5) with an in-house radix-2 complex FFT ----
+typedef std::complex<double> cd;
+
+static void fft(std::vector<cd>& a, int logn, int sign) {
+    const size_t n = a.size();
+    for (size_t i = 0; i < n; i++) {
+        const size_t j = bitrev((uint32_t)i, logn);
+        if (i < j) std::swap(a[i], a[j]);
+    }
+    for (size_t len = 2; len <= n; len <<= 1) {
+        const size_t half = len / 2;
+        const size_t step = n / len;
+        for (size_t i = 0; i < n; i += len) {
+            for (size_t k = 0; k < half; k++) {
+                // twiddle exp(sign * 2 pi i * k*step / n), evaluated directly (no recurrence)
+                const double ang = sign * 2.0 * M_PI * (double)(k * step) / (double)n;
+                const cd w(std::cos(ang), std::sin(ang));
+                const cd u = a[i + k];
+                const cd v = a[i + k + half] * w;
+                a[i + k] = u + v;
+                a[i + k + half] = u - v;
+            }
+        }
+    }
+}
+
+void encode(const double* z, int64_t n_slots, int logn, double scale, int64_t* m_out) {
+    const int64_t n = 1LL << logn;
+    const uint64_t two_n = 2ull * n;
+    std::vector<cd> v(n, cd(0, 0));
+    uint64_t e = 1;
+    for (int64_t j = 0; j < n / 2; j++) {
+        const double zj = j < n_slots ? z[j] : 0.0;
+        v[(e - 1) / 2] = cd(zj, 0.0);
+        v[(two_n - e - 1) / 2] = cd(zj, -0.0);
+        e = e * 5 % two_n;
+    }
+    fft(v, logn, -1);   // w_k = sum_t v_t exp(-2 pi i t k / N)
+    for (int64_t k = 0; k < n; k++) {
+        const cd wk = v[k] / (double)n;
+        const double ang = -M_PI * (double)k / (double)n;
+        const double u = wk.real() * std::cos(ang) - wk.imag() * std::sin(ang);
+        m_out[k] = (int64_t)std::nearbyint(scale * u);
+    }
+}
+
+void decode(const int64_t* m, int logn, double scale, int64_t n_out, double* z_out) {
+    const int64_t n = 1LL << logn;
+    const uint64_t two_n = 2ull * n;
+    std::vector<cd> v(n);
+    for (int64_t k = 0; k < n; k++) {
+        const double ang = M_PI * (double)k / (double)n;
+        v[k] = cd((double)m[k] * std::cos(ang), (double)m[k] * std::sin(ang));
+    }
+    fft(v, logn, +1);   // v_t = sum_k (m_k zeta^k) exp(+2 pi i t k / N)
+    uint64_t e = 1;
+    for (int64_t j = 0; j < n_out; j++) {
+        z_out[j] = v[(e - 1) / 2].real() / scale;
+        e = e * 5 % two_n;
+    }
+}
+
+void crt_lift(const uint64_t* r, int nl, const uint64_t* q, int logn, int64_t* out) {
+    const int64_t n = 1LL << logn;
+    if (nl == 1) {
+        for (int64_t k = 0; k < n; k++) {
+            const uint64_t v = r[k];
+            out[k] = v > q[0] / 2 ? (int64_t)v - (int64_t)q[0] : (int64_t)v;
+        }
+        return;
+    }
+    // m = sum_i y_i Qhat_i - round(sum_i y_i / q_i) Q, evaluated mod 2^64
+    std::vector<uint64_t> qhat_inv(nl), qhat_mod64(nl);
+    uint64_t Q_mod64 = 1;
+    for (int i = 0; i < nl; i++) Q_mod64 *= q[i];
+    for (int i = 0; i < nl; i++) {
+        uint64_t inv = 1, m64 = 1;
+        for (int j = 0; j < nl; j++) {
+            if (j == i) continue;
+            inv = mulmod(inv, q[j] % q[i], q[i]);
+            m64 *= q[j];
+        }
+        qhat_inv[i] = invmod(inv, q[i]);
+        qhat_mod64[i] = m64;
+    }
+    for (int64_t k = 0; k < n; k++) {
+        uint64_t acc = 0;
+        double frac = 0.0;
+        for (int i = 0; i < nl; i++) {
+            const uint64_t y = mulmod(r[(size_t)i * n + k], qhat_inv[i], q[i]);
+            acc += y * qhat_mod64[i];
+            frac += (double)y / (double)q[i];
+        }
+        const uint64_t v = (uint64_t)(int64_t)std::nearbyint(frac);
+        out[k] = (int64_t)(acc - v * Q_mod64);
+    }
+}
+
+}  // namespace host
+}  // namespace edl

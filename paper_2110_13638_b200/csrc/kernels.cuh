@@ -1,0 +1,104 @@
+// kernels.cuh -- launch interface between the C-ABI host code (api.cu) and the
+// sm_100a kernels.  Ciphertext arrays are uint64 [count][2][level+1][N] (NTT domain,
+// canonical residues), SURVEY §8(a) layout.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <vector>
+#include "arith.cuh"
+
+namespace edl {
+
+constexpr int MAXM = 34;   // max moduli (data primes + P)
+
+// Per-chain constants used by rescale / mod-down epilogues.
+struct ChainConsts {
+    int L;                           // highest data level; P is modulus index L+1
+    uint64_t qmod[MAXM][MAXM];       // qmod[a][b] = q_a mod q_b
+    ulonglong2 qinv[MAXM][MAXM];     // qinv[a][b] = q_a^{-1} mod q_b (a != b) with Shoup
+};
+
+__host__ __device__ inline size_t limb_off(int64_t ct, int poly, int limb, int nl, int logn) {
+    return ((((size_t)ct * 2 + poly) * (size_t)nl) + (size_t)limb) << logn;
+}
+
+// Launch accounting + optional per-launch CUDA-event timing (edl_profile).
+struct Prof {
+    struct Rec {
+        const char* name;
+        cudaEvent_t a, b;
+    };
+    bool on = false;
+    int64_t launches = 0;
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    cudaEvent_t ev();
+    void begin(const char* name, cudaStream_t st);
+    void end(cudaStream_t st);
+    void reset();
+    ~Prof();
+};
+
+struct Dev {
+    const ModInfo* mods;        // [L+2]
+    const ChainConsts* cc;
+    int logn;
+    int L;
+    cudaStream_t st;
+    Prof* prof;
+};
+
+#define EDL_LAUNCH(d, name, ...)                         \
+    do {                                                  \
+        (d).prof->begin(name, (d).st);                    \
+        __VA_ARGS__;                                      \
+        (d).prof->end((d).st);                            \
+    } while (0)
+
+// ---- NTT family (ntt_kernels.cu) ----
+void launch_ntt_limbs(const Dev& d, uint64_t* data, int64_t batch, int nl, const int* prime_idx_host, bool inverse);
+// rescale: r_out [cnt][2][N] <- INTT_{q_l}(in[.][.][l] * w_l) ; w may be null
+void launch_rescale_intt(const Dev& d, const uint64_t* in, int64_t cnt, int l, const ulonglong2* w, uint64_t* r_out);
+// out [cnt][2][l][N] <- (in_i * w_i - NTT_i([r]_{q_l} mod q_i)) * q_l^{-1} (+ bias_i on poly 0)
+void launch_rescale_ntt(const Dev& d, const uint64_t* in, int64_t cnt, int l, const ulonglong2* w,
+                        const uint64_t* r, const uint64_t* bias, uint64_t* out);
+// relinearisation of the tensor a (x) b at level l (+ optional rescale by q_l)
+void launch_relin(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t cnt, int l, bool rescale,
+                  const uint64_t* rlk, const uint64_t* rlk_s, uint64_t* scratch, uint64_t* out);
+size_t relin_scratch_words(int64_t cnt, int l, int logn);
+
+// ---- pointwise family (pointwise.cu) ----
+// out [cnt][2][lo+1] = a (level la) + b (level lb), lo <= min(la, lb)
+void launch_add(const Dev& d, const uint64_t* a, int la, const uint64_t* b, int lb, int64_t cnt, int lo, uint64_t* out);
+// out = a * w[c][i] (Shoup consts [cnt][l+1])
+void launch_mul_const(const Dev& d, const uint64_t* a, int64_t cnt, int l, const ulonglong2* w, uint64_t* out);
+// out = a + k[c][i] on poly 0 (consts [cnt][l+1]); out may alias a
+void launch_add_const(const Dev& d, const uint64_t* a, int64_t cnt, int l, const uint64_t* k, uint64_t* out);
+// out (level lo) = limbs 0..lo of a (level la)
+void launch_mod_drop(const Dev& d, const uint64_t* a, int64_t cnt, int la, int lo, uint64_t* out);
+// in place: x mod q_i
+void launch_mod_reduce(const Dev& d, uint64_t* x, int64_t cnt, int l);
+// v (level lo) + w (level lw >= lo) + k[c][i] on poly 0 -> out (level lo)
+void launch_add_add_const(const Dev& d, const uint64_t* v, const uint64_t* w, int lw, int64_t cnt, int lo,
+                          const uint64_t* k, uint64_t* out);
+// cross-correlation MAC: out[f*Ho*Wo + r*Wo + c] = sum_{u,v} x[(r*st+u)*W + c*st+v] * wk[f][u*kw+v][i]
+void launch_cc_mac(const Dev& d, const uint64_t* x, int l, int H, int W, int F, int kh, int kw, int stride,
+                   const uint64_t* wk /*[F][kh*kw][l+1]*/, uint64_t* out);
+// dense MAC: out[o] = sum_k x[k] * wd[o][k][i]  (x: K cts, out: O cts, level l)
+void launch_dense_mac(const Dev& d, const uint64_t* x, int64_t K, int64_t O, int l, const uint64_t* wd, uint64_t* out);
+
+// ---- randomness / keys / encryption (rng.cu) ----
+void launch_keygen(const Dev& d, uint64_t seed, uint64_t* s_hat /*[L+2][N]*/, uint64_t* pk /*[2][L+1][N]*/,
+                   uint64_t* rlk /*[L+1][2][L+2][N]*/, uint64_t* rlk_s, uint64_t* scratch);
+void launch_encrypt(const Dev& d, const int64_t* msg /*[cnt][N]*/, int64_t cnt, int l, uint64_t seed, uint32_t obj0,
+                    const uint64_t* pk, uint64_t* out);
+// m_hat = c0 + c1 s, INTT -> coefficient residues [cnt][l+1][N]
+void launch_decrypt(const Dev& d, const uint64_t* ct, int64_t cnt, int l, const uint64_t* s_hat, uint64_t* out);
+void launch_philox_words(const Dev& d, uint64_t seed, const uint32_t* ctr /*[n][4]*/, int64_t n, uint32_t* out);
+
+void launch_modmul_peak(const Dev& d, uint64_t q, uint64_t w, uint64_t ws, int iters, int blocks, uint64_t* sink);
+
+bool set_smem_attrs(int logn);
+
+}  // namespace edl

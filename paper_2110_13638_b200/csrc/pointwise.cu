@@ -1,0 +1,268 @@
+// pointwise.cu -- limb-parallel element-wise kernels (K3/K4/K8).
+//
+// All HBM-bound: 16-byte vector loads/stores of uint64 residues, one modulus per row
+// (row = one limb of one polynomial).  The MAC layers accumulate full 128-bit
+// products lazily (mad.lo.cc / madc.hi) and reduce once per output (O4: modular sums
+// are order independent, so this is bit-identical to per-step reduction).
+#include "kernels.cuh"
+
+namespace edl {
+
+namespace {
+
+constexpr int PW_THREADS = 256;
+
+__device__ __forceinline__ const ulonglong2* v2(const uint64_t* p) { return reinterpret_cast<const ulonglong2*>(p); }
+__device__ __forceinline__ ulonglong2* v2(uint64_t* p) { return reinterpret_cast<ulonglong2*>(p); }
+
+dim3 rows_grid(int logn, int64_t rows) {
+    const int per_block = PW_THREADS * 2;
+    unsigned gx = (unsigned)(((1 << logn) + per_block - 1) / per_block);
+    unsigned gy = (unsigned)(rows < 65535 ? rows : 65535);
+    return dim3(gx, gy);
+}
+
+// ---------------------------------------------------------------- add
+__global__ void k_add(const uint64_t* __restrict__ a, int la, const uint64_t* __restrict__ b, int lb, int64_t cnt,
+                      int lo, uint64_t* __restrict__ out, const ModInfo* __restrict__ mods, int logn) {
+    const int64_t rows = cnt * 2 * (lo + 1);
+    const int n2 = 1 << (logn - 1);
+    for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
+        const int i = (int)(row % (lo + 1));
+        const int64_t cp = row / (lo + 1);
+        const uint64_t q = mods[i].q;
+        const uint64_t* pa = a + (((size_t)cp * (la + 1) + i) << logn);
+        const uint64_t* pb = b + (((size_t)cp * (lb + 1) + i) << logn);
+        uint64_t* po = out + (((size_t)cp * (lo + 1) + i) << logn);
+        for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n2; k += gridDim.x * blockDim.x) {
+            ulonglong2 x = v2(pa)[k], y = v2(pb)[k];
+            v2(po)[k] = make_ulonglong2(addmod(x.x, y.x, q), addmod(x.y, y.y, q));
+        }
+    }
+}
+
+// ---------------------------------------------------------------- scalar const multiply
+__global__ void k_mul_const(const uint64_t* __restrict__ a, int64_t cnt, int l, const ulonglong2* __restrict__ w,
+                            uint64_t* __restrict__ out, const ModInfo* __restrict__ mods, int logn) {
+    const int64_t rows = cnt * 2 * (l + 1);
+    const int n2 = 1 << (logn - 1);
+    for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
+        const int i = (int)(row % (l + 1));
+        const int64_t c = row / (2 * (l + 1));
+        const uint64_t q = mods[i].q;
+        const ulonglong2 wi = w[c * (l + 1) + i];
+        const uint64_t* pa = a + ((size_t)row << logn);
+        uint64_t* po = out + ((size_t)row << logn);
+        for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n2; k += gridDim.x * blockDim.x) {
+            ulonglong2 x = v2(pa)[k];
+            v2(po)[k] = make_ulonglong2(shoup(x.x, wi.x, wi.y, q), shoup(x.y, wi.x, wi.y, q));
+        }
+    }
+}
+
+// ---------------------------------------------------------------- add constant (poly 0 only)
+__global__ void k_add_const(const uint64_t* __restrict__ a, int64_t cnt, int l, const uint64_t* __restrict__ kc,
+                            uint64_t* __restrict__ out, const ModInfo* __restrict__ mods, int logn) {
+    const int64_t rows = cnt * 2 * (l + 1);
+    const int n2 = 1 << (logn - 1);
+    for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
+        const int i = (int)(row % (l + 1));
+        const int p = (int)((row / (l + 1)) % 2);
+        const int64_t c = row / (2 * (l + 1));
+        const uint64_t q = mods[i].q;
+        const uint64_t kk = (p == 0) ? kc[c * (l + 1) + i] : 0;
+        const uint64_t* pa = a + ((size_t)row << logn);
+        uint64_t* po = out + ((size_t)row << logn);
+        for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n2; k += gridDim.x * blockDim.x) {
+            ulonglong2 x = v2(pa)[k];
+            v2(po)[k] = make_ulonglong2(addmod(x.x, kk, q), addmod(x.y, kk, q));
+        }
+    }
+}
+
+// ---------------------------------------------------------------- mod drop (copy limbs 0..lo)
+__global__ void k_mod_drop(const uint64_t* __restrict__ a, int64_t cnt, int la, int lo, uint64_t* __restrict__ out,
+                           int logn) {
+    const int64_t rows = cnt * 2 * (lo + 1);
+    const int n2 = 1 << (logn - 1);
+    for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
+        const int i = (int)(row % (lo + 1));
+        const int64_t cp = row / (lo + 1);
+        const uint64_t* pa = a + (((size_t)cp * (la + 1) + i) << logn);
+        uint64_t* po = out + ((size_t)row << logn);
+        for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n2; k += gridDim.x * blockDim.x) v2(po)[k] = v2(pa)[k];
+    }
+}
+
+// ---------------------------------------------------------------- in-place x mod q (after NCCL uint64 sum)
+__global__ void k_mod_reduce(uint64_t* __restrict__ x, int64_t cnt, int l, const ModInfo* __restrict__ mods,
+                             int logn) {
+    const int64_t rows = cnt * 2 * (l + 1);
+    const int n2 = 1 << (logn - 1);
+    for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
+        const ModInfo m = mods[row % (l + 1)];
+        uint64_t* p = x + ((size_t)row << logn);
+        for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n2; k += gridDim.x * blockDim.x) {
+            ulonglong2 v = v2(p)[k];
+            v2(p)[k] = make_ulonglong2(reduce64(v.x, m), reduce64(v.y, m));
+        }
+    }
+}
+
+// ---------------------------------------------------------------- v + mod_drop(w) + const
+__global__ void k_add_add_const(const uint64_t* __restrict__ v, const uint64_t* __restrict__ w, int lw, int64_t cnt,
+                                int lo, const uint64_t* __restrict__ kc, uint64_t* __restrict__ out,
+                                const ModInfo* __restrict__ mods, int logn) {
+    const int64_t rows = cnt * 2 * (lo + 1);
+    const int n2 = 1 << (logn - 1);
+    for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
+        const int i = (int)(row % (lo + 1));
+        const int64_t cp = row / (lo + 1);
+        const int p = (int)(cp % 2);
+        const int64_t c = cp / 2;
+        const uint64_t q = mods[i].q;
+        const uint64_t kk = (p == 0 && kc) ? kc[c * (lo + 1) + i] : 0;
+        const uint64_t* pv = v + ((size_t)row << logn);
+        const uint64_t* pw = w + (((size_t)cp * (lw + 1) + i) << logn);
+        uint64_t* po = out + ((size_t)row << logn);
+        for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n2; k += gridDim.x * blockDim.x) {
+            ulonglong2 x = v2(pv)[k], y = v2(pw)[k];
+            v2(po)[k] = make_ulonglong2(addmod(addmod(x.x, y.x, q), kk, q), addmod(addmod(x.y, y.y, q), kk, q));
+        }
+    }
+}
+
+// ---------------------------------------------------------------- cross-correlation MAC
+// grid: x = coefficient blocks, y = poly*(l+1) + limb, z = output window (r*Wo + c).
+// Each thread owns one coefficient of one window and keeps up to FC filters' 128-bit
+// accumulators in registers, so each input residue is read from HBM once per window.
+constexpr int CC_FC = 8;
+
+__global__ void __launch_bounds__(PW_THREADS)
+k_cc_mac(const uint64_t* __restrict__ x, int l, int H, int W, int F, int kh, int kw, int stride,
+         const uint64_t* __restrict__ wk, uint64_t* __restrict__ out, const ModInfo* __restrict__ mods, int logn) {
+    extern __shared__ uint64_t wsm[];   // [F][taps] residues for this limb
+    const int nl = l + 1;
+    const int p = blockIdx.y / nl, i = blockIdx.y % nl;
+    const int Wo = (W - kw) / stride + 1;
+    const int Ho = (H - kh) / stride + 1;
+    const int win = blockIdx.z;
+    const int wr = win / Wo, wc = win % Wo;
+    const int taps = kh * kw;
+    for (int t = threadIdx.x; t < F * taps; t += blockDim.x) wsm[t] = wk[(size_t)t * nl + i];
+    __syncthreads();
+    const ModInfo m = mods[i];
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= (1 << logn)) return;
+    for (int f0 = 0; f0 < F; f0 += CC_FC) {
+        U128 acc[CC_FC];
+#pragma unroll
+        for (int f = 0; f < CC_FC; f++) acc[f].lo = acc[f].hi = 0;
+        for (int u = 0; u < kh; u++) {
+            for (int v = 0; v < kw; v++) {
+                const int pix = (wr * stride + u) * W + (wc * stride + v);
+                const uint64_t xv = x[limb_off(pix, p, i, nl, logn) + n];
+                const int t = u * kw + v;
+#pragma unroll
+                for (int f = 0; f < CC_FC; f++)
+                    if (f0 + f < F) mac128(acc[f], xv, wsm[(f0 + f) * taps + t]);
+            }
+        }
+#pragma unroll
+        for (int f = 0; f < CC_FC; f++) {
+            if (f0 + f < F) {
+                const int64_t o = (int64_t)(f0 + f) * Ho * Wo + win;
+                out[limb_off(o, p, i, nl, logn) + n] = barrett128(acc[f], m);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- dense MAC
+// grid: x = coefficient blocks, y = poly*(l+1) + limb, z = output chunk of DN_OC.
+constexpr int DN_OC = 16;
+constexpr int DN_KC = 256;    // fold 128-bit accumulators every 256 terms (K*q^2 < 2^128)
+
+__global__ void __launch_bounds__(PW_THREADS)
+k_dense_mac(const uint64_t* __restrict__ x, int64_t K, int64_t O, int l, const uint64_t* __restrict__ wd,
+            uint64_t* __restrict__ out, const ModInfo* __restrict__ mods, int logn) {
+    extern __shared__ uint64_t wsm[];   // [DN_OC][DN_KC]
+    const int nl = l + 1;
+    const int p = blockIdx.y / nl, i = blockIdx.y % nl;
+    const int64_t o0 = (int64_t)blockIdx.z * DN_OC;
+    const ModInfo m = mods[i];
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool active = n < (1 << logn);
+    uint64_t folded[DN_OC];
+#pragma unroll
+    for (int o = 0; o < DN_OC; o++) folded[o] = 0;
+    for (int64_t k0 = 0; k0 < K; k0 += DN_KC) {
+        const int kc = (int)((K - k0) < DN_KC ? (K - k0) : DN_KC);
+        __syncthreads();
+        for (int t = threadIdx.x; t < DN_OC * DN_KC; t += blockDim.x) {
+            const int o = t / DN_KC, k = t % DN_KC;
+            wsm[t] = (o0 + o < O && k < kc) ? wd[((size_t)(o0 + o) * K + (k0 + k)) * nl + i] : 0;
+        }
+        __syncthreads();
+        if (!active) continue;
+        U128 acc[DN_OC];
+#pragma unroll
+        for (int o = 0; o < DN_OC; o++) acc[o].lo = acc[o].hi = 0;
+        for (int k = 0; k < kc; k++) {
+            const uint64_t xv = x[limb_off(k0 + k, p, i, nl, logn) + n];
+#pragma unroll
+            for (int o = 0; o < DN_OC; o++) mac128(acc[o], xv, wsm[o * DN_KC + k]);
+        }
+#pragma unroll
+        for (int o = 0; o < DN_OC; o++) folded[o] = addmod(folded[o], barrett128(acc[o], m), m.q);
+    }
+    if (!active) return;
+#pragma unroll
+    for (int o = 0; o < DN_OC; o++)
+        if (o0 + o < O) out[limb_off(o0 + o, p, i, nl, logn) + n] = folded[o];
+}
+
+}  // namespace
+
+void launch_add(const Dev& d, const uint64_t* a, int la, const uint64_t* b, int lb, int64_t cnt, int lo, uint64_t* out) {
+    EDL_LAUNCH(d, "k_add", k_add<<<rows_grid(d.logn, cnt * 2 * (lo + 1)), PW_THREADS, 0, d.st>>>(a, la, b, lb, cnt, lo, out, d.mods, d.logn));
+}
+
+void launch_mul_const(const Dev& d, const uint64_t* a, int64_t cnt, int l, const ulonglong2* w, uint64_t* out) {
+    EDL_LAUNCH(d, "k_mul_const", k_mul_const<<<rows_grid(d.logn, cnt * 2 * (l + 1)), PW_THREADS, 0, d.st>>>(a, cnt, l, w, out, d.mods, d.logn));
+}
+
+void launch_add_const(const Dev& d, const uint64_t* a, int64_t cnt, int l, const uint64_t* k, uint64_t* out) {
+    EDL_LAUNCH(d, "k_add_const", k_add_const<<<rows_grid(d.logn, cnt * 2 * (l + 1)), PW_THREADS, 0, d.st>>>(a, cnt, l, k, out, d.mods, d.logn));
+}
+
+void launch_mod_drop(const Dev& d, const uint64_t* a, int64_t cnt, int la, int lo, uint64_t* out) {
+    EDL_LAUNCH(d, "k_mod_drop", k_mod_drop<<<rows_grid(d.logn, cnt * 2 * (lo + 1)), PW_THREADS, 0, d.st>>>(a, cnt, la, lo, out, d.logn));
+}
+
+void launch_mod_reduce(const Dev& d, uint64_t* x, int64_t cnt, int l) {
+    EDL_LAUNCH(d, "k_mod_reduce", k_mod_reduce<<<rows_grid(d.logn, cnt * 2 * (l + 1)), PW_THREADS, 0, d.st>>>(x, cnt, l, d.mods, d.logn));
+}
+
+void launch_add_add_const(const Dev& d, const uint64_t* v, const uint64_t* w, int lw, int64_t cnt, int lo,
+                          const uint64_t* k, uint64_t* out) {
+    EDL_LAUNCH(d, "k_add_add_const", k_add_add_const<<<rows_grid(d.logn, cnt * 2 * (lo + 1)), PW_THREADS, 0, d.st>>>(v, w, lw, cnt, lo, k, out, d.mods,
+                                                                                   d.logn));
+}
+
+void launch_cc_mac(const Dev& d, const uint64_t* x, int l, int H, int W, int F, int kh, int kw, int stride,
+                   const uint64_t* wk, uint64_t* out) {
+    const int Ho = (H - kh) / stride + 1, Wo = (W - kw) / stride + 1;
+    dim3 grid((unsigned)(((1 << d.logn) + PW_THREADS - 1) / PW_THREADS), (unsigned)(2 * (l + 1)), (unsigned)(Ho * Wo));
+    size_t smem = (size_t)F * kh * kw * sizeof(uint64_t);
+    EDL_LAUNCH(d, "k_cc_mac", k_cc_mac<<<grid, PW_THREADS, smem, d.st>>>(x, l, H, W, F, kh, kw, stride, wk, out, d.mods, d.logn));
+}
+
+void launch_dense_mac(const Dev& d, const uint64_t* x, int64_t K, int64_t O, int l, const uint64_t* wd, uint64_t* out) {
+    dim3 grid((unsigned)(((1 << d.logn) + PW_THREADS - 1) / PW_THREADS), (unsigned)(2 * (l + 1)),
+              (unsigned)((O + DN_OC - 1) / DN_OC));
+    size_t smem = (size_t)DN_OC * DN_KC * sizeof(uint64_t);
+    EDL_LAUNCH(d, "k_dense_mac", k_dense_mac<<<grid, PW_THREADS, smem, d.st>>>(x, K, O, l, wd, out, d.mods, d.logn));
+}
+
+}  // namespace edl

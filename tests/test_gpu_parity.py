@@ -1,0 +1,274 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle, element by element.
+
+Integer work is compared bit-exactly on every residue (the north_star's bar); decrypted
+values within 1e-3 of float64.  Sizes span several tiles and ragged counts.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import ckks as ock, layers as olay, networks as onet, ring as oring  # noqa: E402
+from oracle.params import make_params, params_from_depth  # noqa: E402
+from synth import random_residues, c0_inputs, random_slots  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def edl():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2110_13638_b200 import edl as E
+    return E
+
+
+def _pair(E, depth=None, logn=None, bits=None, seed=1):
+    if depth is not None:
+        pp = E.params_from_depth(depth)
+        po = params_from_depth(depth)
+    else:
+        pp = E.params_from_bits(logn, bits)
+        po = make_params(1 << logn, list(bits))
+    assert pp.qs == po.q and pp.p_special == po.p_special and pp.psis == po.psi
+    g = E.Context(pp).keygen(seed)
+    o = ock.Context(po).keygen(seed)
+    return g, o
+
+
+@pytest.fixture(scope="module")
+def c0pair(edl):
+    return _pair(edl, depth=2)
+
+
+@pytest.fixture(scope="module")
+def c1pair(edl):
+    return _pair(edl, depth=4)
+
+
+def _rand_ct(o, cnt, lvl, seed):
+    mods = o.q[: lvl + 1] * (cnt * 2)
+    return random_residues((cnt, 2, lvl + 1, o.n), mods, seed=seed)
+
+
+def _to_gpu(g, data, lvl, scale, key):
+    return g.from_numpy(data, lvl, scale, key)
+
+
+# ---------------------------------------------------------------- NTT
+@pytest.mark.parametrize("logn", [10, 11, 12, 13, 14])
+def test_ntt_bit_exact(edl, logn):
+    bits = [60, 40, 40, 60] if logn < 14 else [60, 40, 40, 40, 40, 60]
+    pp = edl.params_from_bits(logn, bits)
+    g = edl.Context(pp)
+    po = make_params(1 << logn, bits)
+    lvl = len(bits) - 2
+    n_polys = 3
+    mods = po.q[: lvl + 1] * n_polys
+    psis = po.psi[: lvl + 1] * n_polys
+    a = random_residues((n_polys, lvl + 1, 1 << logn), mods, seed=logn)
+    t = torch.from_numpy(a.view(np.int64).reshape(-1).copy()).cuda()
+    g.ntt_(t, n_polys, lvl, inverse=False)
+    got = t.cpu().numpy().view(np.uint64).reshape(a.shape)
+    want = oring.ntt_fwd(a, mods, psis)
+    assert np.array_equal(got, want)
+    g.ntt_(t, n_polys, lvl, inverse=True)
+    back = t.cpu().numpy().view(np.uint64).reshape(a.shape)
+    assert np.array_equal(back, a)
+    # inverse of arbitrary residues too
+    t2 = torch.from_numpy(a.view(np.int64).reshape(-1).copy()).cuda()
+    g.ntt_(t2, n_polys, lvl, inverse=True)
+    assert np.array_equal(t2.cpu().numpy().view(np.uint64).reshape(a.shape), oring.ntt_inv(a, mods, psis))
+
+
+def test_ntt_special_prime_limb(edl):
+    pp = edl.params_from_depth(2)
+    g = edl.Context(pp)
+    po = params_from_depth(2)
+    n = po.n
+    a = random_residues((2, 4, n), po.moduli * 2, seed=9)
+    t = torch.from_numpy(a.view(np.int64).reshape(-1).copy()).cuda()
+    g.ntt_(t, 2, 3)   # level L+1 = includes P as limb 3
+    assert np.array_equal(t.cpu().numpy().view(np.uint64).reshape(a.shape), oring.ntt_fwd(a, po.moduli * 2, po.psi * 2))
+
+
+# ---------------------------------------------------------------- Philox / keys / encryption
+def test_philox_words(edl, c0pair):
+    from oracle import sampling
+    g, _ = c0pair
+    rng = np.random.default_rng(0)
+    ctr = rng.integers(0, 2 ** 32, (257, 4), dtype=np.uint64).astype(np.uint32)
+    for seed in (0, 1, 0xDEADBEEFCAFEF00D):
+        got = g.philox(seed, ctr)
+        want = np.stack([sampling.philox4x32_10(c, (seed & 0xFFFFFFFF, seed >> 32)) for c in ctr])
+        assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("which", ["c0", "c1"])
+def test_keygen_bit_exact(which, c0pair, c1pair):
+    g, o = c0pair if which == "c0" else c1pair
+    assert np.array_equal(g.export_key(0), o.s_hat)
+    assert np.array_equal(g.export_key(1), o.pk)
+    assert np.array_equal(g.export_key(2), o.rlk)
+
+
+@pytest.mark.parametrize("level", [None, 1])
+def test_encrypt_bit_exact(c1pair, level):
+    g, o = c1pair
+    z = random_slots(5, 8192, seed=3)
+    polys = np.stack([o.encode(v) for v in z])            # same integer polys on both sides (Z1)
+    want = o.encrypt_poly(polys, enc_seed=2, obj0=7, scale=o.p.scale, level=level)
+    got = g.encrypt_poly(polys, scale=o.p.scale, enc_seed=2, obj0=7, level=level)
+    assert got.level == want.level and got.count == 5
+    assert np.array_equal(got.numpy(g.n), want.data)
+
+
+def test_encode_contract(c1pair):
+    """Z1: host FFT encode vs oracle encode: |dm| <= 1 and <= 1% of coefficients differ."""
+    g, o = c1pair
+    z = random_slots(3, 8192, seed=5)
+    got = g.encode(z)
+    want = np.stack([o.encode(v) for v in z])
+    d = np.abs(got - want)
+    assert d.max() <= 1 and (d > 0).mean() <= 0.01
+
+
+def test_decrypt_matches_oracle(c0pair):
+    g, o = c0pair
+    z = random_slots(4, 4096, seed=6, lo=-1, hi=1)
+    polys = np.stack([o.encode(v) for v in z])
+    ct_g = g.encrypt_poly(polys, scale=o.p.scale, enc_seed=2)
+    ct_o = o.encrypt_poly(polys, 2, 0, o.p.scale)
+    dp = g.decrypt_poly(ct_g)
+    want = np.array(o.decrypt_poly(ct_o), dtype=object)
+    assert [[int(v) for v in row] for row in dp] == [[int(v) for v in row] for row in want]
+    assert np.max(np.abs(g.decrypt(ct_g, 4096) - z)) < 1e-6
+
+
+# ---------------------------------------------------------------- ciphertext ops
+@pytest.mark.parametrize("cnt", [1, 3, 7])
+def test_ops_bit_exact(c1pair, cnt):
+    g, o = c1pair
+    L = o.L
+    sc = o.p.scale
+    A = ock.CtArray(_rand_ct(o, cnt, L, 11 + cnt), L, sc, o.key_id)
+    B = ock.CtArray(_rand_ct(o, cnt, L, 12 + cnt), L, sc, o.key_id)
+    ga, gb = _to_gpu(g, A.data, L, sc, o.key_id), _to_gpu(g, B.data, L, sc, o.key_id)
+    assert np.array_equal(g.add(ga, gb).numpy(g.n), o.add(A, B).data)
+    w = np.linspace(-1.5, 2.0, cnt)
+    assert np.array_equal(g.pt_mul(ga, w, 2.0 ** 30).numpy(g.n), o.mul_scalar(A, w, 2.0 ** 30).data)
+    assert np.array_equal(g.pt_add(ga, w).numpy(g.n), o.add_scalar(A, w).data)
+    r_g, r_o = g.rescale(ga), o.rescale(A)
+    assert r_g.level == r_o.level and r_g.scale == r_o.scale
+    assert np.array_equal(r_g.numpy(g.n), r_o.data)
+    assert np.array_equal(g.mod_drop(ga, 2).numpy(g.n), o.mod_drop(A, 2).data)
+    # add with auto mod-drop of the higher operand
+    assert np.array_equal(g.add(r_g, gb).numpy(g.n), o.add(r_o, B).data)
+
+
+@pytest.mark.parametrize("lvl", [1, 2, 3, 4])
+def test_mul_relin_bit_exact(c1pair, lvl):
+    g, o = c1pair
+    cnt = 2
+    A = ock.CtArray(_rand_ct(o, cnt, lvl, 21 + lvl), lvl, 2.0 ** 40, o.key_id)
+    B = ock.CtArray(_rand_ct(o, cnt, lvl, 31 + lvl), lvl, 2.0 ** 40, o.key_id)
+    got = g.mul_relin(_to_gpu(g, A.data, lvl, A.scale, o.key_id), _to_gpu(g, B.data, lvl, B.scale, o.key_id))
+    want = o.mul_relin(A, B)
+    assert got.scale == want.scale
+    assert np.array_equal(got.numpy(g.n), want.data)
+
+
+def test_mul_relin_mixed_levels(c0pair):
+    g, o = c0pair
+    A = ock.CtArray(_rand_ct(o, 2, 2, 41), 2, 2.0 ** 40, o.key_id)
+    B = ock.CtArray(_rand_ct(o, 2, 1, 42), 1, 2.0 ** 40, o.key_id)
+    got = g.mul_relin(_to_gpu(g, A.data, 2, A.scale, o.key_id), _to_gpu(g, B.data, 1, B.scale, o.key_id))
+    assert got.level == 1
+    assert np.array_equal(got.numpy(g.n), o.mul_relin(A, B).data)
+
+
+# ---------------------------------------------------------------- layers
+def test_layers_small_bit_exact(c1pair):
+    """CC (8x8 image, 2 filters) -> sigma_a -> dense 8->3 on ciphertexts encrypted by both sides."""
+    g, o = c1pair
+    rng = np.random.default_rng(0)
+    B = 8192
+    imgs = rng.integers(0, 256, (B, 8, 8)) / 255.0
+    K, kb = rng.normal(0, 0.1, (2, 4, 4)), rng.normal(0, 0.1, 2)
+    W, b = rng.normal(0, 0.1, (3, 8)), rng.normal(0, 0.1, 3)
+    polys = np.stack([o.encode(v) for v in imgs.reshape(B, 64).T])
+    xo = o.encrypt_poly(polys, 2, 0, o.p.scale)
+    xg = g.encrypt_poly(polys, scale=o.p.scale, enc_seed=2)
+    cc_o = olay.cross_correlate(o, xo, 8, 8, K, 4, kb)
+    cc_g = g.cross_correlate(xg, 8, 8, K, 4, kb)
+    assert cc_g.scale == cc_o.scale and np.array_equal(cc_g.numpy(g.n), cc_o.data)
+    act_o = olay.poly_activation(o, cc_o, onet.SIGMA_A)
+    act_g = g.poly_activation(cc_g, onet.SIGMA_A)
+    assert act_g.level == act_o.level and act_g.scale == act_o.scale
+    assert np.array_equal(act_g.numpy(g.n), act_o.data)
+    out_o = olay.dense(o, act_o, W, b)
+    out_g = g.dense(act_g, W, b)
+    assert np.array_equal(out_g.numpy(g.n), out_o.data)
+    want = onet.sigma_a(onet.cc_float64(imgs, K, kb)) @ W.T + b
+    assert np.max(np.abs(g.decrypt(out_g, B).T - want)) < 1e-3
+
+
+def test_dense_ragged_and_deferred(c1pair):
+    """Dense with K > 256 (accumulator folding), O > 16 (several output chunks), and the
+    C4 deferred-rescale + uint64 combine + mod_reduce path (O15)."""
+    g, o = c1pair
+    lvl, K, O = 2, 300, 19
+    X = ock.CtArray(_rand_ct(o, K, lvl, 51), lvl, 2.0 ** 40, o.key_id)
+    W = np.random.default_rng(1).normal(0, 0.1, (O, K))
+    xg = _to_gpu(g, X.data, lvl, X.scale, o.key_id)
+    assert np.array_equal(g.dense(xg, W, None).numpy(g.n), olay.dense(o, X, W, None).data)
+    full = olay.dense_partial(o, X, W)
+    parts = []
+    for r in range(3):
+        sl = list(range(r * K // 3, (r + 1) * K // 3))
+        parts.append(g.dense(_to_gpu(g, X.data[sl], lvl, X.scale, o.key_id), W[:, sl], None, defer_rescale=True))
+    acc = parts[0]
+    acc.tensor = parts[0].tensor + parts[1].tensor + parts[2].tensor      # int64 add == uint64 wrap
+    g.mod_reduce(acc)
+    assert np.array_equal(acc.numpy(g.n), full.data)
+    b = np.arange(O) * 0.01
+    assert np.array_equal(g.dense_finish(acc, b).numpy(g.n), olay.dense_finish(o, full, b).data)
+
+
+def test_c0_end_to_end(c0pair):
+    from paper_2110_13638_b200.networks import C0Net
+    g, o = c0pair
+    inp = c0_inputs()
+    polys = np.stack([o.encode(v) for v in inp.X.T])
+    xo = o.encrypt_poly(polys, 2, 0, o.p.scale)
+    xg = g.encrypt_poly(polys, scale=o.p.scale, enc_seed=2)
+    ro = onet.c0_forward(o, xo, inp.W, inp.b)
+    rg = C0Net(g, inp.W, inp.b).forward(xg, keep=True)
+    assert np.array_equal(rg["dense"].numpy(g.n), ro["dense"].data)
+    assert np.array_equal(rg["out"].numpy(g.n), ro["out"].data)
+    got = g.decrypt(rg["out"], 64).T
+    assert np.max(np.abs(got - onet.c0_float64(inp.X, inp.W, inp.b))) < 1e-3
+
+
+# ---------------------------------------------------------------- errors / edge cases
+def test_errors_and_empty(edl, c0pair):
+    g, o = c0pair
+    A = _to_gpu(g, _rand_ct(o, 2, 0, 61), 0, 2.0 ** 40, o.key_id)
+    with pytest.raises(edl.LevelError):
+        g.rescale(A)
+    B = _to_gpu(g, _rand_ct(o, 2, 0, 62), 0, 2.0 ** 41, o.key_id)
+    with pytest.raises(edl.ScaleError):
+        g.add(A, B)
+    C = _to_gpu(g, _rand_ct(o, 2, 0, 63), 0, 2.0 ** 40, o.key_id + 99)
+    with pytest.raises(edl.KeyMismatch):
+        g.add(A, C)
+    D = _to_gpu(g, _rand_ct(o, 3, 0, 64), 0, 2.0 ** 40, o.key_id)
+    with pytest.raises(edl.ShapeMismatch):
+        g.add(A, D)
+    with pytest.raises(edl.CapacityError):
+        g.encode(np.zeros((1, 4097)))
+    with pytest.raises(edl.ArgError):
+        g.poly_activation(_to_gpu(g, _rand_ct(o, 1, 2, 65), 2, 2.0 ** 40, o.key_id), (1, 2, 3, 4, 5))
+    E = g.empty(0, 2)
+    E.key_id, E.scale = o.key_id, 2.0 ** 40
+    assert g.add(E, E).count == 0
+    assert g.rescale(E).count == 0
