@@ -524,7 +524,7 @@ edl_status edl_rescale(edl_ctx* c, const edl_cts* in, edl_cts* out) {
     if (s != EDL_OK) return s;
     const int l = in->level;
     if (l < 1) return fail(c, EDL_ERR_LEVEL, "LevelExhausted: rescale at level 0");
-    if (out->data == in->data) return fail(c, EDL_ERR_ARG, "rescale: out aliases in");
+    if (in->count > 0 && out->data == in->data) return fail(c, EDL_ERR_ARG, "rescale: out aliases in");
     if (in->count > 0) {
         uint64_t* r = scratch(c, (size_t)in->count * 2 * c->N);
         if (!r) return fail(c, EDL_ERR_CUDA, "rescale: scratch");
@@ -542,7 +542,8 @@ edl_status edl_ct_ct_mul_relin(edl_ctx* c, const edl_cts* a, const edl_cts* b, e
     if ((s = check_ct(c, a)) != EDL_OK || (s = check_ct(c, b)) != EDL_OK) return s;
     if (a->key_id != b->key_id) return fail(c, EDL_ERR_KEY, "KeyMismatch");
     if (a->count != b->count) return fail(c, EDL_ERR_SHAPE, "ShapeMismatch: counts differ");
-    if (out->data == a->data || out->data == b->data) return fail(c, EDL_ERR_ARG, "mul_relin: out aliases input");
+    if (a->count > 0 && (out->data == a->data || out->data == b->data))
+        return fail(c, EDL_ERR_ARG, "mul_relin: out aliases input");
     const int l = a->level < b->level ? a->level : b->level;
     const int64_t cnt = a->count;
     if (cnt > 0) {
@@ -680,7 +681,7 @@ edl_status edl_poly_activation(edl_ctx* c, const edl_cts* x, const double* coeff
     if (!c->has_key) return fail(c, EDL_ERR_NOKEY, "poly_activation: no relinearisation key");
     edl_status s = check_ct(c, x);
     if (s != EDL_OK) return s;
-    if (out->data == x->data) return fail(c, EDL_ERR_ARG, "poly_activation: out aliases x");
+    if (x->count > 0 && out->data == x->data) return fail(c, EDL_ERR_ARG, "poly_activation: out aliases x");
     const int l = x->level;
     const int64_t cnt = x->count;
     Dev d = c->dev();

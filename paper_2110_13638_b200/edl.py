@@ -257,6 +257,11 @@ class Context:
         t = self.torch.empty(words, dtype=self.torch.int64, device=self.device)
         return CtArray(t, count, level, 0.0, 0)
 
+    def wrap(self, tensor, count: int, level: int, scale: float = 0.0) -> CtArray:
+        """View an existing int64 device tensor as a ciphertext array under this context's key."""
+        assert tensor.numel() == cts_bytes(count, level, self.logn) // 8
+        return CtArray(tensor, count, level, scale, self.key_id or 0)
+
     def from_numpy(self, data: np.ndarray, level: int, scale: float, key_id: int) -> CtArray:
         t = self.torch.from_numpy(np.ascontiguousarray(data).view(np.int64).reshape(-1).copy()).to(self.device)
         return CtArray(t, data.shape[0], level, scale, key_id)

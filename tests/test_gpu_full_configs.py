@@ -1,0 +1,76 @@
+"""Full-size parity at BASELINE.json's configs, in the launch configuration bench.py times.
+
+C1 (784 pixel ciphertexts, 8192 images): every residue of every layer boundary equals
+the oracle's (the oracle run takes about a minute on one core), decrypted logits lie
+within 1e-3 of float64 plaintext inference, and argmax agrees on non-near-tie samples.
+C3 (tabular, 2 slot-batches x 32 features): same checks, plus the MSE vs float64.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2110_13638_b200 import edl
+    return edl
+
+
+@pytest.mark.timeout(900)
+def test_c1_full_bit_exact(gpu):
+    from oracle import layers, networks as onet
+    from paper_2110_13638_b200.networks import C1Net
+    from synth import c1_inputs, c1_slots
+
+    inp = c1_inputs(8192)
+    octx = onet.c1_context(1)
+    ctx = gpu.Context(gpu.params_from_depth(4)).keygen(1)
+    polys = np.stack([octx.encode(z) for z in c1_slots(inp.images)])
+    xo = octx.encrypt_poly(polys, 2, 0, octx.p.scale)
+    xg = ctx.encrypt_poly(polys, scale=octx.p.scale, enc_seed=2)
+    assert np.array_equal(xg.numpy(ctx.n), xo.data)
+    rg = C1Net(ctx, inp.K, inp.kb, inp.W, inp.b).forward(xg, keep=True)
+    cc = layers.cross_correlate(octx, xo, 28, 28, inp.K, 4, inp.kb)
+    assert np.array_equal(rg["cc"].numpy(ctx.n), cc.data)
+    act = layers.poly_activation(octx, cc, onet.SIGMA_A)
+    assert np.array_equal(rg["act"].numpy(ctx.n), act.data)
+    out = layers.dense(octx, act, inp.W, inp.b)
+    assert np.array_equal(rg["out"].numpy(ctx.n), out.data)
+    assert rg["out"].scale == out.scale and rg["out"].level == out.level == 0
+    got = ctx.decrypt(rg["out"], 8192).T                      # (8192, 10)
+    ref = onet.c1_float64(inp.images, inp.K, inp.kb, inp.W, inp.b)
+    assert np.max(np.abs(got - ref)) < 1e-3
+    top2 = np.sort(ref, axis=1)[:, -2:]
+    clear = (top2[:, 1] - top2[:, 0]) > 1e-3
+    assert np.array_equal(got.argmax(1)[clear], ref.argmax(1)[clear])
+
+
+@pytest.mark.timeout(900)
+def test_c3_full_bit_exact(gpu):
+    from oracle import networks as onet
+    from paper_2110_13638_b200.networks import C3Net
+    from synth import c3_inputs
+
+    inp = c3_inputs()
+    octx = onet.c3_context(1)
+    ctx = gpu.Context(gpu.params_from_depth(4)).keygen(1)
+    net = C3Net(ctx, inp.W1, inp.b1, inp.W2, inp.b2)
+    preds = []
+    for bidx in range(2):                                    # reading Z12: 2 slot-batches
+        Xb = inp.X[bidx * 8192:(bidx + 1) * 8192]
+        polys = np.stack([octx.encode(z) for z in Xb.T])
+        xo = octx.encrypt_poly(polys, 2, 32 * bidx, octx.p.scale)
+        xg = ctx.encrypt_poly(polys, scale=octx.p.scale, enc_seed=2, obj0=32 * bidx)
+        ro = onet.c3_forward(octx, xo, inp.W1, inp.b1, inp.W2, inp.b2)
+        rg = net.forward(xg, keep=True)
+        for k in ("dense1", "act", "out"):
+            assert np.array_equal(rg[k].numpy(ctx.n), ro[k].data), k
+        preds.append(ctx.decrypt(rg["out"], 8192)[0])
+    pred = np.concatenate(preds)
+    ref = onet.c3_float64(inp.X, inp.W1, inp.b1, inp.W2, inp.b2)[:, 0]
+    assert np.max(np.abs(pred - ref)) < 1e-3
+    assert float(np.mean((pred - ref) ** 2)) < 1e-8

@@ -161,8 +161,12 @@ def test_ops_bit_exact(c1pair, cnt):
     assert r_g.level == r_o.level and r_g.scale == r_o.scale
     assert np.array_equal(r_g.numpy(g.n), r_o.data)
     assert np.array_equal(g.mod_drop(ga, 2).numpy(g.n), o.mod_drop(A, 2).data)
-    # add with auto mod-drop of the higher operand
-    assert np.array_equal(g.add(r_g, gb).numpy(g.n), o.add(r_o, B).data)
+    # add with auto mod-drop of the higher operand (operands at matching scales)
+    B2 = ock.CtArray(B.data, L, r_o.scale, o.key_id)
+    gb2 = _to_gpu(g, B.data, L, r_o.scale, o.key_id)
+    s_g, s_o = g.add(r_g, gb2), o.add(r_o, B2)
+    assert s_g.level == s_o.level == L - 1
+    assert np.array_equal(s_g.numpy(g.n), s_o.data)
 
 
 @pytest.mark.parametrize("lvl", [1, 2, 3, 4])
