@@ -185,14 +185,6 @@ std::vector<uint64_t> residues(const edl_ctx* c, const std::vector<int64_t>& int
     return r;
 }
 
-// ct x scalar at pt_scale, then rescale (fused: 2 launches).  out level l-1.
-void scalar_rescale(edl_ctx* c, const uint64_t* y, int64_t cnt, int l, const ulonglong2* w, uint64_t* r,
-                    uint64_t* out) {
-    Dev d = c->dev();
-    launch_rescale_intt(d, y, cnt, l, w, r);
-    launch_rescale_ntt(d, y, cnt, l, w, r, nullptr, out);
-}
-
 }  // namespace
 
 extern "C" {
@@ -722,10 +714,12 @@ edl_status edl_poly_activation(edl_ctx* c, const edl_cts* x, const double* coeff
         const ulonglong2* w3 = upload(c, shoup_consts(c, i3, l));
         const ulonglong2* w1 = upload(c, shoup_consts(c, i1, l));
         const uint64_t* k0 = upload(c, residues(c, i0, l - 1));
+        uint64_t* r2 = rsc;   // second INTT output shares the relin scratch (used before relin 3.)
         launch_relin(d, x->data, x->data, cnt, l, true, c->d_rlk, c->d_rlk_s, rsc, y2);   // 1.
-        scalar_rescale(c, x->data, cnt, l, w3, r, u);                                          // 2.
+        launch_rescale_intt(d, x->data, cnt, l, w3, r, w1, r2);                             // 2.+4. INTT shared
+        launch_rescale_ntt(d, x->data, cnt, l, w3, r, nullptr, u);                          // 2.
+        launch_rescale_ntt(d, x->data, cnt, l, w1, r2, nullptr, w);                         // 4.
         launch_relin(d, u, y2, cnt, l - 1, true, c->d_rlk, c->d_rlk_s, rsc, v);              // 3.
-        scalar_rescale(c, x->data, cnt, l, w1, r, w);                                          // 4.
         launch_add_add_const(d, v, w, l - 1, cnt, l - 2, k0, out->data);                       // 5.
     }
     set_meta(out, cnt, l - 2, S3, x->key_id);

@@ -59,7 +59,8 @@ struct Dev {
 // ---- NTT family (ntt_kernels.cu) ----
 void launch_ntt_limbs(const Dev& d, uint64_t* data, int64_t batch, int nl, const int* prime_idx_host, bool inverse);
 // rescale: r_out [cnt][2][N] <- INTT_{q_l}(in[.][.][l] * w_l) ; w may be null
-void launch_rescale_intt(const Dev& d, const uint64_t* in, int64_t cnt, int l, const ulonglong2* w, uint64_t* r_out);
+void launch_rescale_intt(const Dev& d, const uint64_t* in, int64_t cnt, int l, const ulonglong2* w, uint64_t* r_out,
+                         const ulonglong2* w2 = nullptr, uint64_t* r_out2 = nullptr);
 // out [cnt][2][l][N] <- (in_i * w_i - NTT_i([r]_{q_l} mod q_i)) * q_l^{-1} (+ bias_i on poly 0)
 void launch_rescale_ntt(const Dev& d, const uint64_t* in, int64_t cnt, int l, const ulonglong2* w,
                         const uint64_t* r, const uint64_t* bias, uint64_t* out);

@@ -20,10 +20,16 @@
 
 namespace edl {
 
-template <int LOGN>
+// Residues per thread: the plain transform keeps 32 per thread (fewer exchanges); the
+// fused kernels, whose prologue/epilogue need registers and more warps to hide their
+// extra global traffic, keep 16 (N = 2^14: 1024 threads).  Measured in round 1.
+__host__ __device__ constexpr int loge_plain(int logn) { return logn >= 14 ? 5 : (logn >= 12 ? 4 : 3); }
+__host__ __device__ constexpr int loge_fused(int logn) { return logn >= 14 ? 4 : 3; }
+
+template <int LOGN, int LOGE_ = loge_fused(LOGN)>
 struct NttShape {
     static constexpr int N = 1 << LOGN;
-    static constexpr int LOGE = (LOGN >= 14) ? 5 : (LOGN >= 12 ? 4 : 3);
+    static constexpr int LOGE = LOGE_;
     static constexpr int E = 1 << LOGE;
     static constexpr int T = N / E;
     static constexpr int NPASS = (LOGN + LOGE - 1) / LOGE;
@@ -89,9 +95,9 @@ __device__ __forceinline__ void inv_pass_regs(uint64_t* x, int high, const ModIn
 }
 
 // Compile-time pass descriptor: pass P covers stages [P*LOGE, min((P+1)*LOGE, LOGN)).
-template <int LOGN, int P>
+template <int LOGN, int LOGE, int P>
 struct PassInfo {
-    using S = NttShape<LOGN>;
+    using S = NttShape<LOGN, LOGE>;
     static constexpr int S0 = P * S::LOGE;
     static constexpr int NS = (S0 + S::LOGE <= LOGN) ? S::LOGE : (LOGN - S0);
     static constexpr int BTOP = LOGN - 1 - S0;
@@ -100,11 +106,11 @@ struct PassInfo {
 };
 
 // Forward middle/last pass: read from smem, compute, write back to smem (natural index).
-template <int LOGN, int P>
+template <int LOGN, int LOGE, int P>
 __device__ __forceinline__ void fwd_pass_smem(uint64_t* sm, const ulonglong2* __restrict__ tw, uint64_t q,
                                               uint64_t two_q) {
-    using PI = PassInfo<LOGN, P>;
-    using S = NttShape<LOGN>;
+    using PI = PassInfo<LOGN, LOGE, P>;
+    using S = NttShape<LOGN, LOGE>;
     uint64_t x[S::E];
 #pragma unroll
     for (int g = 0; g < PI::G; g++) {
@@ -134,10 +140,10 @@ __device__ __forceinline__ void fwd_pass_smem(uint64_t* sm, const ulonglong2* __
     __syncthreads();
 }
 
-template <int LOGN, int P>
+template <int LOGN, int LOGE, int P>
 __device__ __forceinline__ void inv_pass_smem(uint64_t* sm, const ModInfo& m, uint64_t two_q) {
-    using PI = PassInfo<LOGN, P>;
-    using S = NttShape<LOGN>;
+    using PI = PassInfo<LOGN, LOGE, P>;
+    using S = NttShape<LOGN, LOGE>;
     uint64_t x[S::E];
 #pragma unroll
     for (int g = 0; g < PI::G; g++) {
@@ -167,29 +173,29 @@ __device__ __forceinline__ void inv_pass_smem(uint64_t* sm, const ModInfo& m, ui
     __syncthreads();
 }
 
-template <int LOGN, int P>
+template <int LOGN, int LOGE, int P>
 __device__ __forceinline__ void fwd_middle(uint64_t* sm, const ulonglong2* tw, uint64_t q, uint64_t two_q) {
-    if constexpr (P < NttShape<LOGN>::NPASS) {
-        fwd_pass_smem<LOGN, P>(sm, tw, q, two_q);
-        fwd_middle<LOGN, P + 1>(sm, tw, q, two_q);
+    if constexpr (P < NttShape<LOGN, LOGE>::NPASS) {
+        fwd_pass_smem<LOGN, LOGE, P>(sm, tw, q, two_q);
+        fwd_middle<LOGN, LOGE, P + 1>(sm, tw, q, two_q);
     }
 }
 
 // Inverse passes run from the last pass down to pass 1 (pass 0 is register-resident).
-template <int LOGN, int P>
+template <int LOGN, int LOGE, int P>
 __device__ __forceinline__ void inv_middle(uint64_t* sm, const ModInfo& m, uint64_t two_q) {
     if constexpr (P > 0) {
-        inv_pass_smem<LOGN, P>(sm, m, two_q);
-        inv_middle<LOGN, P - 1>(sm, m, two_q);
+        inv_pass_smem<LOGN, LOGE, P>(sm, m, two_q);
+        inv_middle<LOGN, LOGE, P - 1>(sm, m, two_q);
     }
 }
 
 // Forward NTT of one limb.  load(idx) -> residue in [0, 4q) (called with idx = tid + T*r);
 // store(idx, value) receives canonical [0, q) values, idx = tid + T*r (coalesced).
-template <int LOGN, class Load, class Store>
+template <int LOGN, int LOGE = loge_fused(LOGN), class Load, class Store>
 __device__ __forceinline__ void ntt_fwd_block(uint64_t* sm, const ModInfo& m, Load load, Store store) {
-    using S = NttShape<LOGN>;
-    using P0 = PassInfo<LOGN, 0>;
+    using S = NttShape<LOGN, LOGE>;
+    using P0 = PassInfo<LOGN, LOGE, 0>;
     static_assert(P0::G == 1 && P0::BLOW == LOGN - S::LOGE, "pass 0 layout");
     const uint64_t q = m.q, two_q = 2 * q;
     const ulonglong2* tw = m.tw_fwd;
@@ -200,7 +206,7 @@ __device__ __forceinline__ void ntt_fwd_block(uint64_t* sm, const ModInfo& m, Lo
 #pragma unroll
     for (int r = 0; r < S::E; r++) sm[spad(threadIdx.x + r * S::T)] = x[r];
     __syncthreads();
-    fwd_middle<LOGN, 1>(sm, tw, q, two_q);
+    fwd_middle<LOGN, LOGE, 1>(sm, tw, q, two_q);
 #pragma unroll
     for (int r = 0; r < S::E; r++) {
         const int idx = threadIdx.x + r * S::T;
@@ -212,9 +218,9 @@ __device__ __forceinline__ void ntt_fwd_block(uint64_t* sm, const ModInfo& m, Lo
 }
 
 // Inverse NTT of one limb.  load(idx) -> residue in [0, 2q); store(idx, canonical value).
-template <int LOGN, class Load, class Store>
+template <int LOGN, int LOGE = loge_fused(LOGN), class Load, class Store>
 __device__ __forceinline__ void ntt_inv_block(uint64_t* sm, const ModInfo& m, Load load, Store store) {
-    using S = NttShape<LOGN>;
+    using S = NttShape<LOGN, LOGE>;
     const uint64_t q = m.q, two_q = 2 * q;
 #pragma unroll
     for (int r = 0; r < S::E; r++) {
@@ -222,7 +228,7 @@ __device__ __forceinline__ void ntt_inv_block(uint64_t* sm, const ModInfo& m, Lo
         sm[spad(idx)] = load(idx);
     }
     __syncthreads();
-    inv_middle<LOGN, S::NPASS - 1>(sm, m, two_q);
+    inv_middle<LOGN, LOGE, S::NPASS - 1>(sm, m, two_q);
     uint64_t x[S::E];
 #pragma unroll
     for (int r = 0; r < S::E; r++) x[r] = sm[spad(threadIdx.x + r * S::T)];

@@ -24,7 +24,7 @@ struct PrimeMap {
 // ------------------------------------------------------------------------------------
 // K1/K2: plain batched NTT / INTT, in place, data [batch][nl][N], limb j uses pm.idx[j].
 template <int LOGN, bool INV>
-__global__ void __launch_bounds__(NttShape<LOGN>::T, 1)
+__global__ void __launch_bounds__(NttShape<LOGN, loge_plain(LOGN)>::T, 1)
 k_ntt_limbs(uint64_t* __restrict__ data, int nl, PrimeMap pm, const ModInfo* __restrict__ mods) {
     extern __shared__ uint64_t sm[];
     const int limb = blockIdx.x;
@@ -32,27 +32,41 @@ k_ntt_limbs(uint64_t* __restrict__ data, int nl, PrimeMap pm, const ModInfo* __r
     const ModInfo m = mods[pm.idx[limb]];
     auto ld = [&](int idx) { return p[idx]; };
     auto st = [&](int idx, uint64_t v) { p[idx] = v; };
-    if constexpr (INV) ntt_inv_block<LOGN>(sm, m, ld, st);
-    else ntt_fwd_block<LOGN>(sm, m, ld, st);
+    if constexpr (INV) ntt_inv_block<LOGN, loge_plain(LOGN)>(sm, m, ld, st);
+    else ntt_fwd_block<LOGN, loge_plain(LOGN)>(sm, m, ld, st);
 }
 
 // ------------------------------------------------------------------------------------
-// K6 rescale, step 1 (O12): r = INTT_{q_l}(c[l] * w_l) for both polys of every ct.
+// K6 rescale, step 1 (O12): r = INTT_{q_l}(c[l] * w_l) for both polys of every ct.  With a
+// second constant w2 the same INTT also yields r2 = INTT(c[l] * w2_l) (INTT is linear),
+// which the sigma schedule uses for its two scalar products of y (O13 steps 2 and 4).
 template <int LOGN>
 __global__ void __launch_bounds__(NttShape<LOGN>::T, 1)
 k_rescale_intt(const uint64_t* __restrict__ in, int l, const ulonglong2* __restrict__ w,
-               uint64_t* __restrict__ r_out, const ModInfo* __restrict__ mods) {
+               uint64_t* __restrict__ r_out, const ulonglong2* __restrict__ w2, uint64_t* __restrict__ r_out2,
+               const ModInfo* __restrict__ mods) {
     extern __shared__ uint64_t sm[];
     const int p = blockIdx.x;
     const int64_t c = blockIdx.y;
     const uint64_t* src = in + limb_off(c, p, l, l + 1, LOGN);
     uint64_t* dst = r_out + (((size_t)c * 2 + p) << LOGN);
+    uint64_t* dst2 = r_out2 ? r_out2 + (((size_t)c * 2 + p) << LOGN) : nullptr;
     const ModInfo m = mods[l];
-    const bool has_w = (w != nullptr);
-    ulonglong2 wl = has_w ? w[c * (l + 1) + l] : make_ulonglong2(1, 0);
-    auto ld = [&](int idx) { return has_w ? shoup_lazy(src[idx], wl.x, wl.y, m.q) : src[idx]; };
-    auto st = [&](int idx, uint64_t v) { dst[idx] = v; };
-    ntt_inv_block<LOGN>(sm, m, ld, st);
+    if (w2 == nullptr) {
+        const bool has_w = (w != nullptr);
+        ulonglong2 wl = has_w ? w[c * (l + 1) + l] : make_ulonglong2(1, 0);
+        auto ld = [&](int idx) { return has_w ? shoup_lazy(src[idx], wl.x, wl.y, m.q) : src[idx]; };
+        auto st = [&](int idx, uint64_t v) { dst[idx] = v; };
+        ntt_inv_block<LOGN>(sm, m, ld, st);
+    } else {
+        const ulonglong2 wa = w[c * (l + 1) + l], wb = w2[c * (l + 1) + l];
+        auto ld = [&](int idx) { return src[idx]; };
+        auto st = [&](int idx, uint64_t v) {
+            dst[idx] = shoup(v, wa.x, wa.y, m.q);
+            dst2[idx] = shoup(v, wb.x, wb.y, m.q);
+        };
+        ntt_inv_block<LOGN>(sm, m, ld, st);
+    }
 }
 
 // K6 rescale, step 2: out_i = (c_i w_i - NTT_i([r]_{q_l} mod q_i)) q_l^{-1} (+ bias_i).
@@ -276,17 +290,19 @@ void launch_ntt_limbs(const Dev& d, uint64_t* data, int64_t batch, int nl, const
     PrimeMap pm;
     for (int j = 0; j < nl && j < MAXM; j++) pm.idx[j] = (int8_t)prime_idx_host[j];
     EDL_DISPATCH_LOGN(d.logn, {
-        using S = NttShape<LOGN>;
+        using S = NttShape<LOGN, loge_plain(LOGN)>;
         dim3 grid(nl, (unsigned)batch);
         if (inverse) EDL_LAUNCH(d, "k_ntt_limbs", k_ntt_limbs<LOGN, true><<<grid, S::T, S::SMEM_BYTES, d.st>>>(data, nl, pm, d.mods));
         else EDL_LAUNCH(d, "k_ntt_limbs", k_ntt_limbs<LOGN, false><<<grid, S::T, S::SMEM_BYTES, d.st>>>(data, nl, pm, d.mods));
     });
 }
 
-void launch_rescale_intt(const Dev& d, const uint64_t* in, int64_t cnt, int l, const ulonglong2* w, uint64_t* r_out) {
+void launch_rescale_intt(const Dev& d, const uint64_t* in, int64_t cnt, int l, const ulonglong2* w, uint64_t* r_out,
+                         const ulonglong2* w2, uint64_t* r_out2) {
     EDL_DISPATCH_LOGN(d.logn, {
         using S = NttShape<LOGN>;
-        EDL_LAUNCH(d, "k_rescale_intt", k_rescale_intt<LOGN><<<dim3(2, (unsigned)cnt), S::T, S::SMEM_BYTES, d.st>>>(in, l, w, r_out, d.mods));
+        EDL_LAUNCH(d, "k_rescale_intt", k_rescale_intt<LOGN><<<dim3(2, (unsigned)cnt), S::T, S::SMEM_BYTES, d.st>>>(
+            in, l, w, r_out, w2, r_out2, d.mods));
     });
 }
 

@@ -134,11 +134,14 @@ __global__ void k_add_add_const(const uint64_t* __restrict__ v, const uint64_t* 
 
 // ---------------------------------------------------------------- cross-correlation MAC
 // grid: x = coefficient blocks, y = poly*(l+1) + limb, z = output window (r*Wo + c).
-// Each thread owns one coefficient of one window and keeps up to FC filters' 128-bit
-// accumulators in registers, so each input residue is read from HBM once per window.
+// Each thread owns one coefficient of one window: it first issues the loads of all the
+// window's taps (up to CC_TAPS, independent -> memory-level parallelism), then keeps up
+// to CC_FC filters' 128-bit accumulators in registers, so each input residue is read
+// from HBM exactly once.
 constexpr int CC_FC = 8;
+constexpr int CC_TAPS = 16;
 
-__global__ void __launch_bounds__(PW_THREADS)
+__global__ void __launch_bounds__(PW_THREADS, 2)
 k_cc_mac(const uint64_t* __restrict__ x, int l, int H, int W, int F, int kh, int kw, int stride,
          const uint64_t* __restrict__ wk, uint64_t* __restrict__ out, const ModInfo* __restrict__ mods, int logn) {
     extern __shared__ uint64_t wsm[];   // [F][taps] residues for this limb
@@ -154,25 +157,38 @@ k_cc_mac(const uint64_t* __restrict__ x, int l, int H, int W, int F, int kh, int
     const ModInfo m = mods[i];
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= (1 << logn)) return;
-    for (int f0 = 0; f0 < F; f0 += CC_FC) {
-        U128 acc[CC_FC];
+    for (int t0 = 0; t0 < taps; t0 += CC_TAPS) {
+        uint64_t xv[CC_TAPS];
 #pragma unroll
-        for (int f = 0; f < CC_FC; f++) acc[f].lo = acc[f].hi = 0;
-        for (int u = 0; u < kh; u++) {
-            for (int v = 0; v < kw; v++) {
+        for (int t = 0; t < CC_TAPS; t++) {
+            const int tt = t0 + t;
+            if (tt < taps) {
+                const int u = tt / kw, v = tt % kw;
                 const int pix = (wr * stride + u) * W + (wc * stride + v);
-                const uint64_t xv = x[limb_off(pix, p, i, nl, logn) + n];
-                const int t = u * kw + v;
-#pragma unroll
-                for (int f = 0; f < CC_FC; f++)
-                    if (f0 + f < F) mac128(acc[f], xv, wsm[(f0 + f) * taps + t]);
+                xv[t] = __ldg(x + limb_off(pix, p, i, nl, logn) + n);
+            } else {
+                xv[t] = 0;
             }
         }
+        for (int f0 = 0; f0 < F; f0 += CC_FC) {
+            U128 acc[CC_FC];
 #pragma unroll
-        for (int f = 0; f < CC_FC; f++) {
-            if (f0 + f < F) {
-                const int64_t o = (int64_t)(f0 + f) * Ho * Wo + win;
-                out[limb_off(o, p, i, nl, logn) + n] = barrett128(acc[f], m);
+            for (int f = 0; f < CC_FC; f++) acc[f].lo = acc[f].hi = 0;
+#pragma unroll
+            for (int t = 0; t < CC_TAPS; t++) {
+#pragma unroll
+                for (int f = 0; f < CC_FC; f++)
+                    if (f0 + f < F && t0 + t < taps) mac128(acc[f], xv[t], wsm[(f0 + f) * taps + t0 + t]);
+            }
+#pragma unroll
+            for (int f = 0; f < CC_FC; f++) {
+                if (f0 + f < F) {
+                    const int64_t o = (int64_t)(f0 + f) * Ho * Wo + win;
+                    uint64_t* dst = out + limb_off(o, p, i, nl, logn) + n;
+                    uint64_t v = barrett128(acc[f], m);
+                    if (t0 > 0) v = addmod(v, *dst, m.q);
+                    *dst = v;
+                }
             }
         }
     }
@@ -180,10 +196,12 @@ k_cc_mac(const uint64_t* __restrict__ x, int l, int H, int W, int F, int kh, int
 
 // ---------------------------------------------------------------- dense MAC
 // grid: x = coefficient blocks, y = poly*(l+1) + limb, z = output chunk of DN_OC.
-constexpr int DN_OC = 16;
+// The K loop is unrolled by DN_U with all DN_U input loads issued before the MACs.
+constexpr int DN_OC = 12;
 constexpr int DN_KC = 256;    // fold 128-bit accumulators every 256 terms (K*q^2 < 2^128)
+constexpr int DN_U = 4;
 
-__global__ void __launch_bounds__(PW_THREADS)
+__global__ void __launch_bounds__(PW_THREADS, 2)
 k_dense_mac(const uint64_t* __restrict__ x, int64_t K, int64_t O, int l, const uint64_t* __restrict__ wd,
             uint64_t* __restrict__ out, const ModInfo* __restrict__ mods, int logn) {
     extern __shared__ uint64_t wsm[];   // [DN_OC][DN_KC]
@@ -193,9 +211,8 @@ k_dense_mac(const uint64_t* __restrict__ x, int64_t K, int64_t O, int l, const u
     const ModInfo m = mods[i];
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = n < (1 << logn);
-    uint64_t folded[DN_OC];
-#pragma unroll
-    for (int o = 0; o < DN_OC; o++) folded[o] = 0;
+    const size_t kstride = (size_t)2 * nl << logn;            // one ciphertext
+    const uint64_t* xp = x + limb_off(0, p, i, nl, logn) + (active ? n : 0);
     for (int64_t k0 = 0; k0 < K; k0 += DN_KC) {
         const int kc = (int)((K - k0) < DN_KC ? (K - k0) : DN_KC);
         __syncthreads();
@@ -208,18 +225,26 @@ k_dense_mac(const uint64_t* __restrict__ x, int64_t K, int64_t O, int l, const u
         U128 acc[DN_OC];
 #pragma unroll
         for (int o = 0; o < DN_OC; o++) acc[o].lo = acc[o].hi = 0;
-        for (int k = 0; k < kc; k++) {
-            const uint64_t xv = x[limb_off(k0 + k, p, i, nl, logn) + n];
+        for (int k = 0; k < kc; k += DN_U) {
+            uint64_t xv[DN_U];
 #pragma unroll
-            for (int o = 0; o < DN_OC; o++) mac128(acc[o], xv, wsm[o * DN_KC + k]);
+            for (int u = 0; u < DN_U; u++) xv[u] = (k + u < kc) ? __ldg(xp + (size_t)(k0 + k + u) * kstride) : 0;
+#pragma unroll
+            for (int u = 0; u < DN_U; u++) {
+#pragma unroll
+                for (int o = 0; o < DN_OC; o++) mac128(acc[o], xv[u], wsm[o * DN_KC + ((k + u) & (DN_KC - 1))]);
+            }
         }
 #pragma unroll
-        for (int o = 0; o < DN_OC; o++) folded[o] = addmod(folded[o], barrett128(acc[o], m), m.q);
+        for (int o = 0; o < DN_OC; o++) {
+            if (o0 + o < O) {
+                uint64_t* dst = out + limb_off(o0 + o, p, i, nl, logn) + n;
+                uint64_t v = barrett128(acc[o], m);
+                if (k0 > 0) v = addmod(v, *dst, m.q);
+                *dst = v;
+            }
+        }
     }
-    if (!active) return;
-#pragma unroll
-    for (int o = 0; o < DN_OC; o++)
-        if (o0 + o < O) out[limb_off(o0 + o, p, i, nl, logn) + n] = folded[o];
 }
 
 }  // namespace

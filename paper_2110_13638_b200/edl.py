@@ -14,7 +14,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libedl.so")
+LIB_PATH = os.environ.get("EDL_LIB") or os.path.join(_HERE, "libedl.so")
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is not built; run `python -m paper_2110_13638_b200.build` "
                       "(or __graft_entry__.build()).  There is no CPU fallback.")
