@@ -260,6 +260,7 @@ edl_status edl_ctx_create(const edl_params* p, int32_t device, void* stream, edl
         m.r_hi = (uint64_t)(ratio >> 64);
         m.two64 = (uint64_t)((((host::u128)1) << 64) % q);
         m.two64_s = host::shoup_companion(m.two64, q);
+        m.one_s = host::shoup_companion(1, q);   // floor(2^64 / q)
         m.tw_fwd = reinterpret_cast<const ulonglong2*>(dfwd);
         m.tw_inv = reinterpret_cast<const ulonglong2*>(dinv);
         m.ninv = host::invmod((uint64_t)c->N % q, q);
@@ -613,22 +614,26 @@ edl_status edl_dense(edl_ctx* c, const edl_cts* x, const double* Wt, const doubl
     const uint64_t* dw = upload(c, residues(c, wi, l + 1));
     if (!dw) return fail(c, EDL_ERR_ARG, "dense: weight table too large");
     Dev d = c->dev();
+    const size_t part_words = (size_t)dense_split(d, K, O, l) * ct_words(c, O, l);
     if (defer_rescale) {
-        launch_dense_mac(d, x->data, K, O, l, dw, out->data);
+        uint64_t* part = scratch(c, part_words);
+        if (!part) return fail(c, EDL_ERR_CUDA, "dense: scratch");
+        launch_dense_mac(d, x->data, K, O, l, dw, out->data, part);
         set_meta(out, O, l, x->scale * pt_scale, x->key_id);
         return cuda_check(c, "dense");
     }
     const double s_after = (x->scale * pt_scale) / (double)c->prm.q[l];
-    uint64_t* acc = scratch(c, ct_words(c, O, l) + (size_t)O * 2 * c->N);
+    uint64_t* acc = scratch(c, ct_words(c, O, l) + (size_t)O * 2 * c->N + part_words);
     if (!acc) return fail(c, EDL_ERR_CUDA, "dense: scratch");
     uint64_t* r = acc + ct_words(c, O, l);
+    uint64_t* part = r + (size_t)O * 2 * c->N;
     const uint64_t* db = nullptr;
     if (b) {
         std::vector<int64_t> bi(O);
         for (int o = 0; o < O; o++) bi[o] = const_int(b[o], s_after);
         db = upload(c, residues(c, bi, l));
     }
-    launch_dense_mac(d, x->data, K, O, l, dw, acc);
+    launch_dense_mac(d, x->data, K, O, l, dw, acc, part);
     launch_rescale_intt(d, acc, O, l, nullptr, r);
     launch_rescale_ntt(d, acc, O, l, nullptr, r, db, out->data);
     set_meta(out, O, l - 1, s_after, x->key_id);
@@ -718,9 +723,9 @@ edl_status edl_poly_activation(edl_ctx* c, const edl_cts* x, const double* coeff
         launch_relin(d, x->data, x->data, cnt, l, true, c->d_rlk, c->d_rlk_s, rsc, y2);   // 1.
         launch_rescale_intt(d, x->data, cnt, l, w3, r, w1, r2);                             // 2.+4. INTT shared
         launch_rescale_ntt(d, x->data, cnt, l, w3, r, nullptr, u);                          // 2.
-        launch_rescale_ntt(d, x->data, cnt, l, w1, r2, nullptr, w);                         // 4.
+        launch_rescale_ntt(d, x->data, cnt, l, w1, r2, nullptr, w, l - 2);                  // 4. (+ mod_drop)
         launch_relin(d, u, y2, cnt, l - 1, true, c->d_rlk, c->d_rlk_s, rsc, v);              // 3.
-        launch_add_add_const(d, v, w, l - 1, cnt, l - 2, k0, out->data);                       // 5.
+        launch_add_add_const(d, v, w, l - 2, cnt, l - 2, k0, out->data);                       // 5.
     }
     set_meta(out, cnt, l - 2, S3, x->key_id);
     return cuda_check(c, "poly_activation");

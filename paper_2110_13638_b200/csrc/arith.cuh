@@ -22,6 +22,7 @@ struct ModInfo {
     const ulonglong2* tw_inv;   // [N] {psi^-brv(k), shoup}
     uint64_t ninv, ninv_s;      // N^-1 mod q and Shoup companion
     uint64_t w1ninv, w1ninv_s;  // psi^-brv(1) * N^-1 (last INTT stage), Shoup companion
+    uint64_t one_s;             // floor(2^64 / q): Shoup companion of 1 (64-bit reduction)
 };
 
 struct U128 {
@@ -54,10 +55,36 @@ __device__ __forceinline__ uint64_t shoup_lazy(uint64_t y, uint64_t w, uint64_t 
     return y * w - qt * q;
 }
 
-__device__ __forceinline__ uint64_t csub(uint64_t x, uint64_t m) { return x >= m ? x - m : x; }
+// Conditional subtraction x >= m ? x - m : x for x, m < 2^63 (every modulus is < 2^61 and
+// lazy values stay below 4q): the sign of x - m decides, which lowers to IADD3/IADD3.X/
+// ISETP/SEL/SEL on the ALU pipe (the compare-first form adds an IMAD.X on fmaheavy).
+__device__ __forceinline__ uint64_t csub(uint64_t x, uint64_t m) {
+    const uint64_t d = x - m;
+    return ((int64_t)d < 0) ? x : d;
+}
+
+// Shoup with an approximate quotient: qt' = y1 s1 + hi(y1 s0) + hi(y0 s1) drops the
+// lowest partial product and the carries of the middle ones, so qt - qt' is 0, 1 or 2 and
+// the result y w - qt' q lies in [0, 4q).  Costs 3 IMAD.WIDE + 2 IMAD.HI + 4 IMAD on the
+// fmaheavy pipe instead of 6 IMAD.WIDE + 4 IMAD (the NTT's binding pipe, round-1 ncu).
+__device__ __forceinline__ uint64_t shoup_lazy4(uint64_t y, uint64_t w, uint64_t ws, uint64_t q) {
+    const uint32_t y0 = (uint32_t)y, y1 = (uint32_t)(y >> 32);
+    const uint32_t s0 = (uint32_t)ws, s1 = (uint32_t)(ws >> 32);
+    const uint64_t qt = (uint64_t)y1 * s1 + __umulhi(y1, s0) + __umulhi(y0, s1);
+    return y * w - qt * q;
+}
+
+// [0, 2q) result for the butterflies.
+__device__ __forceinline__ uint64_t shoup_lazy2(uint64_t y, uint64_t w, uint64_t ws, uint64_t q) {
+#ifndef EDL_APPROX_SHOUP
+    return shoup_lazy(y, w, ws, q);
+#else
+    return csub(shoup_lazy4(y, w, ws, q), 2 * q);
+#endif
+}
 
 __device__ __forceinline__ uint64_t shoup(uint64_t y, uint64_t w, uint64_t ws, uint64_t q) {
-    return csub(shoup_lazy(y, w, ws, q), q);
+    return csub(shoup_lazy2(y, w, ws, q), q);
 }
 
 // Barrett reduction of a 128-bit value x < q * 2^64 ... in practice x < 2^126.
@@ -88,21 +115,21 @@ __device__ __forceinline__ uint64_t mulmod(uint64_t a, uint64_t b, const ModInfo
     return barrett128(mul_wide(a, b), m);
 }
 
-// Canonical reduction of an arbitrary 64-bit value.
+// Canonical reduction of an arbitrary 64-bit value: Shoup multiplication by 1
+// (a - floor(a floor(2^64/q) / 2^64) q lies in [0, 2q) for every a < 2^64).
 __device__ __forceinline__ uint64_t reduce64(uint64_t a, const ModInfo& m) {
-    U128 x;
-    x.lo = a;
-    x.hi = 0;
-    return barrett128(x, m);
+    return csub(a - __umul64hi(a, m.one_s) * m.q, m.q);
 }
 
 __device__ __forceinline__ uint64_t addmod(uint64_t a, uint64_t b, uint64_t q) { return csub(a + b, q); }
 __device__ __forceinline__ uint64_t submod(uint64_t a, uint64_t b, uint64_t q) { return a >= b ? a - b : a + q - b; }
 
 // Centered lift of r in [0, qf) to (-qf/2, qf/2], reduced into [0, q) where
-// qf_mod_q = qf mod q (precomputed).  qf is odd so the half point never occurs.
+// qf_mod_q = qf mod q (precomputed).  qf is odd so the half point never occurs.  The
+// qf < 2q test is uniform across the CTA (both moduli are per-launch constants), so the
+// common case (a 40-bit lift into a 40- or 60-bit limb) costs one conditional subtraction.
 __device__ __forceinline__ uint64_t center_mod(uint64_t r, uint64_t qf, uint64_t qf_mod_q, const ModInfo& m) {
-    uint64_t rq = (r < m.q) ? r : reduce64(r, m);
+    uint64_t rq = (qf < 2 * m.q) ? csub(r, m.q) : reduce64(r, m);
     if (r > (qf >> 1)) rq = submod(rq, qf_mod_q, m.q);
     return rq;
 }

@@ -61,9 +61,10 @@ void launch_ntt_limbs(const Dev& d, uint64_t* data, int64_t batch, int nl, const
 // rescale: r_out [cnt][2][N] <- INTT_{q_l}(in[.][.][l] * w_l) ; w may be null
 void launch_rescale_intt(const Dev& d, const uint64_t* in, int64_t cnt, int l, const ulonglong2* w, uint64_t* r_out,
                          const ulonglong2* w2 = nullptr, uint64_t* r_out2 = nullptr);
-// out [cnt][2][l][N] <- (in_i * w_i - NTT_i([r]_{q_l} mod q_i)) * q_l^{-1} (+ bias_i on poly 0)
+// out [cnt][2][lo+1][N] <- (in_i * w_i - NTT_i([r]_{q_l} mod q_i)) * q_l^{-1} (+ bias_i on poly 0),
+// i <= lo; lo = -1 means the full rescaled level l-1 (a smaller lo fuses a mod-drop)
 void launch_rescale_ntt(const Dev& d, const uint64_t* in, int64_t cnt, int l, const ulonglong2* w,
-                        const uint64_t* r, const uint64_t* bias, uint64_t* out);
+                        const uint64_t* r, const uint64_t* bias, uint64_t* out, int lo = -1);
 // relinearisation of the tensor a (x) b at level l (+ optional rescale by q_l)
 void launch_relin(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t cnt, int l, bool rescale,
                   const uint64_t* rlk, const uint64_t* rlk_s, uint64_t* scratch, uint64_t* out);
@@ -87,7 +88,10 @@ void launch_add_add_const(const Dev& d, const uint64_t* v, const uint64_t* w, in
 void launch_cc_mac(const Dev& d, const uint64_t* x, int l, int H, int W, int F, int kh, int kw, int stride,
                    const uint64_t* wk /*[F][kh*kw][l+1]*/, uint64_t* out);
 // dense MAC: out[o] = sum_k x[k] * wd[o][k][i]  (x: K cts, out: O cts, level l)
-void launch_dense_mac(const Dev& d, const uint64_t* x, int64_t K, int64_t O, int l, const uint64_t* wd, uint64_t* out);
+// part: scratch for split-K partial sums (dense_split(...) * O * 2 * (l+1) * N words) or null
+void launch_dense_mac(const Dev& d, const uint64_t* x, int64_t K, int64_t O, int l, const uint64_t* wd, uint64_t* out,
+                      uint64_t* part = nullptr);
+int dense_split(const Dev& d, int64_t K, int64_t O, int l);
 
 // ---- randomness / keys / encryption (rng.cu) ----
 void launch_keygen(const Dev& d, uint64_t seed, uint64_t* s_hat /*[L+2][N]*/, uint64_t* pk /*[2][L+1][N]*/,

@@ -42,7 +42,7 @@ __device__ __forceinline__ int spad(int idx) { return idx + (idx >> 4); }
 // ---- forward CT butterfly (Harvey): X, Y in [0,4q) -> [0,4q)
 __device__ __forceinline__ void ct_bfly(uint64_t& X, uint64_t& Y, ulonglong2 w, uint64_t q, uint64_t two_q) {
     uint64_t x = csub(X, two_q);
-    uint64_t t = shoup_lazy(Y, w.x, w.y, q);
+    uint64_t t = shoup_lazy2(Y, w.x, w.y, q);
     X = x + t;
     Y = x - t + two_q;
 }
@@ -51,7 +51,7 @@ __device__ __forceinline__ void ct_bfly(uint64_t& X, uint64_t& Y, ulonglong2 w, 
 __device__ __forceinline__ void gs_bfly(uint64_t& X, uint64_t& Y, uint64_t w, uint64_t ws, uint64_t q, uint64_t two_q) {
     uint64_t x = X, y = Y;
     X = csub(x + y, two_q);
-    Y = shoup_lazy(x - y + two_q, w, ws, q);
+    Y = shoup_lazy2(x - y + two_q, w, ws, q);
 }
 
 // One forward pass over stages [S0, S0+NS) for `v`-th virtual thread's group held in x[].
@@ -83,8 +83,8 @@ __device__ __forceinline__ void inv_pass_regs(uint64_t* x, int high, const ModIn
             if (LAST && S0 + k == 0) {
                 // stage 0 (m = 1): fold N^-1 into both outputs
                 uint64_t a = x[r], b = x[r + half];
-                x[r] = shoup_lazy(a + b, m.ninv, m.ninv_s, m.q);
-                x[r + half] = shoup_lazy(a - b + two_q, m.w1ninv, m.w1ninv_s, m.q);
+                x[r] = shoup_lazy2(a + b, m.ninv, m.ninv_s, m.q);
+                x[r + half] = shoup_lazy2(a - b + two_q, m.w1ninv, m.w1ninv_s, m.q);
             } else {
                 const int tidx = (1 << (S0 + k)) + (high << k) + (r >> (NS - k));
                 ulonglong2 w = __ldg(m.tw_inv + tidx);

@@ -25,7 +25,7 @@ struct PrimeMap {
 // K1/K2: plain batched NTT / INTT, in place, data [batch][nl][N], limb j uses pm.idx[j].
 template <int LOGN, bool INV>
 __global__ void __launch_bounds__(NttShape<LOGN, loge_plain(LOGN)>::T, 1)
-k_ntt_limbs(uint64_t* __restrict__ data, int nl, PrimeMap pm, const ModInfo* __restrict__ mods) {
+k_ntt_limbs(uint64_t* __restrict__ data, int nl, const __grid_constant__ PrimeMap pm, const ModInfo* __restrict__ mods) {
     extern __shared__ uint64_t sm[];
     const int limb = blockIdx.x;
     uint64_t* p = data + (((size_t)blockIdx.y * nl + limb) << LOGN);
@@ -55,7 +55,7 @@ k_rescale_intt(const uint64_t* __restrict__ in, int l, const ulonglong2* __restr
     if (w2 == nullptr) {
         const bool has_w = (w != nullptr);
         ulonglong2 wl = has_w ? w[c * (l + 1) + l] : make_ulonglong2(1, 0);
-        auto ld = [&](int idx) { return has_w ? shoup_lazy(src[idx], wl.x, wl.y, m.q) : src[idx]; };
+        auto ld = [&](int idx) { return has_w ? shoup_lazy2(src[idx], wl.x, wl.y, m.q) : src[idx]; };
         auto st = [&](int idx, uint64_t v) { dst[idx] = v; };
         ntt_inv_block<LOGN>(sm, m, ld, st);
     } else {
@@ -73,7 +73,7 @@ k_rescale_intt(const uint64_t* __restrict__ in, int l, const ulonglong2* __restr
 template <int LOGN>
 __global__ void __launch_bounds__(NttShape<LOGN>::T, 1)
 k_rescale_ntt(const uint64_t* __restrict__ in, int l, const ulonglong2* __restrict__ w,
-              const uint64_t* __restrict__ r, const uint64_t* __restrict__ bias, uint64_t* __restrict__ out,
+              const uint64_t* __restrict__ r, const uint64_t* __restrict__ bias, uint64_t* __restrict__ out, int nlo,
               const ModInfo* __restrict__ mods, const ChainConsts* __restrict__ cc) {
     extern __shared__ uint64_t sm[];
     const int i = blockIdx.x, p = blockIdx.y;
@@ -84,7 +84,7 @@ k_rescale_ntt(const uint64_t* __restrict__ in, int l, const ulonglong2* __restri
     const ulonglong2 qlinv = cc->qinv[l][i];
     const uint64_t* rr = r + (((size_t)c * 2 + p) << LOGN);
     const uint64_t* src = in + limb_off(c, p, i, l + 1, LOGN);
-    uint64_t* dst = out + limb_off(c, p, i, l, LOGN);
+    uint64_t* dst = out + limb_off(c, p, i, nlo, LOGN);
     const bool has_w = (w != nullptr);
     const ulonglong2 wi = has_w ? w[c * (l + 1) + i] : make_ulonglong2(1, 0);
     const uint64_t b = (bias != nullptr && p == 0) ? bias[c * l + i] : 0;
@@ -176,7 +176,7 @@ k_relin_ks_mac(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, i
             }
         } else {
             const uint64_t* src = acoef + (((size_t)c * (l + 1) + j) << LOGN);
-            const bool need_red = mods[j].q > m.q;
+            const bool need_red = mods[j].q > 4 * m.q;   // the forward NTT accepts [0, 4q)
             auto ld = [&](int idx) {
                 uint64_t v = src[idx];
                 return need_red ? reduce64(v, m) : v;
@@ -307,11 +307,12 @@ void launch_rescale_intt(const Dev& d, const uint64_t* in, int64_t cnt, int l, c
 }
 
 void launch_rescale_ntt(const Dev& d, const uint64_t* in, int64_t cnt, int l, const ulonglong2* w,
-                        const uint64_t* r, const uint64_t* bias, uint64_t* out) {
+                        const uint64_t* r, const uint64_t* bias, uint64_t* out, int lo) {
+    const int nlo = (lo < 0 || lo > l - 1) ? l : lo + 1;
     EDL_DISPATCH_LOGN(d.logn, {
         using S = NttShape<LOGN>;
-        EDL_LAUNCH(d, "k_rescale_ntt", k_rescale_ntt<LOGN><<<dim3(l, 2, (unsigned)cnt), S::T, S::SMEM_BYTES, d.st>>>(in, l, w, r, bias, out,
-                                                                                      d.mods, d.cc));
+        EDL_LAUNCH(d, "k_rescale_ntt", k_rescale_ntt<LOGN><<<dim3(nlo, 2, (unsigned)cnt), S::T, S::SMEM_BYTES, d.st>>>(in, l, w, r, bias, out,
+                                                                                      nlo, d.mods, d.cc));
     });
 }
 

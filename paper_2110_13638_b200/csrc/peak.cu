@@ -13,7 +13,7 @@ __global__ void __launch_bounds__(256) k_modmul_peak(uint64_t q, uint64_t w, uin
     for (int k = 0; k < 8; k++) x[k] = (threadIdx.x * 8 + k + 1) % q;
     for (int it = 0; it < iters; it++) {
 #pragma unroll
-        for (int k = 0; k < 8; k++) x[k] = shoup_lazy(x[k], w, ws, q);
+        for (int k = 0; k < 8; k++) x[k] = shoup_lazy2(x[k], w, ws, q);
     }
     uint64_t acc = 0;
 #pragma unroll

@@ -194,34 +194,113 @@ k_cc_mac(const uint64_t* __restrict__ x, int l, int H, int W, int F, int kh, int
     }
 }
 
+// ---------------------------------------------------------------- cross-correlation MAC, FC filters
+// Hot-path variant of k_cc_mac (round 2): each thread owns two consecutive coefficients
+// (16-byte loads and stores) of one (window, poly, limb) and all FC <= 8 filters of a
+// filter chunk, so every weight fetched from shared memory feeds two 128-bit MACs and
+// every input residue is read from HBM once.  Taps stream in batches of CC2_TB with the
+// next batch's loads issued before the current batch's MACs (memory-level parallelism
+// without a second CTA's registers).
+constexpr int CC2_THREADS = 256;
+constexpr int CC2_TB = 4;
+constexpr int CC2_MAXTAPS = 64;
+
+template <int FC>
+__global__ void __launch_bounds__(CC2_THREADS, 2)
+k_cc_mac2(const uint64_t* __restrict__ x, int l, int W, int kw, int stride, int Wo, int taps, int f0, int F,
+          int n_out_per_f, const uint64_t* __restrict__ wk, uint64_t* __restrict__ out,
+          const ModInfo* __restrict__ mods, int logn) {
+    __shared__ uint64_t wsm[FC * CC2_MAXTAPS];   // [f][tap] residues of this limb
+    __shared__ int tpix[CC2_MAXTAPS];            // pixel (ciphertext) index of each tap
+    const int nl = l + 1;
+    const int p = blockIdx.y / nl, i = blockIdx.y % nl;
+    const int win = blockIdx.z;
+    const int wr = win / Wo, wc = win % Wo;
+    for (int t = threadIdx.x; t < FC * taps; t += blockDim.x) {
+        const int f = t / taps, tt = t % taps;
+        wsm[t] = (f0 + f < F) ? wk[((size_t)(f0 + f) * taps + tt) * nl + i] : 0;
+    }
+    for (int t = threadIdx.x; t < taps; t += blockDim.x)
+        tpix[t] = (wr * stride + t / kw) * W + (wc * stride + t % kw);
+    __syncthreads();
+    const int n2 = blockIdx.x * blockDim.x + threadIdx.x;   // coefficient pair
+    if (2 * n2 >= (1 << logn)) return;
+    const ModInfo m = mods[i];
+    const size_t ct_words = (size_t)2 * nl << logn;
+    const uint64_t* xb = x + limb_off(0, p, i, nl, logn) + 2 * (size_t)n2;
+    U128 acc[FC][2];
+#pragma unroll
+    for (int f = 0; f < FC; f++) acc[f][0].lo = acc[f][0].hi = acc[f][1].lo = acc[f][1].hi = 0;
+    ulonglong2 cur[CC2_TB], nxt[CC2_TB];
+#pragma unroll
+    for (int u = 0; u < CC2_TB; u++)
+        cur[u] = (u < taps) ? __ldg(reinterpret_cast<const ulonglong2*>(xb + tpix[u] * ct_words)) : make_ulonglong2(0, 0);
+    for (int t0 = 0; t0 < taps; t0 += CC2_TB) {
+#pragma unroll
+        for (int u = 0; u < CC2_TB; u++) {
+            const int tt = t0 + CC2_TB + u;
+            nxt[u] = (tt < taps) ? __ldg(reinterpret_cast<const ulonglong2*>(xb + tpix[tt] * ct_words))
+                                 : make_ulonglong2(0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < CC2_TB; u++) {
+            const int tt = t0 + u < taps ? t0 + u : 0;   // out-of-range taps carry x = 0
+#pragma unroll
+            for (int f = 0; f < FC; f++) {
+                const uint64_t w = wsm[f * taps + tt];
+                mac128(acc[f][0], cur[u].x, w);
+                mac128(acc[f][1], cur[u].y, w);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < CC2_TB; u++) cur[u] = nxt[u];
+    }
+#pragma unroll
+    for (int f = 0; f < FC; f++) {
+        if (f0 + f < F) {
+            const int64_t o = (int64_t)(f0 + f) * n_out_per_f + win;
+            uint64_t* dst = out + limb_off(o, p, i, nl, logn) + 2 * (size_t)n2;
+            *reinterpret_cast<ulonglong2*>(dst) = make_ulonglong2(barrett128(acc[f][0], m), barrett128(acc[f][1], m));
+        }
+    }
+}
+
 // ---------------------------------------------------------------- dense MAC
-// grid: x = coefficient blocks, y = poly*(l+1) + limb, z = output chunk of DN_OC.
-// The K loop is unrolled by DN_U with all DN_U input loads issued before the MACs.
+// grid: x = coefficient blocks, y = poly*(l+1) + limb, z = output chunk of DN_OC x K split.
+// Split-K (round 2): the K inputs are cut into ks slices so a small layer (C1: 245 -> 10
+// on 2 limbs) still fills every SM; each slice writes its reduced partial sum and
+// k_dense_combine adds the slices mod q (O4: order-independent).  The K loop is
+// unrolled by DN_U with all DN_U input loads issued before the MACs.
 constexpr int DN_OC = 12;
 constexpr int DN_KC = 256;    // fold 128-bit accumulators every 256 terms (K*q^2 < 2^128)
 constexpr int DN_U = 4;
 
 __global__ void __launch_bounds__(PW_THREADS, 2)
-k_dense_mac(const uint64_t* __restrict__ x, int64_t K, int64_t O, int l, const uint64_t* __restrict__ wd,
+k_dense_mac(const uint64_t* __restrict__ x, int64_t K, int64_t O, int l, int ks, const uint64_t* __restrict__ wd,
             uint64_t* __restrict__ out, const ModInfo* __restrict__ mods, int logn) {
     extern __shared__ uint64_t wsm[];   // [DN_OC][DN_KC]
     const int nl = l + 1;
     const int p = blockIdx.y / nl, i = blockIdx.y % nl;
-    const int64_t o0 = (int64_t)blockIdx.z * DN_OC;
+    const int oc = blockIdx.z / ks, sl = blockIdx.z % ks;
+    const int64_t o0 = (int64_t)oc * DN_OC;
+    const int64_t kper = (K + ks - 1) / ks;
+    const int64_t kbeg = sl * kper, kend = (kbeg + kper < K) ? kbeg + kper : K;
+    uint64_t* outp = out + (size_t)sl * ((size_t)O * 2 * nl << logn);
     const ModInfo m = mods[i];
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = n < (1 << logn);
     const size_t kstride = (size_t)2 * nl << logn;            // one ciphertext
     const uint64_t* xp = x + limb_off(0, p, i, nl, logn) + (active ? n : 0);
-    for (int64_t k0 = 0; k0 < K; k0 += DN_KC) {
-        const int kc = (int)((K - k0) < DN_KC ? (K - k0) : DN_KC);
+    bool first = true;
+    for (int64_t k0 = kbeg; k0 < kend || first; k0 += DN_KC) {
+        const int kc = (int)((kend - k0) < DN_KC ? (kend - k0) : DN_KC);
         __syncthreads();
         for (int t = threadIdx.x; t < DN_OC * DN_KC; t += blockDim.x) {
             const int o = t / DN_KC, k = t % DN_KC;
             wsm[t] = (o0 + o < O && k < kc) ? wd[((size_t)(o0 + o) * K + (k0 + k)) * nl + i] : 0;
         }
         __syncthreads();
-        if (!active) continue;
+        if (!active) { first = false; continue; }
         U128 acc[DN_OC];
 #pragma unroll
         for (int o = 0; o < DN_OC; o++) acc[o].lo = acc[o].hi = 0;
@@ -238,11 +317,34 @@ k_dense_mac(const uint64_t* __restrict__ x, int64_t K, int64_t O, int l, const u
 #pragma unroll
         for (int o = 0; o < DN_OC; o++) {
             if (o0 + o < O) {
-                uint64_t* dst = out + limb_off(o0 + o, p, i, nl, logn) + n;
+                uint64_t* dst = outp + limb_off(o0 + o, p, i, nl, logn) + n;
                 uint64_t v = barrett128(acc[o], m);
-                if (k0 > 0) v = addmod(v, *dst, m.q);
+                if (!first) v = addmod(v, *dst, m.q);
                 *dst = v;
             }
+        }
+        first = false;
+    }
+}
+
+// out[r][k] = sum_s part[s][r][k] mod q over ks slices (rows = O * 2 * nl limbs).
+__global__ void k_dense_combine(const uint64_t* __restrict__ part, int ks, int64_t O, int l, uint64_t* __restrict__ out,
+                                const ModInfo* __restrict__ mods, int logn) {
+    const int64_t rows = O * 2 * (l + 1);
+    const int n2 = 1 << (logn - 1);
+    const size_t slice = (size_t)rows << logn;
+    for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
+        const uint64_t q = mods[row % (l + 1)].q;
+        const uint64_t* pp = part + ((size_t)row << logn);
+        uint64_t* po = out + ((size_t)row << logn);
+        for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n2; k += gridDim.x * blockDim.x) {
+            ulonglong2 a = v2(pp)[k];
+            for (int s = 1; s < ks; s++) {
+                const ulonglong2 b = v2(pp + s * slice)[k];
+                a.x = addmod(a.x, b.x, q);
+                a.y = addmod(a.y, b.y, q);
+            }
+            v2(po)[k] = a;
         }
     }
 }
@@ -278,16 +380,49 @@ void launch_add_add_const(const Dev& d, const uint64_t* v, const uint64_t* w, in
 void launch_cc_mac(const Dev& d, const uint64_t* x, int l, int H, int W, int F, int kh, int kw, int stride,
                    const uint64_t* wk, uint64_t* out) {
     const int Ho = (H - kh) / stride + 1, Wo = (W - kw) / stride + 1;
+    const int taps = kh * kw;
+    if (taps <= CC2_MAXTAPS && d.logn >= 9) {
+        dim3 grid((unsigned)((1 << d.logn) / (2 * CC2_THREADS)), (unsigned)(2 * (l + 1)), (unsigned)(Ho * Wo));
+        for (int f0 = 0; f0 < F; f0 += 8) {
+            const int fc = (F - f0) < 8 ? (F - f0) : 8;
+#define EDL_CC2(FCV) EDL_LAUNCH(d, "k_cc_mac", (k_cc_mac2<FCV><<<grid, CC2_THREADS, 0, d.st>>>(x, l, W, kw, stride, Wo, taps, f0, F, Ho * Wo, wk, out, d.mods, d.logn)))
+            switch (fc) {
+                case 1: EDL_CC2(1); break;
+                case 2: EDL_CC2(2); break;
+                case 3: EDL_CC2(3); break;
+                case 4: EDL_CC2(4); break;
+                case 5: EDL_CC2(5); break;
+                case 6: EDL_CC2(6); break;
+                case 7: EDL_CC2(7); break;
+                default: EDL_CC2(8); break;
+            }
+#undef EDL_CC2
+        }
+        return;
+    }
     dim3 grid((unsigned)(((1 << d.logn) + PW_THREADS - 1) / PW_THREADS), (unsigned)(2 * (l + 1)), (unsigned)(Ho * Wo));
     size_t smem = (size_t)F * kh * kw * sizeof(uint64_t);
     EDL_LAUNCH(d, "k_cc_mac", k_cc_mac<<<grid, PW_THREADS, smem, d.st>>>(x, l, H, W, F, kh, kw, stride, wk, out, d.mods, d.logn));
 }
 
-void launch_dense_mac(const Dev& d, const uint64_t* x, int64_t K, int64_t O, int l, const uint64_t* wd, uint64_t* out) {
+int dense_split(const Dev& d, int64_t K, int64_t O, int l) {
+    const int64_t ctas = (int64_t)((1 << d.logn) / PW_THREADS) * 2 * (l + 1) * ((O + DN_OC - 1) / DN_OC);
+    int ks = 1;
+    while (ks < 16 && ctas * ks < 4 * 148 && K / (ks * 2) >= 16) ks *= 2;
+    return ks;
+}
+
+void launch_dense_mac(const Dev& d, const uint64_t* x, int64_t K, int64_t O, int l, const uint64_t* wd, uint64_t* out,
+                      uint64_t* part) {
+    const int ks = part ? dense_split(d, K, O, l) : 1;
     dim3 grid((unsigned)(((1 << d.logn) + PW_THREADS - 1) / PW_THREADS), (unsigned)(2 * (l + 1)),
-              (unsigned)((O + DN_OC - 1) / DN_OC));
+              (unsigned)(((O + DN_OC - 1) / DN_OC) * ks));
     size_t smem = (size_t)DN_OC * DN_KC * sizeof(uint64_t);
-    EDL_LAUNCH(d, "k_dense_mac", k_dense_mac<<<grid, PW_THREADS, smem, d.st>>>(x, K, O, l, wd, out, d.mods, d.logn));
+    uint64_t* dst = ks > 1 ? part : out;
+    EDL_LAUNCH(d, "k_dense_mac", k_dense_mac<<<grid, PW_THREADS, smem, d.st>>>(x, K, O, l, ks, wd, dst, d.mods, d.logn));
+    if (ks > 1)
+        EDL_LAUNCH(d, "k_dense_combine", k_dense_combine<<<rows_grid(d.logn, O * 2 * (l + 1)), PW_THREADS, 0, d.st>>>(
+                                             part, ks, O, l, out, d.mods, d.logn));
 }
 
 }  // namespace edl
