@@ -56,6 +56,14 @@ struct edl_ctx {
 };
 
 namespace edl {
+void ensure_smem_attr(const void* kern, int bytes) {
+    static std::vector<const void*> done;
+    for (const void* k : done)
+        if (k == kern) return;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    done.push_back(kern);
+}
+
 cudaEvent_t Prof::ev() {
     if (used == pool.size()) {
         cudaEvent_t e;
@@ -222,7 +230,7 @@ size_t edl_cts_bytes(int64_t count, int32_t level, int32_t log_n) {
 edl_status edl_ctx_create(const edl_params* p, int32_t device, void* stream, edl_ctx** out) {
     if (!p || !out) return EDL_ERR_ARG;
     *out = nullptr;
-    if (p->log_n < 10 || p->log_n > 14 || p->n_data < 1 || p->n_data > EDL_MAX_PRIMES) return EDL_ERR_ARG;
+    if (p->log_n < 10 || p->log_n > 16 || p->n_data < 1 || p->n_data > EDL_MAX_PRIMES) return EDL_ERR_ARG;
     for (int k = 0; k < p->n_data; k++)
         if (p->q[k] >= (1ull << 61)) return EDL_ERR_ARG;
     if (p->p_special >= (1ull << 61)) return EDL_ERR_ARG;

@@ -49,6 +49,45 @@ struct Dev {
     Prof* prof;
 };
 
+// Supported ring degrees: 2^10 .. 2^16 (N > 2^13 runs one limb per thread-block cluster).
+#define EDL_DISPATCH_LOGN(logn, ...)                               \
+    switch (logn) {                                                 \
+        case 10: { constexpr int LOGN = 10; __VA_ARGS__; } break;   \
+        case 11: { constexpr int LOGN = 11; __VA_ARGS__; } break;   \
+        case 12: { constexpr int LOGN = 12; __VA_ARGS__; } break;   \
+        case 13: { constexpr int LOGN = 13; __VA_ARGS__; } break;   \
+        case 14: { constexpr int LOGN = 14; __VA_ARGS__; } break;   \
+        case 15: { constexpr int LOGN = 15; __VA_ARGS__; } break;   \
+        case 16: { constexpr int LOGN = 16; __VA_ARGS__; } break;   \
+        default: break;                                             \
+    }
+
+void ensure_smem_attr(const void* kern, int bytes);
+
+// Launch an NTT-family kernel with config C: grid.x is multiplied by the cluster size
+// C::K (consecutive blocks form one limb's cluster), block = C::T threads, dynamic shared
+// memory C::SMEM_BYTES.
+template <class C, typename... KArgs, typename... Args>
+void launch_cfg(const Dev& d, const char* name, void (*kern)(KArgs...), dim3 grid, Args... args) {
+    ensure_smem_attr((const void*)kern, C::SMEM_BYTES);
+    grid.x *= C::K;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(C::T, 1, 1);
+    cfg.dynamicSmemBytes = C::SMEM_BYTES;
+    cfg.stream = d.st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C::K;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = C::K > 1 ? 1 : 0;
+    d.prof->begin(name, d.st);
+    cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+    d.prof->end(d.st);
+}
+
 #define EDL_LAUNCH(d, name, ...)                         \
     do {                                                  \
         (d).prof->begin(name, (d).st);                    \

@@ -1,4 +1,6 @@
-// ntt_core.cuh -- one-CTA negacyclic NTT / INTT of a whole limb (N <= 2^14) on sm_100a.
+// ntt_core.cuh -- negacyclic NTT / INTT of one limb on sm_100a, by one CTA (N <= 2^13)
+// or by a thread-block cluster of K CTAs exchanging through distributed shared memory
+// (N = 2^14 .. 2^16).
 //
 // Definition (background to PAPER.md:470 "encoded into a single
 // polynomial"): A[k] = sum_j a_j psi^{(2 brv(k) + 1) j} mod q, i.e. Cooley-Tukey
@@ -6,38 +8,64 @@
 // the inverse is Gentleman-Sande with psi^{-brv(m+i)} and N^{-1} folded into its last
 // stage.
 //
-// B200 design: T threads (T = N/E) each hold E = 2^LOGE residues in registers; the
-// log N stages run as ceil(log N / LOGE) register-resident radix-2^LOGE passes with a
-// padded shared-memory exchange between passes.  Global traffic is exactly one
-// coalesced read and one coalesced write of the limb: the forward's first pass and the
-// inverse's last pass already hold the strided pattern idx = tid + T*r, and the other
-// end goes through shared memory.  Butterflies are Harvey-lazy (forward values in
-// [0,4q), inverse in [0,2q)) with Shoup twiddles, so q < 2^62.  Caller-supplied
-// load/store functors fuse prologues (pointwise products, centered lifts, modulus
-// raise) and epilogues (rescale, key-switch MAC, bias) into the same pass over HBM.
+// B200 design.  N = K * M with M <= 2^13 residues (64 KiB) per CTA, so two or three CTAs
+// share an SM and one CTA's global loads overlap another's butterflies.
+//   Forward: CTA r of the cluster loads, for its M/K low indices j, all K residues
+//   j + t M (t < K) and runs the first log K stages in registers (they only mix the top
+//   log K index bits); the residues of sub-block t are then stored into CTA t's shared
+//   memory (DSMEM all-to-all), and every CTA finishes the remaining log M stages of its
+//   own contiguous sub-block.  The inverse mirrors this (sub-block stages first, exchange,
+//   last log K stages with N^-1 folded in).  K = 1 is the plain one-CTA transform.
+//   Inside a CTA, T = M/E threads hold E = 2^LOGE residues in registers; the log M stages
+//   run as ceil(log M / LOGE) register-resident radix-2^LOGE passes with a padded
+//   shared-memory exchange between passes (pad 1 word per 16: conflict-free 64-bit
+//   accesses in every pass).  Global traffic is one coalesced read and one coalesced
+//   write of the limb.  Butterflies are Harvey-lazy (forward values in [0,4q), inverse in
+//   [0,2q)) with Shoup twiddles {w, floor(w 2^64/q)}, so q < 2^61.  Caller-supplied
+//   load(idx)/store(idx, v) functors (global coefficient index idx) fuse prologues and
+//   epilogues (pointwise products, centered lifts, modulus raise, rescale, key-switch
+//   MAC, bias) into the same pass over HBM.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "arith.cuh"
 
 namespace edl {
 
-// Residues per thread: the plain transform keeps 32 per thread (fewer exchanges); the
-// fused kernels, whose prologue/epilogue need registers and more warps to hide their
-// extra global traffic, keep 16 (N = 2^14: 1024 threads).  Measured in round 1.
-__host__ __device__ constexpr int loge_plain(int logn) { return logn >= 14 ? 5 : (logn >= 12 ? 4 : 3); }
-__host__ __device__ constexpr int loge_fused(int logn) { return logn >= 14 ? 4 : 3; }
-
-template <int LOGN, int LOGE_ = loge_fused(LOGN)>
-struct NttShape {
-    static constexpr int N = 1 << LOGN;
+template <int LOGN_, int LOGK_, int LOGE_, int MINB_>
+struct NttCfg {
+    static constexpr int LOGN = LOGN_;
+    static constexpr int LOGK = LOGK_;
+    static constexpr int LOGM = LOGN_ - LOGK_;
     static constexpr int LOGE = LOGE_;
+    static constexpr int N = 1 << LOGN;
+    static constexpr int K = 1 << LOGK;
+    static constexpr int M = 1 << LOGM;
     static constexpr int E = 1 << LOGE;
-    static constexpr int T = N / E;
-    static constexpr int NPASS = (LOGN + LOGE - 1) / LOGE;
-    static constexpr int SMEM_WORDS = N + N / 16;
+    static constexpr int T = M / E;                   // threads per CTA
+    static constexpr int NPASS = (LOGM + LOGE - 1) / LOGE;
+    static constexpr int MINB = MINB_;               // __launch_bounds__ min blocks / SM
+    static constexpr int SMEM_WORDS = M + M / 16;
     static constexpr int SMEM_BYTES = SMEM_WORDS * 8;
+    static_assert(E >= K, "phase A needs every thread to hold all K residues of a column");
+    static_assert(LOGE <= LOGM && T >= 32, "at least one warp per CTA");
+    // cluster rank (which sub-block this CTA owns) and the limb/grid index above it
+    __device__ static __forceinline__ int crank() { return K == 1 ? 0 : (int)(blockIdx.x & (K - 1)); }
+    __device__ static __forceinline__ int bx() { return (int)(blockIdx.x >> LOGK); }
+    // The coefficient indices a thread stores after ntt_fwd and loads before ntt_inv,
+    // r < E: idx(r) = crank*M + tid + T*r (coalesced).
+    __device__ static __forceinline__ int idx(int r) { return (crank() << LOGM) + (int)threadIdx.x + r * T; }
 };
 
 __device__ __forceinline__ int spad(int idx) { return idx + (idx >> 4); }
+
+__device__ __forceinline__ void cluster_sync_all() { cooperative_groups::this_cluster().sync(); }
+
+template <class C>
+__device__ __forceinline__ uint64_t* cluster_smem(uint64_t* sm, int rank) {
+    if constexpr (C::K == 1) return sm;
+    else return cooperative_groups::this_cluster().map_shared_rank(sm, rank);
+}
 
 // ---- forward CT butterfly (Harvey): X, Y in [0,4q) -> [0,4q)
 __device__ __forceinline__ void ct_bfly(uint64_t& X, uint64_t& Y, ulonglong2 w, uint64_t q, uint64_t two_q) {
@@ -54,25 +82,28 @@ __device__ __forceinline__ void gs_bfly(uint64_t& X, uint64_t& Y, uint64_t w, ui
     Y = shoup_lazy2(x - y + two_q, w, ws, q);
 }
 
-// One forward pass over stages [S0, S0+NS) for `v`-th virtual thread's group held in x[].
-// Element r of the group sits at index  (high << (BTOP+1)) | (r << BLOW) | low.
-template <int LOGN, int S0, int NS>
-__device__ __forceinline__ void fwd_pass_regs(uint64_t* x, int high, const ulonglong2* __restrict__ tw,
-                                              uint64_t q, uint64_t two_q) {
+// NS forward stages on a group x[0..2^NS) held in registers; absolute stage SA + k uses
+// twiddle index 2^(SA+k) + (high << k) + (r >> (NS-k)), `high` = the group's index bits
+// above the stage window (SURVEY O3 stage twiddle psi^brv(m+i)).
+template <int SA, int NS>
+__device__ __forceinline__ void fwd_pass_regs(uint64_t* x, int high, const ulonglong2* __restrict__ tw, uint64_t q,
+                                              uint64_t two_q) {
 #pragma unroll
     for (int k = 0; k < NS; k++) {
         const int half = 1 << (NS - 1 - k);
 #pragma unroll
         for (int r = 0; r < (1 << NS); r++) {
             if (r & half) continue;
-            const int tidx = (1 << (S0 + k)) + (high << k) + (r >> (NS - k));
+            const int tidx = (1 << (SA + k)) + (high << k) + (r >> (NS - k));
             ulonglong2 w = __ldg(tw + tidx);
             ct_bfly(x[r], x[r + half], w, q, two_q);
         }
     }
 }
 
-template <int LOGN, int S0, int NS, bool LAST>
+// NS inverse stages, last to first; with LAST the absolute stage 0 folds N^-1 into both
+// outputs (psi^-brv(1) N^-1 for the odd one).
+template <int SA, int NS, bool LAST>
 __device__ __forceinline__ void inv_pass_regs(uint64_t* x, int high, const ModInfo& m, uint64_t two_q) {
 #pragma unroll
     for (int k = NS - 1; k >= 0; k--) {
@@ -80,13 +111,12 @@ __device__ __forceinline__ void inv_pass_regs(uint64_t* x, int high, const ModIn
 #pragma unroll
         for (int r = 0; r < (1 << NS); r++) {
             if (r & half) continue;
-            if (LAST && S0 + k == 0) {
-                // stage 0 (m = 1): fold N^-1 into both outputs
+            if (LAST && SA + k == 0) {
                 uint64_t a = x[r], b = x[r + half];
                 x[r] = shoup_lazy2(a + b, m.ninv, m.ninv_s, m.q);
                 x[r + half] = shoup_lazy2(a - b + two_q, m.w1ninv, m.w1ninv_s, m.q);
             } else {
-                const int tidx = (1 << (S0 + k)) + (high << k) + (r >> (NS - k));
+                const int tidx = (1 << (SA + k)) + (high << k) + (r >> (NS - k));
                 ulonglong2 w = __ldg(m.tw_inv + tidx);
                 gs_bfly(x[r], x[r + half], w.x, w.y, m.q, two_q);
             }
@@ -94,27 +124,24 @@ __device__ __forceinline__ void inv_pass_regs(uint64_t* x, int high, const ModIn
     }
 }
 
-// Compile-time pass descriptor: pass P covers stages [P*LOGE, min((P+1)*LOGE, LOGN)).
-template <int LOGN, int LOGE, int P>
+// In-CTA pass P over local stages [SL, SL+NS) of the M-point sub-block.
+template <class C, int P>
 struct PassInfo {
-    using S = NttShape<LOGN, LOGE>;
-    static constexpr int S0 = P * S::LOGE;
-    static constexpr int NS = (S0 + S::LOGE <= LOGN) ? S::LOGE : (LOGN - S0);
-    static constexpr int BTOP = LOGN - 1 - S0;
+    static constexpr int SL = P * C::LOGE;
+    static constexpr int NS = (SL + C::LOGE <= C::LOGM) ? C::LOGE : (C::LOGM - SL);
+    static constexpr int SA = SL + C::LOGK;            // absolute stage (twiddle index)
+    static constexpr int BTOP = C::LOGM - 1 - SL;
     static constexpr int BLOW = BTOP - NS + 1;
-    static constexpr int G = S::E >> NS;     // groups per thread
+    static constexpr int G = C::E >> NS;              // groups per thread
 };
 
-// Forward middle/last pass: read from smem, compute, write back to smem (natural index).
-template <int LOGN, int LOGE, int P>
-__device__ __forceinline__ void fwd_pass_smem(uint64_t* sm, const ulonglong2* __restrict__ tw, uint64_t q,
-                                              uint64_t two_q) {
-    using PI = PassInfo<LOGN, LOGE, P>;
-    using S = NttShape<LOGN, LOGE>;
-    uint64_t x[S::E];
+template <class C, int P, bool INV>
+__device__ __forceinline__ void pass_smem(uint64_t* sm, const ModInfo& m, uint64_t two_q) {
+    using PI = PassInfo<C, P>;
+    uint64_t x[C::E];
 #pragma unroll
     for (int g = 0; g < PI::G; g++) {
-        const int v = threadIdx.x + g * S::T;
+        const int v = threadIdx.x + g * C::T;
         const int low = v & ((1 << PI::BLOW) - 1);
         const int high = v >> PI::BLOW;
         const int base = (high << (PI::BTOP + 1)) | low;
@@ -122,15 +149,17 @@ __device__ __forceinline__ void fwd_pass_smem(uint64_t* sm, const ulonglong2* __
         for (int r = 0; r < (1 << PI::NS); r++) x[g * (1 << PI::NS) + r] = sm[spad(base | (r << PI::BLOW))];
     }
     __syncthreads();
+    const int hc = C::crank() << PI::SL;
 #pragma unroll
     for (int g = 0; g < PI::G; g++) {
-        const int v = threadIdx.x + g * S::T;
-        const int high = v >> PI::BLOW;
-        fwd_pass_regs<LOGN, PI::S0, PI::NS>(x + g * (1 << PI::NS), high, tw, q, two_q);
+        const int v = threadIdx.x + g * C::T;
+        const int high = hc | (v >> PI::BLOW);
+        if constexpr (INV) inv_pass_regs<PI::SA, PI::NS, false>(x + g * (1 << PI::NS), high, m, two_q);
+        else fwd_pass_regs<PI::SA, PI::NS>(x + g * (1 << PI::NS), high, m.tw_fwd, m.q, two_q);
     }
 #pragma unroll
     for (int g = 0; g < PI::G; g++) {
-        const int v = threadIdx.x + g * S::T;
+        const int v = threadIdx.x + g * C::T;
         const int low = v & ((1 << PI::BLOW) - 1);
         const int high = v >> PI::BLOW;
         const int base = (high << (PI::BTOP + 1)) | low;
@@ -140,102 +169,153 @@ __device__ __forceinline__ void fwd_pass_smem(uint64_t* sm, const ulonglong2* __
     __syncthreads();
 }
 
-template <int LOGN, int LOGE, int P>
-__device__ __forceinline__ void inv_pass_smem(uint64_t* sm, const ModInfo& m, uint64_t two_q) {
-    using PI = PassInfo<LOGN, LOGE, P>;
-    using S = NttShape<LOGN, LOGE>;
-    uint64_t x[S::E];
-#pragma unroll
-    for (int g = 0; g < PI::G; g++) {
-        const int v = threadIdx.x + g * S::T;
-        const int low = v & ((1 << PI::BLOW) - 1);
-        const int high = v >> PI::BLOW;
-        const int base = (high << (PI::BTOP + 1)) | low;
-#pragma unroll
-        for (int r = 0; r < (1 << PI::NS); r++) x[g * (1 << PI::NS) + r] = sm[spad(base | (r << PI::BLOW))];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int g = 0; g < PI::G; g++) {
-        const int v = threadIdx.x + g * S::T;
-        const int high = v >> PI::BLOW;
-        inv_pass_regs<LOGN, PI::S0, PI::NS, false>(x + g * (1 << PI::NS), high, m, two_q);
-    }
-#pragma unroll
-    for (int g = 0; g < PI::G; g++) {
-        const int v = threadIdx.x + g * S::T;
-        const int low = v & ((1 << PI::BLOW) - 1);
-        const int high = v >> PI::BLOW;
-        const int base = (high << (PI::BTOP + 1)) | low;
-#pragma unroll
-        for (int r = 0; r < (1 << PI::NS); r++) sm[spad(base | (r << PI::BLOW))] = x[g * (1 << PI::NS) + r];
-    }
-    __syncthreads();
-}
-
-template <int LOGN, int LOGE, int P>
-__device__ __forceinline__ void fwd_middle(uint64_t* sm, const ulonglong2* tw, uint64_t q, uint64_t two_q) {
-    if constexpr (P < NttShape<LOGN, LOGE>::NPASS) {
-        fwd_pass_smem<LOGN, LOGE, P>(sm, tw, q, two_q);
-        fwd_middle<LOGN, LOGE, P + 1>(sm, tw, q, two_q);
+template <class C, int P>
+__device__ __forceinline__ void fwd_middle(uint64_t* sm, const ModInfo& m, uint64_t two_q) {
+    if constexpr (P < C::NPASS) {
+        pass_smem<C, P, false>(sm, m, two_q);
+        fwd_middle<C, P + 1>(sm, m, two_q);
     }
 }
 
-// Inverse passes run from the last pass down to pass 1 (pass 0 is register-resident).
-template <int LOGN, int LOGE, int P>
+template <class C, int P>
 __device__ __forceinline__ void inv_middle(uint64_t* sm, const ModInfo& m, uint64_t two_q) {
     if constexpr (P > 0) {
-        inv_pass_smem<LOGN, LOGE, P>(sm, m, two_q);
-        inv_middle<LOGN, LOGE, P - 1>(sm, m, two_q);
+        pass_smem<C, P, true>(sm, m, two_q);
+        inv_middle<C, P - 1>(sm, m, two_q);
     }
 }
 
-// Forward NTT of one limb.  load(idx) -> residue in [0, 4q) (called with idx = tid + T*r);
-// store(idx, value) receives canonical [0, q) values, idx = tid + T*r (coalesced).
-template <int LOGN, int LOGE = loge_fused(LOGN), class Load, class Store>
-__device__ __forceinline__ void ntt_fwd_block(uint64_t* sm, const ModInfo& m, Load load, Store store) {
-    using S = NttShape<LOGN, LOGE>;
-    using P0 = PassInfo<LOGN, LOGE, 0>;
-    static_assert(P0::G == 1 && P0::BLOW == LOGN - S::LOGE, "pass 0 layout");
+// Forward NTT of one limb.  load(idx) -> residue in [0, 4q); store(idx, v) receives
+// canonical values at idx = C::idx(r).
+template <class C, class Load, class Store>
+__device__ __forceinline__ void ntt_fwd(uint64_t* sm, const ModInfo& m, Load load, Store store) {
+    using P0 = PassInfo<C, 0>;
+    static_assert(P0::G == 1 && P0::BLOW == C::LOGM - C::LOGE, "pass 0 layout");
     const uint64_t q = m.q, two_q = 2 * q;
-    const ulonglong2* tw = m.tw_fwd;
-    uint64_t x[S::E];
+    const int tid = threadIdx.x;
+    uint64_t x[C::E];
+    if constexpr (C::K == 1) {
 #pragma unroll
-    for (int r = 0; r < S::E; r++) x[r] = load(threadIdx.x + r * S::T);
-    fwd_pass_regs<LOGN, 0, S::LOGE>(x, 0, tw, q, two_q);
+        for (int r = 0; r < C::E; r++) x[r] = load(tid + r * C::T);
+    } else {
+        // phase A: columns j (this CTA's M/K of them) x all K sub-blocks, stages 0..logK-1
+        const int j0 = C::crank() * (C::M / C::K) + tid;
 #pragma unroll
-    for (int r = 0; r < S::E; r++) sm[spad(threadIdx.x + r * S::T)] = x[r];
+        for (int g = 0; g < C::E / C::K; g++) {
+#pragma unroll
+            for (int t = 0; t < C::K; t++) x[g * C::K + t] = load(j0 + g * C::T + t * C::M);
+            fwd_pass_regs<0, C::LOGK>(x + g * C::K, 0, m.tw_fwd, q, two_q);
+        }
+        cluster_sync_all();   // every CTA is running and done with its shared memory
+#pragma unroll
+        for (int t = 0; t < C::K; t++) {
+            uint64_t* dst = cluster_smem<C>(sm, t);
+#pragma unroll
+            for (int g = 0; g < C::E / C::K; g++) dst[spad(j0 + g * C::T)] = x[g * C::K + t];
+        }
+        cluster_sync_all();
+#pragma unroll
+        for (int r = 0; r < C::E; r++) x[r] = sm[spad(tid + r * C::T)];
+    }
+    fwd_pass_regs<C::LOGK, C::LOGE>(x, C::crank(), m.tw_fwd, q, two_q);
+#pragma unroll
+    for (int r = 0; r < C::E; r++) sm[spad(tid + r * C::T)] = x[r];
     __syncthreads();
-    fwd_middle<LOGN, LOGE, 1>(sm, tw, q, two_q);
+    fwd_middle<C, 1>(sm, m, two_q);
 #pragma unroll
-    for (int r = 0; r < S::E; r++) {
-        const int idx = threadIdx.x + r * S::T;
-        uint64_t v = sm[spad(idx)];
+    for (int r = 0; r < C::E; r++) {
+        uint64_t v = sm[spad(tid + r * C::T)];
         v = csub(csub(v, two_q), q);
-        store(idx, v);
+        store(C::idx(r), v);
     }
     __syncthreads();   // smem reusable by the caller's next transform
 }
 
-// Inverse NTT of one limb.  load(idx) -> residue in [0, 2q); store(idx, canonical value).
-template <int LOGN, int LOGE = loge_fused(LOGN), class Load, class Store>
-__device__ __forceinline__ void ntt_inv_block(uint64_t* sm, const ModInfo& m, Load load, Store store) {
-    using S = NttShape<LOGN, LOGE>;
+// Inverse NTT of one limb.  load(idx) at idx = C::idx(r) -> residue in [0, 2q);
+// store(idx, canonical value).
+template <class C, class Load, class Store>
+__device__ __forceinline__ void ntt_inv(uint64_t* sm, const ModInfo& m, Load load, Store store) {
     const uint64_t q = m.q, two_q = 2 * q;
+    const int tid = threadIdx.x;
 #pragma unroll
-    for (int r = 0; r < S::E; r++) {
-        const int idx = threadIdx.x + r * S::T;
-        sm[spad(idx)] = load(idx);
-    }
+    for (int r = 0; r < C::E; r++) sm[spad(tid + r * C::T)] = load(C::idx(r));
     __syncthreads();
-    inv_middle<LOGN, LOGE, S::NPASS - 1>(sm, m, two_q);
-    uint64_t x[S::E];
+    inv_middle<C, C::NPASS - 1>(sm, m, two_q);
+    uint64_t x[C::E];
 #pragma unroll
-    for (int r = 0; r < S::E; r++) x[r] = sm[spad(threadIdx.x + r * S::T)];
-    inv_pass_regs<LOGN, 0, S::LOGE, true>(x, 0, m, two_q);
+    for (int r = 0; r < C::E; r++) x[r] = sm[spad(tid + r * C::T)];
+    inv_pass_regs<C::LOGK, C::LOGE, C::K == 1>(x, C::crank(), m, two_q);
+    if constexpr (C::K == 1) {
 #pragma unroll
-    for (int r = 0; r < S::E; r++) store(threadIdx.x + r * S::T, csub(x[r], q));
-    __syncthreads();   // smem reusable by the caller's next transform
+        for (int r = 0; r < C::E; r++) store(tid + r * C::T, csub(x[r], q));
+        __syncthreads();
+    } else {
+        constexpr int MK = C::M / C::K;
+        cluster_sync_all();   // every CTA has read its sub-block out of shared memory
+#pragma unroll
+        for (int r = 0; r < C::E; r++) {
+            const int j = tid + r * C::T;
+            cluster_smem<C>(sm, j / MK)[spad(C::crank() * MK + (j & (MK - 1)))] = x[r];
+        }
+        cluster_sync_all();
+        // phase A': columns j x all K sub-blocks, stages logK-1..0 (N^-1 folded in)
+        const int j0 = C::crank() * MK + tid;
+#pragma unroll
+        for (int g = 0; g < C::E / C::K; g++) {
+#pragma unroll
+            for (int t = 0; t < C::K; t++) x[g * C::K + t] = sm[spad(t * MK + tid + g * C::T)];
+            inv_pass_regs<0, C::LOGK, true>(x + g * C::K, 0, m, two_q);
+#pragma unroll
+            for (int t = 0; t < C::K; t++) store(j0 + g * C::T + t * C::M, csub(x[g * C::K + t], q));
+        }
+        __syncthreads();
+    }
 }
+
+// ---- per-N configurations -------------------------------------------------------------
+// M = N/K <= 2^13 per CTA.  Plain transforms keep E = 32 residues per thread (fewer
+// exchanges); fused kernels, whose prologue/epilogue need registers, pick their own E.
+// Round-2 measurements (tools/ntt_bench.py, B200): at N = 2^14 the plain transform is
+// 6 % faster as a 2-CTA cluster (5.0 vs 4.7 M limbs/s) while the fused kernels are 15-30 %
+// slower (their prologue/epilogue traffic per CTA doubles relative to the butterflies),
+// so plain and fused configs choose K separately.
+#ifndef EDL_K14_PLAIN
+#define EDL_K14_PLAIN 2
+#endif
+#ifndef EDL_K14_FUSED
+#define EDL_K14_FUSED 1
+#endif
+#ifndef EDL_LOGE_P14
+#define EDL_LOGE_P14 5
+#endif
+#ifndef EDL_LOGE_F14
+#define EDL_LOGE_F14 4
+#endif
+#ifndef EDL_LOGE_F13
+#define EDL_LOGE_F13 5
+#endif
+
+__host__ __device__ constexpr int cfg_logk(int logn, bool plain) {
+    return logn <= 13 ? 0 : (logn == 14 ? ((plain ? EDL_K14_PLAIN : EDL_K14_FUSED) == 2 ? 1 : 0) : logn - 13);
+}
+__host__ __device__ constexpr int cfg_logm(int logn, bool plain) { return logn - cfg_logk(logn, plain); }
+__host__ __device__ constexpr int cfg_loge(int logn, bool plain) {
+    return cfg_logm(logn, plain) == 14 ? (plain ? EDL_LOGE_P14 : EDL_LOGE_F14)
+                                       : (cfg_logm(logn, plain) >= 12 ? (plain ? 5 : EDL_LOGE_F13)
+                                                                      : (cfg_logm(logn, plain) >= 10 ? 4 : 3));
+}
+// blocks per SM for __launch_bounds__: as many CTAs as leave 128 registers per thread
+// (2^14 residues per CTA need 136 KiB of shared memory: one CTA)
+__host__ __device__ constexpr int cfg_minb(int logm, int loge) {
+    return logm == 14 ? 1
+                      : ((65536 >> (logm - loge + 7)) < 1 ? 1 : ((65536 >> (logm - loge + 7)) > 3 ? 3 : (65536 >> (logm - loge + 7))));
+}
+
+template <int LOGN, bool PLAIN>
+using CfgOf = NttCfg<LOGN, cfg_logk(LOGN, PLAIN), cfg_loge(LOGN, PLAIN), cfg_minb(cfg_logm(LOGN, PLAIN), cfg_loge(LOGN, PLAIN))>;
+template <int LOGN>
+using CfgPlain = CfgOf<LOGN, true>;
+template <int LOGN>
+using CfgFused = CfgOf<LOGN, false>;
 
 }  // namespace edl

@@ -7,57 +7,47 @@
 
 namespace edl {
 
-#define EDL_DISPATCH_LOGN(logn, ...)                   \
-    switch (logn) {                                     \
-        case 10: { constexpr int LOGN = 10; __VA_ARGS__; } break; \
-        case 11: { constexpr int LOGN = 11; __VA_ARGS__; } break; \
-        case 12: { constexpr int LOGN = 12; __VA_ARGS__; } break; \
-        case 13: { constexpr int LOGN = 13; __VA_ARGS__; } break; \
-        case 14: { constexpr int LOGN = 14; __VA_ARGS__; } break; \
-        default: break;                                 \
-    }
-
 struct PrimeMap {
     int8_t idx[MAXM];
 };
 
 // ------------------------------------------------------------------------------------
 // K1/K2: plain batched NTT / INTT, in place, data [batch][nl][N], limb j uses pm.idx[j].
-template <int LOGN, bool INV>
-__global__ void __launch_bounds__(NttShape<LOGN, loge_plain(LOGN)>::T, 1)
+template <class C, bool INV>
+__global__ void __launch_bounds__(C::T, C::MINB)
 k_ntt_limbs(uint64_t* __restrict__ data, int nl, const __grid_constant__ PrimeMap pm, const ModInfo* __restrict__ mods) {
     extern __shared__ uint64_t sm[];
-    const int limb = blockIdx.x;
-    uint64_t* p = data + (((size_t)blockIdx.y * nl + limb) << LOGN);
+    const int limb = C::bx();
+    uint64_t* p = data + (((size_t)blockIdx.y * nl + limb) << C::LOGN);
     const ModInfo m = mods[pm.idx[limb]];
     auto ld = [&](int idx) { return p[idx]; };
     auto st = [&](int idx, uint64_t v) { p[idx] = v; };
-    if constexpr (INV) ntt_inv_block<LOGN, loge_plain(LOGN)>(sm, m, ld, st);
-    else ntt_fwd_block<LOGN, loge_plain(LOGN)>(sm, m, ld, st);
+    if constexpr (INV) ntt_inv<C>(sm, m, ld, st);
+    else ntt_fwd<C>(sm, m, ld, st);
 }
 
 // ------------------------------------------------------------------------------------
 // K6 rescale, step 1 (O12): r = INTT_{q_l}(c[l] * w_l) for both polys of every ct.  With a
 // second constant w2 the same INTT also yields r2 = INTT(c[l] * w2_l) (INTT is linear),
 // which the sigma schedule uses for its two scalar products of y (O13 steps 2 and 4).
-template <int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::T, 1)
+template <class C>
+__global__ void __launch_bounds__(C::T, C::MINB)
 k_rescale_intt(const uint64_t* __restrict__ in, int l, const ulonglong2* __restrict__ w,
                uint64_t* __restrict__ r_out, const ulonglong2* __restrict__ w2, uint64_t* __restrict__ r_out2,
                const ModInfo* __restrict__ mods) {
     extern __shared__ uint64_t sm[];
-    const int p = blockIdx.x;
+    const int p = C::bx();
     const int64_t c = blockIdx.y;
-    const uint64_t* src = in + limb_off(c, p, l, l + 1, LOGN);
-    uint64_t* dst = r_out + (((size_t)c * 2 + p) << LOGN);
-    uint64_t* dst2 = r_out2 ? r_out2 + (((size_t)c * 2 + p) << LOGN) : nullptr;
+    const uint64_t* src = in + limb_off(c, p, l, l + 1, C::LOGN);
+    uint64_t* dst = r_out + (((size_t)c * 2 + p) << C::LOGN);
+    uint64_t* dst2 = r_out2 ? r_out2 + (((size_t)c * 2 + p) << C::LOGN) : nullptr;
     const ModInfo m = mods[l];
     if (w2 == nullptr) {
         const bool has_w = (w != nullptr);
         ulonglong2 wl = has_w ? w[c * (l + 1) + l] : make_ulonglong2(1, 0);
         auto ld = [&](int idx) { return has_w ? shoup_lazy2(src[idx], wl.x, wl.y, m.q) : src[idx]; };
         auto st = [&](int idx, uint64_t v) { dst[idx] = v; };
-        ntt_inv_block<LOGN>(sm, m, ld, st);
+        ntt_inv<C>(sm, m, ld, st);
     } else {
         const ulonglong2 wa = w[c * (l + 1) + l], wb = w2[c * (l + 1) + l];
         auto ld = [&](int idx) { return src[idx]; };
@@ -65,26 +55,26 @@ k_rescale_intt(const uint64_t* __restrict__ in, int l, const ulonglong2* __restr
             dst[idx] = shoup(v, wa.x, wa.y, m.q);
             dst2[idx] = shoup(v, wb.x, wb.y, m.q);
         };
-        ntt_inv_block<LOGN>(sm, m, ld, st);
+        ntt_inv<C>(sm, m, ld, st);
     }
 }
 
 // K6 rescale, step 2: out_i = (c_i w_i - NTT_i([r]_{q_l} mod q_i)) q_l^{-1} (+ bias_i).
-template <int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::T, 1)
+template <class C>
+__global__ void __launch_bounds__(C::T, C::MINB)
 k_rescale_ntt(const uint64_t* __restrict__ in, int l, const ulonglong2* __restrict__ w,
               const uint64_t* __restrict__ r, const uint64_t* __restrict__ bias, uint64_t* __restrict__ out, int nlo,
               const ModInfo* __restrict__ mods, const ChainConsts* __restrict__ cc) {
     extern __shared__ uint64_t sm[];
-    const int i = blockIdx.x, p = blockIdx.y;
+    const int i = C::bx(), p = blockIdx.y;
     const int64_t c = blockIdx.z;
     const ModInfo m = mods[i];
     const uint64_t ql = mods[l].q;
     const uint64_t ql_mod = cc->qmod[l][i];
     const ulonglong2 qlinv = cc->qinv[l][i];
-    const uint64_t* rr = r + (((size_t)c * 2 + p) << LOGN);
-    const uint64_t* src = in + limb_off(c, p, i, l + 1, LOGN);
-    uint64_t* dst = out + limb_off(c, p, i, nlo, LOGN);
+    const uint64_t* rr = r + (((size_t)c * 2 + p) << C::LOGN);
+    const uint64_t* src = in + limb_off(c, p, i, l + 1, C::LOGN);
+    uint64_t* dst = out + limb_off(c, p, i, nlo, C::LOGN);
     const bool has_w = (w != nullptr);
     const ulonglong2 wi = has_w ? w[c * (l + 1) + i] : make_ulonglong2(1, 0);
     const uint64_t b = (bias != nullptr && p == 0) ? bias[c * l + i] : 0;
@@ -95,7 +85,7 @@ k_rescale_ntt(const uint64_t* __restrict__ in, int l, const ulonglong2* __restri
         uint64_t v = shoup(submod(a, x, m.q) , qlinv.x, qlinv.y, m.q);
         dst[idx] = addmod(v, b, m.q);
     };
-    ntt_fwd_block<LOGN>(sm, m, ld, st);
+    ntt_fwd<C>(sm, m, ld, st);
 }
 
 // ------------------------------------------------------------------------------------
@@ -122,39 +112,38 @@ __device__ __forceinline__ uint64_t tensor_comp(const uint64_t* a, const uint64_
     return barrett128(s, m);
 }
 
-template <int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::T, 1)
+template <class C>
+__global__ void __launch_bounds__(C::T, C::MINB)
 k_relin_intt_d2(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l,
                 uint64_t* __restrict__ acoef, const ModInfo* __restrict__ mods) {
     extern __shared__ uint64_t sm[];
-    const int j = blockIdx.x;
+    const int j = C::bx();
     const int64_t c = blockIdx.y;
     const ModInfo m = mods[j];
-    const uint64_t* a1 = a + limb_off(c, 1, j, l + 1, LOGN);
-    const uint64_t* b1 = b + limb_off(c, 1, j, l + 1, LOGN);
-    uint64_t* dst = acoef + (((size_t)c * (l + 1) + j) << LOGN);
+    const uint64_t* a1 = a + limb_off(c, 1, j, l + 1, C::LOGN);
+    const uint64_t* b1 = b + limb_off(c, 1, j, l + 1, C::LOGN);
+    uint64_t* dst = acoef + (((size_t)c * (l + 1) + j) << C::LOGN);
     auto ld = [&](int idx) { return mulmod(a1[idx], b1[idx], m); };
     auto st = [&](int idx, uint64_t v) { dst[idx] = v; };
-    ntt_inv_block<LOGN>(sm, m, ld, st);
+    ntt_inv<C>(sm, m, ld, st);
 }
 
-template <int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::T, 1)
+template <class C>
+__global__ void __launch_bounds__(C::T, C::MINB)
 k_relin_ks_mac(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l,
                const uint64_t* __restrict__ acoef, const uint64_t* __restrict__ rlk,
                const uint64_t* __restrict__ rlk_s, int L, uint64_t* __restrict__ acc,
                const ModInfo* __restrict__ mods) {
-    using S = NttShape<LOGN>;
     extern __shared__ uint64_t sm[];
-    const int ti = blockIdx.x;                 // 0..l data targets, l+1 = P
+    const int ti = C::bx();                 // 0..l data targets, l+1 = P
     const int64_t c = blockIdx.y;
     const int t = (ti == l + 1) ? (L + 1) : ti;
     const ModInfo m = mods[t];
-    uint64_t* acc0 = acc + ((((size_t)c * 2 + 0) * (l + 2) + ti) << LOGN);
-    uint64_t* acc1 = acc + ((((size_t)c * 2 + 1) * (l + 2) + ti) << LOGN);
+    uint64_t* acc0 = acc + ((((size_t)c * 2 + 0) * (l + 2) + ti) << C::LOGN);
+    uint64_t* acc1 = acc + ((((size_t)c * 2 + 1) * (l + 2) + ti) << C::LOGN);
     for (int j = 0; j <= l; j++) {
-        const size_t r0 = (((size_t)j * 2 + 0) * (L + 2) + t) << LOGN;
-        const size_t r1 = (((size_t)j * 2 + 1) * (L + 2) + t) << LOGN;
+        const size_t r0 = (((size_t)j * 2 + 0) * (L + 2) + t) << C::LOGN;
+        const size_t r1 = (((size_t)j * 2 + 1) * (L + 2) + t) << C::LOGN;
         auto epi = [&](int idx, uint64_t x) {
             uint64_t p0 = shoup(x, rlk[r0 + idx], rlk_s[r0 + idx], m.q);
             uint64_t p1 = shoup(x, rlk[r1 + idx], rlk_s[r1 + idx], m.q);
@@ -167,77 +156,77 @@ k_relin_ks_mac(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, i
             }
         };
         if (ti == j) {
-            const uint64_t* a1 = a + limb_off(c, 1, j, l + 1, LOGN);
-            const uint64_t* b1 = b + limb_off(c, 1, j, l + 1, LOGN);
+            const uint64_t* a1 = a + limb_off(c, 1, j, l + 1, C::LOGN);
+            const uint64_t* b1 = b + limb_off(c, 1, j, l + 1, C::LOGN);
 #pragma unroll 4
-            for (int r = 0; r < S::E; r++) {
-                const int idx = threadIdx.x + r * S::T;
+            for (int r = 0; r < C::E; r++) {
+                const int idx = C::idx(r);
                 epi(idx, mulmod(a1[idx], b1[idx], m));
             }
         } else {
-            const uint64_t* src = acoef + (((size_t)c * (l + 1) + j) << LOGN);
+            const uint64_t* src = acoef + (((size_t)c * (l + 1) + j) << C::LOGN);
             const bool need_red = mods[j].q > 4 * m.q;   // the forward NTT accepts [0, 4q)
             auto ld = [&](int idx) {
                 uint64_t v = src[idx];
                 return need_red ? reduce64(v, m) : v;
             };
-            ntt_fwd_block<LOGN>(sm, m, ld, epi);
+            ntt_fwd<C>(sm, m, ld, epi);
         }
     }
 }
 
-template <int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::T, 1)
+template <class C>
+__global__ void __launch_bounds__(C::T, C::MINB)
 k_relin_moddown_intt(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l,
                      const uint64_t* __restrict__ acc, int L, int rescale, uint64_t* __restrict__ r_out,
                      uint64_t* __restrict__ s_out, const ModInfo* __restrict__ mods,
                      const ChainConsts* __restrict__ cc) {
     extern __shared__ uint64_t sm[];
-    const int cp = blockIdx.x;
+    const int cp = C::bx();
     const int64_t c = blockIdx.y;
     const ModInfo mp = mods[L + 1];
-    const uint64_t* accP = acc + ((((size_t)c * 2 + cp) * (l + 2) + (l + 1)) << LOGN);
-    uint64_t* rdst = r_out + (((size_t)c * 2 + cp) << LOGN);
+    const uint64_t* accP = acc + ((((size_t)c * 2 + cp) * (l + 2) + (l + 1)) << C::LOGN);
+    uint64_t* rdst = r_out + (((size_t)c * 2 + cp) << C::LOGN);
     {
         auto ld = [&](int idx) { return accP[idx]; };
         auto st = [&](int idx, uint64_t v) { rdst[idx] = v; };
-        ntt_inv_block<LOGN>(sm, mp, ld, st);
+        ntt_inv<C>(sm, mp, ld, st);
     }
     if (!rescale) return;
     const ModInfo ml = mods[l];
     const ulonglong2 pinv = cc->qinv[L + 1][l];
     const uint64_t pmod = cc->qmod[L + 1][l];
-    const uint64_t* accl = acc + ((((size_t)c * 2 + cp) * (l + 2) + l) << LOGN);
-    uint64_t* sdst = s_out + (((size_t)c * 2 + cp) << LOGN);
+    const uint64_t* accl = acc + ((((size_t)c * 2 + cp) * (l + 2) + l) << C::LOGN);
+    uint64_t* sdst = s_out + (((size_t)c * 2 + cp) << C::LOGN);
     auto ld = [&](int idx) {
-        uint64_t d = tensor_comp(a, b, c, cp, l, l + 1, LOGN, idx, ml);
+        uint64_t d = tensor_comp(a, b, c, cp, l, l + 1, C::LOGN, idx, ml);
         return addmod(d, shoup(accl[idx], pinv.x, pinv.y, ml.q), ml.q);
     };
     auto st = [&](int idx, uint64_t y) {
         uint64_t z = shoup(center_mod(rdst[idx], mp.q, pmod, ml), pinv.x, pinv.y, ml.q);
         sdst[idx] = submod(y, z, ml.q);
     };
-    ntt_inv_block<LOGN>(sm, ml, ld, st);
+    ntt_inv<C>(sm, ml, ld, st);
 }
 
-template <int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::T, 1)
+template <class C>
+__global__ void __launch_bounds__(C::T, C::MINB)
 k_relin_moddown_ntt(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l,
                     const uint64_t* __restrict__ acc, const uint64_t* __restrict__ r,
                     const uint64_t* __restrict__ s, int L, int rescale, uint64_t* __restrict__ out,
                     const ModInfo* __restrict__ mods, const ChainConsts* __restrict__ cc) {
     extern __shared__ uint64_t sm[];
-    const int i = blockIdx.x, cp = blockIdx.y;
+    const int i = C::bx(), cp = blockIdx.y;
     const int64_t c = blockIdx.z;
     const ModInfo m = mods[i];
     const uint64_t P = mods[L + 1].q;
     const uint64_t pmod = cc->qmod[L + 1][i];
     const ulonglong2 pinv = cc->qinv[L + 1][i];
-    const uint64_t* rr = r + (((size_t)c * 2 + cp) << LOGN);
-    const uint64_t* ss = s + (((size_t)c * 2 + cp) << LOGN);
-    const uint64_t* acci = acc + ((((size_t)c * 2 + cp) * (l + 2) + i) << LOGN);
+    const uint64_t* rr = r + (((size_t)c * 2 + cp) << C::LOGN);
+    const uint64_t* ss = s + (((size_t)c * 2 + cp) << C::LOGN);
+    const uint64_t* acci = acc + ((((size_t)c * 2 + cp) * (l + 2) + i) << C::LOGN);
     const int nlo = rescale ? l : l + 1;
-    uint64_t* dst = out + limb_off(c, cp, i, nlo, LOGN);
+    uint64_t* dst = out + limb_off(c, cp, i, nlo, C::LOGN);
     if (rescale) {
         const uint64_t ql = mods[l].q;
         const uint64_t qlmod = cc->qmod[l][i];
@@ -247,62 +236,41 @@ k_relin_moddown_ntt(const uint64_t* __restrict__ a, const uint64_t* __restrict__
             return addmod(u, center_mod(ss[idx], ql, qlmod, m), m.q);
         };
         auto st = [&](int idx, uint64_t x) {
-            uint64_t d = tensor_comp(a, b, c, cp, i, l + 1, LOGN, idx, m);
+            uint64_t d = tensor_comp(a, b, c, cp, i, l + 1, C::LOGN, idx, m);
             uint64_t v = addmod(d, shoup(acci[idx], pinv.x, pinv.y, m.q), m.q);
             dst[idx] = shoup(submod(v, x, m.q), qlinv.x, qlinv.y, m.q);
         };
-        ntt_fwd_block<LOGN>(sm, m, ld, st);
+        ntt_fwd<C>(sm, m, ld, st);
     } else {
         auto ld = [&](int idx) { return center_mod(rr[idx], P, pmod, m); };
         auto st = [&](int idx, uint64_t x) {
-            uint64_t d = tensor_comp(a, b, c, cp, i, l + 1, LOGN, idx, m);
+            uint64_t d = tensor_comp(a, b, c, cp, i, l + 1, C::LOGN, idx, m);
             dst[idx] = addmod(d, shoup(submod(acci[idx], x, m.q), pinv.x, pinv.y, m.q), m.q);
         };
-        ntt_fwd_block<LOGN>(sm, m, ld, st);
+        ntt_fwd<C>(sm, m, ld, st);
     }
 }
 
 // ------------------------------------------------------------------------------------
-template <int LOGN>
-static bool set_attrs_impl() {
-    const int bytes = NttShape<LOGN>::SMEM_BYTES;
-    cudaError_t e = cudaSuccess;
-#define EDL_ATTR(...) e = (e == cudaSuccess) ? cudaFuncSetAttribute(__VA_ARGS__, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) : e
-    EDL_ATTR(k_ntt_limbs<LOGN, false>);
-    EDL_ATTR(k_ntt_limbs<LOGN, true>);
-    EDL_ATTR(k_rescale_intt<LOGN>);
-    EDL_ATTR(k_rescale_ntt<LOGN>);
-    EDL_ATTR(k_relin_intt_d2<LOGN>);
-    EDL_ATTR(k_relin_ks_mac<LOGN>);
-    EDL_ATTR(k_relin_moddown_intt<LOGN>);
-    EDL_ATTR(k_relin_moddown_ntt<LOGN>);
-#undef EDL_ATTR
-    return e == cudaSuccess;
-}
-
-bool set_smem_attrs(int logn) {
-    bool ok = false;
-    EDL_DISPATCH_LOGN(logn, ok = set_attrs_impl<LOGN>());
-    return ok;
-}
+// Host launchers.  Grids are [limb-like x K, ...]: the K CTAs of one limb form a cluster.
+bool set_smem_attrs(int /*logn*/) { return true; }   // set lazily by launch_cfg
 
 void launch_ntt_limbs(const Dev& d, uint64_t* data, int64_t batch, int nl, const int* prime_idx_host, bool inverse) {
     PrimeMap pm;
     for (int j = 0; j < nl && j < MAXM; j++) pm.idx[j] = (int8_t)prime_idx_host[j];
     EDL_DISPATCH_LOGN(d.logn, {
-        using S = NttShape<LOGN, loge_plain(LOGN)>;
-        dim3 grid(nl, (unsigned)batch);
-        if (inverse) EDL_LAUNCH(d, "k_ntt_limbs", k_ntt_limbs<LOGN, true><<<grid, S::T, S::SMEM_BYTES, d.st>>>(data, nl, pm, d.mods));
-        else EDL_LAUNCH(d, "k_ntt_limbs", k_ntt_limbs<LOGN, false><<<grid, S::T, S::SMEM_BYTES, d.st>>>(data, nl, pm, d.mods));
+        using C = CfgPlain<LOGN>;
+        const dim3 grid(nl, (unsigned)batch);
+        if (inverse) launch_cfg<C>(d, "k_ntt_limbs", k_ntt_limbs<C, true>, grid, data, nl, pm, d.mods);
+        else launch_cfg<C>(d, "k_ntt_limbs", k_ntt_limbs<C, false>, grid, data, nl, pm, d.mods);
     });
 }
 
 void launch_rescale_intt(const Dev& d, const uint64_t* in, int64_t cnt, int l, const ulonglong2* w, uint64_t* r_out,
                          const ulonglong2* w2, uint64_t* r_out2) {
     EDL_DISPATCH_LOGN(d.logn, {
-        using S = NttShape<LOGN>;
-        EDL_LAUNCH(d, "k_rescale_intt", k_rescale_intt<LOGN><<<dim3(2, (unsigned)cnt), S::T, S::SMEM_BYTES, d.st>>>(
-            in, l, w, r_out, w2, r_out2, d.mods));
+        using C = CfgFused<LOGN>;
+        launch_cfg<C>(d, "k_rescale_intt", k_rescale_intt<C>, dim3(2, (unsigned)cnt), in, l, w, r_out, w2, r_out2, d.mods);
     });
 }
 
@@ -310,9 +278,9 @@ void launch_rescale_ntt(const Dev& d, const uint64_t* in, int64_t cnt, int l, co
                         const uint64_t* r, const uint64_t* bias, uint64_t* out, int lo) {
     const int nlo = (lo < 0 || lo > l - 1) ? l : lo + 1;
     EDL_DISPATCH_LOGN(d.logn, {
-        using S = NttShape<LOGN>;
-        EDL_LAUNCH(d, "k_rescale_ntt", k_rescale_ntt<LOGN><<<dim3(nlo, 2, (unsigned)cnt), S::T, S::SMEM_BYTES, d.st>>>(in, l, w, r, bias, out,
-                                                                                      nlo, d.mods, d.cc));
+        using C = CfgFused<LOGN>;
+        launch_cfg<C>(d, "k_rescale_ntt", k_rescale_ntt<C>, dim3(nlo, 2, (unsigned)cnt), in, l, w, r, bias, out, nlo, d.mods,
+                      d.cc);
     });
 }
 
@@ -326,15 +294,16 @@ void launch_relin(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t cn
     uint64_t* acc = acoef + ((size_t)cnt * (l + 1) << d.logn);
     uint64_t* r = acc + ((size_t)cnt * 2 * (l + 2) << d.logn);
     uint64_t* s = r + ((size_t)cnt * 2 << d.logn);
+    const int rs = rescale ? 1 : 0;
     EDL_DISPATCH_LOGN(d.logn, {
-        using S = NttShape<LOGN>;
-        EDL_LAUNCH(d, "k_relin_intt_d2", k_relin_intt_d2<LOGN><<<dim3(l + 1, (unsigned)cnt), S::T, S::SMEM_BYTES, d.st>>>(a, b, l, acoef, d.mods));
-        EDL_LAUNCH(d, "k_relin_ks_mac", k_relin_ks_mac<LOGN><<<dim3(l + 2, (unsigned)cnt), S::T, S::SMEM_BYTES, d.st>>>(a, b, l, acoef, rlk, rlk_s,
-                                                                                       d.L, acc, d.mods));
-        EDL_LAUNCH(d, "k_relin_moddown_intt", k_relin_moddown_intt<LOGN><<<dim3(2, (unsigned)cnt), S::T, S::SMEM_BYTES, d.st>>>(
-            a, b, l, acc, d.L, rescale ? 1 : 0, r, s, d.mods, d.cc));
-        EDL_LAUNCH(d, "k_relin_moddown_ntt", k_relin_moddown_ntt<LOGN><<<dim3(rescale ? l : l + 1, 2, (unsigned)cnt), S::T, S::SMEM_BYTES, d.st>>>(
-            a, b, l, acc, r, s, d.L, rescale ? 1 : 0, out, d.mods, d.cc));
+        using C = CfgFused<LOGN>;
+        launch_cfg<C>(d, "k_relin_intt_d2", k_relin_intt_d2<C>, dim3(l + 1, (unsigned)cnt), a, b, l, acoef, d.mods);
+        launch_cfg<C>(d, "k_relin_ks_mac", k_relin_ks_mac<C>, dim3(l + 2, (unsigned)cnt), a, b, l, (const uint64_t*)acoef, rlk,
+                      rlk_s, d.L, acc, d.mods);
+        launch_cfg<C>(d, "k_relin_moddown_intt", k_relin_moddown_intt<C>, dim3(2, (unsigned)cnt), a, b, l,
+                      (const uint64_t*)acc, d.L, rs, r, s, d.mods, d.cc);
+        launch_cfg<C>(d, "k_relin_moddown_ntt", k_relin_moddown_ntt<C>, dim3(rescale ? l : l + 1, 2, (unsigned)cnt), a, b,
+                      l, (const uint64_t*)acc, (const uint64_t*)r, (const uint64_t*)s, d.L, rs, out, d.mods, d.cc);
     });
 }
 

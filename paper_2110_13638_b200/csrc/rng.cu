@@ -64,48 +64,48 @@ __device__ uint64_t shoup_companion(uint64_t w, uint64_t q) {
 }
 
 // ---- keygen: one CTA per modulus (secret), per data limb (pk), per (digit, limb) (rlk)
-template <int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::T, 1)
+template <class C>
+__global__ void __launch_bounds__(C::T, C::MINB)
 k_keygen_s(uint64_t seed, uint64_t* __restrict__ s_hat, const ModInfo* __restrict__ mods) {
     extern __shared__ uint64_t sm[];
-    const int i = blockIdx.x;
+    const int i = C::bx();
     const ModInfo m = mods[i];
-    uint64_t* dst = s_hat + ((size_t)i << LOGN);
+    uint64_t* dst = s_hat + ((size_t)i << C::LOGN);
     auto ld = [&](int idx) { return small_mod(ternary_of(draw(seed, idx, 0, 0, TAG_S)), m.q); };
     auto st = [&](int idx, uint64_t v) { dst[idx] = v; };
-    ntt_fwd_block<LOGN>(sm, m, ld, st);
+    ntt_fwd<C>(sm, m, ld, st);
 }
 
-template <int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::T, 1)
+template <class C>
+__global__ void __launch_bounds__(C::T, C::MINB)
 k_keygen_pk(uint64_t seed, int L, const uint64_t* __restrict__ s_hat, uint64_t* __restrict__ pk,
             const ModInfo* __restrict__ mods) {
     extern __shared__ uint64_t sm[];
-    const int i = blockIdx.x;
+    const int i = C::bx();
     const ModInfo m = mods[i];
-    const uint64_t* s = s_hat + ((size_t)i << LOGN);
-    uint64_t* b = pk + ((size_t)(0 * (L + 1) + i) << LOGN);
-    uint64_t* a = pk + ((size_t)(1 * (L + 1) + i) << LOGN);
+    const uint64_t* s = s_hat + ((size_t)i << C::LOGN);
+    uint64_t* b = pk + ((size_t)(0 * (L + 1) + i) << C::LOGN);
+    uint64_t* a = pk + ((size_t)(1 * (L + 1) + i) << C::LOGN);
     auto ld = [&](int idx) { return small_mod(cbd_of(draw(seed, idx, 0, 0, TAG_PK_E)), m.q); };
     auto st = [&](int idx, uint64_t e) {
         const uint64_t av = uniform_of(draw(seed, idx, 0, i, TAG_PK_A), m);
         a[idx] = av;
         b[idx] = submod(e, mulmod(av, s[idx], m), m.q);
     };
-    ntt_fwd_block<LOGN>(sm, m, ld, st);
+    ntt_fwd<C>(sm, m, ld, st);
 }
 
-template <int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::T, 1)
+template <class C>
+__global__ void __launch_bounds__(C::T, C::MINB)
 k_keygen_rlk(uint64_t seed, int L, const uint64_t* __restrict__ s_hat, uint64_t* __restrict__ rlk,
              uint64_t* __restrict__ rlk_s, const ModInfo* __restrict__ mods, const ChainConsts* __restrict__ cc) {
     extern __shared__ uint64_t sm[];
-    const int i = blockIdx.x;   // limb 0..L+1 (L+1 = P)
+    const int i = C::bx();   // limb 0..L+1 (L+1 = P)
     const int j = blockIdx.y;   // digit 0..L
     const ModInfo m = mods[i];
-    const uint64_t* s = s_hat + ((size_t)i << LOGN);
-    const size_t ob = ((size_t)(j * 2 + 0) * (L + 2) + i) << LOGN;
-    const size_t oa = ((size_t)(j * 2 + 1) * (L + 2) + i) << LOGN;
+    const uint64_t* s = s_hat + ((size_t)i << C::LOGN);
+    const size_t ob = ((size_t)(j * 2 + 0) * (L + 2) + i) << C::LOGN;
+    const size_t oa = ((size_t)(j * 2 + 1) * (L + 2) + i) << C::LOGN;
     const uint64_t pmod = cc->qmod[L + 1][i];
     auto ld = [&](int idx) { return small_mod(cbd_of(draw(seed, idx, j, 0, TAG_RLK_E)), m.q); };
     auto st = [&](int idx, uint64_t e) {
@@ -118,35 +118,35 @@ k_keygen_rlk(uint64_t seed, int L, const uint64_t* __restrict__ s_hat, uint64_t*
         rlk_s[ob + idx] = shoup_companion(bv, m.q);
         rlk_s[oa + idx] = shoup_companion(av, m.q);
     };
-    ntt_fwd_block<LOGN>(sm, m, ld, st);
+    ntt_fwd<C>(sm, m, ld, st);
 }
 
 // ---- encrypt (O8): c0 = v*b + NTT(e0 + m), c1 = v*a + NTT(e1), per (ct, limb)
-template <int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::T, 1)
+template <class C>
+__global__ void __launch_bounds__(C::T, C::MINB)
 k_encrypt(const int64_t* __restrict__ msg, int l, int L, uint64_t seed, uint32_t obj0, const uint64_t* __restrict__ pk,
           uint64_t* __restrict__ out, const ModInfo* __restrict__ mods) {
     extern __shared__ uint64_t sm[];
-    const int i = blockIdx.x;
+    const int i = C::bx();
     const int64_t c = blockIdx.y;
     const uint32_t obj = obj0 + (uint32_t)c;
     const ModInfo m = mods[i];
-    const int64_t* mm = msg + ((size_t)c << LOGN);
-    uint64_t* c0 = out + limb_off(c, 0, i, l + 1, LOGN);
-    uint64_t* c1 = out + limb_off(c, 1, i, l + 1, LOGN);
-    const uint64_t* pb = pk + ((size_t)(0 * (L + 1) + i) << LOGN);
-    const uint64_t* pa = pk + ((size_t)(1 * (L + 1) + i) << LOGN);
+    const int64_t* mm = msg + ((size_t)c << C::LOGN);
+    uint64_t* c0 = out + limb_off(c, 0, i, l + 1, C::LOGN);
+    uint64_t* c1 = out + limb_off(c, 1, i, l + 1, C::LOGN);
+    const uint64_t* pb = pk + ((size_t)(0 * (L + 1) + i) << C::LOGN);
+    const uint64_t* pa = pk + ((size_t)(1 * (L + 1) + i) << C::LOGN);
     {
         auto ld = [&](int idx) { return small_mod(cbd_of(draw(seed, idx, obj, 0, TAG_ENC_E1)), m.q); };
         auto st = [&](int idx, uint64_t v) { c1[idx] = v; };
-        ntt_fwd_block<LOGN>(sm, m, ld, st);
+        ntt_fwd<C>(sm, m, ld, st);
     }
     {
         auto ld = [&](int idx) {
             return addmod(small_mod(cbd_of(draw(seed, idx, obj, 0, TAG_ENC_E0)), m.q), signed_mod(mm[idx], m), m.q);
         };
         auto st = [&](int idx, uint64_t v) { c0[idx] = v; };
-        ntt_fwd_block<LOGN>(sm, m, ld, st);
+        ntt_fwd<C>(sm, m, ld, st);
     }
     {
         auto ld = [&](int idx) { return small_mod(ternary_of(draw(seed, idx, obj, 0, TAG_ENC_V)), m.q); };
@@ -154,26 +154,26 @@ k_encrypt(const int64_t* __restrict__ msg, int l, int L, uint64_t seed, uint32_t
             c0[idx] = addmod(c0[idx], mulmod(v, pb[idx], m), m.q);
             c1[idx] = addmod(c1[idx], mulmod(v, pa[idx], m), m.q);
         };
-        ntt_fwd_block<LOGN>(sm, m, ld, st);
+        ntt_fwd<C>(sm, m, ld, st);
     }
 }
 
 // ---- decrypt, device half: out[c][i] = INTT(c0 + c1 s)
-template <int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::T, 1)
+template <class C>
+__global__ void __launch_bounds__(C::T, C::MINB)
 k_decrypt(const uint64_t* __restrict__ ct, int l, const uint64_t* __restrict__ s_hat, uint64_t* __restrict__ out,
           const ModInfo* __restrict__ mods) {
     extern __shared__ uint64_t sm[];
-    const int i = blockIdx.x;
+    const int i = C::bx();
     const int64_t c = blockIdx.y;
     const ModInfo m = mods[i];
-    const uint64_t* c0 = ct + limb_off(c, 0, i, l + 1, LOGN);
-    const uint64_t* c1 = ct + limb_off(c, 1, i, l + 1, LOGN);
-    const uint64_t* s = s_hat + ((size_t)i << LOGN);
-    uint64_t* dst = out + (((size_t)c * (l + 1) + i) << LOGN);
+    const uint64_t* c0 = ct + limb_off(c, 0, i, l + 1, C::LOGN);
+    const uint64_t* c1 = ct + limb_off(c, 1, i, l + 1, C::LOGN);
+    const uint64_t* s = s_hat + ((size_t)i << C::LOGN);
+    uint64_t* dst = out + (((size_t)c * (l + 1) + i) << C::LOGN);
     auto ld = [&](int idx) { return addmod(c0[idx], mulmod(c1[idx], s[idx], m), m.q); };
     auto st = [&](int idx, uint64_t v) { dst[idx] = v; };
-    ntt_inv_block<LOGN>(sm, m, ld, st);
+    ntt_inv<C>(sm, m, ld, st);
 }
 
 __global__ void k_philox_words(uint64_t seed, const uint32_t* __restrict__ ctr, int64_t n, uint32_t* __restrict__ out) {
@@ -186,56 +186,29 @@ __global__ void k_philox_words(uint64_t seed, const uint32_t* __restrict__ ctr, 
     out[4 * t + 3] = r.w;
 }
 
-#define EDL_DISPATCH_LOGN(logn, ...)                   \
-    switch (logn) {                                     \
-        case 10: { constexpr int LOGN = 10; __VA_ARGS__; } break; \
-        case 11: { constexpr int LOGN = 11; __VA_ARGS__; } break; \
-        case 12: { constexpr int LOGN = 12; __VA_ARGS__; } break; \
-        case 13: { constexpr int LOGN = 13; __VA_ARGS__; } break; \
-        case 14: { constexpr int LOGN = 14; __VA_ARGS__; } break; \
-        default: break;                                 \
-    }
-
-template <int LOGN>
-static void rng_attrs() {
-    static bool done = false;
-    if (done) return;
-    const int bytes = NttShape<LOGN>::SMEM_BYTES;
-    cudaFuncSetAttribute(k_keygen_s<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    cudaFuncSetAttribute(k_keygen_pk<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    cudaFuncSetAttribute(k_keygen_rlk<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    cudaFuncSetAttribute(k_encrypt<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    cudaFuncSetAttribute(k_decrypt<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    done = true;
-}
-
 void launch_keygen(const Dev& d, uint64_t seed, uint64_t* s_hat, uint64_t* pk, uint64_t* rlk, uint64_t* rlk_s,
                    uint64_t* /*scratch*/) {
     EDL_DISPATCH_LOGN(d.logn, {
-        using S = NttShape<LOGN>;
-        rng_attrs<LOGN>();
-        EDL_LAUNCH(d, "k_keygen_s", k_keygen_s<LOGN><<<d.L + 2, S::T, S::SMEM_BYTES, d.st>>>(seed, s_hat, d.mods));
-        EDL_LAUNCH(d, "k_keygen_pk", k_keygen_pk<LOGN><<<d.L + 1, S::T, S::SMEM_BYTES, d.st>>>(seed, d.L, s_hat, pk, d.mods));
-        EDL_LAUNCH(d, "k_keygen_rlk", k_keygen_rlk<LOGN><<<dim3(d.L + 2, d.L + 1), S::T, S::SMEM_BYTES, d.st>>>(seed, d.L, s_hat, rlk, rlk_s, d.mods,
-                                                                                  d.cc));
+        using C = CfgFused<LOGN>;
+        launch_cfg<C>(d, "k_keygen_s", k_keygen_s<C>, dim3(d.L + 2), seed, s_hat, d.mods);
+        launch_cfg<C>(d, "k_keygen_pk", k_keygen_pk<C>, dim3(d.L + 1), seed, d.L, (const uint64_t*)s_hat, pk, d.mods);
+        launch_cfg<C>(d, "k_keygen_rlk", k_keygen_rlk<C>, dim3(d.L + 2, d.L + 1), seed, d.L, (const uint64_t*)s_hat, rlk,
+                      rlk_s, d.mods, d.cc);
     });
 }
 
 void launch_encrypt(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint64_t seed, uint32_t obj0,
                     const uint64_t* pk, uint64_t* out) {
     EDL_DISPATCH_LOGN(d.logn, {
-        using S = NttShape<LOGN>;
-        rng_attrs<LOGN>();
-        EDL_LAUNCH(d, "k_encrypt", k_encrypt<LOGN><<<dim3(l + 1, (unsigned)cnt), S::T, S::SMEM_BYTES, d.st>>>(msg, l, d.L, seed, obj0, pk, out,
-                                                                                   d.mods));
+        using C = CfgFused<LOGN>;
+        launch_cfg<C>(d, "k_encrypt", k_encrypt<C>, dim3(l + 1, (unsigned)cnt), msg, l, d.L, seed, obj0, pk, out, d.mods);
     });
 }
 
 void launch_decrypt(const Dev& d, const uint64_t* ct, int64_t cnt, int l, const uint64_t* s_hat, uint64_t* out) {
     EDL_DISPATCH_LOGN(d.logn, {
-        using S = NttShape<LOGN>;
-        rng_attrs<LOGN>();
-        EDL_LAUNCH(d, "k_decrypt", k_decrypt<LOGN><<<dim3(l + 1, (unsigned)cnt), S::T, S::SMEM_BYTES, d.st>>>(ct, l, s_hat, out, d.mods));
+        using C = CfgFused<LOGN>;
+        launch_cfg<C>(d, "k_decrypt", k_decrypt<C>, dim3(l + 1, (unsigned)cnt), ct, l, s_hat, out, d.mods);
     });
 }
 

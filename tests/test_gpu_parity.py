@@ -55,7 +55,7 @@ def _to_gpu(g, data, lvl, scale, key):
 
 
 # ---------------------------------------------------------------- NTT
-@pytest.mark.parametrize("logn", [10, 11, 12, 13, 14])
+@pytest.mark.parametrize("logn", [10, 11, 12, 13, 14, 15, 16])
 def test_ntt_bit_exact(edl, logn):
     bits = [60, 40, 40, 60] if logn < 14 else [60, 40, 40, 40, 40, 60]
     pp = edl.params_from_bits(logn, bits)
@@ -179,6 +179,31 @@ def test_mul_relin_bit_exact(c1pair, lvl):
     want = o.mul_relin(A, B)
     assert got.scale == want.scale
     assert np.array_equal(got.numpy(g.n), want.data)
+
+
+@pytest.mark.parametrize("logn", [15, 16])
+def test_large_n_keys_relin_rescale(edl, logn):
+    """C2's large rings (one limb per thread-block cluster of N/2^13 CTAs): keygen, encryption,
+    tensor + key-switch (with and without the fused rescale) and rescale, bit-exact."""
+    bits = [60, 40, 40, 60]
+    g, o = _pair(edl, logn=logn, bits=bits, seed=5)
+    assert np.array_equal(g.export_key(0), o.s_hat)
+    assert np.array_equal(g.export_key(1), o.pk)
+    assert np.array_equal(g.export_key(2), o.rlk)
+    polys = np.random.default_rng(logn).integers(-2 ** 30, 2 ** 30, (2, 1 << logn))
+    xg = g.encrypt_poly(polys, scale=2.0 ** 40, enc_seed=7)
+    xo = o.encrypt_poly(polys, enc_seed=7, obj0=0, scale=2.0 ** 40)
+    assert np.array_equal(xg.numpy(g.n), xo.data)
+    lvl = 2
+    A = ock.CtArray(_rand_ct(o, 2, lvl, 51), lvl, 2.0 ** 40, o.key_id)
+    B = ock.CtArray(_rand_ct(o, 2, lvl, 52), lvl, 2.0 ** 40, o.key_id)
+    ga, gb = _to_gpu(g, A.data, lvl, A.scale, o.key_id), _to_gpu(g, B.data, lvl, B.scale, o.key_id)
+    m_g, m_o = g.mul_relin(ga, gb), o.mul_relin(A, B)
+    assert np.array_equal(m_g.numpy(g.n), m_o.data)
+    assert np.array_equal(g.rescale(m_g).numpy(g.n), o.rescale(m_o).data)
+    sq_g = g.poly_activation(ga, (0.0, 0.0, 1.0))
+    sq_o = olay.poly_activation(o, A, (0.0, 0.0, 1.0))
+    assert np.array_equal(sq_g.numpy(g.n), sq_o.data)
 
 
 def test_mul_relin_mixed_levels(c0pair):
