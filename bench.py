@@ -176,11 +176,19 @@ def run_ours(a):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # EDL_BENCH_EMULATE=1 (functional check of the N>1 path on a one-GPU box, never a
+    # timing): every rank on cuda:0, gloo all-reduce through the host
+    emulate = os.environ.get("EDL_BENCH_EMULATE") == "1"
+    if emulate:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if emulate:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    from paper_2110_13638_b200 import edl
+    from paper_2110_13638_b200 import edl, parallel
     from paper_2110_13638_b200.networks import C1Net
     from synth import c1_images, c1_slots, c1_weights
 
@@ -188,18 +196,44 @@ def run_ours(a):
     torch.cuda.set_stream(stream)
     ctx = edl.Context(edl.params_from_depth(4), device=local, stream=stream).keygen(1)
     K, kb, W, b = c1_weights()
-    imgs = c1_images(BATCH, 2110 + rank)           # each rank: its own batch (weak scaling)
-    polys = torch.from_numpy(ctx.encode(c1_slots(imgs))).to(f"cuda:{local}")
-    x = ctx.encrypt_poly(polys, scale=float(2 ** 40), enc_seed=2, obj0=0)
-    del polys
-    net = C1Net(ctx, K, kb, W, b)
+    if world == 1:
+        # C1: one 8192-image batch, the paper's graph engine firing CC -> sigma_a -> dense
+        imgs = c1_images(BATCH, 2110)
+        polys = torch.from_numpy(ctx.encode(c1_slots(imgs))).to(f"cuda:{local}")
+        x = ctx.encrypt_poly(polys, scale=float(2 ** 40), enc_seed=2, obj0=0)
+        del polys
+        net = C1Net(ctx, K, kb, W, b)
+
+        def step(inp):
+            return net.forward(inp)["out"]
+    else:
+        # C4 (configs[4]) at weak scale: `world` batches of 8192 images, their 49*world
+        # (window, batch) units split over the ranks (49 each), dense partials combined by
+        # one NCCL uint64 all-reduce, each rank finishing one batch
+        sh = parallel.ShardedCNN(ctx, K, kb, W, b, world, rank, world)
+        full = []
+        for bi in range(world):
+            polys = torch.from_numpy(ctx.encode(c1_slots(c1_images(BATCH, 2110 + bi)))).to(f"cuda:{local}")
+            full.append(ctx.encrypt_poly(polys, scale=float(2 ** 40), enc_seed=2, obj0=0))
+            del polys
+        x = parallel.rank_inputs(ctx, sh, full)
+        del full
+        torch.cuda.empty_cache()
+        partials = torch.empty(sh.partials_words(), dtype=torch.int64, device=f"cuda:{local}")
+
+        def all_reduce(t):
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)   # int64 two's-complement sum == uint64 sum
+
+        def step(inp):
+            outs = sh.step(inp, partials, all_reduce)
+            return outs[rank]
 
     def barrier():
         if world > 1:
             dist.barrier()
 
     for _ in range(max(a.warmup, 0)):
-        net.forward(x)
+        step(x)
     stream.synchronize()
     barrier()
 
@@ -212,7 +246,7 @@ def run_ours(a):
     barrier()
     e0.record(stream)
     for _ in range(a.steps):
-        out = net.forward(x)["out"]
+        out = step(x)
     e1.record(stream)
     stream.synchronize()
     barrier()
@@ -238,14 +272,14 @@ def run_ours(a):
         host_out = torch.empty(out_words, dtype=torch.int64, pin_memory=True)
         for _ in range(1):
             dev_in.tensor.copy_(host_in, non_blocking=True)
-            host_out.copy_(net.forward(dev_in)["out"].tensor, non_blocking=True)
+            host_out.copy_(step(dev_in).tensor, non_blocking=True)
         stream.synchronize()
         barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         for _ in range(a.e2e_steps):
             dev_in.tensor.copy_(host_in, non_blocking=True)
-            host_out.copy_(net.forward(dev_in)["out"].tensor, non_blocking=True)
+            host_out.copy_(step(dev_in).tensor, non_blocking=True)
         f1.record(stream)
         stream.synchronize()
         barrier()
@@ -285,10 +319,16 @@ def run_ours(a):
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
                 "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-                "config": {"workload": "C1 Fashion-MNIST-shaped encrypted CNN, CKKS N=2^14 {60,40,40,40,40|60}, "
-                                       "batch 8192 in slots (784 pixel ciphertexts), CC 5x4x4/4 -> sigma_a -> "
-                                       "dense 245->10", "global_batch": BATCH * world,
-                           "parallelism": f"batch-replica x{world}", "l2": "inputs 1.03 GB > L2 (no flush)"},
+                "config": {"workload": ("C1 Fashion-MNIST-shaped encrypted CNN, CKKS N=2^14 {60,40,40,40,40|60}, "
+                                        "batch 8192 in slots (784 pixel ciphertexts), CC 5x4x4/4 -> sigma_a -> "
+                                        "dense 245->10") if world == 1 else
+                                       (f"C4 scale-out CNN: {world} batches of 8192 synthetic images (C1 "
+                                        f"architecture and parameters), 49*{world} (window, batch) units over "
+                                        f"{world} GPUs"), "global_batch": BATCH * world,
+                           "parallelism": ("single GPU" if world == 1 else
+                                           f"C4 (window, batch) units sharded x{world}, NCCL uint64 all-reduce of "
+                                           f"dense partials"),
+                           "l2": "inputs 1.03 GB per GPU > L2 (no flush)"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk, "dominant_kernel": dom[0], "kernels": kernels}
         print(json.dumps(line), flush=True)

@@ -74,3 +74,35 @@ def test_c3_full_bit_exact(gpu):
     ref = onet.c3_float64(inp.X, inp.W1, inp.b1, inp.W2, inp.b2)[:, 0]
     assert np.max(np.abs(pred - ref)) < 1e-3
     assert float(np.mean((pred - ref) ** 2)) < 1e-8
+
+
+@pytest.mark.timeout(900)
+def test_c4_sharded_one_gpu_emulation(gpu):
+    """C4 on one GPU: R = 2 ranks' partials computed one after the other through the
+    per-rank driver (parallel.ShardedCNN), summed as uint64 (the NCCL all-reduce's
+    arithmetic), then mod q + rescale + bias: every output residue equals the unsharded
+    C1 network's, for B = 2 batches."""
+    from paper_2110_13638_b200 import parallel
+    from paper_2110_13638_b200.networks import C1Net
+    from synth import c1_images, c1_slots, c1_weights
+
+    ctx = gpu.Context(gpu.params_from_depth(4)).keygen(1)
+    K, kb, W, b = c1_weights()
+    B, R = 2, 2
+    full = []
+    for bi in range(B):
+        polys = ctx.encode(c1_slots(c1_images(8192, 2110 + bi)))
+        full.append(ctx.encrypt_poly(polys, scale=2.0 ** 40, enc_seed=2))
+    want = [C1Net(ctx, K, kb, W, b).forward(full[bi])["out"].numpy(ctx.n) for bi in range(B)]
+    total = None
+    for r in range(R):
+        sh = parallel.ShardedCNN(ctx, K, kb, W, b, R, r, B)
+        assert sh.units in (49 * B // R, 49 * B // R + 1)
+        x = parallel.rank_inputs(ctx, sh, full)
+        part = torch.empty(sh.partials_words(), dtype=torch.int64, device="cuda")
+        lvl, sc = sh.partials(x, part)
+        total = part if total is None else total + part          # int64 wrap == uint64 sum
+    sh0 = parallel.ShardedCNN(ctx, K, kb, W, b, R, 0, B)
+    outs = sh0.finish(total, lvl, sc, batches=range(B))
+    for bi in range(B):
+        assert np.array_equal(outs[bi].numpy(ctx.n), want[bi]), bi
