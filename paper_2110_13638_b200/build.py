@@ -13,8 +13,14 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
-def sources():
-    return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
+def sources(logns=None):
+    """All .cu/.cpp sources; `logns` (development builds) keeps only those ring degrees'
+    ntt_inst_<logN>.cu instantiation units."""
+    out = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
+    if logns:
+        keep = {f"ntt_inst_{k}.cu" for k in logns}
+        out = [p for p in out if not os.path.basename(p).startswith("ntt_inst_") or os.path.basename(p) in keep]
+    return out
 
 
 def deps():
@@ -29,16 +35,23 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False, defines=(), out: str = None) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = None, logns=None) -> str:
     lib = out or LIB
+    if logns:
+        assert out is not None, "a trimmed build must not replace the product library"
+        defines = tuple(defines) + (f"EDL_LOGNS_MASK={sum(1 << k for k in logns)}",)
     if not force and not defines and out is None and up_to_date():
         return LIB
     objdir = os.path.join(HERE, "build" + ("_" + "_".join(d.replace("=", "") for d in defines) if defines else ""))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
-    for src in sources():
+    hdr_time = max(os.path.getmtime(p) for p in deps() if not p.endswith((".cu", ".cpp")))
+    for src in sources(logns):
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(hdr_time, os.path.getmtime(src)):
+            objs.append(obj)    # incremental: object newer than its source and every header
+            continue
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",
                "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3",
                *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
@@ -61,4 +74,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
 if __name__ == "__main__":
     defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
     outs = [a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--out=")]
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs, out=outs[0] if outs else None))
+    ln = [a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--logns=")]
+    logns = [int(x) for x in ln[0].split(",")] if ln else None
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs, out=outs[0] if outs else None,
+                logns=logns))

@@ -181,9 +181,20 @@ std::vector<ulonglong2> shoup_consts(const edl_ctx* c, const std::vector<int64_t
         for (int i = 0; i <= l; i++) {
             const uint64_t q = c->prm.q[i];
             const uint64_t r = signed_mod(ints[k], q);
-            w[k * (l + 1) + i] = make_ulonglong2(r, host::shoup_companion(r, q));
+            w[k * (l + 1) + i] = make_ulonglong2(r, host::mul_companion(r, q));
         }
     return w;
+}
+
+// Constants with their mulc() companions -> [count][nl] {residue, companion}
+std::vector<ulonglong2> residue_pairs(const edl_ctx* c, const std::vector<int64_t>& ints, int nl) {
+    std::vector<ulonglong2> r(ints.size() * nl);
+    for (size_t k = 0; k < ints.size(); k++)
+        for (int i = 0; i < nl; i++) {
+            const uint64_t v = signed_mod(ints[k], c->prm.q[i]);
+            r[k * nl + i] = make_ulonglong2(v, host::mul_companion(v, c->prm.q[i]));
+        }
+    return r;
 }
 
 std::vector<uint64_t> residues(const edl_ctx* c, const std::vector<int64_t>& ints, int nl) {
@@ -269,12 +280,14 @@ edl_status edl_ctx_create(const edl_params* p, int32_t device, void* stream, edl
         m.two64 = (uint64_t)((((host::u128)1) << 64) % q);
         m.two64_s = host::shoup_companion(m.two64, q);
         m.one_s = host::shoup_companion(1, q);   // floor(2^64 / q)
+        m.fp = host::fp_quotient_prime(q) ? 1 : 0;
         m.tw_fwd = reinterpret_cast<const ulonglong2*>(dfwd);
         m.tw_inv = reinterpret_cast<const ulonglong2*>(dinv);
         m.ninv = host::invmod((uint64_t)c->N % q, q);
-        m.ninv_s = host::shoup_companion(m.ninv, q);
+        m.ninv_s = host::mul_companion(m.ninv, q);
         m.w1ninv = host::mulmod(ti[2 * 1], m.ninv, q);
-        m.w1ninv_s = host::shoup_companion(m.w1ninv, q);
+        m.w1ninv_s = host::mul_companion(m.w1ninv, q);
+        m.qinv_d = 1.0 / (double)q;
         c->h_mods[k] = m;
     }
     c->h_cc = new ChainConsts();
@@ -286,7 +299,7 @@ edl_status edl_ctx_create(const edl_params* p, int32_t device, void* stream, edl
             c->h_cc->qmod[a][b] = qa % qb;
             if (a != b) {
                 const uint64_t inv = host::invmod(qa % qb, qb);
-                c->h_cc->qinv[a][b] = make_ulonglong2(inv, host::shoup_companion(inv, qb));
+                c->h_cc->qinv[a][b] = make_ulonglong2(inv, host::mul_companion(inv, qb));
             }
         }
     cudaMalloc(&c->d_mods, nm * sizeof(ModInfo));
@@ -591,7 +604,7 @@ edl_status edl_cross_correlate(edl_ctx* c, const edl_cts* x, int32_t H, int32_t 
     uint64_t* acc = scratch(c, ct_words(c, cnt, l) + (size_t)cnt * 2 * c->N);
     if (!acc) return fail(c, EDL_ERR_CUDA, "cross_correlate: scratch");
     uint64_t* r = acc + ct_words(c, cnt, l);
-    const uint64_t* dw = upload(c, residues(c, wi, l + 1));
+    const ulonglong2* dw = upload(c, residue_pairs(c, wi, l + 1));
     const uint64_t* db = nullptr;
     if (bias) {
         std::vector<int64_t> bi(cnt);
@@ -619,7 +632,7 @@ edl_status edl_dense(edl_ctx* c, const edl_cts* x, const double* Wt, const doubl
     const double pt_scale = (double)c->prm.q[l];
     std::vector<int64_t> wi((size_t)O * K);
     for (size_t t = 0; t < wi.size(); t++) wi[t] = const_int(Wt[t], pt_scale);
-    const uint64_t* dw = upload(c, residues(c, wi, l + 1));
+    const ulonglong2* dw = upload(c, residue_pairs(c, wi, l + 1));
     if (!dw) return fail(c, EDL_ERR_ARG, "dense: weight table too large");
     Dev d = c->dev();
     const size_t part_words = (size_t)dense_split(d, K, O, l) * ct_words(c, O, l);

@@ -2,6 +2,9 @@
 // arithmetic (encode, scale bookkeeping) rounds exactly as written.
 #include "host_math.h"
 
+#include <cfenv>
+#include <cstring>
+
 #include <cmath>
 #include <set>
 
@@ -109,15 +112,34 @@ static uint32_t bitrev(uint32_t x, int bits) {
     return r;
 }
 
+// floor-ish w/q as a binary64 rounded toward -infinity (w, q < 2^53 are exact doubles and
+// IEEE division is correctly rounded in the current mode).
+static uint64_t quotient_rd_bits(uint64_t w, uint64_t q) {
+    const int old = std::fegetround();
+    std::fesetround(FE_DOWNWARD);
+    volatile double a = (double)w, b = (double)q;
+    volatile double r = a / b;
+    std::fesetround(old);
+    uint64_t bits;
+    double rr = r;
+    std::memcpy(&bits, &rr, 8);
+    return bits;
+}
+
+bool fp_quotient_prime(uint64_t q) { return q < (1ull << 50); }
+
+uint64_t mul_companion(uint64_t w, uint64_t q) { return fp_quotient_prime(q) ? quotient_rd_bits(w, q) : shoup_companion(w, q); }
+
 void twiddle_table(uint64_t q, uint64_t psi, int logn, bool inverse, std::vector<uint64_t>& out2) {
     const uint64_t n = 1ull << logn;
     const uint64_t base = inverse ? invmod(psi, q) : psi;
+    const bool fp = fp_quotient_prime(q);
     out2.assign(2 * n, 0);
     uint64_t p = 1;
     for (uint64_t k = 0; k < n; k++) {
         const uint32_t r = bitrev((uint32_t)k, logn);
         out2[2 * r] = p;
-        out2[2 * r + 1] = shoup_companion(p, q);
+        out2[2 * r + 1] = fp ? quotient_rd_bits(p, q) : shoup_companion(p, q);
         p = mulmod(p, base, q);
     }
 }

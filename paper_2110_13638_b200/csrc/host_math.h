@@ -23,7 +23,12 @@ uint64_t minimal_psi(uint64_t q, int logn);
 void parameterise(int c, int s, double p, std::vector<int>& bits, int& logn);
 
 // psi^{brv(k)} (or psi^{-brv(k)}) table with Shoup companions, interleaved {w, w'}
+// [N] pairs {psi^(+-brv(k)), companion}: the Shoup companion floor(w 2^64/q), or for
+// fp_quotient_prime(q) the bits of RD(w/q) (binary64) used by the FP64-quotient butterfly.
 void twiddle_table(uint64_t q, uint64_t psi, int logn, bool inverse, std::vector<uint64_t>& out2);
+bool fp_quotient_prime(uint64_t q);
+// companion of a constant w for the device's mulc(): RD(w/q) bits or floor(w 2^64/q)
+uint64_t mul_companion(uint64_t w, uint64_t q);
 
 // O5 encode: slots z[n_slots] -> m[N] = rint(scale * u_k)
 void encode(const double* z, int64_t n_slots, int logn, double scale, int64_t* m_out);

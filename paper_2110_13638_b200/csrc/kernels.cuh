@@ -50,16 +50,22 @@ struct Dev {
 };
 
 // Supported ring degrees: 2^10 .. 2^16 (N > 2^13 runs one limb per thread-block cluster).
-#define EDL_DISPATCH_LOGN(logn, ...)                               \
-    switch (logn) {                                                 \
-        case 10: { constexpr int LOGN = 10; __VA_ARGS__; } break;   \
-        case 11: { constexpr int LOGN = 11; __VA_ARGS__; } break;   \
-        case 12: { constexpr int LOGN = 12; __VA_ARGS__; } break;   \
-        case 13: { constexpr int LOGN = 13; __VA_ARGS__; } break;   \
-        case 14: { constexpr int LOGN = 14; __VA_ARGS__; } break;   \
-        case 15: { constexpr int LOGN = 15; __VA_ARGS__; } break;   \
-        case 16: { constexpr int LOGN = 16; __VA_ARGS__; } break;   \
-        default: break;                                             \
+// EDL_LOGNS_MASK (bit k = 2^k supported) trims development builds; default: all.
+#ifndef EDL_LOGNS_MASK
+#define EDL_LOGNS_MASK 0x1FC00
+#endif
+#define EDL_LOGN_CASE(K, ...) \
+    case K: { constexpr int LOGN = K; if constexpr (((EDL_LOGNS_MASK) >> K) & 1) { __VA_ARGS__; } } break;
+#define EDL_DISPATCH_LOGN(logn, ...)        \
+    switch (logn) {                          \
+        EDL_LOGN_CASE(10, __VA_ARGS__)       \
+        EDL_LOGN_CASE(11, __VA_ARGS__)       \
+        EDL_LOGN_CASE(12, __VA_ARGS__)       \
+        EDL_LOGN_CASE(13, __VA_ARGS__)       \
+        EDL_LOGN_CASE(14, __VA_ARGS__)       \
+        EDL_LOGN_CASE(15, __VA_ARGS__)       \
+        EDL_LOGN_CASE(16, __VA_ARGS__)       \
+        default: break;                      \
     }
 
 void ensure_smem_attr(const void* kern, int bytes);
@@ -95,6 +101,35 @@ void launch_cfg(const Dev& d, const char* name, void (*kern)(KArgs...), dim3 gri
         (d).prof->end((d).st);                            \
     } while (0)
 
+// ---- per-degree launchers (defined in ntt_kernels.cuh / rng_kernels.cuh, instantiated in
+// ntt_inst_<logN>.cu) ----
+struct PrimeMap {
+    int8_t idx[MAXM];
+};
+template <int LOGN>
+void launch_ntt_limbs_n(const Dev& d, uint64_t* data, int64_t batch, int nl, const PrimeMap& pm, bool inverse);
+template <int LOGN>
+void launch_rescale_intt_n(const Dev& d, const uint64_t* in, int64_t cnt, int l, const ulonglong2* w, uint64_t* r_out,
+                           const ulonglong2* w2, uint64_t* r_out2);
+template <int LOGN>
+void launch_rescale_ntt_n(const Dev& d, const uint64_t* in, int64_t cnt, int l, const ulonglong2* w, const uint64_t* r,
+                          const uint64_t* bias, uint64_t* out, int nlo);
+template <int LOGN>
+void launch_relin_n(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t cnt, int l, bool rescale,
+                    const uint64_t* rlk, const uint64_t* rlk_c, uint64_t* acoef, uint64_t* xh, uint64_t* acc, uint64_t* r,
+                    uint64_t* s, uint64_t* out);
+// key inner product of the relinearisation (pointwise.cu): acc [cnt][2][l+2][N] from the
+// raised digits xh [cnt][l+1][l+2][N], the tensor's d2 (a1 b1) and rlk [L+1][2][L+2][N]
+void launch_relin_mac(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t cnt, int l, const uint64_t* xh,
+                      const uint64_t* rlk, const uint64_t* rlk_c, uint64_t* acc);
+template <int LOGN>
+void launch_keygen_n(const Dev& d, uint64_t seed, uint64_t* s_hat, uint64_t* pk, uint64_t* rlk, uint64_t* rlk_s);
+template <int LOGN>
+void launch_encrypt_n(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint64_t seed, uint32_t obj0,
+                      const uint64_t* pk, uint64_t* out);
+template <int LOGN>
+void launch_decrypt_n(const Dev& d, const uint64_t* ct, int64_t cnt, int l, const uint64_t* s_hat, uint64_t* out);
+
 // ---- NTT family (ntt_kernels.cu) ----
 void launch_ntt_limbs(const Dev& d, uint64_t* data, int64_t batch, int nl, const int* prime_idx_host, bool inverse);
 // rescale: r_out [cnt][2][N] <- INTT_{q_l}(in[.][.][l] * w_l) ; w may be null
@@ -125,10 +160,10 @@ void launch_add_add_const(const Dev& d, const uint64_t* v, const uint64_t* w, in
                           const uint64_t* k, uint64_t* out);
 // cross-correlation MAC: out[f*Ho*Wo + r*Wo + c] = sum_{u,v} x[(r*st+u)*W + c*st+v] * wk[f][u*kw+v][i]
 void launch_cc_mac(const Dev& d, const uint64_t* x, int l, int H, int W, int F, int kh, int kw, int stride,
-                   const uint64_t* wk /*[F][kh*kw][l+1]*/, uint64_t* out);
+                   const ulonglong2* wk /*[F][kh*kw][l+1] {residue, companion}*/, uint64_t* out);
 // dense MAC: out[o] = sum_k x[k] * wd[o][k][i]  (x: K cts, out: O cts, level l)
 // part: scratch for split-K partial sums (dense_split(...) * O * 2 * (l+1) * N words) or null
-void launch_dense_mac(const Dev& d, const uint64_t* x, int64_t K, int64_t O, int l, const uint64_t* wd, uint64_t* out,
+void launch_dense_mac(const Dev& d, const uint64_t* x, int64_t K, int64_t O, int l, const ulonglong2* wd, uint64_t* out,
                       uint64_t* part = nullptr);
 int dense_split(const Dev& d, int64_t K, int64_t O, int l);
 

@@ -68,24 +68,26 @@ __device__ __forceinline__ uint64_t* cluster_smem(uint64_t* sm, int rank) {
 }
 
 // ---- forward CT butterfly (Harvey): X, Y in [0,4q) -> [0,4q)
+template <bool FP>
 __device__ __forceinline__ void ct_bfly(uint64_t& X, uint64_t& Y, ulonglong2 w, uint64_t q, uint64_t two_q) {
     uint64_t x = csub(X, two_q);
-    uint64_t t = shoup_lazy2(Y, w.x, w.y, q);
+    uint64_t t = tw_mul<FP>(Y, w.x, w.y, q);
     X = x + t;
     Y = x - t + two_q;
 }
 
 // ---- inverse GS butterfly (Harvey): X, Y in [0,2q) -> [0,2q)
+template <bool FP>
 __device__ __forceinline__ void gs_bfly(uint64_t& X, uint64_t& Y, uint64_t w, uint64_t ws, uint64_t q, uint64_t two_q) {
     uint64_t x = X, y = Y;
     X = csub(x + y, two_q);
-    Y = shoup_lazy2(x - y + two_q, w, ws, q);
+    Y = tw_mul<FP>(x - y + two_q, w, ws, q);
 }
 
 // NS forward stages on a group x[0..2^NS) held in registers; absolute stage SA + k uses
 // twiddle index 2^(SA+k) + (high << k) + (r >> (NS-k)), `high` = the group's index bits
 // above the stage window (SURVEY O3 stage twiddle psi^brv(m+i)).
-template <int SA, int NS>
+template <int SA, int NS, bool FP>
 __device__ __forceinline__ void fwd_pass_regs(uint64_t* x, int high, const ulonglong2* __restrict__ tw, uint64_t q,
                                               uint64_t two_q) {
 #pragma unroll
@@ -96,14 +98,14 @@ __device__ __forceinline__ void fwd_pass_regs(uint64_t* x, int high, const ulong
             if (r & half) continue;
             const int tidx = (1 << (SA + k)) + (high << k) + (r >> (NS - k));
             ulonglong2 w = __ldg(tw + tidx);
-            ct_bfly(x[r], x[r + half], w, q, two_q);
+            ct_bfly<FP>(x[r], x[r + half], w, q, two_q);
         }
     }
 }
 
 // NS inverse stages, last to first; with LAST the absolute stage 0 folds N^-1 into both
 // outputs (psi^-brv(1) N^-1 for the odd one).
-template <int SA, int NS, bool LAST>
+template <int SA, int NS, bool LAST, bool FP>
 __device__ __forceinline__ void inv_pass_regs(uint64_t* x, int high, const ModInfo& m, uint64_t two_q) {
 #pragma unroll
     for (int k = NS - 1; k >= 0; k--) {
@@ -113,12 +115,12 @@ __device__ __forceinline__ void inv_pass_regs(uint64_t* x, int high, const ModIn
             if (r & half) continue;
             if (LAST && SA + k == 0) {
                 uint64_t a = x[r], b = x[r + half];
-                x[r] = shoup_lazy2(a + b, m.ninv, m.ninv_s, m.q);
-                x[r + half] = shoup_lazy2(a - b + two_q, m.w1ninv, m.w1ninv_s, m.q);
+                x[r] = tw_mul<FP>(a + b, m.ninv, m.ninv_s, m.q);
+                x[r + half] = tw_mul<FP>(a - b + two_q, m.w1ninv, m.w1ninv_s, m.q);
             } else {
                 const int tidx = (1 << (SA + k)) + (high << k) + (r >> (NS - k));
                 ulonglong2 w = __ldg(m.tw_inv + tidx);
-                gs_bfly(x[r], x[r + half], w.x, w.y, m.q, two_q);
+                gs_bfly<FP>(x[r], x[r + half], w.x, w.y, m.q, two_q);
             }
         }
     }
@@ -135,7 +137,7 @@ struct PassInfo {
     static constexpr int G = C::E >> NS;              // groups per thread
 };
 
-template <class C, int P, bool INV>
+template <class C, int P, bool INV, bool FP>
 __device__ __forceinline__ void pass_smem(uint64_t* sm, const ModInfo& m, uint64_t two_q) {
     using PI = PassInfo<C, P>;
     uint64_t x[C::E];
@@ -154,8 +156,8 @@ __device__ __forceinline__ void pass_smem(uint64_t* sm, const ModInfo& m, uint64
     for (int g = 0; g < PI::G; g++) {
         const int v = threadIdx.x + g * C::T;
         const int high = hc | (v >> PI::BLOW);
-        if constexpr (INV) inv_pass_regs<PI::SA, PI::NS, false>(x + g * (1 << PI::NS), high, m, two_q);
-        else fwd_pass_regs<PI::SA, PI::NS>(x + g * (1 << PI::NS), high, m.tw_fwd, m.q, two_q);
+        if constexpr (INV) inv_pass_regs<PI::SA, PI::NS, false, FP>(x + g * (1 << PI::NS), high, m, two_q);
+        else fwd_pass_regs<PI::SA, PI::NS, FP>(x + g * (1 << PI::NS), high, m.tw_fwd, m.q, two_q);
     }
 #pragma unroll
     for (int g = 0; g < PI::G; g++) {
@@ -169,26 +171,26 @@ __device__ __forceinline__ void pass_smem(uint64_t* sm, const ModInfo& m, uint64
     __syncthreads();
 }
 
-template <class C, int P>
+template <class C, int P, bool FP>
 __device__ __forceinline__ void fwd_middle(uint64_t* sm, const ModInfo& m, uint64_t two_q) {
     if constexpr (P < C::NPASS) {
-        pass_smem<C, P, false>(sm, m, two_q);
-        fwd_middle<C, P + 1>(sm, m, two_q);
+        pass_smem<C, P, false, FP>(sm, m, two_q);
+        fwd_middle<C, P + 1, FP>(sm, m, two_q);
     }
 }
 
-template <class C, int P>
+template <class C, int P, bool FP>
 __device__ __forceinline__ void inv_middle(uint64_t* sm, const ModInfo& m, uint64_t two_q) {
     if constexpr (P > 0) {
-        pass_smem<C, P, true>(sm, m, two_q);
-        inv_middle<C, P - 1>(sm, m, two_q);
+        pass_smem<C, P, true, FP>(sm, m, two_q);
+        inv_middle<C, P - 1, FP>(sm, m, two_q);
     }
 }
 
 // Forward NTT of one limb.  load(idx) -> residue in [0, 4q); store(idx, v) receives
 // canonical values at idx = C::idx(r).
-template <class C, class Load, class Store>
-__device__ __forceinline__ void ntt_fwd(uint64_t* sm, const ModInfo& m, Load load, Store store) {
+template <class C, bool FP, class Load, class Store>
+__device__ __forceinline__ void ntt_fwd_impl(uint64_t* sm, const ModInfo& m, Load load, Store store) {
     using P0 = PassInfo<C, 0>;
     static_assert(P0::G == 1 && P0::BLOW == C::LOGM - C::LOGE, "pass 0 layout");
     const uint64_t q = m.q, two_q = 2 * q;
@@ -204,7 +206,7 @@ __device__ __forceinline__ void ntt_fwd(uint64_t* sm, const ModInfo& m, Load loa
         for (int g = 0; g < C::E / C::K; g++) {
 #pragma unroll
             for (int t = 0; t < C::K; t++) x[g * C::K + t] = load(j0 + g * C::T + t * C::M);
-            fwd_pass_regs<0, C::LOGK>(x + g * C::K, 0, m.tw_fwd, q, two_q);
+            fwd_pass_regs<0, C::LOGK, FP>(x + g * C::K, 0, m.tw_fwd, q, two_q);
         }
         cluster_sync_all();   // every CTA is running and done with its shared memory
 #pragma unroll
@@ -217,11 +219,11 @@ __device__ __forceinline__ void ntt_fwd(uint64_t* sm, const ModInfo& m, Load loa
 #pragma unroll
         for (int r = 0; r < C::E; r++) x[r] = sm[spad(tid + r * C::T)];
     }
-    fwd_pass_regs<C::LOGK, C::LOGE>(x, C::crank(), m.tw_fwd, q, two_q);
+    fwd_pass_regs<C::LOGK, C::LOGE, FP>(x, C::crank(), m.tw_fwd, q, two_q);
 #pragma unroll
     for (int r = 0; r < C::E; r++) sm[spad(tid + r * C::T)] = x[r];
     __syncthreads();
-    fwd_middle<C, 1>(sm, m, two_q);
+    fwd_middle<C, 1, FP>(sm, m, two_q);
 #pragma unroll
     for (int r = 0; r < C::E; r++) {
         uint64_t v = sm[spad(tid + r * C::T)];
@@ -233,18 +235,18 @@ __device__ __forceinline__ void ntt_fwd(uint64_t* sm, const ModInfo& m, Load loa
 
 // Inverse NTT of one limb.  load(idx) at idx = C::idx(r) -> residue in [0, 2q);
 // store(idx, canonical value).
-template <class C, class Load, class Store>
-__device__ __forceinline__ void ntt_inv(uint64_t* sm, const ModInfo& m, Load load, Store store) {
+template <class C, bool FP, class Load, class Store>
+__device__ __forceinline__ void ntt_inv_impl(uint64_t* sm, const ModInfo& m, Load load, Store store) {
     const uint64_t q = m.q, two_q = 2 * q;
     const int tid = threadIdx.x;
 #pragma unroll
     for (int r = 0; r < C::E; r++) sm[spad(tid + r * C::T)] = load(C::idx(r));
     __syncthreads();
-    inv_middle<C, C::NPASS - 1>(sm, m, two_q);
+    inv_middle<C, C::NPASS - 1, FP>(sm, m, two_q);
     uint64_t x[C::E];
 #pragma unroll
     for (int r = 0; r < C::E; r++) x[r] = sm[spad(tid + r * C::T)];
-    inv_pass_regs<C::LOGK, C::LOGE, C::K == 1>(x, C::crank(), m, two_q);
+    inv_pass_regs<C::LOGK, C::LOGE, C::K == 1, FP>(x, C::crank(), m, two_q);
     if constexpr (C::K == 1) {
 #pragma unroll
         for (int r = 0; r < C::E; r++) store(tid + r * C::T, csub(x[r], q));
@@ -264,12 +266,32 @@ __device__ __forceinline__ void ntt_inv(uint64_t* sm, const ModInfo& m, Load loa
         for (int g = 0; g < C::E / C::K; g++) {
 #pragma unroll
             for (int t = 0; t < C::K; t++) x[g * C::K + t] = sm[spad(t * MK + tid + g * C::T)];
-            inv_pass_regs<0, C::LOGK, true>(x + g * C::K, 0, m, two_q);
+            inv_pass_regs<0, C::LOGK, true, FP>(x + g * C::K, 0, m, two_q);
 #pragma unroll
             for (int t = 0; t < C::K; t++) store(j0 + g * C::T + t * C::M, csub(x[g * C::K + t], q));
         }
         __syncthreads();
     }
+}
+
+// Public entry points: the twiddle-product flavour is uniform per limb (ModInfo::fp), so
+// the branch is uniform across the CTA.
+template <class C, class Load, class Store>
+__device__ __forceinline__ void ntt_fwd(uint64_t* sm, const ModInfo& m, Load load, Store store) {
+#ifndef EDL_NO_FP_QUOTIENT
+    if (m.fp) ntt_fwd_impl<C, true>(sm, m, load, store);
+    else
+#endif
+        ntt_fwd_impl<C, false>(sm, m, load, store);
+}
+
+template <class C, class Load, class Store>
+__device__ __forceinline__ void ntt_inv(uint64_t* sm, const ModInfo& m, Load load, Store store) {
+#ifndef EDL_NO_FP_QUOTIENT
+    if (m.fp) ntt_inv_impl<C, true>(sm, m, load, store);
+    else
+#endif
+        ntt_inv_impl<C, false>(sm, m, load, store);
 }
 
 // ---- per-N configurations -------------------------------------------------------------
@@ -313,6 +335,13 @@ __host__ __device__ constexpr int cfg_minb(int logm, int loge) {
 
 template <int LOGN, bool PLAIN>
 using CfgOf = NttCfg<LOGN, cfg_logk(LOGN, PLAIN), cfg_loge(LOGN, PLAIN), cfg_minb(cfg_logm(LOGN, PLAIN), cfg_loge(LOGN, PLAIN))>;
+template <int LOGN, int LOGE>   // fused config with an explicit residues-per-thread
+using CfgFusedE = NttCfg<LOGN, cfg_logk(LOGN, false), LOGE, cfg_minb(cfg_logm(LOGN, false), LOGE)>;
+#ifndef EDL_LOGE_KS14
+#define EDL_LOGE_KS14 EDL_LOGE_F14
+#endif
+template <int LOGN>   // key-switch MAC kernel (largest epilogue)
+using CfgKs = CfgFusedE<LOGN, cfg_logm(LOGN, false) == 14 ? EDL_LOGE_KS14 : cfg_loge(LOGN, false)>;
 template <int LOGN>
 using CfgPlain = CfgOf<LOGN, true>;
 template <int LOGN>

@@ -1,0 +1,284 @@
+// ntt_kernels.cu -- NTT-based kernels of the hot path (
+// K1/K2/K5/K6).  Each CTA transforms whole limbs with ntt_core.cuh and fuses the
+// surrounding pointwise work into the transform's prologue/epilogue, so every rescale
+// and key-switch touches HBM once per input and once per output limb.
+#pragma once
+#include "kernels.cuh"
+#include "ntt_core.cuh"
+
+namespace edl {
+
+
+// ------------------------------------------------------------------------------------
+// K1/K2: plain batched NTT / INTT, in place, data [batch][nl][N], limb j uses pm.idx[j].
+template <class C, bool INV>
+__global__ void __launch_bounds__(C::T, C::MINB)
+k_ntt_limbs(uint64_t* __restrict__ data, int nl, const __grid_constant__ PrimeMap pm, const ModInfo* __restrict__ mods) {
+    extern __shared__ uint64_t sm[];
+    const int limb = blockIdx.y;    // limb-major grid: co-resident CTAs share a prime (code path, twiddles)
+    uint64_t* p = data + (((size_t)C::bx() * nl + limb) << C::LOGN);
+    const ModInfo& m = mods[pm.idx[limb]];
+    auto ld = [&](int idx) { return p[idx]; };
+    auto st = [&](int idx, uint64_t v) { p[idx] = v; };
+    if constexpr (INV) ntt_inv<C>(sm, m, ld, st);
+    else ntt_fwd<C>(sm, m, ld, st);
+}
+
+// ------------------------------------------------------------------------------------
+// K6 rescale, step 1 (O12): r = INTT_{q_l}(c[l] * w_l) for both polys of every ct.  With a
+// second constant w2 the same INTT also yields r2 = INTT(c[l] * w2_l) (INTT is linear),
+// which the sigma schedule uses for its two scalar products of y (O13 steps 2 and 4).
+template <class C>
+__global__ void __launch_bounds__(C::T, C::MINB)
+k_rescale_intt(const uint64_t* __restrict__ in, int l, const ulonglong2* __restrict__ w,
+               uint64_t* __restrict__ r_out, const ulonglong2* __restrict__ w2, uint64_t* __restrict__ r_out2,
+               const ModInfo* __restrict__ mods) {
+    extern __shared__ uint64_t sm[];
+    const int p = blockIdx.y;
+    const int64_t c = C::bx();
+    const uint64_t* src = in + limb_off(c, p, l, l + 1, C::LOGN);
+    uint64_t* dst = r_out + (((size_t)c * 2 + p) << C::LOGN);
+    uint64_t* dst2 = r_out2 ? r_out2 + (((size_t)c * 2 + p) << C::LOGN) : nullptr;
+    const ModInfo& m = mods[l];
+    if (w2 == nullptr) {
+        const bool has_w = (w != nullptr);
+        ulonglong2 wl = has_w ? w[c * (l + 1) + l] : make_ulonglong2(1, 0);
+        auto ld = [&](int idx) { return has_w ? mulc_lazy(src[idx], wl, m) : src[idx]; };
+        auto st = [&](int idx, uint64_t v) { dst[idx] = v; };
+        ntt_inv<C>(sm, m, ld, st);
+    } else {
+        const ulonglong2 wa = w[c * (l + 1) + l], wb = w2[c * (l + 1) + l];
+        auto ld = [&](int idx) { return src[idx]; };
+        auto st = [&](int idx, uint64_t v) {
+            dst[idx] = mulc(v, wa, m);
+            dst2[idx] = mulc(v, wb, m);
+        };
+        ntt_inv<C>(sm, m, ld, st);
+    }
+}
+
+// K6 rescale, step 2: out_i = (c_i w_i - NTT_i([r]_{q_l} mod q_i)) q_l^{-1} (+ bias_i).
+template <class C>
+__global__ void __launch_bounds__(C::T, C::MINB)
+k_rescale_ntt(const uint64_t* __restrict__ in, int l, const ulonglong2* __restrict__ w,
+              const uint64_t* __restrict__ r, const uint64_t* __restrict__ bias, uint64_t* __restrict__ out, int nlo,
+              const ModInfo* __restrict__ mods, const ChainConsts* __restrict__ cc) {
+    extern __shared__ uint64_t sm[];
+    const int i = blockIdx.z, p = blockIdx.y;
+    const int64_t c = C::bx();
+    const ModInfo& m = mods[i];
+    const uint64_t ql = mods[l].q;
+    const uint64_t ql_mod = cc->qmod[l][i];
+    const ulonglong2 qlinv = cc->qinv[l][i];
+    const uint64_t* rr = r + (((size_t)c * 2 + p) << C::LOGN);
+    const uint64_t* src = in + limb_off(c, p, i, l + 1, C::LOGN);
+    uint64_t* dst = out + limb_off(c, p, i, nlo, C::LOGN);
+    const bool has_w = (w != nullptr);
+    const ulonglong2 wi = has_w ? w[c * (l + 1) + i] : make_ulonglong2(1, 0);
+    const uint64_t b = (bias != nullptr && p == 0) ? bias[c * l + i] : 0;
+    auto ld = [&](int idx) { return center_mod(rr[idx], ql, ql_mod, m); };
+    auto st = [&](int idx, uint64_t x) {
+        uint64_t a = src[idx];
+        if (has_w) a = mulc(a, wi, m);
+        uint64_t v = mulc(submod(a, x, m.q), qlinv, m);
+        dst[idx] = addmod(v, b, m.q);
+    };
+    ntt_fwd<C>(sm, m, ld, st);
+}
+
+// ------------------------------------------------------------------------------------
+// K5 relinearisation (O11) of the tensor product d = a (x) b at level l, in 4 launches:
+//   M1 acoef_j = INTT_{q_j}(a1_j b1_j)                                   [cnt][l+1]
+//   M2a xh_{j,t} = NTT_t(acoef_j mod t), t != q_j                        [cnt][l+1][l+2]
+//   M2b acc_{c,t} = sum_j xh_{j,t} * rlk_j[c][t]  (t = q_0..q_l, P; the t == q_j term
+//      uses d2_j = a1_j b1_j directly), 128-bit lazy sums, one Barrett     [cnt][2][l+2]
+//   M3 r_c = INTT_P(acc_{c,P}); if rescaling also
+//      s_c = INTT_{q_l}(d_c,l + acc_{c,l} P^-1) - [r_c]_{q_l} P^-1  (= INTT of the
+//      relinearised limb l, by linearity)                                 [cnt][2]
+//   M4 out_{c,i} = d_c,i + (acc_{c,i} - NTT_i([r_c]_{q_i})) P^-1                 (no rescale)
+//      out_{c,i} = (d_c,i + acc_{c,i} P^-1 - NTT_i([r_c]_{q_i} P^-1 + [s_c]_{q_i})) q_l^-1
+//      which is bit-identical to mod-down followed by O12 rescale (all steps are exact
+//      Z_q-linear maps of the same centered lifts).
+__device__ __forceinline__ uint64_t tensor_comp(const uint64_t* a, const uint64_t* b, int64_t c, int cp, int i,
+                                                int nl, int logn, int idx, const ModInfo& m) {
+    const uint64_t a0 = a[limb_off(c, 0, i, nl, logn) + idx];
+    const uint64_t b1 = b[limb_off(c, 1, i, nl, logn) + idx];
+    const uint64_t b0 = b[limb_off(c, 0, i, nl, logn) + idx];
+    if (cp == 0) return mulmod(a0, b0, m);
+    const uint64_t a1 = a[limb_off(c, 1, i, nl, logn) + idx];
+    U128 s = mul_wide(a0, b1);
+    mac128(s, a1, b0);
+    return barrett128(s, m);
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::T, C::MINB)
+k_relin_intt_d2(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l,
+                uint64_t* __restrict__ acoef, const ModInfo* __restrict__ mods) {
+    extern __shared__ uint64_t sm[];
+    const int j = blockIdx.y;
+    const int64_t c = C::bx();
+    const ModInfo& m = mods[j];
+    const uint64_t* a1 = a + limb_off(c, 1, j, l + 1, C::LOGN);
+    const uint64_t* b1 = b + limb_off(c, 1, j, l + 1, C::LOGN);
+    uint64_t* dst = acoef + (((size_t)c * (l + 1) + j) << C::LOGN);
+    auto ld = [&](int idx) { return mulmod(a1[idx], b1[idx], m); };
+    auto st = [&](int idx, uint64_t v) { dst[idx] = v; };
+    ntt_inv<C>(sm, m, ld, st);
+}
+
+// M2a modulus raise: xh_{j,t} = NTT_t(acoef_j mod t) for every digit j and target t != j
+// (t = q_0..q_l, P), one limb transform per CTA with no epilogue work, so it runs at the
+// plain transform's rate; the key products are a separate streaming pass (M2b).
+template <class C>
+__global__ void __launch_bounds__(C::T, C::MINB)
+k_relin_modup(const uint64_t* __restrict__ acoef, int l, int L, uint64_t* __restrict__ xh,
+              const ModInfo* __restrict__ mods) {
+    extern __shared__ uint64_t sm[];
+    const int j = blockIdx.y / (l + 1), tt = blockIdx.y % (l + 1);
+    const int ti = tt < j ? tt : tt + 1;          // target slot 0..l+1 (l+1 = P), skipping j
+    const int t = (ti == l + 1) ? (L + 1) : ti;
+    const int64_t c = C::bx();
+    const ModInfo& m = mods[t];
+    const uint64_t* src = acoef + (((size_t)c * (l + 1) + j) << C::LOGN);
+    uint64_t* dst = xh + ((((size_t)c * (l + 1) + j) * (l + 2) + ti) << C::LOGN);
+    const bool need_red = mods[j].q > 4 * m.q;   // the forward NTT accepts [0, 4q)
+    auto ld = [&](int idx) {
+        uint64_t v = src[idx];
+        return need_red ? reduce64(v, m) : v;
+    };
+    auto st = [&](int idx, uint64_t v) { dst[idx] = v; };
+    ntt_fwd<C>(sm, m, ld, st);
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::T, C::MINB)
+k_relin_moddown_intt(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l,
+                     const uint64_t* __restrict__ acc, int L, int rescale, uint64_t* __restrict__ r_out,
+                     uint64_t* __restrict__ s_out, const ModInfo* __restrict__ mods,
+                     const ChainConsts* __restrict__ cc) {
+    extern __shared__ uint64_t sm[];
+    const int cp = blockIdx.y;
+    const int64_t c = C::bx();
+    const ModInfo& mp = mods[L + 1];
+    const uint64_t* accP = acc + ((((size_t)c * 2 + cp) * (l + 2) + (l + 1)) << C::LOGN);
+    uint64_t* rdst = r_out + (((size_t)c * 2 + cp) << C::LOGN);
+    {
+        auto ld = [&](int idx) { return accP[idx]; };
+        auto st = [&](int idx, uint64_t v) { rdst[idx] = v; };
+        ntt_inv<C>(sm, mp, ld, st);
+    }
+    if (!rescale) return;
+    const ModInfo& ml = mods[l];
+    const ulonglong2 pinv = cc->qinv[L + 1][l];
+    const uint64_t pmod = cc->qmod[L + 1][l];
+    const uint64_t* accl = acc + ((((size_t)c * 2 + cp) * (l + 2) + l) << C::LOGN);
+    uint64_t* sdst = s_out + (((size_t)c * 2 + cp) << C::LOGN);
+    auto ld = [&](int idx) {
+        uint64_t d = tensor_comp(a, b, c, cp, l, l + 1, C::LOGN, idx, ml);
+        return addmod(d, mulc(accl[idx], pinv, ml), ml.q);
+    };
+    auto st = [&](int idx, uint64_t y) {
+        uint64_t z = mulc(center_mod(rdst[idx], mp.q, pmod, ml), pinv, ml);
+        sdst[idx] = submod(y, z, ml.q);
+    };
+    ntt_inv<C>(sm, ml, ld, st);
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::T, C::MINB)
+k_relin_moddown_ntt(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l,
+                    const uint64_t* __restrict__ acc, const uint64_t* __restrict__ r,
+                    const uint64_t* __restrict__ s, int L, int rescale, uint64_t* __restrict__ out,
+                    const ModInfo* __restrict__ mods, const ChainConsts* __restrict__ cc) {
+    extern __shared__ uint64_t sm[];
+    const int i = blockIdx.z, cp = blockIdx.y;
+    const int64_t c = C::bx();
+    const ModInfo& m = mods[i];
+    const uint64_t P = mods[L + 1].q;
+    const uint64_t pmod = cc->qmod[L + 1][i];
+    const ulonglong2 pinv = cc->qinv[L + 1][i];
+    const uint64_t* rr = r + (((size_t)c * 2 + cp) << C::LOGN);
+    const uint64_t* ss = s + (((size_t)c * 2 + cp) << C::LOGN);
+    const uint64_t* acci = acc + ((((size_t)c * 2 + cp) * (l + 2) + i) << C::LOGN);
+    const int nlo = rescale ? l : l + 1;
+    uint64_t* dst = out + limb_off(c, cp, i, nlo, C::LOGN);
+    if (rescale) {
+        const uint64_t ql = mods[l].q;
+        const uint64_t qlmod = cc->qmod[l][i];
+        const ulonglong2 qlinv = cc->qinv[l][i];
+        auto ld = [&](int idx) {
+            uint64_t u = mulc(center_mod(rr[idx], P, pmod, m), pinv, m);
+            return addmod(u, center_mod(ss[idx], ql, qlmod, m), m.q);
+        };
+        auto st = [&](int idx, uint64_t x) {
+            uint64_t d = tensor_comp(a, b, c, cp, i, l + 1, C::LOGN, idx, m);
+            uint64_t v = addmod(d, mulc(acci[idx], pinv, m), m.q);
+            dst[idx] = mulc(submod(v, x, m.q), qlinv, m);
+        };
+        ntt_fwd<C>(sm, m, ld, st);
+    } else {
+        auto ld = [&](int idx) { return center_mod(rr[idx], P, pmod, m); };
+        auto st = [&](int idx, uint64_t x) {
+            uint64_t d = tensor_comp(a, b, c, cp, i, l + 1, C::LOGN, idx, m);
+            dst[idx] = addmod(d, mulc(submod(acci[idx], x, m.q), pinv, m), m.q);
+        };
+        ntt_fwd<C>(sm, m, ld, st);
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// Per-N launchers (explicitly instantiated once per ring degree in ntt_inst_<logN>.cu so the
+// heavy template expansion compiles in parallel).  Grids are [limb-like x K, ...]: the K CTAs
+// of one limb form a cluster.
+template <int LOGN>
+void launch_ntt_limbs_n(const Dev& d, uint64_t* data, int64_t batch, int nl, const PrimeMap& pm, bool inverse) {
+    using C = CfgPlain<LOGN>;
+    const dim3 grid((unsigned)batch, nl);
+    if (inverse) launch_cfg<C>(d, "k_ntt_limbs", k_ntt_limbs<C, true>, grid, data, nl, pm, d.mods);
+    else launch_cfg<C>(d, "k_ntt_limbs", k_ntt_limbs<C, false>, grid, data, nl, pm, d.mods);
+}
+
+template <int LOGN>
+void launch_rescale_intt_n(const Dev& d, const uint64_t* in, int64_t cnt, int l, const ulonglong2* w, uint64_t* r_out,
+                           const ulonglong2* w2, uint64_t* r_out2) {
+    using C = CfgFused<LOGN>;
+    launch_cfg<C>(d, "k_rescale_intt", k_rescale_intt<C>, dim3((unsigned)cnt, 2), in, l, w, r_out, w2, r_out2, d.mods);
+}
+
+template <int LOGN>
+void launch_rescale_ntt_n(const Dev& d, const uint64_t* in, int64_t cnt, int l, const ulonglong2* w, const uint64_t* r,
+                          const uint64_t* bias, uint64_t* out, int nlo) {
+    using C = CfgFused<LOGN>;
+    launch_cfg<C>(d, "k_rescale_ntt", k_rescale_ntt<C>, dim3((unsigned)cnt, 2, nlo), in, l, w, r, bias, out, nlo, d.mods,
+                  d.cc);
+}
+
+template <int LOGN>
+void launch_relin_n(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t cnt, int l, bool rescale,
+                    const uint64_t* rlk, const uint64_t* rlk_c, uint64_t* acoef, uint64_t* xh, uint64_t* acc, uint64_t* r,
+                    uint64_t* s, uint64_t* out) {
+    using C = CfgFused<LOGN>;
+    using CP = CfgPlain<LOGN>;
+    const int rs = rescale ? 1 : 0;
+    launch_cfg<C>(d, "k_relin_intt_d2", k_relin_intt_d2<C>, dim3((unsigned)cnt, l + 1), a, b, l, acoef, d.mods);
+    launch_cfg<CP>(d, "k_relin_modup", k_relin_modup<CP>, dim3((unsigned)cnt, (l + 1) * (l + 1)), (const uint64_t*)acoef,
+                   l, d.L, xh, d.mods);
+    launch_relin_mac(d, a, b, cnt, l, xh, rlk, rlk_c, acc);
+    launch_cfg<C>(d, "k_relin_moddown_intt", k_relin_moddown_intt<C>, dim3((unsigned)cnt, 2), a, b, l, (const uint64_t*)acc,
+                  d.L, rs, r, s, d.mods, d.cc);
+    launch_cfg<C>(d, "k_relin_moddown_ntt", k_relin_moddown_ntt<C>, dim3((unsigned)cnt, 2, rescale ? l : l + 1), a, b, l,
+                  (const uint64_t*)acc, (const uint64_t*)r, (const uint64_t*)s, d.L, rs, out, d.mods, d.cc);
+}
+
+#define EDL_INSTANTIATE_NTT(LOGN)                                                                                   \
+    template void launch_ntt_limbs_n<LOGN>(const Dev&, uint64_t*, int64_t, int, const PrimeMap&, bool);            \
+    template void launch_rescale_intt_n<LOGN>(const Dev&, const uint64_t*, int64_t, int, const ulonglong2*,         \
+                                              uint64_t*, const ulonglong2*, uint64_t*);                             \
+    template void launch_rescale_ntt_n<LOGN>(const Dev&, const uint64_t*, int64_t, int, const ulonglong2*,          \
+                                             const uint64_t*, const uint64_t*, uint64_t*, int);                     \
+    template void launch_relin_n<LOGN>(const Dev&, const uint64_t*, const uint64_t*, int64_t, int, bool,            \
+                                       const uint64_t*, const uint64_t*, uint64_t*, uint64_t*, uint64_t*, uint64_t*, \
+                                       uint64_t*, uint64_t*);
+
+}  // namespace edl

@@ -49,13 +49,13 @@ __global__ void k_mul_const(const uint64_t* __restrict__ a, int64_t cnt, int l, 
     for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
         const int i = (int)(row % (l + 1));
         const int64_t c = row / (2 * (l + 1));
-        const uint64_t q = mods[i].q;
+        const ModInfo& m = mods[i];
         const ulonglong2 wi = w[c * (l + 1) + i];
         const uint64_t* pa = a + ((size_t)row << logn);
         uint64_t* po = out + ((size_t)row << logn);
         for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n2; k += gridDim.x * blockDim.x) {
             ulonglong2 x = v2(pa)[k];
-            v2(po)[k] = make_ulonglong2(shoup(x.x, wi.x, wi.y, q), shoup(x.y, wi.x, wi.y, q));
+            v2(po)[k] = make_ulonglong2(mulc(x.x, wi, m), mulc(x.y, wi, m));
         }
     }
 }
@@ -143,7 +143,7 @@ constexpr int CC_TAPS = 16;
 
 __global__ void __launch_bounds__(PW_THREADS, 2)
 k_cc_mac(const uint64_t* __restrict__ x, int l, int H, int W, int F, int kh, int kw, int stride,
-         const uint64_t* __restrict__ wk, uint64_t* __restrict__ out, const ModInfo* __restrict__ mods, int logn) {
+         const ulonglong2* __restrict__ wk, uint64_t* __restrict__ out, const ModInfo* __restrict__ mods, int logn) {
     extern __shared__ uint64_t wsm[];   // [F][taps] residues for this limb
     const int nl = l + 1;
     const int p = blockIdx.y / nl, i = blockIdx.y % nl;
@@ -152,7 +152,7 @@ k_cc_mac(const uint64_t* __restrict__ x, int l, int H, int W, int F, int kh, int
     const int win = blockIdx.z;
     const int wr = win / Wo, wc = win % Wo;
     const int taps = kh * kw;
-    for (int t = threadIdx.x; t < F * taps; t += blockDim.x) wsm[t] = wk[(size_t)t * nl + i];
+    for (int t = threadIdx.x; t < F * taps; t += blockDim.x) wsm[t] = wk[(size_t)t * nl + i].x;
     __syncthreads();
     const ModInfo m = mods[i];
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
@@ -208,9 +208,9 @@ constexpr int CC2_MAXTAPS = 64;
 template <int FC>
 __global__ void __launch_bounds__(CC2_THREADS, 2)
 k_cc_mac2(const uint64_t* __restrict__ x, int l, int W, int kw, int stride, int Wo, int taps, int f0, int F,
-          int n_out_per_f, const uint64_t* __restrict__ wk, uint64_t* __restrict__ out,
+          int n_out_per_f, const ulonglong2* __restrict__ wk, uint64_t* __restrict__ out,
           const ModInfo* __restrict__ mods, int logn) {
-    __shared__ uint64_t wsm[FC * CC2_MAXTAPS];   // [f][tap] residues of this limb
+    __shared__ ulonglong2 wsm[FC * CC2_MAXTAPS];  // [f][tap] {residue, companion} of this limb
     __shared__ int tpix[CC2_MAXTAPS];            // pixel (ciphertext) index of each tap
     const int nl = l + 1;
     const int p = blockIdx.y / nl, i = blockIdx.y % nl;
@@ -218,16 +218,19 @@ k_cc_mac2(const uint64_t* __restrict__ x, int l, int W, int kw, int stride, int 
     const int wr = win / Wo, wc = win % Wo;
     for (int t = threadIdx.x; t < FC * taps; t += blockDim.x) {
         const int f = t / taps, tt = t % taps;
-        wsm[t] = (f0 + f < F) ? wk[((size_t)(f0 + f) * taps + tt) * nl + i] : 0;
+        wsm[t] = (f0 + f < F) ? wk[((size_t)(f0 + f) * taps + tt) * nl + i] : make_ulonglong2(0, 0);
     }
     for (int t = threadIdx.x; t < taps; t += blockDim.x)
         tpix[t] = (wr * stride + t / kw) * W + (wc * stride + t % kw);
     __syncthreads();
     const int n2 = blockIdx.x * blockDim.x + threadIdx.x;   // coefficient pair
     if (2 * n2 >= (1 << logn)) return;
-    const ModInfo m = mods[i];
+    const ModInfo& m = mods[i];
     const size_t ct_words = (size_t)2 * nl << logn;
     const uint64_t* xb = x + limb_off(0, p, i, nl, logn) + 2 * (size_t)n2;
+    const bool fp = m.fp != 0;
+    // FP64-quotient limbs: lazy products in [0, 2q) summed in 64 bits (taps * 2q < 2^57);
+    // others: full 128-bit products summed lazily (O4), one reduction per output
     U128 acc[FC][2];
 #pragma unroll
     for (int f = 0; f < FC; f++) acc[f][0].lo = acc[f][0].hi = acc[f][1].lo = acc[f][1].hi = 0;
@@ -242,14 +245,27 @@ k_cc_mac2(const uint64_t* __restrict__ x, int l, int W, int kw, int stride, int 
             nxt[u] = (tt < taps) ? __ldg(reinterpret_cast<const ulonglong2*>(xb + tpix[tt] * ct_words))
                                  : make_ulonglong2(0, 0);
         }
+        if (fp) {
 #pragma unroll
-        for (int u = 0; u < CC2_TB; u++) {
-            const int tt = t0 + u < taps ? t0 + u : 0;   // out-of-range taps carry x = 0
+            for (int u = 0; u < CC2_TB; u++) {
+                const int tt = t0 + u < taps ? t0 + u : 0;   // out-of-range taps carry x = 0
 #pragma unroll
-            for (int f = 0; f < FC; f++) {
-                const uint64_t w = wsm[f * taps + tt];
-                mac128(acc[f][0], cur[u].x, w);
-                mac128(acc[f][1], cur[u].y, w);
+                for (int f = 0; f < FC; f++) {
+                    const ulonglong2 w = wsm[f * taps + tt];
+                    acc[f][0].lo += tw_mul_fp(cur[u].x, w.x, w.y, m.q);
+                    acc[f][1].lo += tw_mul_fp(cur[u].y, w.x, w.y, m.q);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < CC2_TB; u++) {
+                const int tt = t0 + u < taps ? t0 + u : 0;
+#pragma unroll
+                for (int f = 0; f < FC; f++) {
+                    const uint64_t w = wsm[f * taps + tt].x;
+                    mac128(acc[f][0], cur[u].x, w);
+                    mac128(acc[f][1], cur[u].y, w);
+                }
             }
         }
 #pragma unroll
@@ -260,7 +276,9 @@ k_cc_mac2(const uint64_t* __restrict__ x, int l, int W, int kw, int stride, int 
         if (f0 + f < F) {
             const int64_t o = (int64_t)(f0 + f) * n_out_per_f + win;
             uint64_t* dst = out + limb_off(o, p, i, nl, logn) + 2 * (size_t)n2;
-            *reinterpret_cast<ulonglong2*>(dst) = make_ulonglong2(barrett128(acc[f][0], m), barrett128(acc[f][1], m));
+            const ulonglong2 v = fp ? make_ulonglong2(reduce64(acc[f][0].lo, m), reduce64(acc[f][1].lo, m))
+                                    : make_ulonglong2(barrett128(acc[f][0], m), barrett128(acc[f][1], m));
+            *reinterpret_cast<ulonglong2*>(dst) = v;
         }
     }
 }
@@ -276,9 +294,9 @@ constexpr int DN_KC = 256;    // fold 128-bit accumulators every 256 terms (K*q^
 constexpr int DN_U = 4;
 
 __global__ void __launch_bounds__(PW_THREADS, 2)
-k_dense_mac(const uint64_t* __restrict__ x, int64_t K, int64_t O, int l, int ks, const uint64_t* __restrict__ wd,
+k_dense_mac(const uint64_t* __restrict__ x, int64_t K, int64_t O, int l, int ks, const ulonglong2* __restrict__ wd,
             uint64_t* __restrict__ out, const ModInfo* __restrict__ mods, int logn) {
-    extern __shared__ uint64_t wsm[];   // [DN_OC][DN_KC]
+    extern __shared__ ulonglong2 wsm2[];   // [DN_OC][DN_KC] {residue, companion}
     const int nl = l + 1;
     const int p = blockIdx.y / nl, i = blockIdx.y % nl;
     const int oc = blockIdx.z / ks, sl = blockIdx.z % ks;
@@ -286,7 +304,8 @@ k_dense_mac(const uint64_t* __restrict__ x, int64_t K, int64_t O, int l, int ks,
     const int64_t kper = (K + ks - 1) / ks;
     const int64_t kbeg = sl * kper, kend = (kbeg + kper < K) ? kbeg + kper : K;
     uint64_t* outp = out + (size_t)sl * ((size_t)O * 2 * nl << logn);
-    const ModInfo m = mods[i];
+    const ModInfo& m = mods[i];
+    const bool fp = m.fp != 0;
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = n < (1 << logn);
     const size_t kstride = (size_t)2 * nl << logn;            // one ciphertext
@@ -297,7 +316,7 @@ k_dense_mac(const uint64_t* __restrict__ x, int64_t K, int64_t O, int l, int ks,
         __syncthreads();
         for (int t = threadIdx.x; t < DN_OC * DN_KC; t += blockDim.x) {
             const int o = t / DN_KC, k = t % DN_KC;
-            wsm[t] = (o0 + o < O && k < kc) ? wd[((size_t)(o0 + o) * K + (k0 + k)) * nl + i] : 0;
+            wsm2[t] = (o0 + o < O && k < kc) ? wd[((size_t)(o0 + o) * K + (k0 + k)) * nl + i] : make_ulonglong2(0, 0);
         }
         __syncthreads();
         if (!active) { first = false; continue; }
@@ -308,17 +327,28 @@ k_dense_mac(const uint64_t* __restrict__ x, int64_t K, int64_t O, int l, int ks,
             uint64_t xv[DN_U];
 #pragma unroll
             for (int u = 0; u < DN_U; u++) xv[u] = (k + u < kc) ? __ldg(xp + (size_t)(k0 + k + u) * kstride) : 0;
+            if (fp) {   // lazy [0, 2q) products summed in 64 bits (256 * 2q < 2^59)
 #pragma unroll
-            for (int u = 0; u < DN_U; u++) {
+                for (int u = 0; u < DN_U; u++) {
 #pragma unroll
-                for (int o = 0; o < DN_OC; o++) mac128(acc[o], xv[u], wsm[o * DN_KC + ((k + u) & (DN_KC - 1))]);
+                    for (int o = 0; o < DN_OC; o++) {
+                        const ulonglong2 w = wsm2[o * DN_KC + ((k + u) & (DN_KC - 1))];
+                        acc[o].lo += tw_mul_fp(xv[u], w.x, w.y, m.q);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < DN_U; u++) {
+#pragma unroll
+                    for (int o = 0; o < DN_OC; o++) mac128(acc[o], xv[u], wsm2[o * DN_KC + ((k + u) & (DN_KC - 1))].x);
+                }
             }
         }
 #pragma unroll
         for (int o = 0; o < DN_OC; o++) {
             if (o0 + o < O) {
                 uint64_t* dst = outp + limb_off(o0 + o, p, i, nl, logn) + n;
-                uint64_t v = barrett128(acc[o], m);
+                uint64_t v = fp ? reduce64(acc[o].lo, m) : barrett128(acc[o], m);
                 if (!first) v = addmod(v, *dst, m.q);
                 *dst = v;
             }
@@ -349,7 +379,82 @@ __global__ void k_dense_combine(const uint64_t* __restrict__ part, int ks, int64
     }
 }
 
+// ---------------------------------------------------------------- key inner product (M2b)
+// acc_{c,t} = sum_{j<=l} x_{j,t} rlk_j[c][t] mod q_t with x_{j,t} = xh_{j,t} (raised digit)
+// or, for t == j, d2_j = a1_j b1_j.  Two coefficients per thread (16-byte accesses); both
+// components share the digit loads; 128-bit lazy sums (l+1 < 2^8 terms of < 2^122), one
+// Barrett reduction per output (O4).
+__global__ void __launch_bounds__(PW_THREADS)
+k_relin_mac(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l, int L,
+            const uint64_t* __restrict__ xh, const uint64_t* __restrict__ rlk, const uint64_t* __restrict__ rlk_c,
+            uint64_t* __restrict__ acc, const ModInfo* __restrict__ mods, int logn) {
+    const int ti = blockIdx.y;                 // 0..l data targets, l+1 = P
+    const int64_t c = blockIdx.z;
+    const int t = (ti == l + 1) ? (L + 1) : ti;
+    const ModInfo& m = mods[t];
+    const bool fp = m.fp != 0;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;   // coefficient pair
+    if (2 * k >= (1 << logn)) return;
+    U128 s[2][2];
+#pragma unroll
+    for (int cc = 0; cc < 2; cc++) s[cc][0].lo = s[cc][0].hi = s[cc][1].lo = s[cc][1].hi = 0;
+    // digits in groups of MAC_G with every load of a group issued before its MACs
+    constexpr int MAC_G = 4;
+    for (int j0 = 0; j0 <= l; j0 += MAC_G) {
+        ulonglong2 x[MAC_G], r0[MAC_G], r1[MAC_G], c0[MAC_G], c1[MAC_G];
+#pragma unroll
+        for (int u = 0; u < MAC_G; u++) {
+            const int j = j0 + u;
+            if (j > l) break;
+            if (j == ti) {
+                const ulonglong2 a1 = v2(a + limb_off(c, 1, j, l + 1, logn))[k];
+                const ulonglong2 b1 = v2(b + limb_off(c, 1, j, l + 1, logn))[k];
+                x[u] = make_ulonglong2(mulmod(a1.x, b1.x, m), mulmod(a1.y, b1.y, m));
+            } else {
+                x[u] = v2(xh + ((((size_t)c * (l + 1) + j) * (l + 2) + ti) << logn))[k];
+            }
+            const size_t o0 = (((size_t)j * 2 + 0) * (L + 2) + t) << logn, o1 = (((size_t)j * 2 + 1) * (L + 2) + t) << logn;
+            r0[u] = __ldg(v2(rlk + o0) + k);
+            r1[u] = __ldg(v2(rlk + o1) + k);
+            if (fp) {
+                c0[u] = __ldg(v2(rlk_c + o0) + k);
+                c1[u] = __ldg(v2(rlk_c + o1) + k);
+            }
+        }
+        if (fp) {   // lazy [0, 2q) products, 64-bit sums ((l+1) * 2q < 2^60)
+#pragma unroll
+            for (int u = 0; u < MAC_G; u++) {
+                if (j0 + u > l) break;
+                s[0][0].lo += tw_mul_fp(x[u].x, r0[u].x, c0[u].x, m.q);
+                s[0][1].lo += tw_mul_fp(x[u].y, r0[u].y, c0[u].y, m.q);
+                s[1][0].lo += tw_mul_fp(x[u].x, r1[u].x, c1[u].x, m.q);
+                s[1][1].lo += tw_mul_fp(x[u].y, r1[u].y, c1[u].y, m.q);
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < MAC_G; u++) {
+                if (j0 + u > l) break;
+                mac128(s[0][0], x[u].x, r0[u].x);
+                mac128(s[0][1], x[u].y, r0[u].y);
+                mac128(s[1][0], x[u].x, r1[u].x);
+                mac128(s[1][1], x[u].y, r1[u].y);
+            }
+        }
+    }
+#pragma unroll
+    for (int cc = 0; cc < 2; cc++)
+        v2(acc + ((((size_t)c * 2 + cc) * (l + 2) + ti) << logn))[k] =
+            fp ? make_ulonglong2(reduce64(s[cc][0].lo, m), reduce64(s[cc][1].lo, m))
+               : make_ulonglong2(barrett128(s[cc][0], m), barrett128(s[cc][1], m));
+}
+
 }  // namespace
+
+void launch_relin_mac(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t cnt, int l, const uint64_t* xh,
+                      const uint64_t* rlk, const uint64_t* rlk_c, uint64_t* acc) {
+    dim3 grid((unsigned)((1 << d.logn) / (2 * PW_THREADS)), (unsigned)(l + 2), (unsigned)cnt);
+    EDL_LAUNCH(d, "k_relin_mac", k_relin_mac<<<grid, PW_THREADS, 0, d.st>>>(a, b, l, d.L, xh, rlk, rlk_c, acc, d.mods, d.logn));
+}
 
 void launch_add(const Dev& d, const uint64_t* a, int la, const uint64_t* b, int lb, int64_t cnt, int lo, uint64_t* out) {
     EDL_LAUNCH(d, "k_add", k_add<<<rows_grid(d.logn, cnt * 2 * (lo + 1)), PW_THREADS, 0, d.st>>>(a, la, b, lb, cnt, lo, out, d.mods, d.logn));
@@ -378,7 +483,7 @@ void launch_add_add_const(const Dev& d, const uint64_t* v, const uint64_t* w, in
 }
 
 void launch_cc_mac(const Dev& d, const uint64_t* x, int l, int H, int W, int F, int kh, int kw, int stride,
-                   const uint64_t* wk, uint64_t* out) {
+                   const ulonglong2* wk, uint64_t* out) {
     const int Ho = (H - kh) / stride + 1, Wo = (W - kw) / stride + 1;
     const int taps = kh * kw;
     if (taps <= CC2_MAXTAPS && d.logn >= 9) {
@@ -412,12 +517,12 @@ int dense_split(const Dev& d, int64_t K, int64_t O, int l) {
     return ks;
 }
 
-void launch_dense_mac(const Dev& d, const uint64_t* x, int64_t K, int64_t O, int l, const uint64_t* wd, uint64_t* out,
+void launch_dense_mac(const Dev& d, const uint64_t* x, int64_t K, int64_t O, int l, const ulonglong2* wd, uint64_t* out,
                       uint64_t* part) {
     const int ks = part ? dense_split(d, K, O, l) : 1;
     dim3 grid((unsigned)(((1 << d.logn) + PW_THREADS - 1) / PW_THREADS), (unsigned)(2 * (l + 1)),
               (unsigned)(((O + DN_OC - 1) / DN_OC) * ks));
-    size_t smem = (size_t)DN_OC * DN_KC * sizeof(uint64_t);
+    size_t smem = (size_t)DN_OC * DN_KC * sizeof(ulonglong2);
     uint64_t* dst = ks > 1 ? part : out;
     EDL_LAUNCH(d, "k_dense_mac", k_dense_mac<<<grid, PW_THREADS, smem, d.st>>>(x, K, O, l, ks, wd, dst, d.mods, d.logn));
     if (ks > 1)

@@ -1,180 +1,8 @@
-// rng.cu -- Philox4x32-10 sampling, key generation, public-key encryption and the
-// device half of decryption (client-side steps a1/a12).
-//
-// Counter layout (c0, c1, c2, c3) = (coefficient, object id, limb, domain tag), key =
-// (seed lo, seed hi).  Samples are drawn on the fly inside the NTT prologues, so the
-// secret/error polynomials never touch HBM in coefficient form.
-#include "kernels.cuh"
-#include "ntt_core.cuh"
+// rng.cu -- host dispatch of key generation, encryption and decryption (rng_kernels.cuh,
+// instantiated per ring degree in ntt_inst_<logN>.cu) and the raw Philox word kernel.
+#include "rng_kernels.cuh"
 
 namespace edl {
-
-enum : uint32_t { TAG_S = 1, TAG_PK_A = 2, TAG_PK_E = 3, TAG_RLK_A = 4, TAG_RLK_E = 5, TAG_ENC_V = 6, TAG_ENC_E0 = 7,
-                  TAG_ENC_E1 = 8 };
-
-__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
-#pragma unroll
-    for (int r = 0; r < 10; r++) {
-        if (r > 0) {
-            k.x += 0x9E3779B9u;
-            k.y += 0xBB67AE85u;
-        }
-        const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
-        const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
-        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
-    }
-    return c;
-}
-
-__device__ __forceinline__ uint4 draw(uint64_t seed, uint32_t coef, uint32_t obj, uint32_t limb, uint32_t tag) {
-    return philox4x32_10(make_uint4(coef, obj, limb, tag), make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
-}
-
-__device__ __forceinline__ int ternary_of(uint4 x) { return (int)(x.x % 3u) - 1; }
-__device__ __forceinline__ int cbd_of(uint4 x) { return __popc(x.x & 0x1FFFFFu) - __popc(x.y & 0x1FFFFFu); }
-
-__device__ __forceinline__ uint64_t uniform_of(uint4 x, const ModInfo& m) {
-    U128 u;
-    u.lo = (uint64_t)x.x | ((uint64_t)x.y << 32);
-    u.hi = (uint64_t)x.z | ((uint64_t)x.w << 32);
-    return barrett128(u, m);
-}
-
-__device__ __forceinline__ uint64_t small_mod(int v, uint64_t q) { return v >= 0 ? (uint64_t)v : q - (uint64_t)(-v); }
-
-__device__ __forceinline__ uint64_t signed_mod(int64_t v, const ModInfo& m) {
-    if (v >= 0) return reduce64((uint64_t)v, m);
-    uint64_t r = reduce64((uint64_t)(-(v + 1)) + 1, m);   // |v| without overflow at INT64_MIN
-    return r == 0 ? 0 : m.q - r;
-}
-
-// floor(w * 2^64 / q) by restoring division (key generation only).
-__device__ uint64_t shoup_companion(uint64_t w, uint64_t q) {
-    uint64_t rem = w, quo = 0;
-    for (int b = 0; b < 64; b++) {
-        const bool top = (rem >> 63) != 0;
-        rem <<= 1;
-        quo <<= 1;
-        if (top || rem >= q) {
-            rem -= q;
-            quo |= 1;
-        }
-    }
-    return quo;
-}
-
-// ---- keygen: one CTA per modulus (secret), per data limb (pk), per (digit, limb) (rlk)
-template <class C>
-__global__ void __launch_bounds__(C::T, C::MINB)
-k_keygen_s(uint64_t seed, uint64_t* __restrict__ s_hat, const ModInfo* __restrict__ mods) {
-    extern __shared__ uint64_t sm[];
-    const int i = C::bx();
-    const ModInfo m = mods[i];
-    uint64_t* dst = s_hat + ((size_t)i << C::LOGN);
-    auto ld = [&](int idx) { return small_mod(ternary_of(draw(seed, idx, 0, 0, TAG_S)), m.q); };
-    auto st = [&](int idx, uint64_t v) { dst[idx] = v; };
-    ntt_fwd<C>(sm, m, ld, st);
-}
-
-template <class C>
-__global__ void __launch_bounds__(C::T, C::MINB)
-k_keygen_pk(uint64_t seed, int L, const uint64_t* __restrict__ s_hat, uint64_t* __restrict__ pk,
-            const ModInfo* __restrict__ mods) {
-    extern __shared__ uint64_t sm[];
-    const int i = C::bx();
-    const ModInfo m = mods[i];
-    const uint64_t* s = s_hat + ((size_t)i << C::LOGN);
-    uint64_t* b = pk + ((size_t)(0 * (L + 1) + i) << C::LOGN);
-    uint64_t* a = pk + ((size_t)(1 * (L + 1) + i) << C::LOGN);
-    auto ld = [&](int idx) { return small_mod(cbd_of(draw(seed, idx, 0, 0, TAG_PK_E)), m.q); };
-    auto st = [&](int idx, uint64_t e) {
-        const uint64_t av = uniform_of(draw(seed, idx, 0, i, TAG_PK_A), m);
-        a[idx] = av;
-        b[idx] = submod(e, mulmod(av, s[idx], m), m.q);
-    };
-    ntt_fwd<C>(sm, m, ld, st);
-}
-
-template <class C>
-__global__ void __launch_bounds__(C::T, C::MINB)
-k_keygen_rlk(uint64_t seed, int L, const uint64_t* __restrict__ s_hat, uint64_t* __restrict__ rlk,
-             uint64_t* __restrict__ rlk_s, const ModInfo* __restrict__ mods, const ChainConsts* __restrict__ cc) {
-    extern __shared__ uint64_t sm[];
-    const int i = C::bx();   // limb 0..L+1 (L+1 = P)
-    const int j = blockIdx.y;   // digit 0..L
-    const ModInfo m = mods[i];
-    const uint64_t* s = s_hat + ((size_t)i << C::LOGN);
-    const size_t ob = ((size_t)(j * 2 + 0) * (L + 2) + i) << C::LOGN;
-    const size_t oa = ((size_t)(j * 2 + 1) * (L + 2) + i) << C::LOGN;
-    const uint64_t pmod = cc->qmod[L + 1][i];
-    auto ld = [&](int idx) { return small_mod(cbd_of(draw(seed, idx, j, 0, TAG_RLK_E)), m.q); };
-    auto st = [&](int idx, uint64_t e) {
-        const uint64_t av = uniform_of(draw(seed, idx, j, i, TAG_RLK_A), m);
-        const uint64_t sv = s[idx];
-        uint64_t bv = submod(e, mulmod(av, sv, m), m.q);
-        if (i == j) bv = addmod(bv, mulmod(mulmod(sv, sv, m), pmod, m), m.q);
-        rlk[ob + idx] = bv;
-        rlk[oa + idx] = av;
-        rlk_s[ob + idx] = shoup_companion(bv, m.q);
-        rlk_s[oa + idx] = shoup_companion(av, m.q);
-    };
-    ntt_fwd<C>(sm, m, ld, st);
-}
-
-// ---- encrypt (O8): c0 = v*b + NTT(e0 + m), c1 = v*a + NTT(e1), per (ct, limb)
-template <class C>
-__global__ void __launch_bounds__(C::T, C::MINB)
-k_encrypt(const int64_t* __restrict__ msg, int l, int L, uint64_t seed, uint32_t obj0, const uint64_t* __restrict__ pk,
-          uint64_t* __restrict__ out, const ModInfo* __restrict__ mods) {
-    extern __shared__ uint64_t sm[];
-    const int i = C::bx();
-    const int64_t c = blockIdx.y;
-    const uint32_t obj = obj0 + (uint32_t)c;
-    const ModInfo m = mods[i];
-    const int64_t* mm = msg + ((size_t)c << C::LOGN);
-    uint64_t* c0 = out + limb_off(c, 0, i, l + 1, C::LOGN);
-    uint64_t* c1 = out + limb_off(c, 1, i, l + 1, C::LOGN);
-    const uint64_t* pb = pk + ((size_t)(0 * (L + 1) + i) << C::LOGN);
-    const uint64_t* pa = pk + ((size_t)(1 * (L + 1) + i) << C::LOGN);
-    {
-        auto ld = [&](int idx) { return small_mod(cbd_of(draw(seed, idx, obj, 0, TAG_ENC_E1)), m.q); };
-        auto st = [&](int idx, uint64_t v) { c1[idx] = v; };
-        ntt_fwd<C>(sm, m, ld, st);
-    }
-    {
-        auto ld = [&](int idx) {
-            return addmod(small_mod(cbd_of(draw(seed, idx, obj, 0, TAG_ENC_E0)), m.q), signed_mod(mm[idx], m), m.q);
-        };
-        auto st = [&](int idx, uint64_t v) { c0[idx] = v; };
-        ntt_fwd<C>(sm, m, ld, st);
-    }
-    {
-        auto ld = [&](int idx) { return small_mod(ternary_of(draw(seed, idx, obj, 0, TAG_ENC_V)), m.q); };
-        auto st = [&](int idx, uint64_t v) {
-            c0[idx] = addmod(c0[idx], mulmod(v, pb[idx], m), m.q);
-            c1[idx] = addmod(c1[idx], mulmod(v, pa[idx], m), m.q);
-        };
-        ntt_fwd<C>(sm, m, ld, st);
-    }
-}
-
-// ---- decrypt, device half: out[c][i] = INTT(c0 + c1 s)
-template <class C>
-__global__ void __launch_bounds__(C::T, C::MINB)
-k_decrypt(const uint64_t* __restrict__ ct, int l, const uint64_t* __restrict__ s_hat, uint64_t* __restrict__ out,
-          const ModInfo* __restrict__ mods) {
-    extern __shared__ uint64_t sm[];
-    const int i = C::bx();
-    const int64_t c = blockIdx.y;
-    const ModInfo m = mods[i];
-    const uint64_t* c0 = ct + limb_off(c, 0, i, l + 1, C::LOGN);
-    const uint64_t* c1 = ct + limb_off(c, 1, i, l + 1, C::LOGN);
-    const uint64_t* s = s_hat + ((size_t)i << C::LOGN);
-    uint64_t* dst = out + (((size_t)c * (l + 1) + i) << C::LOGN);
-    auto ld = [&](int idx) { return addmod(c0[idx], mulmod(c1[idx], s[idx], m), m.q); };
-    auto st = [&](int idx, uint64_t v) { dst[idx] = v; };
-    ntt_inv<C>(sm, m, ld, st);
-}
 
 __global__ void k_philox_words(uint64_t seed, const uint32_t* __restrict__ ctr, int64_t n, uint32_t* __restrict__ out) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -188,28 +16,16 @@ __global__ void k_philox_words(uint64_t seed, const uint32_t* __restrict__ ctr, 
 
 void launch_keygen(const Dev& d, uint64_t seed, uint64_t* s_hat, uint64_t* pk, uint64_t* rlk, uint64_t* rlk_s,
                    uint64_t* /*scratch*/) {
-    EDL_DISPATCH_LOGN(d.logn, {
-        using C = CfgFused<LOGN>;
-        launch_cfg<C>(d, "k_keygen_s", k_keygen_s<C>, dim3(d.L + 2), seed, s_hat, d.mods);
-        launch_cfg<C>(d, "k_keygen_pk", k_keygen_pk<C>, dim3(d.L + 1), seed, d.L, (const uint64_t*)s_hat, pk, d.mods);
-        launch_cfg<C>(d, "k_keygen_rlk", k_keygen_rlk<C>, dim3(d.L + 2, d.L + 1), seed, d.L, (const uint64_t*)s_hat, rlk,
-                      rlk_s, d.mods, d.cc);
-    });
+    EDL_DISPATCH_LOGN(d.logn, launch_keygen_n<LOGN>(d, seed, s_hat, pk, rlk, rlk_s));
 }
 
 void launch_encrypt(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint64_t seed, uint32_t obj0,
                     const uint64_t* pk, uint64_t* out) {
-    EDL_DISPATCH_LOGN(d.logn, {
-        using C = CfgFused<LOGN>;
-        launch_cfg<C>(d, "k_encrypt", k_encrypt<C>, dim3(l + 1, (unsigned)cnt), msg, l, d.L, seed, obj0, pk, out, d.mods);
-    });
+    EDL_DISPATCH_LOGN(d.logn, launch_encrypt_n<LOGN>(d, msg, cnt, l, seed, obj0, pk, out));
 }
 
 void launch_decrypt(const Dev& d, const uint64_t* ct, int64_t cnt, int l, const uint64_t* s_hat, uint64_t* out) {
-    EDL_DISPATCH_LOGN(d.logn, {
-        using C = CfgFused<LOGN>;
-        launch_cfg<C>(d, "k_decrypt", k_decrypt<C>, dim3(l + 1, (unsigned)cnt), ct, l, s_hat, out, d.mods);
-    });
+    EDL_DISPATCH_LOGN(d.logn, launch_decrypt_n<LOGN>(d, ct, cnt, l, s_hat, out));
 }
 
 void launch_philox_words(const Dev& d, uint64_t seed, const uint32_t* ctr, int64_t n, uint32_t* out) {
