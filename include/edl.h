@@ -179,6 +179,13 @@ edl_status edl_philox(edl_ctx* ctx, uint64_t seed, const uint32_t* ctr_host, int
 /* Integer-pipe ceiling: lazy Shoup 64-bit modular multiplications per second measured
  * by a register-only kernel on all SMs (the "alu" roofline peak). */
 edl_status edl_modmul_peak(edl_ctx* ctx, int32_t iters, double* modmul_per_s);
+
+/* Butterfly ceiling of the NTT's arithmetic for modulus `prime_index` (0..L data primes,
+ * L+1 = P): a register-only kernel of independent Harvey Cooley-Tukey butterflies
+ * on every SM, through the same twiddle-product path the NTT kernels
+ * take for that modulus (FP64 quotient if q < 2^50, Shoup otherwise).  Writes butterflies
+ * per second to *bfly_per_s.  Synchronises.  EDL_ERR_ARG on a bad index or iters <= 0. */
+edl_status edl_bfly_peak(edl_ctx* ctx, int32_t prime_index, int32_t iters, double* bfly_per_s);
 /* Copy the secret key s_hat [L+2][N], public key [2][L+1][N] or rlk [L+1][2][L+2][N]
  * to host (which: 0, 1, 2).  For parity tests. */
 edl_status edl_export_key(edl_ctx* ctx, int32_t which, uint64_t* host_out, size_t words);

@@ -776,6 +776,30 @@ edl_status edl_philox(edl_ctx* c, uint64_t seed, const uint32_t* ctr, int64_t n,
     return cuda_check(c, "philox");
 }
 
+edl_status edl_bfly_peak(edl_ctx* c, int32_t prime_index, int32_t iters, double* bfly_per_s) {
+    if (!c || !bfly_per_s || iters <= 0 || prime_index < 0 || prime_index > c->L + 1) return EDL_ERR_ARG;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    const int blocks = sms * 8;
+    uint64_t* sink = scratch(c, 1);
+    if (!sink) return fail(c, EDL_ERR_CUDA, "bfly_peak: scratch");
+    const ModInfo& m = c->h_mods[prime_index];
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    launch_bfly_peak(c->dev(), m.q, m.fp != 0, m.tw_fwd + 1, iters, blocks, sink);   // warm-up
+    cudaEventRecord(a, c->st);
+    launch_bfly_peak(c->dev(), m.q, m.fp != 0, m.tw_fwd + 1, iters, blocks, sink);
+    cudaEventRecord(b, c->st);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *bfly_per_s = (double)blocks * 256.0 * 8.0 * (double)iters / (ms * 1e-3);
+    return cuda_check(c, "bfly_peak");
+}
+
 edl_status edl_modmul_peak(edl_ctx* c, int32_t iters, double* modmul_per_s) {
     if (!c || !modmul_per_s || iters <= 0) return EDL_ERR_ARG;
     int sms = 0;

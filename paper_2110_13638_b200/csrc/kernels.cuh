@@ -176,6 +176,7 @@ void launch_encrypt(const Dev& d, const int64_t* msg /*[cnt][N]*/, int64_t cnt, 
 void launch_decrypt(const Dev& d, const uint64_t* ct, int64_t cnt, int l, const uint64_t* s_hat, uint64_t* out);
 void launch_philox_words(const Dev& d, uint64_t seed, const uint32_t* ctr /*[n][4]*/, int64_t n, uint32_t* out);
 
+void launch_bfly_peak(const Dev& d, uint64_t q, bool fp, const ulonglong2* tw, int iters, int blocks, uint64_t* sink);
 void launch_modmul_peak(const Dev& d, uint64_t q, uint64_t w, uint64_t ws, int iters, int blocks, uint64_t* sink);
 
 bool set_smem_attrs(int logn);

@@ -17,6 +17,8 @@ k_ntt_limbs(uint64_t* __restrict__ data, int nl, const __grid_constant__ PrimeMa
     extern __shared__ uint64_t sm[];
     const int limb = blockIdx.y;    // limb-major grid: co-resident CTAs share a prime (code path, twiddles)
     uint64_t* p = data + (((size_t)C::bx() * nl + limb) << C::LOGN);
+    if (threadIdx.x == 0)
+        pf_next_wave<C>([&](int64_t bx, int cr, int y, int) { pf_sub<C>(data + (((size_t)bx * nl + y) << C::LOGN), cr, !INV); });
     const ModInfo& m = mods[pm.idx[limb]];
     auto ld = [&](int idx) { return p[idx]; };
     auto st = [&](int idx, uint64_t v) { p[idx] = v; };
@@ -40,6 +42,8 @@ k_rescale_intt(const uint64_t* __restrict__ in, int l, const ulonglong2* __restr
     uint64_t* dst = r_out + (((size_t)c * 2 + p) << C::LOGN);
     uint64_t* dst2 = r_out2 ? r_out2 + (((size_t)c * 2 + p) << C::LOGN) : nullptr;
     const ModInfo& m = mods[l];
+    if (threadIdx.x == 0)
+        pf_next_wave<C>([&](int64_t bx, int cr, int y, int) { pf_sub<C>(in + limb_off(bx, y, l, l + 1, C::LOGN), cr, false); });
     if (w2 == nullptr) {
         const bool has_w = (w != nullptr);
         ulonglong2 wl = has_w ? w[c * (l + 1) + l] : make_ulonglong2(1, 0);
@@ -76,6 +80,10 @@ k_rescale_ntt(const uint64_t* __restrict__ in, int l, const ulonglong2* __restri
     const bool has_w = (w != nullptr);
     const ulonglong2 wi = has_w ? w[c * (l + 1) + i] : make_ulonglong2(1, 0);
     const uint64_t b = (bias != nullptr && p == 0) ? bias[c * l + i] : 0;
+    if (threadIdx.x == 0) {
+        pf_own<C>(src);
+        pf_next_wave<C>([&](int64_t bx, int cr, int y, int) { pf_sub<C>(r + (((size_t)bx * 2 + y) << C::LOGN), cr, true); });
+    }
     auto ld = [&](int idx) { return center_mod(rr[idx], ql, ql_mod, m); };
     auto st = [&](int idx, uint64_t x) {
         uint64_t a = src[idx];
@@ -122,6 +130,11 @@ k_relin_intt_d2(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, 
     const uint64_t* a1 = a + limb_off(c, 1, j, l + 1, C::LOGN);
     const uint64_t* b1 = b + limb_off(c, 1, j, l + 1, C::LOGN);
     uint64_t* dst = acoef + (((size_t)c * (l + 1) + j) << C::LOGN);
+    if (threadIdx.x == 0)
+        pf_next_wave<C>([&](int64_t bx, int cr, int y, int) {
+            pf_sub<C>(a + limb_off(bx, 1, y, l + 1, C::LOGN), cr, false);
+            if (b != a) pf_sub<C>(b + limb_off(bx, 1, y, l + 1, C::LOGN), cr, false);
+        });
     auto ld = [&](int idx) { return mulmod(a1[idx], b1[idx], m); };
     auto st = [&](int idx, uint64_t v) { dst[idx] = v; };
     ntt_inv<C>(sm, m, ld, st);
@@ -143,6 +156,10 @@ k_relin_modup(const uint64_t* __restrict__ acoef, int l, int L, uint64_t* __rest
     const uint64_t* src = acoef + (((size_t)c * (l + 1) + j) << C::LOGN);
     uint64_t* dst = xh + ((((size_t)c * (l + 1) + j) * (l + 2) + ti) << C::LOGN);
     const bool need_red = mods[j].q > 4 * m.q;   // the forward NTT accepts [0, 4q)
+    if (threadIdx.x == 0)
+        pf_next_wave<C>([&](int64_t bx, int cr, int y, int) {
+            pf_sub<C>(acoef + (((size_t)bx * (l + 1) + y / (l + 1)) << C::LOGN), cr, true);
+        });
     auto ld = [&](int idx) {
         uint64_t v = src[idx];
         return need_red ? reduce64(v, m) : v;
@@ -163,6 +180,18 @@ k_relin_moddown_intt(const uint64_t* __restrict__ a, const uint64_t* __restrict_
     const ModInfo& mp = mods[L + 1];
     const uint64_t* accP = acc + ((((size_t)c * 2 + cp) * (l + 2) + (l + 1)) << C::LOGN);
     uint64_t* rdst = r_out + (((size_t)c * 2 + cp) << C::LOGN);
+    if (threadIdx.x == 0) {
+        if (rescale) {   // the second transform's prologue operands (limb l)
+            pf_own<C>(a + limb_off(c, 0, l, l + 1, C::LOGN));
+            pf_own<C>(b + limb_off(c, 1, l, l + 1, C::LOGN));
+            if (b != a) pf_own<C>(b + limb_off(c, 0, l, l + 1, C::LOGN));
+            if (cp == 1 && b != a) pf_own<C>(a + limb_off(c, 1, l, l + 1, C::LOGN));
+            pf_own<C>(acc + ((((size_t)c * 2 + cp) * (l + 2) + l) << C::LOGN));
+        }
+        pf_next_wave<C>([&](int64_t bx, int cr, int y, int) {
+            pf_sub<C>(acc + ((((size_t)bx * 2 + y) * (l + 2) + (l + 1)) << C::LOGN), cr, false);
+        });
+    }
     {
         auto ld = [&](int idx) { return accP[idx]; };
         auto st = [&](int idx, uint64_t v) { rdst[idx] = v; };
@@ -203,6 +232,17 @@ k_relin_moddown_ntt(const uint64_t* __restrict__ a, const uint64_t* __restrict__
     const uint64_t* acci = acc + ((((size_t)c * 2 + cp) * (l + 2) + i) << C::LOGN);
     const int nlo = rescale ? l : l + 1;
     uint64_t* dst = out + limb_off(c, cp, i, nlo, C::LOGN);
+    if (threadIdx.x == 0) {   // epilogue operands of this CTA, prologue inputs of the next wave
+        pf_own<C>(a + limb_off(c, 0, i, l + 1, C::LOGN));
+        pf_own<C>(b + limb_off(c, 1, i, l + 1, C::LOGN));
+        if (b != a) pf_own<C>(b + limb_off(c, 0, i, l + 1, C::LOGN));
+        if (cp == 1 && b != a) pf_own<C>(a + limb_off(c, 1, i, l + 1, C::LOGN));
+        pf_own<C>(acci);
+        pf_next_wave<C>([&](int64_t bx, int cr, int y, int) {
+            pf_sub<C>(r + (((size_t)bx * 2 + y) << C::LOGN), cr, true);
+            if (rescale) pf_sub<C>(s + (((size_t)bx * 2 + y) << C::LOGN), cr, true);
+        });
+    }
     if (rescale) {
         const uint64_t ql = mods[l].q;
         const uint64_t qlmod = cc->qmod[l][i];

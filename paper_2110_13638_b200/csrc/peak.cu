@@ -21,6 +21,48 @@ __global__ void __launch_bounds__(256) k_modmul_peak(uint64_t q, uint64_t w, uin
     if (acc == 0x123456789ull) sink[0] = acc;   // keep the chains alive
 }
 
+// Register-only Harvey CT butterflies (the NTT's inner operation, ntt_core.cuh) on 16
+// residues per thread: 8 independent butterflies per round, twiddles held in registers, so
+// the kernel measures the butterfly issue ceiling of one arithmetic path (FP64-quotient
+// for q < 2^50, Shoup otherwise) with no memory traffic.  The "alu" roofline of the NTT
+// kernels (bench.py) is this rate for their mix of primes.
+template <bool FP>
+__global__ void __launch_bounds__(256) k_bfly_peak(uint64_t q, const ulonglong2* __restrict__ tw, int iters,
+                                                   uint64_t* sink) {
+    uint64_t x[16];
+    ulonglong2 w[8];
+#pragma unroll
+    for (int k = 0; k < 16; k++) x[k] = (threadIdx.x * 16 + k + 1) % q;
+#pragma unroll
+    for (int k = 0; k < 8; k++) w[k] = tw[k];
+    const uint64_t two_q = 2 * q;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            uint64_t X = x[k], Y = x[k + 8];
+            const uint64_t xx = csub(X, two_q);
+            const uint64_t t = tw_mul<FP>(Y, w[k].x, w[k].y, q);
+            x[k] = xx + t;
+            x[k + 8] = xx - t + two_q;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; k++) {   // pair different lanes next round
+            const uint64_t tmp = x[k];
+            x[k] = x[(k + 3) & 15];
+            x[(k + 3) & 15] = tmp;
+        }
+    }
+    uint64_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < 16; k++) acc ^= x[k];
+    if (acc == 0x123456789ull) sink[0] = acc;
+}
+
+void launch_bfly_peak(const Dev& d, uint64_t q, bool fp, const ulonglong2* tw, int iters, int blocks, uint64_t* sink) {
+    if (fp) EDL_LAUNCH(d, "k_bfly_peak", k_bfly_peak<true><<<blocks, 256, 0, d.st>>>(q, tw, iters, sink));
+    else EDL_LAUNCH(d, "k_bfly_peak", k_bfly_peak<false><<<blocks, 256, 0, d.st>>>(q, tw, iters, sink));
+}
+
 void launch_modmul_peak(const Dev& d, uint64_t q, uint64_t w, uint64_t ws, int iters, int blocks, uint64_t* sink) {
     EDL_LAUNCH(d, "k_modmul_peak", k_modmul_peak<<<blocks, 256, 0, d.st>>>(q, w, ws, iters, sink));
 }

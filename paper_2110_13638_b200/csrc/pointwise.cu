@@ -381,79 +381,87 @@ __global__ void k_dense_combine(const uint64_t* __restrict__ part, int ks, int64
 
 // ---------------------------------------------------------------- key inner product (M2b)
 // acc_{c,t} = sum_{j<=l} x_{j,t} rlk_j[c][t] mod q_t with x_{j,t} = xh_{j,t} (raised digit)
-// or, for t == j, d2_j = a1_j b1_j.  Two coefficients per thread (16-byte accesses); both
-// components share the digit loads; 128-bit lazy sums (l+1 < 2^8 terms of < 2^122), one
-// Barrett reduction per output (O4).
+// or, for t == j, d2_j = a1_j b1_j.  A thread owns two coefficients (16-byte accesses) of
+// MAC_CB ciphertexts, so each key residue fetched from L2 serves MAC_CB ciphertexts and
+// both components share the digit loads.  FP64-quotient limbs: lazy [0, 2q) products
+// summed in 64 bits; others: 128-bit lazy sums; one reduction per output (O4).
+constexpr int MAC_CB = 4;
+
 __global__ void __launch_bounds__(PW_THREADS)
-k_relin_mac(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l, int L,
+k_relin_mac(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l, int L, int64_t cnt,
             const uint64_t* __restrict__ xh, const uint64_t* __restrict__ rlk, const uint64_t* __restrict__ rlk_c,
             uint64_t* __restrict__ acc, const ModInfo* __restrict__ mods, int logn) {
     const int ti = blockIdx.y;                 // 0..l data targets, l+1 = P
-    const int64_t c = blockIdx.z;
+    const int64_t c0 = (int64_t)blockIdx.z * MAC_CB;
     const int t = (ti == l + 1) ? (L + 1) : ti;
     const ModInfo& m = mods[t];
     const bool fp = m.fp != 0;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;   // coefficient pair
     if (2 * k >= (1 << logn)) return;
-    U128 s[2][2];
+    U128 s[MAC_CB][2][2];
 #pragma unroll
-    for (int cc = 0; cc < 2; cc++) s[cc][0].lo = s[cc][0].hi = s[cc][1].lo = s[cc][1].hi = 0;
-    // digits in groups of MAC_G with every load of a group issued before its MACs
-    constexpr int MAC_G = 4;
-    for (int j0 = 0; j0 <= l; j0 += MAC_G) {
-        ulonglong2 x[MAC_G], r0[MAC_G], r1[MAC_G], c0[MAC_G], c1[MAC_G];
+    for (int e = 0; e < MAC_CB; e++)
 #pragma unroll
-        for (int u = 0; u < MAC_G; u++) {
-            const int j = j0 + u;
-            if (j > l) break;
+        for (int cc = 0; cc < 2; cc++) s[e][cc][0].lo = s[e][cc][0].hi = s[e][cc][1].lo = s[e][cc][1].hi = 0;
+    for (int j = 0; j <= l; j++) {
+        const size_t o0 = (((size_t)j * 2 + 0) * (L + 2) + t) << logn, o1 = (((size_t)j * 2 + 1) * (L + 2) + t) << logn;
+        const ulonglong2 r0 = __ldg(v2(rlk + o0) + k), r1 = __ldg(v2(rlk + o1) + k);
+        ulonglong2 q0 = make_ulonglong2(0, 0), q1 = q0;
+        if (fp) {
+            q0 = __ldg(v2(rlk_c + o0) + k);
+            q1 = __ldg(v2(rlk_c + o1) + k);
+        }
+        ulonglong2 x[MAC_CB];
+#pragma unroll
+        for (int e = 0; e < MAC_CB; e++) {
+            const int64_t c = c0 + e;
+            x[e] = make_ulonglong2(0, 0);
+            if (c >= cnt) continue;
             if (j == ti) {
                 const ulonglong2 a1 = v2(a + limb_off(c, 1, j, l + 1, logn))[k];
                 const ulonglong2 b1 = v2(b + limb_off(c, 1, j, l + 1, logn))[k];
-                x[u] = make_ulonglong2(mulmod(a1.x, b1.x, m), mulmod(a1.y, b1.y, m));
+                x[e] = make_ulonglong2(mulmod(a1.x, b1.x, m), mulmod(a1.y, b1.y, m));
             } else {
-                x[u] = v2(xh + ((((size_t)c * (l + 1) + j) * (l + 2) + ti) << logn))[k];
-            }
-            const size_t o0 = (((size_t)j * 2 + 0) * (L + 2) + t) << logn, o1 = (((size_t)j * 2 + 1) * (L + 2) + t) << logn;
-            r0[u] = __ldg(v2(rlk + o0) + k);
-            r1[u] = __ldg(v2(rlk + o1) + k);
-            if (fp) {
-                c0[u] = __ldg(v2(rlk_c + o0) + k);
-                c1[u] = __ldg(v2(rlk_c + o1) + k);
+                x[e] = v2(xh + ((((size_t)c * (l + 1) + j) * (l + 2) + ti) << logn))[k];
             }
         }
-        if (fp) {   // lazy [0, 2q) products, 64-bit sums ((l+1) * 2q < 2^60)
+        if (fp) {   // (l+1) * 2q < 2^60
 #pragma unroll
-            for (int u = 0; u < MAC_G; u++) {
-                if (j0 + u > l) break;
-                s[0][0].lo += tw_mul_fp(x[u].x, r0[u].x, c0[u].x, m.q);
-                s[0][1].lo += tw_mul_fp(x[u].y, r0[u].y, c0[u].y, m.q);
-                s[1][0].lo += tw_mul_fp(x[u].x, r1[u].x, c1[u].x, m.q);
-                s[1][1].lo += tw_mul_fp(x[u].y, r1[u].y, c1[u].y, m.q);
+            for (int e = 0; e < MAC_CB; e++) {
+                s[e][0][0].lo += tw_mul_fp(x[e].x, r0.x, q0.x, m.q);
+                s[e][0][1].lo += tw_mul_fp(x[e].y, r0.y, q0.y, m.q);
+                s[e][1][0].lo += tw_mul_fp(x[e].x, r1.x, q1.x, m.q);
+                s[e][1][1].lo += tw_mul_fp(x[e].y, r1.y, q1.y, m.q);
             }
         } else {
 #pragma unroll
-            for (int u = 0; u < MAC_G; u++) {
-                if (j0 + u > l) break;
-                mac128(s[0][0], x[u].x, r0[u].x);
-                mac128(s[0][1], x[u].y, r0[u].y);
-                mac128(s[1][0], x[u].x, r1[u].x);
-                mac128(s[1][1], x[u].y, r1[u].y);
+            for (int e = 0; e < MAC_CB; e++) {
+                mac128(s[e][0][0], x[e].x, r0.x);
+                mac128(s[e][0][1], x[e].y, r0.y);
+                mac128(s[e][1][0], x[e].x, r1.x);
+                mac128(s[e][1][1], x[e].y, r1.y);
             }
         }
     }
 #pragma unroll
-    for (int cc = 0; cc < 2; cc++)
-        v2(acc + ((((size_t)c * 2 + cc) * (l + 2) + ti) << logn))[k] =
-            fp ? make_ulonglong2(reduce64(s[cc][0].lo, m), reduce64(s[cc][1].lo, m))
-               : make_ulonglong2(barrett128(s[cc][0], m), barrett128(s[cc][1], m));
+    for (int e = 0; e < MAC_CB; e++) {
+        const int64_t c = c0 + e;
+        if (c >= cnt) continue;
+#pragma unroll
+        for (int cc = 0; cc < 2; cc++)
+            v2(acc + ((((size_t)c * 2 + cc) * (l + 2) + ti) << logn))[k] =
+                fp ? make_ulonglong2(reduce64(s[e][cc][0].lo, m), reduce64(s[e][cc][1].lo, m))
+                   : make_ulonglong2(barrett128(s[e][cc][0], m), barrett128(s[e][cc][1], m));
+    }
 }
 
 }  // namespace
 
 void launch_relin_mac(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t cnt, int l, const uint64_t* xh,
                       const uint64_t* rlk, const uint64_t* rlk_c, uint64_t* acc) {
-    dim3 grid((unsigned)((1 << d.logn) / (2 * PW_THREADS)), (unsigned)(l + 2), (unsigned)cnt);
-    EDL_LAUNCH(d, "k_relin_mac", k_relin_mac<<<grid, PW_THREADS, 0, d.st>>>(a, b, l, d.L, xh, rlk, rlk_c, acc, d.mods, d.logn));
+    dim3 grid((unsigned)((1 << d.logn) / (2 * PW_THREADS)), (unsigned)(l + 2), (unsigned)((cnt + MAC_CB - 1) / MAC_CB));
+    EDL_LAUNCH(d, "k_relin_mac", k_relin_mac<<<grid, PW_THREADS, 0, d.st>>>(a, b, l, d.L, cnt, xh, rlk, rlk_c, acc, d.mods,
+                                                                           d.logn));
 }
 
 void launch_add(const Dev& d, const uint64_t* a, int la, const uint64_t* b, int lb, int64_t cnt, int lo, uint64_t* out) {

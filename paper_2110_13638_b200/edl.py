@@ -135,6 +135,7 @@ _sigs = {
     "edl_philox": (_c.c_int32, [_c.c_void_p, _c.c_uint64, _c.c_void_p, _c.c_int64, _c.c_void_p]),
     "edl_export_key": (_c.c_int32, [_c.c_void_p, _c.c_int32, _c.c_void_p, _c.c_size_t]),
     "edl_modmul_peak": (_c.c_int32, [_c.c_void_p, _c.c_int32, _P(_c.c_double)]),
+    "edl_bfly_peak": (_c.c_int32, [_c.c_void_p, _c.c_int32, _c.c_int32, _P(_c.c_double)]),
 }
 for _name, (_res, _args) in _sigs.items():
     _f = getattr(_lib, _name)
@@ -415,6 +416,12 @@ class Context:
     def modmul_peak(self, iters: int = 20000) -> float:
         v = ctypes.c_double()
         self._check(_lib.edl_modmul_peak(self._h, iters, ctypes.byref(v)), "modmul_peak")
+        return float(v.value)
+
+    def bfly_peak(self, prime_index: int, iters: int = 20000) -> float:
+        """Register-only NTT butterflies/s through modulus `prime_index`'s arithmetic path."""
+        v = ctypes.c_double()
+        self._check(_lib.edl_bfly_peak(self._h, prime_index, iters, ctypes.byref(v)), "bfly_peak")
         return float(v.value)
 
     def export_key(self, which: int) -> np.ndarray:
