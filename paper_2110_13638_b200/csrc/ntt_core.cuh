@@ -343,15 +343,17 @@ __device__ __forceinline__ void ntt_inv(uint64_t* sm, const ModInfo& m, Load loa
 // ---- per-N configurations -------------------------------------------------------------
 // M = N/K <= 2^13 per CTA.  Plain transforms keep E = 32 residues per thread (fewer
 // exchanges); fused kernels, whose prologue/epilogue need registers, pick their own E.
-// Round-2 measurements (tools/ntt_bench.py, B200): at N = 2^14 the plain transform is
-// 6 % faster as a 2-CTA cluster (5.0 vs 4.7 M limbs/s) while the fused kernels are 15-30 %
-// slower (their prologue/epilogue traffic per CTA doubles relative to the butterflies),
-// so plain and fused configs choose K separately.
+// Measured on B200 (tools/ntt_bench.py, C1 step): the plain transform at N = 2^14 is 6 %
+// faster as a 2-CTA cluster (5.0 vs 4.7 M limbs/s); the fused kernels are fastest as
+// 2-CTA clusters of 512 threads x 16 residues with two CTAs per SM (64 registers, 32 warps
+// per SM): 6.76 ms/step vs 6.92 (one 1024-thread CTA per limb), 7.50 (128 registers, one
+// CTA per SM) and 8.87 (512 threads x 32 residues).  Latency hiding needs the warps more
+// than the spill-free register budget.
 #ifndef EDL_K14_PLAIN
 #define EDL_K14_PLAIN 2
 #endif
 #ifndef EDL_K14_FUSED
-#define EDL_K14_FUSED 1
+#define EDL_K14_FUSED 2
 #endif
 #ifndef EDL_LOGE_P14
 #define EDL_LOGE_P14 5
@@ -360,7 +362,7 @@ __device__ __forceinline__ void ntt_inv(uint64_t* sm, const ModInfo& m, Load loa
 #define EDL_LOGE_F14 4
 #endif
 #ifndef EDL_LOGE_F13
-#define EDL_LOGE_F13 5
+#define EDL_LOGE_F13 4
 #endif
 
 __host__ __device__ constexpr int cfg_logk(int logn, bool plain) {
@@ -372,11 +374,18 @@ __host__ __device__ constexpr int cfg_loge(int logn, bool plain) {
                                        : (cfg_logm(logn, plain) >= 12 ? (plain ? 5 : EDL_LOGE_F13)
                                                                       : (cfg_logm(logn, plain) >= 10 ? 4 : 3));
 }
-// blocks per SM for __launch_bounds__: as many CTAs as leave 128 registers per thread
-// (2^14 residues per CTA need 136 KiB of shared memory: one CTA)
+// blocks per SM for __launch_bounds__.  Plain transforms: as many CTAs as leave 128
+// registers per thread.  Fused kernels: 1024 threads per SM (64 registers), at most 4 CTAs.
+// A whole 2^14 limb per CTA (136 KiB of shared memory) always runs one CTA.
 __host__ __device__ constexpr int cfg_minb(int logm, int loge) {
     return logm == 14 ? 1
                       : ((65536 >> (logm - loge + 7)) < 1 ? 1 : ((65536 >> (logm - loge + 7)) > 3 ? 3 : (65536 >> (logm - loge + 7))));
+}
+// (8-CTA clusters, N = 2^16, keep 128 registers and one CTA per SM: with 64 registers the
+// keygen kernels died with illegal-instruction / illegal-address errors on B200.)
+__host__ __device__ constexpr int cfg_minb_fused(int logm, int loge, int logk = 0) {
+    return (logm == 14 || logk >= 3) ? 1
+                                     : ((1024 >> (logm - loge)) < 1 ? 1 : ((1024 >> (logm - loge)) > 4 ? 4 : (1024 >> (logm - loge))));
 }
 
 #ifndef EDL_MINB_F
@@ -384,9 +393,11 @@ __host__ __device__ constexpr int cfg_minb(int logm, int loge) {
 #endif
 template <int LOGN, bool PLAIN>
 using CfgOf = NttCfg<LOGN, cfg_logk(LOGN, PLAIN), cfg_loge(LOGN, PLAIN),
-                     (!PLAIN && EDL_MINB_F > 0) ? EDL_MINB_F : cfg_minb(cfg_logm(LOGN, PLAIN), cfg_loge(LOGN, PLAIN))>;
+                     PLAIN ? cfg_minb(cfg_logm(LOGN, PLAIN), cfg_loge(LOGN, PLAIN))
+                           : (EDL_MINB_F > 0 ? EDL_MINB_F
+                                             : cfg_minb_fused(cfg_logm(LOGN, PLAIN), cfg_loge(LOGN, PLAIN), cfg_logk(LOGN, PLAIN)))>;
 template <int LOGN, int LOGE>   // fused config with an explicit residues-per-thread
-using CfgFusedE = NttCfg<LOGN, cfg_logk(LOGN, false), LOGE, cfg_minb(cfg_logm(LOGN, false), LOGE)>;
+using CfgFusedE = NttCfg<LOGN, cfg_logk(LOGN, false), LOGE, cfg_minb_fused(cfg_logm(LOGN, false), LOGE, cfg_logk(LOGN, false))>;
 #ifndef EDL_LOGE_KS14
 #define EDL_LOGE_KS14 EDL_LOGE_F14
 #endif

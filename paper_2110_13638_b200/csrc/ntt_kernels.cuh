@@ -99,26 +99,15 @@ k_rescale_ntt(const uint64_t* __restrict__ in, int l, const ulonglong2* __restri
 //   M1 acoef_j = INTT_{q_j}(a1_j b1_j)                                   [cnt][l+1]
 //   M2a xh_{j,t} = NTT_t(acoef_j mod t), t != q_j                        [cnt][l+1][l+2]
 //   M2b acc_{c,t} = sum_j xh_{j,t} * rlk_j[c][t]  (t = q_0..q_l, P; the t == q_j term
-//      uses d2_j = a1_j b1_j directly), 128-bit lazy sums, one Barrett     [cnt][2][l+2]
+//      uses d2_j = a1_j b1_j directly); for data limbs the same pass stores
+//      v_{c,i} = d_{c,i} + acc_{c,i} P^-1 (the tensor's d0, d1 folded in)  [cnt][2][l+2]
 //   M3 r_c = INTT_P(acc_{c,P}); if rescaling also
-//      s_c = INTT_{q_l}(d_c,l + acc_{c,l} P^-1) - [r_c]_{q_l} P^-1  (= INTT of the
-//      relinearised limb l, by linearity)                                 [cnt][2]
-//   M4 out_{c,i} = d_c,i + (acc_{c,i} - NTT_i([r_c]_{q_i})) P^-1                 (no rescale)
-//      out_{c,i} = (d_c,i + acc_{c,i} P^-1 - NTT_i([r_c]_{q_i} P^-1 + [s_c]_{q_i})) q_l^-1
+//      s_c = INTT_{q_l}(v_{c,l}) - [r_c]_{q_l} P^-1  (= INTT of the relinearised limb l,
+//      by linearity)                                                       [cnt][2]
+//   M4 out_{c,i} = v_{c,i} - NTT_i([r_c]_{q_i} P^-1)                         (no rescale)
+//      out_{c,i} = (v_{c,i} - NTT_i([r_c]_{q_i} P^-1 + [s_c]_{q_i})) q_l^-1
 //      which is bit-identical to mod-down followed by O12 rescale (all steps are exact
 //      Z_q-linear maps of the same centered lifts).
-__device__ __forceinline__ uint64_t tensor_comp(const uint64_t* a, const uint64_t* b, int64_t c, int cp, int i,
-                                                int nl, int logn, int idx, const ModInfo& m) {
-    const uint64_t a0 = a[limb_off(c, 0, i, nl, logn) + idx];
-    const uint64_t b1 = b[limb_off(c, 1, i, nl, logn) + idx];
-    const uint64_t b0 = b[limb_off(c, 0, i, nl, logn) + idx];
-    if (cp == 0) return mulmod(a0, b0, m);
-    const uint64_t a1 = a[limb_off(c, 1, i, nl, logn) + idx];
-    U128 s = mul_wide(a0, b1);
-    mac128(s, a1, b0);
-    return barrett128(s, m);
-}
-
 template <class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
 k_relin_intt_d2(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l,
@@ -181,13 +170,7 @@ k_relin_moddown_intt(const uint64_t* __restrict__ a, const uint64_t* __restrict_
     const uint64_t* accP = acc + ((((size_t)c * 2 + cp) * (l + 2) + (l + 1)) << C::LOGN);
     uint64_t* rdst = r_out + (((size_t)c * 2 + cp) << C::LOGN);
     if (threadIdx.x == 0) {
-        if (rescale) {   // the second transform's prologue operands (limb l)
-            pf_own<C>(a + limb_off(c, 0, l, l + 1, C::LOGN));
-            pf_own<C>(b + limb_off(c, 1, l, l + 1, C::LOGN));
-            if (b != a) pf_own<C>(b + limb_off(c, 0, l, l + 1, C::LOGN));
-            if (cp == 1 && b != a) pf_own<C>(a + limb_off(c, 1, l, l + 1, C::LOGN));
-            pf_own<C>(acc + ((((size_t)c * 2 + cp) * (l + 2) + l) << C::LOGN));
-        }
+        if (rescale) pf_own<C>(acc + ((((size_t)c * 2 + cp) * (l + 2) + l) << C::LOGN));
         pf_next_wave<C>([&](int64_t bx, int cr, int y, int) {
             pf_sub<C>(acc + ((((size_t)bx * 2 + y) * (l + 2) + (l + 1)) << C::LOGN), cr, false);
         });
@@ -201,12 +184,9 @@ k_relin_moddown_intt(const uint64_t* __restrict__ a, const uint64_t* __restrict_
     const ModInfo& ml = mods[l];
     const ulonglong2 pinv = cc->qinv[L + 1][l];
     const uint64_t pmod = cc->qmod[L + 1][l];
-    const uint64_t* accl = acc + ((((size_t)c * 2 + cp) * (l + 2) + l) << C::LOGN);
+    const uint64_t* vl = acc + ((((size_t)c * 2 + cp) * (l + 2) + l) << C::LOGN);   // d_l + acc_l P^-1 (M2b)
     uint64_t* sdst = s_out + (((size_t)c * 2 + cp) << C::LOGN);
-    auto ld = [&](int idx) {
-        uint64_t d = tensor_comp(a, b, c, cp, l, l + 1, C::LOGN, idx, ml);
-        return addmod(d, mulc(accl[idx], pinv, ml), ml.q);
-    };
+    auto ld = [&](int idx) { return vl[idx]; };
     auto st = [&](int idx, uint64_t y) {
         uint64_t z = mulc(center_mod(rdst[idx], mp.q, pmod, ml), pinv, ml);
         sdst[idx] = submod(y, z, ml.q);
@@ -229,15 +209,11 @@ k_relin_moddown_ntt(const uint64_t* __restrict__ a, const uint64_t* __restrict__
     const ulonglong2 pinv = cc->qinv[L + 1][i];
     const uint64_t* rr = r + (((size_t)c * 2 + cp) << C::LOGN);
     const uint64_t* ss = s + (((size_t)c * 2 + cp) << C::LOGN);
-    const uint64_t* acci = acc + ((((size_t)c * 2 + cp) * (l + 2) + i) << C::LOGN);
+    const uint64_t* vi = acc + ((((size_t)c * 2 + cp) * (l + 2) + i) << C::LOGN);   // d_i + acc_i P^-1 (M2b)
     const int nlo = rescale ? l : l + 1;
     uint64_t* dst = out + limb_off(c, cp, i, nlo, C::LOGN);
-    if (threadIdx.x == 0) {   // epilogue operands of this CTA, prologue inputs of the next wave
-        pf_own<C>(a + limb_off(c, 0, i, l + 1, C::LOGN));
-        pf_own<C>(b + limb_off(c, 1, i, l + 1, C::LOGN));
-        if (b != a) pf_own<C>(b + limb_off(c, 0, i, l + 1, C::LOGN));
-        if (cp == 1 && b != a) pf_own<C>(a + limb_off(c, 1, i, l + 1, C::LOGN));
-        pf_own<C>(acci);
+    if (threadIdx.x == 0) {   // epilogue operand of this CTA, prologue inputs of the next wave
+        pf_own<C>(vi);
         pf_next_wave<C>([&](int64_t bx, int cr, int y, int) {
             pf_sub<C>(r + (((size_t)bx * 2 + y) << C::LOGN), cr, true);
             if (rescale) pf_sub<C>(s + (((size_t)bx * 2 + y) << C::LOGN), cr, true);
@@ -251,26 +227,16 @@ k_relin_moddown_ntt(const uint64_t* __restrict__ a, const uint64_t* __restrict__
             uint64_t u = mulc(center_mod(rr[idx], P, pmod, m), pinv, m);
             return addmod(u, center_mod(ss[idx], ql, qlmod, m), m.q);
         };
-        auto st = [&](int idx, uint64_t x) {
-            uint64_t d = tensor_comp(a, b, c, cp, i, l + 1, C::LOGN, idx, m);
-            uint64_t v = addmod(d, mulc(acci[idx], pinv, m), m.q);
-            dst[idx] = mulc(submod(v, x, m.q), qlinv, m);
-        };
+        auto st = [&](int idx, uint64_t x) { dst[idx] = mulc(submod(vi[idx], x, m.q), qlinv, m); };
         ntt_fwd<C>(sm, m, ld, st);
     } else {
-        auto ld = [&](int idx) { return center_mod(rr[idx], P, pmod, m); };
-        auto st = [&](int idx, uint64_t x) {
-            uint64_t d = tensor_comp(a, b, c, cp, i, l + 1, C::LOGN, idx, m);
-            dst[idx] = addmod(d, mulc(submod(acci[idx], x, m.q), pinv, m), m.q);
-        };
+        // out = d + (acc - NTT([r])) P^-1 = v - NTT([r] P^-1)  (Z_q-linear, exact)
+        auto ld = [&](int idx) { return mulc(center_mod(rr[idx], P, pmod, m), pinv, m); };
+        auto st = [&](int idx, uint64_t x) { dst[idx] = submod(vi[idx], x, m.q); };
         ntt_fwd<C>(sm, m, ld, st);
     }
 }
 
-// ------------------------------------------------------------------------------------
-// Per-N launchers (explicitly instantiated once per ring degree in ntt_inst_<logN>.cu so the
-// heavy template expansion compiles in parallel).  Grids are [limb-like x K, ...]: the K CTAs
-// of one limb form a cluster.
 template <int LOGN>
 void launch_ntt_limbs_n(const Dev& d, uint64_t* data, int64_t batch, int nl, const PrimeMap& pm, bool inverse) {
     using C = CfgPlain<LOGN>;
@@ -304,7 +270,7 @@ void launch_relin_n(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t 
     launch_cfg<C>(d, "k_relin_intt_d2", k_relin_intt_d2<C>, dim3((unsigned)cnt, l + 1), a, b, l, acoef, d.mods);
     launch_cfg<CP>(d, "k_relin_modup", k_relin_modup<CP>, dim3((unsigned)cnt, (l + 1) * (l + 1)), (const uint64_t*)acoef,
                    l, d.L, xh, d.mods);
-    launch_relin_mac(d, a, b, cnt, l, xh, rlk, rlk_c, acc);
+    launch_relin_mac(d, a, b, cnt, l, xh, rlk, rlk_c, acc);   // acc slots 0..l hold v
     launch_cfg<C>(d, "k_relin_moddown_intt", k_relin_moddown_intt<C>, dim3((unsigned)cnt, 2), a, b, l, (const uint64_t*)acc,
                   d.L, rs, r, s, d.mods, d.cc);
     launch_cfg<C>(d, "k_relin_moddown_ntt", k_relin_moddown_ntt<C>, dim3((unsigned)cnt, 2, rescale ? l : l + 1), a, b, l,

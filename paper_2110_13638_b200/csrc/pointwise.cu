@@ -390,7 +390,8 @@ constexpr int MAC_CB = 4;
 __global__ void __launch_bounds__(PW_THREADS)
 k_relin_mac(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l, int L, int64_t cnt,
             const uint64_t* __restrict__ xh, const uint64_t* __restrict__ rlk, const uint64_t* __restrict__ rlk_c,
-            uint64_t* __restrict__ acc, const ModInfo* __restrict__ mods, int logn) {
+            uint64_t* __restrict__ acc, const ModInfo* __restrict__ mods, const ChainConsts* __restrict__ chain,
+            int logn) {
     const int ti = blockIdx.y;                 // 0..l data targets, l+1 = P
     const int64_t c0 = (int64_t)blockIdx.z * MAC_CB;
     const int t = (ti == l + 1) ? (L + 1) : ti;
@@ -443,15 +444,28 @@ k_relin_mac(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int 
             }
         }
     }
+    // data limbs: fold the tensor's d0 = a0 b0, d1 = a0 b1 + a1 b0 in, v = d + acc P^-1
+    const ulonglong2 pinv = (ti <= l) ? chain->qinv[L + 1][t] : make_ulonglong2(0, 0);
 #pragma unroll
     for (int e = 0; e < MAC_CB; e++) {
         const int64_t c = c0 + e;
         if (c >= cnt) continue;
+        ulonglong2 v[2];
 #pragma unroll
         for (int cc = 0; cc < 2; cc++)
-            v2(acc + ((((size_t)c * 2 + cc) * (l + 2) + ti) << logn))[k] =
-                fp ? make_ulonglong2(reduce64(s[e][cc][0].lo, m), reduce64(s[e][cc][1].lo, m))
-                   : make_ulonglong2(barrett128(s[e][cc][0], m), barrett128(s[e][cc][1], m));
+            v[cc] = fp ? make_ulonglong2(reduce64(s[e][cc][0].lo, m), reduce64(s[e][cc][1].lo, m))
+                       : make_ulonglong2(barrett128(s[e][cc][0], m), barrett128(s[e][cc][1], m));
+        if (ti <= l) {
+            const ulonglong2 a0 = v2(a + limb_off(c, 0, ti, l + 1, logn))[k], a1 = v2(a + limb_off(c, 1, ti, l + 1, logn))[k];
+            const ulonglong2 b0 = v2(b + limb_off(c, 0, ti, l + 1, logn))[k], b1 = v2(b + limb_off(c, 1, ti, l + 1, logn))[k];
+            const uint64_t d0x = mulmod(a0.x, b0.x, m), d0y = mulmod(a0.y, b0.y, m);
+            const uint64_t d1x = addmod(mulmod(a0.x, b1.x, m), mulmod(a1.x, b0.x, m), m.q);
+            const uint64_t d1y = addmod(mulmod(a0.y, b1.y, m), mulmod(a1.y, b0.y, m), m.q);
+            v[0] = make_ulonglong2(addmod(d0x, mulc(v[0].x, pinv, m), m.q), addmod(d0y, mulc(v[0].y, pinv, m), m.q));
+            v[1] = make_ulonglong2(addmod(d1x, mulc(v[1].x, pinv, m), m.q), addmod(d1y, mulc(v[1].y, pinv, m), m.q));
+        }
+#pragma unroll
+        for (int cc = 0; cc < 2; cc++) v2(acc + ((((size_t)c * 2 + cc) * (l + 2) + ti) << logn))[k] = v[cc];
     }
 }
 
@@ -461,7 +475,7 @@ void launch_relin_mac(const Dev& d, const uint64_t* a, const uint64_t* b, int64_
                       const uint64_t* rlk, const uint64_t* rlk_c, uint64_t* acc) {
     dim3 grid((unsigned)((1 << d.logn) / (2 * PW_THREADS)), (unsigned)(l + 2), (unsigned)((cnt + MAC_CB - 1) / MAC_CB));
     EDL_LAUNCH(d, "k_relin_mac", k_relin_mac<<<grid, PW_THREADS, 0, d.st>>>(a, b, l, d.L, cnt, xh, rlk, rlk_c, acc, d.mods,
-                                                                           d.logn));
+                                                                           d.cc, d.logn));
 }
 
 void launch_add(const Dev& d, const uint64_t* a, int la, const uint64_t* b, int lb, int64_t cnt, int lo, uint64_t* out) {
