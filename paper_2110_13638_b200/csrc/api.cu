@@ -45,6 +45,7 @@ struct edl_ctx {
     Dev dev() const {
         Dev d;
         d.mods = d_mods;
+        d.hmods = h_mods.data();
         d.cc = d_cc;
         d.logn = logn;
         d.L = L;

@@ -41,7 +41,8 @@ struct Prof {
 };
 
 struct Dev {
-    const ModInfo* mods;        // [L+2]
+    const ModInfo* mods;        // [L+2] (device)
+    const ModInfo* hmods;       // [L+2] (host copy: launch-time decisions such as the arithmetic path)
     const ChainConsts* cc;
     int logn;
     int L;

@@ -79,7 +79,14 @@ __device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
 // Prefetch the CTA's own sub-block [crank*M, crank*M + M) of a limb starting at `limb`.
 template <class C>
 __device__ __forceinline__ void pf_own(const uint64_t* limb) {
+#ifdef EDL_L2_PREFETCH_OWN
+    if (limb)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(limb + ((size_t)C::crank() << C::LOGM)),
+                     "r"((uint32_t)C::M * 8u)
+                     : "memory");
+#else
     if (limb) l2_prefetch(limb + ((size_t)C::crank() << C::LOGM), (uint32_t)C::M * 8u);
+#endif
 }
 
 // Calls f(bx, crank, y, z) for the block that starts one wave (SMs x MINB CTAs) after this
@@ -235,8 +242,8 @@ __device__ __forceinline__ void inv_middle(uint64_t* sm, const ModInfo& m, uint6
 
 // Forward NTT of one limb.  load(idx) -> residue in [0, 4q); store(idx, v) receives
 // canonical values at idx = C::idx(r).
-template <class C, bool FP, class Load, class Store>
-__device__ __forceinline__ void ntt_fwd_impl(uint64_t* sm, const ModInfo& m, Load load, Store store) {
+template <class C, bool FP, class Load, class Pre, class Store>
+__device__ __forceinline__ void ntt_fwd_impl(uint64_t* sm, const ModInfo& m, Load load, Pre pre, Store store) {
     using P0 = PassInfo<C, 0>;
     static_assert(P0::G == 1 && P0::BLOW == C::LOGM - C::LOGE, "pass 0 layout");
     const uint64_t q = m.q, two_q = 2 * q;
@@ -270,19 +277,24 @@ __device__ __forceinline__ void ntt_fwd_impl(uint64_t* sm, const ModInfo& m, Loa
     for (int r = 0; r < C::E; r++) sm[spad(tid + r * C::T)] = x[r];
     __syncthreads();
     fwd_middle<C, 1, FP>(sm, m, two_q);
+    // epilogue operands first (all E loads in flight), then the outputs
+    using PT = decltype(pre(0));
+    PT pv[C::E];
+#pragma unroll
+    for (int r = 0; r < C::E; r++) pv[r] = pre(C::idx(r));
 #pragma unroll
     for (int r = 0; r < C::E; r++) {
         uint64_t v = sm[spad(tid + r * C::T)];
         v = csub(csub(v, two_q), q);
-        store(C::idx(r), v);
+        store(C::idx(r), v, pv[r]);
     }
     __syncthreads();   // smem reusable by the caller's next transform
 }
 
 // Inverse NTT of one limb.  load(idx) at idx = C::idx(r) -> residue in [0, 2q);
 // store(idx, canonical value).
-template <class C, bool FP, class Load, class Store>
-__device__ __forceinline__ void ntt_inv_impl(uint64_t* sm, const ModInfo& m, Load load, Store store) {
+template <class C, bool FP, class Load, class Pre, class Store>
+__device__ __forceinline__ void ntt_inv_impl(uint64_t* sm, const ModInfo& m, Load load, Pre pre, Store store) {
     const uint64_t q = m.q, two_q = 2 * q;
     const int tid = threadIdx.x;
 #pragma unroll
@@ -293,9 +305,13 @@ __device__ __forceinline__ void ntt_inv_impl(uint64_t* sm, const ModInfo& m, Loa
 #pragma unroll
     for (int r = 0; r < C::E; r++) x[r] = sm[spad(tid + r * C::T)];
     inv_pass_regs<C::LOGK, C::LOGE, C::K == 1, FP>(x, C::crank(), m, two_q);
+    using PT = decltype(pre(0));
+    PT pv[C::E];
     if constexpr (C::K == 1) {
 #pragma unroll
-        for (int r = 0; r < C::E; r++) store(tid + r * C::T, csub(x[r], q));
+        for (int r = 0; r < C::E; r++) pv[r] = pre(tid + r * C::T);
+#pragma unroll
+        for (int r = 0; r < C::E; r++) store(tid + r * C::T, csub(x[r], q), pv[r]);
         __syncthreads();
     } else {
         constexpr int MK = C::M / C::K;
@@ -309,12 +325,16 @@ __device__ __forceinline__ void ntt_inv_impl(uint64_t* sm, const ModInfo& m, Loa
         // phase A': columns j x all K sub-blocks, stages logK-1..0 (N^-1 folded in)
         const int j0 = C::crank() * MK + tid;
 #pragma unroll
+        for (int g = 0; g < C::E / C::K; g++)
+#pragma unroll
+            for (int t = 0; t < C::K; t++) pv[g * C::K + t] = pre(j0 + g * C::T + t * C::M);
+#pragma unroll
         for (int g = 0; g < C::E / C::K; g++) {
 #pragma unroll
             for (int t = 0; t < C::K; t++) x[g * C::K + t] = sm[spad(t * MK + tid + g * C::T)];
             inv_pass_regs<0, C::LOGK, true, FP>(x + g * C::K, 0, m, two_q);
 #pragma unroll
-            for (int t = 0; t < C::K; t++) store(j0 + g * C::T + t * C::M, csub(x[g * C::K + t], q));
+            for (int t = 0; t < C::K; t++) store(j0 + g * C::T + t * C::M, csub(x[g * C::K + t], q), pv[g * C::K + t]);
         }
         __syncthreads();
     }
@@ -322,41 +342,61 @@ __device__ __forceinline__ void ntt_inv_impl(uint64_t* sm, const ModInfo& m, Loa
 
 // Public entry points: the twiddle-product flavour is uniform per limb (ModInfo::fp), so
 // the branch is uniform across the CTA.
-template <class C, class Load, class Store>
-__device__ __forceinline__ void ntt_fwd(uint64_t* sm, const ModInfo& m, Load load, Store store) {
+// Epilogues come in two flavours: store(idx, v) or, with an operand fetcher,
+// pre(idx) -> operand (issued for all E outputs of a thread before the first store, so
+// the operand loads overlap) and store(idx, v, operand).
+struct NoPre {
+    __device__ __forceinline__ int operator()(int) const { return 0; }
+};
+
+template <class C, class Load, class Pre, class Store>
+__device__ __forceinline__ void ntt_fwd(uint64_t* sm, const ModInfo& m, Load load, Pre pre, Store store) {
 #ifndef EDL_NO_FP_QUOTIENT
-    if (m.fp) ntt_fwd_impl<C, true>(sm, m, load, store);
+    if (m.fp) ntt_fwd_impl<C, true>(sm, m, load, pre, store);
     else
 #endif
-        ntt_fwd_impl<C, false>(sm, m, load, store);
+        ntt_fwd_impl<C, false>(sm, m, load, pre, store);
+}
+
+template <class C, class Load, class Store>
+__device__ __forceinline__ void ntt_fwd(uint64_t* sm, const ModInfo& m, Load load, Store store) {
+    auto st3 = [&](int idx, uint64_t v, int) { store(idx, v); };
+    ntt_fwd<C>(sm, m, load, NoPre(), st3);
+}
+
+template <class C, class Load, class Pre, class Store>
+__device__ __forceinline__ void ntt_inv(uint64_t* sm, const ModInfo& m, Load load, Pre pre, Store store) {
+#ifndef EDL_NO_FP_QUOTIENT
+    if (m.fp) ntt_inv_impl<C, true>(sm, m, load, pre, store);
+    else
+#endif
+        ntt_inv_impl<C, false>(sm, m, load, pre, store);
 }
 
 template <class C, class Load, class Store>
 __device__ __forceinline__ void ntt_inv(uint64_t* sm, const ModInfo& m, Load load, Store store) {
-#ifndef EDL_NO_FP_QUOTIENT
-    if (m.fp) ntt_inv_impl<C, true>(sm, m, load, store);
-    else
-#endif
-        ntt_inv_impl<C, false>(sm, m, load, store);
+    auto st3 = [&](int idx, uint64_t v, int) { store(idx, v); };
+    ntt_inv<C>(sm, m, load, NoPre(), st3);
 }
 
 // ---- per-N configurations -------------------------------------------------------------
 // M = N/K <= 2^13 per CTA.  Plain transforms keep E = 32 residues per thread (fewer
 // exchanges); fused kernels, whose prologue/epilogue need registers, pick their own E.
-// Measured on B200 (tools/ntt_bench.py, C1 step): the plain transform at N = 2^14 is 6 %
-// faster as a 2-CTA cluster (5.0 vs 4.7 M limbs/s); the fused kernels are fastest as
+// Measured on B200 (tools/ntt_bench.py, C1 step): the plain transform at N = 2^14 is
+// fastest as one 1024-thread CTA x 16 residues (5.42 M limbs/s; 5.3 as a 2-CTA cluster of
+// 256 x 32, 4.7 as one 512 x 32 CTA); the fused kernels are fastest as
 // 2-CTA clusters of 512 threads x 16 residues with two CTAs per SM (64 registers, 32 warps
 // per SM): 6.76 ms/step vs 6.92 (one 1024-thread CTA per limb), 7.50 (128 registers, one
 // CTA per SM) and 8.87 (512 threads x 32 residues).  Latency hiding needs the warps more
 // than the spill-free register budget.
 #ifndef EDL_K14_PLAIN
-#define EDL_K14_PLAIN 2
+#define EDL_K14_PLAIN 1
 #endif
 #ifndef EDL_K14_FUSED
 #define EDL_K14_FUSED 2
 #endif
 #ifndef EDL_LOGE_P14
-#define EDL_LOGE_P14 5
+#define EDL_LOGE_P14 4
 #endif
 #ifndef EDL_LOGE_F14
 #define EDL_LOGE_F14 4

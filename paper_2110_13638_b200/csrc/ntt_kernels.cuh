@@ -85,13 +85,13 @@ k_rescale_ntt(const uint64_t* __restrict__ in, int l, const ulonglong2* __restri
         pf_next_wave<C>([&](int64_t bx, int cr, int y, int) { pf_sub<C>(r + (((size_t)bx * 2 + y) << C::LOGN), cr, true); });
     }
     auto ld = [&](int idx) { return center_mod(rr[idx], ql, ql_mod, m); };
-    auto st = [&](int idx, uint64_t x) {
-        uint64_t a = src[idx];
+    auto pre = [&](int idx) { return src[idx]; };
+    auto st = [&](int idx, uint64_t x, uint64_t a) {
         if (has_w) a = mulc(a, wi, m);
         uint64_t v = mulc(submod(a, x, m.q), qlinv, m);
         dst[idx] = addmod(v, b, m.q);
     };
-    ntt_fwd<C>(sm, m, ld, st);
+    ntt_fwd<C>(sm, m, ld, pre, st);
 }
 
 // ------------------------------------------------------------------------------------
@@ -137,8 +137,18 @@ __global__ void __launch_bounds__(C::T, C::MINB)
 k_relin_modup(const uint64_t* __restrict__ acoef, int l, int L, uint64_t* __restrict__ xh,
               const ModInfo* __restrict__ mods) {
     extern __shared__ uint64_t sm[];
-    const int j = blockIdx.y / (l + 1), tt = blockIdx.y % (l + 1);
-    const int ti = tt < j ? tt : tt + 1;          // target slot 0..l+1 (l+1 = P), skipping j
+    // y enumerates (target, digit) target-major: data targets ti = 0..l with the l digits
+    // j != ti, then P (ti = l+1) with all l+1 digits, so co-resident CTAs (limb-major
+    // grid) share one prime: one arithmetic path in the I-cache, one twiddle table
+    int ti, j;
+    if ((int)blockIdx.y < (l + 1) * l) {
+        ti = blockIdx.y / l;
+        const int jj = blockIdx.y % l;
+        j = jj < ti ? jj : jj + 1;
+    } else {
+        ti = l + 1;
+        j = blockIdx.y - (l + 1) * l;
+    }
     const int t = (ti == l + 1) ? (L + 1) : ti;
     const int64_t c = C::bx();
     const ModInfo& m = mods[t];
@@ -147,7 +157,8 @@ k_relin_modup(const uint64_t* __restrict__ acoef, int l, int L, uint64_t* __rest
     const bool need_red = mods[j].q > 4 * m.q;   // the forward NTT accepts [0, 4q)
     if (threadIdx.x == 0)
         pf_next_wave<C>([&](int64_t bx, int cr, int y, int) {
-            pf_sub<C>(acoef + (((size_t)bx * (l + 1) + y / (l + 1)) << C::LOGN), cr, true);
+            const int jn = y < (l + 1) * l ? ((y % l) < (y / l) ? (y % l) : (y % l) + 1) : y - (l + 1) * l;
+            pf_sub<C>(acoef + (((size_t)bx * (l + 1) + jn) << C::LOGN), cr, true);
         });
     auto ld = [&](int idx) {
         uint64_t v = src[idx];
@@ -187,11 +198,12 @@ k_relin_moddown_intt(const uint64_t* __restrict__ a, const uint64_t* __restrict_
     const uint64_t* vl = acc + ((((size_t)c * 2 + cp) * (l + 2) + l) << C::LOGN);   // d_l + acc_l P^-1 (M2b)
     uint64_t* sdst = s_out + (((size_t)c * 2 + cp) << C::LOGN);
     auto ld = [&](int idx) { return vl[idx]; };
-    auto st = [&](int idx, uint64_t y) {
-        uint64_t z = mulc(center_mod(rdst[idx], mp.q, pmod, ml), pinv, ml);
+    auto pre = [&](int idx) { return rdst[idx]; };
+    auto st = [&](int idx, uint64_t y, uint64_t rv) {
+        uint64_t z = mulc(center_mod(rv, mp.q, pmod, ml), pinv, ml);
         sdst[idx] = submod(y, z, ml.q);
     };
-    ntt_inv<C>(sm, ml, ld, st);
+    ntt_inv<C>(sm, ml, ld, pre, st);
 }
 
 template <class C>
@@ -227,13 +239,15 @@ k_relin_moddown_ntt(const uint64_t* __restrict__ a, const uint64_t* __restrict__
             uint64_t u = mulc(center_mod(rr[idx], P, pmod, m), pinv, m);
             return addmod(u, center_mod(ss[idx], ql, qlmod, m), m.q);
         };
-        auto st = [&](int idx, uint64_t x) { dst[idx] = mulc(submod(vi[idx], x, m.q), qlinv, m); };
-        ntt_fwd<C>(sm, m, ld, st);
+        auto pre = [&](int idx) { return vi[idx]; };
+        auto st = [&](int idx, uint64_t x, uint64_t v) { dst[idx] = mulc(submod(v, x, m.q), qlinv, m); };
+        ntt_fwd<C>(sm, m, ld, pre, st);
     } else {
         // out = d + (acc - NTT([r])) P^-1 = v - NTT([r] P^-1)  (Z_q-linear, exact)
         auto ld = [&](int idx) { return mulc(center_mod(rr[idx], P, pmod, m), pinv, m); };
-        auto st = [&](int idx, uint64_t x) { dst[idx] = submod(vi[idx], x, m.q); };
-        ntt_fwd<C>(sm, m, ld, st);
+        auto pre = [&](int idx) { return vi[idx]; };
+        auto st = [&](int idx, uint64_t x, uint64_t v) { dst[idx] = submod(v, x, m.q); };
+        ntt_fwd<C>(sm, m, ld, pre, st);
     }
 }
 

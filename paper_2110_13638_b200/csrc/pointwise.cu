@@ -4,6 +4,8 @@
 // (row = one limb of one polynomial).  The MAC layers accumulate full 128-bit
 // products lazily (mad.lo.cc / madc.hi) and reduce once per output (O4: modular sums
 // are order independent, so this is bit-identical to per-step reduction).
+#include <type_traits>
+
 #include "kernels.cuh"
 
 namespace edl {
@@ -387,28 +389,40 @@ __global__ void k_dense_combine(const uint64_t* __restrict__ part, int ks, int64
 // summed in 64 bits; others: 128-bit lazy sums; one reduction per output (O4).
 constexpr int MAC_CB = 4;
 
-__global__ void __launch_bounds__(PW_THREADS)
+struct TargetList {
+    int8_t slot[MAXM];
+};
+
+template <bool FP>
+__global__ void __launch_bounds__(PW_THREADS, 3)
 k_relin_mac(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l, int L, int64_t cnt,
             const uint64_t* __restrict__ xh, const uint64_t* __restrict__ rlk, const uint64_t* __restrict__ rlk_c,
-            uint64_t* __restrict__ acc, const ModInfo* __restrict__ mods, const ChainConsts* __restrict__ chain,
-            int logn) {
-    const int ti = blockIdx.y;                 // 0..l data targets, l+1 = P
+            uint64_t* __restrict__ acc, const __grid_constant__ TargetList tl, const ModInfo* __restrict__ mods,
+            const ChainConsts* __restrict__ chain, int logn) {
+    const int ti = tl.slot[blockIdx.y];        // 0..l data targets, l+1 = P
     const int64_t c0 = (int64_t)blockIdx.z * MAC_CB;
     const int t = (ti == l + 1) ? (L + 1) : ti;
     const ModInfo& m = mods[t];
-    const bool fp = m.fp != 0;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;   // coefficient pair
     if (2 * k >= (1 << logn)) return;
-    U128 s[MAC_CB][2][2];
+    // FP64-quotient limbs: lazy [0, 2q) products summed in 64 bits ((l+1) 2q < 2^60);
+    // others: full 128-bit products summed lazily
+    using Acc = typename std::conditional<FP, uint64_t, U128>::type;
+    Acc s[MAC_CB][2][2];
 #pragma unroll
     for (int e = 0; e < MAC_CB; e++)
 #pragma unroll
-        for (int cc = 0; cc < 2; cc++) s[e][cc][0].lo = s[e][cc][0].hi = s[e][cc][1].lo = s[e][cc][1].hi = 0;
+        for (int cc = 0; cc < 2; cc++)
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                if constexpr (FP) s[e][cc][h] = 0;
+                else s[e][cc][h].lo = s[e][cc][h].hi = 0;
+            }
     for (int j = 0; j <= l; j++) {
         const size_t o0 = (((size_t)j * 2 + 0) * (L + 2) + t) << logn, o1 = (((size_t)j * 2 + 1) * (L + 2) + t) << logn;
         const ulonglong2 r0 = __ldg(v2(rlk + o0) + k), r1 = __ldg(v2(rlk + o1) + k);
         ulonglong2 q0 = make_ulonglong2(0, 0), q1 = q0;
-        if (fp) {
+        if constexpr (FP) {
             q0 = __ldg(v2(rlk_c + o0) + k);
             q1 = __ldg(v2(rlk_c + o1) + k);
         }
@@ -426,17 +440,14 @@ k_relin_mac(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int 
                 x[e] = v2(xh + ((((size_t)c * (l + 1) + j) * (l + 2) + ti) << logn))[k];
             }
         }
-        if (fp) {   // (l+1) * 2q < 2^60
 #pragma unroll
-            for (int e = 0; e < MAC_CB; e++) {
-                s[e][0][0].lo += tw_mul_fp(x[e].x, r0.x, q0.x, m.q);
-                s[e][0][1].lo += tw_mul_fp(x[e].y, r0.y, q0.y, m.q);
-                s[e][1][0].lo += tw_mul_fp(x[e].x, r1.x, q1.x, m.q);
-                s[e][1][1].lo += tw_mul_fp(x[e].y, r1.y, q1.y, m.q);
-            }
-        } else {
-#pragma unroll
-            for (int e = 0; e < MAC_CB; e++) {
+        for (int e = 0; e < MAC_CB; e++) {
+            if constexpr (FP) {
+                s[e][0][0] += tw_mul_fp(x[e].x, r0.x, q0.x, m.q);
+                s[e][0][1] += tw_mul_fp(x[e].y, r0.y, q0.y, m.q);
+                s[e][1][0] += tw_mul_fp(x[e].x, r1.x, q1.x, m.q);
+                s[e][1][1] += tw_mul_fp(x[e].y, r1.y, q1.y, m.q);
+            } else {
                 mac128(s[e][0][0], x[e].x, r0.x);
                 mac128(s[e][0][1], x[e].y, r0.y);
                 mac128(s[e][1][0], x[e].x, r1.x);
@@ -452,9 +463,10 @@ k_relin_mac(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int 
         if (c >= cnt) continue;
         ulonglong2 v[2];
 #pragma unroll
-        for (int cc = 0; cc < 2; cc++)
-            v[cc] = fp ? make_ulonglong2(reduce64(s[e][cc][0].lo, m), reduce64(s[e][cc][1].lo, m))
-                       : make_ulonglong2(barrett128(s[e][cc][0], m), barrett128(s[e][cc][1], m));
+        for (int cc = 0; cc < 2; cc++) {
+            if constexpr (FP) v[cc] = make_ulonglong2(reduce64(s[e][cc][0], m), reduce64(s[e][cc][1], m));
+            else v[cc] = make_ulonglong2(barrett128(s[e][cc][0], m), barrett128(s[e][cc][1], m));
+        }
         if (ti <= l) {
             const ulonglong2 a0 = v2(a + limb_off(c, 0, ti, l + 1, logn))[k], a1 = v2(a + limb_off(c, 1, ti, l + 1, logn))[k];
             const ulonglong2 b0 = v2(b + limb_off(c, 0, ti, l + 1, logn))[k], b1 = v2(b + limb_off(c, 1, ti, l + 1, logn))[k];
@@ -473,9 +485,21 @@ k_relin_mac(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int 
 
 void launch_relin_mac(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t cnt, int l, const uint64_t* xh,
                       const uint64_t* rlk, const uint64_t* rlk_c, uint64_t* acc) {
-    dim3 grid((unsigned)((1 << d.logn) / (2 * PW_THREADS)), (unsigned)(l + 2), (unsigned)((cnt + MAC_CB - 1) / MAC_CB));
-    EDL_LAUNCH(d, "k_relin_mac", k_relin_mac<<<grid, PW_THREADS, 0, d.st>>>(a, b, l, d.L, cnt, xh, rlk, rlk_c, acc, d.mods,
-                                                                           d.cc, d.logn));
+    // one launch per arithmetic path (targets grouped by their modulus' mode)
+    TargetList tf, ti;
+    int nf = 0, ni = 0;
+    for (int s = 0; s <= l + 1; s++) {
+        const int t = (s == l + 1) ? d.L + 1 : s;
+        if (d.hmods[t].fp) tf.slot[nf++] = (int8_t)s;
+        else ti.slot[ni++] = (int8_t)s;
+    }
+    const unsigned gx = (unsigned)((1 << d.logn) / (2 * PW_THREADS)), gz = (unsigned)((cnt + MAC_CB - 1) / MAC_CB);
+    if (nf)
+        EDL_LAUNCH(d, "k_relin_mac", (k_relin_mac<true><<<dim3(gx, nf, gz), PW_THREADS, 0, d.st>>>(
+                                         a, b, l, d.L, cnt, xh, rlk, rlk_c, acc, tf, d.mods, d.cc, d.logn)));
+    if (ni)
+        EDL_LAUNCH(d, "k_relin_mac", (k_relin_mac<false><<<dim3(gx, ni, gz), PW_THREADS, 0, d.st>>>(
+                                         a, b, l, d.L, cnt, xh, rlk, rlk_c, acc, ti, d.mods, d.cc, d.logn)));
 }
 
 void launch_add(const Dev& d, const uint64_t* a, int la, const uint64_t* b, int lb, int64_t cnt, int lo, uint64_t* out) {
