@@ -169,6 +169,17 @@ C1_TRANSFORMS = {
 }
 
 
+# Algorithmic HBM bytes per launch (average over the step's launches) of the kernels that
+# can dominate: every operand limb read once, every output limb written once (N=2^14).
+_LIMB = 8 << 14
+C1_ALG_BYTES = {
+    # modulus raise: reads (l+1) digit limbs, writes (l+1)^2 raised limbs; l = 3 and 2
+    "k_relin_modup": 245 * _LIMB * ((4 + 16) + (3 + 9)) / 2,
+    # rescale: reads last limb (2 polys) + kept limbs, writes kept limbs; 4 launches
+    "k_rescale_ntt": _LIMB * (245 * 2 * (2 + 4 + 4 + 4) + 245 * 2 * (3 + 3) + 245 * 2 * (2 + 2) + 10 * 2 * 2) / 4,
+}
+
+
 def ntt_roofline(name, ms_total, steps, n, peak_int, peak_fp):
     """Achieved algorithmic butterflies/s of one NTT-family kernel over the timed region
     against the register-only butterfly ceiling for its mix of primes."""
@@ -317,14 +328,39 @@ def run_ours(a):
     if ntt_doms:
         k = ntt_doms[0]
         r = ntt_roofs[k]
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", "round1", "ncu_traffic.json")
+        if os.path.exists(tf):
+            tj = json.load(open(tf))
+            if k in tj:
+                traffic = tj[k]["dram_bytes_per_launch"]
         roof = {"kernel": k, "bound": "alu", "unit": "Gbutterfly/s", "achieved": r["achieved_Gbfly_s"],
-                "peak": r["peak_Gbfly_s"], "frac": r["frac"], "traffic": None,
+                "peak": r["peak_Gbfly_s"], "frac": r["frac"], "traffic": traffic,
+                "traffic_unit": "DRAM bytes per launch (profiles/round1/ncu_traffic.json, ncu --set full)",
+                "algorithmic_bytes_per_launch": C1_ALG_BYTES.get(k),
                 "peak_kind": "measured: register-only Harvey CT butterflies (edl_bfly_peak) through the "
                              "kernel's own arithmetic paths, weighted by its 60-bit/40-bit transform mix",
                 "peak_int_Gbfly_s": peak_int / 1e9, "peak_fp_Gbfly_s": peak_fp / 1e9,
                 "share_of_step": r["share_of_step"], "avg_launch_ms": prof[k][0] / prof[k][1],
                 "largest_kernel_overall": dom[0], "all_ntt_kernels": ntt_roofs}
     kernels = {k: {"ms_per_step": v[0] / a.steps, "launches_per_step": v[1] / a.steps} for k, v in prof.items()}
+
+    # ---- second half of BASELINE's metric: NTT limb-transforms/s (C2 shape at N = 2^14:
+    # 256 ciphertexts x 2 polys x 5 limbs of the C1 chain, forward, device-timed)
+    ntt_rate = None
+    if rank == 0:
+        nb = 256 * 2
+        tl = torch.randint(0, 2 ** 39, (nb * 5 * n,), dtype=torch.int64, device=f"cuda:{local}")
+        ctx.ntt_(tl, nb, 4, False)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        stream.synchronize()
+        g0.record(stream)
+        for _ in range(5):
+            ctx.ntt_(tl, nb, 4, False)
+        g1.record(stream)
+        stream.synchronize()
+        ntt_rate = nb * 5 * 5 / (g0.elapsed_time(g1) / 1e3)
+        del tl
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -349,7 +385,10 @@ def run_ours(a):
                                            f"dense partials"),
                            "l2": "inputs 1.03 GB per GPU > L2 (no flush)"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "clocks": clk, "dominant_kernel": dom[0], "kernels": kernels}
+                "clocks": clk, "dominant_kernel": dom[0], "kernels": kernels,
+                "ntt_limb_transforms_per_s": {"value": ntt_rate, "config": "N=2^14, C1 chain limbs q0..q4, 256 "
+                                              "ciphertexts x 2 polys, forward NTT, device-timed (outside the "
+                                              "timed C1 region)"}}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -155,9 +155,13 @@ edl_status edl_mod_drop(edl_ctx* ctx, const edl_cts* in, int32_t level, edl_cts*
  * Rescale(sum_taps x * const(k, q_l)) + const(b). */
 edl_status edl_cross_correlate(edl_ctx* ctx, const edl_cts* x, int32_t H, int32_t W, const double* k, int32_t F,
                                int32_t kh, int32_t kw, int32_t stride, const double* bias, edl_cts* out);
-/* Polynomial activation: coeffs c_0..c_degree.  Supported schedules: degree 3 with
- * c_2 = 0 (sigma_a = 0.5 + 0.197x - 0.004x^3; 2 levels) and degree 2 with
- * (0, 0, 1) (x^2; 1 level).  Others: EDL_ERR_ARG. */
+/* Polynomial activation: coeffs c_0..c_degree.  Schedules:
+ *   degree 3 with c_2 = 0: sigma_a = 0.5 + 0.197x - 0.004x^3, 2 levels;
+ *   degree 2 (0, 0, 1): x^2 (C0), 1 level;
+ *   degree 2 general: c0 + c1 x + c2 x^2, e.g. ReLU_a = 4/(3 pi q) x^2 + x/2 + q/(3 pi)
+ *     (PAPER.md:416), 2 levels: Rescale(Rescale(Relin(x x)) * c2) + drop(Rescale(x * c1)) + c0;
+ *   degree 1: c0 + c1 x, e.g. the linear sigmoid 0.5 + 0.197x, 1 level.
+ * Output level: x.level - levels; EDL_ERR_LEVEL if x.level is too low; others EDL_ERR_ARG. */
 edl_status edl_poly_activation(edl_ctx* ctx, const edl_cts* x, const double* coeffs, int32_t degree, edl_cts* out);
 /* Dense: out_o = Rescale(sum_k x_k * const(Wt[o][k], q_l)) + const(b_o).
  * Wt host doubles [O][K] (K = x->count), b [O] or NULL.  defer_rescale != 0 returns the

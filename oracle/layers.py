@@ -115,10 +115,43 @@ def sigmoid_approx(ctx: Context, y: CtArray, c0: float = 0.5, c1: float = 0.197,
     return ctx.add_scalar(out, [c0] * y.count)
 
 
+def linear_activation(ctx: Context, y: CtArray, c0: float, c1: float) -> CtArray:
+    """c0 + c1 y on 1 level: Rescale(y x const(c1, q_l)) + c0 -- the paper's linear
+    sigmoid 0.5 + 0.197x."""
+    l = y.level
+    if l < 1:
+        raise CkksError("LevelExhausted")
+    u = ctx.rescale(ctx.mul_scalar(y, [c1] * y.count, float(ctx.q[l])))
+    return ctx.add_scalar(u, [c0] * y.count)
+
+
+def quadratic_activation(ctx: Context, y: CtArray, c0: float, c1: float, c2: float) -> CtArray:
+    """c0 + c1 y + c2 y^2 on 2 levels (the paper's ReLU approximation R_a):
+      y2 = Rescale(Relin(y (x) y))                  level l-1, scale S2 = S^2/q_l
+      a  = Rescale(y2 x const(c2, q_{l-1}))         level l-2, scale (S2 q_{l-1})/q_{l-1}
+      b  = mod_drop(Rescale(y x const(c1, p1)))     level l-2, p1 = S2 q_l / S so S p1/q_l ~ S2
+      out = a + b + c0"""
+    l = y.level
+    if l < 2:
+        raise CkksError("LevelExhausted")
+    ql, qlm1 = float(ctx.q[l]), float(ctx.q[l - 1])
+    y2 = ctx.rescale(ctx.mul_relin(y, y))
+    a = ctx.rescale(ctx.mul_scalar(y2, [c2] * y.count, qlm1))
+    p1 = y2.scale * ql / y.scale
+    b = ctx.mod_drop(ctx.rescale(ctx.mul_scalar(y, [c1] * y.count, p1)), l - 2)
+    return ctx.add_scalar(ctx.add(a, b), [c0] * y.count)
+
+
 def poly_activation(ctx: Context, y: CtArray, coeffs: Sequence[float]) -> CtArray:
+    """Fixed schedules (SURVEY O13 + NEXT f2): x^2 (C0), degree 1 (linear sigmoid),
+    degree 2 (ReLU_a), degree 3 with c2 = 0 (sigma_a)."""
     coeffs = list(coeffs)
     if len(coeffs) == 3 and coeffs[0] == 0.0 and coeffs[1] == 0.0 and coeffs[2] == 1.0:
         return square(ctx, y)
+    if len(coeffs) == 2:
+        return linear_activation(ctx, y, coeffs[0], coeffs[1])
+    if len(coeffs) == 3:
+        return quadratic_activation(ctx, y, coeffs[0], coeffs[1], coeffs[2])
     if len(coeffs) == 4 and coeffs[2] == 0.0:
         return sigmoid_approx(ctx, y, coeffs[0], coeffs[1], coeffs[3])
     raise CkksError("unsupported polynomial schedule")

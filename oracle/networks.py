@@ -9,6 +9,8 @@ from __future__ import annotations
 
 from typing import Dict, Optional
 
+import math
+
 import numpy as np
 
 from . import layers
@@ -16,6 +18,17 @@ from .ckks import Context, CtArray
 from .params import params_from_depth
 
 SIGMA_A = (0.5, 0.197, 0.0, -0.004)   # PAPER.md:407 (reading Z9)
+SIGMA_LINEAR = (0.5, 0.197)           # PAPER.md:292 (linear part of sigma_a)
+
+
+def relu_a_coeffs(q: float = 1.0):
+    """R_a(x) = 4/(3 pi q) x^2 + x/2 + q/(3 pi) as (c0, c1, c2)."""
+    return (q / (3.0 * math.pi), 0.5, 4.0 / (3.0 * math.pi * q))
+
+
+def relu_a(x, q: float = 1.0):
+    c0, c1, c2 = relu_a_coeffs(q)
+    return c0 + c1 * x + c2 * x * x
 SQUARE = (0.0, 0.0, 1.0)
 
 

@@ -25,6 +25,7 @@ struct edl_ctx {
     cudaStream_t st = nullptr;
     std::vector<ModInfo> h_mods;
     ModInfo* d_mods = nullptr;
+    ModTable h_mt;
     ChainConsts* h_cc = nullptr;
     ChainConsts* d_cc = nullptr;
     uint64_t* d_tw = nullptr;
@@ -45,6 +46,7 @@ struct edl_ctx {
     Dev dev() const {
         Dev d;
         d.mods = d_mods;
+        d.mt = &h_mt;
         d.hmods = h_mods.data();
         d.cc = d_cc;
         d.logn = logn;
@@ -305,6 +307,8 @@ edl_status edl_ctx_create(const edl_params* p, int32_t device, void* stream, edl
         }
     cudaMalloc(&c->d_mods, nm * sizeof(ModInfo));
     cudaMemcpy(c->d_mods, c->h_mods.data(), nm * sizeof(ModInfo), cudaMemcpyHostToDevice);
+    std::memset(&c->h_mt, 0, sizeof(c->h_mt));
+    for (int k = 0; k < nm && k < MAXM; k++) c->h_mt.m[k] = c->h_mods[k];
     cudaMalloc(&c->d_cc, sizeof(ChainConsts));
     cudaMemcpy(c->d_cc, c->h_cc, sizeof(ChainConsts), cudaMemcpyHostToDevice);
     c->const_cap = 16u << 20;
@@ -712,6 +716,57 @@ edl_status edl_poly_activation(edl_ctx* c, const edl_cts* x, const double* coeff
             launch_relin(d, x->data, x->data, cnt, l, true, c->d_rlk, c->d_rlk_s, base, out->data);
         }
         set_meta(out, cnt, l - 1, (x->scale * x->scale) / (double)c->prm.q[l], x->key_id);
+        return cuda_check(c, "poly_activation");
+    }
+    if (degree == 1) {   // c0 + c1 y: Rescale(y x c1@q_l) + c0 (PAPER.md:292 linear sigmoid)
+        if (l < 1) return fail(c, EDL_ERR_LEVEL, "LevelExhausted");
+        const double ql = (double)c->prm.q[l];
+        const double Su = (x->scale * ql) / ql;
+        if (cnt > 0) {
+            uint64_t* r = scratch(c, (size_t)cnt * 2 * c->N);
+            if (!r) return fail(c, EDL_ERR_CUDA, "poly_activation: scratch");
+            std::vector<int64_t> i1(cnt, const_int(coeffs[1], ql)), i0(cnt, const_int(coeffs[0], Su));
+            const ulonglong2* w1 = upload(c, shoup_consts(c, i1, l));
+            const uint64_t* k0 = upload(c, residues(c, i0, l));
+            launch_rescale_intt(d, x->data, cnt, l, w1, r);
+            launch_rescale_ntt(d, x->data, cnt, l, w1, r, k0, out->data);
+        }
+        set_meta(out, cnt, l - 1, Su, x->key_id);
+        return cuda_check(c, "poly_activation");
+    }
+    if (degree == 2) {   // c0 + c1 y + c2 y^2 on 2 levels (PAPER.md:416 ReLU_a), oracle order
+        if (l < 2) return fail(c, EDL_ERR_LEVEL, "LevelExhausted");
+        const double c0 = coeffs[0], c1 = coeffs[1], c2 = coeffs[2];
+        const double ql = (double)c->prm.q[l], qlm1 = (double)c->prm.q[l - 1];
+        const double Sy = x->scale;
+        const double S2 = (Sy * Sy) / ql;                    // y2 = Rescale(Relin(y*y))
+        const double Sa = (S2 * qlm1) / qlm1;                // a = Rescale(y2 * c2@q_{l-1})
+        const double p1 = (S2 * ql) / Sy;                    // b = drop(Rescale(y * c1@p1))
+        const double Sb = (Sy * p1) / ql;
+        if (!scales_match(Sa, Sb)) return fail(c, EDL_ERR_SCALE, "poly_activation: scale drift");
+        if (cnt > 0) {
+            const size_t wl = ct_words(c, cnt, l - 1), wd = ct_words(c, cnt, l - 2);
+            const size_t rs = relin_scratch_words(cnt, l, c->logn);
+            uint64_t* base = scratch(c, wl + 2 * wd + 2 * (size_t)cnt * 2 * c->N + rs);
+            if (!base) return fail(c, EDL_ERR_CUDA, "poly_activation: scratch");
+            uint64_t* y2 = base;
+            uint64_t* av = y2 + wl;
+            uint64_t* bv = av + wd;
+            uint64_t* r = bv + wd;
+            uint64_t* r2 = r + (size_t)cnt * 2 * c->N;
+            uint64_t* rsc = r2 + (size_t)cnt * 2 * c->N;
+            std::vector<int64_t> i2(cnt, const_int(c2, qlm1)), i1(cnt, const_int(c1, p1)), i0(cnt, const_int(c0, Sa));
+            const ulonglong2* w2 = upload(c, shoup_consts(c, i2, l - 1));
+            const ulonglong2* w1 = upload(c, shoup_consts(c, i1, l));
+            const uint64_t* k0 = upload(c, residues(c, i0, l - 1));   // output level l-2: l-1 limbs
+            launch_relin(d, x->data, x->data, cnt, l, true, c->d_rlk, c->d_rlk_s, rsc, y2);
+            launch_rescale_intt(d, y2, cnt, l - 1, w2, r);
+            launch_rescale_ntt(d, y2, cnt, l - 1, w2, r, nullptr, av);
+            launch_rescale_intt(d, x->data, cnt, l, w1, r2);
+            launch_rescale_ntt(d, x->data, cnt, l, w1, r2, nullptr, bv, l - 2);
+            launch_add_add_const(d, av, bv, l - 2, cnt, l - 2, k0, out->data);
+        }
+        set_meta(out, cnt, l - 2, Sa, x->key_id);
         return cuda_check(c, "poly_activation");
     }
     if (!(degree == 3 && coeffs[2] == 0.0)) return fail(c, EDL_ERR_ARG, "poly_activation: unsupported schedule");

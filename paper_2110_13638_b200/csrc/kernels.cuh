@@ -40,8 +40,16 @@ struct Prof {
     ~Prof();
 };
 
+// All moduli of a context as one kernel parameter (constant bank: uniform loads, no
+// vector registers held for the per-limb constants).
+struct ModTable {
+    ModInfo m[MAXM];
+    __host__ __device__ const ModInfo& operator[](int i) const { return m[i]; }
+};
+
 struct Dev {
     const ModInfo* mods;        // [L+2] (device)
+    const ModTable* mt;         // host copy passed by value to every kernel
     const ModInfo* hmods;       // [L+2] (host copy: launch-time decisions such as the arithmetic path)
     const ChainConsts* cc;
     int logn;

@@ -153,6 +153,9 @@ __device__ __forceinline__ void fwd_pass_regs(uint64_t* x, int high, const ulong
             ulonglong2 w = __ldg(tw + tidx);
             ct_bfly<FP>(x[r], x[r + half], w, q, two_q);
         }
+#ifdef EDL_STAGE_FENCE
+        asm volatile("" ::: "memory");
+#endif
     }
 }
 
@@ -176,6 +179,9 @@ __device__ __forceinline__ void inv_pass_regs(uint64_t* x, int high, const ModIn
                 gs_bfly<FP>(x[r], x[r + half], w.x, w.y, m.q, two_q);
             }
         }
+#ifdef EDL_STAGE_FENCE
+        asm volatile("" ::: "memory");
+#endif
     }
 }
 

@@ -13,7 +13,7 @@ namespace edl {
 // K1/K2: plain batched NTT / INTT, in place, data [batch][nl][N], limb j uses pm.idx[j].
 template <class C, bool INV>
 __global__ void __launch_bounds__(C::T, C::MINB)
-k_ntt_limbs(uint64_t* __restrict__ data, int nl, const __grid_constant__ PrimeMap pm, const ModInfo* __restrict__ mods) {
+k_ntt_limbs(uint64_t* __restrict__ data, int nl, const __grid_constant__ PrimeMap pm, const __grid_constant__ ModTable mods) {
     extern __shared__ uint64_t sm[];
     const int limb = blockIdx.y;    // limb-major grid: co-resident CTAs share a prime (code path, twiddles)
     uint64_t* p = data + (((size_t)C::bx() * nl + limb) << C::LOGN);
@@ -34,7 +34,7 @@ template <class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
 k_rescale_intt(const uint64_t* __restrict__ in, int l, const ulonglong2* __restrict__ w,
                uint64_t* __restrict__ r_out, const ulonglong2* __restrict__ w2, uint64_t* __restrict__ r_out2,
-               const ModInfo* __restrict__ mods) {
+               const __grid_constant__ ModTable mods) {
     extern __shared__ uint64_t sm[];
     const int p = blockIdx.y;
     const int64_t c = C::bx();
@@ -66,7 +66,7 @@ template <class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
 k_rescale_ntt(const uint64_t* __restrict__ in, int l, const ulonglong2* __restrict__ w,
               const uint64_t* __restrict__ r, const uint64_t* __restrict__ bias, uint64_t* __restrict__ out, int nlo,
-              const ModInfo* __restrict__ mods, const ChainConsts* __restrict__ cc) {
+              const __grid_constant__ ModTable mods, const ChainConsts* __restrict__ cc) {
     extern __shared__ uint64_t sm[];
     const int i = blockIdx.z, p = blockIdx.y;
     const int64_t c = C::bx();
@@ -111,7 +111,7 @@ k_rescale_ntt(const uint64_t* __restrict__ in, int l, const ulonglong2* __restri
 template <class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
 k_relin_intt_d2(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l,
-                uint64_t* __restrict__ acoef, const ModInfo* __restrict__ mods) {
+                uint64_t* __restrict__ acoef, const __grid_constant__ ModTable mods) {
     extern __shared__ uint64_t sm[];
     const int j = blockIdx.y;
     const int64_t c = C::bx();
@@ -135,7 +135,7 @@ k_relin_intt_d2(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, 
 template <class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
 k_relin_modup(const uint64_t* __restrict__ acoef, int l, int L, uint64_t* __restrict__ xh,
-              const ModInfo* __restrict__ mods) {
+              const __grid_constant__ ModTable mods) {
     extern __shared__ uint64_t sm[];
     // y enumerates (target, digit) target-major: data targets ti = 0..l with the l digits
     // j != ti, then P (ti = l+1) with all l+1 digits, so co-resident CTAs (limb-major
@@ -172,7 +172,7 @@ template <class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
 k_relin_moddown_intt(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l,
                      const uint64_t* __restrict__ acc, int L, int rescale, uint64_t* __restrict__ r_out,
-                     uint64_t* __restrict__ s_out, const ModInfo* __restrict__ mods,
+                     uint64_t* __restrict__ s_out, const __grid_constant__ ModTable mods,
                      const ChainConsts* __restrict__ cc) {
     extern __shared__ uint64_t sm[];
     const int cp = blockIdx.y;
@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(C::T, C::MINB)
 k_relin_moddown_ntt(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l,
                     const uint64_t* __restrict__ acc, const uint64_t* __restrict__ r,
                     const uint64_t* __restrict__ s, int L, int rescale, uint64_t* __restrict__ out,
-                    const ModInfo* __restrict__ mods, const ChainConsts* __restrict__ cc) {
+                    const __grid_constant__ ModTable mods, const ChainConsts* __restrict__ cc) {
     extern __shared__ uint64_t sm[];
     const int i = blockIdx.z, cp = blockIdx.y;
     const int64_t c = C::bx();
@@ -255,22 +255,22 @@ template <int LOGN>
 void launch_ntt_limbs_n(const Dev& d, uint64_t* data, int64_t batch, int nl, const PrimeMap& pm, bool inverse) {
     using C = CfgPlain<LOGN>;
     const dim3 grid((unsigned)batch, nl);
-    if (inverse) launch_cfg<C>(d, "k_ntt_limbs", k_ntt_limbs<C, true>, grid, data, nl, pm, d.mods);
-    else launch_cfg<C>(d, "k_ntt_limbs", k_ntt_limbs<C, false>, grid, data, nl, pm, d.mods);
+    if (inverse) launch_cfg<C>(d, "k_ntt_limbs", k_ntt_limbs<C, true>, grid, data, nl, pm, *d.mt);
+    else launch_cfg<C>(d, "k_ntt_limbs", k_ntt_limbs<C, false>, grid, data, nl, pm, *d.mt);
 }
 
 template <int LOGN>
 void launch_rescale_intt_n(const Dev& d, const uint64_t* in, int64_t cnt, int l, const ulonglong2* w, uint64_t* r_out,
                            const ulonglong2* w2, uint64_t* r_out2) {
     using C = CfgFused<LOGN>;
-    launch_cfg<C>(d, "k_rescale_intt", k_rescale_intt<C>, dim3((unsigned)cnt, 2), in, l, w, r_out, w2, r_out2, d.mods);
+    launch_cfg<C>(d, "k_rescale_intt", k_rescale_intt<C>, dim3((unsigned)cnt, 2), in, l, w, r_out, w2, r_out2, *d.mt);
 }
 
 template <int LOGN>
 void launch_rescale_ntt_n(const Dev& d, const uint64_t* in, int64_t cnt, int l, const ulonglong2* w, const uint64_t* r,
                           const uint64_t* bias, uint64_t* out, int nlo) {
     using C = CfgFused<LOGN>;
-    launch_cfg<C>(d, "k_rescale_ntt", k_rescale_ntt<C>, dim3((unsigned)cnt, 2, nlo), in, l, w, r, bias, out, nlo, d.mods,
+    launch_cfg<C>(d, "k_rescale_ntt", k_rescale_ntt<C>, dim3((unsigned)cnt, 2, nlo), in, l, w, r, bias, out, nlo, *d.mt,
                   d.cc);
 }
 
@@ -281,14 +281,14 @@ void launch_relin_n(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t 
     using C = CfgFused<LOGN>;
     using CP = CfgPlain<LOGN>;
     const int rs = rescale ? 1 : 0;
-    launch_cfg<C>(d, "k_relin_intt_d2", k_relin_intt_d2<C>, dim3((unsigned)cnt, l + 1), a, b, l, acoef, d.mods);
+    launch_cfg<C>(d, "k_relin_intt_d2", k_relin_intt_d2<C>, dim3((unsigned)cnt, l + 1), a, b, l, acoef, *d.mt);
     launch_cfg<CP>(d, "k_relin_modup", k_relin_modup<CP>, dim3((unsigned)cnt, (l + 1) * (l + 1)), (const uint64_t*)acoef,
-                   l, d.L, xh, d.mods);
+                   l, d.L, xh, *d.mt);
     launch_relin_mac(d, a, b, cnt, l, xh, rlk, rlk_c, acc);   // acc slots 0..l hold v
     launch_cfg<C>(d, "k_relin_moddown_intt", k_relin_moddown_intt<C>, dim3((unsigned)cnt, 2), a, b, l, (const uint64_t*)acc,
-                  d.L, rs, r, s, d.mods, d.cc);
+                  d.L, rs, r, s, *d.mt, d.cc);
     launch_cfg<C>(d, "k_relin_moddown_ntt", k_relin_moddown_ntt<C>, dim3((unsigned)cnt, 2, rescale ? l : l + 1), a, b, l,
-                  (const uint64_t*)acc, (const uint64_t*)r, (const uint64_t*)s, d.L, rs, out, d.mods, d.cc);
+                  (const uint64_t*)acc, (const uint64_t*)r, (const uint64_t*)s, d.L, rs, out, *d.mt, d.cc);
 }
 
 #define EDL_INSTANTIATE_NTT(LOGN)                                                                                   \

@@ -26,7 +26,7 @@ dim3 rows_grid(int logn, int64_t rows) {
 
 // ---------------------------------------------------------------- add
 __global__ void k_add(const uint64_t* __restrict__ a, int la, const uint64_t* __restrict__ b, int lb, int64_t cnt,
-                      int lo, uint64_t* __restrict__ out, const ModInfo* __restrict__ mods, int logn) {
+                      int lo, uint64_t* __restrict__ out, const __grid_constant__ ModTable mods, int logn) {
     const int64_t rows = cnt * 2 * (lo + 1);
     const int n2 = 1 << (logn - 1);
     for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
@@ -45,7 +45,7 @@ __global__ void k_add(const uint64_t* __restrict__ a, int la, const uint64_t* __
 
 // ---------------------------------------------------------------- scalar const multiply
 __global__ void k_mul_const(const uint64_t* __restrict__ a, int64_t cnt, int l, const ulonglong2* __restrict__ w,
-                            uint64_t* __restrict__ out, const ModInfo* __restrict__ mods, int logn) {
+                            uint64_t* __restrict__ out, const __grid_constant__ ModTable mods, int logn) {
     const int64_t rows = cnt * 2 * (l + 1);
     const int n2 = 1 << (logn - 1);
     for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
@@ -64,7 +64,7 @@ __global__ void k_mul_const(const uint64_t* __restrict__ a, int64_t cnt, int l, 
 
 // ---------------------------------------------------------------- add constant (poly 0 only)
 __global__ void k_add_const(const uint64_t* __restrict__ a, int64_t cnt, int l, const uint64_t* __restrict__ kc,
-                            uint64_t* __restrict__ out, const ModInfo* __restrict__ mods, int logn) {
+                            uint64_t* __restrict__ out, const __grid_constant__ ModTable mods, int logn) {
     const int64_t rows = cnt * 2 * (l + 1);
     const int n2 = 1 << (logn - 1);
     for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
@@ -97,7 +97,7 @@ __global__ void k_mod_drop(const uint64_t* __restrict__ a, int64_t cnt, int la, 
 }
 
 // ---------------------------------------------------------------- in-place x mod q (after NCCL uint64 sum)
-__global__ void k_mod_reduce(uint64_t* __restrict__ x, int64_t cnt, int l, const ModInfo* __restrict__ mods,
+__global__ void k_mod_reduce(uint64_t* __restrict__ x, int64_t cnt, int l, const __grid_constant__ ModTable mods,
                              int logn) {
     const int64_t rows = cnt * 2 * (l + 1);
     const int n2 = 1 << (logn - 1);
@@ -114,7 +114,7 @@ __global__ void k_mod_reduce(uint64_t* __restrict__ x, int64_t cnt, int l, const
 // ---------------------------------------------------------------- v + mod_drop(w) + const
 __global__ void k_add_add_const(const uint64_t* __restrict__ v, const uint64_t* __restrict__ w, int lw, int64_t cnt,
                                 int lo, const uint64_t* __restrict__ kc, uint64_t* __restrict__ out,
-                                const ModInfo* __restrict__ mods, int logn) {
+                                const __grid_constant__ ModTable mods, int logn) {
     const int64_t rows = cnt * 2 * (lo + 1);
     const int n2 = 1 << (logn - 1);
     for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
@@ -145,7 +145,7 @@ constexpr int CC_TAPS = 16;
 
 __global__ void __launch_bounds__(PW_THREADS, 2)
 k_cc_mac(const uint64_t* __restrict__ x, int l, int H, int W, int F, int kh, int kw, int stride,
-         const ulonglong2* __restrict__ wk, uint64_t* __restrict__ out, const ModInfo* __restrict__ mods, int logn) {
+         const ulonglong2* __restrict__ wk, uint64_t* __restrict__ out, const __grid_constant__ ModTable mods, int logn) {
     extern __shared__ uint64_t wsm[];   // [F][taps] residues for this limb
     const int nl = l + 1;
     const int p = blockIdx.y / nl, i = blockIdx.y % nl;
@@ -211,7 +211,7 @@ template <int FC>
 __global__ void __launch_bounds__(CC2_THREADS, 2)
 k_cc_mac2(const uint64_t* __restrict__ x, int l, int W, int kw, int stride, int Wo, int taps, int f0, int F,
           int n_out_per_f, const ulonglong2* __restrict__ wk, uint64_t* __restrict__ out,
-          const ModInfo* __restrict__ mods, int logn) {
+          const __grid_constant__ ModTable mods, int logn) {
     __shared__ ulonglong2 wsm[FC * CC2_MAXTAPS];  // [f][tap] {residue, companion} of this limb
     __shared__ int tpix[CC2_MAXTAPS];            // pixel (ciphertext) index of each tap
     const int nl = l + 1;
@@ -297,7 +297,7 @@ constexpr int DN_U = 4;
 
 __global__ void __launch_bounds__(PW_THREADS, 2)
 k_dense_mac(const uint64_t* __restrict__ x, int64_t K, int64_t O, int l, int ks, const ulonglong2* __restrict__ wd,
-            uint64_t* __restrict__ out, const ModInfo* __restrict__ mods, int logn) {
+            uint64_t* __restrict__ out, const __grid_constant__ ModTable mods, int logn) {
     extern __shared__ ulonglong2 wsm2[];   // [DN_OC][DN_KC] {residue, companion}
     const int nl = l + 1;
     const int p = blockIdx.y / nl, i = blockIdx.y % nl;
@@ -361,7 +361,7 @@ k_dense_mac(const uint64_t* __restrict__ x, int64_t K, int64_t O, int l, int ks,
 
 // out[r][k] = sum_s part[s][r][k] mod q over ks slices (rows = O * 2 * nl limbs).
 __global__ void k_dense_combine(const uint64_t* __restrict__ part, int ks, int64_t O, int l, uint64_t* __restrict__ out,
-                                const ModInfo* __restrict__ mods, int logn) {
+                                const __grid_constant__ ModTable mods, int logn) {
     const int64_t rows = O * 2 * (l + 1);
     const int n2 = 1 << (logn - 1);
     const size_t slice = (size_t)rows << logn;
@@ -397,7 +397,7 @@ template <bool FP>
 __global__ void __launch_bounds__(PW_THREADS, 3)
 k_relin_mac(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l, int L, int64_t cnt,
             const uint64_t* __restrict__ xh, const uint64_t* __restrict__ rlk, const uint64_t* __restrict__ rlk_c,
-            uint64_t* __restrict__ acc, const __grid_constant__ TargetList tl, const ModInfo* __restrict__ mods,
+            uint64_t* __restrict__ acc, const __grid_constant__ TargetList tl, const __grid_constant__ ModTable mods,
             const ChainConsts* __restrict__ chain, int logn) {
     const int ti = tl.slot[blockIdx.y];        // 0..l data targets, l+1 = P
     const int64_t c0 = (int64_t)blockIdx.z * MAC_CB;
@@ -496,22 +496,22 @@ void launch_relin_mac(const Dev& d, const uint64_t* a, const uint64_t* b, int64_
     const unsigned gx = (unsigned)((1 << d.logn) / (2 * PW_THREADS)), gz = (unsigned)((cnt + MAC_CB - 1) / MAC_CB);
     if (nf)
         EDL_LAUNCH(d, "k_relin_mac", (k_relin_mac<true><<<dim3(gx, nf, gz), PW_THREADS, 0, d.st>>>(
-                                         a, b, l, d.L, cnt, xh, rlk, rlk_c, acc, tf, d.mods, d.cc, d.logn)));
+                                         a, b, l, d.L, cnt, xh, rlk, rlk_c, acc, tf, *d.mt, d.cc, d.logn)));
     if (ni)
         EDL_LAUNCH(d, "k_relin_mac", (k_relin_mac<false><<<dim3(gx, ni, gz), PW_THREADS, 0, d.st>>>(
-                                         a, b, l, d.L, cnt, xh, rlk, rlk_c, acc, ti, d.mods, d.cc, d.logn)));
+                                         a, b, l, d.L, cnt, xh, rlk, rlk_c, acc, ti, *d.mt, d.cc, d.logn)));
 }
 
 void launch_add(const Dev& d, const uint64_t* a, int la, const uint64_t* b, int lb, int64_t cnt, int lo, uint64_t* out) {
-    EDL_LAUNCH(d, "k_add", k_add<<<rows_grid(d.logn, cnt * 2 * (lo + 1)), PW_THREADS, 0, d.st>>>(a, la, b, lb, cnt, lo, out, d.mods, d.logn));
+    EDL_LAUNCH(d, "k_add", k_add<<<rows_grid(d.logn, cnt * 2 * (lo + 1)), PW_THREADS, 0, d.st>>>(a, la, b, lb, cnt, lo, out, *d.mt, d.logn));
 }
 
 void launch_mul_const(const Dev& d, const uint64_t* a, int64_t cnt, int l, const ulonglong2* w, uint64_t* out) {
-    EDL_LAUNCH(d, "k_mul_const", k_mul_const<<<rows_grid(d.logn, cnt * 2 * (l + 1)), PW_THREADS, 0, d.st>>>(a, cnt, l, w, out, d.mods, d.logn));
+    EDL_LAUNCH(d, "k_mul_const", k_mul_const<<<rows_grid(d.logn, cnt * 2 * (l + 1)), PW_THREADS, 0, d.st>>>(a, cnt, l, w, out, *d.mt, d.logn));
 }
 
 void launch_add_const(const Dev& d, const uint64_t* a, int64_t cnt, int l, const uint64_t* k, uint64_t* out) {
-    EDL_LAUNCH(d, "k_add_const", k_add_const<<<rows_grid(d.logn, cnt * 2 * (l + 1)), PW_THREADS, 0, d.st>>>(a, cnt, l, k, out, d.mods, d.logn));
+    EDL_LAUNCH(d, "k_add_const", k_add_const<<<rows_grid(d.logn, cnt * 2 * (l + 1)), PW_THREADS, 0, d.st>>>(a, cnt, l, k, out, *d.mt, d.logn));
 }
 
 void launch_mod_drop(const Dev& d, const uint64_t* a, int64_t cnt, int la, int lo, uint64_t* out) {
@@ -519,12 +519,12 @@ void launch_mod_drop(const Dev& d, const uint64_t* a, int64_t cnt, int la, int l
 }
 
 void launch_mod_reduce(const Dev& d, uint64_t* x, int64_t cnt, int l) {
-    EDL_LAUNCH(d, "k_mod_reduce", k_mod_reduce<<<rows_grid(d.logn, cnt * 2 * (l + 1)), PW_THREADS, 0, d.st>>>(x, cnt, l, d.mods, d.logn));
+    EDL_LAUNCH(d, "k_mod_reduce", k_mod_reduce<<<rows_grid(d.logn, cnt * 2 * (l + 1)), PW_THREADS, 0, d.st>>>(x, cnt, l, *d.mt, d.logn));
 }
 
 void launch_add_add_const(const Dev& d, const uint64_t* v, const uint64_t* w, int lw, int64_t cnt, int lo,
                           const uint64_t* k, uint64_t* out) {
-    EDL_LAUNCH(d, "k_add_add_const", k_add_add_const<<<rows_grid(d.logn, cnt * 2 * (lo + 1)), PW_THREADS, 0, d.st>>>(v, w, lw, cnt, lo, k, out, d.mods,
+    EDL_LAUNCH(d, "k_add_add_const", k_add_add_const<<<rows_grid(d.logn, cnt * 2 * (lo + 1)), PW_THREADS, 0, d.st>>>(v, w, lw, cnt, lo, k, out, *d.mt,
                                                                                    d.logn));
 }
 
@@ -536,7 +536,7 @@ void launch_cc_mac(const Dev& d, const uint64_t* x, int l, int H, int W, int F, 
         dim3 grid((unsigned)((1 << d.logn) / (2 * CC2_THREADS)), (unsigned)(2 * (l + 1)), (unsigned)(Ho * Wo));
         for (int f0 = 0; f0 < F; f0 += 8) {
             const int fc = (F - f0) < 8 ? (F - f0) : 8;
-#define EDL_CC2(FCV) EDL_LAUNCH(d, "k_cc_mac", (k_cc_mac2<FCV><<<grid, CC2_THREADS, 0, d.st>>>(x, l, W, kw, stride, Wo, taps, f0, F, Ho * Wo, wk, out, d.mods, d.logn)))
+#define EDL_CC2(FCV) EDL_LAUNCH(d, "k_cc_mac", (k_cc_mac2<FCV><<<grid, CC2_THREADS, 0, d.st>>>(x, l, W, kw, stride, Wo, taps, f0, F, Ho * Wo, wk, out, *d.mt, d.logn)))
             switch (fc) {
                 case 1: EDL_CC2(1); break;
                 case 2: EDL_CC2(2); break;
@@ -553,7 +553,7 @@ void launch_cc_mac(const Dev& d, const uint64_t* x, int l, int H, int W, int F, 
     }
     dim3 grid((unsigned)(((1 << d.logn) + PW_THREADS - 1) / PW_THREADS), (unsigned)(2 * (l + 1)), (unsigned)(Ho * Wo));
     size_t smem = (size_t)F * kh * kw * sizeof(uint64_t);
-    EDL_LAUNCH(d, "k_cc_mac", k_cc_mac<<<grid, PW_THREADS, smem, d.st>>>(x, l, H, W, F, kh, kw, stride, wk, out, d.mods, d.logn));
+    EDL_LAUNCH(d, "k_cc_mac", k_cc_mac<<<grid, PW_THREADS, smem, d.st>>>(x, l, H, W, F, kh, kw, stride, wk, out, *d.mt, d.logn));
 }
 
 int dense_split(const Dev& d, int64_t K, int64_t O, int l) {
@@ -570,10 +570,10 @@ void launch_dense_mac(const Dev& d, const uint64_t* x, int64_t K, int64_t O, int
               (unsigned)(((O + DN_OC - 1) / DN_OC) * ks));
     size_t smem = (size_t)DN_OC * DN_KC * sizeof(ulonglong2);
     uint64_t* dst = ks > 1 ? part : out;
-    EDL_LAUNCH(d, "k_dense_mac", k_dense_mac<<<grid, PW_THREADS, smem, d.st>>>(x, K, O, l, ks, wd, dst, d.mods, d.logn));
+    EDL_LAUNCH(d, "k_dense_mac", k_dense_mac<<<grid, PW_THREADS, smem, d.st>>>(x, K, O, l, ks, wd, dst, *d.mt, d.logn));
     if (ks > 1)
         EDL_LAUNCH(d, "k_dense_combine", k_dense_combine<<<rows_grid(d.logn, O * 2 * (l + 1)), PW_THREADS, 0, d.st>>>(
-                                             part, ks, O, l, out, d.mods, d.logn));
+                                             part, ks, O, l, out, *d.mt, d.logn));
 }
 
 }  // namespace edl

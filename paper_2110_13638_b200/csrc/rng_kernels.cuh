@@ -73,7 +73,7 @@ __device__ __forceinline__ uint64_t key_companion(uint64_t v, const ModInfo& m) 
 // ---- keygen: one CTA per modulus (secret), per data limb (pk), per (digit, limb) (rlk)
 template <class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
-k_keygen_s(uint64_t seed, uint64_t* __restrict__ s_hat, const ModInfo* __restrict__ mods) {
+k_keygen_s(uint64_t seed, uint64_t* __restrict__ s_hat, const __grid_constant__ ModTable mods) {
     extern __shared__ uint64_t sm[];
     const int i = C::bx();
     const ModInfo& m = mods[i];
@@ -86,7 +86,7 @@ k_keygen_s(uint64_t seed, uint64_t* __restrict__ s_hat, const ModInfo* __restric
 template <class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
 k_keygen_pk(uint64_t seed, int L, const uint64_t* __restrict__ s_hat, uint64_t* __restrict__ pk,
-            const ModInfo* __restrict__ mods) {
+            const __grid_constant__ ModTable mods) {
     extern __shared__ uint64_t sm[];
     const int i = C::bx();
     const ModInfo& m = mods[i];
@@ -105,7 +105,7 @@ k_keygen_pk(uint64_t seed, int L, const uint64_t* __restrict__ s_hat, uint64_t* 
 template <class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
 k_keygen_rlk(uint64_t seed, int L, const uint64_t* __restrict__ s_hat, uint64_t* __restrict__ rlk,
-             uint64_t* __restrict__ rlk_s, const ModInfo* __restrict__ mods, const ChainConsts* __restrict__ cc) {
+             uint64_t* __restrict__ rlk_s, const __grid_constant__ ModTable mods, const ChainConsts* __restrict__ cc) {
     extern __shared__ uint64_t sm[];
     const int i = C::bx();   // limb 0..L+1 (L+1 = P)
     const int j = blockIdx.y;   // digit 0..L
@@ -132,7 +132,7 @@ k_keygen_rlk(uint64_t seed, int L, const uint64_t* __restrict__ s_hat, uint64_t*
 template <class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
 k_encrypt(const int64_t* __restrict__ msg, int l, int L, uint64_t seed, uint32_t obj0, const uint64_t* __restrict__ pk,
-          uint64_t* __restrict__ out, const ModInfo* __restrict__ mods) {
+          uint64_t* __restrict__ out, const __grid_constant__ ModTable mods) {
     extern __shared__ uint64_t sm[];
     const int i = blockIdx.y;
     const int64_t c = C::bx();
@@ -169,7 +169,7 @@ k_encrypt(const int64_t* __restrict__ msg, int l, int L, uint64_t seed, uint32_t
 template <class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
 k_decrypt(const uint64_t* __restrict__ ct, int l, const uint64_t* __restrict__ s_hat, uint64_t* __restrict__ out,
-          const ModInfo* __restrict__ mods) {
+          const __grid_constant__ ModTable mods) {
     extern __shared__ uint64_t sm[];
     const int i = blockIdx.y;
     const int64_t c = C::bx();
@@ -186,23 +186,23 @@ k_decrypt(const uint64_t* __restrict__ ct, int l, const uint64_t* __restrict__ s
 template <int LOGN>
 void launch_keygen_n(const Dev& d, uint64_t seed, uint64_t* s_hat, uint64_t* pk, uint64_t* rlk, uint64_t* rlk_s) {
     using C = CfgFused<LOGN>;
-    launch_cfg<C>(d, "k_keygen_s", k_keygen_s<C>, dim3(d.L + 2), seed, s_hat, d.mods);
-    launch_cfg<C>(d, "k_keygen_pk", k_keygen_pk<C>, dim3(d.L + 1), seed, d.L, (const uint64_t*)s_hat, pk, d.mods);
+    launch_cfg<C>(d, "k_keygen_s", k_keygen_s<C>, dim3(d.L + 2), seed, s_hat, *d.mt);
+    launch_cfg<C>(d, "k_keygen_pk", k_keygen_pk<C>, dim3(d.L + 1), seed, d.L, (const uint64_t*)s_hat, pk, *d.mt);
     launch_cfg<C>(d, "k_keygen_rlk", k_keygen_rlk<C>, dim3(d.L + 2, d.L + 1), seed, d.L, (const uint64_t*)s_hat, rlk,
-                  rlk_s, d.mods, d.cc);
+                  rlk_s, *d.mt, d.cc);
 }
 
 template <int LOGN>
 void launch_encrypt_n(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint64_t seed, uint32_t obj0,
                       const uint64_t* pk, uint64_t* out) {
     using C = CfgFused<LOGN>;
-    launch_cfg<C>(d, "k_encrypt", k_encrypt<C>, dim3((unsigned)cnt, l + 1), msg, l, d.L, seed, obj0, pk, out, d.mods);
+    launch_cfg<C>(d, "k_encrypt", k_encrypt<C>, dim3((unsigned)cnt, l + 1), msg, l, d.L, seed, obj0, pk, out, *d.mt);
 }
 
 template <int LOGN>
 void launch_decrypt_n(const Dev& d, const uint64_t* ct, int64_t cnt, int l, const uint64_t* s_hat, uint64_t* out) {
     using C = CfgFused<LOGN>;
-    launch_cfg<C>(d, "k_decrypt", k_decrypt<C>, dim3((unsigned)cnt, l + 1), ct, l, s_hat, out, d.mods);
+    launch_cfg<C>(d, "k_decrypt", k_decrypt<C>, dim3((unsigned)cnt, l + 1), ct, l, s_hat, out, *d.mt);
 }
 
 #define EDL_INSTANTIATE_RNG(LOGN)                                                                               \

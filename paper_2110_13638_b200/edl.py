@@ -369,7 +369,7 @@ class Context:
     def poly_activation(self, x: CtArray, coeffs: Sequence[float], out: Optional[CtArray] = None) -> CtArray:
         cf = np.ascontiguousarray(coeffs, dtype=np.float64)
         deg = cf.size - 1
-        drop = 2 if deg == 3 else 1
+        drop = 1 if (deg == 1 or (deg == 2 and tuple(cf) == (0.0, 0.0, 1.0))) else 2
         o = out if out is not None else self.empty(x.count, max(x.level - drop, 0))
         cx, co = x.cts(), o.cts()
         self._check(_lib.edl_poly_activation(self._h, ctypes.byref(cx), _ptr(cf), deg, ctypes.byref(co)),

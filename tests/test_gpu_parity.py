@@ -301,3 +301,21 @@ def test_errors_and_empty(edl, c0pair):
     E.key_id, E.scale = o.key_id, 2.0 ** 40
     assert g.add(E, E).count == 0
     assert g.rescale(E).count == 0
+
+
+@pytest.mark.parametrize("which", ["linear", "relu_a"])
+def test_linear_and_relu_activations_bit_exact(c1pair, which):
+    """NEXT f2: the paper's linear sigmoid and ReLU_a schedules, GPU residues == oracle,
+    decrypted values == float64 polynomial within 1e-3."""
+    from oracle import networks as onet
+    g, o = c1pair
+    z = random_slots(3, 8192, seed=11, lo=-1, hi=1)
+    polys = np.stack([o.encode(v) for v in z])
+    xo = o.encrypt_poly(polys, enc_seed=2, obj0=0, scale=o.p.scale)
+    xg = g.encrypt_poly(polys, scale=o.p.scale, enc_seed=2)
+    cf = onet.SIGMA_LINEAR if which == "linear" else onet.relu_a_coeffs(1.0)
+    got, want = g.poly_activation(xg, cf), olay.poly_activation(o, xo, cf)
+    assert got.level == want.level and got.scale == want.scale
+    assert np.array_equal(got.numpy(g.n), want.data)
+    ref = 0.5 + 0.197 * z if which == "linear" else onet.relu_a(z, 1.0)
+    assert np.max(np.abs(g.decrypt(got, 8192) - ref)) < 1e-3

@@ -18,6 +18,14 @@ def test_activation_closed_forms():
     for x, y in g["sigma_a"]["values"]:
         assert abs(networks.sigma_a(x) - y) < 1e-12
     assert networks.SIGMA_A == (0.5, 0.197, 0.0, -0.004)
+    for x, q, y in g["relu_a"]["values"]:
+        assert abs(networks.relu_a(x, q) - y) < 5e-6          # golden value printed to 5 digits
+    # R_a is a degree-2 polynomial with odd part x/2: R_a(x) - R_a(-x) = x for every q
+    for q in (1.0, 5.0):
+        for x in (0.3, 1.7, -2.2):
+            assert abs(networks.relu_a(x, q) - networks.relu_a(-x, q) - x) < 1e-12
+    # it meets max(0, x) within q/(3 pi) at x = +-q (R_a(+-q) = q (1/2 +- 1/2) + 5 q/(3 pi) - ... )
+    assert abs(networks.relu_a(1.0, 1.0) - (4 / (3 * np.pi) + 0.5 + 1 / (3 * np.pi))) < 1e-12
 
 
 def test_c0_network_vs_float64():
@@ -88,3 +96,25 @@ def test_unsupported_schedule(small_ctx):
     y = ctx.encrypt(np.zeros((1, 4)), 2)
     with pytest.raises(ckks.CkksError):
         layers.poly_activation(ctx, y, (1.0, 2.0, 3.0, 4.0, 5.0))
+    with pytest.raises(ckks.CkksError):
+        layers.poly_activation(ctx, y, (1.0, 2.0, 3.0, 4.0))      # cubic with c2 != 0
+    with pytest.raises(ckks.CkksError):                               # level exhausted
+        layers.poly_activation(ctx, ctx.encrypt(np.zeros((1, 4)), 2, level=1), networks.relu_a_coeffs())
+
+
+@pytest.mark.parametrize("which", ["linear", "relu_a"])
+def test_linear_and_relu_activations_vs_float64(small_ctx, which):
+    """NEXT f2: the paper's linear sigmoid and ReLU approximation
+     schedules decrypt to the float64 polynomial within 1e-4."""
+    ctx = small_ctx
+    z = np.random.default_rng(3).uniform(-1, 1, (3, 512))
+    y = ctx.encrypt(z, 2)
+    if which == "linear":
+        out = layers.poly_activation(ctx, y, networks.SIGMA_LINEAR)
+        want = 0.5 + 0.197 * z
+        assert out.level == y.level - 1
+    else:
+        out = layers.poly_activation(ctx, y, networks.relu_a_coeffs(1.0))
+        want = networks.relu_a(z, 1.0)
+        assert out.level == y.level - 2
+    assert np.max(np.abs(ctx.decrypt(out, 512) - want)) < 1e-4
