@@ -180,6 +180,24 @@ edl_status edl_dense_finish(edl_ctx* ctx, const edl_cts* acc, const double* b, e
 edl_status edl_ntt(edl_ctx* ctx, uint64_t* limbs, int64_t n_polys, int32_t level, int32_t inverse);
 /* Raw Philox4x32-10 words for host counters ctr[n][4] with key (seed lo, seed hi). */
 edl_status edl_philox(edl_ctx* ctx, uint64_t seed, const uint32_t* ctr_host, int64_t n, uint32_t* out_host);
+/* ---- wire format (client <-> server transfer of ciphertext arrays) ----
+ * Every residue of limb i is stored in bits_i = bit length of q_i bits (60 or 40 for the
+ * Alg. 8 chains) instead of 64: per polynomial, limb i occupies
+ * N*bits_i/64 little-endian 64-bit words and coefficient k sits at bit offset k*bits_i;
+ * polynomials follow the [count][2] order of edl_cts, limbs 0..level inside each.  For C1
+ * (60 + 4 x 40 bits) this is 27.5 instead of 40 bytes per coefficient pair-limb-set:
+ * 0.69x the PCIe bytes of the 64-bit layout.
+ * edl_cts_packed_bytes: size of `count` ciphertexts at `level` (0 on bad arguments).
+ * edl_cts_pack: device array `in` -> device buffer `packed` (caller-allocated, that size).
+ * edl_cts_unpack: device buffer `packed` -> device array `out` (caller-allocated,
+ *   edl_cts_bytes), setting out's count/level/scale/key_id.  Residues must be canonical
+ *   (< q_i), which every library output is.  Asynchronous on the context's stream.
+ * Errors: EDL_ERR_ARG on null buffers or a level outside 0..L. */
+size_t edl_cts_packed_bytes(const edl_ctx* ctx, int64_t count, int32_t level);
+edl_status edl_cts_pack(edl_ctx* ctx, const edl_cts* in, void* packed);
+edl_status edl_cts_unpack(edl_ctx* ctx, const void* packed, int64_t count, int32_t level, double scale,
+                          uint64_t key_id, edl_cts* out);
+
 /* Integer-pipe ceiling: lazy Shoup 64-bit modular multiplications per second measured
  * by a register-only kernel on all SMs (the "alu" roofline peak). */
 edl_status edl_modmul_peak(edl_ctx* ctx, int32_t iters, double* modmul_per_s);

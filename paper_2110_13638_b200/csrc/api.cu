@@ -666,6 +666,51 @@ edl_status edl_dense(edl_ctx* c, const edl_cts* x, const double* Wt, const doubl
     return cuda_check(c, "dense");
 }
 
+static void limb_bits(const edl_ctx* c, int nl, int* bits) {
+    for (int i = 0; i < nl; i++) {
+        const uint64_t q = c->prm.q[i];
+        int b = 0;
+        while (b < 64 && (q >> b) != 0) b++;
+        bits[i] = b;
+    }
+}
+
+size_t edl_cts_packed_bytes(const edl_ctx* c, int64_t count, int32_t level) {
+    if (!c || count < 0 || level < 0 || level > c->L) return 0;
+    int bits[MAXM];
+    limb_bits(c, level + 1, bits);
+    size_t words = 0;
+    for (int i = 0; i <= level; i++) words += ((size_t)bits[i] << c->logn) >> 6;
+    return (size_t)count * 2 * words * 8;
+}
+
+edl_status edl_cts_pack(edl_ctx* c, const edl_cts* in, void* packed) {
+    if (!c) return EDL_ERR_ARG;
+    edl_status s = check_ct(c, in);
+    if (s != EDL_OK) return s;
+    if (in->count > 0 && !packed) return fail(c, EDL_ERR_ARG, "cts_pack: null output");
+    if (in->count > 0) {
+        int bits[MAXM];
+        limb_bits(c, in->level + 1, bits);
+        launch_pack(c->dev(), in->data, in->count * 2, in->level + 1, bits, reinterpret_cast<uint64_t*>(packed));
+    }
+    return cuda_check(c, "cts_pack");
+}
+
+edl_status edl_cts_unpack(edl_ctx* c, const void* packed, int64_t count, int32_t level, double scale, uint64_t key_id,
+                          edl_cts* out) {
+    if (!c || !out || count < 0) return EDL_ERR_ARG;
+    if (level < 0 || level > c->L) return fail(c, EDL_ERR_ARG, "cts_unpack: level out of range");
+    if (count > 0 && (!packed || !out->data)) return fail(c, EDL_ERR_ARG, "cts_unpack: null buffer");
+    if (count > 0) {
+        int bits[MAXM];
+        limb_bits(c, level + 1, bits);
+        launch_unpack(c->dev(), reinterpret_cast<const uint64_t*>(packed), count * 2, level + 1, bits, out->data);
+    }
+    set_meta(out, count, level, scale, key_id);
+    return cuda_check(c, "cts_unpack");
+}
+
 edl_status edl_mod_reduce(edl_ctx* c, edl_cts* x) {
     if (!c) return EDL_ERR_ARG;
     edl_status s = check_ct(c, x);

@@ -176,6 +176,10 @@ void launch_dense_mac(const Dev& d, const uint64_t* x, int64_t K, int64_t O, int
                       uint64_t* part = nullptr);
 int dense_split(const Dev& d, int64_t K, int64_t O, int l);
 
+// wire format: residues of limb i in bits[i] bits (pointwise.cu); polys = count * 2
+void launch_unpack(const Dev& d, const uint64_t* in, int64_t polys, int nl, const int* bits, uint64_t* out);
+void launch_pack(const Dev& d, const uint64_t* in, int64_t polys, int nl, const int* bits, uint64_t* out);
+
 // ---- randomness / keys / encryption (rng.cu) ----
 void launch_keygen(const Dev& d, uint64_t seed, uint64_t* s_hat /*[L+2][N]*/, uint64_t* pk /*[2][L+1][N]*/,
                    uint64_t* rlk /*[L+1][2][L+2][N]*/, uint64_t* rlk_s, uint64_t* scratch);

@@ -141,6 +141,15 @@ k_relin_modup(const uint64_t* __restrict__ acoef, int l, int L, uint64_t* __rest
     // j != ti, then P (ti = l+1) with all l+1 digits, so co-resident CTAs (limb-major
     // grid) share one prime: one arithmetic path in the I-cache, one twiddle table
     int ti, j;
+#ifndef EDL_MODUP_TARGET_MAJOR
+    // digit-major: the l+1 targets of one digit are consecutive rows, so the digit limb is
+    // re-read from L2
+    j = blockIdx.y / (l + 1);
+    {
+        const int tt = blockIdx.y % (l + 1);
+        ti = tt < j ? tt : tt + 1;
+    }
+#else
     if ((int)blockIdx.y < (l + 1) * l) {
         ti = blockIdx.y / l;
         const int jj = blockIdx.y % l;
@@ -149,6 +158,7 @@ k_relin_modup(const uint64_t* __restrict__ acoef, int l, int L, uint64_t* __rest
         ti = l + 1;
         j = blockIdx.y - (l + 1) * l;
     }
+#endif
     const int t = (ti == l + 1) ? (L + 1) : ti;
     const int64_t c = C::bx();
     const ModInfo& m = mods[t];

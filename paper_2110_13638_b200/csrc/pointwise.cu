@@ -481,7 +481,93 @@ k_relin_mac(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int 
     }
 }
 
+// ---------------------------------------------------------------- wire format (pack/unpack)
+// A ciphertext array travels host<->device with every residue of limb i stored in
+// bits_i = bit length of q_i (60 or 40 for the Alg. 8 chains) instead of 64: limb i of a
+// polynomial is N*bits_i/64 little-endian words, coefficient k at bit offset k*bits_i.
+// Limbs follow the [count][2][level+1] order; `loff` holds each limb's word offset within
+// one polynomial and `pw` the words per polynomial.
+struct PackInfo {
+    int bits[MAXM];
+    int64_t loff[MAXM];
+};
+
+__global__ void k_unpack(const uint64_t* __restrict__ in, int64_t polys, int nl, int64_t pw,
+                         const __grid_constant__ PackInfo pi, uint64_t* __restrict__ out, int logn) {
+    const int64_t rows = polys * nl;
+    const int n = 1 << logn;
+    for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
+        const int i = (int)(row % nl);
+        const int64_t pl = row / nl;
+        const int b = pi.bits[i];
+        const uint64_t mask = (b == 64) ? ~0ull : ((1ull << b) - 1);
+        const uint64_t* src = in + pl * pw + pi.loff[i];
+        uint64_t* dst = out + ((size_t)row << logn);
+        for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+            const uint64_t off = (uint64_t)k * b;
+            const uint64_t w = off >> 6;
+            const int sh = (int)(off & 63);
+            uint64_t v = __ldg(src + w) >> sh;
+            if (sh + b > 64) v |= __ldg(src + w + 1) << (64 - sh);
+            dst[k] = v & mask;
+        }
+    }
+}
+
+__global__ void k_pack(const uint64_t* __restrict__ in, int64_t polys, int nl, int64_t pw,
+                       const __grid_constant__ PackInfo pi, uint64_t* __restrict__ out, int logn) {
+    const int64_t rows = polys * nl;
+    const int n = 1 << logn;
+    for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
+        const int i = (int)(row % nl);
+        const int64_t pl = row / nl;
+        const int b = pi.bits[i];
+        const int64_t words = ((int64_t)n * b) >> 6;
+        const uint64_t* src = in + ((size_t)row << logn);
+        uint64_t* dst = out + pl * pw + pi.loff[i];
+        for (int64_t w = blockIdx.x * blockDim.x + threadIdx.x; w < words; w += gridDim.x * blockDim.x) {
+            // coefficients overlapping bits [64 w, 64 w + 64)
+            const uint64_t lo = (uint64_t)w << 6;
+            const int64_t k0 = lo / b, k1 = (lo + 63) / b;
+            uint64_t v = 0;
+            for (int64_t k = k0; k <= k1 && k < n; k++) {
+                const int64_t off = k * b - (int64_t)lo;   // may be negative for k0
+                const uint64_t c = src[k];
+                if (off >= 0) v |= c << off;
+                else v |= c >> (-off);
+            }
+            dst[w] = v;
+        }
+    }
+}
+
 }  // namespace
+
+static PackInfo pack_info(const Dev& d, int nl, const int* bits, int64_t* pw) {
+    PackInfo pi;
+    int64_t off = 0;
+    for (int i = 0; i < nl && i < MAXM; i++) {
+        pi.bits[i] = bits[i];
+        pi.loff[i] = off;
+        off += ((int64_t)bits[i] << d.logn) >> 6;
+    }
+    *pw = off;
+    return pi;
+}
+
+void launch_unpack(const Dev& d, const uint64_t* in, int64_t polys, int nl, const int* bits, uint64_t* out) {
+    int64_t pw = 0;
+    const PackInfo pi = pack_info(d, nl, bits, &pw);
+    EDL_LAUNCH(d, "k_unpack", k_unpack<<<rows_grid(d.logn + 1, polys * nl), PW_THREADS, 0, d.st>>>(in, polys, nl, pw, pi,
+                                                                                                     out, d.logn));
+}
+
+void launch_pack(const Dev& d, const uint64_t* in, int64_t polys, int nl, const int* bits, uint64_t* out) {
+    int64_t pw = 0;
+    const PackInfo pi = pack_info(d, nl, bits, &pw);
+    EDL_LAUNCH(d, "k_pack", k_pack<<<rows_grid(d.logn + 1, polys * nl), PW_THREADS, 0, d.st>>>(in, polys, nl, pw, pi, out,
+                                                                                                 d.logn));
+}
 
 void launch_relin_mac(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t cnt, int l, const uint64_t* xh,
                       const uint64_t* rlk, const uint64_t* rlk_c, uint64_t* acc) {

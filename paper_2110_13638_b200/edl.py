@@ -130,6 +130,10 @@ _sigs = {
     "edl_poly_activation": (_c.c_int32, [_c.c_void_p, _P(Cts), _c.c_void_p, _c.c_int32, _P(Cts)]),
     "edl_dense": (_c.c_int32, [_c.c_void_p, _P(Cts), _c.c_void_p, _c.c_void_p, _c.c_int32, _c.c_int32, _P(Cts)]),
     "edl_mod_reduce": (_c.c_int32, [_c.c_void_p, _P(Cts)]),
+    "edl_cts_packed_bytes": (_c.c_size_t, [_c.c_void_p, _c.c_int64, _c.c_int32]),
+    "edl_cts_pack": (_c.c_int32, [_c.c_void_p, _P(Cts), _c.c_void_p]),
+    "edl_cts_unpack": (_c.c_int32, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int32, _c.c_double, _c.c_uint64,
+                                    _P(Cts)]),
     "edl_dense_finish": (_c.c_int32, [_c.c_void_p, _P(Cts), _c.c_void_p, _P(Cts)]),
     "edl_ntt": (_c.c_int32, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int32, _c.c_int32]),
     "edl_philox": (_c.c_int32, [_c.c_void_p, _c.c_uint64, _c.c_void_p, _c.c_int64, _c.c_void_p]),
@@ -386,6 +390,26 @@ class Context:
         cx, co = x.cts(), o.cts()
         self._check(_lib.edl_dense(self._h, ctypes.byref(cx), _ptr(Wt), None if bb is None else _ptr(bb), O,
                                    1 if defer_rescale else 0, ctypes.byref(co)), "dense")
+        return o.update(co)
+
+    # ---- wire format
+    def packed_bytes(self, count: int, level: int) -> int:
+        return int(_lib.edl_cts_packed_bytes(self._h, count, level))
+
+    def pack(self, x: CtArray, out=None):
+        """Device ciphertext array -> packed wire bytes (int64 device tensor)."""
+        words = self.packed_bytes(x.count, x.level) // 8
+        out = out if out is not None else self.torch.empty(words, dtype=self.torch.int64, device=self.device)
+        c = x.cts()
+        self._check(_lib.edl_cts_pack(self._h, ctypes.byref(c), ctypes.c_void_p(out.data_ptr())), "cts_pack")
+        return out
+
+    def unpack(self, packed, count: int, level: int, scale: float, key_id: int, out: Optional[CtArray] = None) -> CtArray:
+        """Packed wire bytes (device tensor) -> device ciphertext array."""
+        o = out if out is not None else self.empty(count, level)
+        co = o.cts()
+        self._check(_lib.edl_cts_unpack(self._h, ctypes.c_void_p(packed.data_ptr()), count, level, scale, key_id,
+                                        ctypes.byref(co)), "cts_unpack")
         return o.update(co)
 
     def mod_reduce(self, x: CtArray) -> CtArray:

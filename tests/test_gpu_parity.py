@@ -319,3 +319,39 @@ def test_linear_and_relu_activations_bit_exact(c1pair, which):
     assert np.array_equal(got.numpy(g.n), want.data)
     ref = 0.5 + 0.197 * z if which == "linear" else onet.relu_a(z, 1.0)
     assert np.max(np.abs(g.decrypt(got, 8192) - ref)) < 1e-3
+
+
+def _host_pack(data, qs, n):
+    """Independent numpy packer of the wire format (edl.h): limb i's residues in bits(q_i)
+    bits, little-endian, coefficient k at bit k*bits."""
+    out = []
+    cnt, two, nl, _ = data.shape
+    for c in range(cnt):
+        for p in range(two):
+            for i in range(nl):
+                b = int(qs[i]).bit_length()
+                acc = 0
+                for k, v in enumerate(data[c, p, i].tolist()):
+                    acc |= int(v) << (k * b)
+                words = n * b // 64
+                out.extend((acc >> (64 * w)) & ((1 << 64) - 1) for w in range(words))
+    return np.array(out, dtype=np.uint64)
+
+
+@pytest.mark.parametrize("level", [0, 2, 4])
+def test_wire_format_pack_unpack(c1pair, level):
+    """Packed transfer format: device pack == independent host packing of the same
+    residues, unpack(pack(x)) == x, and the size is 27.5/40 of the 64-bit layout at L=4."""
+    g, o = c1pair
+    A = _rand_ct(o, 3, level, 70 + level)
+    x = _to_gpu(g, A, level, 2.0 ** 40, o.key_id)
+    nbytes = g.packed_bytes(3, level)
+    assert nbytes == 3 * 2 * sum(g.n * int(q).bit_length() // 8 for q in o.q[: level + 1])
+    packed = g.pack(x)
+    assert packed.numel() * 8 == nbytes
+    host = packed.cpu().numpy().view(np.uint64)
+    if level == 0:   # the pure-Python packer is slow; pin the bit layout on the smallest case
+        assert np.array_equal(host, _host_pack(A, o.q, g.n))
+    y = g.unpack(packed, 3, level, 2.0 ** 40, o.key_id)
+    assert y.level == level and y.count == 3 and y.scale == 2.0 ** 40
+    assert np.array_equal(y.numpy(g.n), A)
