@@ -1,0 +1,56 @@
+"""C3 tabular regression net (BASELINE.json configs[3]): dense 32->64 -> sigma_a -> dense 64->1
+on 16384 standardised N(0,1) samples (2 slot-batches of 8192, reading Z12), CKKS N=2^14.
+Reports device-timed samples/s of the encrypted forward pass (inputs resident) and the MSE
+/ max error of the decrypted predictions against float64 plaintext inference of the same
+polynomial network (numpy, no oracle).
+
+Usage: python tools/c3_bench.py [--reps 5]
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+from paper_2110_13638_b200 import edl
+from paper_2110_13638_b200.networks import C3Net, SIGMA_A
+from synth import c3_inputs
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=5)
+    a = ap.parse_args()
+    inp = c3_inputs()
+    ctx = edl.Context(edl.params_from_depth(4)).keygen(1)
+    net = C3Net(ctx, inp.W1, inp.b1, inp.W2, inp.b2)
+    xs = []
+    for b in range(2):
+        Xb = inp.X[b * 8192:(b + 1) * 8192]
+        xs.append(ctx.encrypt(Xb.T, enc_seed=2, obj0=32 * b))
+    st = ctx.stream
+    for x in xs:
+        net.forward(x)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(a.reps):
+        outs = [net.forward(x)["out"] for x in xs]
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / a.reps
+    pred = np.concatenate([ctx.decrypt(o, 8192)[0] for o in outs])
+    c0, c1, _, c3 = SIGMA_A
+    h = inp.X @ inp.W1.T + inp.b1
+    ref = (c0 + c1 * h + c3 * h ** 3) @ inp.W2.T + inp.b2
+    err = pred - ref[:, 0]
+    print(json.dumps({"config": "C3 tabular: 16384 samples x 32 features, dense 32->64, sigma_a, dense 64->1, "
+                                "N=2^14 {60,40,40,40,40|60}", "ms_per_pass": ms, "samples_per_s": 16384 / (ms / 1e3),
+                      "mse_vs_float64": float(np.mean(err ** 2)), "max_abs_err": float(np.max(np.abs(err)))}))
+
+
+if __name__ == "__main__":
+    main()
