@@ -481,6 +481,97 @@ k_relin_mac(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int 
     }
 }
 
+// Smem-staged key-product pass (l + 1 <= MAC2_MAXD digits): a thread owns one coefficient
+// pair of one target for MAC2_CTS ciphertexts; the key entries of its pair (all digits,
+// both components, with companions) are staged once in shared memory and reused for every
+// ciphertext, so each key residue is fetched from L2 once per MAC2_CTS ciphertexts, and
+// a ciphertext's l+1 digit loads are all issued before its MACs.
+constexpr int MAC2_THREADS = 128;
+constexpr int MAC2_MAXD = 8;
+constexpr int MAC2_CTS = 16;
+
+template <bool FP, int MAXD>
+__global__ void __launch_bounds__(MAC2_THREADS, 6)
+k_relin_mac2(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l, int L, int64_t cnt,
+             const uint64_t* __restrict__ xh, const uint64_t* __restrict__ rlk, const uint64_t* __restrict__ rlk_c,
+             uint64_t* __restrict__ acc, const __grid_constant__ TargetList tl, const __grid_constant__ ModTable mods,
+             const ChainConsts* __restrict__ chain, int logn) {
+    // [digit][comp][thread] {key pair, companion pair}
+    extern __shared__ ulonglong2 ks[];
+    const int ti = tl.slot[blockIdx.y];
+    const int t = (ti == l + 1) ? (L + 1) : ti;
+    const ModInfo& m = mods[t];
+    const int k = blockIdx.x * MAC2_THREADS + threadIdx.x;   // coefficient pair
+    const int nd = l + 1;
+    const bool active = 2 * k < (1 << logn);
+    if (active) {
+        for (int j = 0; j < nd; j++)
+#pragma unroll
+            for (int cc = 0; cc < 2; cc++) {
+                const size_t o = (((size_t)j * 2 + cc) * (L + 2) + t) << logn;
+                ks[((j * 2 + cc) * 2 + 0) * MAC2_THREADS + threadIdx.x] = __ldg(v2(rlk + o) + k);
+                if constexpr (FP) ks[((j * 2 + cc) * 2 + 1) * MAC2_THREADS + threadIdx.x] = __ldg(v2(rlk_c + o) + k);
+            }
+    }
+    if (!active) return;   // no block-wide barrier below: each thread reads only its own slice
+    const ulonglong2 pinv = (ti <= l) ? chain->qinv[L + 1][t] : make_ulonglong2(0, 0);
+    const int64_t c_end = ((int64_t)blockIdx.z + 1) * MAC2_CTS < cnt ? ((int64_t)blockIdx.z + 1) * MAC2_CTS : cnt;
+    // (a software pipeline over the ciphertexts measured slower: 124 registers cost more
+    // occupancy than the overlap bought)
+    for (int64_t c = (int64_t)blockIdx.z * MAC2_CTS; c < c_end; c++) {
+        ulonglong2 x[MAXD];
+#pragma unroll
+        for (int j = 0; j < MAXD; j++) {
+            if (j >= nd) break;
+            if (j == ti) {
+                const ulonglong2 a1 = v2(a + limb_off(c, 1, j, l + 1, logn))[k];
+                const ulonglong2 b1 = v2(b + limb_off(c, 1, j, l + 1, logn))[k];
+                x[j] = make_ulonglong2(mulmod(a1.x, b1.x, m), mulmod(a1.y, b1.y, m));
+            } else {
+                x[j] = v2(xh + ((((size_t)c * (l + 1) + j) * (l + 2) + ti) << logn))[k];
+            }
+        }
+        ulonglong2 v[2];
+#pragma unroll
+        for (int cc = 0; cc < 2; cc++) {
+            if constexpr (FP) {
+                uint64_t s0 = 0, s1 = 0;
+#pragma unroll
+                for (int j = 0; j < MAXD; j++) {
+                    if (j >= nd) break;
+                    const ulonglong2 r = ks[((j * 2 + cc) * 2 + 0) * MAC2_THREADS + threadIdx.x];
+                    const ulonglong2 q = ks[((j * 2 + cc) * 2 + 1) * MAC2_THREADS + threadIdx.x];
+                    s0 += tw_mul_fp(x[j].x, r.x, q.x, m.q);
+                    s1 += tw_mul_fp(x[j].y, r.y, q.y, m.q);
+                }
+                v[cc] = make_ulonglong2(reduce64(s0, m), reduce64(s1, m));
+            } else {
+                U128 s0, s1;
+                s0.lo = s0.hi = s1.lo = s1.hi = 0;
+#pragma unroll
+                for (int j = 0; j < MAXD; j++) {
+                    if (j >= nd) break;
+                    const ulonglong2 r = ks[((j * 2 + cc) * 2 + 0) * MAC2_THREADS + threadIdx.x];
+                    mac128(s0, x[j].x, r.x);
+                    mac128(s1, x[j].y, r.y);
+                }
+                v[cc] = make_ulonglong2(barrett128(s0, m), barrett128(s1, m));
+            }
+        }
+        if (ti <= l) {   // fold the tensor's d0, d1: v = d + acc P^-1
+            const ulonglong2 a0 = v2(a + limb_off(c, 0, ti, l + 1, logn))[k], a1 = v2(a + limb_off(c, 1, ti, l + 1, logn))[k];
+            const ulonglong2 b0 = v2(b + limb_off(c, 0, ti, l + 1, logn))[k], b1 = v2(b + limb_off(c, 1, ti, l + 1, logn))[k];
+            const uint64_t d0x = mulmod(a0.x, b0.x, m), d0y = mulmod(a0.y, b0.y, m);
+            const uint64_t d1x = addmod(mulmod(a0.x, b1.x, m), mulmod(a1.x, b0.x, m), m.q);
+            const uint64_t d1y = addmod(mulmod(a0.y, b1.y, m), mulmod(a1.y, b0.y, m), m.q);
+            v[0] = make_ulonglong2(addmod(d0x, mulc(v[0].x, pinv, m), m.q), addmod(d0y, mulc(v[0].y, pinv, m), m.q));
+            v[1] = make_ulonglong2(addmod(d1x, mulc(v[1].x, pinv, m), m.q), addmod(d1y, mulc(v[1].y, pinv, m), m.q));
+        }
+#pragma unroll
+        for (int cc = 0; cc < 2; cc++) v2(acc + ((((size_t)c * 2 + cc) * (l + 2) + ti) << logn))[k] = v[cc];
+    }
+}
+
 // ---------------------------------------------------------------- wire format (pack/unpack)
 // A ciphertext array travels host<->device with every residue of limb i stored in
 // bits_i = bit length of q_i (60 or 40 for the Alg. 8 chains) instead of 64: limb i of a
@@ -578,6 +669,31 @@ void launch_relin_mac(const Dev& d, const uint64_t* a, const uint64_t* b, int64_
         const int t = (s == l + 1) ? d.L + 1 : s;
         if (d.hmods[t].fp) tf.slot[nf++] = (int8_t)s;
         else ti.slot[ni++] = (int8_t)s;
+    }
+    if (l + 1 <= MAC2_MAXD && d.logn >= 8) {
+        const unsigned gx2 = (unsigned)((1 << d.logn) / (2 * MAC2_THREADS)), gz2 = (unsigned)((cnt + MAC2_CTS - 1) / MAC2_CTS);
+        const size_t smem = (size_t)(l + 1) * 2 * 2 * MAC2_THREADS * sizeof(ulonglong2);
+        static bool attr = false;
+        if (!attr) {
+            const int mx = MAC2_MAXD * 2 * 2 * MAC2_THREADS * 16;
+            cudaFuncSetAttribute(k_relin_mac2<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+            cudaFuncSetAttribute(k_relin_mac2<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+            cudaFuncSetAttribute(k_relin_mac2<true, MAC2_MAXD>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+            cudaFuncSetAttribute(k_relin_mac2<false, MAC2_MAXD>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+            attr = true;
+        }
+#define EDL_MAC2(FPV, MD, LIST, NT)                                                                         \
+    EDL_LAUNCH(d, "k_relin_mac", (k_relin_mac2<FPV, MD><<<dim3(gx2, NT, gz2), MAC2_THREADS, smem, d.st>>>( \
+                                     a, b, l, d.L, cnt, xh, rlk, rlk_c, acc, LIST, *d.mt, d.cc, d.logn)))
+        if (l + 1 <= 4) {
+            if (nf) EDL_MAC2(true, 4, tf, nf);
+            if (ni) EDL_MAC2(false, 4, ti, ni);
+        } else {
+            if (nf) EDL_MAC2(true, MAC2_MAXD, tf, nf);
+            if (ni) EDL_MAC2(false, MAC2_MAXD, ti, ni);
+        }
+#undef EDL_MAC2
+        return;
     }
     const unsigned gx = (unsigned)((1 << d.logn) / (2 * PW_THREADS)), gz = (unsigned)((cnt + MAC_CB - 1) / MAC_CB);
     if (nf)
