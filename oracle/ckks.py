@@ -262,8 +262,11 @@ class Context:
                 d[c, 2, i] = ring.mul(a1, b1, q)
         return d, lvl, a.scale * b.scale
 
-    def keyswitch_acc(self, d2: np.ndarray, lvl: int) -> np.ndarray:
-        """O11 steps 1-3: acc [2][lvl+2][N] over targets (q_0..q_lvl, P), NTT domain."""
+    def keyswitch_acc(self, d2: np.ndarray, lvl: int, key: Optional[np.ndarray] = None) -> np.ndarray:
+        """O11 steps 1-3: acc [2][lvl+2][N] over targets (q_0..q_lvl, P), NTT domain.
+        `key` [L+1][2][L+2][N] defaults to the relinearisation key (Galois keys, NEXT f1,
+        use the same digit structure)."""
+        key = self.rlk if key is None else key
         n = self.n
         pidx = self.L + 1
         # step 1: a_j = INTT_{q_j}(d2[j])
@@ -277,7 +280,7 @@ class Context:
                 x = self.ntt(ring.reduce(a[j].copy(), mt)[None, :], [t])[0]
                 # step 3: acc_{c,t} += x * rlk_j[c][t]
                 for c in range(2):
-                    acc[c, ti] = ring.add(acc[c, ti], ring.mul(x, self.rlk[j, c, t], mt), mt)
+                    acc[c, ti] = ring.add(acc[c, ti], ring.mul(x, key[j, c, t], mt), mt)
         return acc
 
     def mod_down(self, acc: np.ndarray, lvl: int) -> np.ndarray:
@@ -292,9 +295,9 @@ class Context:
                 out[c, i] = ring.mul_scalar(ring.sub(acc[c, i], rq, q), ring.inv(P % q, q), q)
         return out
 
-    def keyswitch(self, d2: np.ndarray, lvl: int) -> np.ndarray:
+    def keyswitch(self, d2: np.ndarray, lvl: int, key: Optional[np.ndarray] = None) -> np.ndarray:
         """O11 steps 1-4 for one polynomial d2 [lvl+1][N] (NTT) -> (out0, out1) [2][lvl+1][N]."""
-        return self.mod_down(self.keyswitch_acc(d2, lvl), lvl)
+        return self.mod_down(self.keyswitch_acc(d2, lvl, key), lvl)
 
     def relinearize(self, d: np.ndarray, lvl: int, scale: float) -> CtArray:
         count = d.shape[0]

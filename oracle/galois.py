@@ -1,0 +1,154 @@
+"""Oracle: Galois rotations and plaintext-vector products for the paper's own CNN layout
+(kernel masquerading).  TEST INFRASTRUCTURE ONLY.
+
+Background (not in the paper, which delegates to MS-SEAL): the automorphism
+sigma_g : a(X) -> a(X^g) (g odd) maps a CKKS slot vector z to z rotated left by r when
+g = 5^r mod 2N (slot j <-> zeta^{5^j}, O5).  A ciphertext (c0, c1) under s becomes
+(sigma_g c0, sigma_g c1) under sigma_g s; switching sigma_g c1 back to s uses a Galois key
+with the relinearisation key's digit structure (O11) and gadget term P sigma_g(s):
+  gk_j[0][i] = -a_j s + e_j + delta_ij (P mod q_i) sigma_g(s),  gk_j[1][i] = a_j,
+a_j ~ Philox uniform (tag 9, object 64 g + j, limb i), e_j ~ CBD (tag 10, object 64 g + j).
+Every function follows the definition step by step (coefficient-domain automorphism,
+then NTT); the GPU path permutes NTT-domain residues instead and shares nothing.
+"""
+from __future__ import annotations
+
+from typing import Dict, Sequence
+
+import numpy as np
+
+from . import ring, sampling as smp
+from .ckks import Context, CtArray, CkksError
+
+
+def galois_element(r: int, n: int) -> int:
+    """g = 5^r mod 2N: left rotation of the N/2 slots by r (negative r: right)."""
+    return pow(5, r % (n // 2), 2 * n)
+
+
+def automorphism_coeff(a: np.ndarray, g: int, q: int) -> np.ndarray:
+    """Coefficient domain: X^j -> X^{j g mod 2N} with X^N = -1 (residues mod q)."""
+    n = a.shape[-1]
+    out = np.zeros(n, dtype=np.uint64)
+    for j in range(n):
+        e = (j * g) % (2 * n)
+        v = int(a[j])
+        if e >= n:
+            e -= n
+            v = (q - v) % q
+        out[e] = v
+    return out
+
+
+def automorphism_ntt(ctx: Context, a_hat: np.ndarray, g: int, idx: Sequence[int]) -> np.ndarray:
+    """sigma_g on NTT-domain rows [len(idx)][N] (modulus index idx[r] for row r)."""
+    coeff = ctx.intt(a_hat.copy(), list(idx))
+    rows = np.stack([automorphism_coeff(coeff[r], g, ctx.moduli[i]) for r, i in enumerate(idx)])
+    return ctx.ntt(rows, list(idx))
+
+
+def galois_keygen(ctx: Context, seed: int, g: int) -> np.ndarray:
+    """Galois key for element g: [L+1 digits][2][L+2 limbs][N], NTT domain."""
+    n, L = ctx.n, ctx.L
+    all_idx = list(range(L + 2))
+    s_g = automorphism_ntt(ctx, ctx.s_hat, g, all_idx)             # sigma_g(s), every limb incl. P
+    gk = np.zeros((L + 1, 2, L + 2, n), dtype=np.uint64)
+    for j in range(L + 1):
+        obj = 64 * g + j
+        ej_hat = ctx.signed_to_ntt(smp.cbd(n, seed, obj, smp.TAG_GK_E), all_idx)
+        for i in all_idx:
+            m = ctx.moduli[i]
+            aj = smp.uniform(n, seed, obj, i, smp.TAG_GK_A, m)
+            bj = ring.sub(ej_hat[i], ring.mul(aj, ctx.s_hat[i], m), m)
+            if i == j:
+                bj = ring.add(bj, ring.mul_scalar(s_g[i], ctx.P % m, m), m)
+            gk[j, 0, i] = bj
+            gk[j, 1, i] = aj
+    return gk
+
+
+def rotate(ctx: Context, ct: CtArray, r: int, gkeys: Dict[int, np.ndarray]) -> CtArray:
+    """Slots rotated left by r: (sigma_g c0 + ks_0, ks_1), ks = keyswitch(sigma_g c1, gk_g)."""
+    n = ctx.n
+    g = galois_element(r, n)
+    if g not in gkeys:
+        raise CkksError(f"no Galois key for rotation {r}")
+    lvl = ct.level
+    idx = list(range(lvl + 1))
+    out = np.empty_like(ct.data)
+    for c in range(ct.count):
+        c0 = automorphism_ntt(ctx, ct.data[c, 0], g, idx)
+        c1 = automorphism_ntt(ctx, ct.data[c, 1], g, idx)
+        ks = ctx.keyswitch(c1, lvl, gkeys[g])
+        for i in idx:
+            out[c, 0, i] = ring.add(c0[i], ks[0, i], ctx.q[i])
+            out[c, 1, i] = ks[1, i]
+    return CtArray(out, lvl, ct.scale, ct.key_id)
+
+
+def encode_plain(ctx: Context, z: np.ndarray, scale: float, level: int) -> np.ndarray:
+    """Plaintext vector z -> NTT-domain residues [level+1][N] (O5 encode, then NTT)."""
+    m = ctx.encode(z, scale)
+    return ctx.signed_to_ntt(m, list(range(level + 1)))
+
+
+def mul_plain(ctx: Context, ct: CtArray, pt_hat: np.ndarray, pt_scale: float) -> CtArray:
+    """ct_c <- ct_c (.) pt_c (NTT-domain pointwise, both polys); pt_hat [count][L'+1][N]
+    with L' >= ct.level; no rescale (O10 with a vector plaintext)."""
+    out = np.empty_like(ct.data)
+    for c in range(ct.count):
+        for k in range(2):
+            for i in range(ct.level + 1):
+                out[c, k, i] = ring.mul(ct.data[c, k, i], pt_hat[c, i], ctx.q[i])
+    return CtArray(out, ct.level, ct.scale * pt_scale, ct.key_id)
+
+
+def masquerade_masks(K: np.ndarray, H: int, W: int, stride: int) -> np.ndarray:
+    """Kernel masquerading (SPEC masquerade_kernel) for non-overlapping
+    windows: one H*W mask per filter holding K[f] at every window position."""
+    F, kh, kw = K.shape
+    Ho, Wo = (H - kh) // stride + 1, (W - kw) // stride + 1
+    masks = np.zeros((F, H * W))
+    for f in range(F):
+        for r in range(Ho):
+            for c in range(Wo):
+                for u in range(kh):
+                    for v in range(kw):
+                        masks[f, (r * stride + u) * W + c * stride + v] += K[f, u, v]
+    return masks
+
+
+def window_rotations(kh: int, kw: int, W: int):
+    """Rotations that sum a kh x kw window into its top-left slot (power-of-two sizes)."""
+    out = []
+    s = 1
+    while s < kw:
+        out.append(s)
+        s *= 2
+    s = 1
+    while s < kh:
+        out.append(s * W)
+        s *= 2
+    return out
+
+
+def masked_cc(ctx: Context, x: CtArray, K: np.ndarray, H: int, W: int, stride: int, bias, gkeys) -> CtArray:
+    """The paper's CC on one-image-per-ciphertext input (kernel masquerading): per filter,
+    Rescale(x (.) mask_f @ q_l), then the window sums by rotations and adds, then + b_f.
+    Output [count*F] (image-major), window (r, c)'s value in slot (r stride) W + c stride."""
+    F, kh, kw = K.shape
+    l = x.level
+    ql = float(ctx.q[l])
+    masks = masquerade_masks(K, H, W, stride)
+    outs = []
+    for f in range(F):
+        pt = encode_plain(ctx, masks[f], ql, l)
+        pts = np.broadcast_to(pt, (x.count,) + pt.shape)
+        y = ctx.rescale(mul_plain(ctx, x, pts, ql))
+        for rr in window_rotations(kh, kw, W):
+            y = ctx.add(y, rotate(ctx, y, rr, gkeys))
+        if bias is not None:
+            y = ctx.add_scalar(y, [bias[f]] * y.count)
+        outs.append(y)
+    data = np.stack([o.data for o in outs], axis=1).reshape((x.count * F,) + outs[0].data.shape[1:])
+    return CtArray(data, outs[0].level, outs[0].scale, x.key_id)

@@ -4,6 +4,7 @@
 // every residue is produced by the sm_100a kernels in *.cu.
 #include <cuda_runtime.h>
 
+#include <cfenv>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -291,6 +292,14 @@ edl_status edl_ctx_create(const edl_params* p, int32_t device, void* stream, edl
         m.w1ninv = host::mulmod(ti[2 * 1], m.ninv, q);
         m.w1ninv_s = host::mul_companion(m.w1ninv, q);
         m.qinv_d = 1.0 / (double)q;
+        {
+            const int old = std::fegetround();
+            std::fesetround(FE_DOWNWARD);
+            volatile double one = 1.0, qd = (double)q;
+            volatile double r = one / qd;
+            std::fesetround(old);
+            m.qinv_rd = r;
+        }
         c->h_mods[k] = m;
     }
     c->h_cc = new ChainConsts();

@@ -26,6 +26,7 @@ struct ModInfo {
     uint64_t fp;                // 1: q < 2^50, every constant companion is RD(w/q) as binary64
                                 //    (tw_mul<true>) and variable products use mulmod_fp
     double qinv_d;              // RN(1/q) (mulmod_fp)
+    double qinv_rd;             // RD(1/q) (twiddle companions computed on the fly)
 };
 
 struct U128 {
@@ -96,6 +97,18 @@ __device__ __forceinline__ uint64_t tw_mul_fp(uint64_t y, uint64_t w, uint64_t w
     const double magic = 4503599627370496.0;   // 2^52
     const double yd = __hiloint2double(0x43300000 | (uint32_t)(y >> 32), (uint32_t)y) - magic;
     const double t = __fma_rd(yd, __longlong_as_double((long long)wq_bits), magic);
+    const uint64_t qt = (uint64_t)__double_as_longlong(t) & 0xFFFFFFFFFFFFFull;
+    return y * w - qt * q;
+}
+
+// FP64-quotient product with the companion made on the fly from w alone:
+// wq = RD(w_d RD(1/q)) <= w/q and w/q - wq < 2^-52, so y (w/q - wq) < 1 for y < 2^52 and
+// floor(y wq) is again qt or qt - 1 (2 more FP64 instructions, half the twiddle bytes).
+__device__ __forceinline__ uint64_t tw_mul_fp_w(uint64_t y, uint64_t w, double qinv_rd, uint64_t q) {
+    const double magic = 4503599627370496.0;   // 2^52
+    const double wq = __dmul_rd(__hiloint2double(0x43300000 | (uint32_t)(w >> 32), (uint32_t)w) - magic, qinv_rd);
+    const double yd = __hiloint2double(0x43300000 | (uint32_t)(y >> 32), (uint32_t)y) - magic;
+    const double t = __fma_rd(yd, wq, magic);
     const uint64_t qt = (uint64_t)__double_as_longlong(t) & 0xFFFFFFFFFFFFFull;
     return y * w - qt * q;
 }

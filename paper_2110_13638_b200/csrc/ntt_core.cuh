@@ -142,7 +142,7 @@ __device__ __forceinline__ void gs_bfly(uint64_t& X, uint64_t& Y, uint64_t w, ui
 // above the stage window (SURVEY O3 stage twiddle psi^brv(m+i)).
 template <int SA, int NS, bool FP>
 __device__ __forceinline__ void fwd_pass_regs(uint64_t* x, int high, const ulonglong2* __restrict__ tw, uint64_t q,
-                                              uint64_t two_q) {
+                                              uint64_t two_q, double qinv_rd = 0.0) {
 #pragma unroll
     for (int k = 0; k < NS; k++) {
         const int half = 1 << (NS - 1 - k);
@@ -150,6 +150,16 @@ __device__ __forceinline__ void fwd_pass_regs(uint64_t* x, int high, const ulong
         for (int r = 0; r < (1 << NS); r++) {
             if (r & half) continue;
             const int tidx = (1 << (SA + k)) + (high << k) + (r >> (NS - k));
+#ifdef EDL_FP_TW_COMPACT
+            if constexpr (FP) {
+                const uint64_t wv = __ldg(reinterpret_cast<const unsigned long long*>(tw + tidx));
+                uint64_t xx = csub(x[r], two_q);
+                uint64_t t = tw_mul_fp_w(x[r + half], wv, qinv_rd, q);
+                x[r] = xx + t;
+                x[r + half] = xx - t + two_q;
+                continue;
+            }
+#endif
             ulonglong2 w = __ldg(tw + tidx);
             ct_bfly<FP>(x[r], x[r + half], w, q, two_q);
         }
@@ -175,6 +185,15 @@ __device__ __forceinline__ void inv_pass_regs(uint64_t* x, int high, const ModIn
                 x[r + half] = tw_mul<FP>(a - b + two_q, m.w1ninv, m.w1ninv_s, m.q);
             } else {
                 const int tidx = (1 << (SA + k)) + (high << k) + (r >> (NS - k));
+#ifdef EDL_FP_TW_COMPACT
+                if constexpr (FP) {
+                    const uint64_t wv = __ldg(reinterpret_cast<const unsigned long long*>(m.tw_inv + tidx));
+                    const uint64_t xa = x[r], ya = x[r + half];
+                    x[r] = csub(xa + ya, two_q);
+                    x[r + half] = tw_mul_fp_w(xa - ya + two_q, wv, m.qinv_rd, m.q);
+                    continue;
+                }
+#endif
                 ulonglong2 w = __ldg(m.tw_inv + tidx);
                 gs_bfly<FP>(x[r], x[r + half], w.x, w.y, m.q, two_q);
             }
@@ -216,7 +235,7 @@ __device__ __forceinline__ void pass_smem(uint64_t* sm, const ModInfo& m, uint64
         const int v = threadIdx.x + g * C::T;
         const int high = hc | (v >> PI::BLOW);
         if constexpr (INV) inv_pass_regs<PI::SA, PI::NS, false, FP>(x + g * (1 << PI::NS), high, m, two_q);
-        else fwd_pass_regs<PI::SA, PI::NS, FP>(x + g * (1 << PI::NS), high, m.tw_fwd, m.q, two_q);
+        else fwd_pass_regs<PI::SA, PI::NS, FP>(x + g * (1 << PI::NS), high, m.tw_fwd, m.q, two_q, m.qinv_rd);
     }
 #pragma unroll
     for (int g = 0; g < PI::G; g++) {
@@ -265,7 +284,7 @@ __device__ __forceinline__ void ntt_fwd_impl(uint64_t* sm, const ModInfo& m, Loa
         for (int g = 0; g < C::E / C::K; g++) {
 #pragma unroll
             for (int t = 0; t < C::K; t++) x[g * C::K + t] = load(j0 + g * C::T + t * C::M);
-            fwd_pass_regs<0, C::LOGK, FP>(x + g * C::K, 0, m.tw_fwd, q, two_q);
+            fwd_pass_regs<0, C::LOGK, FP>(x + g * C::K, 0, m.tw_fwd, q, two_q, m.qinv_rd);
         }
         cluster_sync_all();   // every CTA is running and done with its shared memory
 #pragma unroll
@@ -278,7 +297,7 @@ __device__ __forceinline__ void ntt_fwd_impl(uint64_t* sm, const ModInfo& m, Loa
 #pragma unroll
         for (int r = 0; r < C::E; r++) x[r] = sm[spad(tid + r * C::T)];
     }
-    fwd_pass_regs<C::LOGK, C::LOGE, FP>(x, C::crank(), m.tw_fwd, q, two_q);
+    fwd_pass_regs<C::LOGK, C::LOGE, FP>(x, C::crank(), m.tw_fwd, q, two_q, m.qinv_rd);
 #pragma unroll
     for (int r = 0; r < C::E; r++) sm[spad(tid + r * C::T)] = x[r];
     __syncthreads();

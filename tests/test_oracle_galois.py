@@ -1,0 +1,89 @@
+"""Pins for the oracle's Galois rotations, plaintext-vector products and kernel
+masquerading (NEXT f1): group identities of the automorphism,
+decrypt(rotate(encrypt(z), r)) == z rotated by r, masked cross-correlation == the float64
+cross-correlation at every window anchor."""
+import numpy as np
+import pytest
+
+from oracle import ckks, galois, networks, ring
+from oracle.params import make_params
+
+
+@pytest.fixture(scope="module")
+def small():
+    ctx = ckks.Context(make_params(1024, [60, 40, 40, 40, 40, 60])).keygen(1)
+    return ctx
+
+
+def test_automorphism_group_identities(small):
+    ctx = small
+    n, q = ctx.n, ctx.q[1]
+    a = np.random.default_rng(0).integers(0, q, n, dtype=np.uint64)
+    assert np.array_equal(galois.automorphism_coeff(a, 1, q), a)
+    for g, h in ((5, 25), (3, 7), (5, 2 * n - 1)):
+        lhs = galois.automorphism_coeff(galois.automorphism_coeff(a, h, q), g, q)
+        assert np.array_equal(lhs, galois.automorphism_coeff(a, (g * h) % (2 * n), q))
+    # X -> X^(2N-1) = -X^(N-1) on the monomial X
+    x = np.zeros(n, dtype=np.uint64)
+    x[1] = 1
+    y = galois.automorphism_coeff(x, 2 * n - 1, q)
+    assert int(y[n - 1]) == q - 1 and int(y.sum()) == q - 1
+    assert galois.galois_element(0, n) == 1 and galois.galois_element(1, n) == 5
+    assert galois.galois_element(-1, n) * 5 % (2 * n) == 1
+
+
+def test_automorphism_ntt_matches_coefficients(small):
+    ctx = small
+    idx = [0, 1]
+    a = np.random.default_rng(1).integers(0, ctx.q[1], (2, ctx.n), dtype=np.uint64)
+    a[0] %= np.uint64(ctx.q[0])
+    a_hat = ctx.ntt(a.copy(), idx)
+    got = ctx.intt(galois.automorphism_ntt(ctx, a_hat, 25, idx), idx)
+    for r, i in enumerate(idx):
+        assert np.array_equal(got[r], galois.automorphism_coeff(a[r], 25, ctx.q[i]))
+
+
+@pytest.mark.parametrize("r", [1, 3, -2])
+def test_rotation_decrypts_to_rotated_slots(small, r):
+    ctx = small
+    z = np.random.default_rng(2).uniform(-1, 1, (2, ctx.n // 2))
+    x = ctx.encrypt(z, 2)
+    gk = {galois.galois_element(r, ctx.n): galois.galois_keygen(ctx, 7, galois.galois_element(r, ctx.n))}
+    y = galois.rotate(ctx, x, r, gk)
+    assert y.level == x.level and y.scale == x.scale
+    assert np.max(np.abs(ctx.decrypt(y, ctx.n // 2) - np.roll(z, -r, axis=1))) < 1e-5
+
+
+def test_plain_vector_product(small):
+    ctx = small
+    rng = np.random.default_rng(3)
+    z, w = rng.uniform(-1, 1, (2, 512)), rng.uniform(-1, 1, 512)
+    x = ctx.encrypt(z, 2)
+    l = x.level
+    pt = galois.encode_plain(ctx, w, float(ctx.q[l]), l)
+    y = ctx.rescale(galois.mul_plain(ctx, x, np.broadcast_to(pt, (2,) + pt.shape), float(ctx.q[l])))
+    assert np.max(np.abs(ctx.decrypt(y, 512) - z * w)) < 1e-5
+
+
+def test_masked_cc_matches_float64(small):
+    """Kernel masquerading + rotation sums on an 8x8 image, 2 filters 4x4 stride 4."""
+    ctx = small
+    rng = np.random.default_rng(4)
+    imgs = rng.integers(0, 256, (2, 8, 8)) / 255.0
+    K, kb = rng.normal(0, 0.1, (2, 4, 4)), rng.normal(0, 0.1, 2)
+    slots = np.zeros((2, ctx.n // 2))
+    slots[:, :64] = imgs.reshape(2, 64)
+    x = ctx.encrypt(slots, 2)
+    rots = galois.window_rotations(4, 4, 8)
+    assert rots == [1, 2, 8, 16]
+    gk = {galois.galois_element(r, ctx.n): galois.galois_keygen(ctx, 7, galois.galois_element(r, ctx.n)) for r in rots}
+    y = galois.masked_cc(ctx, x, K, 8, 8, 4, kb, gk)
+    assert y.count == 4 and y.level == x.level - 1
+    dec = ctx.decrypt(y, 64).reshape(2, 2, 64)                     # [image][filter][slot]
+    want = networks.cc_float64(imgs, K, kb)                         # [image][filter*windows]
+    for b in range(2):
+        for f in range(2):
+            for rr in range(2):
+                for cc in range(2):
+                    got = dec[b, f, (rr * 4) * 8 + cc * 4]
+                    assert abs(got - want[b, f * 4 + rr * 2 + cc]) < 1e-4
