@@ -180,6 +180,32 @@ edl_status edl_dense_finish(edl_ctx* ctx, const edl_cts* acc, const double* b, e
 edl_status edl_ntt(edl_ctx* ctx, uint64_t* limbs, int64_t n_polys, int32_t level, int32_t inverse);
 /* Raw Philox4x32-10 words for host counters ctr[n][4] with key (seed lo, seed hi). */
 edl_status edl_philox(edl_ctx* ctx, uint64_t seed, const uint32_t* ctr_host, int64_t n, uint32_t* out_host);
+/* ---- NEXT f1: the paper's one-image-per-ciphertext layout (kernel masquerading,
+ * PAPER.md:279-292): Galois rotations and plaintext vectors ----
+ * Rotation by r slots (left; negative r: right) = the automorphism sigma_g, g = 5^r mod 2N
+ * (a permutation of NTT-domain residues), then the key switch of sigma_g(c1) back to s
+ * with a Galois key that has the relinearisation key's digit structure and gadget term
+ * P sigma_g(s) (Philox tags 9/10, object 64 g + digit).  Bit-exact with oracle/galois.py.
+ * edl_galois_keygen: keys for each rotation in steps[0..n) (after edl_keygen; the keys live
+ *   in the context, ~2 x (L+1)(L+2) 2 N x 8 bytes each).  EDL_ERR_NOKEY without a secret key.
+ * edl_rotate: out = in rotated by `steps` slots, same level and scale.  EDL_ERR_NOKEY if no
+ *   Galois key for that rotation; out must not alias in.
+ * edl_encode_pt: host slots [n_vec][n_slots] -> device NTT-domain plaintexts
+ *   pt_out [n_vec][level+1][N] at `scale` (O5 encode, then NTT per limb).  Synchronises.
+ * edl_encode_pt_poly: device integer polynomials [n_vec][N] -> pt_out (the bit-exact entry
+ *   point, like edl_encrypt_poly: host encoders differ by +-1 in rounding, reading Z1).
+ * edl_ct_pt_vec_mul: out = a (.) pt (both polys, NTT domain), scale a.scale * pt_scale, no
+ *   rescale; pt_count = 1 (broadcast) or a.count, pt_level >= a.level (else EDL_ERR_LEVEL).
+ * edl_export_galois_key: copy the key of rotation `steps` to host ([L+1][2][L+2][N]). */
+edl_status edl_galois_keygen(edl_ctx* ctx, uint64_t seed, const int32_t* steps, int32_t n_steps);
+edl_status edl_rotate(edl_ctx* ctx, const edl_cts* in, int32_t steps, edl_cts* out);
+edl_status edl_encode_pt(edl_ctx* ctx, const double* slots, int64_t n_vec, int64_t n_slots, double scale, int32_t level,
+                         uint64_t* pt_out);
+edl_status edl_encode_pt_poly(edl_ctx* ctx, const int64_t* poly, int64_t n_vec, int32_t level, uint64_t* pt_out);
+edl_status edl_ct_pt_vec_mul(edl_ctx* ctx, const edl_cts* a, const uint64_t* pt, int64_t pt_count, int32_t pt_level,
+                             double pt_scale, edl_cts* out);
+edl_status edl_export_galois_key(edl_ctx* ctx, int32_t steps, uint64_t* host_out, size_t words);
+
 /* ---- wire format (client <-> server transfer of ciphertext arrays) ----
  * Every residue of limb i is stored in bits_i = bit length of q_i bits (60 or 40 for the
  * Alg. 8 chains) instead of 64: per polynomial, limb i occupies

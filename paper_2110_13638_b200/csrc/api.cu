@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -34,6 +35,7 @@ struct edl_ctx {
     uint64_t* d_pk = nullptr;
     uint64_t* d_rlk = nullptr;
     uint64_t* d_rlk_s = nullptr;
+    std::map<uint32_t, std::pair<uint64_t*, uint64_t*>> gkeys;   // Galois element -> (key, companions)
     bool has_key = false;
     uint64_t key_id = 0;
     uint64_t* d_scratch = nullptr;
@@ -345,6 +347,10 @@ void edl_ctx_destroy(edl_ctx* c) {
     cudaFree(c->d_pk);
     cudaFree(c->d_rlk);
     cudaFree(c->d_rlk_s);
+    for (auto& kv : c->gkeys) {
+        cudaFree(kv.second.first);
+        cudaFree(kv.second.second);
+    }
     cudaFree(c->d_scratch);
     cudaFree(c->d_const);
     if (c->h_pin) cudaFreeHost(c->h_pin);
@@ -720,6 +726,100 @@ edl_status edl_cts_unpack(edl_ctx* c, const void* packed, int64_t count, int32_t
     return cuda_check(c, "cts_unpack");
 }
 
+// ---- NEXT f1: Galois rotations and plaintext vectors ----
+static uint32_t galois_elt(const edl_ctx* c, int32_t steps) {
+    const int64_t half = c->N / 2, two_n = 2 * c->N;
+    int64_t r = ((int64_t)steps % half + half) % half;
+    uint64_t g = 1, b = 5;
+    while (r) {
+        if (r & 1) g = (g * b) % (uint64_t)two_n;
+        b = (b * b) % (uint64_t)two_n;
+        r >>= 1;
+    }
+    return (uint32_t)g;
+}
+
+edl_status edl_galois_keygen(edl_ctx* c, uint64_t seed, const int32_t* steps, int32_t n_steps) {
+    if (!c || (n_steps > 0 && !steps) || n_steps < 0) return EDL_ERR_ARG;
+    if (!c->has_key) return fail(c, EDL_ERR_NOKEY, "galois_keygen: no secret key");
+    const size_t words = (size_t)(c->L + 1) * 2 * (c->L + 2) * c->N;
+    for (int32_t k = 0; k < n_steps; k++) {
+        const uint32_t g = galois_elt(c, steps[k]);
+        if (g == 1 || c->gkeys.count(g)) continue;
+        uint64_t *gk = nullptr, *gc = nullptr;
+        if (cudaMalloc(&gk, words * 8) != cudaSuccess || cudaMalloc(&gc, words * 8) != cudaSuccess) {
+            cudaFree(gk);
+            return fail(c, EDL_ERR_CUDA, "galois_keygen: out of memory");
+        }
+        launch_keygen_galois(c->dev(), seed, g, c->d_s, gk, gc);
+        c->gkeys[g] = std::make_pair(gk, gc);
+    }
+    cudaStreamSynchronize(c->st);
+    return cuda_check(c, "galois_keygen");
+}
+
+edl_status edl_rotate(edl_ctx* c, const edl_cts* in, int32_t steps, edl_cts* out) {
+    if (!c || !out) return EDL_ERR_ARG;
+    edl_status s = check_ct(c, in);
+    if (s != EDL_OK) return s;
+    if (in->count > 0 && out->data == in->data) return fail(c, EDL_ERR_ARG, "rotate: out aliases in");
+    const int l = in->level;
+    const int64_t cnt = in->count;
+    const uint32_t g = galois_elt(c, steps);
+    if (cnt > 0) {
+        if (g == 1) {
+            cudaMemcpyAsync(out->data, in->data, ct_words(c, cnt, l) * 8, cudaMemcpyDeviceToDevice, c->st);
+        } else {
+            auto it = c->gkeys.find(g);
+            if (it == c->gkeys.end()) return fail(c, EDL_ERR_NOKEY, "rotate: no Galois key for this rotation");
+            uint64_t* tmp = scratch(c, ct_words(c, cnt, l) + relin_scratch_words(cnt, l, c->logn));
+            if (!tmp) return fail(c, EDL_ERR_CUDA, "rotate: scratch");
+            Dev d = c->dev();
+            launch_automorphism(d, in->data, cnt, l, g, tmp);
+            launch_relin(d, tmp, nullptr, cnt, l, false, it->second.first, it->second.second, tmp + ct_words(c, cnt, l),
+                         out->data);
+        }
+    }
+    set_meta(out, cnt, l, in->scale, in->key_id);
+    return cuda_check(c, "rotate");
+}
+
+edl_status edl_encode_pt(edl_ctx* c, const double* slots, int64_t n_vec, int64_t n_slots, double scale, int32_t level,
+                         uint64_t* pt_out) {
+    if (!c || n_vec < 0 || (n_vec > 0 && (!slots || !pt_out))) return fail(c, EDL_ERR_ARG, "encode_pt: bad arguments");
+    if (level < 0 || level > c->L) return fail(c, EDL_ERR_LEVEL, "encode_pt: level out of range");
+    if (n_vec == 0) return EDL_OK;
+    std::vector<int64_t> polys((size_t)n_vec * c->N);
+    edl_status s = edl_encode(c, slots, n_vec, n_slots, scale, polys.data());
+    if (s != EDL_OK) return s;
+    int64_t* dp = reinterpret_cast<int64_t*>(scratch(c, polys.size()));
+    if (!dp) return fail(c, EDL_ERR_CUDA, "encode_pt: scratch");
+    cudaMemcpyAsync(dp, polys.data(), polys.size() * 8, cudaMemcpyHostToDevice, c->st);
+    launch_encode_pt(c->dev(), dp, n_vec, level, pt_out);
+    cudaStreamSynchronize(c->st);
+    return cuda_check(c, "encode_pt");
+}
+
+edl_status edl_encode_pt_poly(edl_ctx* c, const int64_t* poly, int64_t n_vec, int32_t level, uint64_t* pt_out) {
+    if (!c || n_vec < 0 || (n_vec > 0 && (!poly || !pt_out))) return fail(c, EDL_ERR_ARG, "encode_pt_poly: bad arguments");
+    if (level < 0 || level > c->L) return fail(c, EDL_ERR_LEVEL, "encode_pt_poly: level out of range");
+    if (n_vec > 0) launch_encode_pt(c->dev(), poly, n_vec, level, pt_out);
+    return cuda_check(c, "encode_pt_poly");
+}
+
+edl_status edl_ct_pt_vec_mul(edl_ctx* c, const edl_cts* a, const uint64_t* pt, int64_t pt_count, int32_t pt_level,
+                             double pt_scale, edl_cts* out) {
+    if (!c || !out) return EDL_ERR_ARG;
+    edl_status s = check_ct(c, a);
+    if (s != EDL_OK) return s;
+    if (a->count > 0 && !pt) return fail(c, EDL_ERR_ARG, "ct_pt_vec_mul: null plaintext");
+    if (pt_count != 1 && pt_count != a->count) return fail(c, EDL_ERR_SHAPE, "ct_pt_vec_mul: plaintext count");
+    if (pt_level < a->level) return fail(c, EDL_ERR_LEVEL, "ct_pt_vec_mul: plaintext level below ciphertext level");
+    if (a->count > 0) launch_mul_pt(c->dev(), a->data, a->count, a->level, pt, pt_count, pt_level, out->data);
+    set_meta(out, a->count, a->level, a->scale * pt_scale, a->key_id);
+    return cuda_check(c, "ct_pt_vec_mul");
+}
+
 edl_status edl_mod_reduce(edl_ctx* c, edl_cts* x) {
     if (!c) return EDL_ERR_ARG;
     edl_status s = check_ct(c, x);
@@ -933,6 +1033,16 @@ edl_status edl_modmul_peak(edl_ctx* c, int32_t iters, double* modmul_per_s) {
     cudaEventDestroy(b);
     *modmul_per_s = (double)blocks * 256.0 * 8.0 * (double)iters / (ms * 1e-3);
     return cuda_check(c, "modmul_peak");
+}
+
+edl_status edl_export_galois_key(edl_ctx* c, int32_t steps, uint64_t* host_out, size_t words) {
+    if (!c || !host_out) return EDL_ERR_ARG;
+    auto it = c->gkeys.find(galois_elt(c, steps));
+    if (it == c->gkeys.end()) return fail(c, EDL_ERR_NOKEY, "export_galois_key: no key");
+    const size_t need = (size_t)(c->L + 1) * 2 * (c->L + 2) * c->N;
+    if (words < need) return fail(c, EDL_ERR_ARG, "export_galois_key: buffer too small");
+    cudaMemcpy(host_out, it->second.first, need * 8, cudaMemcpyDeviceToHost);
+    return cuda_check(c, "export_galois_key");
 }
 
 edl_status edl_export_key(edl_ctx* c, int32_t which, uint64_t* host_out, size_t words) {

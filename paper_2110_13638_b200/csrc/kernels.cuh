@@ -137,6 +137,10 @@ template <int LOGN>
 void launch_encrypt_n(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint64_t seed, uint32_t obj0,
                       const uint64_t* pk, uint64_t* out);
 template <int LOGN>
+void launch_keygen_galois_n(const Dev& d, uint64_t seed, uint32_t g, const uint64_t* s_hat, uint64_t* gk, uint64_t* gk_c);
+template <int LOGN>
+void launch_encode_pt_n(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint64_t* out);
+template <int LOGN>
 void launch_decrypt_n(const Dev& d, const uint64_t* ct, int64_t cnt, int l, const uint64_t* s_hat, uint64_t* out);
 
 // ---- NTT family (ntt_kernels.cu) ----
@@ -175,6 +179,15 @@ void launch_cc_mac(const Dev& d, const uint64_t* x, int l, int H, int W, int F, 
 void launch_dense_mac(const Dev& d, const uint64_t* x, int64_t K, int64_t O, int l, const ulonglong2* wd, uint64_t* out,
                       uint64_t* part = nullptr);
 int dense_split(const Dev& d, int64_t K, int64_t O, int l);
+
+// NEXT f1: Galois key [L+1][2][L+2][N] (+ companions) for element g; NTT-domain plaintexts
+// [cnt][l+1][N] from integer polynomials; sigma_g of ct arrays; ct (.) plaintext vectors
+void launch_keygen_galois(const Dev& d, uint64_t seed, uint32_t g, const uint64_t* s_hat, uint64_t* gk, uint64_t* gk_c);
+void launch_encode_pt(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint64_t* out);
+void launch_automorphism(const Dev& d, const uint64_t* in, int64_t cnt, int l, uint32_t g, uint64_t* out);
+// out = a (.) pt ; pt [pt_count][pt_level+1][N], pt_count = 1 (broadcast) or cnt, pt_level >= l
+void launch_mul_pt(const Dev& d, const uint64_t* a, int64_t cnt, int l, const uint64_t* pt, int64_t pt_count,
+                   int pt_level, uint64_t* out);
 
 // wire format: residues of limb i in bits[i] bits (pointwise.cu); polys = count * 2
 void launch_unpack(const Dev& d, const uint64_t* in, int64_t polys, int nl, const int* bits, uint64_t* out);

@@ -118,14 +118,16 @@ k_relin_intt_d2(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, 
     const int64_t c = C::bx();
     const ModInfo& m = mods[j];
     const uint64_t* a1 = a + limb_off(c, 1, j, l + 1, C::LOGN);
-    const uint64_t* b1 = b + limb_off(c, 1, j, l + 1, C::LOGN);
+    // b == null: key switch of the single polynomial a1 (Galois rotation, NEXT f1)
+    const uint64_t* b1 = b ? b + limb_off(c, 1, j, l + 1, C::LOGN) : a1;
+    const bool single = (b == nullptr);
     uint64_t* dst = acoef + (((size_t)c * (l + 1) + j) << C::LOGN);
     if (threadIdx.x == 0)
         pf_next_wave<C>([&](int64_t bx, int cr, int y, int) {
             pf_sub<C>(a + limb_off(bx, 1, y, l + 1, C::LOGN), cr, false);
-            if (b != a) pf_sub<C>(b + limb_off(bx, 1, y, l + 1, C::LOGN), cr, false);
+            if (b && b != a) pf_sub<C>(b + limb_off(bx, 1, y, l + 1, C::LOGN), cr, false);
         });
-    auto ld = [&](int idx) { return mulmod(a1[idx], b1[idx], m); };
+    auto ld = [&](int idx) { return single ? a1[idx] : mulmod(a1[idx], b1[idx], m); };
     auto st = [&](int idx, uint64_t v) { dst[idx] = v; };
     ntt_inv<C>(sm, m, ld, st);
 }

@@ -434,8 +434,12 @@ k_relin_mac(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int 
             if (c >= cnt) continue;
             if (j == ti) {
                 const ulonglong2 a1 = v2(a + limb_off(c, 1, j, l + 1, logn))[k];
-                const ulonglong2 b1 = v2(b + limb_off(c, 1, j, l + 1, logn))[k];
-                x[e] = make_ulonglong2(mulmod(a1.x, b1.x, m), mulmod(a1.y, b1.y, m));
+                if (b == nullptr) {
+                    x[e] = a1;
+                } else {
+                    const ulonglong2 b1 = v2(b + limb_off(c, 1, j, l + 1, logn))[k];
+                    x[e] = make_ulonglong2(mulmod(a1.x, b1.x, m), mulmod(a1.y, b1.y, m));
+                }
             } else {
                 x[e] = v2(xh + ((((size_t)c * (l + 1) + j) * (l + 2) + ti) << logn))[k];
             }
@@ -468,11 +472,16 @@ k_relin_mac(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int 
             else v[cc] = make_ulonglong2(barrett128(s[e][cc][0], m), barrett128(s[e][cc][1], m));
         }
         if (ti <= l) {
-            const ulonglong2 a0 = v2(a + limb_off(c, 0, ti, l + 1, logn))[k], a1 = v2(a + limb_off(c, 1, ti, l + 1, logn))[k];
-            const ulonglong2 b0 = v2(b + limb_off(c, 0, ti, l + 1, logn))[k], b1 = v2(b + limb_off(c, 1, ti, l + 1, logn))[k];
-            const uint64_t d0x = mulmod(a0.x, b0.x, m), d0y = mulmod(a0.y, b0.y, m);
-            const uint64_t d1x = addmod(mulmod(a0.x, b1.x, m), mulmod(a1.x, b0.x, m), m.q);
-            const uint64_t d1y = addmod(mulmod(a0.y, b1.y, m), mulmod(a1.y, b0.y, m), m.q);
+            const ulonglong2 a0 = v2(a + limb_off(c, 0, ti, l + 1, logn))[k];
+            uint64_t d0x = a0.x, d0y = a0.y, d1x = 0, d1y = 0;   // single polynomial: (d0, d1) = (a0, 0)
+            if (b != nullptr) {
+                const ulonglong2 a1 = v2(a + limb_off(c, 1, ti, l + 1, logn))[k];
+                const ulonglong2 b0 = v2(b + limb_off(c, 0, ti, l + 1, logn))[k], b1 = v2(b + limb_off(c, 1, ti, l + 1, logn))[k];
+                d0x = mulmod(a0.x, b0.x, m);
+                d0y = mulmod(a0.y, b0.y, m);
+                d1x = addmod(mulmod(a0.x, b1.x, m), mulmod(a1.x, b0.x, m), m.q);
+                d1y = addmod(mulmod(a0.y, b1.y, m), mulmod(a1.y, b0.y, m), m.q);
+            }
             v[0] = make_ulonglong2(addmod(d0x, mulc(v[0].x, pinv, m), m.q), addmod(d0y, mulc(v[0].y, pinv, m), m.q));
             v[1] = make_ulonglong2(addmod(d1x, mulc(v[1].x, pinv, m), m.q), addmod(d1y, mulc(v[1].y, pinv, m), m.q));
         }
@@ -525,8 +534,12 @@ k_relin_mac2(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int
             if (j >= nd) break;
             if (j == ti) {
                 const ulonglong2 a1 = v2(a + limb_off(c, 1, j, l + 1, logn))[k];
-                const ulonglong2 b1 = v2(b + limb_off(c, 1, j, l + 1, logn))[k];
-                x[j] = make_ulonglong2(mulmod(a1.x, b1.x, m), mulmod(a1.y, b1.y, m));
+                if (b == nullptr) {   // single-polynomial key switch (rotation): d2 = a1
+                    x[j] = a1;
+                } else {
+                    const ulonglong2 b1 = v2(b + limb_off(c, 1, j, l + 1, logn))[k];
+                    x[j] = make_ulonglong2(mulmod(a1.x, b1.x, m), mulmod(a1.y, b1.y, m));
+                }
             } else {
                 x[j] = v2(xh + ((((size_t)c * (l + 1) + j) * (l + 2) + ti) << logn))[k];
             }
@@ -559,16 +572,58 @@ k_relin_mac2(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int
             }
         }
         if (ti <= l) {   // fold the tensor's d0, d1: v = d + acc P^-1
-            const ulonglong2 a0 = v2(a + limb_off(c, 0, ti, l + 1, logn))[k], a1 = v2(a + limb_off(c, 1, ti, l + 1, logn))[k];
-            const ulonglong2 b0 = v2(b + limb_off(c, 0, ti, l + 1, logn))[k], b1 = v2(b + limb_off(c, 1, ti, l + 1, logn))[k];
-            const uint64_t d0x = mulmod(a0.x, b0.x, m), d0y = mulmod(a0.y, b0.y, m);
-            const uint64_t d1x = addmod(mulmod(a0.x, b1.x, m), mulmod(a1.x, b0.x, m), m.q);
-            const uint64_t d1y = addmod(mulmod(a0.y, b1.y, m), mulmod(a1.y, b0.y, m), m.q);
+            const ulonglong2 a0 = v2(a + limb_off(c, 0, ti, l + 1, logn))[k];
+            uint64_t d0x = a0.x, d0y = a0.y, d1x = 0, d1y = 0;   // single polynomial: (d0, d1) = (a0, 0)
+            if (b != nullptr) {
+                const ulonglong2 a1 = v2(a + limb_off(c, 1, ti, l + 1, logn))[k];
+                const ulonglong2 b0 = v2(b + limb_off(c, 0, ti, l + 1, logn))[k], b1 = v2(b + limb_off(c, 1, ti, l + 1, logn))[k];
+                d0x = mulmod(a0.x, b0.x, m);
+                d0y = mulmod(a0.y, b0.y, m);
+                d1x = addmod(mulmod(a0.x, b1.x, m), mulmod(a1.x, b0.x, m), m.q);
+                d1y = addmod(mulmod(a0.y, b1.y, m), mulmod(a1.y, b0.y, m), m.q);
+            }
             v[0] = make_ulonglong2(addmod(d0x, mulc(v[0].x, pinv, m), m.q), addmod(d0y, mulc(v[0].y, pinv, m), m.q));
             v[1] = make_ulonglong2(addmod(d1x, mulc(v[1].x, pinv, m), m.q), addmod(d1y, mulc(v[1].y, pinv, m), m.q));
         }
 #pragma unroll
         for (int cc = 0; cc < 2; cc++) v2(acc + ((((size_t)c * 2 + cc) * (l + 2) + ti) << logn))[k] = v[cc];
+    }
+}
+
+// ---------------------------------------------------------------- NEXT f1: automorphism, ct (.) pt
+// sigma_g in the NTT domain is a permutation of the evaluation points (same for every limb):
+// out[k] = in[src_g(k)], (2 brv(src) + 1) = (2 brv(k) + 1) g mod 2N.
+__global__ void k_automorphism(const uint64_t* __restrict__ in, int64_t rows, uint32_t g, uint64_t* __restrict__ out,
+                               int logn) {
+    const int n = 1 << logn;
+    const uint32_t two_n = 2u << logn;
+    for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
+        const uint64_t* src = in + ((size_t)row << logn);
+        uint64_t* dst = out + ((size_t)row << logn);
+        for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+            const uint32_t bk = __brev((uint32_t)k) >> (32 - logn);
+            const uint32_t e = (uint32_t)(((uint64_t)(2 * bk + 1) * g) % two_n);
+            dst[k] = __ldg(src + (__brev((e - 1) >> 1) >> (32 - logn)));
+        }
+    }
+}
+
+__global__ void k_mul_pt(const uint64_t* __restrict__ a, int64_t cnt, int l, const uint64_t* __restrict__ pt,
+                         int64_t pt_count, int pt_level, uint64_t* __restrict__ out,
+                         const __grid_constant__ ModTable mods, int logn) {
+    const int64_t rows = cnt * 2 * (l + 1);
+    const int n2 = 1 << (logn - 1);
+    for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
+        const int i = (int)(row % (l + 1));
+        const int64_t c = row / (2 * (l + 1));
+        const ModInfo& m = mods[i];
+        const uint64_t* pa = a + ((size_t)row << logn);
+        const uint64_t* pp = pt + ((((size_t)(pt_count == 1 ? 0 : c)) * (pt_level + 1) + i) << logn);
+        uint64_t* po = out + ((size_t)row << logn);
+        for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n2; k += gridDim.x * blockDim.x) {
+            const ulonglong2 x = v2(pa)[k], w = v2(pp)[k];
+            v2(po)[k] = make_ulonglong2(mulmod(x.x, w.x, m), mulmod(x.y, w.y, m));
+        }
     }
 }
 
@@ -633,6 +688,17 @@ __global__ void k_pack(const uint64_t* __restrict__ in, int64_t polys, int nl, i
 }
 
 }  // namespace
+
+void launch_automorphism(const Dev& d, const uint64_t* in, int64_t cnt, int l, uint32_t g, uint64_t* out) {
+    EDL_LAUNCH(d, "k_automorphism", k_automorphism<<<rows_grid(d.logn + 1, cnt * 2 * (l + 1)), PW_THREADS, 0, d.st>>>(
+                                        in, cnt * 2 * (l + 1), g, out, d.logn));
+}
+
+void launch_mul_pt(const Dev& d, const uint64_t* a, int64_t cnt, int l, const uint64_t* pt, int64_t pt_count,
+                   int pt_level, uint64_t* out) {
+    EDL_LAUNCH(d, "k_mul_pt", k_mul_pt<<<rows_grid(d.logn, cnt * 2 * (l + 1)), PW_THREADS, 0, d.st>>>(
+                                  a, cnt, l, pt, pt_count, pt_level, out, *d.mt, d.logn));
+}
 
 static PackInfo pack_info(const Dev& d, int nl, const int* bits, int64_t* pw) {
     PackInfo pi;

@@ -24,6 +24,14 @@ void launch_encrypt(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint64
     EDL_DISPATCH_LOGN(d.logn, launch_encrypt_n<LOGN>(d, msg, cnt, l, seed, obj0, pk, out));
 }
 
+void launch_keygen_galois(const Dev& d, uint64_t seed, uint32_t g, const uint64_t* s_hat, uint64_t* gk, uint64_t* gk_c) {
+    EDL_DISPATCH_LOGN(d.logn, launch_keygen_galois_n<LOGN>(d, seed, g, s_hat, gk, gk_c));
+}
+
+void launch_encode_pt(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint64_t* out) {
+    EDL_DISPATCH_LOGN(d.logn, launch_encode_pt_n<LOGN>(d, msg, cnt, l, out));
+}
+
 void launch_decrypt(const Dev& d, const uint64_t* ct, int64_t cnt, int l, const uint64_t* s_hat, uint64_t* out) {
     EDL_DISPATCH_LOGN(d.logn, launch_decrypt_n<LOGN>(d, ct, cnt, l, s_hat, out));
 }

@@ -11,7 +11,16 @@
 namespace edl {
 
 enum : uint32_t { TAG_S = 1, TAG_PK_A = 2, TAG_PK_E = 3, TAG_RLK_A = 4, TAG_RLK_E = 5, TAG_ENC_V = 6, TAG_ENC_E0 = 7,
-                  TAG_ENC_E1 = 8 };
+                  TAG_ENC_E1 = 8, TAG_GK_A = 9, TAG_GK_E = 10 };
+
+// NTT-domain index of sigma_g: evaluation point psi^{2 brv(k)+1} maps to psi^{(2 brv(k)+1) g}
+// (NEXT f1), so sigma_g(a)[k] = a[src_g(k)].
+__device__ __forceinline__ int galois_src(int k, uint32_t g, int logn) {
+    const uint32_t two_n = 2u << logn;
+    const uint32_t bk = __brev((uint32_t)k) >> (32 - logn);
+    const uint32_t e = (uint32_t)(((uint64_t)(2 * bk + 1) * g) % two_n);
+    return (int)(__brev((e - 1) >> 1) >> (32 - logn));
+}
 
 __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
 #pragma unroll
@@ -128,6 +137,49 @@ k_keygen_rlk(uint64_t seed, int L, const uint64_t* __restrict__ s_hat, uint64_t*
     ntt_fwd<C>(sm, m, ld, st);
 }
 
+// ---- Galois key for element g (NEXT f1): rlk's digit structure with gadget P sigma_g(s);
+// a ~ uniform (tag 9), e ~ CBD (tag 10), object id 64 g + j
+template <class C>
+__global__ void __launch_bounds__(C::T, C::MINB)
+k_keygen_galois(uint64_t seed, int L, uint32_t g, const uint64_t* __restrict__ s_hat, uint64_t* __restrict__ gk,
+                uint64_t* __restrict__ gk_c, const __grid_constant__ ModTable mods, const ChainConsts* __restrict__ cc) {
+    extern __shared__ uint64_t sm[];
+    const int i = C::bx();      // limb 0..L+1 (L+1 = P)
+    const int j = blockIdx.y;   // digit 0..L
+    const ModInfo& m = mods[i];
+    const uint64_t* s = s_hat + ((size_t)i << C::LOGN);
+    const size_t ob = ((size_t)(j * 2 + 0) * (L + 2) + i) << C::LOGN;
+    const size_t oa = ((size_t)(j * 2 + 1) * (L + 2) + i) << C::LOGN;
+    const uint64_t pmod = cc->qmod[L + 1][i];
+    const uint32_t obj = 64u * g + (uint32_t)j;
+    auto ld = [&](int idx) { return small_mod(cbd_of(draw(seed, idx, obj, 0, TAG_GK_E)), m.q); };
+    auto st = [&](int idx, uint64_t e) {
+        const uint64_t av = uniform_of(draw(seed, idx, obj, i, TAG_GK_A), m);
+        uint64_t bv = submod(e, mulmod(av, s[idx], m), m.q);
+        if (i == j) bv = addmod(bv, mulmod(s[galois_src(idx, g, C::LOGN)], pmod, m), m.q);
+        gk[ob + idx] = bv;
+        gk[oa + idx] = av;
+        gk_c[ob + idx] = key_companion(bv, m);
+        gk_c[oa + idx] = key_companion(av, m);
+    };
+    ntt_fwd<C>(sm, m, ld, st);
+}
+
+// ---- plaintext vectors: integer polynomial -> NTT-domain residues, per (vector, limb)
+template <class C>
+__global__ void __launch_bounds__(C::T, C::MINB)
+k_encode_pt(const int64_t* __restrict__ msg, int l, uint64_t* __restrict__ out, const __grid_constant__ ModTable mods) {
+    extern __shared__ uint64_t sm[];
+    const int i = blockIdx.y;
+    const int64_t c = C::bx();
+    const ModInfo& m = mods[i];
+    const int64_t* mm = msg + ((size_t)c << C::LOGN);
+    uint64_t* dst = out + (((size_t)c * (l + 1) + i) << C::LOGN);
+    auto ld = [&](int idx) { return signed_mod(mm[idx], m); };
+    auto st = [&](int idx, uint64_t v) { dst[idx] = v; };
+    ntt_fwd<C>(sm, m, ld, st);
+}
+
 // ---- encrypt (O8): c0 = v*b + NTT(e0 + m), c1 = v*a + NTT(e1), per (ct, limb)
 template <class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
@@ -205,10 +257,25 @@ void launch_decrypt_n(const Dev& d, const uint64_t* ct, int64_t cnt, int l, cons
     launch_cfg<C>(d, "k_decrypt", k_decrypt<C>, dim3((unsigned)cnt, l + 1), ct, l, s_hat, out, *d.mt);
 }
 
+template <int LOGN>
+void launch_keygen_galois_n(const Dev& d, uint64_t seed, uint32_t g, const uint64_t* s_hat, uint64_t* gk, uint64_t* gk_c) {
+    using C = CfgFused<LOGN>;
+    launch_cfg<C>(d, "k_keygen_galois", k_keygen_galois<C>, dim3(d.L + 2, d.L + 1), seed, d.L, g, s_hat, gk, gk_c,
+                  *d.mt, d.cc);
+}
+
+template <int LOGN>
+void launch_encode_pt_n(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint64_t* out) {
+    using C = CfgFused<LOGN>;
+    launch_cfg<C>(d, "k_encode_pt", k_encode_pt<C>, dim3((unsigned)cnt, l + 1), msg, l, out, *d.mt);
+}
+
 #define EDL_INSTANTIATE_RNG(LOGN)                                                                               \
     template void launch_keygen_n<LOGN>(const Dev&, uint64_t, uint64_t*, uint64_t*, uint64_t*, uint64_t*);      \
     template void launch_encrypt_n<LOGN>(const Dev&, const int64_t*, int64_t, int, uint64_t, uint32_t,          \
                                          const uint64_t*, uint64_t*);                                           \
-    template void launch_decrypt_n<LOGN>(const Dev&, const uint64_t*, int64_t, int, const uint64_t*, uint64_t*);
+    template void launch_decrypt_n<LOGN>(const Dev&, const uint64_t*, int64_t, int, const uint64_t*, uint64_t*);  \
+    template void launch_keygen_galois_n<LOGN>(const Dev&, uint64_t, uint32_t, const uint64_t*, uint64_t*, uint64_t*); \
+    template void launch_encode_pt_n<LOGN>(const Dev&, const int64_t*, int64_t, int, uint64_t*);
 
 }  // namespace edl

@@ -131,6 +131,14 @@ _sigs = {
     "edl_dense": (_c.c_int32, [_c.c_void_p, _P(Cts), _c.c_void_p, _c.c_void_p, _c.c_int32, _c.c_int32, _P(Cts)]),
     "edl_mod_reduce": (_c.c_int32, [_c.c_void_p, _P(Cts)]),
     "edl_cts_packed_bytes": (_c.c_size_t, [_c.c_void_p, _c.c_int64, _c.c_int32]),
+    "edl_galois_keygen": (_c.c_int32, [_c.c_void_p, _c.c_uint64, _c.c_void_p, _c.c_int32]),
+    "edl_rotate": (_c.c_int32, [_c.c_void_p, _P(Cts), _c.c_int32, _P(Cts)]),
+    "edl_encode_pt": (_c.c_int32, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int64, _c.c_double, _c.c_int32,
+                                   _c.c_void_p]),
+    "edl_encode_pt_poly": (_c.c_int32, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int32, _c.c_void_p]),
+    "edl_ct_pt_vec_mul": (_c.c_int32, [_c.c_void_p, _P(Cts), _c.c_void_p, _c.c_int64, _c.c_int32, _c.c_double,
+                                       _P(Cts)]),
+    "edl_export_galois_key": (_c.c_int32, [_c.c_void_p, _c.c_int32, _c.c_void_p, _c.c_size_t]),
     "edl_cts_pack": (_c.c_int32, [_c.c_void_p, _P(Cts), _c.c_void_p]),
     "edl_cts_unpack": (_c.c_int32, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int32, _c.c_double, _c.c_uint64,
                                     _P(Cts)]),
@@ -391,6 +399,51 @@ class Context:
         self._check(_lib.edl_dense(self._h, ctypes.byref(cx), _ptr(Wt), None if bb is None else _ptr(bb), O,
                                    1 if defer_rescale else 0, ctypes.byref(co)), "dense")
         return o.update(co)
+
+    # ---- NEXT f1: rotations and plaintext vectors
+    def galois_keygen(self, seed: int, steps: Sequence[int]):
+        st = np.ascontiguousarray(list(steps), dtype=np.int32)
+        self._check(_lib.edl_galois_keygen(self._h, seed, _ptr(st), st.size), "galois_keygen")
+        return self
+
+    def rotate(self, x: CtArray, steps: int) -> CtArray:
+        o = self.empty(x.count, x.level)
+        cx, co = x.cts(), o.cts()
+        self._check(_lib.edl_rotate(self._h, ctypes.byref(cx), steps, ctypes.byref(co)), "rotate")
+        return o.update(co)
+
+    def encode_pt(self, slots: np.ndarray, scale: float, level: int):
+        """Plaintext vectors [n_vec][n_slots] -> device NTT-domain plaintexts (int64 tensor
+        [n_vec][level+1][N])."""
+        z = np.ascontiguousarray(np.atleast_2d(slots), dtype=np.float64)
+        out = self.torch.empty(z.shape[0] * (level + 1) * self.n, dtype=self.torch.int64, device=self.device)
+        self._check(_lib.edl_encode_pt(self._h, _ptr(z), z.shape[0], z.shape[1], scale, level,
+                                       ctypes.c_void_p(out.data_ptr())), "encode_pt")
+        return out
+
+    def encode_pt_poly(self, polys, level: int):
+        """Integer polynomials [n_vec][N] (numpy or device tensor) -> device NTT plaintexts."""
+        t = self.torch
+        p = polys if isinstance(polys, t.Tensor) else t.from_numpy(np.ascontiguousarray(polys, dtype=np.int64))
+        p = p.to(self.device).contiguous().view(-1, self.n)
+        out = t.empty(p.shape[0] * (level + 1) * self.n, dtype=t.int64, device=self.device)
+        self._check(_lib.edl_encode_pt_poly(self._h, ctypes.c_void_p(p.data_ptr()), p.shape[0], level,
+                                            ctypes.c_void_p(out.data_ptr())), "encode_pt_poly")
+        self._stream.synchronize()   # `p` may be a temporary of this call
+        return out
+
+    def pt_vec_mul(self, a: CtArray, pt, pt_count: int, pt_level: int, pt_scale: float) -> CtArray:
+        o = self.empty(a.count, a.level)
+        ca, co = a.cts(), o.cts()
+        self._check(_lib.edl_ct_pt_vec_mul(self._h, ctypes.byref(ca), ctypes.c_void_p(pt.data_ptr()), pt_count,
+                                           pt_level, pt_scale, ctypes.byref(co)), "ct_pt_vec_mul")
+        return o.update(co)
+
+    def export_galois_key(self, steps: int) -> np.ndarray:
+        L, nm, n = self.L, self.L + 2, self.n
+        out = np.empty((L + 1, 2, nm, n), dtype=np.uint64)
+        self._check(_lib.edl_export_galois_key(self._h, steps, _ptr(out), out.size), "export_galois_key")
+        return out
 
     # ---- wire format
     def packed_bytes(self, count: int, level: int) -> int:

@@ -1,0 +1,80 @@
+"""The paper's own CNN layout (NEXT f1): one image per ciphertext, kernel masquerading
+(SPEC.md `masquerade_kernel` / `cc_forward`).
+
+"Kernel-masquerading shall mean the merging of weights and a respective zeros mask into a
+sparse n-dimensional array such that they become a single operation conducted on the
+input cyphertext".  With non-overlapping windows (C1: 4x4, stride 4) one
+mask per filter carries the filter at every window position, so a single plaintext
+product covers all windows of that filter; the products of a window are then summed into
+its top-left slot by log2(kh) + log2(kw) rotations and additions (the paper's "key
+rotation to sum", done here with Galois rotations on the GPU instead of a client round
+trip).  Every step is a C-ABI call (plaintext-vector product, rescale, rotate, add).
+"""
+from __future__ import annotations
+
+from typing import Callable, List, Optional, Sequence
+
+import numpy as np
+
+from .edl import Context, CtArray
+
+
+def masquerade_masks(K: np.ndarray, H: int, W: int, stride: int) -> np.ndarray:
+    """[F][H*W]: filter f's weights at every window position (zeros elsewhere)."""
+    F, kh, kw = K.shape
+    if kh > H or kw > W:
+        raise ValueError("kernel larger than input")
+    Ho, Wo = (H - kh) // stride + 1, (W - kw) // stride + 1
+    masks = np.zeros((F, H * W))
+    for r in range(Ho):
+        for c in range(Wo):
+            for u in range(kh):
+                base = (r * stride + u) * W + c * stride
+                masks[:, base:base + kw] += K[:, u, :]
+    return masks
+
+
+def window_rotations(kh: int, kw: int, W: int) -> List[int]:
+    """Rotations summing a kh x kw window (power-of-two sides) into its top-left slot."""
+    if kh & (kh - 1) or kw & (kw - 1):
+        raise ValueError("window sums by rotation need power-of-two kernel sides")
+    out, s = [], 1
+    while s < kw:
+        out.append(s)
+        s *= 2
+    s = 1
+    while s < kh:
+        out.append(s * W)
+        s *= 2
+    return out
+
+
+def anchor_slots(H: int, W: int, kh: int, kw: int, stride: int) -> List[int]:
+    Ho, Wo = (H - kh) // stride + 1, (W - kw) // stride + 1
+    return [(r * stride) * W + c * stride for r in range(Ho) for c in range(Wo)]
+
+
+def masked_cc(ctx: Context, x: CtArray, K: np.ndarray, H: int, W: int, stride: int,
+              bias: Optional[Sequence[float]] = None, encode: Optional[Callable] = None) -> CtArray:
+    """x: one image per ciphertext (pixel p in slot p).  Returns [count*F] ciphertexts
+    (image-major) whose window (r, c) value sits in slot anchor_slots(...)[r*Wo + c];
+    level x.level - 1, scale x.scale.  Needs Galois keys for window_rotations(kh, kw, W).
+    `encode(z, scale) -> int64 poly` picks the slot encoder (default: the library's host
+    FFT); the masks then enter through edl_encode_pt_poly."""
+    F, kh, kw = K.shape
+    l = x.level
+    ql = float(ctx.params.qs[l])
+    masks = masquerade_masks(np.asarray(K, dtype=np.float64), H, W, stride)
+    outs = []
+    for f in range(F):
+        poly = ctx.encode(masks[f][None, :], ql) if encode is None else np.asarray(encode(masks[f], ql))[None, :]
+        pt = ctx.encode_pt_poly(poly, l)
+        y = ctx.rescale(ctx.pt_vec_mul(x, pt, 1, l, ql))
+        for r in window_rotations(kh, kw, W):
+            y = ctx.add(y, ctx.rotate(y, r))
+        if bias is not None:
+            y = ctx.pt_add(y, [float(bias[f])] * y.count)
+        outs.append(y)
+    torch = ctx.torch
+    t = torch.stack([o.tensor.view(x.count, -1) for o in outs], dim=1).reshape(-1)
+    return CtArray(t, x.count * F, outs[0].level, outs[0].scale, outs[0].key_id)

@@ -355,3 +355,74 @@ def test_wire_format_pack_unpack(c1pair, level):
     y = g.unpack(packed, 3, level, 2.0 ** 40, o.key_id)
     assert y.level == level and y.count == 3 and y.scale == 2.0 ** 40
     assert np.array_equal(y.numpy(g.n), A)
+
+
+# ---------------------------------------------------------------- NEXT f1: rotations, plaintext vectors
+@pytest.fixture(scope="module")
+def f1pair(c1pair):
+    from oracle import galois as og
+    g, o = c1pair
+    steps = [1, 2, 8, 16, -2, 28]
+    g.galois_keygen(7, steps)
+    gk = {og.galois_element(r, o.n): og.galois_keygen(o, 7, og.galois_element(r, o.n)) for r in steps}
+    return g, o, gk
+
+
+def test_galois_key_bit_exact(f1pair):
+    from oracle import galois as og
+    g, o, gk = f1pair
+    assert np.array_equal(g.export_galois_key(1), gk[og.galois_element(1, o.n)])
+
+
+@pytest.mark.parametrize("r", [1, -2, 28])
+def test_rotate_bit_exact(f1pair, r):
+    from oracle import galois as og
+    g, o, gk = f1pair
+    lvl = 3
+    A = ock.CtArray(_rand_ct(o, 2, lvl, 90 + r), lvl, 2.0 ** 40, o.key_id)
+    got = g.rotate(_to_gpu(g, A.data, lvl, A.scale, o.key_id), r)
+    want = og.rotate(o, A, r, gk)
+    assert got.level == lvl and got.scale == A.scale
+    assert np.array_equal(got.numpy(g.n), want.data)
+
+
+def test_plain_vector_product_bit_exact(f1pair):
+    from oracle import galois as og
+    g, o, _ = f1pair
+    w = np.random.default_rng(5).uniform(-1, 1, 784)
+    lvl = 4
+    pt_o = og.encode_plain(o, w, float(o.q[lvl]), lvl)
+    pt_g = g.encode_pt_poly(o.encode(w, float(o.q[lvl]))[None, :], lvl)   # same integer poly (Z1)
+    pt_h = g.encode_pt(w, float(o.q[lvl]), lvl)                           # library host encoder
+    assert pt_h.numel() == pt_g.numel()
+    assert np.array_equal(pt_g.cpu().numpy().view(np.uint64).reshape(pt_o.shape), pt_o)
+    A = ock.CtArray(_rand_ct(o, 3, lvl, 95), lvl, 2.0 ** 40, o.key_id)
+    got = g.pt_vec_mul(_to_gpu(g, A.data, lvl, A.scale, o.key_id), pt_g, 1, lvl, float(o.q[lvl]))
+    want = og.mul_plain(o, A, np.broadcast_to(pt_o, (3,) + pt_o.shape), float(o.q[lvl]))
+    assert got.scale == want.scale
+    assert np.array_equal(got.numpy(g.n), want.data)
+
+
+def test_masked_cc_bit_exact_and_float64(f1pair):
+    """The paper's one-image-per-ciphertext CC (kernel masquerading + rotation window sums)
+    on 8x8 images, 2 filters 4x4 stride 4: GPU residues == oracle, anchors == float64."""
+    from oracle import galois as og, networks as onet
+    from paper_2110_13638_b200 import masquerade
+    g, o, gk = f1pair
+    rng = np.random.default_rng(6)
+    imgs = rng.integers(0, 256, (2, 8, 8)) / 255.0
+    K, kb = rng.normal(0, 0.1, (2, 4, 4)), rng.normal(0, 0.1, 2)
+    assert np.array_equal(masquerade.masquerade_masks(K, 8, 8, 4), og.masquerade_masks(K, 8, 8, 4))
+    polys = np.stack([o.encode(v) for v in imgs.reshape(2, 64)])
+    xo = o.encrypt_poly(polys, enc_seed=2, obj0=0, scale=o.p.scale)
+    xg = g.encrypt_poly(polys, scale=o.p.scale, enc_seed=2)
+    yg = masquerade.masked_cc(g, xg, K, 8, 8, 4, kb, encode=lambda z, sc: o.encode(z, sc))
+    yo = og.masked_cc(o, xo, K, 8, 8, 4, kb, gk)
+    assert yg.count == 4 and yg.level == yo.level
+    assert np.array_equal(yg.numpy(g.n), yo.data)
+    dec = g.decrypt(yg, 64).reshape(2, 2, 64)
+    want = onet.cc_float64(imgs, K, kb)
+    anchors = masquerade.anchor_slots(8, 8, 4, 4, 4)
+    for b in range(2):
+        for f in range(2):
+            assert np.max(np.abs(dec[b, f, anchors] - want[b, f * 4:(f + 1) * 4])) < 1e-4
