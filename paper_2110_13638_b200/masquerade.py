@@ -78,3 +78,61 @@ def masked_cc(ctx: Context, x: CtArray, K: np.ndarray, H: int, W: int, stride: i
     torch = ctx.torch
     t = torch.stack([o.tensor.view(x.count, -1) for o in outs], dim=1).reshape(-1)
     return CtArray(t, x.count * F, outs[0].level, outs[0].scale, outs[0].key_id)
+
+
+def sum_rotations(span: int) -> List[int]:
+    """Rotations 1, 2, 4, ... summing slots [0, span) (zero elsewhere) into slot 0."""
+    out, s = [], 1
+    while s < span:
+        out.append(s)
+        s *= 2
+    return out
+
+
+def network_rotations(H: int, W: int, kh: int, kw: int) -> List[int]:
+    return sorted(set(window_rotations(kh, kw, W) + sum_rotations(H * W)))
+
+
+def masked_dense(ctx: Context, feats: CtArray, F: int, anchors: Sequence[int], Wt: np.ndarray, b, span: int,
+                 encode: Optional[Callable] = None) -> CtArray:
+    """Dense layer on the masked-CC feature ciphertexts [count*F] (image-major, window w's
+    feature in slot anchors[w]): class o = sum_f Rescale(feat_f (.) pt_{o,f}) with
+    pt_{o,f}[anchors[w]] = W[o][f*len(anchors) + w], summed over all slots by rotations
+    into slot 0, + b_o.  Returns [count*O] (image-major), logit o of an image in slot 0."""
+    O = Wt.shape[0]
+    nimg = feats.count // F
+    l = feats.level
+    ql = float(ctx.params.qs[l])
+    words = 2 * (l + 1) * ctx.n
+    fv = feats.tensor.view(nimg, F, words)
+    torch = ctx.torch
+    outs = []
+    for o in range(O):
+        acc = None
+        for f in range(F):
+            z = np.zeros(span)
+            z[list(anchors)] = Wt[o, f * len(anchors):(f + 1) * len(anchors)]
+            poly = ctx.encode(z[None, :], ql) if encode is None else np.asarray(encode(z, ql))[None, :]
+            pt = ctx.encode_pt_poly(poly, l)
+            xf = CtArray(fv[:, f].contiguous().view(-1), nimg, l, feats.scale, feats.key_id)
+            y = ctx.pt_vec_mul(xf, pt, 1, l, ql)
+            acc = y if acc is None else ctx.add(acc, y)
+        acc = ctx.rescale(acc)
+        for r in sum_rotations(span):
+            acc = ctx.add(acc, ctx.rotate(acc, r))
+        if b is not None:
+            acc = ctx.pt_add(acc, [float(b[o])] * acc.count)
+        outs.append(acc)
+    t = torch.stack([x.tensor.view(nimg, -1) for x in outs], dim=1).reshape(-1)
+    return CtArray(t, nimg * O, outs[0].level, outs[0].scale, outs[0].key_id)
+
+
+def masked_cnn(ctx: Context, x: CtArray, K, kb, Wt, b, H: int = 28, W: int = 28, stride: int = 4,
+               coeffs=(0.5, 0.197, 0.0, -0.004), encode: Optional[Callable] = None) -> CtArray:
+    """C1's architecture in the paper's layout: masked CC -> sigma_a -> masked dense.
+    x: one image per ciphertext (level >= 4).  Returns [count*10] ciphertexts, logit o of
+    image i in slot 0 of ciphertext i*10 + o."""
+    F, kh, kw = np.asarray(K).shape
+    cc = masked_cc(ctx, x, K, H, W, stride, kb, encode=encode)
+    act = ctx.poly_activation(cc, coeffs)
+    return masked_dense(ctx, act, F, anchor_slots(H, W, kh, kw, stride), np.asarray(Wt), b, H * W, encode=encode)

@@ -106,3 +106,23 @@ def test_c4_sharded_one_gpu_emulation(gpu):
     outs = sh0.finish(total, lvl, sc, batches=range(B))
     for bi in range(B):
         assert np.array_equal(outs[bi].numpy(ctx.n), want[bi]), bi
+
+
+@pytest.mark.timeout(900)
+def test_f1_masked_cnn_vs_float64(gpu):
+    """NEXT f1: C1's CNN in the paper's own layout (one image per ciphertext, kernel
+    masquerading, rotation sums) decrypts to the float64 logits within 1e-3."""
+    from oracle import networks as onet
+    from paper_2110_13638_b200 import masquerade
+    from synth import c1_images, c1_weights
+
+    ctx = gpu.Context(gpu.params_from_depth(4)).keygen(1)
+    ctx.galois_keygen(7, masquerade.network_rotations(28, 28, 4, 4))
+    K, kb, W, b = c1_weights()
+    imgs = c1_images(3, 2110)
+    x = ctx.encrypt(imgs.reshape(3, 784), enc_seed=2)
+    out = masquerade.masked_cnn(ctx, x, K, kb, W, b)
+    assert out.count == 30 and out.level == 0
+    got = ctx.decrypt(out, 1)[:, 0].reshape(3, 10)
+    ref = onet.c1_float64(imgs, K, kb, W, b)
+    assert np.max(np.abs(got - ref)) < 1e-3
