@@ -206,6 +206,19 @@ edl_status edl_ct_pt_vec_mul(edl_ctx* ctx, const edl_cts* a, const uint64_t* pt,
                              double pt_scale, edl_cts* out);
 edl_status edl_export_galois_key(edl_ctx* ctx, int32_t steps, uint64_t* host_out, size_t words);
 
+/* ---- NEXT f3: client encode / decode on the device (O5 canonical embedding) ----
+ * edl_encode_device: device slots [n_vec][n_slots] (float64) -> device integer polynomials
+ *   [n_vec][N], m_k = rint(scale u_k) with u the inverse canonical embedding (slot j <->
+ *   zeta^{5^j}); a four-step fp64 DFT of length N.  Same +-1 contract with the oracle as
+ *   edl_encode (reading Z1).  Feed the result to edl_encrypt_poly.  Asynchronous.
+ * edl_decrypt_device: in (count ciphertexts) -> device slots [count][n_slots] (float64):
+ *   m = c0 + c1 s, INTT, exact mod-2^64 CRT lift to signed integers (valid while |m| < 2^63,
+ *   i.e. for every in-range CKKS message), forward embedding, / scale.  Asynchronous.
+ * Errors: EDL_ERR_CAPACITY if n_slots > N/2; EDL_ERR_NOKEY without a secret key. */
+edl_status edl_encode_device(edl_ctx* ctx, const double* slots, int64_t n_vec, int64_t n_slots, double scale,
+                             int64_t* poly_out);
+edl_status edl_decrypt_device(edl_ctx* ctx, const edl_cts* in, double* slots_out, int64_t n_slots);
+
 /* ---- wire format (client <-> server transfer of ciphertext arrays) ----
  * Every residue of limb i is stored in bits_i = bit length of q_i bits (60 or 40 for the
  * Alg. 8 chains) instead of 64: per polynomial, limb i occupies

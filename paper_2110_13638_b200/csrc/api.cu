@@ -496,6 +496,55 @@ edl_status edl_decrypt(edl_ctx* c, const edl_cts* in, double* slots_out, int64_t
     return EDL_OK;
 }
 
+// ---- NEXT f3: client encode / decrypt+decode on the device ----
+edl_status edl_encode_device(edl_ctx* c, const double* slots, int64_t n_vec, int64_t n_slots, double scale,
+                             int64_t* poly_out) {
+    if (!c || n_vec < 0 || n_slots < 0 || (n_vec > 0 && (!slots || !poly_out)))
+        return fail(c, EDL_ERR_ARG, "encode_device: bad arguments");
+    if (n_slots > c->N / 2) return fail(c, EDL_ERR_CAPACITY, "CapacityError: n_slots > N/2");
+    if (c->logn < 8) return fail(c, EDL_ERR_ARG, "encode_device: N >= 256 required");
+    if (n_vec == 0) return EDL_OK;
+    void* tmp = scratch(c, fft_scratch_bytes(n_vec, c->logn) / 8);
+    if (!tmp) return fail(c, EDL_ERR_CUDA, "encode_device: scratch");
+    launch_encode_slots(c->dev(), slots, n_vec, n_slots, scale, poly_out, tmp);
+    return cuda_check(c, "encode_device");
+}
+
+edl_status edl_decrypt_device(edl_ctx* c, const edl_cts* in, double* slots_out, int64_t n_slots) {
+    if (!c || !in || (in->count > 0 && !slots_out)) return EDL_ERR_ARG;
+    if (!c->has_key) return fail(c, EDL_ERR_NOKEY, "decrypt: no key");
+    edl_status s = check_ct(c, in);
+    if (s != EDL_OK) return s;
+    if (n_slots > c->N / 2) return fail(c, EDL_ERR_CAPACITY, "CapacityError: n_slots > N/2");
+    if (c->logn < 8) return fail(c, EDL_ERR_ARG, "decrypt_device: N >= 256 required");
+    if (in->count == 0) return EDL_OK;
+    const int l = in->level, nl = l + 1;
+    // exact-mod-2^64 CRT constants (as host::crt_lift)
+    std::vector<uint64_t> tab(3 * nl);
+    uint64_t Q64 = 1;
+    for (int i = 0; i < nl; i++) Q64 *= c->prm.q[i];
+    for (int i = 0; i < nl; i++) {
+        uint64_t inv = 1, m64 = 1;
+        for (int j = 0; j < nl; j++) {
+            if (j == i) continue;
+            inv = host::mulmod(inv, c->prm.q[j] % c->prm.q[i], c->prm.q[i]);
+            m64 *= c->prm.q[j];
+        }
+        tab[i] = c->prm.q[i];
+        tab[nl + i] = host::invmod(inv, c->prm.q[i]);
+        tab[2 * nl + i] = m64;
+    }
+    const uint64_t* dtab = upload(c, tab);
+    const size_t words = (size_t)in->count * nl * c->N;
+    uint64_t* res = scratch(c, words + fft_scratch_bytes(in->count, c->logn) / 8);
+    if (!res) return fail(c, EDL_ERR_CUDA, "decrypt_device: scratch");
+    Dev d = c->dev();
+    launch_decrypt(d, in->data, in->count, l, c->d_s, res);
+    launch_decode_slots(d, res, in->count, nl, dtab, dtab + nl, dtab + 2 * nl, Q64, n_slots, in->scale, slots_out,
+                        res + words);
+    return cuda_check(c, "decrypt_device");
+}
+
 edl_status edl_ct_add(edl_ctx* c, const edl_cts* a, const edl_cts* b, edl_cts* out) {
     if (!c || !out) return EDL_ERR_ARG;
     edl_status s;

@@ -189,6 +189,14 @@ void launch_automorphism(const Dev& d, const uint64_t* in, int64_t cnt, int l, u
 void launch_mul_pt(const Dev& d, const uint64_t* a, int64_t cnt, int l, const uint64_t* pt, int64_t pt_count,
                    int pt_level, uint64_t* out);
 
+// NEXT f3 (fft.cu): device canonical embedding; scratch fft_scratch_bytes(n_vec, logn)
+size_t fft_scratch_bytes(int64_t n_vec, int logn);
+void launch_encode_slots(const Dev& d, const double* z, int64_t n_vec, int64_t n_slots, double scale, int64_t* m,
+                         void* scratch);
+void launch_decode_slots(const Dev& d, const uint64_t* r, int64_t n_vec, int nl, const uint64_t* q,
+                         const uint64_t* qhat_inv, const uint64_t* qhat64, uint64_t Q64, int64_t n_slots, double scale,
+                         double* z, void* scratch);
+
 // wire format: residues of limb i in bits[i] bits (pointwise.cu); polys = count * 2
 void launch_unpack(const Dev& d, const uint64_t* in, int64_t polys, int nl, const int* bits, uint64_t* out);
 void launch_pack(const Dev& d, const uint64_t* in, int64_t polys, int nl, const int* bits, uint64_t* out);

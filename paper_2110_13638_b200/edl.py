@@ -131,6 +131,8 @@ _sigs = {
     "edl_dense": (_c.c_int32, [_c.c_void_p, _P(Cts), _c.c_void_p, _c.c_void_p, _c.c_int32, _c.c_int32, _P(Cts)]),
     "edl_mod_reduce": (_c.c_int32, [_c.c_void_p, _P(Cts)]),
     "edl_cts_packed_bytes": (_c.c_size_t, [_c.c_void_p, _c.c_int64, _c.c_int32]),
+    "edl_encode_device": (_c.c_int32, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int64, _c.c_double, _c.c_void_p]),
+    "edl_decrypt_device": (_c.c_int32, [_c.c_void_p, _P(Cts), _c.c_void_p, _c.c_int64]),
     "edl_galois_keygen": (_c.c_int32, [_c.c_void_p, _c.c_uint64, _c.c_void_p, _c.c_int32]),
     "edl_rotate": (_c.c_int32, [_c.c_void_p, _P(Cts), _c.c_int32, _P(Cts)]),
     "edl_encode_pt": (_c.c_int32, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int64, _c.c_double, _c.c_int32,
@@ -399,6 +401,30 @@ class Context:
         self._check(_lib.edl_dense(self._h, ctypes.byref(cx), _ptr(Wt), None if bb is None else _ptr(bb), O,
                                    1 if defer_rescale else 0, ctypes.byref(co)), "dense")
         return o.update(co)
+
+    # ---- NEXT f3: device client path
+    def encode_device(self, slots, scale: Optional[float] = None):
+        """Slots (device float64 tensor [n_vec][n_slots] or numpy) -> device int64 polys [n_vec][N]."""
+        t = self.torch
+        z = slots if isinstance(slots, t.Tensor) else t.from_numpy(np.ascontiguousarray(np.atleast_2d(slots),
+                                                                                        dtype=np.float64))
+        z = z.to(self.device, dtype=t.float64).contiguous()
+        if z.dim() == 1:
+            z = z.view(1, -1)
+        sc = float(2 ** self.params.scale_bits) if scale is None else scale
+        out = t.empty((z.shape[0], self.n), dtype=t.int64, device=self.device)
+        self._check(_lib.edl_encode_device(self._h, ctypes.c_void_p(z.data_ptr()), z.shape[0], z.shape[1], sc,
+                                           ctypes.c_void_p(out.data_ptr())), "encode_device")
+        self._stream.synchronize()   # z may be a temporary of this call
+        return out
+
+    def decrypt_device(self, x: CtArray, n_slots: int):
+        """Device float64 slots [count][n_slots]."""
+        out = self.torch.empty((x.count, n_slots), dtype=self.torch.float64, device=self.device)
+        c = x.cts()
+        self._check(_lib.edl_decrypt_device(self._h, ctypes.byref(c), ctypes.c_void_p(out.data_ptr()), n_slots),
+                    "decrypt_device")
+        return out
 
     # ---- NEXT f1: rotations and plaintext vectors
     def galois_keygen(self, seed: int, steps: Sequence[int]):

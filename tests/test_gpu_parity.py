@@ -426,3 +426,34 @@ def test_masked_cc_bit_exact_and_float64(f1pair):
     for b in range(2):
         for f in range(2):
             assert np.max(np.abs(dec[b, f, anchors] - want[b, f * 4:(f + 1) * 4])) < 1e-4
+
+
+
+# ---------------------------------------------------------------- NEXT f3: device encode / decode
+@pytest.mark.parametrize("logn", [13, 14])
+def test_device_encode_contract(edl, logn):
+    """Device canonical embedding vs the oracle encoder: the +-1 contract (reading Z1)."""
+    from oracle import encoding
+    g = edl.Context(edl.params_from_depth(2 if logn == 13 else 4))
+    z = random_slots(3, 1 << (logn - 1), seed=logn, lo=-1, hi=1)
+    got = g.encode_device(z, 2.0 ** 40).cpu().numpy()
+    want = np.stack([encoding.encode(v, 1 << logn, 2.0 ** 40) for v in z])
+    d = np.abs(got - want)
+    assert d.max() <= 1 and (d > 0).mean() <= 0.01
+
+
+def test_device_round_trip_and_decrypt(c1pair):
+    """encode_device -> encrypt_poly -> (ops) -> decrypt_device matches the host decrypt
+    and the slots."""
+    g, o = c1pair
+    z = random_slots(4, 8192, seed=8, lo=-1, hi=1)
+    polys = g.encode_device(z, o.p.scale)
+    x = g.encrypt_poly(polys, scale=o.p.scale, enc_seed=2)
+    dev = g.decrypt_device(x, 8192).cpu().numpy()
+    assert np.max(np.abs(dev - z)) < 1e-6
+    assert np.max(np.abs(dev - g.decrypt(x, 8192))) < 1e-9
+    y = g.rescale(g.mul_relin(x, x))                              # multi-limb CRT lift, level 3
+    assert np.max(np.abs(g.decrypt_device(y, 8192).cpu().numpy() - z * z)) < 1e-5
+    r = g.rescale(g.rescale(g.rescale(y)))                        # level 0: single-limb lift
+    hd, dd = g.decrypt(r, 100), g.decrypt_device(r, 100).cpu().numpy()   # (scale ~1e-24: large values)
+    assert np.max(np.abs(dd - hd) / np.maximum(1.0, np.abs(hd))) < 1e-9
