@@ -126,7 +126,10 @@ static uint64_t quotient_rd_bits(uint64_t w, uint64_t q) {
     return bits;
 }
 
-bool fp_quotient_prime(uint64_t q) { return q < (1ull << 50); }
+// q < 2^46: the FP64-quotient products need inputs below 2^52, and the forward NTT lets
+// its values grow by 2q per stage without reduction (at most (4 + 2*16) q < 2^52 for
+// N <= 2^16).
+bool fp_quotient_prime(uint64_t q) { return q < (1ull << 46); }
 
 uint64_t mul_companion(uint64_t w, uint64_t q) { return fp_quotient_prime(q) ? quotient_rd_bits(w, q) : shoup_companion(w, q); }
 

@@ -120,13 +120,32 @@ __device__ __forceinline__ uint64_t* cluster_smem(uint64_t* sm, int rank) {
     else return cooperative_groups::this_cluster().map_shared_rank(sm, rank);
 }
 
-// ---- forward CT butterfly (Harvey): X, Y in [0,4q) -> [0,4q)
+// ---- forward CT butterfly.  Shoup path (Harvey): X, Y in [0,4q) -> [0,4q).
+// FP64-quotient path (q < 2^46): no reduction at all -- t = Y w mod q lands in [0, 2q) for
+// any Y < 2^52, so X' = X + t and Y' = X + 2q - t grow by at most 2q per stage and stay far
+// below 2^52 through 16 stages; the outputs are reduced once at the end (reduce_grown).
 template <bool FP>
 __device__ __forceinline__ void ct_bfly(uint64_t& X, uint64_t& Y, ulonglong2 w, uint64_t q, uint64_t two_q) {
-    uint64_t x = csub(X, two_q);
-    uint64_t t = tw_mul<FP>(Y, w.x, w.y, q);
-    X = x + t;
-    Y = x - t + two_q;
+    if constexpr (FP) {
+        const uint64_t t = tw_mul_fp(Y, w.x, w.y, q);
+        Y = X + two_q - t;
+        X = X + t;
+    } else {
+        uint64_t x = csub(X, two_q);
+        uint64_t t = tw_mul<FP>(Y, w.x, w.y, q);
+        X = x + t;
+        Y = x - t + two_q;
+    }
+}
+
+// Canonical value of v < 2^52 (the grown forward-NTT outputs of the FP64 path): quotient
+// floor(v RD(1/q)) is floor(v/q) or one less, so one conditional subtraction finishes.
+__device__ __forceinline__ uint64_t reduce_grown(uint64_t v, const ModInfo& m) {
+    const double magic = 4503599627370496.0;   // 2^52
+    const double vd = __hiloint2double(0x43300000 | (uint32_t)(v >> 32), (uint32_t)v) - magic;
+    const double t = __fma_rd(vd, m.qinv_rd, magic);
+    const uint64_t qt = (uint64_t)__double_as_longlong(t) & 0xFFFFFFFFFFFFFull;
+    return csub(v - qt * m.q, m.q);
 }
 
 // ---- inverse GS butterfly (Harvey): X, Y in [0,2q) -> [0,2q)
@@ -310,7 +329,8 @@ __device__ __forceinline__ void ntt_fwd_impl(uint64_t* sm, const ModInfo& m, Loa
 #pragma unroll
     for (int r = 0; r < C::E; r++) {
         uint64_t v = sm[spad(tid + r * C::T)];
-        v = csub(csub(v, two_q), q);
+        if constexpr (FP) v = reduce_grown(v, m);
+        else v = csub(csub(v, two_q), q);
         store(C::idx(r), v, pv[r]);
     }
     __syncthreads();   // smem reusable by the caller's next transform

@@ -4,6 +4,7 @@
 // the kernel measures how many 64-bit modmuls/s the SMs can issue with no memory
 // traffic.  Reported in the same unit as the hot kernels' algorithmic work.
 #include "kernels.cuh"
+#include "ntt_core.cuh"
 
 namespace edl {
 
@@ -21,7 +22,7 @@ __global__ void __launch_bounds__(256) k_modmul_peak(uint64_t q, uint64_t w, uin
     if (acc == 0x123456789ull) sink[0] = acc;   // keep the chains alive
 }
 
-// Register-only Harvey CT butterflies (the NTT's inner operation, ntt_core.cuh) on 16
+// Register-only CT butterflies (ntt_core.cuh ct_bfly, the NTT's inner operation) on 16
 // residues per thread: 8 independent butterflies per round, twiddles held in registers, so
 // the kernel measures the butterfly issue ceiling of one arithmetic path (FP64-quotient
 // for q < 2^50, Shoup otherwise) with no memory traffic.  The "alu" roofline of the NTT
@@ -38,13 +39,7 @@ __global__ void __launch_bounds__(256) k_bfly_peak(uint64_t q, const ulonglong2*
     const uint64_t two_q = 2 * q;
     for (int it = 0; it < iters; it++) {
 #pragma unroll
-        for (int k = 0; k < 8; k++) {
-            uint64_t X = x[k], Y = x[k + 8];
-            const uint64_t xx = csub(X, two_q);
-            const uint64_t t = tw_mul<FP>(Y, w[k].x, w[k].y, q);
-            x[k] = xx + t;
-            x[k + 8] = xx - t + two_q;
-        }
+        for (int k = 0; k < 8; k++) ct_bfly<FP>(x[k], x[k + 8], w[k], q, two_q);   // the NTT's own butterfly
 #pragma unroll
         for (int k = 0; k < 8; k++) {   // pair different lanes next round
             const uint64_t tmp = x[k];
