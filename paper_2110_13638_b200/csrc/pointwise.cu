@@ -499,8 +499,30 @@ constexpr int MAC2_THREADS = 128;
 constexpr int MAC2_MAXD = 8;
 constexpr int MAC2_CTS = 16;
 
-template <bool FP, int MAXD>
-__global__ void __launch_bounds__(MAC2_THREADS, 6)
+// FP selects the arithmetic path at compile time (the launch groups targets by path); ND is
+// the exact digit count l+1 (loops fully unrolled, no per-digit branches); CPI ciphertexts
+// are processed per iteration so their loads are in flight together.
+template <bool FP>
+__device__ __forceinline__ uint64_t mulmod_path(uint64_t a, uint64_t b, const ModInfo& m) {
+    if constexpr (FP) return mulmod_fp(a, b, m);
+    else return mulmod_barrett(a, b, m);
+}
+template <bool FP>
+__device__ __forceinline__ uint64_t mulc_path(uint64_t y, ulonglong2 w, const ModInfo& m) {
+    if constexpr (FP) return csub(tw_mul_fp(y, w.x, w.y, m.q), m.q);
+    else return shoup(y, w.x, w.y, m.q);
+}
+
+#ifndef EDL_MAC2_CPI
+#define EDL_MAC2_CPI 2
+#endif
+constexpr int MAC2_CPI = EDL_MAC2_CPI;
+
+#ifndef EDL_MAC2_LB
+#define EDL_MAC2_LB 4
+#endif
+template <bool FP, int ND>
+__global__ void __launch_bounds__(MAC2_THREADS, EDL_MAC2_LB)
 k_relin_mac2(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l, int L, int64_t cnt,
              const uint64_t* __restrict__ xh, const uint64_t* __restrict__ rlk, const uint64_t* __restrict__ rlk_c,
              uint64_t* __restrict__ acc, const __grid_constant__ TargetList tl, const __grid_constant__ ModTable mods,
@@ -511,82 +533,95 @@ k_relin_mac2(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int
     const int t = (ti == l + 1) ? (L + 1) : ti;
     const ModInfo& m = mods[t];
     const int k = blockIdx.x * MAC2_THREADS + threadIdx.x;   // coefficient pair
-    const int nd = l + 1;
-    const bool active = 2 * k < (1 << logn);
-    if (active) {
-        for (int j = 0; j < nd; j++)
+    if (2 * k >= (1 << logn)) return;   // no block-wide barrier below: each thread reads only its own slice
 #pragma unroll
-            for (int cc = 0; cc < 2; cc++) {
-                const size_t o = (((size_t)j * 2 + cc) * (L + 2) + t) << logn;
-                ks[((j * 2 + cc) * 2 + 0) * MAC2_THREADS + threadIdx.x] = __ldg(v2(rlk + o) + k);
-                if constexpr (FP) ks[((j * 2 + cc) * 2 + 1) * MAC2_THREADS + threadIdx.x] = __ldg(v2(rlk_c + o) + k);
-            }
-    }
-    if (!active) return;   // no block-wide barrier below: each thread reads only its own slice
-    const ulonglong2 pinv = (ti <= l) ? chain->qinv[L + 1][t] : make_ulonglong2(0, 0);
-    const int64_t c_end = ((int64_t)blockIdx.z + 1) * MAC2_CTS < cnt ? ((int64_t)blockIdx.z + 1) * MAC2_CTS : cnt;
-    // (a software pipeline over the ciphertexts measured slower: 124 registers cost more
-    // occupancy than the overlap bought)
-    for (int64_t c = (int64_t)blockIdx.z * MAC2_CTS; c < c_end; c++) {
-        ulonglong2 x[MAXD];
-#pragma unroll
-        for (int j = 0; j < MAXD; j++) {
-            if (j >= nd) break;
-            if (j == ti) {
-                const ulonglong2 a1 = v2(a + limb_off(c, 1, j, l + 1, logn))[k];
-                if (b == nullptr) {   // single-polynomial key switch (rotation): d2 = a1
-                    x[j] = a1;
-                } else {
-                    const ulonglong2 b1 = v2(b + limb_off(c, 1, j, l + 1, logn))[k];
-                    x[j] = make_ulonglong2(mulmod(a1.x, b1.x, m), mulmod(a1.y, b1.y, m));
-                }
-            } else {
-                x[j] = v2(xh + ((((size_t)c * (l + 1) + j) * (l + 2) + ti) << logn))[k];
-            }
-        }
-        ulonglong2 v[2];
+    for (int j = 0; j < ND; j++)
 #pragma unroll
         for (int cc = 0; cc < 2; cc++) {
-            if constexpr (FP) {
-                uint64_t s0 = 0, s1 = 0;
+            const size_t o = (((size_t)j * 2 + cc) * (L + 2) + t) << logn;
+            ks[((j * 2 + cc) * 2 + 0) * MAC2_THREADS + threadIdx.x] = __ldg(v2(rlk + o) + k);
+            if constexpr (FP) ks[((j * 2 + cc) * 2 + 1) * MAC2_THREADS + threadIdx.x] = __ldg(v2(rlk_c + o) + k);
+        }
+    const ulonglong2 pinv = (ti <= l) ? chain->qinv[L + 1][t] : make_ulonglong2(0, 0);
+    const bool single = (b == nullptr);
+    const size_t limb = (size_t)1 << logn;
+    const size_t xs_j = (size_t)(l + 2) << logn, xs_c = (size_t)(l + 1) * xs_j;   // xh strides
+    const size_t cs = (size_t)2 * (l + 1) << logn;                                 // one ciphertext
+    const ulonglong2* xb = v2(xh + ((size_t)ti << logn)) + k;
+    const ulonglong2* a0b = v2(a + ((size_t)ti << logn)) + k;                      // poly 0, limb ti
+    const ulonglong2* a1b = v2(a + ((size_t)(l + 1 + ti) << logn)) + k;            // poly 1, limb ti
+    const ulonglong2* b0b = single ? a0b : v2(b + ((size_t)ti << logn)) + k;
+    const ulonglong2* b1b = single ? a1b : v2(b + ((size_t)(l + 1 + ti) << logn)) + k;
+    (void)limb;
+    const int64_t c_beg = (int64_t)blockIdx.z * MAC2_CTS;
+    const int64_t c_end = c_beg + MAC2_CTS < cnt ? c_beg + MAC2_CTS : cnt;
+    for (int64_t c0 = c_beg; c0 < c_end; c0 += MAC2_CPI) {
+        ulonglong2 x[MAC2_CPI][ND], ta0[MAC2_CPI], ta1[MAC2_CPI], tb0[MAC2_CPI], tb1[MAC2_CPI];
 #pragma unroll
-                for (int j = 0; j < MAXD; j++) {
-                    if (j >= nd) break;
-                    const ulonglong2 r = ks[((j * 2 + cc) * 2 + 0) * MAC2_THREADS + threadIdx.x];
-                    const ulonglong2 q = ks[((j * 2 + cc) * 2 + 1) * MAC2_THREADS + threadIdx.x];
-                    s0 += tw_mul_fp(x[j].x, r.x, q.x, m.q);
-                    s1 += tw_mul_fp(x[j].y, r.y, q.y, m.q);
-                }
-                v[cc] = make_ulonglong2(reduce64(s0, m), reduce64(s1, m));
-            } else {
-                U128 s0, s1;
-                s0.lo = s0.hi = s1.lo = s1.hi = 0;
+        for (int e = 0; e < MAC2_CPI; e++) {   // issue every load of the CPI ciphertexts first
+            const int64_t c = (c0 + e < c_end) ? c0 + e : c0;
+            const size_t oc = (size_t)c * cs / 2;   // in ulonglong2 units
 #pragma unroll
-                for (int j = 0; j < MAXD; j++) {
-                    if (j >= nd) break;
-                    const ulonglong2 r = ks[((j * 2 + cc) * 2 + 0) * MAC2_THREADS + threadIdx.x];
-                    mac128(s0, x[j].x, r.x);
-                    mac128(s1, x[j].y, r.y);
-                }
-                v[cc] = make_ulonglong2(barrett128(s0, m), barrett128(s1, m));
+            for (int j = 0; j < ND; j++)
+                if (j != ti) x[e][j] = xb[((size_t)c * xs_c + (size_t)j * xs_j) / 2];
+            ta1[e] = a1b[oc];
+            tb1[e] = b1b[oc];
+            if (ti <= l) {
+                ta0[e] = a0b[oc];
+                tb0[e] = b0b[oc];
             }
         }
-        if (ti <= l) {   // fold the tensor's d0, d1: v = d + acc P^-1
-            const ulonglong2 a0 = v2(a + limb_off(c, 0, ti, l + 1, logn))[k];
-            uint64_t d0x = a0.x, d0y = a0.y, d1x = 0, d1y = 0;   // single polynomial: (d0, d1) = (a0, 0)
-            if (b != nullptr) {
-                const ulonglong2 a1 = v2(a + limb_off(c, 1, ti, l + 1, logn))[k];
-                const ulonglong2 b0 = v2(b + limb_off(c, 0, ti, l + 1, logn))[k], b1 = v2(b + limb_off(c, 1, ti, l + 1, logn))[k];
-                d0x = mulmod(a0.x, b0.x, m);
-                d0y = mulmod(a0.y, b0.y, m);
-                d1x = addmod(mulmod(a0.x, b1.x, m), mulmod(a1.x, b0.x, m), m.q);
-                d1y = addmod(mulmod(a0.y, b1.y, m), mulmod(a1.y, b0.y, m), m.q);
-            }
-            v[0] = make_ulonglong2(addmod(d0x, mulc(v[0].x, pinv, m), m.q), addmod(d0y, mulc(v[0].y, pinv, m), m.q));
-            v[1] = make_ulonglong2(addmod(d1x, mulc(v[1].x, pinv, m), m.q), addmod(d1y, mulc(v[1].y, pinv, m), m.q));
-        }
 #pragma unroll
-        for (int cc = 0; cc < 2; cc++) v2(acc + ((((size_t)c * 2 + cc) * (l + 2) + ti) << logn))[k] = v[cc];
+        for (int e = 0; e < MAC2_CPI; e++) {
+            const int64_t c = c0 + e;
+            if (c >= c_end) break;
+#pragma unroll
+            for (int j = 0; j < ND; j++)   // digit j = ti: d2 = a1 b1 (or a1 alone for a rotation)
+                if (j == ti)
+                    x[e][j] = single ? ta1[e]
+                                     : make_ulonglong2(mulmod_path<FP>(ta1[e].x, tb1[e].x, m),
+                                                       mulmod_path<FP>(ta1[e].y, tb1[e].y, m));
+            ulonglong2 v[2];
+#pragma unroll
+            for (int cc = 0; cc < 2; cc++) {
+                if constexpr (FP) {
+                    uint64_t s0 = 0, s1 = 0;
+#pragma unroll
+                    for (int j = 0; j < ND; j++) {
+                        const ulonglong2 r = ks[((j * 2 + cc) * 2 + 0) * MAC2_THREADS + threadIdx.x];
+                        const ulonglong2 q = ks[((j * 2 + cc) * 2 + 1) * MAC2_THREADS + threadIdx.x];
+                        s0 += tw_mul_fp(x[e][j].x, r.x, q.x, m.q);
+                        s1 += tw_mul_fp(x[e][j].y, r.y, q.y, m.q);
+                    }
+                    v[cc] = make_ulonglong2(reduce64(s0, m), reduce64(s1, m));
+                } else {
+                    U128 s0, s1;
+                    s0.lo = s0.hi = s1.lo = s1.hi = 0;
+#pragma unroll
+                    for (int j = 0; j < ND; j++) {
+                        const ulonglong2 r = ks[((j * 2 + cc) * 2 + 0) * MAC2_THREADS + threadIdx.x];
+                        mac128(s0, x[e][j].x, r.x);
+                        mac128(s1, x[e][j].y, r.y);
+                    }
+                    v[cc] = make_ulonglong2(barrett128(s0, m), barrett128(s1, m));
+                }
+            }
+            if (ti <= l) {   // fold the tensor's d0, d1: v = d + acc P^-1 (rotation: d = (a0, 0))
+                uint64_t d0x = ta0[e].x, d0y = ta0[e].y, d1x = 0, d1y = 0;
+                if (!single) {
+                    d0x = mulmod_path<FP>(ta0[e].x, tb0[e].x, m);
+                    d0y = mulmod_path<FP>(ta0[e].y, tb0[e].y, m);
+                    d1x = addmod(mulmod_path<FP>(ta0[e].x, tb1[e].x, m), mulmod_path<FP>(ta1[e].x, tb0[e].x, m), m.q);
+                    d1y = addmod(mulmod_path<FP>(ta0[e].y, tb1[e].y, m), mulmod_path<FP>(ta1[e].y, tb0[e].y, m), m.q);
+                }
+                v[0] = make_ulonglong2(addmod(d0x, mulc_path<FP>(v[0].x, pinv, m), m.q),
+                                       addmod(d0y, mulc_path<FP>(v[0].y, pinv, m), m.q));
+                v[1] = make_ulonglong2(addmod(d1x, mulc_path<FP>(v[1].x, pinv, m), m.q),
+                                       addmod(d1y, mulc_path<FP>(v[1].y, pinv, m), m.q));
+            }
+#pragma unroll
+            for (int cc = 0; cc < 2; cc++) v2(acc + ((((size_t)c * 2 + cc) * (l + 2) + ti) << logn))[k] = v[cc];
+        }
     }
 }
 
@@ -736,28 +771,24 @@ void launch_relin_mac(const Dev& d, const uint64_t* a, const uint64_t* b, int64_
         if (d.hmods[t].fp) tf.slot[nf++] = (int8_t)s;
         else ti.slot[ni++] = (int8_t)s;
     }
-    if (l + 1 <= MAC2_MAXD && d.logn >= 8) {
+    if (l + 1 <= 4 && d.logn >= 8) {
         const unsigned gx2 = (unsigned)((1 << d.logn) / (2 * MAC2_THREADS)), gz2 = (unsigned)((cnt + MAC2_CTS - 1) / MAC2_CTS);
         const size_t smem = (size_t)(l + 1) * 2 * 2 * MAC2_THREADS * sizeof(ulonglong2);
-        static bool attr = false;
-        if (!attr) {
-            const int mx = MAC2_MAXD * 2 * 2 * MAC2_THREADS * 16;
-            cudaFuncSetAttribute(k_relin_mac2<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-            cudaFuncSetAttribute(k_relin_mac2<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-            cudaFuncSetAttribute(k_relin_mac2<true, MAC2_MAXD>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-            cudaFuncSetAttribute(k_relin_mac2<false, MAC2_MAXD>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-            attr = true;
-        }
-#define EDL_MAC2(FPV, MD, LIST, NT)                                                                         \
-    EDL_LAUNCH(d, "k_relin_mac", (k_relin_mac2<FPV, MD><<<dim3(gx2, NT, gz2), MAC2_THREADS, smem, d.st>>>( \
+#define EDL_MAC2(FPV, ND, LIST, NT)                                                                         \
+    EDL_LAUNCH(d, "k_relin_mac", (k_relin_mac2<FPV, ND><<<dim3(gx2, NT, gz2), MAC2_THREADS, smem, d.st>>>( \
                                      a, b, l, d.L, cnt, xh, rlk, rlk_c, acc, LIST, *d.mt, d.cc, d.logn)))
-        if (l + 1 <= 4) {
-            if (nf) EDL_MAC2(true, 4, tf, nf);
-            if (ni) EDL_MAC2(false, 4, ti, ni);
-        } else {
-            if (nf) EDL_MAC2(true, MAC2_MAXD, tf, nf);
-            if (ni) EDL_MAC2(false, MAC2_MAXD, ti, ni);
+#define EDL_MAC2_ND(ND)                                  \
+    case ND:                                             \
+        if (nf) EDL_MAC2(true, ND, tf, nf);              \
+        if (ni) EDL_MAC2(false, ND, ti, ni);             \
+        break;
+        switch (l + 1) {
+            EDL_MAC2_ND(1)
+            EDL_MAC2_ND(2)
+            EDL_MAC2_ND(3)
+            EDL_MAC2_ND(4)
         }
+#undef EDL_MAC2_ND
 #undef EDL_MAC2
         return;
     }
