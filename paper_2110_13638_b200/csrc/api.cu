@@ -286,12 +286,18 @@ edl_status edl_ctx_create(const edl_params* p, int32_t device, void* stream, edl
         m.two64 = (uint64_t)((((host::u128)1) << 64) % q);
         m.two64_s = host::shoup_companion(m.two64, q);
         m.one_s = host::shoup_companion(1, q);   // floor(2^64 / q)
-        m.fp = host::fp_quotient_prime(q) ? 1 : 0;
+        m.fp = host::fp_quotient_prime(q) ? (host::f64_ntt_prime(q) ? 2 : 1) : 0;
         m.tw_fwd = reinterpret_cast<const ulonglong2*>(dfwd);
         m.tw_inv = reinterpret_cast<const ulonglong2*>(dinv);
         m.ninv = host::invmod((uint64_t)c->N % q, q);
         m.ninv_s = host::mul_companion(m.ninv, q);
-        m.w1ninv = host::mulmod(ti[2 * 1], m.ninv, q);
+        uint64_t w1 = ti[2 * 1];   // psi^-brv(1): table word (binary64 bits on the F64 path)
+        if (m.fp == 2) {
+            double wd;
+            std::memcpy(&wd, &w1, 8);
+            w1 = (uint64_t)wd;
+        }
+        m.w1ninv = host::mulmod(w1, m.ninv, q);
         m.w1ninv_s = host::mul_companion(m.w1ninv, q);
         m.qinv_d = 1.0 / (double)q;
         {
@@ -1046,9 +1052,9 @@ edl_status edl_bfly_peak(edl_ctx* c, int32_t prime_index, int32_t iters, double*
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    launch_bfly_peak(c->dev(), m.q, m.fp != 0, m.tw_fwd + 1, iters, blocks, sink);   // warm-up
+    launch_bfly_peak(c->dev(), m.q, m.fp == 2, m.tw_fwd + 1, iters, blocks, sink);   // warm-up
     cudaEventRecord(a, c->st);
-    launch_bfly_peak(c->dev(), m.q, m.fp != 0, m.tw_fwd + 1, iters, blocks, sink);
+    launch_bfly_peak(c->dev(), m.q, m.fp == 2, m.tw_fwd + 1, iters, blocks, sink);
     cudaEventRecord(b, c->st);
     cudaEventSynchronize(b);
     float ms = 0.f;

@@ -23,8 +23,10 @@ struct ModInfo {
     uint64_t ninv, ninv_s;      // N^-1 mod q and Shoup companion
     uint64_t w1ninv, w1ninv_s;  // psi^-brv(1) * N^-1 (last INTT stage), Shoup companion
     uint64_t one_s;             // floor(2^64 / q): Shoup companion of 1 (64-bit reduction)
-    uint64_t fp;                // 1: q < 2^50, every constant companion is RD(w/q) as binary64
-                                //    (tw_mul<true>) and variable products use mulmod_fp
+    uint64_t fp;                // 1: q < 2^46, every constant companion is RD(w/q) as binary64
+                                //    (tw_mul<true>) and variable products use mulmod_fp;
+                                // 2: additionally q < 2^44, NTT butterflies on the FP64 pipe
+                                //    (twiddle tables hold binary64 {w, RD(w/q)})
     double qinv_d;              // RN(1/q) (mulmod_fp)
     double qinv_rd;             // RD(1/q) (twiddle companions computed on the fly)
 };

@@ -131,18 +131,27 @@ static uint64_t quotient_rd_bits(uint64_t w, uint64_t q) {
 // N <= 2^16).
 bool fp_quotient_prime(uint64_t q) { return q < (1ull << 46); }
 
+// q < 2^44: NTT butterflies on the FP64 pipe keep every intermediate below 2^50
+// (ntt_core.cuh F64 path bounds: forward < 15 q, inverse < 64 q).
+bool f64_ntt_prime(uint64_t q) { return q < (1ull << 44); }
+
 uint64_t mul_companion(uint64_t w, uint64_t q) { return fp_quotient_prime(q) ? quotient_rd_bits(w, q) : shoup_companion(w, q); }
 
 void twiddle_table(uint64_t q, uint64_t psi, int logn, bool inverse, std::vector<uint64_t>& out2) {
     const uint64_t n = 1ull << logn;
     const uint64_t base = inverse ? invmod(psi, q) : psi;
-    const bool fp = fp_quotient_prime(q);
+    const bool f64 = f64_ntt_prime(q);
     out2.assign(2 * n, 0);
     uint64_t p = 1;
     for (uint64_t k = 0; k < n; k++) {
         const uint32_t r = bitrev((uint32_t)k, logn);
-        out2[2 * r] = p;
-        out2[2 * r + 1] = fp ? quotient_rd_bits(p, q) : shoup_companion(p, q);
+        if (f64) {
+            const double pd = (double)p;   // exact: p < 2^44
+            std::memcpy(&out2[2 * r], &pd, 8);
+        } else {
+            out2[2 * r] = p;
+        }
+        out2[2 * r + 1] = f64 ? quotient_rd_bits(p, q) : shoup_companion(p, q);
         p = mulmod(p, base, q);
     }
 }

@@ -22,11 +22,12 @@ uint64_t minimal_psi(uint64_t q, int logn);
 // Alg. 8: returns chain bits (c+2 entries) and log2 N
 void parameterise(int c, int s, double p, std::vector<int>& bits, int& logn);
 
-// psi^{brv(k)} (or psi^{-brv(k)}) table with Shoup companions, interleaved {w, w'}
-// [N] pairs {psi^(+-brv(k)), companion}: the Shoup companion floor(w 2^64/q), or for
-// fp_quotient_prime(q) the bits of RD(w/q) (binary64) used by the FP64-quotient butterfly.
+// psi^{brv(k)} (or psi^{-brv(k)}) table, interleaved {w, w'}: [N] pairs
+// {psi^(+-brv(k)), floor(w 2^64/q)} (Shoup butterflies), or for f64_ntt_prime(q) the
+// binary64 bits of {w, RD(w/q)} used by the FP64-pipe butterflies (ntt_core.cuh).
 void twiddle_table(uint64_t q, uint64_t psi, int logn, bool inverse, std::vector<uint64_t>& out2);
 bool fp_quotient_prime(uint64_t q);
+bool f64_ntt_prime(uint64_t q);
 // companion of a constant w for the device's mulc(): RD(w/q) bits or floor(w 2^64/q)
 uint64_t mul_companion(uint64_t w, uint64_t q);
 

@@ -120,40 +120,65 @@ __device__ __forceinline__ uint64_t* cluster_smem(uint64_t* sm, int rank) {
     else return cooperative_groups::this_cluster().map_shared_rank(sm, rank);
 }
 
-// ---- forward CT butterfly.  Shoup path (Harvey): X, Y in [0,4q) -> [0,4q).
-// FP64-quotient path (q < 2^46): no reduction at all -- t = Y w mod q lands in [0, 2q) for
-// any Y < 2^52, so X' = X + t and Y' = X + 2q - t grow by at most 2q per stage and stay far
-// below 2^52 through 16 stages; the outputs are reduced once at the end (reduce_grown).
+// ---- forward CT butterfly, Shoup path (Harvey): X, Y in [0,4q) -> [0,4q).
+// ---- F64 path (ModInfo::fp == 2, q < 2^44): residues are held as exact binary64
+// integers (bit patterns in the same 64-bit registers / shared-memory words) and every
+// butterfly runs on the FP64 pipe, which the integer (fmaheavy) path leaves idle:
+//   t = Y w mod q:  hi = RN(Y w), lo = Y w - hi (exact, one FMA), qt = nearest integer to
+//   Y RD(w/q) (one FMA against 1.5 2^52, the product inside it exact), t = RN(hi - qt q) + lo.
+//   |Y (w/q - RD(w/q))| < |Y| 2^-53 <= 1/8 for |Y| < 2^50, so |t| <= 0.625 q, hi - qt q is an
+//   integer below 2^47 (exact), and t is exact.  Forward values stay signed and unreduced:
+//   |x| <= 4q + 0.625 q per stage < 15 q through 16 stages, far below 2^50.
+// 8 FP64 instructions per butterfly (B200: 64 FP64 lanes/clk/SM, measured 2.0 T
+// butterflies/s register-only vs 1.26 T for the integer FP64-quotient path).
+constexpr double F64_RND = 6755399441055744.0;   // 1.5 * 2^52: v + F64_RND - F64_RND = rint(v), |v| < 2^51
+constexpr double F64_TWO52 = 4503599627370496.0;
+
+__device__ __forceinline__ double f64_of(uint64_t bits) { return __longlong_as_double((long long)bits); }
+__device__ __forceinline__ uint64_t bits_of(double d) { return (uint64_t)__double_as_longlong(d); }
+
+// b w mod q in [-0.625 q, 0.625 q] for |b| < 2^50, w < q, wq = RD(w/q)
+__device__ __forceinline__ double f64_mulc(double b, double w, double wq, double q) {
+    const double hi = __dmul_rn(b, w);
+    const double lo = __fma_rn(b, w, -hi);
+    const double qt = __dsub_rn(__fma_rn(b, wq, F64_RND), F64_RND);
+    return __dadd_rn(__fma_rn(-qt, q, hi), lo);
+}
+// v mod q in [-0.51 q, 0.51 q] for |v| < 2^50 (qinv = RN(1/q))
+__device__ __forceinline__ double f64_reduce(double v, double q, double qinv) {
+    const double qt = __dsub_rn(__fma_rn(v, qinv, F64_RND), F64_RND);
+    return __fma_rn(-qt, q, v);
+}
+// canonical residue of an exact integer |r| < q, as uint64
+__device__ __forceinline__ uint64_t f64_to_canon(double r, double q) {
+    const double c = r < 0.0 ? __dadd_rn(q, F64_TWO52) : F64_TWO52;
+    return bits_of(__dadd_rn(r, c)) & 0xFFFFFFFFFFFFFull;
+}
+__device__ __forceinline__ uint64_t f64_from_u(uint64_t v) {   // v < 2^52 -> bits of (double)v
+    return bits_of(__hiloint2double(0x43300000 | (uint32_t)(v >> 32), (uint32_t)v) - F64_TWO52);
+}
+
 template <bool FP>
-__device__ __forceinline__ void ct_bfly(uint64_t& X, uint64_t& Y, ulonglong2 w, uint64_t q, uint64_t two_q) {
+__device__ __forceinline__ void ct_bfly(uint64_t& X, uint64_t& Y, ulonglong2 w, uint64_t q, uint64_t two_q,
+                                        double qd = 0.0) {
     if constexpr (FP) {
-        const uint64_t t = tw_mul_fp(Y, w.x, w.y, q);
-        Y = X + two_q - t;
-        X = X + t;
+        const double x = f64_of(X);
+        const double t = f64_mulc(f64_of(Y), f64_of(w.x), f64_of(w.y), qd);
+        X = bits_of(__dadd_rn(x, t));
+        Y = bits_of(__dsub_rn(x, t));
     } else {
         uint64_t x = csub(X, two_q);
-        uint64_t t = tw_mul<FP>(Y, w.x, w.y, q);
+        uint64_t t = shoup_lazy2(Y, w.x, w.y, q);
         X = x + t;
         Y = x - t + two_q;
     }
 }
 
-// Canonical value of v < 2^52 (the grown forward-NTT outputs of the FP64 path): quotient
-// floor(v RD(1/q)) is floor(v/q) or one less, so one conditional subtraction finishes.
-__device__ __forceinline__ uint64_t reduce_grown(uint64_t v, const ModInfo& m) {
-    const double magic = 4503599627370496.0;   // 2^52
-    const double vd = __hiloint2double(0x43300000 | (uint32_t)(v >> 32), (uint32_t)v) - magic;
-    const double t = __fma_rd(vd, m.qinv_rd, magic);
-    const uint64_t qt = (uint64_t)__double_as_longlong(t) & 0xFFFFFFFFFFFFFull;
-    return csub(v - qt * m.q, m.q);
-}
-
 // ---- inverse GS butterfly (Harvey): X, Y in [0,2q) -> [0,2q)
-template <bool FP>
 __device__ __forceinline__ void gs_bfly(uint64_t& X, uint64_t& Y, uint64_t w, uint64_t ws, uint64_t q, uint64_t two_q) {
     uint64_t x = X, y = Y;
     X = csub(x + y, two_q);
-    Y = tw_mul<FP>(x - y + two_q, w, ws, q);
+    Y = shoup_lazy2(x - y + two_q, w, ws, q);
 }
 
 // NS forward stages on a group x[0..2^NS) held in registers; absolute stage SA + k uses
@@ -161,7 +186,7 @@ __device__ __forceinline__ void gs_bfly(uint64_t& X, uint64_t& Y, uint64_t w, ui
 // above the stage window (SURVEY O3 stage twiddle psi^brv(m+i)).
 template <int SA, int NS, bool FP>
 __device__ __forceinline__ void fwd_pass_regs(uint64_t* x, int high, const ulonglong2* __restrict__ tw, uint64_t q,
-                                              uint64_t two_q, double qinv_rd = 0.0) {
+                                              uint64_t two_q, double qd) {
 #pragma unroll
     for (int k = 0; k < NS; k++) {
         const int half = 1 << (NS - 1 - k);
@@ -169,18 +194,8 @@ __device__ __forceinline__ void fwd_pass_regs(uint64_t* x, int high, const ulong
         for (int r = 0; r < (1 << NS); r++) {
             if (r & half) continue;
             const int tidx = (1 << (SA + k)) + (high << k) + (r >> (NS - k));
-#ifdef EDL_FP_TW_COMPACT
-            if constexpr (FP) {
-                const uint64_t wv = __ldg(reinterpret_cast<const unsigned long long*>(tw + tidx));
-                uint64_t xx = csub(x[r], two_q);
-                uint64_t t = tw_mul_fp_w(x[r + half], wv, qinv_rd, q);
-                x[r] = xx + t;
-                x[r + half] = xx - t + two_q;
-                continue;
-            }
-#endif
             ulonglong2 w = __ldg(tw + tidx);
-            ct_bfly<FP>(x[r], x[r + half], w, q, two_q);
+            ct_bfly<FP>(x[r], x[r + half], w, q, two_q, qd);
         }
 #ifdef EDL_STAGE_FENCE
         asm volatile("" ::: "memory");
@@ -189,32 +204,43 @@ __device__ __forceinline__ void fwd_pass_regs(uint64_t* x, int high, const ulong
 }
 
 // NS inverse stages, last to first; with LAST the absolute stage 0 folds N^-1 into both
-// outputs (psi^-brv(1) N^-1 for the odd one).
+// outputs (psi^-brv(1) N^-1 for the odd one).  F64 path: the differences leave through
+// f64_mulc (|.| <= 0.625 q) and the sums of the pass's last stage are reduced, so every
+// pass starts from |x| < 2q (first pass: loads in [0, 2q)) and grows to at most
+// 2q 2^NS <= 64 q < 2^50 inside it.
 template <int SA, int NS, bool LAST, bool FP>
 __device__ __forceinline__ void inv_pass_regs(uint64_t* x, int high, const ModInfo& m, uint64_t two_q) {
+    double qd = 0.0;
+    if constexpr (FP) qd = u52_to_double(m.q);
 #pragma unroll
     for (int k = NS - 1; k >= 0; k--) {
         const int half = 1 << (NS - 1 - k);
 #pragma unroll
         for (int r = 0; r < (1 << NS); r++) {
             if (r & half) continue;
-            if (LAST && SA + k == 0) {
+            if constexpr (FP) {
+                const double a = f64_of(x[r]), b = f64_of(x[r + half]);
+                if (LAST && SA + k == 0) {
+                    x[r] = bits_of(f64_mulc(__dadd_rn(a, b), u52_to_double(m.ninv), f64_of(m.ninv_s), qd));
+                    x[r + half] = bits_of(f64_mulc(__dsub_rn(a, b), u52_to_double(m.w1ninv), f64_of(m.w1ninv_s), qd));
+                } else {
+                    const int tidx = (1 << (SA + k)) + (high << k) + (r >> (NS - k));
+                    const ulonglong2 w = __ldg(m.tw_inv + tidx);
+                    double s = __dadd_rn(a, b);
+                    if (k == 0) s = f64_reduce(s, qd, m.qinv_d);
+                    x[r] = bits_of(s);
+                    x[r + half] = bits_of(f64_mulc(__dsub_rn(a, b), f64_of(w.x), f64_of(w.y), qd));
+                }
+            } else if (LAST && SA + k == 0) {
                 uint64_t a = x[r], b = x[r + half];
-                x[r] = tw_mul<FP>(a + b, m.ninv, m.ninv_s, m.q);
-                x[r + half] = tw_mul<FP>(a - b + two_q, m.w1ninv, m.w1ninv_s, m.q);
+                // fp == 1 primes (2^44 <= q < 2^46) take this path with RD(w/q) companions
+                x[r] = m.fp ? tw_mul_fp(a + b, m.ninv, m.ninv_s, m.q) : shoup_lazy2(a + b, m.ninv, m.ninv_s, m.q);
+                x[r + half] = m.fp ? tw_mul_fp(a - b + two_q, m.w1ninv, m.w1ninv_s, m.q)
+                                   : shoup_lazy2(a - b + two_q, m.w1ninv, m.w1ninv_s, m.q);
             } else {
                 const int tidx = (1 << (SA + k)) + (high << k) + (r >> (NS - k));
-#ifdef EDL_FP_TW_COMPACT
-                if constexpr (FP) {
-                    const uint64_t wv = __ldg(reinterpret_cast<const unsigned long long*>(m.tw_inv + tidx));
-                    const uint64_t xa = x[r], ya = x[r + half];
-                    x[r] = csub(xa + ya, two_q);
-                    x[r + half] = tw_mul_fp_w(xa - ya + two_q, wv, m.qinv_rd, m.q);
-                    continue;
-                }
-#endif
                 ulonglong2 w = __ldg(m.tw_inv + tidx);
-                gs_bfly<FP>(x[r], x[r + half], w.x, w.y, m.q, two_q);
+                gs_bfly(x[r], x[r + half], w.x, w.y, m.q, two_q);
             }
         }
 #ifdef EDL_STAGE_FENCE
@@ -254,7 +280,7 @@ __device__ __forceinline__ void pass_smem(uint64_t* sm, const ModInfo& m, uint64
         const int v = threadIdx.x + g * C::T;
         const int high = hc | (v >> PI::BLOW);
         if constexpr (INV) inv_pass_regs<PI::SA, PI::NS, false, FP>(x + g * (1 << PI::NS), high, m, two_q);
-        else fwd_pass_regs<PI::SA, PI::NS, FP>(x + g * (1 << PI::NS), high, m.tw_fwd, m.q, two_q, m.qinv_rd);
+        else fwd_pass_regs<PI::SA, PI::NS, FP>(x + g * (1 << PI::NS), high, m.tw_fwd, m.q, two_q, u52_to_double(m.q));
     }
 #pragma unroll
     for (int g = 0; g < PI::G; g++) {
@@ -291,19 +317,26 @@ __device__ __forceinline__ void ntt_fwd_impl(uint64_t* sm, const ModInfo& m, Loa
     using P0 = PassInfo<C, 0>;
     static_assert(P0::G == 1 && P0::BLOW == C::LOGM - C::LOGE, "pass 0 layout");
     const uint64_t q = m.q, two_q = 2 * q;
+    const double qd = FP ? u52_to_double(q) : 0.0;
     const int tid = threadIdx.x;
+    // F64 path: the loaded residues (< 4q) become exact binary64 integers
+    auto ld = [&](int idx) {
+        const uint64_t v = load(idx);
+        if constexpr (FP) return f64_from_u(v);
+        else return v;
+    };
     uint64_t x[C::E];
     if constexpr (C::K == 1) {
 #pragma unroll
-        for (int r = 0; r < C::E; r++) x[r] = load(tid + r * C::T);
+        for (int r = 0; r < C::E; r++) x[r] = ld(tid + r * C::T);
     } else {
         // phase A: columns j (this CTA's M/K of them) x all K sub-blocks, stages 0..logK-1
         const int j0 = C::crank() * (C::M / C::K) + tid;
 #pragma unroll
         for (int g = 0; g < C::E / C::K; g++) {
 #pragma unroll
-            for (int t = 0; t < C::K; t++) x[g * C::K + t] = load(j0 + g * C::T + t * C::M);
-            fwd_pass_regs<0, C::LOGK, FP>(x + g * C::K, 0, m.tw_fwd, q, two_q, m.qinv_rd);
+            for (int t = 0; t < C::K; t++) x[g * C::K + t] = ld(j0 + g * C::T + t * C::M);
+            fwd_pass_regs<0, C::LOGK, FP>(x + g * C::K, 0, m.tw_fwd, q, two_q, qd);
         }
         cluster_sync_all();   // every CTA is running and done with its shared memory
 #pragma unroll
@@ -316,7 +349,7 @@ __device__ __forceinline__ void ntt_fwd_impl(uint64_t* sm, const ModInfo& m, Loa
 #pragma unroll
         for (int r = 0; r < C::E; r++) x[r] = sm[spad(tid + r * C::T)];
     }
-    fwd_pass_regs<C::LOGK, C::LOGE, FP>(x, C::crank(), m.tw_fwd, q, two_q, m.qinv_rd);
+    fwd_pass_regs<C::LOGK, C::LOGE, FP>(x, C::crank(), m.tw_fwd, q, two_q, qd);
 #pragma unroll
     for (int r = 0; r < C::E; r++) sm[spad(tid + r * C::T)] = x[r];
     __syncthreads();
@@ -329,7 +362,7 @@ __device__ __forceinline__ void ntt_fwd_impl(uint64_t* sm, const ModInfo& m, Loa
 #pragma unroll
     for (int r = 0; r < C::E; r++) {
         uint64_t v = sm[spad(tid + r * C::T)];
-        if constexpr (FP) v = reduce_grown(v, m);
+        if constexpr (FP) v = f64_to_canon(f64_reduce(f64_of(v), qd, m.qinv_d), qd);
         else v = csub(csub(v, two_q), q);
         store(C::idx(r), v, pv[r]);
     }
@@ -341,9 +374,19 @@ __device__ __forceinline__ void ntt_fwd_impl(uint64_t* sm, const ModInfo& m, Loa
 template <class C, bool FP, class Load, class Pre, class Store>
 __device__ __forceinline__ void ntt_inv_impl(uint64_t* sm, const ModInfo& m, Load load, Pre pre, Store store) {
     const uint64_t q = m.q, two_q = 2 * q;
+    const double qd = FP ? u52_to_double(q) : 0.0;
     const int tid = threadIdx.x;
+    // F64 path: residues (< 2q) in as exact binary64 integers, canonical uint64 out
+    auto canon = [&](uint64_t v) {
+        if constexpr (FP) return f64_to_canon(f64_of(v), qd);
+        else return csub(v, q);
+    };
 #pragma unroll
-    for (int r = 0; r < C::E; r++) sm[spad(tid + r * C::T)] = load(C::idx(r));
+    for (int r = 0; r < C::E; r++) {
+        const uint64_t v = load(C::idx(r));
+        if constexpr (FP) sm[spad(tid + r * C::T)] = f64_from_u(v);
+        else sm[spad(tid + r * C::T)] = v;
+    }
     __syncthreads();
     inv_middle<C, C::NPASS - 1, FP>(sm, m, two_q);
     uint64_t x[C::E];
@@ -356,7 +399,7 @@ __device__ __forceinline__ void ntt_inv_impl(uint64_t* sm, const ModInfo& m, Loa
 #pragma unroll
         for (int r = 0; r < C::E; r++) pv[r] = pre(tid + r * C::T);
 #pragma unroll
-        for (int r = 0; r < C::E; r++) store(tid + r * C::T, csub(x[r], q), pv[r]);
+        for (int r = 0; r < C::E; r++) store(tid + r * C::T, canon(x[r]), pv[r]);
         __syncthreads();
     } else {
         constexpr int MK = C::M / C::K;
@@ -379,14 +422,14 @@ __device__ __forceinline__ void ntt_inv_impl(uint64_t* sm, const ModInfo& m, Loa
             for (int t = 0; t < C::K; t++) x[g * C::K + t] = sm[spad(t * MK + tid + g * C::T)];
             inv_pass_regs<0, C::LOGK, true, FP>(x + g * C::K, 0, m, two_q);
 #pragma unroll
-            for (int t = 0; t < C::K; t++) store(j0 + g * C::T + t * C::M, csub(x[g * C::K + t], q), pv[g * C::K + t]);
+            for (int t = 0; t < C::K; t++) store(j0 + g * C::T + t * C::M, canon(x[g * C::K + t]), pv[g * C::K + t]);
         }
         __syncthreads();
     }
 }
 
-// Public entry points: the twiddle-product flavour is uniform per limb (ModInfo::fp), so
-// the branch is uniform across the CTA.
+// Public entry points: the butterfly path is uniform per limb (ModInfo::fp == 2: F64,
+// else Shoup), so the branch is uniform across the CTA.
 // Epilogues come in two flavours: store(idx, v) or, with an operand fetcher,
 // pre(idx) -> operand (issued for all E outputs of a thread before the first store, so
 // the operand loads overlap) and store(idx, v, operand).
@@ -397,7 +440,7 @@ struct NoPre {
 template <class C, class Load, class Pre, class Store>
 __device__ __forceinline__ void ntt_fwd(uint64_t* sm, const ModInfo& m, Load load, Pre pre, Store store) {
 #ifndef EDL_NO_FP_QUOTIENT
-    if (m.fp) ntt_fwd_impl<C, true>(sm, m, load, pre, store);
+    if (m.fp == 2) ntt_fwd_impl<C, true>(sm, m, load, pre, store);
     else
 #endif
         ntt_fwd_impl<C, false>(sm, m, load, pre, store);
@@ -412,7 +455,7 @@ __device__ __forceinline__ void ntt_fwd(uint64_t* sm, const ModInfo& m, Load loa
 template <class C, class Load, class Pre, class Store>
 __device__ __forceinline__ void ntt_inv(uint64_t* sm, const ModInfo& m, Load load, Pre pre, Store store) {
 #ifndef EDL_NO_FP_QUOTIENT
-    if (m.fp) ntt_inv_impl<C, true>(sm, m, load, pre, store);
+    if (m.fp == 2) ntt_inv_impl<C, true>(sm, m, load, pre, store);
     else
 #endif
         ntt_inv_impl<C, false>(sm, m, load, pre, store);

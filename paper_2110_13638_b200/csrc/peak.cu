@@ -24,8 +24,8 @@ __global__ void __launch_bounds__(256) k_modmul_peak(uint64_t q, uint64_t w, uin
 
 // Register-only CT butterflies (ntt_core.cuh ct_bfly, the NTT's inner operation) on 16
 // residues per thread: 8 independent butterflies per round, twiddles held in registers, so
-// the kernel measures the butterfly issue ceiling of one arithmetic path (FP64-quotient
-// for q < 2^50, Shoup otherwise) with no memory traffic.  The "alu" roofline of the NTT
+// the kernel measures the butterfly issue ceiling of one arithmetic path (FP64 pipe for
+// q < 2^44, Shoup otherwise) with no memory traffic.  The "alu" roofline of the NTT
 // kernels (bench.py) is this rate for their mix of primes.
 template <bool FP>
 __global__ void __launch_bounds__(256) k_bfly_peak(uint64_t q, const ulonglong2* __restrict__ tw, int iters,
@@ -33,18 +33,28 @@ __global__ void __launch_bounds__(256) k_bfly_peak(uint64_t q, const ulonglong2*
     uint64_t x[16];
     ulonglong2 w[8];
 #pragma unroll
-    for (int k = 0; k < 16; k++) x[k] = (threadIdx.x * 16 + k + 1) % q;
+    for (int k = 0; k < 16; k++) {
+        x[k] = (threadIdx.x * 16 + k + 1) % q;
+        if constexpr (FP) x[k] = f64_from_u(x[k]);
+    }
 #pragma unroll
     for (int k = 0; k < 8; k++) w[k] = tw[k];
     const uint64_t two_q = 2 * q;
+    const double qd = u52_to_double(q);
     for (int it = 0; it < iters; it++) {
 #pragma unroll
-        for (int k = 0; k < 8; k++) ct_bfly<FP>(x[k], x[k + 8], w[k], q, two_q);   // the NTT's own butterfly
+        for (int k = 0; k < 8; k++) ct_bfly<FP>(x[k], x[k + 8], w[k], q, two_q, qd);   // the NTT's own butterfly
 #pragma unroll
         for (int k = 0; k < 8; k++) {   // pair different lanes next round
             const uint64_t tmp = x[k];
             x[k] = x[(k + 3) & 15];
             x[(k + 3) & 15] = tmp;
+        }
+        if constexpr (FP) {   // the F64 values grow by <= 0.625 q per round: reduce every 16 rounds
+            if ((it & 15) == 15) {
+#pragma unroll
+                for (int k = 0; k < 16; k++) x[k] = bits_of(f64_reduce(f64_of(x[k]), qd, 1.0 / qd));
+            }
         }
     }
     uint64_t acc = 0;

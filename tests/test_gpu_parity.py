@@ -80,6 +80,31 @@ def test_ntt_bit_exact(edl, logn):
     assert np.array_equal(t2.cpu().numpy().view(np.uint64).reshape(a.shape), oring.ntt_inv(a, mods, psis))
 
 
+@pytest.mark.parametrize("logn", [12, 14, 16])
+def test_ntt_prime_classes(edl, logn):
+    """Every butterfly path of the NTT core against the oracle: q < 2^44 (FP64-pipe
+    butterflies: 30- and 44-bit primes), 2^44 <= q < 2^46 (Shoup butterflies, FP64-quotient
+    constants: 45 bits), and Shoup with integer constants (50, 60 bits); one polynomial of
+    all-(q-1) residues drives the unreduced FP64 intermediates to their largest values."""
+    bits = [60, 30, 44, 45, 50, 60]
+    pp = edl.params_from_bits(logn, bits)
+    g = edl.Context(pp)
+    po = make_params(1 << logn, bits)
+    lvl = len(bits) - 2
+    n_polys = 3
+    mods = po.q[: lvl + 1] * n_polys
+    psis = po.psi[: lvl + 1] * n_polys
+    a = random_residues((n_polys, lvl + 1, 1 << logn), mods, seed=logn + 100)
+    for i in range(lvl + 1):
+        a[0, i, :] = np.uint64(po.q[i] - 1)
+    for inverse in (False, True):
+        t = torch.from_numpy(a.view(np.int64).reshape(-1).copy()).cuda()
+        g.ntt_(t, n_polys, lvl, inverse=inverse)
+        got = t.cpu().numpy().view(np.uint64).reshape(a.shape)
+        want = (oring.ntt_inv if inverse else oring.ntt_fwd)(a, mods, psis)
+        assert np.array_equal(got, want), ("inverse" if inverse else "forward")
+
+
 def test_ntt_special_prime_limb(edl):
     pp = edl.params_from_depth(2)
     g = edl.Context(pp)
