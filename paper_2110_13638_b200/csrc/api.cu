@@ -80,6 +80,7 @@ cudaEvent_t Prof::ev() {
 }
 void Prof::begin(const char* name, cudaStream_t st) {
     launches++;
+    last = name;
     if (!on) return;
     Rec r;
     r.name = name;
@@ -89,6 +90,13 @@ void Prof::begin(const char* name, cudaStream_t st) {
     recs.push_back(r);
 }
 void Prof::end(cudaStream_t st) {
+    if (sync_check) {
+        const cudaError_t e = cudaStreamSynchronize(st);
+        const cudaError_t l = cudaGetLastError();
+        if (e != cudaSuccess || l != cudaSuccess)
+            std::fprintf(stderr, "edl: kernel %s failed: %s\n", last ? last : "?",
+                         cudaGetErrorString(e != cudaSuccess ? e : l));
+    }
     if (!on || recs.empty()) return;
     cudaEventRecord(recs.back().b, st);
 }

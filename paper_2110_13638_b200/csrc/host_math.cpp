@@ -133,7 +133,14 @@ bool fp_quotient_prime(uint64_t q) { return q < (1ull << 46); }
 
 // q < 2^44: NTT butterflies on the FP64 pipe keep every intermediate below 2^50
 // (ntt_core.cuh F64 path bounds: forward < 15 q, inverse < 64 q).
-bool f64_ntt_prime(uint64_t q) { return q < (1ull << 44); }
+bool f64_ntt_prime(uint64_t q) {
+#ifdef EDL_NO_F64
+    (void)q;
+    return false;
+#else
+    return q < (1ull << 44);
+#endif
+}
 
 uint64_t mul_companion(uint64_t w, uint64_t q) { return fp_quotient_prime(q) ? quotient_rd_bits(w, q) : shoup_companion(w, q); }
 

@@ -2,6 +2,7 @@
 // sm_100a kernels.  Ciphertext arrays are uint64 [count][2][level+1][N] (NTT domain,
 // canonical residues), SURVEY §8(a) layout.
 #pragma once
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <vector>
@@ -29,6 +30,8 @@ struct Prof {
         cudaEvent_t a, b;
     };
     bool on = false;
+    bool sync_check = std::getenv("EDL_DEBUG_SYNC") != nullptr;   // debug: synchronise + check after every launch
+    const char* last = nullptr;
     int64_t launches = 0;
     std::vector<Rec> recs;
     std::vector<cudaEvent_t> pool;

@@ -113,6 +113,49 @@ __device__ __forceinline__ void pf_sub(const uint64_t* limb, int cr, bool whole)
 }
 
 __device__ __forceinline__ void cluster_sync_all() { cooperative_groups::this_cluster().sync(); }
+// Split cluster barrier without the release fence: arrive once this CTA's shared memory may
+// be overwritten by its peers (no pending reads: program start or after a __syncthreads),
+// wait (acquire) right before writing into a peer's shared memory.
+__device__ __forceinline__ void cluster_arrive_relaxed() { asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
+
+// ---- DSMEM exchange with asynchronous remote stores (K > 1) ---------------------------
+// Each CTA's residues for peer t leave as st.async (shared::cluster, 8 bytes) that count
+// their bytes against t's mbarrier; a CTA then waits on its own mbarrier for the (K-1)M/K
+// words its peers owe it instead of a second full cluster barrier with a release fence.
+// The mbarrier lives for one transform: initialised (and fenced for the cluster) before
+// the transform's relaxed cluster arrive, which every peer waits on before its first
+// remote store, and invalidated after the transform's closing __syncthreads.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_async_b64(uint32_t raddr, uint64_t v, uint32_t rmbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr), "l"(v), "r"(rmbar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_init_cluster(uint32_t mbar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n\tfence.mbarrier_init.release.cluster;" ::"r"(mbar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint32_t mbar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait0(uint32_t mbar) {   // phase 0 of a fresh mbarrier
+    uint32_t done;
+    do {
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], 0;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(done)
+                     : "r"(mbar)
+                     : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void mbar_inval(uint32_t mbar) { asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(mbar) : "memory"); }
+#ifndef EDL_XCHG_SYNC
+#define EDL_XCHG_ASYNC 1
+#endif
 
 template <class C>
 __device__ __forceinline__ uint64_t* cluster_smem(uint64_t* sm, int rank) {
@@ -319,6 +362,9 @@ __device__ __forceinline__ void ntt_fwd_impl(uint64_t* sm, const ModInfo& m, Loa
     const uint64_t q = m.q, two_q = 2 * q;
     const double qd = FP ? u52_to_double(q) : 0.0;
     const int tid = threadIdx.x;
+    __shared__ alignas(8) uint64_t xchg_mbar;
+    const uint32_t mb = smem_u32(&xchg_mbar);
+    (void)mb;
     // F64 path: the loaded residues (< 4q) become exact binary64 integers
     auto ld = [&](int idx) {
         const uint64_t v = load(idx);
@@ -330,6 +376,12 @@ __device__ __forceinline__ void ntt_fwd_impl(uint64_t* sm, const ModInfo& m, Loa
 #pragma unroll
         for (int r = 0; r < C::E; r++) x[r] = ld(tid + r * C::T);
     } else {
+#ifdef EDL_XCHG_ASYNC
+        if (tid == 0) mbar_init_cluster(mb);
+#endif
+#ifndef EDL_FULL_CLUSTER_SYNC
+        cluster_arrive_relaxed();   // shared memory free: kernel start or past the caller's last __syncthreads
+#endif
         // phase A: columns j (this CTA's M/K of them) x all K sub-blocks, stages 0..logK-1
         const int j0 = C::crank() * (C::M / C::K) + tid;
 #pragma unroll
@@ -338,7 +390,28 @@ __device__ __forceinline__ void ntt_fwd_impl(uint64_t* sm, const ModInfo& m, Loa
             for (int t = 0; t < C::K; t++) x[g * C::K + t] = ld(j0 + g * C::T + t * C::M);
             fwd_pass_regs<0, C::LOGK, FP>(x + g * C::K, 0, m.tw_fwd, q, two_q, qd);
         }
-        cluster_sync_all();   // every CTA is running and done with its shared memory
+#ifndef EDL_FULL_CLUSTER_SYNC
+        cluster_wait();       // every CTA is running and done with its shared memory
+#else
+        cluster_sync_all();
+#endif
+#ifdef EDL_XCHG_ASYNC
+        if (tid == 0) mbar_expect(mb, (uint32_t)((C::K - 1) * (C::M / C::K) * 8));
+#pragma unroll
+        for (int t = 0; t < C::K; t++) {
+            if (t == C::crank()) {
+#pragma unroll
+                for (int g = 0; g < C::E / C::K; g++) sm[spad(j0 + g * C::T)] = x[g * C::K + t];
+            } else {
+                const uint32_t rb = mapa_u32(mb, t);
+                const uint32_t rs = mapa_u32(smem_u32(sm), t);
+#pragma unroll
+                for (int g = 0; g < C::E / C::K; g++) st_async_b64(rs + 8u * spad(j0 + g * C::T), x[g * C::K + t], rb);
+            }
+        }
+        __syncthreads();
+        mbar_wait0(mb);
+#else
 #pragma unroll
         for (int t = 0; t < C::K; t++) {
             uint64_t* dst = cluster_smem<C>(sm, t);
@@ -346,6 +419,7 @@ __device__ __forceinline__ void ntt_fwd_impl(uint64_t* sm, const ModInfo& m, Loa
             for (int g = 0; g < C::E / C::K; g++) dst[spad(j0 + g * C::T)] = x[g * C::K + t];
         }
         cluster_sync_all();
+#endif
 #pragma unroll
         for (int r = 0; r < C::E; r++) x[r] = sm[spad(tid + r * C::T)];
     }
@@ -367,6 +441,9 @@ __device__ __forceinline__ void ntt_fwd_impl(uint64_t* sm, const ModInfo& m, Loa
         store(C::idx(r), v, pv[r]);
     }
     __syncthreads();   // smem reusable by the caller's next transform
+#ifdef EDL_XCHG_ASYNC
+    if (C::K > 1 && tid == 0) mbar_inval(mb);
+#endif
 }
 
 // Inverse NTT of one limb.  load(idx) at idx = C::idx(r) -> residue in [0, 2q);
@@ -376,6 +453,9 @@ __device__ __forceinline__ void ntt_inv_impl(uint64_t* sm, const ModInfo& m, Loa
     const uint64_t q = m.q, two_q = 2 * q;
     const double qd = FP ? u52_to_double(q) : 0.0;
     const int tid = threadIdx.x;
+    __shared__ alignas(8) uint64_t xchg_mbar;
+    const uint32_t mb = smem_u32(&xchg_mbar);
+    (void)mb;
     // F64 path: residues (< 2q) in as exact binary64 integers, canonical uint64 out
     auto canon = [&](uint64_t v) {
         if constexpr (FP) return f64_to_canon(f64_of(v), qd);
@@ -403,13 +483,37 @@ __device__ __forceinline__ void ntt_inv_impl(uint64_t* sm, const ModInfo& m, Loa
         __syncthreads();
     } else {
         constexpr int MK = C::M / C::K;
+#if defined(EDL_INV_RELAXED) || defined(EDL_XCHG_ASYNC)
+        __syncthreads();      // this CTA's reads of its sub-block are performed
+#ifdef EDL_XCHG_ASYNC
+        if (tid == 0) mbar_init_cluster(mb);
+#endif
+        cluster_arrive_relaxed();
+        cluster_wait();       // ... and every peer's
+#else
         cluster_sync_all();   // every CTA has read its sub-block out of shared memory
+#endif
+#ifdef EDL_XCHG_ASYNC
+        if (tid == 0) mbar_expect(mb, (uint32_t)((C::K - 1) * MK * 8));
+        const uint32_t rs0 = smem_u32(sm);
+#pragma unroll
+        for (int r = 0; r < C::E; r++) {
+            const int j = tid + r * C::T;
+            const int t = r / (C::E / C::K);   // == j / MK (T divides MK)
+            const int w = spad(C::crank() * MK + (j & (MK - 1)));
+            if (t == C::crank()) sm[w] = x[r];
+            else st_async_b64(mapa_u32(rs0, t) + 8u * w, x[r], mapa_u32(mb, t));
+        }
+        __syncthreads();
+        mbar_wait0(mb);
+#else
 #pragma unroll
         for (int r = 0; r < C::E; r++) {
             const int j = tid + r * C::T;
             cluster_smem<C>(sm, j / MK)[spad(C::crank() * MK + (j & (MK - 1)))] = x[r];
         }
         cluster_sync_all();
+#endif
         // phase A': columns j x all K sub-blocks, stages logK-1..0 (N^-1 folded in)
         const int j0 = C::crank() * MK + tid;
 #pragma unroll
@@ -425,6 +529,9 @@ __device__ __forceinline__ void ntt_inv_impl(uint64_t* sm, const ModInfo& m, Loa
             for (int t = 0; t < C::K; t++) store(j0 + g * C::T + t * C::M, canon(x[g * C::K + t]), pv[g * C::K + t]);
         }
         __syncthreads();
+#ifdef EDL_XCHG_ASYNC
+        if (tid == 0) mbar_inval(mb);
+#endif
     }
 }
 
@@ -494,7 +601,9 @@ __device__ __forceinline__ void ntt_inv(uint64_t* sm, const ModInfo& m, Load loa
 #endif
 
 __host__ __device__ constexpr int cfg_logk(int logn, bool plain) {
-    return logn <= 13 ? 0 : (logn == 14 ? ((plain ? EDL_K14_PLAIN : EDL_K14_FUSED) == 2 ? 1 : 0) : logn - 13);
+    return logn <= 13 ? 0
+                      : (logn == 14 ? ((plain ? EDL_K14_PLAIN : EDL_K14_FUSED) == 4 ? 2 : ((plain ? EDL_K14_PLAIN : EDL_K14_FUSED) == 2 ? 1 : 0))
+                                    : logn - 13);
 }
 __host__ __device__ constexpr int cfg_logm(int logn, bool plain) { return logn - cfg_logk(logn, plain); }
 __host__ __device__ constexpr int cfg_loge(int logn, bool plain) {

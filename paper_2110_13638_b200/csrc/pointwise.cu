@@ -564,9 +564,9 @@ k_relin_mac2(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int
 #pragma unroll
             for (int j = 0; j < ND; j++)
                 if (j != ti) x[e][j] = xb[((size_t)c * xs_c + (size_t)j * xs_j) / 2];
-            ta1[e] = a1b[oc];
-            tb1[e] = b1b[oc];
-            if (ti <= l) {
+            if (ti <= l) {   // target P (ti = l + 1) has no limb in the input ciphertexts
+                ta1[e] = a1b[oc];
+                tb1[e] = b1b[oc];
                 ta0[e] = a0b[oc];
                 tb0[e] = b0b[oc];
             }
@@ -771,7 +771,11 @@ void launch_relin_mac(const Dev& d, const uint64_t* a, const uint64_t* b, int64_
         if (d.hmods[t].fp) tf.slot[nf++] = (int8_t)s;
         else ti.slot[ni++] = (int8_t)s;
     }
+#ifdef EDL_NO_MAC2
+    if (false) {
+#else
     if (l + 1 <= 4 && d.logn >= 8) {
+#endif
         const unsigned gx2 = (unsigned)((1 << d.logn) / (2 * MAC2_THREADS)), gz2 = (unsigned)((cnt + MAC2_CTS - 1) / MAC2_CTS);
         const size_t smem = (size_t)(l + 1) * 2 * 2 * MAC2_THREADS * sizeof(ulonglong2);
 #define EDL_MAC2(FPV, ND, LIST, NT)                                                                         \

@@ -231,6 +231,24 @@ def test_large_n_keys_relin_rescale(edl, logn):
     assert np.array_equal(sq_g.numpy(g.n), sq_o.data)
 
 
+def test_mul_relin_c2_chain_batch(edl):
+    """C2's L=3 chain (60, 40, 60 | 60: the last data limb on the integer path) with a batch
+    of 64 ciphertexts: tensor + key-switch and the following rescale on the GPU, the last
+    two ciphertexts (whose successors lie past the array end) checked against the oracle."""
+    g, o = _pair(edl, logn=13, bits=[60, 40, 60, 60], seed=7)
+    lvl, cnt = 2, 64
+    A = ock.CtArray(_rand_ct(o, cnt, lvl, 61), lvl, 2.0 ** 40, o.key_id)
+    B = ock.CtArray(_rand_ct(o, cnt, lvl, 62), lvl, 2.0 ** 40, o.key_id)
+    m_g = g.mul_relin(_to_gpu(g, A.data, lvl, A.scale, o.key_id), _to_gpu(g, B.data, lvl, B.scale, o.key_id))
+    r_g = g.rescale(m_g)
+    tail = slice(cnt - 2, cnt)
+    At = ock.CtArray(A.data[tail], lvl, A.scale, o.key_id)
+    Bt = ock.CtArray(B.data[tail], lvl, B.scale, o.key_id)
+    m_o = o.mul_relin(At, Bt)
+    assert np.array_equal(m_g.numpy(g.n)[tail], m_o.data)
+    assert np.array_equal(r_g.numpy(g.n)[tail], o.rescale(m_o).data)
+
+
 def test_mul_relin_mixed_levels(c0pair):
     g, o = c0pair
     A = ock.CtArray(_rand_ct(o, 2, 2, 41), 2, 2.0 ** 40, o.key_id)
