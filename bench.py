@@ -38,7 +38,7 @@ def _args():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-steps", type=int, default=12)
     ap.add_argument("--cpu-windows", type=int, default=8, help="oracle sample size (windows of 49)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -304,21 +304,33 @@ def run_ours(a):
         copied = [torch.cuda.Event() for _ in range(2)]
         used = [torch.cuda.Event() for _ in range(2)]
 
+        trace = [] if os.environ.get("EDL_E2E_TRACE") else None
+
         def run_pipeline(nsteps, first_event=None):
             for k in range(nsteps):
                 buf = k % 2
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if trace is not None else None
                 with torch.cuda.stream(copy_stream):
                     if k >= 2:
                         copy_stream.wait_event(used[buf])      # step k-2 is done with this buffer
                     if k == 0 and first_event is not None:
                         first_event.record(copy_stream)
+                    if ev:
+                        ev[0].record(copy_stream)
                     wire[buf].copy_(host_in, non_blocking=True)
                     copied[buf].record(copy_stream)
+                    if ev:
+                        ev[1].record(copy_stream)
                 stream.wait_event(copied[buf])
+                if ev:
+                    ev[2].record(stream)
                 ctx.unpack(wire[buf], x.count, x.level, x.scale, x.key_id, out=dev_in[buf])
                 res = step(dev_in[buf])
                 host_out[buf].copy_(res.tensor, non_blocking=True)
                 used[buf].record(stream)
+                if ev:
+                    ev[3].record(stream)
+                    trace.append(ev)
 
         run_pipeline(2)
         stream.synchronize()
@@ -330,6 +342,12 @@ def run_ours(a):
         stream.synchronize()
         copy_stream.synchronize()
         barrier()
+        if trace:
+            t0 = trace[2][0]
+            for k, ev in enumerate(trace[2:]):
+                print("e2e trace step %d: h2d %.2f-%.2f  compute %.2f-%.2f ms" % (
+                    k, t0.elapsed_time(ev[0]), t0.elapsed_time(ev[1]), t0.elapsed_time(ev[2]), t0.elapsed_time(ev[3])),
+                    file=sys.stderr)
         te = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=f"cuda:{local}")
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)

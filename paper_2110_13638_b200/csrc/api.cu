@@ -40,7 +40,8 @@ struct edl_ctx {
     uint64_t key_id = 0;
     uint64_t* d_scratch = nullptr;
     size_t scratch_words = 0;
-    uint8_t* h_pin = nullptr;
+    uint8_t* h_pin = nullptr;       // mapped pinned staging ring (host view)
+    uint8_t* h_pin_dev = nullptr;   // ... and its device view
     uint8_t* d_const = nullptr;
     size_t const_cap = 0, const_off = 0;
     std::string err;
@@ -141,9 +142,12 @@ uint64_t* scratch(edl_ctx* c, size_t words) {
     return c->d_scratch;
 }
 
-// Small constant tables (encoded weights): staged through a pinned ring, copied on
-// the stream.  Wrapping synchronises the stream, so a slot is never overwritten while
-// an earlier copy or kernel may still read it.
+// Small constant tables (encoded weights): staged through a mapped pinned ring and pulled
+// into the device ring by a copy kernel on the stream (zero-copy PCIe reads by the SMs),
+// not by the DMA engine: a large host->device transfer the caller overlaps with compute
+// (the next batch's ciphertexts) would otherwise hold the constants -- and the whole
+// stream behind them -- in the engine's queue.  Wrapping synchronises the stream, so a
+// slot is never overwritten while an earlier copy or kernel may still read it.
 template <class T>
 const T* upload(edl_ctx* c, const std::vector<T>& v) {
     const size_t bytes = (v.size() * sizeof(T) + 255) & ~size_t(255);
@@ -155,7 +159,9 @@ const T* upload(edl_ctx* c, const std::vector<T>& v) {
     uint8_t* h = c->h_pin + c->const_off;
     uint8_t* d = c->d_const + c->const_off;
     std::memcpy(h, v.data(), v.size() * sizeof(T));
-    cudaMemcpyAsync(d, h, v.size() * sizeof(T), cudaMemcpyHostToDevice, c->st);
+    static_assert(sizeof(T) % 8 == 0, "constant tables are 64-bit words");
+    launch_fetch_mapped(c->dev(), reinterpret_cast<const uint64_t*>(c->h_pin_dev + c->const_off),
+                        reinterpret_cast<uint64_t*>(d), (int64_t)(v.size() * sizeof(T) / 8));
     c->const_off += bytes;
     return reinterpret_cast<const T*>(d);
 }
@@ -337,7 +343,11 @@ edl_status edl_ctx_create(const edl_params* p, int32_t device, void* stream, edl
     cudaMalloc(&c->d_cc, sizeof(ChainConsts));
     cudaMemcpy(c->d_cc, c->h_cc, sizeof(ChainConsts), cudaMemcpyHostToDevice);
     c->const_cap = 16u << 20;
-    cudaMallocHost(&c->h_pin, c->const_cap);
+    if (cudaHostAlloc(&c->h_pin, c->const_cap, cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->h_pin_dev), c->h_pin, 0) != cudaSuccess) {
+        edl_ctx_destroy(c);
+        return EDL_ERR_CUDA;
+    }
     cudaMalloc(&c->d_const, c->const_cap);
     if (!set_smem_attrs(c->logn)) {
         edl_ctx_destroy(c);

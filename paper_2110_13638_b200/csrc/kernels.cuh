@@ -203,6 +203,8 @@ void launch_decode_slots(const Dev& d, const uint64_t* r, int64_t n_vec, int nl,
 // wire format: residues of limb i in bits[i] bits (pointwise.cu); polys = count * 2
 void launch_unpack(const Dev& d, const uint64_t* in, int64_t polys, int nl, const int* bits, uint64_t* out);
 void launch_pack(const Dev& d, const uint64_t* in, int64_t polys, int nl, const int* bits, uint64_t* out);
+// dst[0..words) = src (mapped pinned host memory read by the SMs: no DMA engine)
+void launch_fetch_mapped(const Dev& d, const uint64_t* src, uint64_t* dst, int64_t words);
 
 // ---- randomness / keys / encryption (rng.cu) ----
 void launch_keygen(const Dev& d, uint64_t seed, uint64_t* s_hat /*[L+2][N]*/, uint64_t* pk /*[2][L+1][N]*/,

@@ -6,6 +6,8 @@
 // are order independent, so this is bit-identical to per-step reduction).
 #include <type_traits>
 
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace edl {
@@ -752,6 +754,17 @@ void launch_unpack(const Dev& d, const uint64_t* in, int64_t polys, int nl, cons
     const PackInfo pi = pack_info(d, nl, bits, &pw);
     EDL_LAUNCH(d, "k_unpack", k_unpack<<<rows_grid(d.logn + 1, polys * nl), PW_THREADS, 0, d.st>>>(in, polys, nl, pw, pi,
                                                                                                      out, d.logn));
+}
+
+__global__ void k_fetch_mapped(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst, int64_t words) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < words; k += (int64_t)gridDim.x * blockDim.x)
+        dst[k] = src[k];
+}
+
+void launch_fetch_mapped(const Dev& d, const uint64_t* src, uint64_t* dst, int64_t words) {
+    if (words <= 0) return;
+    const unsigned blocks = (unsigned)std::min<int64_t>((words + 255) / 256, 148);
+    EDL_LAUNCH(d, "k_fetch_mapped", k_fetch_mapped<<<blocks, 256, 0, d.st>>>(src, dst, words));
 }
 
 void launch_pack(const Dev& d, const uint64_t* in, int64_t polys, int nl, const int* bits, uint64_t* out) {
