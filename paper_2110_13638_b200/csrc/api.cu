@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -42,8 +43,14 @@ struct edl_ctx {
     size_t scratch_words = 0;
     uint8_t* h_pin = nullptr;       // mapped pinned staging ring (host view)
     uint8_t* h_pin_dev = nullptr;   // ... and its device view
-    uint8_t* d_const = nullptr;
-    size_t const_cap = 0, const_off = 0;
+    uint8_t* d_const = nullptr;     // device cache of constant tables (bump-allocated)
+    size_t const_cap = 0, const_off = 0;     // staging ring
+    size_t cache_cap = 0, cache_off = 0;     // device cache
+    struct CacheEnt {
+        size_t off;
+        std::vector<uint8_t> bytes;
+    };
+    std::unordered_multimap<uint64_t, CacheEnt> cache;   // content hash -> device copy
     std::string err;
     mutable Prof prof;
 
@@ -148,21 +155,43 @@ uint64_t* scratch(edl_ctx* c, size_t words) {
 // (the next batch's ciphertexts) would otherwise hold the constants -- and the whole
 // stream behind them -- in the engine's queue.  Wrapping synchronises the stream, so a
 // slot is never overwritten while an earlier copy or kernel may still read it.
+// Tables are cached on the device by content (a served model's encoded weights repeat
+// every batch): a hit costs a host hash + compare and no transfer at all.  A full cache
+// is dropped after synchronising the stream (queued kernels may still read it).
 template <class T>
 const T* upload(edl_ctx* c, const std::vector<T>& v) {
-    const size_t bytes = (v.size() * sizeof(T) + 255) & ~size_t(255);
-    if (bytes > c->const_cap) return nullptr;
+    static_assert(sizeof(T) % 8 == 0, "constant tables are 64-bit words");
+    const size_t raw = v.size() * sizeof(T);
+    const size_t bytes = (raw + 255) & ~size_t(255);
+    if (bytes > c->const_cap || bytes > c->cache_cap) return nullptr;
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(v.data());
+    uint64_t h = 1469598103934665603ull ^ raw;
+    for (size_t k = 0; k < raw / 8; k++) {
+        uint64_t w;
+        std::memcpy(&w, src + 8 * k, 8);
+        h = (h ^ w) * 1099511628211ull;
+        h ^= h >> 29;
+    }
+    auto range = c->cache.equal_range(h);
+    for (auto it = range.first; it != range.second; ++it)
+        if (it->second.bytes.size() == raw && std::memcmp(it->second.bytes.data(), src, raw) == 0)
+            return reinterpret_cast<const T*>(c->d_const + it->second.off);
+    if (c->cache_off + bytes > c->cache_cap) {
+        cudaStreamSynchronize(c->st);
+        c->cache.clear();
+        c->cache_off = 0;
+    }
     if (c->const_off + bytes > c->const_cap) {
         cudaStreamSynchronize(c->st);
         c->const_off = 0;
     }
-    uint8_t* h = c->h_pin + c->const_off;
-    uint8_t* d = c->d_const + c->const_off;
-    std::memcpy(h, v.data(), v.size() * sizeof(T));
-    static_assert(sizeof(T) % 8 == 0, "constant tables are 64-bit words");
+    std::memcpy(c->h_pin + c->const_off, src, raw);
+    uint8_t* d = c->d_const + c->cache_off;
     launch_fetch_mapped(c->dev(), reinterpret_cast<const uint64_t*>(c->h_pin_dev + c->const_off),
-                        reinterpret_cast<uint64_t*>(d), (int64_t)(v.size() * sizeof(T) / 8));
+                        reinterpret_cast<uint64_t*>(d), (int64_t)(raw / 8));
     c->const_off += bytes;
+    c->cache.emplace(h, edl_ctx::CacheEnt{c->cache_off, std::vector<uint8_t>(src, src + raw)});
+    c->cache_off += bytes;
     return reinterpret_cast<const T*>(d);
 }
 
@@ -343,12 +372,13 @@ edl_status edl_ctx_create(const edl_params* p, int32_t device, void* stream, edl
     cudaMalloc(&c->d_cc, sizeof(ChainConsts));
     cudaMemcpy(c->d_cc, c->h_cc, sizeof(ChainConsts), cudaMemcpyHostToDevice);
     c->const_cap = 16u << 20;
+    c->cache_cap = 64u << 20;
     if (cudaHostAlloc(&c->h_pin, c->const_cap, cudaHostAllocMapped) != cudaSuccess ||
         cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->h_pin_dev), c->h_pin, 0) != cudaSuccess) {
         edl_ctx_destroy(c);
         return EDL_ERR_CUDA;
     }
-    cudaMalloc(&c->d_const, c->const_cap);
+    cudaMalloc(&c->d_const, c->cache_cap);
     if (!set_smem_attrs(c->logn)) {
         edl_ctx_destroy(c);
         return EDL_ERR_CUDA;
