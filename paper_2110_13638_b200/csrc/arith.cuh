@@ -157,6 +157,34 @@ __device__ __forceinline__ double u52_to_double(uint64_t a) {   // exact for a <
     return __hiloint2double(0x43300000 | (uint32_t)(a >> 32), (uint32_t)a) - 4503599627370496.0;
 }
 
+// ---- exact binary64 residue arithmetic (ModInfo::fp == 2 moduli, q < 2^44; ntt_core.cuh)
+constexpr double F64_RND = 6755399441055744.0;   // 1.5 * 2^52: v + F64_RND - F64_RND = rint(v), |v| < 2^51
+constexpr double F64_TWO52 = 4503599627370496.0;
+
+__device__ __forceinline__ double f64_of(uint64_t bits) { return __longlong_as_double((long long)bits); }
+__device__ __forceinline__ uint64_t bits_of(double d) { return (uint64_t)__double_as_longlong(d); }
+
+// b w mod q in [-0.625 q, 0.625 q] for |b| < 2^50, w < q, wq = RD(w/q)
+__device__ __forceinline__ double f64_mulc(double b, double w, double wq, double q) {
+    const double hi = __dmul_rn(b, w);
+    const double lo = __fma_rn(b, w, -hi);
+    const double qt = __dsub_rn(__fma_rn(b, wq, F64_RND), F64_RND);
+    return __dadd_rn(__fma_rn(-qt, q, hi), lo);
+}
+// v mod q in [-0.51 q, 0.51 q] for |v| < 2^50 (qinv = RN(1/q))
+__device__ __forceinline__ double f64_reduce(double v, double q, double qinv) {
+    const double qt = __dsub_rn(__fma_rn(v, qinv, F64_RND), F64_RND);
+    return __fma_rn(-qt, q, v);
+}
+// canonical residue of an exact integer |r| < q, as uint64
+__device__ __forceinline__ uint64_t f64_to_canon(double r, double q) {
+    const double c = r < 0.0 ? __dadd_rn(q, F64_TWO52) : F64_TWO52;
+    return bits_of(__dadd_rn(r, c)) & 0xFFFFFFFFFFFFFull;
+}
+__device__ __forceinline__ uint64_t f64_from_u(uint64_t v) {   // v < 2^52 -> bits of (double)v
+    return bits_of(__hiloint2double(0x43300000 | (uint32_t)(v >> 32), (uint32_t)v) - F64_TWO52);
+}
+
 // Variable x variable product for q < 2^50 with the quotient from the FP64 pipe:
 // t = fma_rd(fl(a b), RN(1/q), 2^52) gives floor of a b/q within +-1 (relative error
 // < 2^-51 of a value < 2^50), so a b - qt q lies in [-q, 2q) and one signed correction

@@ -174,33 +174,6 @@ __device__ __forceinline__ uint64_t* cluster_smem(uint64_t* sm, int rank) {
 //   |x| <= 4q + 0.625 q per stage < 15 q through 16 stages, far below 2^50.
 // 8 FP64 instructions per butterfly (B200: 64 FP64 lanes/clk/SM, measured 2.0 T
 // butterflies/s register-only vs 1.26 T for the integer FP64-quotient path).
-constexpr double F64_RND = 6755399441055744.0;   // 1.5 * 2^52: v + F64_RND - F64_RND = rint(v), |v| < 2^51
-constexpr double F64_TWO52 = 4503599627370496.0;
-
-__device__ __forceinline__ double f64_of(uint64_t bits) { return __longlong_as_double((long long)bits); }
-__device__ __forceinline__ uint64_t bits_of(double d) { return (uint64_t)__double_as_longlong(d); }
-
-// b w mod q in [-0.625 q, 0.625 q] for |b| < 2^50, w < q, wq = RD(w/q)
-__device__ __forceinline__ double f64_mulc(double b, double w, double wq, double q) {
-    const double hi = __dmul_rn(b, w);
-    const double lo = __fma_rn(b, w, -hi);
-    const double qt = __dsub_rn(__fma_rn(b, wq, F64_RND), F64_RND);
-    return __dadd_rn(__fma_rn(-qt, q, hi), lo);
-}
-// v mod q in [-0.51 q, 0.51 q] for |v| < 2^50 (qinv = RN(1/q))
-__device__ __forceinline__ double f64_reduce(double v, double q, double qinv) {
-    const double qt = __dsub_rn(__fma_rn(v, qinv, F64_RND), F64_RND);
-    return __fma_rn(-qt, q, v);
-}
-// canonical residue of an exact integer |r| < q, as uint64
-__device__ __forceinline__ uint64_t f64_to_canon(double r, double q) {
-    const double c = r < 0.0 ? __dadd_rn(q, F64_TWO52) : F64_TWO52;
-    return bits_of(__dadd_rn(r, c)) & 0xFFFFFFFFFFFFFull;
-}
-__device__ __forceinline__ uint64_t f64_from_u(uint64_t v) {   // v < 2^52 -> bits of (double)v
-    return bits_of(__hiloint2double(0x43300000 | (uint32_t)(v >> 32), (uint32_t)v) - F64_TWO52);
-}
-
 template <bool FP>
 __device__ __forceinline__ void ct_bfly(uint64_t& X, uint64_t& Y, ulonglong2 w, uint64_t q, uint64_t two_q,
                                         double qd = 0.0) {

@@ -220,9 +220,12 @@ k_cc_mac2(const uint64_t* __restrict__ x, int l, int W, int kw, int stride, int 
     const int p = blockIdx.y / nl, i = blockIdx.y % nl;
     const int win = blockIdx.z;
     const int wr = win / Wo, wc = win % Wo;
+    const bool f64 = mods[i].fp == 2;   // uniform per CTA (limb i)
     for (int t = threadIdx.x; t < FC * taps; t += blockDim.x) {
         const int f = t / taps, tt = t % taps;
-        wsm[t] = (f0 + f < F) ? wk[((size_t)(f0 + f) * taps + tt) * nl + i] : make_ulonglong2(0, 0);
+        ulonglong2 w = (f0 + f < F) ? wk[((size_t)(f0 + f) * taps + tt) * nl + i] : make_ulonglong2(0, 0);
+        if (f64) w.x = f64_from_u(w.x);   // {binary64 w, RD(w/q)} for the FP64-pipe products
+        wsm[t] = w;
     }
     for (int t = threadIdx.x; t < taps; t += blockDim.x)
         tpix[t] = (wr * stride + t / kw) * W + (wc * stride + t % kw);
@@ -249,7 +252,23 @@ k_cc_mac2(const uint64_t* __restrict__ x, int l, int W, int kw, int stride, int 
             nxt[u] = (tt < taps) ? __ldg(reinterpret_cast<const ulonglong2*>(xb + tpix[tt] * ct_words))
                                  : make_ulonglong2(0, 0);
         }
-        if (fp) {
+        if (f64) {
+            // exact binary64 products t = x w mod q in [-0.625q, 0.625q] summed exactly
+            // (taps * 0.625 q < 2^51), reduced once at the end; accumulators hold doubles
+            const double qd = u52_to_double(m.q);
+#pragma unroll
+            for (int u = 0; u < CC2_TB; u++) {
+                const int tt = t0 + u < taps ? t0 + u : 0;
+                const double x0 = u52_to_double(cur[u].x), x1 = u52_to_double(cur[u].y);
+#pragma unroll
+                for (int f = 0; f < FC; f++) {
+                    const ulonglong2 w = wsm[f * taps + tt];
+                    const double wd = f64_of(w.x), wq = f64_of(w.y);
+                    acc[f][0].lo = bits_of(__dadd_rn(f64_of(acc[f][0].lo), f64_mulc(x0, wd, wq, qd)));
+                    acc[f][1].lo = bits_of(__dadd_rn(f64_of(acc[f][1].lo), f64_mulc(x1, wd, wq, qd)));
+                }
+            }
+        } else if (fp) {
 #pragma unroll
             for (int u = 0; u < CC2_TB; u++) {
                 const int tt = t0 + u < taps ? t0 + u : 0;   // out-of-range taps carry x = 0
@@ -280,8 +299,15 @@ k_cc_mac2(const uint64_t* __restrict__ x, int l, int W, int kw, int stride, int 
         if (f0 + f < F) {
             const int64_t o = (int64_t)(f0 + f) * n_out_per_f + win;
             uint64_t* dst = out + limb_off(o, p, i, nl, logn) + 2 * (size_t)n2;
-            const ulonglong2 v = fp ? make_ulonglong2(reduce64(acc[f][0].lo, m), reduce64(acc[f][1].lo, m))
-                                    : make_ulonglong2(barrett128(acc[f][0], m), barrett128(acc[f][1], m));
+            ulonglong2 v;
+            if (f64) {
+                const double qd = u52_to_double(m.q);
+                v = make_ulonglong2(f64_to_canon(f64_reduce(f64_of(acc[f][0].lo), qd, m.qinv_d), qd),
+                                    f64_to_canon(f64_reduce(f64_of(acc[f][1].lo), qd, m.qinv_d), qd));
+            } else {
+                v = fp ? make_ulonglong2(reduce64(acc[f][0].lo, m), reduce64(acc[f][1].lo, m))
+                       : make_ulonglong2(barrett128(acc[f][0], m), barrett128(acc[f][1], m));
+            }
             *reinterpret_cast<ulonglong2*>(dst) = v;
         }
     }
@@ -310,6 +336,8 @@ k_dense_mac(const uint64_t* __restrict__ x, int64_t K, int64_t O, int l, int ks,
     uint64_t* outp = out + (size_t)sl * ((size_t)O * 2 * nl << logn);
     const ModInfo& m = mods[i];
     const bool fp = m.fp != 0;
+    const bool f64 = m.fp == 2;   // FP64-pipe products (uniform per CTA)
+    const double qd = u52_to_double(m.q);
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = n < (1 << logn);
     const size_t kstride = (size_t)2 * nl << logn;            // one ciphertext
@@ -320,7 +348,9 @@ k_dense_mac(const uint64_t* __restrict__ x, int64_t K, int64_t O, int l, int ks,
         __syncthreads();
         for (int t = threadIdx.x; t < DN_OC * DN_KC; t += blockDim.x) {
             const int o = t / DN_KC, k = t % DN_KC;
-            wsm2[t] = (o0 + o < O && k < kc) ? wd[((size_t)(o0 + o) * K + (k0 + k)) * nl + i] : make_ulonglong2(0, 0);
+            ulonglong2 w = (o0 + o < O && k < kc) ? wd[((size_t)(o0 + o) * K + (k0 + k)) * nl + i] : make_ulonglong2(0, 0);
+            if (f64) w.x = f64_from_u(w.x);
+            wsm2[t] = w;
         }
         __syncthreads();
         if (!active) { first = false; continue; }
@@ -331,7 +361,17 @@ k_dense_mac(const uint64_t* __restrict__ x, int64_t K, int64_t O, int l, int ks,
             uint64_t xv[DN_U];
 #pragma unroll
             for (int u = 0; u < DN_U; u++) xv[u] = (k + u < kc) ? __ldg(xp + (size_t)(k0 + k + u) * kstride) : 0;
-            if (fp) {   // lazy [0, 2q) products summed in 64 bits (256 * 2q < 2^59)
+            if (f64) {   // exact binary64 products in [-0.625q, 0.625q], exact sums (DN_KC terms)
+#pragma unroll
+                for (int u = 0; u < DN_U; u++) {
+                    const double xd = u52_to_double(xv[u]);
+#pragma unroll
+                    for (int o = 0; o < DN_OC; o++) {
+                        const ulonglong2 w = wsm2[o * DN_KC + ((k + u) & (DN_KC - 1))];
+                        acc[o].lo = bits_of(__dadd_rn(f64_of(acc[o].lo), f64_mulc(xd, f64_of(w.x), f64_of(w.y), qd)));
+                    }
+                }
+            } else if (fp) {   // lazy [0, 2q) products summed in 64 bits (256 * 2q < 2^59)
 #pragma unroll
                 for (int u = 0; u < DN_U; u++) {
 #pragma unroll
@@ -352,7 +392,8 @@ k_dense_mac(const uint64_t* __restrict__ x, int64_t K, int64_t O, int l, int ks,
         for (int o = 0; o < DN_OC; o++) {
             if (o0 + o < O) {
                 uint64_t* dst = outp + limb_off(o0 + o, p, i, nl, logn) + n;
-                uint64_t v = fp ? reduce64(acc[o].lo, m) : barrett128(acc[o], m);
+                uint64_t v = f64 ? f64_to_canon(f64_reduce(f64_of(acc[o].lo), qd, m.qinv_d), qd)
+                                 : (fp ? reduce64(acc[o].lo, m) : barrett128(acc[o], m));
                 if (!first) v = addmod(v, *dst, m.q);
                 *dst = v;
             }
@@ -523,7 +564,7 @@ constexpr int MAC2_CPI = EDL_MAC2_CPI;
 #ifndef EDL_MAC2_LB
 #define EDL_MAC2_LB 4
 #endif
-template <bool FP, int ND>
+template <int MODE, int ND>   // MODE = ModInfo::fp of the launch's targets (0 Shoup/Barrett, 1 FP64 quotient, 2 FP64 pipe)
 __global__ void __launch_bounds__(MAC2_THREADS, EDL_MAC2_LB)
 k_relin_mac2(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l, int L, int64_t cnt,
              const uint64_t* __restrict__ xh, const uint64_t* __restrict__ rlk, const uint64_t* __restrict__ rlk_c,
@@ -531,6 +572,8 @@ k_relin_mac2(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int
              const ChainConsts* __restrict__ chain, int logn) {
     // [digit][comp][thread] {key pair, companion pair}
     extern __shared__ ulonglong2 ks[];
+    constexpr bool FP = MODE != 0;
+    constexpr bool F64 = MODE == 2;
     const int ti = tl.slot[blockIdx.y];
     const int t = (ti == l + 1) ? (L + 1) : ti;
     const ModInfo& m = mods[t];
@@ -541,7 +584,9 @@ k_relin_mac2(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int
 #pragma unroll
         for (int cc = 0; cc < 2; cc++) {
             const size_t o = (((size_t)j * 2 + cc) * (L + 2) + t) << logn;
-            ks[((j * 2 + cc) * 2 + 0) * MAC2_THREADS + threadIdx.x] = __ldg(v2(rlk + o) + k);
+            ulonglong2 kv = __ldg(v2(rlk + o) + k);
+            if constexpr (F64) kv = make_ulonglong2(f64_from_u(kv.x), f64_from_u(kv.y));   // binary64 key residues
+            ks[((j * 2 + cc) * 2 + 0) * MAC2_THREADS + threadIdx.x] = kv;
             if constexpr (FP) ks[((j * 2 + cc) * 2 + 1) * MAC2_THREADS + threadIdx.x] = __ldg(v2(rlk_c + o) + k);
         }
     const ulonglong2 pinv = (ti <= l) ? chain->qinv[L + 1][t] : make_ulonglong2(0, 0);
@@ -586,7 +631,19 @@ k_relin_mac2(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int
             ulonglong2 v[2];
 #pragma unroll
             for (int cc = 0; cc < 2; cc++) {
-                if constexpr (FP) {
+                if constexpr (F64) {   // exact binary64 products and sums (ND * 0.625 q < 2^47)
+                    const double qd = u52_to_double(m.q);
+                    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+                    for (int j = 0; j < ND; j++) {
+                        const ulonglong2 r = ks[((j * 2 + cc) * 2 + 0) * MAC2_THREADS + threadIdx.x];
+                        const ulonglong2 q = ks[((j * 2 + cc) * 2 + 1) * MAC2_THREADS + threadIdx.x];
+                        s0 = __dadd_rn(s0, f64_mulc(u52_to_double(x[e][j].x), f64_of(r.x), f64_of(q.x), qd));
+                        s1 = __dadd_rn(s1, f64_mulc(u52_to_double(x[e][j].y), f64_of(r.y), f64_of(q.y), qd));
+                    }
+                    v[cc] = make_ulonglong2(f64_to_canon(f64_reduce(s0, qd, m.qinv_d), qd),
+                                            f64_to_canon(f64_reduce(s1, qd, m.qinv_d), qd));
+                } else if constexpr (FP) {
                     uint64_t s0 = 0, s1 = 0;
 #pragma unroll
                     for (int j = 0; j < ND; j++) {
@@ -777,11 +834,12 @@ void launch_pack(const Dev& d, const uint64_t* in, int64_t polys, int nl, const 
 void launch_relin_mac(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t cnt, int l, const uint64_t* xh,
                       const uint64_t* rlk, const uint64_t* rlk_c, uint64_t* acc) {
     // one launch per arithmetic path (targets grouped by their modulus' mode)
-    TargetList tf, ti;
-    int nf = 0, ni = 0;
+    TargetList tf, ti, t6;
+    int nf = 0, ni = 0, n6 = 0;
     for (int s = 0; s <= l + 1; s++) {
         const int t = (s == l + 1) ? d.L + 1 : s;
-        if (d.hmods[t].fp) tf.slot[nf++] = (int8_t)s;
+        if (d.hmods[t].fp == 2) t6.slot[n6++] = (int8_t)s;
+        else if (d.hmods[t].fp) tf.slot[nf++] = (int8_t)s;
         else ti.slot[ni++] = (int8_t)s;
     }
 #ifdef EDL_NO_MAC2
@@ -796,8 +854,9 @@ void launch_relin_mac(const Dev& d, const uint64_t* a, const uint64_t* b, int64_
                                      a, b, l, d.L, cnt, xh, rlk, rlk_c, acc, LIST, *d.mt, d.cc, d.logn)))
 #define EDL_MAC2_ND(ND)                                  \
     case ND:                                             \
-        if (nf) EDL_MAC2(true, ND, tf, nf);              \
-        if (ni) EDL_MAC2(false, ND, ti, ni);             \
+        if (n6) EDL_MAC2(2, ND, t6, n6);                 \
+        if (nf) EDL_MAC2(1, ND, tf, nf);                 \
+        if (ni) EDL_MAC2(0, ND, ti, ni);                 \
         break;
         switch (l + 1) {
             EDL_MAC2_ND(1)
@@ -810,6 +869,7 @@ void launch_relin_mac(const Dev& d, const uint64_t* a, const uint64_t* b, int64_
         return;
     }
     const unsigned gx = (unsigned)((1 << d.logn) / (2 * PW_THREADS)), gz = (unsigned)((cnt + MAC_CB - 1) / MAC_CB);
+    for (int k = 0; k < n6; k++) tf.slot[nf++] = t6.slot[k];   // the generic pass runs every fp target on the FP64-quotient path
     if (nf)
         EDL_LAUNCH(d, "k_relin_mac", (k_relin_mac<true><<<dim3(gx, nf, gz), PW_THREADS, 0, d.st>>>(
                                          a, b, l, d.L, cnt, xh, rlk, rlk_c, acc, tf, *d.mt, d.cc, d.logn)));
