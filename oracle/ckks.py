@@ -166,6 +166,32 @@ class Context:
                 out[c, 1, i] = ring.add(ring.mul(v_hat[i], self.pk[1, i], q), e1_hat[i], q)
         return CtArray(out, lvl, float(scale), self.key_id)
 
+    def encrypt_poly_sk(self, polys: np.ndarray, enc_seed: int, obj0: int, scale: float,
+                        level: Optional[int] = None) -> CtArray:
+        """Secret-key encryption (DESIGN reading Z16; the paper's client owns s, PAPER.md:258-260,
+        314-316): for ciphertext c (object id obj = obj0 + c) and limb i,
+            c1_i = a_i = uniform(enc_seed, obj, limb i, TAG_SK_A)  (an NTT-domain residue vector),
+            c0_i = NTT_i(m + e) - a_i s_i,  e = CBD(enc_seed, obj, TAG_SK_E),
+        so c0 + c1 s = m + e exactly and c1 is a public function of (enc_seed, obj): the
+        ciphertext can travel as c0 plus the seed."""
+        if self.key_id is None:
+            raise CkksError("no key")
+        lvl = self.L if level is None else level
+        idx = list(range(lvl + 1))
+        polys = np.asarray(polys, dtype=np.int64)
+        count = polys.shape[0]
+        out = np.zeros((count, 2, lvl + 1, self.n), dtype=np.uint64)
+        for c in range(count):
+            obj = obj0 + c
+            e_hat = self.signed_to_ntt(smp.cbd(self.n, enc_seed, obj, smp.TAG_SK_E), idx)
+            m_hat = self.signed_to_ntt(polys[c], idx)
+            for i in idx:
+                q = self.q[i]
+                a = smp.uniform(self.n, enc_seed, obj, i, smp.TAG_SK_A, q)
+                out[c, 0, i] = ring.sub(ring.add(m_hat[i], e_hat[i], q), ring.mul(a, self.s_hat[i], q), q)
+                out[c, 1, i] = a
+        return CtArray(out, lvl, float(scale), self.key_id)
+
     def encrypt(self, slots: np.ndarray, enc_seed: int, obj0: int = 0, scale: Optional[float] = None,
                 level: Optional[int] = None) -> CtArray:
         """slots: float64 [count][n_slots]."""

@@ -13,6 +13,7 @@ from ._lib import lib
 
 TAG_S, TAG_PK_A, TAG_PK_E, TAG_RLK_A, TAG_RLK_E, TAG_ENC_V, TAG_ENC_E0, TAG_ENC_E1 = 1, 2, 3, 4, 5, 6, 7, 8
 TAG_GK_A, TAG_GK_E = 9, 10      # Galois keys (NEXT f1): object id = 64 * g + digit j
+TAG_SK_A, TAG_SK_E = 11, 12     # secret-key encryption (wire compression, DESIGN reading Z16)
 
 
 def philox4x32_10(ctr, key) -> np.ndarray:

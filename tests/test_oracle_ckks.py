@@ -181,3 +181,31 @@ def test_bookkeeping_errors(c0ctx):
     lo = c0ctx.rescale(c0ctx.mul_scalar(a, [1.0], float(c0ctx.q[2])))
     s = c0ctx.add(lo, a)
     assert s.level == 1
+
+
+def test_encrypt_sk_error_identity(c0ctx):
+    """Secret-key encryption (DESIGN reading Z16): c0 + c1 s = m + e exactly, with e the
+    TAG_SK_E CBD sample and the decryption pinned above; c1 is the seeded uniform draw."""
+    from oracle import sampling as smp
+    rng = np.random.default_rng(5)
+    polys = rng.integers(-2 ** 40, 2 ** 40, (2, c0ctx.n))
+    ct = c0ctx.encrypt_poly_sk(polys, enc_seed=9, obj0=4, scale=2.0 ** 40)
+    assert ct.data.shape == (2, 2, c0ctx.L + 1, c0ctx.n)
+    dec = c0ctx.decrypt_poly(ct)
+    for c in range(2):
+        e = smp.cbd(c0ctx.n, 9, 4 + c, smp.TAG_SK_E)
+        assert dec[c] == [int(m) + int(x) for m, x in zip(polys[c], e)]
+        for i in range(c0ctx.L + 1):
+            assert np.array_equal(ct.data[c, 1, i], smp.uniform(c0ctx.n, 9, 4 + c, i, smp.TAG_SK_A, c0ctx.q[i]))
+
+
+def test_encrypt_sk_homomorphic(c0ctx):
+    """A secret-key ciphertext computes with public-key ones under the same key."""
+    rng = np.random.default_rng(6)
+    z1, z2 = rng.uniform(-1, 1, (2, 1, 4096))
+    sc = c0ctx.p.scale
+    a = c0ctx.encrypt_poly_sk(np.stack([c0ctx.encode(z1[0], sc)]), 3, 0, sc)
+    b = c0ctx.encrypt(z2, 2, obj0=1)
+    m = c0ctx.rescale(c0ctx.mul_relin(a, b))
+    assert np.max(np.abs(c0ctx.decrypt(m, 4096) - z1 * z2)) < 1e-5
+    assert np.max(np.abs(c0ctx.decrypt(a, 4096) - z1)) < 1e-6
