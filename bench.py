@@ -224,6 +224,8 @@ def run_ours(a):
         imgs = c1_images(BATCH, 2110)
         polys = torch.from_numpy(ctx.encode(c1_slots(imgs))).to(f"cuda:{local}")
         x = ctx.encrypt_poly(polys, scale=float(2 ** 40), enc_seed=2, obj0=0)
+        # the same images as secret-key ciphertexts for the seeded wire format (e2e)
+        x_sk = ctx.encrypt_poly_sk(polys, scale=float(2 ** 40), enc_seed=3, obj0=0)
         del polys
         net = C1Net(ctx, K, kb, W, b)
 
@@ -240,6 +242,7 @@ def run_ours(a):
             full.append(ctx.encrypt_poly(polys, scale=float(2 ** 40), enc_seed=2, obj0=0))
             del polys
         x = parallel.rank_inputs(ctx, sh, full)
+        x_sk = None   # rank inputs are gathered ciphertexts: the e2e at N > 1 uses the public-key wire
         del full
         torch.cuda.empty_cache()
         partials = torch.empty(sh.partials_words(), dtype=torch.int64, device=f"cuda:{local}")
@@ -291,71 +294,96 @@ def run_ours(a):
     # device input buffers), so the pipeline is bound by the slower of PCIe and compute.
     e2e = None
     if not a.no_e2e:
-        # inputs travel in the packed wire format (edl.h: residues in bit-length-of-q bits)
-        packed = ctx.pack(x)
-        host_in = torch.empty(packed.numel(), dtype=torch.int64, pin_memory=True)
-        host_in.copy_(packed.cpu())
-        del packed
-        wire = [torch.empty(host_in.numel(), dtype=torch.int64, device=f"cuda:{local}") for _ in range(2)]
-        dev_in = [edl.CtArray(torch.empty_like(x.tensor), x.count, x.level, x.scale, x.key_id) for _ in range(2)]
         out_words = out.tensor.numel()
         host_out = [torch.empty(out_words, dtype=torch.int64, pin_memory=True) for _ in range(2)]
+        dev_in = [edl.CtArray(torch.empty_like(x.tensor), x.count, x.level, x.scale, x.key_id) for _ in range(2)]
         copy_stream = torch.cuda.Stream(device=local)
         copied = [torch.cuda.Event() for _ in range(2)]
         used = [torch.cuda.Event() for _ in range(2)]
-
         trace = [] if os.environ.get("EDL_E2E_TRACE") else None
 
-        def run_pipeline(nsteps, first_event=None):
-            for k in range(nsteps):
-                buf = k % 2
-                ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if trace is not None else None
-                with torch.cuda.stream(copy_stream):
-                    if k >= 2:
-                        copy_stream.wait_event(used[buf])      # step k-2 is done with this buffer
-                    if k == 0 and first_event is not None:
-                        first_event.record(copy_stream)
-                    if ev:
-                        ev[0].record(copy_stream)
-                    wire[buf].copy_(host_in, non_blocking=True)
-                    copied[buf].record(copy_stream)
-                    if ev:
-                        ev[1].record(copy_stream)
-                stream.wait_event(copied[buf])
-                if ev:
-                    ev[2].record(stream)
-                ctx.unpack(wire[buf], x.count, x.level, x.scale, x.key_id, out=dev_in[buf])
-                res = step(dev_in[buf])
-                host_out[buf].copy_(res.tensor, non_blocking=True)
-                used[buf].record(stream)
-                if ev:
-                    ev[3].record(stream)
-                    trace.append(ev)
+        def measure_e2e(host_in, unpack_into):
+            wire = [torch.empty(host_in.numel(), dtype=torch.int64, device=f"cuda:{local}") for _ in range(2)]
 
-        run_pipeline(2)
-        stream.synchronize()
-        copy_stream.synchronize()
-        barrier()
-        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        run_pipeline(a.e2e_steps, first_event=f0)
-        f1.record(stream)
-        stream.synchronize()
-        copy_stream.synchronize()
-        barrier()
-        if trace:
-            t0 = trace[2][0]
-            for k, ev in enumerate(trace[2:]):
-                print("e2e trace step %d: h2d %.2f-%.2f  compute %.2f-%.2f ms" % (
-                    k, t0.elapsed_time(ev[0]), t0.elapsed_time(ev[1]), t0.elapsed_time(ev[2]), t0.elapsed_time(ev[3])),
-                    file=sys.stderr)
-        te = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=f"cuda:{local}")
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * BATCH * a.e2e_steps / (float(te.item()) / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": int(host_in.numel() * 8), "d2h_bytes_per_step": int(out_words * 8),
-               "pipeline": "H2D of step k+1 on a copy stream overlaps step k (2 device input buffers); "
-                           "inputs in the packed wire format (edl_cts_pack/unpack), unpack inside the step",
-               "unpacked_bytes_per_step": int(x.tensor.numel() * 8)}
+            def run_pipeline(nsteps, first_event=None):
+                for k in range(nsteps):
+                    buf = k % 2
+                    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if trace is not None else None
+                    with torch.cuda.stream(copy_stream):
+                        if k >= 2:
+                            copy_stream.wait_event(used[buf])      # step k-2 is done with this buffer
+                        if k == 0 and first_event is not None:
+                            first_event.record(copy_stream)
+                        if ev:
+                            ev[0].record(copy_stream)
+                        wire[buf].copy_(host_in, non_blocking=True)
+                        copied[buf].record(copy_stream)
+                        if ev:
+                            ev[1].record(copy_stream)
+                    stream.wait_event(copied[buf])
+                    if ev:
+                        ev[2].record(stream)
+                    unpack_into(wire[buf], dev_in[buf])
+                    res = step(dev_in[buf])
+                    host_out[buf].copy_(res.tensor, non_blocking=True)
+                    used[buf].record(stream)
+                    if ev:
+                        ev[3].record(stream)
+                        trace.append(ev)
+
+            run_pipeline(2)
+            stream.synchronize()
+            copy_stream.synchronize()
+            barrier()
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if trace is not None:
+                trace.clear()
+            run_pipeline(a.e2e_steps, first_event=f0)
+            f1.record(stream)
+            stream.synchronize()
+            copy_stream.synchronize()
+            barrier()
+            if trace:
+                t0 = trace[0][0]
+                for k, ev in enumerate(trace):
+                    print("e2e trace step %d: h2d %.2f-%.2f  compute %.2f-%.2f ms" % (
+                        k, t0.elapsed_time(ev[0]), t0.elapsed_time(ev[1]), t0.elapsed_time(ev[2]),
+                        t0.elapsed_time(ev[3])), file=sys.stderr)
+            te = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=f"cuda:{local}")
+            if world > 1:
+                dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            del wire
+            return world * BATCH * a.e2e_steps / (float(te.item()) / 1e3)
+
+        def pinned(t):
+            h = torch.empty(t.numel(), dtype=torch.int64, pin_memory=True)
+            h.copy_(t.cpu())
+            return h
+
+        # public-key ciphertexts in the packed wire format (edl.h: residues in bit-length-of-q bits)
+        host_pk = pinned(ctx.pack(x))
+        v_pk = measure_e2e(host_pk, lambda w, o: ctx.unpack(w, x.count, x.level, x.scale, x.key_id, out=o))
+        e2e_pk = {"value": v_pk, "unit": UNIT, "h2d_bytes_per_step": int(host_pk.numel() * 8),
+                  "d2h_bytes_per_step": int(out_words * 8),
+                  "inputs": "public-key ciphertexts, packed wire format (edl_cts_pack/unpack)"}
+        del host_pk
+        pipeline = ("H2D of step k+1 on a copy stream overlaps step k (2 device input buffers); unpack and "
+                    "the step's kernels inside the timed region; 10 output ciphertexts read back every step")
+        if x_sk is not None:
+            # secret-key ciphertexts of the same images (reading Z16): c0 packed, c1 regenerated on the
+            # device from (enc_seed, object id) by edl_cts_unpack_seeded inside each step
+            host_sk = pinned(ctx.pack_c0(x_sk))
+            v_sk = measure_e2e(host_sk, lambda w, o: ctx.unpack_seeded(w, x_sk.count, x_sk.level, x_sk.scale,
+                                                                        x_sk.key_id, enc_seed=3, obj0=0, out=o))
+            e2e = {"value": v_sk, "unit": UNIT, "h2d_bytes_per_step": int(host_sk.numel() * 8),
+                   "d2h_bytes_per_step": int(out_words * 8),
+                   "inputs": "secret-key ciphertexts of the same 8192 images (DESIGN reading Z16): c0 in the "
+                             "packed wire format, c1 regenerated on the device from the 8-byte seed",
+                   "pipeline": pipeline, "public_key": e2e_pk,
+                   "unpacked_bytes_per_step": int(x.tensor.numel() * 8)}
+            del host_sk
+        else:
+            e2e = dict(e2e_pk, pipeline=pipeline, unpacked_bytes_per_step=int(x.tensor.numel() * 8))
 
     # ---- roofline of the dominant kernel (largest share of the timed region)
     n = ctx.n

@@ -123,6 +123,16 @@ edl_status edl_encode(edl_ctx* ctx, const double* slots, int64_t n_vec, int64_t 
 edl_status edl_encrypt_poly(edl_ctx* ctx, const int64_t* poly_dev, int64_t n_vec, int32_t level, double scale,
                             uint64_t enc_seed, uint32_t obj0, edl_cts* out);
 
+/* Secret-key encryption (DESIGN reading Z16; the client owns s in EDLaaS, PAPER.md:258-260,
+ * 314-316): for ciphertext c (Philox object id obj0 + c) and limb i,
+ *   c1_i = uniform(enc_seed, obj0 + c, limb i, tag 11)      (drawn in the NTT domain),
+ *   c0_i = NTT_i(m + e) - c1_i s_i,   e = CBD(enc_seed, obj0 + c, tag 12),
+ * so c0 + c1 s = m + e exactly and c1 is a public function of (enc_seed, obj0 + c): such
+ * ciphertexts can cross PCIe as c0 plus the seed (edl_cts_pack_c0 / edl_cts_unpack_seeded).
+ * Arguments, layout and errors as edl_encrypt_poly.  Asynchronous. */
+edl_status edl_encrypt_poly_sk(edl_ctx* ctx, const int64_t* poly_dev, int64_t n_vec, int32_t level, double scale,
+                               uint64_t enc_seed, uint32_t obj0, edl_cts* out);
+
 /* Host convenience: encode (host) + copy + encrypt at the top level L, scale 2^scale_bits. */
 edl_status edl_encrypt(edl_ctx* ctx, const double* slots, int64_t n_vec, int64_t n_slots, uint64_t enc_seed,
                        uint32_t obj0, edl_cts* out);
@@ -236,6 +246,20 @@ size_t edl_cts_packed_bytes(const edl_ctx* ctx, int64_t count, int32_t level);
 edl_status edl_cts_pack(edl_ctx* ctx, const edl_cts* in, void* packed);
 edl_status edl_cts_unpack(edl_ctx* ctx, const void* packed, int64_t count, int32_t level, double scale,
                           uint64_t key_id, edl_cts* out);
+
+/* Seeded wire format for secret-key ciphertexts: only c0 travels, in the packed layout
+ * above (half of edl_cts_packed_bytes); the receiver regenerates c1 from the seed.
+ * edl_cts_seeded_bytes: size of `count` ciphertexts at `level` (0 on bad arguments).
+ * edl_cts_pack_c0: device array `in` -> device buffer (caller-allocated, that size): the
+ *   c0 polynomials of every ciphertext (c1 is not read).
+ * edl_cts_unpack_seeded: device buffer -> device array `out` (edl_cts_bytes): c0 unpacked,
+ *   c1_i[k] = uniform(enc_seed, obj0 + c, limb i, tag 11) regenerated on the device (the
+ *   arguments the ciphertexts were encrypted with by edl_encrypt_poly_sk).  Sets out's
+ *   metadata.  Asynchronous.  Errors: EDL_ERR_ARG on null buffers or a bad level. */
+size_t edl_cts_seeded_bytes(const edl_ctx* ctx, int64_t count, int32_t level);
+edl_status edl_cts_pack_c0(edl_ctx* ctx, const edl_cts* in, void* packed);
+edl_status edl_cts_unpack_seeded(edl_ctx* ctx, const void* packed, int64_t count, int32_t level, double scale,
+                                 uint64_t key_id, uint64_t enc_seed, uint32_t obj0, edl_cts* out);
 
 /* Integer-pipe ceiling: lazy Shoup 64-bit modular multiplications per second measured
  * by a register-only kernel on all SMs (the "alu" roofline peak). */

@@ -504,6 +504,17 @@ edl_status edl_encrypt_poly(edl_ctx* c, const int64_t* poly, int64_t n_vec, int3
     return cuda_check(c, "encrypt");
 }
 
+edl_status edl_encrypt_poly_sk(edl_ctx* c, const int64_t* poly, int64_t n_vec, int32_t level, double scale,
+                               uint64_t enc_seed, uint32_t obj0, edl_cts* out) {
+    if (!c || !out || (!poly && n_vec > 0) || n_vec < 0) return fail(c, EDL_ERR_ARG, "encrypt_sk: bad arguments");
+    if (!c->has_key) return fail(c, EDL_ERR_NOKEY, "encrypt_sk: no key");
+    if (level < 0 || level > c->L) return fail(c, EDL_ERR_LEVEL, "encrypt_sk: level out of range");
+    if (!out->data && n_vec > 0) return fail(c, EDL_ERR_ARG, "encrypt_sk: null output");
+    if (n_vec > 0) launch_encrypt_sk(c->dev(), poly, n_vec, level, enc_seed, obj0, c->d_s, out->data);
+    set_meta(out, n_vec, level, scale, c->key_id);
+    return cuda_check(c, "encrypt_sk");
+}
+
 edl_status edl_encrypt(edl_ctx* c, const double* slots, int64_t n_vec, int64_t n_slots, uint64_t enc_seed,
                        uint32_t obj0, edl_cts* out) {
     if (!c) return EDL_ERR_ARG;
@@ -827,6 +838,38 @@ edl_status edl_cts_unpack(edl_ctx* c, const void* packed, int64_t count, int32_t
     }
     set_meta(out, count, level, scale, key_id);
     return cuda_check(c, "cts_unpack");
+}
+
+size_t edl_cts_seeded_bytes(const edl_ctx* c, int64_t count, int32_t level) {
+    return edl_cts_packed_bytes(c, count, level) / 2;
+}
+
+edl_status edl_cts_pack_c0(edl_ctx* c, const edl_cts* in, void* packed) {
+    if (!c) return EDL_ERR_ARG;
+    edl_status s = check_ct(c, in);
+    if (s != EDL_OK) return s;
+    if (in->count > 0 && !packed) return fail(c, EDL_ERR_ARG, "cts_pack_c0: null output");
+    if (in->count > 0) {
+        int bits[MAXM];
+        limb_bits(c, in->level + 1, bits);
+        launch_pack(c->dev(), in->data, in->count, in->level + 1, bits, reinterpret_cast<uint64_t*>(packed), 2);
+    }
+    return cuda_check(c, "cts_pack_c0");
+}
+
+edl_status edl_cts_unpack_seeded(edl_ctx* c, const void* packed, int64_t count, int32_t level, double scale,
+                                 uint64_t key_id, uint64_t enc_seed, uint32_t obj0, edl_cts* out) {
+    if (!c || !out || count < 0) return EDL_ERR_ARG;
+    if (level < 0 || level > c->L) return fail(c, EDL_ERR_ARG, "cts_unpack_seeded: level out of range");
+    if (count > 0 && (!packed || !out->data)) return fail(c, EDL_ERR_ARG, "cts_unpack_seeded: null buffer");
+    if (count > 0) {
+        int bits[MAXM];
+        limb_bits(c, level + 1, bits);
+        launch_unpack(c->dev(), reinterpret_cast<const uint64_t*>(packed), count, level + 1, bits, out->data, 2);
+        launch_expand_sk_a(c->dev(), out->data, count, level, enc_seed, obj0);
+    }
+    set_meta(out, count, level, scale, key_id);
+    return cuda_check(c, "cts_unpack_seeded");
 }
 
 // ---- NEXT f1: Galois rotations and plaintext vectors ----

@@ -140,6 +140,9 @@ template <int LOGN>
 void launch_encrypt_n(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint64_t seed, uint32_t obj0,
                       const uint64_t* pk, uint64_t* out);
 template <int LOGN>
+void launch_encrypt_sk_n(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint64_t seed, uint32_t obj0,
+                         const uint64_t* s_hat, uint64_t* out);
+template <int LOGN>
 void launch_keygen_galois_n(const Dev& d, uint64_t seed, uint32_t g, const uint64_t* s_hat, uint64_t* gk, uint64_t* gk_c);
 template <int LOGN>
 void launch_encode_pt_n(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint64_t* out);
@@ -201,8 +204,10 @@ void launch_decode_slots(const Dev& d, const uint64_t* r, int64_t n_vec, int nl,
                          double* z, void* scratch);
 
 // wire format: residues of limb i in bits[i] bits (pointwise.cu); polys = count * 2
-void launch_unpack(const Dev& d, const uint64_t* in, int64_t polys, int nl, const int* bits, uint64_t* out);
-void launch_pack(const Dev& d, const uint64_t* in, int64_t polys, int nl, const int* bits, uint64_t* out);
+void launch_unpack(const Dev& d, const uint64_t* in, int64_t polys, int nl, const int* bits, uint64_t* out,
+                   int stride = 1);
+void launch_pack(const Dev& d, const uint64_t* in, int64_t polys, int nl, const int* bits, uint64_t* out,
+                 int stride = 1);
 // dst[0..words) = src (mapped pinned host memory read by the SMs: no DMA engine)
 void launch_fetch_mapped(const Dev& d, const uint64_t* src, uint64_t* dst, int64_t words);
 
@@ -211,6 +216,10 @@ void launch_keygen(const Dev& d, uint64_t seed, uint64_t* s_hat /*[L+2][N]*/, ui
                    uint64_t* rlk /*[L+1][2][L+2][N]*/, uint64_t* rlk_s, uint64_t* scratch);
 void launch_encrypt(const Dev& d, const int64_t* msg /*[cnt][N]*/, int64_t cnt, int l, uint64_t seed, uint32_t obj0,
                     const uint64_t* pk, uint64_t* out);
+// secret-key encryption (reading Z16) and the server-side regeneration of its seeded c1
+void launch_encrypt_sk(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint64_t seed, uint32_t obj0,
+                       const uint64_t* s_hat, uint64_t* out);
+void launch_expand_sk_a(const Dev& d, uint64_t* ct, int64_t cnt, int l, uint64_t seed, uint32_t obj0);
 // m_hat = c0 + c1 s, INTT -> coefficient residues [cnt][l+1][N]
 void launch_decrypt(const Dev& d, const uint64_t* ct, int64_t cnt, int l, const uint64_t* s_hat, uint64_t* out);
 void launch_philox_words(const Dev& d, uint64_t seed, const uint32_t* ctr /*[n][4]*/, int64_t n, uint32_t* out);

@@ -732,8 +732,10 @@ struct PackInfo {
     int64_t loff[MAXM];
 };
 
+// `stride` = 2 packs/unpacks only polynomial 0 of each ciphertext (c0 of a seeded
+// secret-key ciphertext): wire polynomial p <-> array polynomial stride * p.
 __global__ void k_unpack(const uint64_t* __restrict__ in, int64_t polys, int nl, int64_t pw,
-                         const __grid_constant__ PackInfo pi, uint64_t* __restrict__ out, int logn) {
+                         const __grid_constant__ PackInfo pi, uint64_t* __restrict__ out, int logn, int stride) {
     const int64_t rows = polys * nl;
     const int n = 1 << logn;
     for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
@@ -742,7 +744,7 @@ __global__ void k_unpack(const uint64_t* __restrict__ in, int64_t polys, int nl,
         const int b = pi.bits[i];
         const uint64_t mask = (b == 64) ? ~0ull : ((1ull << b) - 1);
         const uint64_t* src = in + pl * pw + pi.loff[i];
-        uint64_t* dst = out + ((size_t)row << logn);
+        uint64_t* dst = out + (((size_t)pl * stride * nl + i) << logn);
         for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
             const uint64_t off = (uint64_t)k * b;
             const uint64_t w = off >> 6;
@@ -755,7 +757,7 @@ __global__ void k_unpack(const uint64_t* __restrict__ in, int64_t polys, int nl,
 }
 
 __global__ void k_pack(const uint64_t* __restrict__ in, int64_t polys, int nl, int64_t pw,
-                       const __grid_constant__ PackInfo pi, uint64_t* __restrict__ out, int logn) {
+                       const __grid_constant__ PackInfo pi, uint64_t* __restrict__ out, int logn, int stride) {
     const int64_t rows = polys * nl;
     const int n = 1 << logn;
     for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
@@ -763,7 +765,7 @@ __global__ void k_pack(const uint64_t* __restrict__ in, int64_t polys, int nl, i
         const int64_t pl = row / nl;
         const int b = pi.bits[i];
         const int64_t words = ((int64_t)n * b) >> 6;
-        const uint64_t* src = in + ((size_t)row << logn);
+        const uint64_t* src = in + (((size_t)pl * stride * nl + i) << logn);
         uint64_t* dst = out + pl * pw + pi.loff[i];
         for (int64_t w = blockIdx.x * blockDim.x + threadIdx.x; w < words; w += gridDim.x * blockDim.x) {
             // coefficients overlapping bits [64 w, 64 w + 64)
@@ -806,11 +808,11 @@ static PackInfo pack_info(const Dev& d, int nl, const int* bits, int64_t* pw) {
     return pi;
 }
 
-void launch_unpack(const Dev& d, const uint64_t* in, int64_t polys, int nl, const int* bits, uint64_t* out) {
+void launch_unpack(const Dev& d, const uint64_t* in, int64_t polys, int nl, const int* bits, uint64_t* out, int stride) {
     int64_t pw = 0;
     const PackInfo pi = pack_info(d, nl, bits, &pw);
     EDL_LAUNCH(d, "k_unpack", k_unpack<<<rows_grid(d.logn + 1, polys * nl), PW_THREADS, 0, d.st>>>(in, polys, nl, pw, pi,
-                                                                                                     out, d.logn));
+                                                                                                     out, d.logn, stride));
 }
 
 __global__ void k_fetch_mapped(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst, int64_t words) {
@@ -824,11 +826,11 @@ void launch_fetch_mapped(const Dev& d, const uint64_t* src, uint64_t* dst, int64
     EDL_LAUNCH(d, "k_fetch_mapped", k_fetch_mapped<<<blocks, 256, 0, d.st>>>(src, dst, words));
 }
 
-void launch_pack(const Dev& d, const uint64_t* in, int64_t polys, int nl, const int* bits, uint64_t* out) {
+void launch_pack(const Dev& d, const uint64_t* in, int64_t polys, int nl, const int* bits, uint64_t* out, int stride) {
     int64_t pw = 0;
     const PackInfo pi = pack_info(d, nl, bits, &pw);
     EDL_LAUNCH(d, "k_pack", k_pack<<<rows_grid(d.logn + 1, polys * nl), PW_THREADS, 0, d.st>>>(in, polys, nl, pw, pi, out,
-                                                                                                 d.logn));
+                                                                                                 d.logn, stride));
 }
 
 void launch_relin_mac(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t cnt, int l, const uint64_t* xh,

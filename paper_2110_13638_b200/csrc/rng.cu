@@ -24,6 +24,32 @@ void launch_encrypt(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint64
     EDL_DISPATCH_LOGN(d.logn, launch_encrypt_n<LOGN>(d, msg, cnt, l, seed, obj0, pk, out));
 }
 
+void launch_encrypt_sk(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint64_t seed, uint32_t obj0,
+                       const uint64_t* s_hat, uint64_t* out) {
+    EDL_DISPATCH_LOGN(d.logn, launch_encrypt_sk_n<LOGN>(d, msg, cnt, l, seed, obj0, s_hat, out));
+}
+
+// Seeded public component of secret-key ciphertexts: c1[c][i][k] = uniform(seed, k, obj0 + c, i, TAG_SK_A).
+__global__ void k_expand_sk_a(uint64_t* __restrict__ ct, int64_t cnt, int l, uint64_t seed, uint32_t obj0,
+                              const __grid_constant__ ModTable mods, int logn) {
+    const int64_t rows = cnt * (l + 1);
+    const int n = 1 << logn;
+    for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
+        const int i = (int)(row % (l + 1));
+        const int64_t c = row / (l + 1);
+        const ModInfo& m = mods[i];
+        uint64_t* c1 = ct + limb_off(c, 1, i, l + 1, logn);
+        for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+            c1[k] = uniform_of(draw(seed, (uint32_t)k, obj0 + (uint32_t)c, (uint32_t)i, TAG_SK_A), m);
+    }
+}
+
+void launch_expand_sk_a(const Dev& d, uint64_t* ct, int64_t cnt, int l, uint64_t seed, uint32_t obj0) {
+    const int64_t rows = cnt * (l + 1);
+    const dim3 grid((unsigned)((1 << d.logn) / 256), (unsigned)(rows < 65535 ? rows : 65535));
+    EDL_LAUNCH(d, "k_expand_sk_a", k_expand_sk_a<<<grid, 256, 0, d.st>>>(ct, cnt, l, seed, obj0, *d.mt, d.logn));
+}
+
 void launch_keygen_galois(const Dev& d, uint64_t seed, uint32_t g, const uint64_t* s_hat, uint64_t* gk, uint64_t* gk_c) {
     EDL_DISPATCH_LOGN(d.logn, launch_keygen_galois_n<LOGN>(d, seed, g, s_hat, gk, gk_c));
 }

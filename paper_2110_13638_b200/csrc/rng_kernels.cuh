@@ -11,7 +11,7 @@
 namespace edl {
 
 enum : uint32_t { TAG_S = 1, TAG_PK_A = 2, TAG_PK_E = 3, TAG_RLK_A = 4, TAG_RLK_E = 5, TAG_ENC_V = 6, TAG_ENC_E0 = 7,
-                  TAG_ENC_E1 = 8, TAG_GK_A = 9, TAG_GK_E = 10 };
+                  TAG_ENC_E1 = 8, TAG_GK_A = 9, TAG_GK_E = 10, TAG_SK_A = 11, TAG_SK_E = 12 };
 
 // NTT-domain index of sigma_g: evaluation point psi^{2 brv(k)+1} maps to psi^{(2 brv(k)+1) g}
 // (NEXT f1), so sigma_g(a)[k] = a[src_g(k)].
@@ -217,6 +217,32 @@ k_encrypt(const int64_t* __restrict__ msg, int l, int L, uint64_t seed, uint32_t
     }
 }
 
+// ---- secret-key encryption (DESIGN reading Z16): c1_i = a_i = uniform(seed, obj, i, TAG_SK_A)
+// drawn directly in the NTT domain, c0_i = NTT_i(m + e) - a_i s_i with e = CBD(TAG_SK_E).
+template <class C>
+__global__ void __launch_bounds__(C::T, C::MINB)
+k_encrypt_sk(const int64_t* __restrict__ msg, int l, uint64_t seed, uint32_t obj0, const uint64_t* __restrict__ s_hat,
+             uint64_t* __restrict__ out, const __grid_constant__ ModTable mods) {
+    extern __shared__ uint64_t sm[];
+    const int i = blockIdx.y;
+    const int64_t c = C::bx();
+    const uint32_t obj = obj0 + (uint32_t)c;
+    const ModInfo& m = mods[i];
+    const int64_t* mm = msg + ((size_t)c << C::LOGN);
+    uint64_t* c0 = out + limb_off(c, 0, i, l + 1, C::LOGN);
+    uint64_t* c1 = out + limb_off(c, 1, i, l + 1, C::LOGN);
+    const uint64_t* s = s_hat + ((size_t)i << C::LOGN);
+    auto ld = [&](int idx) {
+        return addmod(small_mod(cbd_of(draw(seed, idx, obj, 0, TAG_SK_E)), m.q), signed_mod(mm[idx], m), m.q);
+    };
+    auto st = [&](int idx, uint64_t v) {
+        const uint64_t a = uniform_of(draw(seed, idx, obj, i, TAG_SK_A), m);
+        c1[idx] = a;
+        c0[idx] = submod(v, mulmod(a, s[idx], m), m.q);
+    };
+    ntt_fwd<C>(sm, m, ld, st);
+}
+
 // ---- decrypt, device half: out[c][i] = INTT(c0 + c1 s)
 template <class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
@@ -252,6 +278,13 @@ void launch_encrypt_n(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint
 }
 
 template <int LOGN>
+void launch_encrypt_sk_n(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint64_t seed, uint32_t obj0,
+                         const uint64_t* s_hat, uint64_t* out) {
+    using C = CfgFused<LOGN>;
+    launch_cfg<C>(d, "k_encrypt_sk", k_encrypt_sk<C>, dim3((unsigned)cnt, l + 1), msg, l, seed, obj0, s_hat, out, *d.mt);
+}
+
+template <int LOGN>
 void launch_decrypt_n(const Dev& d, const uint64_t* ct, int64_t cnt, int l, const uint64_t* s_hat, uint64_t* out) {
     using C = CfgFused<LOGN>;
     launch_cfg<C>(d, "k_decrypt", k_decrypt<C>, dim3((unsigned)cnt, l + 1), ct, l, s_hat, out, *d.mt);
@@ -275,6 +308,8 @@ void launch_encode_pt_n(const Dev& d, const int64_t* msg, int64_t cnt, int l, ui
     template void launch_encrypt_n<LOGN>(const Dev&, const int64_t*, int64_t, int, uint64_t, uint32_t,          \
                                          const uint64_t*, uint64_t*);                                           \
     template void launch_decrypt_n<LOGN>(const Dev&, const uint64_t*, int64_t, int, const uint64_t*, uint64_t*);  \
+    template void launch_encrypt_sk_n<LOGN>(const Dev&, const int64_t*, int64_t, int, uint64_t, uint32_t,       \
+                                            const uint64_t*, uint64_t*);                                        \
     template void launch_keygen_galois_n<LOGN>(const Dev&, uint64_t, uint32_t, const uint64_t*, uint64_t*, uint64_t*); \
     template void launch_encode_pt_n<LOGN>(const Dev&, const int64_t*, int64_t, int, uint64_t*);
 

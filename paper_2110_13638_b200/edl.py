@@ -117,6 +117,12 @@ _sigs = {
                                       _c.c_uint32, _P(Cts)]),
     "edl_encrypt": (_c.c_int32, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int64, _c.c_uint64, _c.c_uint32,
                                  _P(Cts)]),
+    "edl_encrypt_poly_sk": (_c.c_int32, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int32, _c.c_double,
+                                         _c.c_uint64, _c.c_uint32, _P(Cts)]),
+    "edl_cts_seeded_bytes": (_c.c_size_t, [_c.c_void_p, _c.c_int64, _c.c_int32]),
+    "edl_cts_pack_c0": (_c.c_int32, [_c.c_void_p, _P(Cts), _c.c_void_p]),
+    "edl_cts_unpack_seeded": (_c.c_int32, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int32, _c.c_double,
+                                           _c.c_uint64, _c.c_uint64, _c.c_uint32, _P(Cts)]),
     "edl_decrypt_poly": (_c.c_int32, [_c.c_void_p, _P(Cts), _c.c_void_p]),
     "edl_decrypt": (_c.c_int32, [_c.c_void_p, _P(Cts), _c.c_void_p, _c.c_int64]),
     "edl_ct_add": (_c.c_int32, [_c.c_void_p, _P(Cts), _P(Cts), _P(Cts)]),
@@ -307,6 +313,19 @@ class Context:
                                           obj0, ctypes.byref(c)), "encrypt_poly")
         return o.update(c)
 
+    def encrypt_poly_sk(self, polys, scale: float, enc_seed: int, obj0: int = 0, level: Optional[int] = None,
+                        out: Optional[CtArray] = None) -> CtArray:
+        """Secret-key encryption with a seeded c1 (edl_encrypt_poly_sk, DESIGN reading Z16)."""
+        if isinstance(polys, np.ndarray):
+            polys = self.torch.from_numpy(np.ascontiguousarray(polys, dtype=np.int64)).to(self.device)
+        count = polys.shape[0]
+        lvl = self.L if level is None else level
+        o = out if out is not None else self.empty(count, lvl)
+        c = o.cts()
+        self._check(_lib.edl_encrypt_poly_sk(self._h, ctypes.c_void_p(polys.data_ptr()), count, lvl, scale,
+                                             enc_seed, obj0, ctypes.byref(c)), "encrypt_poly_sk")
+        return o.update(c)
+
     def encrypt(self, slots: np.ndarray, enc_seed: int, obj0: int = 0) -> CtArray:
         slots = np.ascontiguousarray(np.atleast_2d(slots), dtype=np.float64)
         o = self.empty(slots.shape[0], self.L)
@@ -489,6 +508,26 @@ class Context:
         co = o.cts()
         self._check(_lib.edl_cts_unpack(self._h, ctypes.c_void_p(packed.data_ptr()), count, level, scale, key_id,
                                         ctypes.byref(co)), "cts_unpack")
+        return o.update(co)
+
+    def seeded_bytes(self, count: int, level: int) -> int:
+        return int(_lib.edl_cts_seeded_bytes(self._h, count, level))
+
+    def pack_c0(self, x: CtArray, out=None):
+        """c0 of every ciphertext -> packed wire bytes (the seeded format of edl.h)."""
+        words = self.seeded_bytes(x.count, x.level) // 8
+        out = out if out is not None else self.torch.empty(words, dtype=self.torch.int64, device=self.device)
+        c = x.cts()
+        self._check(_lib.edl_cts_pack_c0(self._h, ctypes.byref(c), ctypes.c_void_p(out.data_ptr())), "cts_pack_c0")
+        return out
+
+    def unpack_seeded(self, packed, count: int, level: int, scale: float, key_id: int, enc_seed: int, obj0: int = 0,
+                      out: Optional[CtArray] = None) -> CtArray:
+        """Seeded wire bytes -> device ciphertext array (c1 regenerated from the seed)."""
+        o = out if out is not None else self.empty(count, level)
+        co = o.cts()
+        self._check(_lib.edl_cts_unpack_seeded(self._h, ctypes.c_void_p(packed.data_ptr()), count, level, scale,
+                                               key_id, enc_seed, obj0, ctypes.byref(co)), "cts_unpack_seeded")
         return o.update(co)
 
     def mod_reduce(self, x: CtArray) -> CtArray:
