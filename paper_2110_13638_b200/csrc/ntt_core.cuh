@@ -27,6 +27,7 @@
 //   MAC, bias) into the same pass over HBM.
 #pragma once
 #include <cooperative_groups.h>
+#include <type_traits>
 
 #include "arith.cuh"
 
@@ -265,6 +266,14 @@ __device__ __forceinline__ void inv_pass_regs(uint64_t* x, int high, const ModIn
     }
 }
 
+// A forward-transform epilogue may take the F64 path's outputs before canonicalisation:
+// a Store with a member f64(idx, x, operand) receives x as the exact binary64 integer
+// (|x| < 15 q, any residue class representative) and does its arithmetic on the FP64 pipe.
+template <class S, class = void>
+struct HasF64Store : std::false_type {};
+template <class S>
+struct HasF64Store<S, std::void_t<decltype(&S::f64)>> : std::true_type {};
+
 // In-CTA pass P over local stages [SL, SL+NS) of the M-point sub-block.
 template <class C, int P>
 struct PassInfo {
@@ -409,9 +418,13 @@ __device__ __forceinline__ void ntt_fwd_impl(uint64_t* sm, const ModInfo& m, Loa
 #pragma unroll
     for (int r = 0; r < C::E; r++) {
         uint64_t v = sm[spad(tid + r * C::T)];
-        if constexpr (FP) v = f64_to_canon(f64_reduce(f64_of(v), qd, m.qinv_d), qd);
-        else v = csub(csub(v, two_q), q);
-        store(C::idx(r), v, pv[r]);
+        if constexpr (FP && HasF64Store<Store>::value) {
+            store.f64(C::idx(r), f64_of(v), pv[r]);
+        } else {
+            if constexpr (FP) v = f64_to_canon(f64_reduce(f64_of(v), qd, m.qinv_d), qd);
+            else v = csub(csub(v, two_q), q);
+            store(C::idx(r), v, pv[r]);
+        }
     }
     __syncthreads();   // smem reusable by the caller's next transform
 #ifdef EDL_XCHG_ASYNC

@@ -87,12 +87,28 @@ k_rescale_ntt(const uint64_t* __restrict__ in, int l, const ulonglong2* __restri
     }
     auto ld = [&](int idx) { return center_mod(rr[idx], ql, ql_mod, m); };
     auto pre = [&](int idx) { return src[idx]; };
-    auto st = [&](int idx, uint64_t x, uint64_t a) {
-        if (has_w) a = mulc(a, wi, m);
-        uint64_t v = mulc(submod(a, x, m.q), qlinv, m);
-        dst[idx] = addmod(v, b, m.q);
+    // out = (a w_i - x) q_l^-1 + b: integer path on canonical x, or (F64 limbs) on the
+    // transform's unreduced binary64 output with exact FP64-pipe products
+    struct Store {
+        uint64_t* dst;
+        const ModInfo& m;
+        bool has_w;
+        ulonglong2 wi, qlinv;
+        uint64_t b;
+        __device__ __forceinline__ void operator()(int idx, uint64_t x, uint64_t a) const {
+            if (has_w) a = mulc(a, wi, m);
+            uint64_t v = mulc(submod(a, x, m.q), qlinv, m);
+            dst[idx] = addmod(v, b, m.q);
+        }
+        __device__ __forceinline__ void f64(int idx, double x, uint64_t a) const {
+            const double qd = u52_to_double(m.q);
+            double ad = u52_to_double(a);
+            if (has_w) ad = f64_mulc(ad, u52_to_double(wi.x), f64_of(wi.y), qd);
+            const double v = f64_mulc(__dsub_rn(ad, x), u52_to_double(qlinv.x), f64_of(qlinv.y), qd);
+            dst[idx] = f64_to_canon(f64_reduce(__dadd_rn(v, u52_to_double(b)), qd, m.qinv_d), qd);
+        }
     };
-    ntt_fwd<C>(sm, m, ld, pre, st);
+    ntt_fwd<C>(sm, m, ld, pre, Store{dst, m, has_w, wi, qlinv, b});
 }
 
 // ------------------------------------------------------------------------------------
@@ -253,8 +269,20 @@ k_relin_moddown_ntt(const uint64_t* __restrict__ a, const uint64_t* __restrict__
             return addmod(u, center_mod(ss[idx], ql, qlmod, m), m.q);
         };
         auto pre = [&](int idx) { return vi[idx]; };
-        auto st = [&](int idx, uint64_t x, uint64_t v) { dst[idx] = mulc(submod(v, x, m.q), qlinv, m); };
-        ntt_fwd<C>(sm, m, ld, pre, st);
+        struct Store {   // (v - x) q_l^-1; F64 limbs: on the unreduced binary64 transform output
+            uint64_t* dst;
+            const ModInfo& m;
+            ulonglong2 qlinv;
+            __device__ __forceinline__ void operator()(int idx, uint64_t x, uint64_t v) const {
+                dst[idx] = mulc(submod(v, x, m.q), qlinv, m);
+            }
+            __device__ __forceinline__ void f64(int idx, double x, uint64_t v) const {
+                const double qd = u52_to_double(m.q);
+                const double t = f64_mulc(__dsub_rn(u52_to_double(v), x), u52_to_double(qlinv.x), f64_of(qlinv.y), qd);
+                dst[idx] = f64_to_canon(t, qd);
+            }
+        };
+        ntt_fwd<C>(sm, m, ld, pre, Store{dst, m, qlinv});
     } else {
         // out = d + (acc - NTT([r])) P^-1 = v - NTT([r] P^-1)  (Z_q-linear, exact)
         auto ld = [&](int idx) { return mulc(center_mod(rr[idx], P, pmod, m), pinv, m); };
