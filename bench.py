@@ -435,6 +435,37 @@ def run_ours(a):
         ntt_rate = nb * 5 * 5 / (g0.elapsed_time(g1) / 1e3)
         del tl
 
+    # ---- C4's companion series: replica data parallelism, one independent
+    # 8192-image C1 batch per GPU and no communication, timed the same way (max over ranks)
+    replica = None
+    if world > 1:
+        polys = torch.from_numpy(ctx.encode(c1_slots(c1_images(BATCH, 2110 + rank)))).to(f"cuda:{local}")
+        xr = ctx.encrypt_poly(polys, scale=float(2 ** 40), enc_seed=2, obj0=0)
+        del polys
+        net_r = C1Net(ctx, K, kb, W, b)
+        for _ in range(max(a.warmup, 1)):
+            net_r.forward(xr)
+        stream.synchronize()
+        barrier()
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0.record(stream)
+        for _ in range(a.steps):
+            net_r.forward(xr)
+        r1.record(stream)
+        stream.synchronize()
+        barrier()
+        tr = torch.tensor([r0.elapsed_time(r1)], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(tr, op=dist.ReduceOp.MAX)
+        replica = {"value": world * BATCH * a.steps / (float(tr.item()) / 1e3), "unit": UNIT,
+                   "ms_per_step": float(tr.item()) / a.steps,
+                   "config": f"{world} independent C1 batches (one per GPU), no communication"}
+        del xr, net_r
+
+    props = torch.cuda.get_device_properties(local)
+    device = {"name": props.name, "sms": props.multi_processor_count,
+              "smem_per_sm_bytes": getattr(props, "shared_memory_per_multiprocessor", None),
+              "l2_bytes": getattr(props, "L2_cache_size", None), "hbm_bytes": props.total_memory}
+
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         ts = oracle_sample_seconds(a.cpu_windows)
@@ -458,7 +489,8 @@ def run_ours(a):
                                            f"dense partials"),
                            "l2": "inputs 1.03 GB per GPU > L2 (no flush)"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "clocks": clk, "dominant_kernel": dom[0], "kernels": kernels,
+                "clocks": clk, "dominant_kernel": dom[0], "kernels": kernels, "device": device,
+                "replica_dp": replica,
                 "ntt_limb_transforms_per_s": {"value": ntt_rate, "config": "N=2^14, C1 chain limbs q0..q4, 256 "
                                               "ciphertexts x 2 polys, forward NTT, device-timed (outside the "
                                               "timed C1 region)"}}

@@ -291,6 +291,7 @@ edl_status edl_ctx_create(const edl_params* p, int32_t device, void* stream, edl
     if (!p || !out) return EDL_ERR_ARG;
     *out = nullptr;
     if (p->log_n < 10 || p->log_n > 16 || p->n_data < 1 || p->n_data > EDL_MAX_PRIMES) return EDL_ERR_ARG;
+    if (!(((EDL_LOGNS_MASK) >> p->log_n) & 1)) return EDL_ERR_ARG;   // ring degree not compiled into this build
     for (int k = 0; k < p->n_data; k++)
         if (p->q[k] >= (1ull << 61)) return EDL_ERR_ARG;
     if (p->p_special >= (1ull << 61)) return EDL_ERR_ARG;
