@@ -560,6 +560,9 @@ __device__ __forceinline__ uint64_t mulc_path(uint64_t y, ulonglong2 w, const Mo
 #define EDL_MAC2_CPI 2
 #endif
 constexpr int MAC2_CPI = EDL_MAC2_CPI;
+#ifndef EDL_MAC2_CPI_F64
+#define EDL_MAC2_CPI_F64 1   // measured: 0.770 vs 0.786 ms (C1) with 2
+#endif
 
 #ifndef EDL_MAC2_LB
 #define EDL_MAC2_LB 4
@@ -602,10 +605,11 @@ k_relin_mac2(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int
     (void)limb;
     const int64_t c_beg = (int64_t)blockIdx.z * MAC2_CTS;
     const int64_t c_end = c_beg + MAC2_CTS < cnt ? c_beg + MAC2_CTS : cnt;
-    for (int64_t c0 = c_beg; c0 < c_end; c0 += MAC2_CPI) {
-        ulonglong2 x[MAC2_CPI][ND], ta0[MAC2_CPI], ta1[MAC2_CPI], tb0[MAC2_CPI], tb1[MAC2_CPI];
+    constexpr int CPI = F64 ? EDL_MAC2_CPI_F64 : MAC2_CPI;
+    for (int64_t c0 = c_beg; c0 < c_end; c0 += CPI) {
+        ulonglong2 x[CPI][ND], ta0[CPI], ta1[CPI], tb0[CPI], tb1[CPI];
 #pragma unroll
-        for (int e = 0; e < MAC2_CPI; e++) {   // issue every load of the CPI ciphertexts first
+        for (int e = 0; e < CPI; e++) {   // issue every load of the CPI ciphertexts first
             const int64_t c = (c0 + e < c_end) ? c0 + e : c0;
             const size_t oc = (size_t)c * cs / 2;   // in ulonglong2 units
 #pragma unroll
@@ -619,7 +623,7 @@ k_relin_mac2(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int
             }
         }
 #pragma unroll
-        for (int e = 0; e < MAC2_CPI; e++) {
+        for (int e = 0; e < CPI; e++) {
             const int64_t c = c0 + e;
             if (c >= c_end) break;
 #pragma unroll
