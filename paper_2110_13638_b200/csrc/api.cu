@@ -26,6 +26,8 @@ struct edl_ctx {
     int L = 0;              // top data level
     int device = 0;
     cudaStream_t st = nullptr;
+    cudaStream_t st2 = nullptr;              // side stream for independent branches of a schedule
+    cudaEvent_t fork = nullptr, join = nullptr;
     std::vector<ModInfo> h_mods;
     ModInfo* d_mods = nullptr;
     ModTable h_mt;
@@ -380,6 +382,12 @@ edl_status edl_ctx_create(const edl_params* p, int32_t device, void* stream, edl
         return EDL_ERR_CUDA;
     }
     cudaMalloc(&c->d_const, c->cache_cap);
+    if (cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming) != cudaSuccess) {
+        edl_ctx_destroy(c);
+        return EDL_ERR_CUDA;
+    }
     if (!set_smem_attrs(c->logn)) {
         edl_ctx_destroy(c);
         return EDL_ERR_CUDA;
@@ -408,6 +416,9 @@ void edl_ctx_destroy(edl_ctx* c) {
     }
     cudaFree(c->d_scratch);
     cudaFree(c->d_const);
+    if (c->st2) cudaStreamDestroy(c->st2);
+    if (c->fork) cudaEventDestroy(c->fork);
+    if (c->join) cudaEventDestroy(c->join);
     if (c->h_pin) cudaFreeHost(c->h_pin);
     delete c->h_cc;
     delete c;
@@ -1085,7 +1096,7 @@ edl_status edl_poly_activation(edl_ctx* c, const edl_cts* x, const double* coeff
     if (cnt > 0) {
         const size_t wl = ct_words(c, cnt, l - 1), wv = ct_words(c, cnt, l - 2);
         const size_t rs = relin_scratch_words(cnt, l, c->logn);
-        uint64_t* base = scratch(c, 3 * wl + wv + (size_t)cnt * 2 * c->N + rs);
+        uint64_t* base = scratch(c, 3 * wl + wv + 2 * (size_t)cnt * 2 * c->N + rs);
         if (!base) return fail(c, EDL_ERR_CUDA, "poly_activation: scratch");
         uint64_t* y2 = base;
         uint64_t* u = y2 + wl;
@@ -1097,11 +1108,23 @@ edl_status edl_poly_activation(edl_ctx* c, const edl_cts* x, const double* coeff
         const ulonglong2* w3 = upload(c, shoup_consts(c, i3, l));
         const ulonglong2* w1 = upload(c, shoup_consts(c, i1, l));
         const uint64_t* k0 = upload(c, residues(c, i0, l - 1));
-        uint64_t* r2 = rsc;   // second INTT output shares the relin scratch (used before relin 3.)
+        uint64_t* r2 = rsc + rs;   // second INTT output
+        // 2.+4. (independent of 1.) run on the side stream, overlapping 1.'s tails and its
+        // memory-light phases; 3. joins them
+        // (per-kernel profiling keeps one stream so every launch's event pair times it alone)
+        const bool side = !c->prof.on;
+        Dev d2 = d;
+        if (side) {
+            d2.st = c->st2;
+            cudaEventRecord(c->fork, c->st);
+            cudaStreamWaitEvent(c->st2, c->fork, 0);
+        }
+        launch_rescale_intt(d2, x->data, cnt, l, w3, r, w1, r2);                            // 2.+4. INTT shared
+        launch_rescale_ntt(d2, x->data, cnt, l, w3, r, nullptr, u);                         // 2.
+        launch_rescale_ntt(d2, x->data, cnt, l, w1, r2, nullptr, w, l - 2);                 // 4. (+ mod_drop)
+        if (side) cudaEventRecord(c->join, c->st2);
         launch_relin(d, x->data, x->data, cnt, l, true, c->d_rlk, c->d_rlk_s, rsc, y2);   // 1.
-        launch_rescale_intt(d, x->data, cnt, l, w3, r, w1, r2);                             // 2.+4. INTT shared
-        launch_rescale_ntt(d, x->data, cnt, l, w3, r, nullptr, u);                          // 2.
-        launch_rescale_ntt(d, x->data, cnt, l, w1, r2, nullptr, w, l - 2);                  // 4. (+ mod_drop)
+        if (side) cudaStreamWaitEvent(c->st, c->join, 0);
         launch_relin(d, u, y2, cnt, l - 1, true, c->d_rlk, c->d_rlk_s, rsc, v);              // 3.
         launch_add_add_const(d, v, w, l - 2, cnt, l - 2, k0, out->data);                       // 5.
     }

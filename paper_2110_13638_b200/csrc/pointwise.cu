@@ -206,11 +206,17 @@ k_cc_mac(const uint64_t* __restrict__ x, int l, int H, int W, int F, int kh, int
 // next batch's loads issued before the current batch's MACs (memory-level parallelism
 // without a second CTA's registers).
 constexpr int CC2_THREADS = 256;
-constexpr int CC2_TB = 4;
+#ifndef EDL_CC2_TB
+#define EDL_CC2_TB 4
+#endif
+#ifndef EDL_CC2_MINB
+#define EDL_CC2_MINB 2
+#endif
+constexpr int CC2_TB = EDL_CC2_TB;
 constexpr int CC2_MAXTAPS = 64;
 
 template <int FC>
-__global__ void __launch_bounds__(CC2_THREADS, 2)
+__global__ void __launch_bounds__(CC2_THREADS, EDL_CC2_MINB)
 k_cc_mac2(const uint64_t* __restrict__ x, int l, int W, int kw, int stride, int Wo, int taps, int f0, int F,
           int n_out_per_f, const ulonglong2* __restrict__ wk, uint64_t* __restrict__ out,
           const __grid_constant__ ModTable mods, int logn) {
