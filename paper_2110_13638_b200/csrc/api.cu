@@ -197,6 +197,32 @@ const T* upload(edl_ctx* c, const std::vector<T>& v) {
     return reinterpret_cast<const T*>(d);
 }
 
+// Key switch of a ciphertext batch split in two halves on the context's two streams: the
+// five-kernel pipeline of one half (ALU-bound transforms) overlaps the other's memory-bound
+// key-product pass and both halves' wave tails.  The halves use disjoint slices of every
+// per-ciphertext array (inputs, scratch, output), so they are independent; the main stream
+// joins the side stream before returning.  Profiling keeps one stream.
+void relin_split(edl_ctx* c, const Dev& d, const uint64_t* a, const uint64_t* b, int64_t cnt, int l, bool rescale,
+                 const uint64_t* rlk, const uint64_t* rlk_s, uint64_t* scr, uint64_t* out) {
+    const int64_t c0 = cnt / 2;
+    if (c->prof.on || c0 < 8) {
+        launch_relin(d, a, b, cnt, l, rescale, rlk, rlk_s, scr, out);
+        return;
+    }
+    const size_t in_w = (size_t)2 * (l + 1) << c->logn, out_w = (size_t)2 * (rescale ? l : l + 1) << c->logn;
+    Dev d2 = d;
+    d2.st = c->st2;
+    // (measured: starting the second half only after the first half's d2 INTT, to pair
+    // transforms with the key-product pass, is slower than the halves side by side)
+    cudaEventRecord(c->fork, c->st);
+    cudaStreamWaitEvent(c->st2, c->fork, 0);
+    launch_relin(d, a, b, c0, l, rescale, rlk, rlk_s, scr, out);
+    launch_relin(d2, a + c0 * in_w, b ? b + c0 * in_w : nullptr, cnt - c0, l, rescale, rlk, rlk_s,
+                 scr + relin_scratch_words(c0, l, c->logn), out + c0 * out_w);
+    cudaEventRecord(c->join, c->st2);
+    cudaStreamWaitEvent(c->st, c->join, 0);
+}
+
 bool scales_match(double a, double b) { return std::fabs(a - b) <= std::ldexp(1.0, -30) * std::fmax(a, b); }
 
 // O10: a constant encodes to rint(value * scale) (one IEEE multiply, round-half-even).
@@ -723,7 +749,7 @@ edl_status edl_ct_ct_mul_relin(edl_ctx* c, const edl_cts* a, const edl_cts* b, e
             launch_mod_drop(c->dev(), b->data, cnt, b->level, l, extra);
             pb = extra;
         }
-        launch_relin(c->dev(), pa, pb, cnt, l, false, c->d_rlk, c->d_rlk_s, base, out->data);
+        relin_split(c, c->dev(), pa, pb, cnt, l, false, c->d_rlk, c->d_rlk_s, base, out->data);
     }
     set_meta(out, cnt, l, a->scale * b->scale, a->key_id);
     return cuda_check(c, "mul_relin");
@@ -1025,7 +1051,7 @@ edl_status edl_poly_activation(edl_ctx* c, const edl_cts* x, const double* coeff
         if (cnt > 0) {
             uint64_t* base = scratch(c, relin_scratch_words(cnt, l, c->logn));
             if (!base) return fail(c, EDL_ERR_CUDA, "poly_activation: scratch");
-            launch_relin(d, x->data, x->data, cnt, l, true, c->d_rlk, c->d_rlk_s, base, out->data);
+            relin_split(c, d, x->data, x->data, cnt, l, true, c->d_rlk, c->d_rlk_s, base, out->data);
         }
         set_meta(out, cnt, l - 1, (x->scale * x->scale) / (double)c->prm.q[l], x->key_id);
         return cuda_check(c, "poly_activation");
@@ -1071,7 +1097,7 @@ edl_status edl_poly_activation(edl_ctx* c, const edl_cts* x, const double* coeff
             const ulonglong2* w2 = upload(c, shoup_consts(c, i2, l - 1));
             const ulonglong2* w1 = upload(c, shoup_consts(c, i1, l));
             const uint64_t* k0 = upload(c, residues(c, i0, l - 1));   // output level l-2: l-1 limbs
-            launch_relin(d, x->data, x->data, cnt, l, true, c->d_rlk, c->d_rlk_s, rsc, y2);
+            relin_split(c, d, x->data, x->data, cnt, l, true, c->d_rlk, c->d_rlk_s, rsc, y2);
             launch_rescale_intt(d, y2, cnt, l - 1, w2, r);
             launch_rescale_ntt(d, y2, cnt, l - 1, w2, r, nullptr, av);
             launch_rescale_intt(d, x->data, cnt, l, w1, r2);
@@ -1123,9 +1149,9 @@ edl_status edl_poly_activation(edl_ctx* c, const edl_cts* x, const double* coeff
         launch_rescale_ntt(d2, x->data, cnt, l, w3, r, nullptr, u);                         // 2.
         launch_rescale_ntt(d2, x->data, cnt, l, w1, r2, nullptr, w, l - 2);                 // 4. (+ mod_drop)
         if (side) cudaEventRecord(c->join, c->st2);
-        launch_relin(d, x->data, x->data, cnt, l, true, c->d_rlk, c->d_rlk_s, rsc, y2);   // 1.
+        relin_split(c, d, x->data, x->data, cnt, l, true, c->d_rlk, c->d_rlk_s, rsc, y2);    // 1.
         if (side) cudaStreamWaitEvent(c->st, c->join, 0);
-        launch_relin(d, u, y2, cnt, l - 1, true, c->d_rlk, c->d_rlk_s, rsc, v);              // 3.
+        relin_split(c, d, u, y2, cnt, l - 1, true, c->d_rlk, c->d_rlk_s, rsc, v);               // 3.
         launch_add_add_const(d, v, w, l - 2, cnt, l - 2, k0, out->data);                       // 5.
     }
     set_meta(out, cnt, l - 2, S3, x->key_id);
