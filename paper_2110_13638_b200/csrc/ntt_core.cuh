@@ -574,7 +574,7 @@ __device__ __forceinline__ void ntt_inv(uint64_t* sm, const ModInfo& m, Load loa
 #define EDL_K14_PLAIN 1
 #endif
 #ifndef EDL_K14_FUSED
-#define EDL_K14_FUSED 2
+#define EDL_K14_FUSED 4   // fused kernels at 2^14: 4-CTA clusters x 256 threads x 16 residues, 4 CTAs/SM
 #endif
 #ifndef EDL_LOGE_P14
 #define EDL_LOGE_P14 4
@@ -628,6 +628,13 @@ template <int LOGN>   // key-switch MAC kernel (largest epilogue)
 using CfgKs = CfgFusedE<LOGN, cfg_logm(LOGN, false) == 14 ? EDL_LOGE_KS14 : cfg_loge(LOGN, false)>;
 template <int LOGN>
 using CfgPlain = CfgOf<LOGN, true>;
+// Batched plain transforms (k_ntt_limbs): at 2^14 a 2-CTA cluster of 512 threads x 16
+// residues, 2 CTAs/SM (7.6 M limb-transforms/s forward vs 7.2 with the fused kernels'
+// 4-CTA clusters, whose 12 local stages avoid the 1-stage pass that 13 local stages need
+// and win inside the fused kernels: C1 4.77 vs 4.85 ms); below 2^14 the fused config.
+template <int LOGN>
+using CfgNttLimbs = typename std::conditional<
+    (LOGN == 14), NttCfg<14, 1, 4, 2>, typename std::conditional<(LOGN < 14), CfgOf<LOGN, false>, CfgOf<LOGN, true>>::type>::type;
 template <int LOGN>
 using CfgFused = CfgOf<LOGN, false>;
 

@@ -294,9 +294,7 @@ k_relin_moddown_ntt(const uint64_t* __restrict__ a, const uint64_t* __restrict__
 
 template <int LOGN>
 void launch_ntt_limbs_n(const Dev& d, uint64_t* data, int64_t batch, int nl, const PrimeMap& pm, bool inverse) {
-    // N <= 2^14: the fused configuration (16 residues x 512 threads, 2 CTAs/SM) is also the
-    // fastest plain transform (2^14: 5.78 vs 5.58 M limb/s fwd; 2^13 inverse 12.3 vs 10.8)
-    using C = typename std::conditional<(LOGN <= 14), CfgFused<LOGN>, CfgPlain<LOGN>>::type;
+    using C = CfgNttLimbs<LOGN>;   // (ntt_core.cuh: measured per degree)
     const dim3 grid((unsigned)batch, nl);
     if (inverse) launch_cfg<C>(d, "k_ntt_limbs", k_ntt_limbs<C, true>, grid, data, nl, pm, *d.mt);
     else launch_cfg<C>(d, "k_ntt_limbs", k_ntt_limbs<C, false>, grid, data, nl, pm, *d.mt);
