@@ -544,9 +544,15 @@ k_relin_mac(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int 
 // both components, with companions) are staged once in shared memory and reused for every
 // ciphertext, so each key residue is fetched from L2 once per MAC2_CTS ciphertexts, and
 // a ciphertext's l+1 digit loads are all issued before its MACs.
-constexpr int MAC2_THREADS = 128;
+#ifndef EDL_MAC2_THREADS
+#define EDL_MAC2_THREADS 128
+#endif
+#ifndef EDL_MAC2_CTS
+#define EDL_MAC2_CTS 8   // measured 0.745 vs 0.773 ms (16), 0.757 (4)
+#endif
+constexpr int MAC2_THREADS = EDL_MAC2_THREADS;
 constexpr int MAC2_MAXD = 8;
-constexpr int MAC2_CTS = 16;
+constexpr int MAC2_CTS = EDL_MAC2_CTS;
 
 // FP selects the arithmetic path at compile time (the launch groups targets by path); ND is
 // the exact digit count l+1 (loops fully unrolled, no per-digit branches); CPI ciphertexts
