@@ -6,9 +6,8 @@
 //
 // The length-N complex DFT (N up to 2^16 doubles: more than one CTA's shared memory)
 // runs as a four-step transform N = 128 x (N/128): 128-point DFTs down the columns, the
-// exp(+-2 pi i k1 c / N) twist, then (N/128)-point DFTs along the rows, each output a
-// direct sum over a shared-memory copy of its column/row with an exact root table (fp64;
-// sincospi).  The encoder's +-1 contract with the oracle (reading Z1) is checked in the
+// exp(+-2 pi i k1 c / N) twist, then (N/128)-point DFTs along the rows, each a radix-2
+// FFT on a shared-memory copy of its column/row with a sincospi root table (fp64).  The encoder's +-1 contract with the oracle (reading Z1) is checked in the
 // GPU tests.  Decrypted coefficients are lifted from residues to signed 64-bit integers
 // with the same exact-mod-2^64 CRT as the host path.
 #include "kernels.cuh"
@@ -48,11 +47,38 @@ __global__ void k_encode_prep(const double* __restrict__ z, int64_t n_vec, int64
     }
 }
 
+// In-place radix-2 DFT of length L = 2^logL held in shared memory, X[k] = sum_r x[r] w^{rk},
+// w = exp(sign 2 pi i / L): bit-reversal permutation, then logL Cooley-Tukey stages with the
+// roots root[k] = w^k (k < L/2) from a shared table.  All threads of the block take part.
+__device__ void fft_smem(double2* a, const double2* root, int L, int logL) {
+    for (int i = threadIdx.x; i < L; i += blockDim.x) {
+        const int j = (int)(__brev((uint32_t)i) >> (32 - logL));
+        if (i < j) {
+            const double2 t = a[i];
+            a[i] = a[j];
+            a[j] = t;
+        }
+    }
+    __syncthreads();
+    for (int s = 0; s < logL; s++) {
+        const int half = 1 << s;
+        for (int t = threadIdx.x; t < L / 2; t += blockDim.x) {
+            const int k = t & (half - 1);
+            const int i0 = ((t >> s) << (s + 1)) + k;
+            const double2 w = root[k << (logL - 1 - s)];
+            const double2 u = a[i0], v = cmul(a[i0 + half], w);
+            a[i0] = make_double2(u.x + v.x, u.y + v.y);
+            a[i0 + half] = make_double2(u.x - v.x, u.y - v.y);
+        }
+        __syncthreads();
+    }
+}
+
 // stage 1: for vector b, column c < n2: X1[k1][c] = twist^(k1 c) sum_r x[r n2 + c] w128^(r k1)
 __global__ void __launch_bounds__(FFT_N1) k_fft_cols(const double2* __restrict__ in, double2* __restrict__ out, int logn,
                                                      int sign) {
     __shared__ double2 col[FFT_N1];
-    __shared__ double2 root[FFT_N1];
+    __shared__ double2 root[FFT_N1 / 2];
     const int64_t n = 1LL << logn;
     const int n2 = (int)(n / FFT_N1);
     const int c = blockIdx.x;
@@ -60,44 +86,37 @@ __global__ void __launch_bounds__(FFT_N1) k_fft_cols(const double2* __restrict__
     const int k1 = threadIdx.x;
     col[k1] = in[b * n + (int64_t)k1 * n2 + c];
     double s, co;
-    sincospi(2.0 * (double)k1 / FFT_N1, &s, &co);
-    root[k1] = make_double2(co, sign * s);
-    __syncthreads();
-    double2 acc = make_double2(0.0, 0.0);
-    for (int r = 0; r < FFT_N1; r++) {
-        const double2 p = cmul(col[r], root[(r * k1) & (FFT_N1 - 1)]);
-        acc.x += p.x;
-        acc.y += p.y;
+    if (k1 < FFT_N1 / 2) {
+        sincospi(2.0 * (double)k1 / FFT_N1, &s, &co);
+        root[k1] = make_double2(co, sign * s);
     }
+    __syncthreads();
+    fft_smem(col, root, FFT_N1, 7);
     sincospi(2.0 * (double)(((int64_t)k1 * c) % n) / (double)n, &s, &co);
-    out[b * n + (int64_t)k1 * n2 + c] = cmul(acc, make_double2(co, sign * s));
+    out[b * n + (int64_t)k1 * n2 + c] = cmul(col[k1], make_double2(co, sign * s));
 }
 
 // stage 2: for vector b, row k1: X[k1 + 128 k2] = sum_c X1[k1][c] w_{n2}^(c k2)
 __global__ void k_fft_rows(const double2* __restrict__ in, double2* __restrict__ out, int logn, int sign) {
-    extern __shared__ double2 sh[];   // row [n2] then roots [n2]
+    extern __shared__ double2 sh[];   // row [n2] then roots [n2 / 2]
     const int64_t n = 1LL << logn;
     const int n2 = (int)(n / FFT_N1);
+    const int log2n2 = logn - 7;
     double2* row = sh;
     double2* root = sh + n2;
     const int k1 = blockIdx.x;
     const int64_t b = blockIdx.y;
     for (int c = threadIdx.x; c < n2; c += blockDim.x) {
         row[c] = in[b * n + (int64_t)k1 * n2 + c];
-        double s, co;
-        sincospi(2.0 * (double)c / (double)n2, &s, &co);
-        root[c] = make_double2(co, sign * s);
+        if (c < n2 / 2) {
+            double s, co;
+            sincospi(2.0 * (double)c / (double)n2, &s, &co);
+            root[c] = make_double2(co, sign * s);
+        }
     }
     __syncthreads();
-    for (int k2 = threadIdx.x; k2 < n2; k2 += blockDim.x) {
-        double2 acc = make_double2(0.0, 0.0);
-        for (int c = 0; c < n2; c++) {
-            const double2 p = cmul(row[c], root[(int)(((int64_t)c * k2) & (n2 - 1))]);
-            acc.x += p.x;
-            acc.y += p.y;
-        }
-        out[b * n + k1 + (int64_t)FFT_N1 * k2] = acc;
-    }
+    fft_smem(row, root, n2, log2n2);
+    for (int k2 = threadIdx.x; k2 < n2; k2 += blockDim.x) out[b * n + k1 + (int64_t)FFT_N1 * k2] = row[k2];
 }
 
 __global__ void k_encode_finish(const double2* __restrict__ w, int64_t n_vec, int logn, double scale,
@@ -157,7 +176,7 @@ void launch_dft(const Dev& d, double2* buf, double2* tmp, int64_t n_vec, int sig
     const int64_t n = 1LL << d.logn;
     const int n2 = (int)(n / FFT_N1);
     EDL_LAUNCH(d, "k_fft_cols", k_fft_cols<<<dim3(n2, (unsigned)n_vec), FFT_N1, 0, d.st>>>(buf, tmp, d.logn, sign));
-    EDL_LAUNCH(d, "k_fft_rows", k_fft_rows<<<dim3(FFT_N1, (unsigned)n_vec), 128, 2 * n2 * sizeof(double2), d.st>>>(
+    EDL_LAUNCH(d, "k_fft_rows", k_fft_rows<<<dim3(FFT_N1, (unsigned)n_vec), 128, (n2 + n2 / 2) * sizeof(double2), d.st>>>(
                                     tmp, buf, d.logn, sign));
 }
 

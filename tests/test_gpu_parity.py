@@ -490,11 +490,15 @@ def test_masked_cc_bit_exact_and_float64(f1pair):
 
 
 # ---------------------------------------------------------------- NEXT f3: device encode / decode
-@pytest.mark.parametrize("logn", [13, 14])
+@pytest.mark.parametrize("logn", [10, 11, 13, 14, 15, 16])
 def test_device_encode_contract(edl, logn):
-    """Device canonical embedding vs the oracle encoder: the +-1 contract (reading Z1)."""
+    """Device canonical embedding vs the oracle encoder: the +-1 contract (reading Z1), at
+    every row length of the four-step FFT (N/128 = 8 .. 512)."""
     from oracle import encoding
-    g = edl.Context(edl.params_from_depth(2 if logn == 13 else 4))
+    if logn in (13, 14):
+        g = edl.Context(edl.params_from_depth(2 if logn == 13 else 4))
+    else:
+        g = edl.Context(edl.params_from_bits(logn, [60, 40, 60]))
     z = random_slots(3, 1 << (logn - 1), seed=logn, lo=-1, hi=1)
     got = g.encode_device(z, 2.0 ** 40).cpu().numpy()
     want = np.stack([encoding.encode(v, 1 << logn, 2.0 ** 40) for v in z])
