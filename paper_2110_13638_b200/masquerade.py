@@ -127,12 +127,119 @@ def masked_dense(ctx: Context, feats: CtArray, F: int, anchors: Sequence[int], W
     return CtArray(t, nimg * O, outs[0].level, outs[0].scale, outs[0].key_id)
 
 
+def packed_block(span: int) -> int:
+    """Smallest power of two >= span: the slot block one class occupies in the packed dense."""
+    blk = 1
+    while blk < span:
+        blk *= 2
+    return blk
+
+
+def packed_rotations(n_slots: int, span: int) -> List[int]:
+    """Rotations of the packed dense: replication of block 0 into every block (right shifts
+    by blk, 2 blk, ..., as left rotations n_slots - s) and the in-block sums 1 .. blk/2."""
+    blk = packed_block(span)
+    reps, s = [], blk
+    while s < n_slots:
+        reps.append(n_slots - s)
+        s *= 2
+    return reps + sum_rotations(blk)
+
+
+def masked_dense_packed(ctx: Context, feats: CtArray, F: int, anchors: Sequence[int], Wt: np.ndarray, b,
+                        span: int, fill: Optional[Sequence[float]] = None) -> CtArray:
+    """Dense layer with the classes packed into slot blocks (fewer rotations than
+    `masked_dense`'s 10 per class): every feature ciphertext is replicated into the
+    n_slots / blk blocks of blk = 2^ceil(log2 span) slots (log2(n_slots / blk) rotations,
+    block 0 holds the features and zeros above span), one plaintext product per feature
+    puts class o's weights in block o (o < n_slots / blk; further classes in a second
+    product ciphertext over the same replicas), and log2(blk) rotations sum every block
+    into its first slot.  Returns [count * G] ciphertexts, G = ceil(O / (n_slots / blk)):
+    logit o of image i in slot (o % nb) * blk of ciphertext i * G + o // nb; bias added
+    per block through a trivially encrypted plaintext vector.
+    Feature f holds the constant fill[f] in every slot outside the masked CC's data region
+    (C1: sigma_a(kb_f), the activation of the CC bias that pt_add put in every slot); it is
+    subtracted from every slot before the replication (no level used) so the other blocks'
+    copies add exact zeros at the anchors, and sum_f fill[f] * sum_w W[o][f*A + w] is added
+    back through the bias.
+    C1: 5 * 3 replication + 2 * 10 block-sum rotations = 35 per image instead of 100."""
+    O = Wt.shape[0]
+    nimg = feats.count // F
+    l = feats.level
+    n_slots = ctx.n // 2
+    blk = packed_block(span)
+    nb = n_slots // blk
+    G = (O + nb - 1) // nb
+    ql = float(ctx.params.qs[l])
+    words = 2 * (l + 1) * ctx.n
+    fv = feats.tensor.view(nimg, F, words)
+    torch = ctx.torch
+    reps = []
+    for f in range(F):
+        r = CtArray(fv[:, f].contiguous().view(-1), nimg, l, feats.scale, feats.key_id)
+        if fill is not None and fill[f] != 0.0:
+            r = ctx.pt_add(r, [-float(fill[f])] * nimg)
+        s = blk
+        while s < n_slots:
+            r = ctx.add(r, ctx.rotate(r, n_slots - s))
+            s *= 2
+        reps.append(r)
+    outs = []
+    for g in range(G):
+        acc = None
+        for f in range(F):
+            z = np.zeros(n_slots)
+            for k in range(nb):
+                o = g * nb + k
+                if o < O:
+                    z[k * blk + np.asarray(anchors)] = Wt[o, f * len(anchors):(f + 1) * len(anchors)]
+            pt = ctx.encode_pt(z[None, :], ql, l)
+            y = ctx.pt_vec_mul(reps[f], pt, 1, l, ql)
+            acc = y if acc is None else ctx.add(acc, y)
+        acc = ctx.rescale(acc)
+        for r in sum_rotations(blk):
+            acc = ctx.add(acc, ctx.rotate(acc, r))
+        if b is not None or fill is not None:
+            zb = np.zeros(n_slots)
+            for k in range(nb):
+                o = g * nb + k
+                if o < O:
+                    zb[k * blk] = 0.0 if b is None else float(b[o])
+                    if fill is not None:
+                        A = len(anchors)
+                        zb[k * blk] += sum(float(fill[f]) * float(np.sum(Wt[o, f * A:(f + 1) * A])) for f in range(F))
+            ptb = ctx.encode_pt(zb[None, :], acc.scale, acc.level).view(acc.level + 1, ctx.n)
+            triv = torch.zeros((acc.count, 2, acc.level + 1, ctx.n), dtype=torch.int64, device=acc.tensor.device)
+            triv[:, 0] = ptb
+            acc = ctx.add(acc, CtArray(triv.view(-1), acc.count, acc.level, acc.scale, acc.key_id))
+        outs.append(acc)
+    t = torch.stack([x.tensor.view(nimg, -1) for x in outs], dim=1).reshape(-1)
+    return CtArray(t, nimg * G, outs[0].level, outs[0].scale, outs[0].key_id)
+
+
+def packed_logits(ctx: Context, out: CtArray, O: int, span: int) -> np.ndarray:
+    """Decrypt `masked_dense_packed` outputs into [images][O] logits."""
+    n_slots = ctx.n // 2
+    blk = packed_block(span)
+    nb = n_slots // blk
+    G = (O + nb - 1) // nb
+    z = ctx.decrypt(out, n_slots).reshape(out.count // G, G, n_slots)
+    return np.stack([z[:, o // nb, (o % nb) * blk] for o in range(O)], axis=1)
+
+
 def masked_cnn(ctx: Context, x: CtArray, K, kb, Wt, b, H: int = 28, W: int = 28, stride: int = 4,
-               coeffs=(0.5, 0.197, 0.0, -0.004), encode: Optional[Callable] = None) -> CtArray:
+               coeffs=(0.5, 0.197, 0.0, -0.004), encode: Optional[Callable] = None,
+               packed: bool = False) -> CtArray:
     """C1's architecture in the paper's layout: masked CC -> sigma_a -> masked dense.
     x: one image per ciphertext (level >= 4).  Returns [count*10] ciphertexts, logit o of
-    image i in slot 0 of ciphertext i*10 + o."""
+    image i in slot 0 of ciphertext i*10 + o; with packed=True the dense is
+    `masked_dense_packed` (read the logits with `packed_logits`)."""
     F, kh, kw = np.asarray(K).shape
     cc = masked_cc(ctx, x, K, H, W, stride, kb, encode=encode)
     act = ctx.poly_activation(cc, coeffs)
+    if packed:
+        kbv = np.zeros(F) if kb is None else np.asarray(kb, dtype=np.float64)
+        fill = [float(sum(c * v ** k for k, c in enumerate(coeffs))) for v in kbv]   # sigma(kb_f)
+        return masked_dense_packed(ctx, act, F, anchor_slots(H, W, kh, kw, stride), np.asarray(Wt), b, H * W,
+                                   fill=fill)
     return masked_dense(ctx, act, F, anchor_slots(H, W, kh, kw, stride), np.asarray(Wt), b, H * W, encode=encode)

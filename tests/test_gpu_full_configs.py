@@ -126,3 +126,9 @@ def test_f1_masked_cnn_vs_float64(gpu):
     got = ctx.decrypt(out, 1)[:, 0].reshape(3, 10)
     ref = onet.c1_float64(imgs, K, kb, W, b)
     assert np.max(np.abs(got - ref)) < 1e-3
+    # the class-packed dense (35 instead of 100 dense rotations per image), same logits
+    ctx.galois_keygen(8, masquerade.packed_rotations(ctx.n // 2, 784))
+    outp = masquerade.masked_cnn(ctx, x, K, kb, W, b, packed=True)
+    assert outp.count == 6 and outp.level == 0
+    gotp = masquerade.packed_logits(ctx, outp, 10, 784)
+    assert np.max(np.abs(gotp - ref)) < 1e-3
