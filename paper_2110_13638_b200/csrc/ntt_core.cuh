@@ -447,11 +447,18 @@ __device__ __forceinline__ void ntt_inv_impl(uint64_t* sm, const ModInfo& m, Loa
         if constexpr (FP) return f64_to_canon(f64_of(v), qd);
         else return csub(v, q);
     };
+    {
+        // every load of the thread first, then the shared-memory stores: interleaved, a store
+        // (generic pointer: possible alias of the load's source) would pin each next load
+        // behind the previous one's full latency
+        uint64_t t[C::E];
 #pragma unroll
-    for (int r = 0; r < C::E; r++) {
-        const uint64_t v = load(C::idx(r));
-        if constexpr (FP) sm[spad(tid + r * C::T)] = f64_from_u(v);
-        else sm[spad(tid + r * C::T)] = v;
+        for (int r = 0; r < C::E; r++) t[r] = load(C::idx(r));
+#pragma unroll
+        for (int r = 0; r < C::E; r++) {
+            if constexpr (FP) sm[spad(tid + r * C::T)] = f64_from_u(t[r]);
+            else sm[spad(tid + r * C::T)] = t[r];
+        }
     }
     __syncthreads();
     inv_middle<C, C::NPASS - 1, FP>(sm, m, two_q);
