@@ -361,6 +361,14 @@ def test_errors_and_empty(edl, c0pair):
     E.key_id, E.scale = o.key_id, 2.0 ** 40
     assert g.add(E, E).count == 0
     assert g.rescale(E).count == 0
+    # empty batches through every batched entry point of the hot path and the wire formats
+    assert g.mul_relin(E, E).count == 0
+    assert g.poly_activation(E, (0.5, 0.197, 0.0, -0.004)).count == 0
+    assert g.pt_mul(E, np.zeros(0), 2.0 ** 20).count == 0
+    assert g.packed_bytes(0, 2) == 0 and g.seeded_bytes(0, 2) == 0
+    assert g.encrypt_poly_sk(np.zeros((0, g.n), dtype=np.int64), scale=2.0 ** 40, enc_seed=1).count == 0
+    wire = g.torch.empty(0, dtype=g.torch.int64, device="cuda")
+    assert g.unpack_seeded(wire, 0, 2, 2.0 ** 40, o.key_id, enc_seed=1).count == 0
 
 
 @pytest.mark.parametrize("which", ["linear", "relu_a"])
