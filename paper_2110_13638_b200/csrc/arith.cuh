@@ -24,7 +24,7 @@ struct ModInfo {
     uint64_t w1ninv, w1ninv_s;  // psi^-brv(1) * N^-1 (last INTT stage), Shoup companion
     uint64_t one_s;             // floor(2^64 / q): Shoup companion of 1 (64-bit reduction)
     uint64_t fp;                // 1: q < 2^46, every constant companion is RD(w/q) as binary64
-                                //    (tw_mul<true>) and variable products use mulmod_fp;
+                                //    (tw_mul_fp / mulc) and variable products use mulmod_fp;
                                 // 2: additionally q < 2^44, NTT butterflies on the FP64 pipe
                                 //    (twiddle tables hold binary64 {w, RD(w/q)})
     double qinv_d;              // RN(1/q) (mulmod_fp)
@@ -103,23 +103,6 @@ __device__ __forceinline__ uint64_t tw_mul_fp(uint64_t y, uint64_t w, uint64_t w
     return y * w - qt * q;
 }
 
-// FP64-quotient product with the companion made on the fly from w alone:
-// wq = RD(w_d RD(1/q)) <= w/q and w/q - wq < 2^-52, so y (w/q - wq) < 1 for y < 2^52 and
-// floor(y wq) is again qt or qt - 1 (2 more FP64 instructions, half the twiddle bytes).
-__device__ __forceinline__ uint64_t tw_mul_fp_w(uint64_t y, uint64_t w, double qinv_rd, uint64_t q) {
-    const double magic = 4503599627370496.0;   // 2^52
-    const double wq = __dmul_rd(__hiloint2double(0x43300000 | (uint32_t)(w >> 32), (uint32_t)w) - magic, qinv_rd);
-    const double yd = __hiloint2double(0x43300000 | (uint32_t)(y >> 32), (uint32_t)y) - magic;
-    const double t = __fma_rd(yd, wq, magic);
-    const uint64_t qt = (uint64_t)__double_as_longlong(t) & 0xFFFFFFFFFFFFFull;
-    return y * w - qt * q;
-}
-
-template <bool FP>
-__device__ __forceinline__ uint64_t tw_mul(uint64_t y, uint64_t w, uint64_t wc, uint64_t q) {
-    if constexpr (FP) return tw_mul_fp(y, w, wc, q);
-    else return shoup_lazy2(y, w, wc, q);
-}
 
 __device__ __forceinline__ uint64_t shoup(uint64_t y, uint64_t w, uint64_t ws, uint64_t q) {
     return csub(shoup_lazy2(y, w, ws, q), q);
