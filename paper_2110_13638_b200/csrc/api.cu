@@ -203,12 +203,14 @@ const T* upload(edl_ctx* c, const std::vector<T>& v) {
 // per-ciphertext array (inputs, scratch, output), so they are independent; the main stream
 // joins the side stream before returning.  Profiling keeps one stream.
 void relin_split(edl_ctx* c, const Dev& d, const uint64_t* a, const uint64_t* b, int64_t cnt, int l, bool rescale,
-                 const uint64_t* rlk, const uint64_t* rlk_s, uint64_t* scr, uint64_t* out) {
+                 const uint64_t* rlk, const uint64_t* rlk_s, uint64_t* scr, uint64_t* out,
+                 const uint64_t* add_w = nullptr, const uint64_t* add_k = nullptr) {
     const int64_t c0 = cnt / 2;
     if (c->prof.on || c0 < 8) {
-        launch_relin(d, a, b, cnt, l, rescale, rlk, rlk_s, scr, out);
+        launch_relin(d, a, b, cnt, l, rescale, rlk, rlk_s, scr, out, add_w, add_k);
         return;
     }
+    const int nlo = rescale ? l : l + 1;
     const size_t in_w = (size_t)2 * (l + 1) << c->logn, out_w = (size_t)2 * (rescale ? l : l + 1) << c->logn;
     Dev d2 = d;
     d2.st = c->st2;
@@ -216,9 +218,10 @@ void relin_split(edl_ctx* c, const Dev& d, const uint64_t* a, const uint64_t* b,
     // transforms with the key-product pass, is slower than the halves side by side)
     cudaEventRecord(c->fork, c->st);
     cudaStreamWaitEvent(c->st2, c->fork, 0);
-    launch_relin(d, a, b, c0, l, rescale, rlk, rlk_s, scr, out);
+    launch_relin(d, a, b, c0, l, rescale, rlk, rlk_s, scr, out, add_w, add_k);
     launch_relin(d2, a + c0 * in_w, b ? b + c0 * in_w : nullptr, cnt - c0, l, rescale, rlk, rlk_s,
-                 scr + relin_scratch_words(c0, l, c->logn), out + c0 * out_w);
+                 scr + relin_scratch_words(c0, l, c->logn), out + c0 * out_w, add_w ? add_w + c0 * out_w : nullptr,
+                 add_k ? add_k + c0 * nlo : nullptr);
     cudaEventRecord(c->join, c->st2);
     cudaStreamWaitEvent(c->st, c->join, 0);
 }
@@ -1151,8 +1154,9 @@ edl_status edl_poly_activation(edl_ctx* c, const edl_cts* x, const double* coeff
         if (side) cudaEventRecord(c->join, c->st2);
         relin_split(c, d, x->data, x->data, cnt, l, true, c->d_rlk, c->d_rlk_s, rsc, y2);    // 1.
         if (side) cudaStreamWaitEvent(c->st, c->join, 0);
-        relin_split(c, d, u, y2, cnt, l - 1, true, c->d_rlk, c->d_rlk_s, rsc, v);               // 3.
-        launch_add_add_const(d, v, w, l - 2, cnt, l - 2, k0, out->data);                       // 5.
+        // 3. + 5.: out = Rs(Relin(u y2)) + w + c0, the assembly fused into the last kernel
+        relin_split(c, d, u, y2, cnt, l - 1, true, c->d_rlk, c->d_rlk_s, rsc, out->data, w, k0);
+        (void)v;
     }
     set_meta(out, cnt, l - 2, S3, x->key_id);
     return cuda_check(c, "poly_activation");

@@ -129,7 +129,7 @@ void launch_rescale_ntt_n(const Dev& d, const uint64_t* in, int64_t cnt, int l, 
 template <int LOGN>
 void launch_relin_n(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t cnt, int l, bool rescale,
                     const uint64_t* rlk, const uint64_t* rlk_c, uint64_t* acoef, uint64_t* xh, uint64_t* acc, uint64_t* r,
-                    uint64_t* s, uint64_t* out);
+                    uint64_t* s, uint64_t* out, const uint64_t* add_w, const uint64_t* add_k);
 // key inner product of the relinearisation (pointwise.cu): acc [cnt][2][l+2][N] from the
 // raised digits xh [cnt][l+1][l+2][N], the tensor's d2 (a1 b1) and rlk [L+1][2][L+2][N]
 void launch_relin_mac(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t cnt, int l, const uint64_t* xh,
@@ -159,8 +159,11 @@ void launch_rescale_intt(const Dev& d, const uint64_t* in, int64_t cnt, int l, c
 void launch_rescale_ntt(const Dev& d, const uint64_t* in, int64_t cnt, int l, const ulonglong2* w,
                         const uint64_t* r, const uint64_t* bias, uint64_t* out, int lo = -1);
 // relinearisation of the tensor a (x) b at level l (+ optional rescale by q_l)
+// add_w / add_k (rescale only, optional): out += add_w (a ciphertext array at the output
+// level) + add_k[c][i] on polynomial 0, fused into the last kernel's epilogue
 void launch_relin(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t cnt, int l, bool rescale,
-                  const uint64_t* rlk, const uint64_t* rlk_s, uint64_t* scratch, uint64_t* out);
+                  const uint64_t* rlk, const uint64_t* rlk_s, uint64_t* scratch, uint64_t* out,
+                  const uint64_t* add_w = nullptr, const uint64_t* add_k = nullptr);
 size_t relin_scratch_words(int64_t cnt, int l, int logn);
 
 // ---- pointwise family (pointwise.cu) ----

@@ -28,13 +28,14 @@ size_t relin_scratch_words(int64_t cnt, int l, int logn) {
 }
 
 void launch_relin(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t cnt, int l, bool rescale,
-                  const uint64_t* rlk, const uint64_t* rlk_s, uint64_t* scratch, uint64_t* out) {
+                  const uint64_t* rlk, const uint64_t* rlk_s, uint64_t* scratch, uint64_t* out, const uint64_t* add_w,
+                  const uint64_t* add_k) {
     uint64_t* acoef = scratch;
     uint64_t* xh = acoef + ((size_t)cnt * (l + 1) << d.logn);
     uint64_t* acc = xh + ((size_t)cnt * (l + 1) * (l + 2) << d.logn);
     uint64_t* r = acc + ((size_t)cnt * 2 * (l + 2) << d.logn);
     uint64_t* s = r + ((size_t)cnt * 2 << d.logn);
-    EDL_DISPATCH_LOGN(d.logn, launch_relin_n<LOGN>(d, a, b, cnt, l, rescale, rlk, rlk_s, acoef, xh, acc, r, s, out));
+    EDL_DISPATCH_LOGN(d.logn, launch_relin_n<LOGN>(d, a, b, cnt, l, rescale, rlk, rlk_s, acoef, xh, acc, r, s, out, add_w, add_k));
 }
 
 }  // namespace edl

@@ -240,6 +240,7 @@ __global__ void __launch_bounds__(C::T, C::MINB)
 k_relin_moddown_ntt(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l,
                     const uint64_t* __restrict__ acc, const uint64_t* __restrict__ r,
                     const uint64_t* __restrict__ s, int L, int rescale, uint64_t* __restrict__ out,
+                    const uint64_t* __restrict__ add_w, const uint64_t* __restrict__ add_k,
                     const __grid_constant__ ModTable mods, const ChainConsts* __restrict__ cc) {
     extern __shared__ uint64_t sm[];
     const int i = blockIdx.z, cp = blockIdx.y;
@@ -269,20 +270,32 @@ k_relin_moddown_ntt(const uint64_t* __restrict__ a, const uint64_t* __restrict__
             return addmod(u, center_mod(ss[idx], ql, qlmod, m), m.q);
         };
         auto pre = [&](int idx) { return vi[idx]; };
-        struct Store {   // (v - x) q_l^-1; F64 limbs: on the unreduced binary64 transform output
+        // (v - x) q_l^-1 (+ w + k: a fused ciphertext + constant addend, e.g. sigma's output
+        // assembly); F64 limbs: on the unreduced binary64 transform output
+        const uint64_t* wl = add_w ? add_w + limb_off(c, cp, i, nlo, C::LOGN) : nullptr;
+        const uint64_t kk = (add_k && cp == 0) ? add_k[c * nlo + i] : 0;
+        struct Store {
             uint64_t* dst;
+            const uint64_t* wl;
+            uint64_t kk;
             const ModInfo& m;
             ulonglong2 qlinv;
             __device__ __forceinline__ void operator()(int idx, uint64_t x, uint64_t v) const {
-                dst[idx] = mulc(submod(v, x, m.q), qlinv, m);
+                uint64_t y = mulc(submod(v, x, m.q), qlinv, m);
+                if (wl) y = addmod(addmod(y, wl[idx], m.q), kk, m.q);
+                dst[idx] = y;
             }
             __device__ __forceinline__ void f64(int idx, double x, uint64_t v) const {
                 const double qd = u52_to_double(m.q);
-                const double t = f64_mulc(__dsub_rn(u52_to_double(v), x), u52_to_double(qlinv.x), f64_of(qlinv.y), qd);
+                double t = f64_mulc(__dsub_rn(u52_to_double(v), x), u52_to_double(qlinv.x), f64_of(qlinv.y), qd);
+                if (wl) {
+                    t = __dadd_rn(t, u52_to_double(wl[idx]) + u52_to_double(kk));   // < 2.7 q: exact
+                    t = f64_reduce(t, qd, m.qinv_d);
+                }
                 dst[idx] = f64_to_canon(t, qd);
             }
         };
-        ntt_fwd<C>(sm, m, ld, pre, Store{dst, m, qlinv});
+        ntt_fwd<C>(sm, m, ld, pre, Store{dst, wl, kk, m, qlinv});
     } else {
         // out = d + (acc - NTT([r])) P^-1 = v - NTT([r] P^-1)  (Z_q-linear, exact)
         auto ld = [&](int idx) { return mulc(center_mod(rr[idx], P, pmod, m), pinv, m); };
@@ -318,7 +331,7 @@ void launch_rescale_ntt_n(const Dev& d, const uint64_t* in, int64_t cnt, int l, 
 template <int LOGN>
 void launch_relin_n(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t cnt, int l, bool rescale,
                     const uint64_t* rlk, const uint64_t* rlk_c, uint64_t* acoef, uint64_t* xh, uint64_t* acc, uint64_t* r,
-                    uint64_t* s, uint64_t* out) {
+                    uint64_t* s, uint64_t* out, const uint64_t* add_w, const uint64_t* add_k) {
     using C = CfgFused<LOGN>;
     // the modulus raise is a plain transform but runs fastest in the fused configuration
     // (2-CTA clusters of 512 threads, 2 CTAs/SM at 2^14): 1.22 vs 1.32 ms per C1 step
@@ -331,7 +344,7 @@ void launch_relin_n(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t 
     launch_cfg<C>(d, "k_relin_moddown_intt", k_relin_moddown_intt<C>, dim3((unsigned)cnt, 2), a, b, l, (const uint64_t*)acc,
                   d.L, rs, r, s, *d.mt, d.cc);
     launch_cfg<C>(d, "k_relin_moddown_ntt", k_relin_moddown_ntt<C>, dim3((unsigned)cnt, 2, rescale ? l : l + 1), a, b, l,
-                  (const uint64_t*)acc, (const uint64_t*)r, (const uint64_t*)s, d.L, rs, out, *d.mt, d.cc);
+                  (const uint64_t*)acc, (const uint64_t*)r, (const uint64_t*)s, d.L, rs, out, add_w, add_k, *d.mt, d.cc);
 }
 
 #define EDL_INSTANTIATE_NTT(LOGN)                                                                                   \
@@ -342,6 +355,6 @@ void launch_relin_n(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t 
                                              const uint64_t*, const uint64_t*, uint64_t*, int);                     \
     template void launch_relin_n<LOGN>(const Dev&, const uint64_t*, const uint64_t*, int64_t, int, bool,            \
                                        const uint64_t*, const uint64_t*, uint64_t*, uint64_t*, uint64_t*, uint64_t*, \
-                                       uint64_t*, uint64_t*);
+                                       uint64_t*, uint64_t*, const uint64_t*, const uint64_t*);
 
 }  // namespace edl
