@@ -205,12 +205,15 @@ k_cc_mac(const uint64_t* __restrict__ x, int l, int H, int W, int F, int kh, int
 // every input residue is read from HBM once.  Taps stream in batches of CC2_TB with the
 // next batch's loads issued before the current batch's MACs (memory-level parallelism
 // without a second CTA's registers).
-constexpr int CC2_THREADS = 256;
+#ifndef EDL_CC2_THREADS
+#define EDL_CC2_THREADS 128   // measured: 0.468 vs 0.483 ms (256 x 2 CTAs/SM)
+#endif
+constexpr int CC2_THREADS = EDL_CC2_THREADS;
 #ifndef EDL_CC2_TB
 #define EDL_CC2_TB 4
 #endif
 #ifndef EDL_CC2_MINB
-#define EDL_CC2_MINB 2
+#define EDL_CC2_MINB 4
 #endif
 constexpr int CC2_TB = EDL_CC2_TB;
 constexpr int CC2_MAXTAPS = 64;
