@@ -1123,15 +1123,14 @@ edl_status edl_poly_activation(edl_ctx* c, const edl_cts* x, const double* coeff
     const double Sw = (Sy * p1) / ql;
     if (!scales_match(S3, Sw)) return fail(c, EDL_ERR_SCALE, "poly_activation: scale drift");
     if (cnt > 0) {
-        const size_t wl = ct_words(c, cnt, l - 1), wv = ct_words(c, cnt, l - 2);
+        const size_t wl = ct_words(c, cnt, l - 1);
         const size_t rs = relin_scratch_words(cnt, l, c->logn);
-        uint64_t* base = scratch(c, 3 * wl + wv + 2 * (size_t)cnt * 2 * c->N + rs);
+        uint64_t* base = scratch(c, 3 * wl + 2 * (size_t)cnt * 2 * c->N + rs);
         if (!base) return fail(c, EDL_ERR_CUDA, "poly_activation: scratch");
         uint64_t* y2 = base;
         uint64_t* u = y2 + wl;
         uint64_t* w = u + wl;
-        uint64_t* v = w + wl;
-        uint64_t* r = v + wv;
+        uint64_t* r = w + wl;
         uint64_t* rsc = r + (size_t)cnt * 2 * c->N;
         std::vector<int64_t> i3(cnt, const_int(c3, ql)), i1(cnt, const_int(c1, p1)), i0(cnt, const_int(c0, S3));
         const ulonglong2* w3 = upload(c, shoup_consts(c, i3, l));
@@ -1156,7 +1155,6 @@ edl_status edl_poly_activation(edl_ctx* c, const edl_cts* x, const double* coeff
         if (side) cudaStreamWaitEvent(c->st, c->join, 0);
         // 3. + 5.: out = Rs(Relin(u y2)) + w + c0, the assembly fused into the last kernel
         relin_split(c, d, u, y2, cnt, l - 1, true, c->d_rlk, c->d_rlk_s, rsc, out->data, w, k0);
-        (void)v;
     }
     set_meta(out, cnt, l - 2, S3, x->key_id);
     return cuda_check(c, "poly_activation");
