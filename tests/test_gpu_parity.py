@@ -301,6 +301,26 @@ def test_layers_small_bit_exact(c1pair):
     assert np.max(np.abs(g.decrypt(out_g, B).T - want)) < 1e-3
 
 
+def test_mac_layers_extreme_residues(c1pair):
+    """CC and dense MACs on ciphertexts whose residues are all q_i - 1 (the largest operands
+    of every arithmetic path: FP64-pipe products and sums on the 40-bit limbs, 128-bit sums
+    on q0), GPU == oracle on every residue."""
+    g, o = c1pair
+    lvl = o.L
+    data = np.zeros((64, 2, lvl + 1, o.n), dtype=np.uint64)
+    for i in range(lvl + 1):
+        data[:, :, i, :] = np.uint64(o.q[i] - 1)
+    xo = ock.CtArray(data, lvl, 2.0 ** 40, o.key_id)
+    xg = _to_gpu(g, data, lvl, 2.0 ** 40, o.key_id)
+    rng = np.random.default_rng(21)
+    K, kb = rng.normal(0, 0.5, (3, 4, 4)), rng.normal(0, 0.1, 3)
+    cc_o = olay.cross_correlate(o, xo, 8, 8, K, 4, kb)
+    cc_g = g.cross_correlate(xg, 8, 8, K, 4, kb)
+    assert np.array_equal(cc_g.numpy(g.n), cc_o.data)
+    W, b = rng.normal(0, 0.5, (5, cc_o.count)), rng.normal(0, 0.1, 5)
+    assert np.array_equal(g.dense(cc_g, W, b).numpy(g.n), olay.dense(o, cc_o, W, b).data)
+
+
 def test_dense_ragged_and_deferred(c1pair):
     """Dense with K > 256 (accumulator folding), O > 16 (several output chunks), and the
     C4 deferred-rescale + uint64 combine + mod_reduce path (O15)."""
