@@ -319,6 +319,13 @@ def test_mac_layers_extreme_residues(c1pair):
     assert np.array_equal(cc_g.numpy(g.n), cc_o.data)
     W, b = rng.normal(0, 0.5, (5, cc_o.count)), rng.normal(0, 0.1, 5)
     assert np.array_equal(g.dense(cc_g, W, b).numpy(g.n), olay.dense(o, cc_o, W, b).data)
+    # key switch (+ fused rescale epilogues) on the same extreme operands
+    A = ock.CtArray(data[:2, :, :lvl].copy(), lvl - 1, 2.0 ** 40, o.key_id)
+    Ag = _to_gpu(g, A.data, lvl - 1, 2.0 ** 40, o.key_id)
+    m_o = o.mul_relin(A, A)
+    m_g = g.mul_relin(Ag, Ag)
+    assert np.array_equal(m_g.numpy(g.n), m_o.data)
+    assert np.array_equal(g.rescale(m_g).numpy(g.n), o.rescale(m_o).data)
 
 
 def test_dense_ragged_and_deferred(c1pair):
