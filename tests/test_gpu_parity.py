@@ -416,6 +416,22 @@ def test_linear_and_relu_activations_bit_exact(c1pair, which):
     assert np.max(np.abs(g.decrypt(got, 8192) - ref)) < 1e-3
 
 
+@pytest.mark.parametrize("coeffs", ["relu_a", "sigma_a"])
+def test_activations_two_stream_batches(c0pair, coeffs):
+    """Batches large enough for the two-stream schedules (key switches split in halves,
+    sigma's scalar rescales on the side stream, fused output assembly): 34 ciphertexts,
+    GPU == oracle on every residue (N=2^13, level 2)."""
+    from oracle import networks as onet
+    g, o = c0pair
+    lvl, cnt = 2, 34
+    A = ock.CtArray(_rand_ct(o, cnt, lvl, 71), lvl, 2.0 ** 40, o.key_id)
+    cf = onet.relu_a_coeffs(1.0) if coeffs == "relu_a" else onet.SIGMA_A
+    got = g.poly_activation(_to_gpu(g, A.data, lvl, A.scale, o.key_id), cf)
+    want = olay.poly_activation(o, A, cf)
+    assert got.level == want.level and got.scale == want.scale
+    assert np.array_equal(got.numpy(g.n), want.data)
+
+
 def _host_pack(data, qs, n):
     """Independent numpy packer of the wire format (edl.h): limb i's residues in bits(q_i)
     bits, little-endian, coefficient k at bit k*bits."""
