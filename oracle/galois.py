@@ -86,6 +86,48 @@ def rotate(ctx: Context, ct: CtArray, r: int, gkeys: Dict[int, np.ndarray]) -> C
     return CtArray(out, lvl, ct.scale, ct.key_id)
 
 
+def rotate_hoisted(ctx: Context, ct: CtArray, rs: Sequence[int], gkeys: Dict[int, np.ndarray]):
+    """Several rotations of the same ciphertexts sharing one modulus raise ("hoisting",
+    background, not in the paper): the digits of c1 are raised once,
+        a_j = INTT_{q_j}(c1_j),  x_{j,t} = NTT_t(a_j mod t)  for every target t (q_0..q_l, P),
+    and rotation r (g = 5^r) applies sigma_g to the raised digits instead of to c1:
+        acc_{c,t} = sum_j sigma_g(x_{j,t}) gk_j[c][t],  (ks_0, ks_1) = ModDown(acc),
+        out = (sigma_g(c0) + ks_0, ks_1).
+    sigma_g(x_{j,t}) is the raise of sigma_g(a_j) up to the lift of the negated
+    coefficients, so the result differs from `rotate` in its noise only; it decrypts to
+    the rotated slots.  Returns one CtArray per rotation."""
+    n, lvl = ctx.n, ct.level
+    idx = list(range(lvl + 1))
+    targets = idx + [ctx.L + 1]
+    outs = []
+    raised = []
+    for c in range(ct.count):
+        a = ctx.intt(ct.data[c, 1].copy(), idx)
+        raised.append(np.stack([np.stack([ctx.ntt(ring.reduce(a[j].copy(), ctx.moduli[t])[None, :], [t])[0]
+                                          for t in targets]) for j in idx]))   # [j][t][N]
+    for r in rs:
+        g = galois_element(r, n)
+        if g not in gkeys:
+            raise CkksError(f"no Galois key for rotation {r}")
+        key = gkeys[g]
+        out = np.empty_like(ct.data)
+        for c in range(ct.count):
+            acc = np.zeros((2, len(targets), n), dtype=np.uint64)
+            for ti, t in enumerate(targets):
+                mt = ctx.moduli[t]
+                for j in idx:
+                    xg = automorphism_ntt(ctx, raised[c][j][ti][None, :], g, [t])[0]
+                    for k in range(2):
+                        acc[k, ti] = ring.add(acc[k, ti], ring.mul(xg, key[j, k, t], mt), mt)
+            ks = ctx.mod_down(acc, lvl)
+            c0 = automorphism_ntt(ctx, ct.data[c, 0], g, idx)
+            for i in idx:
+                out[c, 0, i] = ring.add(c0[i], ks[0, i], ctx.q[i])
+                out[c, 1, i] = ks[1, i]
+        outs.append(CtArray(out, lvl, ct.scale, ct.key_id))
+    return outs
+
+
 def encode_plain(ctx: Context, z: np.ndarray, scale: float, level: int) -> np.ndarray:
     """Plaintext vector z -> NTT-domain residues [level+1][N] (O5 encode, then NTT)."""
     m = ctx.encode(z, scale)

@@ -54,6 +54,23 @@ def test_rotation_decrypts_to_rotated_slots(small, r):
     assert np.max(np.abs(ctx.decrypt(y, ctx.n // 2) - np.roll(z, -r, axis=1))) < 1e-5
 
 
+def test_hoisted_rotations_decrypt_to_rotated_slots(small):
+    """rotate_hoisted (one modulus raise shared by several rotations) decrypts to the rotated
+    slots, and its c0/c1 differ from the plain rotation's only within the key-switch noise."""
+    ctx = small
+    z = np.random.default_rng(4).uniform(-1, 1, (2, ctx.n // 2))
+    x = ctx.encrypt(z, 2)
+    rs = [1, -2, 5]
+    gk = {galois.galois_element(r, ctx.n): galois.galois_keygen(ctx, 7, galois.galois_element(r, ctx.n)) for r in rs}
+    ys = galois.rotate_hoisted(ctx, x, rs, gk)
+    for r, y in zip(rs, ys):
+        assert y.level == x.level and y.scale == x.scale
+        assert np.max(np.abs(ctx.decrypt(y, ctx.n // 2) - np.roll(z, -r, axis=1))) < 1e-5
+        y0 = galois.rotate(ctx, x, r, gk)
+        d = np.abs(ctx.decrypt(y, ctx.n // 2) - ctx.decrypt(y0, ctx.n // 2))
+        assert d.max() < 1e-6 and not np.array_equal(y.data, y0.data)
+
+
 def test_plain_vector_product(small):
     ctx = small
     rng = np.random.default_rng(3)
