@@ -209,6 +209,15 @@ edl_status edl_philox(edl_ctx* ctx, uint64_t seed, const uint32_t* ctr_host, int
  * edl_export_galois_key: copy the key of rotation `steps` to host ([L+1][2][L+2][N]). */
 edl_status edl_galois_keygen(edl_ctx* ctx, uint64_t seed, const int32_t* steps, int32_t n_steps);
 edl_status edl_rotate(edl_ctx* ctx, const edl_cts* in, int32_t steps, edl_cts* out);
+/* Hoisted rotations (background; oracle/galois.py rotate_hoisted): the digits of c1 are
+ * raised to the key-switch basis ONCE (d2 INTT + modulus raise) and every rotation
+ * steps[k] applies sigma_g to the raised digits and to c0, then runs the key products and
+ * the mod-down: the n_steps outputs cost one raise plus n_steps (permute + MAC + mod-down)
+ * instead of n_steps full key switches.  Results decrypt to the rotated slots and differ
+ * from edl_rotate's in the key-switch noise only (the lift of sigma_g-negated digit
+ * coefficients).  outs[k]: caller-allocated, edl_cts_bytes(count, level) each, must not
+ * alias `in`.  Errors: EDL_ERR_NOKEY (a missing Galois key), EDL_ERR_ARG.  Asynchronous. */
+edl_status edl_rotate_hoisted(edl_ctx* ctx, const edl_cts* in, const int32_t* steps, int32_t n_steps, edl_cts* outs);
 edl_status edl_encode_pt(edl_ctx* ctx, const double* slots, int64_t n_vec, int64_t n_slots, double scale, int32_t level,
                          uint64_t* pt_out);
 edl_status edl_encode_pt_poly(edl_ctx* ctx, const int64_t* poly, int64_t n_vec, int32_t level, uint64_t* pt_out);

@@ -971,6 +971,47 @@ edl_status edl_rotate(edl_ctx* c, const edl_cts* in, int32_t steps, edl_cts* out
     return cuda_check(c, "rotate");
 }
 
+edl_status edl_rotate_hoisted(edl_ctx* c, const edl_cts* in, const int32_t* steps, int32_t n_steps, edl_cts* outs) {
+    if (!c || n_steps < 0 || (n_steps > 0 && (!steps || !outs))) return EDL_ERR_ARG;
+    edl_status s = check_ct(c, in);
+    if (s != EDL_OK) return s;
+    const int l = in->level;
+    const int64_t cnt = in->count;
+    for (int k = 0; k < n_steps; k++) {
+        if (cnt > 0 && (!outs[k].data || outs[k].data == in->data))
+            return fail(c, EDL_ERR_ARG, "rotate_hoisted: null output or output aliases input");
+        const uint32_t g = galois_elt(c, steps[k]);
+        if (g != 1 && c->gkeys.find(g) == c->gkeys.end())
+            return fail(c, EDL_ERR_NOKEY, "rotate_hoisted: no Galois key for a rotation");
+    }
+    if (cnt > 0 && n_steps > 0) {
+        const size_t ctw = ct_words(c, cnt, l), rs = relin_scratch_words(cnt, l, c->logn);
+        const size_t xw = (size_t)cnt * (l + 1) * (l + 2) << c->logn;
+        uint64_t* base = scratch(c, ctw + rs + xw);
+        if (!base) return fail(c, EDL_ERR_CUDA, "rotate_hoisted: scratch");
+        uint64_t* ctg = base;
+        uint64_t* scr = base + ctw;
+        uint64_t* xh_base = scr + rs;
+        uint64_t* xh = relin_scratch_xh(scr, cnt, l, c->logn);
+        Dev d = c->dev();
+        launch_relin_raise(d, in->data, cnt, l, scr);   // c1's digits raised once
+        cudaMemcpyAsync(xh_base, xh, xw * 8, cudaMemcpyDeviceToDevice, c->st);
+        for (int k = 0; k < n_steps; k++) {
+            const uint32_t g = galois_elt(c, steps[k]);
+            if (g == 1) {
+                cudaMemcpyAsync(outs[k].data, in->data, ctw * 8, cudaMemcpyDeviceToDevice, c->st);
+                continue;
+            }
+            const auto& key = c->gkeys.find(g)->second;
+            launch_automorphism_rows(d, xh_base, (int64_t)cnt * (l + 1) * (l + 2), g, xh);   // sigma_g(raised digits)
+            launch_automorphism(d, in->data, cnt, l, g, ctg);                                // sigma_g(c0, c1)
+            launch_relin_finish(d, ctg, cnt, l, key.first, key.second, scr, outs[k].data);
+        }
+    }
+    for (int k = 0; k < n_steps; k++) set_meta(&outs[k], cnt, l, in->scale, in->key_id);
+    return cuda_check(c, "rotate_hoisted");
+}
+
 edl_status edl_encode_pt(edl_ctx* c, const double* slots, int64_t n_vec, int64_t n_slots, double scale, int32_t level,
                          uint64_t* pt_out) {
     if (!c || n_vec < 0 || (n_vec > 0 && (!slots || !pt_out))) return fail(c, EDL_ERR_ARG, "encode_pt: bad arguments");

@@ -165,6 +165,20 @@ void launch_relin(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t cn
                   const uint64_t* rlk, const uint64_t* rlk_s, uint64_t* scratch, uint64_t* out,
                   const uint64_t* add_w = nullptr, const uint64_t* add_k = nullptr);
 size_t relin_scratch_words(int64_t cnt, int l, int logn);
+template <int LOGN>
+void launch_relin_raise_n(const Dev& d, const uint64_t* a, int64_t cnt, int l, uint64_t* acoef, uint64_t* xh);
+template <int LOGN>
+void launch_relin_finish_n(const Dev& d, const uint64_t* a, int64_t cnt, int l, const uint64_t* rlk,
+                           const uint64_t* rlk_c, uint64_t* xh, uint64_t* acc, uint64_t* r, uint64_t* s, uint64_t* out);
+// hoisted rotations on the relin scratch layout: raise c1 of `a` once, finish per element
+// (the raised digits at the scratch's xh slot, already permuted by the caller)
+void launch_relin_raise(const Dev& d, const uint64_t* a, int64_t cnt, int l, uint64_t* scratch);
+void launch_relin_finish(const Dev& d, const uint64_t* a, int64_t cnt, int l, const uint64_t* rlk, const uint64_t* rlk_s,
+                         uint64_t* scratch, uint64_t* out);
+// pointer to the raised digits [cnt][l+1][l+2][N] inside a relin scratch block
+uint64_t* relin_scratch_xh(uint64_t* scratch, int64_t cnt, int l, int logn);
+// sigma_g on `rows` NTT-domain rows of N residues
+void launch_automorphism_rows(const Dev& d, const uint64_t* in, int64_t rows, uint32_t g, uint64_t* out);
 
 // ---- pointwise family (pointwise.cu) ----
 // out [cnt][2][lo+1] = a (level la) + b (level lb), lo <= min(la, lb)

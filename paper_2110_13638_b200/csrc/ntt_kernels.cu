@@ -38,4 +38,23 @@ void launch_relin(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t cn
     EDL_DISPATCH_LOGN(d.logn, launch_relin_n<LOGN>(d, a, b, cnt, l, rescale, rlk, rlk_s, acoef, xh, acc, r, s, out, add_w, add_k));
 }
 
+uint64_t* relin_scratch_xh(uint64_t* scratch, int64_t cnt, int l, int logn) {
+    return scratch + ((size_t)cnt * (l + 1) << logn);
+}
+
+void launch_relin_raise(const Dev& d, const uint64_t* a, int64_t cnt, int l, uint64_t* scratch) {
+    uint64_t* acoef = scratch;
+    uint64_t* xh = relin_scratch_xh(scratch, cnt, l, d.logn);
+    EDL_DISPATCH_LOGN(d.logn, launch_relin_raise_n<LOGN>(d, a, cnt, l, acoef, xh));
+}
+
+void launch_relin_finish(const Dev& d, const uint64_t* a, int64_t cnt, int l, const uint64_t* rlk, const uint64_t* rlk_s,
+                         uint64_t* scratch, uint64_t* out) {
+    uint64_t* xh = relin_scratch_xh(scratch, cnt, l, d.logn);
+    uint64_t* acc = xh + ((size_t)cnt * (l + 1) * (l + 2) << d.logn);
+    uint64_t* r = acc + ((size_t)cnt * 2 * (l + 2) << d.logn);
+    uint64_t* s = r + ((size_t)cnt * 2 << d.logn);
+    EDL_DISPATCH_LOGN(d.logn, launch_relin_finish_n<LOGN>(d, a, cnt, l, rlk, rlk_s, xh, acc, r, s, out));
+}
+
 }  // namespace edl

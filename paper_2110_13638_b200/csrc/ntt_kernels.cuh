@@ -347,6 +347,31 @@ void launch_relin_n(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t 
                   (const uint64_t*)acc, (const uint64_t*)r, (const uint64_t*)s, d.L, rs, out, add_w, add_k, *d.mt, d.cc);
 }
 
+// Hoisted rotations (several Galois elements of the same ciphertexts): the modulus raise of
+// c1 once (single-polynomial d2 INTT + modup) ...
+template <int LOGN>
+void launch_relin_raise_n(const Dev& d, const uint64_t* a, int64_t cnt, int l, uint64_t* acoef, uint64_t* xh) {
+    using C = CfgFused<LOGN>;
+    launch_cfg<C>(d, "k_relin_intt_d2", k_relin_intt_d2<C>, dim3((unsigned)cnt, l + 1), a, (const uint64_t*)nullptr, l,
+                  acoef, *d.mt);
+    launch_cfg<C>(d, "k_relin_modup", k_relin_modup<C>, dim3((unsigned)cnt, (l + 1) * (l + 1)), (const uint64_t*)acoef,
+                  l, d.L, xh, *d.mt);
+}
+
+// ... then per element: key products of the (permuted) raised digits with d = (a0, 0) and
+// the mod-down (no rescale), as in launch_relin_n's single-polynomial mode.
+template <int LOGN>
+void launch_relin_finish_n(const Dev& d, const uint64_t* a, int64_t cnt, int l, const uint64_t* rlk,
+                           const uint64_t* rlk_c, uint64_t* xh, uint64_t* acc, uint64_t* r, uint64_t* s, uint64_t* out) {
+    using C = CfgFused<LOGN>;
+    const uint64_t* b = nullptr;
+    launch_relin_mac(d, a, b, cnt, l, xh, rlk, rlk_c, acc);
+    launch_cfg<C>(d, "k_relin_moddown_intt", k_relin_moddown_intt<C>, dim3((unsigned)cnt, 2), a, b, l, (const uint64_t*)acc,
+                  d.L, 0, r, s, *d.mt, d.cc);
+    launch_cfg<C>(d, "k_relin_moddown_ntt", k_relin_moddown_ntt<C>, dim3((unsigned)cnt, 2, l + 1), a, b, l,
+                  (const uint64_t*)acc, (const uint64_t*)r, (const uint64_t*)s, d.L, 0, out, b, b, *d.mt, d.cc);
+}
+
 #define EDL_INSTANTIATE_NTT(LOGN)                                                                                   \
     template void launch_ntt_limbs_n<LOGN>(const Dev&, uint64_t*, int64_t, int, const PrimeMap&, bool);            \
     template void launch_rescale_intt_n<LOGN>(const Dev&, const uint64_t*, int64_t, int, const ulonglong2*,         \
@@ -355,6 +380,9 @@ void launch_relin_n(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t 
                                              const uint64_t*, const uint64_t*, uint64_t*, int);                     \
     template void launch_relin_n<LOGN>(const Dev&, const uint64_t*, const uint64_t*, int64_t, int, bool,            \
                                        const uint64_t*, const uint64_t*, uint64_t*, uint64_t*, uint64_t*, uint64_t*, \
-                                       uint64_t*, uint64_t*, const uint64_t*, const uint64_t*);
+                                       uint64_t*, uint64_t*, const uint64_t*, const uint64_t*);                \
+    template void launch_relin_raise_n<LOGN>(const Dev&, const uint64_t*, int64_t, int, uint64_t*, uint64_t*);     \
+    template void launch_relin_finish_n<LOGN>(const Dev&, const uint64_t*, int64_t, int, const uint64_t*,          \
+                                              const uint64_t*, uint64_t*, uint64_t*, uint64_t*, uint64_t*, uint64_t*);
 
 }  // namespace edl

@@ -804,6 +804,11 @@ __global__ void k_pack(const uint64_t* __restrict__ in, int64_t polys, int nl, i
 
 }  // namespace
 
+void launch_automorphism_rows(const Dev& d, const uint64_t* in, int64_t rows, uint32_t g, uint64_t* out) {
+    EDL_LAUNCH(d, "k_automorphism", k_automorphism<<<rows_grid(d.logn + 1, rows), PW_THREADS, 0, d.st>>>(in, rows, g, out,
+                                                                                                      d.logn));
+}
+
 void launch_automorphism(const Dev& d, const uint64_t* in, int64_t cnt, int l, uint32_t g, uint64_t* out) {
     EDL_LAUNCH(d, "k_automorphism", k_automorphism<<<rows_grid(d.logn + 1, cnt * 2 * (l + 1)), PW_THREADS, 0, d.st>>>(
                                         in, cnt * 2 * (l + 1), g, out, d.logn));

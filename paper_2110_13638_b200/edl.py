@@ -9,7 +9,7 @@ from __future__ import annotations
 import ctypes
 import os
 from dataclasses import dataclass
-from typing import Optional, Sequence
+from typing import List, Optional, Sequence
 
 import numpy as np
 
@@ -141,6 +141,7 @@ _sigs = {
     "edl_decrypt_device": (_c.c_int32, [_c.c_void_p, _P(Cts), _c.c_void_p, _c.c_int64]),
     "edl_galois_keygen": (_c.c_int32, [_c.c_void_p, _c.c_uint64, _c.c_void_p, _c.c_int32]),
     "edl_rotate": (_c.c_int32, [_c.c_void_p, _P(Cts), _c.c_int32, _P(Cts)]),
+    "edl_rotate_hoisted": (_c.c_int32, [_c.c_void_p, _P(Cts), _c.c_void_p, _c.c_int32, _c.c_void_p]),
     "edl_encode_pt": (_c.c_int32, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int64, _c.c_double, _c.c_int32,
                                    _c.c_void_p]),
     "edl_encode_pt_poly": (_c.c_int32, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int32, _c.c_void_p]),
@@ -450,6 +451,15 @@ class Context:
         st = np.ascontiguousarray(list(steps), dtype=np.int32)
         self._check(_lib.edl_galois_keygen(self._h, seed, _ptr(st), st.size), "galois_keygen")
         return self
+
+    def rotate_hoisted(self, x: CtArray, steps: Sequence[int]) -> List[CtArray]:
+        """Several rotations of x sharing one modulus raise (edl_rotate_hoisted)."""
+        st = np.ascontiguousarray(list(steps), dtype=np.int32)
+        outs = [self.empty(x.count, x.level) for _ in range(st.size)]
+        arr = (Cts * max(st.size, 1))(*[o.cts() for o in outs])
+        cx = x.cts()
+        self._check(_lib.edl_rotate_hoisted(self._h, ctypes.byref(cx), _ptr(st), st.size, arr), "rotate_hoisted")
+        return [o.update(arr[k]) for k, o in enumerate(outs)]
 
     def rotate(self, x: CtArray, steps: int) -> CtArray:
         o = self.empty(x.count, x.level)

@@ -266,6 +266,23 @@ def test_encrypt_sk_and_seeded_wire(which, c0pair, c1pair):
     assert np.allclose(g.decrypt(back, 8)[:, :8], o.decrypt(xo, 8)[:, :8], atol=1e-9)
 
 
+def test_rotate_hoisted_bit_exact(edl):
+    """Hoisted rotations (one modulus raise, several Galois elements) == the oracle's
+    rotate_hoisted on every residue; rotation 0 is a copy."""
+    from oracle import galois
+    g, o = _pair(edl, logn=10, bits=[60, 40, 40, 40, 40, 60], seed=1)
+    rs = [1, -2, 5, 0]
+    g.galois_keygen(7, [r for r in rs if r])
+    gk = {galois.galois_element(r, o.n): galois.galois_keygen(o, 7, galois.galois_element(r, o.n)) for r in rs if r}
+    lvl = 3
+    X = ock.CtArray(_rand_ct(o, 3, lvl, 81), lvl, 2.0 ** 40, o.key_id)
+    got = g.rotate_hoisted(_to_gpu(g, X.data, lvl, X.scale, o.key_id), rs)
+    want = galois.rotate_hoisted(o, X, [r for r in rs if r], gk)
+    for y, w in zip(got[:3], want):
+        assert y.level == w.level and np.array_equal(y.numpy(g.n), w.data)
+    assert np.array_equal(got[3].numpy(g.n), X.data)
+
+
 def test_mul_relin_mixed_levels(c0pair):
     g, o = c0pair
     A = ock.CtArray(_rand_ct(o, 2, 2, 41), 2, 2.0 ** 40, o.key_id)
