@@ -80,6 +80,46 @@ def masked_cc(ctx: Context, x: CtArray, K: np.ndarray, H: int, W: int, stride: i
     return CtArray(t, x.count * F, outs[0].level, outs[0].scale, outs[0].key_id)
 
 
+def tap_rotations(kh: int, kw: int, W: int) -> List[int]:
+    """Rotations bringing tap (u, v) of every window onto the window's anchor: u W + v."""
+    return [u * W + v for u in range(kh) for v in range(kw)]
+
+
+def masked_cc_hoisted(ctx: Context, x: CtArray, K: np.ndarray, H: int, W: int, stride: int,
+                      bias: Optional[Sequence[float]] = None) -> CtArray:
+    """The masked CC computed tap by tap from hoisted rotations of the input (one modulus
+    raise for all kh*kw - 1 rotations, `edl_rotate_hoisted`):
+        y_f = sum_{u,v} rot(x, u W + v) (.) pt_{f,u,v},   pt_{f,u,v}[anchor] = K_f[u][v],
+    so every window's value lands on its anchor slot and every other slot holds 0 (+ the
+    bias).  Same output layout, level and scale as `masked_cc`; the 5 x 16 plaintexts are
+    encoded on the GPU (f3) in one batch.  Needs Galois keys for tap_rotations(kh, kw, W)."""
+    F, kh, kw = K.shape
+    l = x.level
+    ql = float(ctx.params.qs[l])
+    n_slots = ctx.n // 2
+    anchors = np.asarray(anchor_slots(H, W, kh, kw, stride))
+    taps = tap_rotations(kh, kw, W)
+    z = np.zeros((F * len(taps), n_slots))
+    for f in range(F):
+        for k, (u, v) in enumerate((u, v) for u in range(kh) for v in range(kw)):
+            z[f * len(taps) + k, anchors] = K[f, u, v]
+    pts = ctx.encode_pt_poly(ctx.encode_device(z, ql), l).view(F * len(taps), -1)
+    rots = ctx.rotate_hoisted(x, taps)          # taps[0] = 0: a copy of x
+    outs = []
+    for f in range(F):
+        acc = None
+        for k in range(len(taps)):
+            y = ctx.pt_vec_mul(rots[k], pts[f * len(taps) + k], 1, l, ql)
+            acc = y if acc is None else ctx.add(acc, y)
+        acc = ctx.rescale(acc)
+        if bias is not None:
+            acc = ctx.pt_add(acc, [float(bias[f])] * acc.count)
+        outs.append(acc)
+    torch = ctx.torch
+    t = torch.stack([o.tensor.view(x.count, -1) for o in outs], dim=1).reshape(-1)
+    return CtArray(t, x.count * F, outs[0].level, outs[0].scale, outs[0].key_id)
+
+
 def sum_rotations(span: int) -> List[int]:
     """Rotations 1, 2, 4, ... summing slots [0, span) (zero elsewhere) into slot 0."""
     out, s = [], 1
@@ -229,13 +269,17 @@ def packed_logits(ctx: Context, out: CtArray, O: int, span: int) -> np.ndarray:
 
 def masked_cnn(ctx: Context, x: CtArray, K, kb, Wt, b, H: int = 28, W: int = 28, stride: int = 4,
                coeffs=(0.5, 0.197, 0.0, -0.004), encode: Optional[Callable] = None,
-               packed: bool = False) -> CtArray:
+               packed: bool = False, hoisted: bool = False) -> CtArray:
     """C1's architecture in the paper's layout: masked CC -> sigma_a -> masked dense.
     x: one image per ciphertext (level >= 4).  Returns [count*10] ciphertexts, logit o of
     image i in slot 0 of ciphertext i*10 + o; with packed=True the dense is
-    `masked_dense_packed` (read the logits with `packed_logits`)."""
+    `masked_dense_packed` (read the logits with `packed_logits`); with hoisted=True the CC is
+    `masked_cc_hoisted`."""
     F, kh, kw = np.asarray(K).shape
-    cc = masked_cc(ctx, x, K, H, W, stride, kb, encode=encode)
+    if hoisted:
+        cc = masked_cc_hoisted(ctx, x, np.asarray(K, dtype=np.float64), H, W, stride, kb)
+    else:
+        cc = masked_cc(ctx, x, K, H, W, stride, kb, encode=encode)
     act = ctx.poly_activation(cc, coeffs)
     if packed:
         kbv = np.zeros(F) if kb is None else np.asarray(kb, dtype=np.float64)

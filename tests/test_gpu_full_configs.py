@@ -132,3 +132,7 @@ def test_f1_masked_cnn_vs_float64(gpu):
     assert outp.count == 6 and outp.level == 0
     gotp = masquerade.packed_logits(ctx, outp, 10, 784)
     assert np.max(np.abs(gotp - ref)) < 1e-3
+    # CC from hoisted tap rotations (one modulus raise for the 15 rotations of an image)
+    ctx.galois_keygen(9, [r for r in masquerade.tap_rotations(4, 4, 28) if r])
+    outh = masquerade.masked_cnn(ctx, x, K, kb, W, b, packed=True, hoisted=True)
+    assert np.max(np.abs(masquerade.packed_logits(ctx, outh, 10, 784) - ref)) < 1e-3
