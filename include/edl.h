@@ -223,6 +223,14 @@ edl_status edl_encode_pt(edl_ctx* ctx, const double* slots, int64_t n_vec, int64
 edl_status edl_encode_pt_poly(edl_ctx* ctx, const int64_t* poly, int64_t n_vec, int32_t level, uint64_t* pt_out);
 edl_status edl_ct_pt_vec_mul(edl_ctx* ctx, const edl_cts* a, const uint64_t* pt, int64_t pt_count, int32_t pt_level,
                              double pt_scale, edl_cts* out);
+/* Multi-plaintext MAC (NEXT f1, the tap-by-tap masked CC over hoisted rotations):
+ * rots holds T blocks of n ciphertexts ([T][n][2][level+1][N], count = T n); pts holds
+ * F x T NTT-domain plaintexts ([F][T][pt_level+1][N]); out[c F + f] = sum_t rots[t][c] (.)
+ * pts[f][t] for both polynomials, scale rots.scale * pt_scale, no rescale (out: n F
+ * ciphertexts at rots' level, caller-allocated).  Errors: EDL_ERR_SHAPE (count not a
+ * multiple of T), EDL_ERR_LEVEL, EDL_ERR_ARG (T > 64 or null buffers).  Asynchronous. */
+edl_status edl_ct_pt_mac_multi(edl_ctx* ctx, const edl_cts* rots, int32_t T, const uint64_t* pts, int32_t F,
+                               int32_t pt_level, double pt_scale, edl_cts* out);
 edl_status edl_export_galois_key(edl_ctx* ctx, int32_t steps, uint64_t* host_out, size_t words);
 
 /* ---- NEXT f3: client encode / decode on the device (O5 canonical embedding) ----

@@ -1048,6 +1048,20 @@ edl_status edl_ct_pt_vec_mul(edl_ctx* c, const edl_cts* a, const uint64_t* pt, i
     return cuda_check(c, "ct_pt_vec_mul");
 }
 
+edl_status edl_ct_pt_mac_multi(edl_ctx* c, const edl_cts* rots, int32_t T, const uint64_t* pts, int32_t F,
+                               int32_t pt_level, double pt_scale, edl_cts* out) {
+    if (!c || !out || T < 1 || F < 1 || T > 64) return EDL_ERR_ARG;
+    edl_status s = check_ct(c, rots);
+    if (s != EDL_OK) return s;
+    if (rots->count % T) return fail(c, EDL_ERR_SHAPE, "ct_pt_mac_multi: count not a multiple of T");
+    if (pt_level < rots->level) return fail(c, EDL_ERR_LEVEL, "ct_pt_mac_multi: plaintext level below ciphertext level");
+    const int64_t n = rots->count / T;
+    if (n > 0 && (!pts || !out->data)) return fail(c, EDL_ERR_ARG, "ct_pt_mac_multi: null buffer");
+    if (n > 0) launch_pt_mac_multi(c->dev(), rots->data, T, n, rots->level, pts, F, pt_level, out->data);
+    set_meta(out, n * F, rots->level, rots->scale * pt_scale, rots->key_id);
+    return cuda_check(c, "ct_pt_mac_multi");
+}
+
 edl_status edl_mod_reduce(edl_ctx* c, edl_cts* x) {
     if (!c) return EDL_ERR_ARG;
     edl_status s = check_ct(c, x);

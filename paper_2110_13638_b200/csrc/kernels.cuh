@@ -177,6 +177,9 @@ void launch_relin_finish(const Dev& d, const uint64_t* a, int64_t cnt, int l, co
                          uint64_t* scratch, uint64_t* out);
 // pointer to the raised digits [cnt][l+1][l+2][N] inside a relin scratch block
 uint64_t* relin_scratch_xh(uint64_t* scratch, int64_t cnt, int l, int logn);
+// out [n*F] = sum_t rots[t] (.) pts[f][t]; rots [T][n][2][l+1][N], pts [F][T][ptl+1][N]
+void launch_pt_mac_multi(const Dev& d, const uint64_t* rots, int T, int64_t n, int l, const uint64_t* pts, int F, int ptl,
+                         uint64_t* out);
 // sigma_g on `rows` NTT-domain rows of N residues
 void launch_automorphism_rows(const Dev& d, const uint64_t* in, int64_t rows, uint32_t g, uint64_t* out);
 

@@ -804,6 +804,55 @@ __global__ void k_pack(const uint64_t* __restrict__ in, int64_t polys, int nl, i
 
 }  // namespace
 
+// out[c*F + f] = sum_t rots[t][c] (.) pts[f][t]  (NTT domain, both polynomials): every
+// rotated residue is read once and feeds all F filters; FP64-pipe limbs accumulate exact
+// binary64 products (T <= 64 terms of |.| <= 0.51 q), the others 128-bit sums.
+__global__ void k_pt_mac_multi(const uint64_t* __restrict__ rots, int T, int64_t n, int l,
+                               const uint64_t* __restrict__ pts, int F, int ptl, uint64_t* __restrict__ out,
+                               const __grid_constant__ ModTable mods, int logn) {
+    const int nl = l + 1;
+    const int64_t row = blockIdx.y;                 // (c, p, i)
+    const int i = (int)(row % nl);
+    const int64_t cp = row / nl;                    // c * 2 + p
+    const int64_t c = cp / 2;
+    const int p = (int)(cp % 2);
+    const ModInfo& m = mods[i];
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= (1 << logn)) return;
+    const size_t rot_stride = (size_t)n * 2 * nl << logn;   // one rotation block
+    const uint64_t* xr = rots + ((size_t)row << logn) + k;
+    const bool f64 = m.fp == 2;
+    const double qd = u52_to_double(m.q);
+    for (int f = 0; f < F; f++) {
+        const uint64_t* pf = pts + ((((size_t)f * T) * (ptl + 1) + i) << logn) + k;
+        const size_t pt_stride = (size_t)(ptl + 1) << logn;
+        uint64_t* dst = out + ((((size_t)c * F + f) * 2 + p) * nl + i << logn) + k;
+        if (f64) {
+            double acc = 0.0;
+            for (int t = 0; t < T; t++) {
+                const double x = u52_to_double(__ldg(xr + t * rot_stride)), y = u52_to_double(__ldg(pf + t * pt_stride));
+                const double hi = __dmul_rn(x, y);
+                const double lo = __fma_rn(x, y, -hi);
+                const double qt = __dsub_rn(__fma_rn(hi, m.qinv_d, F64_RND), F64_RND);
+                acc = __dadd_rn(acc, __dadd_rn(__fma_rn(-qt, qd, hi), lo));
+            }
+            *dst = f64_to_canon(f64_reduce(acc, qd, m.qinv_d), qd);
+        } else {
+            U128 acc;
+            acc.lo = acc.hi = 0;
+            for (int t = 0; t < T; t++) mac128(acc, __ldg(xr + t * rot_stride), __ldg(pf + t * pt_stride));
+            *dst = barrett128(acc, m);
+        }
+    }
+}
+
+void launch_pt_mac_multi(const Dev& d, const uint64_t* rots, int T, int64_t n, int l, const uint64_t* pts, int F, int ptl,
+                         uint64_t* out) {
+    const dim3 grid((unsigned)((1 << d.logn) / PW_THREADS), (unsigned)(n * 2 * (l + 1)));
+    EDL_LAUNCH(d, "k_pt_mac_multi", k_pt_mac_multi<<<grid, PW_THREADS, 0, d.st>>>(rots, T, n, l, pts, F, ptl, out, *d.mt,
+                                                                                  d.logn));
+}
+
 void launch_automorphism_rows(const Dev& d, const uint64_t* in, int64_t rows, uint32_t g, uint64_t* out) {
     EDL_LAUNCH(d, "k_automorphism", k_automorphism<<<rows_grid(d.logn + 1, rows), PW_THREADS, 0, d.st>>>(in, rows, g, out,
                                                                                                       d.logn));

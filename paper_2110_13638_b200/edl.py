@@ -142,6 +142,8 @@ _sigs = {
     "edl_galois_keygen": (_c.c_int32, [_c.c_void_p, _c.c_uint64, _c.c_void_p, _c.c_int32]),
     "edl_rotate": (_c.c_int32, [_c.c_void_p, _P(Cts), _c.c_int32, _P(Cts)]),
     "edl_rotate_hoisted": (_c.c_int32, [_c.c_void_p, _P(Cts), _c.c_void_p, _c.c_int32, _c.c_void_p]),
+    "edl_ct_pt_mac_multi": (_c.c_int32, [_c.c_void_p, _P(Cts), _c.c_int32, _c.c_void_p, _c.c_int32, _c.c_int32,
+                                         _c.c_double, _P(Cts)]),
     "edl_encode_pt": (_c.c_int32, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int64, _c.c_double, _c.c_int32,
                                    _c.c_void_p]),
     "edl_encode_pt_poly": (_c.c_int32, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int32, _c.c_void_p]),
@@ -452,14 +454,22 @@ class Context:
         self._check(_lib.edl_galois_keygen(self._h, seed, _ptr(st), st.size), "galois_keygen")
         return self
 
-    def rotate_hoisted(self, x: CtArray, steps: Sequence[int]) -> List[CtArray]:
+    def rotate_hoisted(self, x: CtArray, steps: Sequence[int], outs: Optional[List[CtArray]] = None) -> List[CtArray]:
         """Several rotations of x sharing one modulus raise (edl_rotate_hoisted)."""
         st = np.ascontiguousarray(list(steps), dtype=np.int32)
-        outs = [self.empty(x.count, x.level) for _ in range(st.size)]
+        outs = outs if outs is not None else [self.empty(x.count, x.level) for _ in range(st.size)]
         arr = (Cts * max(st.size, 1))(*[o.cts() for o in outs])
         cx = x.cts()
         self._check(_lib.edl_rotate_hoisted(self._h, ctypes.byref(cx), _ptr(st), st.size, arr), "rotate_hoisted")
         return [o.update(arr[k]) for k, o in enumerate(outs)]
+
+    def pt_mac_multi(self, rots: CtArray, T: int, pts, F: int, pt_level: int, pt_scale: float) -> CtArray:
+        """out[c*F + f] = sum_t rots[t][c] (.) pts[f][t] (edl_ct_pt_mac_multi)."""
+        o = self.empty(rots.count // T * F, rots.level)
+        cr, co = rots.cts(), o.cts()
+        self._check(_lib.edl_ct_pt_mac_multi(self._h, ctypes.byref(cr), T, ctypes.c_void_p(pts.data_ptr()), F, pt_level,
+                                             pt_scale, ctypes.byref(co)), "ct_pt_mac_multi")
+        return o.update(co)
 
     def rotate(self, x: CtArray, steps: int) -> CtArray:
         o = self.empty(x.count, x.level)

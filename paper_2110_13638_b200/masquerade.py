@@ -103,21 +103,17 @@ def masked_cc_hoisted(ctx: Context, x: CtArray, K: np.ndarray, H: int, W: int, s
     for f in range(F):
         for k, (u, v) in enumerate((u, v) for u in range(kh) for v in range(kw)):
             z[f * len(taps) + k, anchors] = K[f, u, v]
-    pts = ctx.encode_pt_poly(ctx.encode_device(z, ql), l).view(F * len(taps), -1)
-    rots = ctx.rotate_hoisted(x, taps)          # taps[0] = 0: a copy of x
-    outs = []
-    for f in range(F):
-        acc = None
-        for k in range(len(taps)):
-            y = ctx.pt_vec_mul(rots[k], pts[f * len(taps) + k], 1, l, ql)
-            acc = y if acc is None else ctx.add(acc, y)
-        acc = ctx.rescale(acc)
-        if bias is not None:
-            acc = ctx.pt_add(acc, [float(bias[f])] * acc.count)
-        outs.append(acc)
-    torch = ctx.torch
-    t = torch.stack([o.tensor.view(x.count, -1) for o in outs], dim=1).reshape(-1)
-    return CtArray(t, x.count * F, outs[0].level, outs[0].scale, outs[0].key_id)
+    T = len(taps)
+    pts = ctx.encode_pt_poly(ctx.encode_device(z, ql), l)          # [F][T][l+1][N]
+    words = x.tensor.numel()
+    big = ctx.torch.empty(T * words, dtype=ctx.torch.int64, device=x.tensor.device)
+    views = [CtArray(big[k * words:(k + 1) * words], x.count, l, x.scale, x.key_id) for k in range(T)]
+    ctx.rotate_hoisted(x, taps, outs=views)     # taps[0] = 0: a copy of x
+    rots = CtArray(big, T * x.count, l, x.scale, x.key_id)
+    y = ctx.rescale(ctx.pt_mac_multi(rots, T, pts, F, l, ql))   # [count*F], image-major
+    if bias is not None:
+        y = ctx.pt_add(y, [float(bias[f]) for _ in range(x.count) for f in range(F)])
+    return y
 
 
 def sum_rotations(span: int) -> List[int]:
