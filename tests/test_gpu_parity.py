@@ -283,6 +283,30 @@ def test_rotate_hoisted_bit_exact(edl):
     assert np.array_equal(got[3].numpy(g.n), X.data)
 
 
+def test_pt_mac_multi_bit_exact(c1pair):
+    """edl_ct_pt_mac_multi == the oracle's sum over t of plaintext products (every limb
+    path: q0 with 128-bit sums, the 40-bit limbs with FP64-pipe products), incl. all-(q-1)."""
+    from oracle import galois
+    g, o = c1pair
+    lvl, T, F, n = 4, 3, 2, 2
+    rots = _rand_ct(o, T * n, lvl, 91)
+    rots[0] = np.stack([np.stack([np.full(o.n, o.q[i] - 1, dtype=np.uint64) for i in range(lvl + 1)])] * 2)
+    pts = random_residues((F, T, lvl + 1, o.n), o.q[: lvl + 1] * (F * T), seed=92)
+    pts[0, 0] = np.stack([np.full(o.n, o.q[i] - 1, dtype=np.uint64) for i in range(lvl + 1)])
+    rg = _to_gpu(g, rots, lvl, 2.0 ** 40, o.key_id)
+    ptg = g.torch.from_numpy(pts.view(np.int64).reshape(-1).copy()).cuda()
+    got = g.pt_mac_multi(rg, T, ptg, F, lvl, 2.0 ** 20)
+    assert got.count == n * F and got.scale == 2.0 ** 60
+    R = rots.reshape(T, n, 2, lvl + 1, o.n)
+    for c in range(n):
+        for f in range(F):
+            acc = None
+            for t in range(T):
+                y = galois.mul_plain(o, ock.CtArray(R[t, c:c + 1], lvl, 2.0 ** 40, o.key_id), pts[f, t][None], 2.0 ** 20)
+                acc = y if acc is None else o.add(acc, y)
+            assert np.array_equal(got.numpy(g.n)[c * F + f], acc.data[0])
+
+
 def test_mul_relin_mixed_levels(c0pair):
     g, o = c0pair
     A = ock.CtArray(_rand_ct(o, 2, 2, 41), 2, 2.0 ** 40, o.key_id)
