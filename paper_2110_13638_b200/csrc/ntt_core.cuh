@@ -269,6 +269,10 @@ __device__ __forceinline__ void inv_pass_regs(uint64_t* x, int high, const ModIn
 // A forward-transform epilogue may take the F64 path's outputs before canonicalisation:
 // a Store with a member f64(idx, x, operand) receives x as the exact binary64 integer
 // (|x| < 15 q, any residue class representative) and does its arithmetic on the FP64 pipe.
+template <class L, class = void>
+struct HasF64Load : std::false_type {};
+template <class L>
+struct HasF64Load<L, std::void_t<decltype(&L::f64)>> : std::true_type {};
 template <class S, class = void>
 struct HasF64Store : std::false_type {};
 template <class S>
@@ -348,10 +352,16 @@ __device__ __forceinline__ void ntt_fwd_impl(uint64_t* sm, const ModInfo& m, Loa
     const uint32_t mb = smem_u32(&xchg_mbar);
     (void)mb;
     // F64 path: the loaded residues (< 4q) become exact binary64 integers
+    // (a Load with a member f64(idx) hands the F64 path its prologue's result directly as
+    //  an exact binary64 integer of magnitude < 4q, any residue class representative)
     auto ld = [&](int idx) {
-        const uint64_t v = load(idx);
-        if constexpr (FP) return f64_from_u(v);
-        else return v;
+        if constexpr (FP && HasF64Load<Load>::value) {
+            return bits_of(load.f64(idx));
+        } else {
+            const uint64_t v = load(idx);
+            if constexpr (FP) return f64_from_u(v);
+            else return v;
+        }
     };
     uint64_t x[C::E];
     if constexpr (C::K == 1) {
@@ -453,10 +463,13 @@ __device__ __forceinline__ void ntt_inv_impl(uint64_t* sm, const ModInfo& m, Loa
         // behind the previous one's full latency
         uint64_t t[C::E];
 #pragma unroll
-        for (int r = 0; r < C::E; r++) t[r] = load(C::idx(r));
+        for (int r = 0; r < C::E; r++) {
+            if constexpr (FP && HasF64Load<Load>::value) t[r] = bits_of(load.f64(C::idx(r)));   // |.| < 2q
+            else t[r] = load(C::idx(r));
+        }
 #pragma unroll
         for (int r = 0; r < C::E; r++) {
-            if constexpr (FP) sm[spad(tid + r * C::T)] = f64_from_u(t[r]);
+            if constexpr (FP && !HasF64Load<Load>::value) sm[spad(tid + r * C::T)] = f64_from_u(t[r]);
             else sm[spad(tid + r * C::T)] = t[r];
         }
     }

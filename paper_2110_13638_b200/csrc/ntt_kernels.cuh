@@ -138,14 +138,30 @@ k_relin_intt_d2(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, 
     const uint64_t* b1 = b ? b + limb_off(c, 1, j, l + 1, C::LOGN) : a1;
     const bool single = (b == nullptr);
     uint64_t* dst = acoef + (((size_t)c * (l + 1) + j) << C::LOGN);
+    struct Load {   // d2 = a1 b1 (or a1); F64 limbs: the exact product on the FP64 pipe, |.| <= 0.51 q
+        const uint64_t *a1, *b1;
+        bool single;
+        const ModInfo& m;
+        __device__ __forceinline__ uint64_t operator()(int idx) const {
+            return single ? a1[idx] : mulmod(a1[idx], b1[idx], m);
+        }
+        __device__ __forceinline__ double f64(int idx) const {
+            const double x = u52_to_double(a1[idx]);
+            if (single) return x;
+            const double y = u52_to_double(b1[idx]), qd = u52_to_double(m.q);
+            const double hi = __dmul_rn(x, y);
+            const double lo = __fma_rn(x, y, -hi);
+            const double qt = __dsub_rn(__fma_rn(hi, m.qinv_d, F64_RND), F64_RND);
+            return __dadd_rn(__fma_rn(-qt, qd, hi), lo);
+        }
+    };
     if (threadIdx.x == 0)
         pf_next_wave<C>([&](int64_t bx, int cr, int y, int) {
             pf_sub<C>(a + limb_off(bx, 1, y, l + 1, C::LOGN), cr, false);
             if (b && b != a) pf_sub<C>(b + limb_off(bx, 1, y, l + 1, C::LOGN), cr, false);
         });
-    auto ld = [&](int idx) { return single ? a1[idx] : mulmod(a1[idx], b1[idx], m); };
     auto st = [&](int idx, uint64_t v) { dst[idx] = v; };
-    ntt_inv<C>(sm, m, ld, st);
+    ntt_inv<C>(sm, m, Load{a1, b1, single, m}, st);
 }
 
 // M2a modulus raise: xh_{j,t} = NTT_t(acoef_j mod t) for every digit j and target t != j
@@ -265,10 +281,23 @@ k_relin_moddown_ntt(const uint64_t* __restrict__ a, const uint64_t* __restrict__
         const uint64_t ql = mods[l].q;
         const uint64_t qlmod = cc->qmod[l][i];
         const ulonglong2 qlinv = cc->qinv[l][i];
-        auto ld = [&](int idx) {
-            uint64_t u = mulc(center_mod(rr[idx], P, pmod, m), pinv, m);
-            return addmod(u, center_mod(ss[idx], ql, qlmod, m), m.q);
+        struct Load {   // [r] P^-1 + [s]; F64 limbs: the product on the FP64 pipe, |.| < 1.7 q
+            const uint64_t *rr, *ss;
+            uint64_t P, pmod, ql, qlmod;
+            ulonglong2 pinv;
+            const ModInfo& m;
+            __device__ __forceinline__ uint64_t operator()(int idx) const {
+                uint64_t u = mulc(center_mod(rr[idx], P, pmod, m), pinv, m);
+                return addmod(u, center_mod(ss[idx], ql, qlmod, m), m.q);
+            }
+            __device__ __forceinline__ double f64(int idx) const {
+                const double qd = u52_to_double(m.q);
+                const double u = f64_mulc(u52_to_double(center_mod(rr[idx], P, pmod, m)), u52_to_double(pinv.x),
+                                          f64_of(pinv.y), qd);
+                return __dadd_rn(u, u52_to_double(center_mod(ss[idx], ql, qlmod, m)));
+            }
         };
+        const Load ld{rr, ss, P, pmod, ql, qlmod, pinv, m};
         auto pre = [&](int idx) { return vi[idx]; };
         // (v - x) q_l^-1 (+ w + k: a fused ciphertext + constant addend, e.g. sigma's output
         // assembly); F64 limbs: on the unreduced binary64 transform output
@@ -298,7 +327,20 @@ k_relin_moddown_ntt(const uint64_t* __restrict__ a, const uint64_t* __restrict__
         ntt_fwd<C>(sm, m, ld, pre, Store{dst, wl, kk, m, qlinv});
     } else {
         // out = d + (acc - NTT([r])) P^-1 = v - NTT([r] P^-1)  (Z_q-linear, exact)
-        auto ld = [&](int idx) { return mulc(center_mod(rr[idx], P, pmod, m), pinv, m); };
+        struct Load {   // [r] P^-1; F64 limbs: on the FP64 pipe, |.| <= 0.625 q
+            const uint64_t* rr;
+            uint64_t P, pmod;
+            ulonglong2 pinv;
+            const ModInfo& m;
+            __device__ __forceinline__ uint64_t operator()(int idx) const {
+                return mulc(center_mod(rr[idx], P, pmod, m), pinv, m);
+            }
+            __device__ __forceinline__ double f64(int idx) const {
+                return f64_mulc(u52_to_double(center_mod(rr[idx], P, pmod, m)), u52_to_double(pinv.x), f64_of(pinv.y),
+                                u52_to_double(m.q));
+            }
+        };
+        const Load ld{rr, P, pmod, pinv, m};
         auto pre = [&](int idx) { return vi[idx]; };
         auto st = [&](int idx, uint64_t x, uint64_t v) { dst[idx] = submod(v, x, m.q); };
         ntt_fwd<C>(sm, m, ld, pre, st);
