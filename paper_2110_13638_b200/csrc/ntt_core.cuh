@@ -457,6 +457,11 @@ __device__ __forceinline__ void ntt_inv_impl(uint64_t* sm, const ModInfo& m, Loa
         if constexpr (FP) return f64_to_canon(f64_of(v), qd);
         else return csub(v, q);
     };
+    // outputs: canonical uint64, or (F64 path, Store with f64()) the binary64 value, |.| <= 0.625 q
+    auto put = [&](int idx, uint64_t v, auto pvv) {
+        if constexpr (FP && HasF64Store<Store>::value) store.f64(idx, f64_of(v), pvv);
+        else store(idx, canon(v), pvv);
+    };
     {
         // every load of the thread first, then the shared-memory stores: interleaved, a store
         // (generic pointer: possible alias of the load's source) would pin each next load
@@ -485,7 +490,7 @@ __device__ __forceinline__ void ntt_inv_impl(uint64_t* sm, const ModInfo& m, Loa
 #pragma unroll
         for (int r = 0; r < C::E; r++) pv[r] = pre(tid + r * C::T);
 #pragma unroll
-        for (int r = 0; r < C::E; r++) store(tid + r * C::T, canon(x[r]), pv[r]);
+        for (int r = 0; r < C::E; r++) put(tid + r * C::T, x[r], pv[r]);
         __syncthreads();
     } else {
         constexpr int MK = C::M / C::K;
@@ -532,7 +537,7 @@ __device__ __forceinline__ void ntt_inv_impl(uint64_t* sm, const ModInfo& m, Loa
             for (int t = 0; t < C::K; t++) x[g * C::K + t] = sm[spad(t * MK + tid + g * C::T)];
             inv_pass_regs<0, C::LOGK, true, FP>(x + g * C::K, 0, m, two_q);
 #pragma unroll
-            for (int t = 0; t < C::K; t++) store(j0 + g * C::T + t * C::M, canon(x[g * C::K + t]), pv[g * C::K + t]);
+            for (int t = 0; t < C::K; t++) put(j0 + g * C::T + t * C::M, x[g * C::K + t], pv[g * C::K + t]);
         }
         __syncthreads();
 #ifdef EDL_XCHG_ASYNC

@@ -54,11 +54,21 @@ k_rescale_intt(const uint64_t* __restrict__ in, int l, const ulonglong2* __restr
     } else {
         const ulonglong2 wa = w[c * (l + 1) + l], wb = w2[c * (l + 1) + l];
         auto ld = [&](int idx) { return src[idx]; };
-        auto st = [&](int idx, uint64_t v) {
-            dst[idx] = mulc(v, wa, m);
-            dst2[idx] = mulc(v, wb, m);
+        struct Store {   // two scalar products of the INTT; F64 limbs on the FP64 pipe
+            uint64_t *dst, *dst2;
+            ulonglong2 wa, wb;
+            const ModInfo& m;
+            __device__ __forceinline__ void operator()(int idx, uint64_t v, int) const {
+                dst[idx] = mulc(v, wa, m);
+                dst2[idx] = mulc(v, wb, m);
+            }
+            __device__ __forceinline__ void f64(int idx, double v, int) const {
+                const double qd = u52_to_double(m.q);
+                dst[idx] = f64_to_canon(f64_mulc(v, u52_to_double(wa.x), f64_of(wa.y), qd), qd);
+                dst2[idx] = f64_to_canon(f64_mulc(v, u52_to_double(wb.x), f64_of(wb.y), qd), qd);
+            }
         };
-        ntt_inv<C>(sm, m, ld, st);
+        ntt_inv<C>(sm, m, ld, NoPre(), Store{dst, dst2, wa, wb, m});
     }
 }
 
@@ -244,11 +254,22 @@ k_relin_moddown_intt(const uint64_t* __restrict__ a, const uint64_t* __restrict_
     uint64_t* sdst = s_out + (((size_t)c * 2 + cp) << C::LOGN);
     auto ld = [&](int idx) { return vl[idx]; };
     auto pre = [&](int idx) { return rdst[idx]; };
-    auto st = [&](int idx, uint64_t y, uint64_t rv) {
-        uint64_t z = mulc(center_mod(rv, mp.q, pmod, ml), pinv, ml);
-        sdst[idx] = submod(y, z, ml.q);
+    struct Store {   // s = y - [r] P^-1; F64 limbs: y unreduced (|y| <= 0.625 q), product on the FP64 pipe
+        uint64_t* sdst;
+        uint64_t Pq, pmod;
+        ulonglong2 pinv;
+        const ModInfo& ml;
+        __device__ __forceinline__ void operator()(int idx, uint64_t y, uint64_t rv) const {
+            uint64_t z = mulc(center_mod(rv, Pq, pmod, ml), pinv, ml);
+            sdst[idx] = submod(y, z, ml.q);
+        }
+        __device__ __forceinline__ void f64(int idx, double y, uint64_t rv) const {
+            const double qd = u52_to_double(ml.q);
+            const double z = f64_mulc(u52_to_double(center_mod(rv, Pq, pmod, ml)), u52_to_double(pinv.x), f64_of(pinv.y), qd);
+            sdst[idx] = f64_to_canon(f64_reduce(__dsub_rn(y, z), qd, ml.qinv_d), qd);
+        }
     };
-    ntt_inv<C>(sm, ml, ld, pre, st);
+    ntt_inv<C>(sm, ml, ld, pre, Store{sdst, mp.q, pmod, pinv, ml});
 }
 
 template <class C>
