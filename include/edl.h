@@ -92,7 +92,10 @@ edl_status edl_params_from_bits(int32_t log_n, const int32_t* bits, int32_t n_bi
 size_t edl_cts_bytes(int64_t count, int32_t level, int32_t log_n);
 
 /* Create a context on CUDA `device`, enqueueing on `cuda_stream` (a cudaStream_t; NULL =
- * legacy default stream).  Uploads twiddle tables.  log_n must be in [10, 14]. */
+ * legacy default stream).  Uploads twiddle tables.  log_n must be in [10, 16] (N > 2^13
+ * runs one limb per thread-block cluster) and compiled into the build (EDL_LOGNS_MASK);
+ * every modulus must be below 2^60 (the MAC kernels fold up to 256 full 128-bit products
+ * before reducing).  EDL_ERR_ARG otherwise. */
 edl_status edl_ctx_create(const edl_params* params, int32_t device, void* cuda_stream, edl_ctx** out);
 void edl_ctx_destroy(edl_ctx* ctx);
 edl_status edl_ctx_set_stream(edl_ctx* ctx, void* cuda_stream);
@@ -108,8 +111,14 @@ int32_t edl_profile_read(edl_ctx* ctx, char* names, size_t names_len, double* ms
                          int32_t max_entries);
 
 /* O7 key generation from Philox4x32-10(seed): secret s (ternary), public key over
- * q_0..q_L, relinearisation key over q_0..q_L, P.  key_id := seed.  Synchronises. */
+ * q_0..q_L, relinearisation key over q_0..q_L, P.  The seed is secret key material: the
+ * context keeps it on the host (secret-key encryption's error PRF) and never exposes it.
+ * key_id := the first 8 bytes of SHA-256("edl-key\0" || seed) (edl_key_id), a one-way
+ * function of the seed, equal on every rank that generated the same key.  Galois keys of
+ * a previous key are freed.  Synchronises. */
 edl_status edl_keygen(edl_ctx* ctx, uint64_t seed);
+/* The current key's identifier (0 before edl_keygen). */
+uint64_t edl_key_id(const edl_ctx* ctx);
 
 /* O5 encode on the host: slots [n_vec][n_slots] doubles -> int64 coefficient polys
  * poly_out [n_vec][N] (host), m_k = rint(scale * u_k).  EDL_ERR_CAPACITY if
@@ -119,16 +128,22 @@ edl_status edl_encode(edl_ctx* ctx, const double* slots, int64_t n_vec, int64_t 
 
 /* O8 public-key encryption of integer polys (DEVICE pointer int64 [n_vec][N]) at
  * `level` with scale `scale`; ciphertext c uses Philox object id obj0 + c.  out->data
- * must hold edl_cts_bytes(n_vec, level); out's metadata is filled in. */
+ * must hold edl_cts_bytes(n_vec, level); out's metadata is filled in.  enc_seed is the
+ * encryptor's secret randomness (v, e0, e1 are functions of (enc_seed, object id)): a pair
+ * (enc_seed, object id) must never be used twice under one key, or the two ciphertexts
+ * differ by exactly (m - m', 0). */
 edl_status edl_encrypt_poly(edl_ctx* ctx, const int64_t* poly_dev, int64_t n_vec, int32_t level, double scale,
                             uint64_t enc_seed, uint32_t obj0, edl_cts* out);
 
 /* Secret-key encryption (DESIGN reading Z16; the client owns s in EDLaaS, PAPER.md:258-260,
  * 314-316): for ciphertext c (Philox object id obj0 + c) and limb i,
  *   c1_i = uniform(enc_seed, obj0 + c, limb i, tag 11)      (drawn in the NTT domain),
- *   c0_i = NTT_i(m + e) - c1_i s_i,   e = CBD(enc_seed, obj0 + c, tag 12),
- * so c0 + c1 s = m + e exactly and c1 is a public function of (enc_seed, obj0 + c): such
- * ciphertexts can cross PCIe as c0 plus the seed (edl_cts_pack_c0 / edl_cts_unpack_seeded).
+ *   c0_i = NTT_i(m + e) - c1_i s_i,   e = CBD(k_e, obj0 + c, tag 12),
+ *   k_e = words 0,1 of Philox_{key seed}(enc_seed lo, enc_seed hi, 0, 13)  (a PRF keyed by
+ *         the secret key's seed, so the error is NOT a function of the public enc_seed),
+ * so c0 + c1 s = m + e exactly and only c1 is a public function of (enc_seed, obj0 + c):
+ * such ciphertexts can cross PCIe as c0 plus the seed (edl_cts_pack_c0 /
+ * edl_cts_unpack_seeded).  (enc_seed, object id) must never repeat under one key.
  * Arguments, layout and errors as edl_encrypt_poly.  Asynchronous. */
 edl_status edl_encrypt_poly_sk(edl_ctx* ctx, const int64_t* poly_dev, int64_t n_vec, int32_t level, double scale,
                                uint64_t enc_seed, uint32_t obj0, edl_cts* out);

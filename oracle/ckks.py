@@ -15,6 +15,7 @@ rescale, keygen error identity, decrypt(encrypt(z)) ~ z, homomorphic ops vs floa
 """
 from __future__ import annotations
 
+import hashlib
 from dataclasses import dataclass
 from typing import List, Optional, Sequence
 
@@ -134,7 +135,8 @@ class Context:
                 rlk[j, 0, i] = bj
                 rlk[j, 1, i] = aj
         self.rlk = rlk
-        self.key_id = seed
+        self.key_id = key_identifier(seed)
+        self.sk_seed = seed               # secret: keys the secret-key encryption error PRF
         self.pk_e = e
         return self
 
@@ -171,9 +173,10 @@ class Context:
         """Secret-key encryption (DESIGN reading Z16; the paper's client owns s, PAPER.md:258-260,
         314-316): for ciphertext c (object id obj = obj0 + c) and limb i,
             c1_i = a_i = uniform(enc_seed, obj, limb i, TAG_SK_A)  (an NTT-domain residue vector),
-            c0_i = NTT_i(m + e) - a_i s_i,  e = CBD(enc_seed, obj, TAG_SK_E),
-        so c0 + c1 s = m + e exactly and c1 is a public function of (enc_seed, obj): the
-        ciphertext can travel as c0 plus the seed."""
+            c0_i = NTT_i(m + e) - a_i s_i,  e = CBD(k_e, obj, TAG_SK_E),
+            k_e = sk_error_key(key seed, enc_seed)   (a PRF keyed by the secret key's seed),
+        so c0 + c1 s = m + e exactly and only c1 is a public function of (enc_seed, obj): the
+        ciphertext can travel as c0 plus the seed, and the wire data does not determine e."""
         if self.key_id is None:
             raise CkksError("no key")
         lvl = self.L if level is None else level
@@ -181,9 +184,10 @@ class Context:
         polys = np.asarray(polys, dtype=np.int64)
         count = polys.shape[0]
         out = np.zeros((count, 2, lvl + 1, self.n), dtype=np.uint64)
+        k_e = sk_error_key(self.sk_seed, enc_seed)
         for c in range(count):
             obj = obj0 + c
-            e_hat = self.signed_to_ntt(smp.cbd(self.n, enc_seed, obj, smp.TAG_SK_E), idx)
+            e_hat = self.signed_to_ntt(smp.cbd(self.n, k_e, obj, smp.TAG_SK_E), idx)
             m_hat = self.signed_to_ntt(polys[c], idx)
             for i in idx:
                 q = self.q[i]
@@ -355,6 +359,22 @@ class Context:
                     rq = self.ntt(ring.center_mod(r, ql, q)[None, :], [i])[0]
                     out[c, k, i] = ring.mul_scalar(ring.sub(a.data[c, k, i], rq, q), ring.inv(ql % q, q), q)
         return CtArray(out, l - 1, a.scale / float(ql), a.key_id)
+
+
+def key_identifier(seed: int) -> int:
+    """Public key identifier: the first 8 bytes (little-endian) of
+    SHA-256(b"edl-key\\0" || seed as 8 little-endian bytes), never 0 -- a one-way function of
+    the secret seed (the seed itself is never published)."""
+    d = hashlib.sha256(b"edl-key\0" + int(seed).to_bytes(8, "little")).digest()
+    return int.from_bytes(d[:8], "little") or 1
+
+
+def sk_error_key(sk_seed: int, enc_seed: int) -> int:
+    """Philox key of the secret-key encryption error (DESIGN reading Z16):
+    words 0, 1 of Philox4x32-10 with key (sk_seed lo, hi) at counter
+    (enc_seed lo, enc_seed hi, 0, 13)."""
+    w = smp.philox4x32_10([enc_seed & 0xFFFFFFFF, enc_seed >> 32, 0, 13], [sk_seed & 0xFFFFFFFF, sk_seed >> 32])
+    return int(w[0]) | (int(w[1]) << 32)
 
 
 def crt_lift_centered(m: np.ndarray, qs: Sequence[int]) -> List[int]:

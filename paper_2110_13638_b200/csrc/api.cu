@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cfenv>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -40,7 +41,8 @@ struct edl_ctx {
     uint64_t* d_rlk_s = nullptr;
     std::map<uint32_t, std::pair<uint64_t*, uint64_t*>> gkeys;   // Galois element -> (key, companions)
     bool has_key = false;
-    uint64_t key_id = 0;
+    uint64_t key_id = 0;       // host::key_identifier(seed): public, one-way in the seed
+    uint64_t sk_seed = 0;      // secret: the key seed (secret-key encryption's error PRF)
     uint64_t* d_scratch = nullptr;
     size_t scratch_words = 0;
     uint8_t* h_pin = nullptr;       // mapped pinned staging ring (host view)
@@ -55,6 +57,11 @@ struct edl_ctx {
     std::unordered_multimap<uint64_t, CacheEnt> cache;   // content hash -> device copy
     std::string err;
     mutable Prof prof;
+    // Key-switch variant (N = 2^14): the fused target-major kernel k_relin_ks (modulus raise
+    // and key products in one pass, accumulators in shared memory) or the two-kernel
+    // k_relin_modup + k_relin_mac (default: measured faster on B200).
+    // EDL_KS_FUSED=1 in the environment at context creation selects the fused kernel.
+    bool ks_fused = false;
 
     Dev dev() const {
         Dev d;
@@ -66,6 +73,7 @@ struct edl_ctx {
         d.L = L;
         d.st = st;
         d.prof = &prof;
+        d.ks_fused = ks_fused;
         return d;
     }
     uint64_t modulus(int idx) const { return idx <= L ? prm.q[idx] : prm.p_special; }
@@ -323,9 +331,10 @@ edl_status edl_ctx_create(const edl_params* p, int32_t device, void* stream, edl
     *out = nullptr;
     if (p->log_n < 10 || p->log_n > 16 || p->n_data < 1 || p->n_data > EDL_MAX_PRIMES) return EDL_ERR_ARG;
     if (!(((EDL_LOGNS_MASK) >> p->log_n) & 1)) return EDL_ERR_ARG;   // ring degree not compiled into this build
+    // every modulus < 2^60: the MAC kernels fold up to 256 full 128-bit products (256 q^2 < 2^128)
     for (int k = 0; k < p->n_data; k++)
-        if (p->q[k] >= (1ull << 61)) return EDL_ERR_ARG;
-    if (p->p_special >= (1ull << 61)) return EDL_ERR_ARG;
+        if (p->q[k] >= (1ull << 60)) return EDL_ERR_ARG;
+    if (p->p_special >= (1ull << 60)) return EDL_ERR_ARG;
     if (cudaSetDevice(device) != cudaSuccess) return EDL_ERR_CUDA;
     edl_ctx* c = new edl_ctx();
     c->prm = *p;
@@ -334,6 +343,10 @@ edl_status edl_ctx_create(const edl_params* p, int32_t device, void* stream, edl
     c->L = p->n_data - 1;
     c->device = device;
     c->st = (cudaStream_t)stream;
+    {
+        const char* e = std::getenv("EDL_KS_FUSED");
+        c->ks_fused = e && e[0] == '1';
+    }
     const int nm = c->L + 2;
     // twiddle tables: per modulus [fwd N][inv N] of {w, w'}
     const size_t tw_words = (size_t)nm * 4 * c->N;
@@ -350,8 +363,18 @@ edl_status edl_ctx_create(const edl_params* p, int32_t device, void* stream, edl
         host::twiddle_table(q, psi, c->logn, true, ti);
         uint64_t* dfwd = c->d_tw + (size_t)k * 4 * c->N;
         uint64_t* dinv = dfwd + 2 * c->N;
-        cudaMemcpy(dfwd, tf.data(), tf.size() * 8, cudaMemcpyHostToDevice);
-        cudaMemcpy(dinv, ti.data(), ti.size() * 8, cudaMemcpyHostToDevice);
+        if (host::f64_ntt_prime(q)) {   // FP64-pipe butterflies: compact [N] binary64 w (f64_mult, no companion)
+            std::vector<uint64_t> cf(c->N), ci(c->N);
+            for (int64_t j = 0; j < c->N; j++) {
+                cf[j] = tf[2 * j];
+                ci[j] = ti[2 * j];
+            }
+            cudaMemcpy(dfwd, cf.data(), cf.size() * 8, cudaMemcpyHostToDevice);
+            cudaMemcpy(dinv, ci.data(), ci.size() * 8, cudaMemcpyHostToDevice);
+        } else {
+            cudaMemcpy(dfwd, tf.data(), tf.size() * 8, cudaMemcpyHostToDevice);
+            cudaMemcpy(dinv, ti.data(), ti.size() * 8, cudaMemcpyHostToDevice);
+        }
         ModInfo m;
         std::memset(&m, 0, sizeof(m));
         m.q = q;
@@ -462,6 +485,7 @@ edl_status edl_ctx_set_stream(edl_ctx* c, void* stream) {
 
 const char* edl_last_error(const edl_ctx* c) { return c ? c->err.c_str() : "null context"; }
 int64_t edl_launch_count(const edl_ctx* c) { return c ? c->prof.launches : 0; }
+uint64_t edl_key_id(const edl_ctx* c) { return (c && c->has_key) ? c->key_id : 0; }
 
 edl_status edl_profile(edl_ctx* c, int32_t enable) {
     if (!c) return EDL_ERR_ARG;
@@ -516,10 +540,18 @@ edl_status edl_keygen(edl_ctx* c, uint64_t seed) {
             cudaMalloc(&c->d_rlk_s, (size_t)(c->L + 1) * 2 * nm * N * 8) != cudaSuccess)
             return fail(c, EDL_ERR_CUDA, "keygen: out of device memory");
     }
+    // Galois keys belong to the previous secret: drop them (edl_galois_keygen regenerates)
+    cudaStreamSynchronize(c->st);
+    for (auto& kv : c->gkeys) {
+        cudaFree(kv.second.first);
+        cudaFree(kv.second.second);
+    }
+    c->gkeys.clear();
     launch_keygen(c->dev(), seed, c->d_s, c->d_pk, c->d_rlk, c->d_rlk_s, nullptr);
     if (cudaStreamSynchronize(c->st) != cudaSuccess) return cuda_check(c, "keygen");
     c->has_key = true;
-    c->key_id = seed;
+    c->key_id = host::key_identifier(seed);
+    c->sk_seed = seed;
     return cuda_check(c, "keygen");
 }
 
@@ -551,7 +583,9 @@ edl_status edl_encrypt_poly_sk(edl_ctx* c, const int64_t* poly, int64_t n_vec, i
     if (!c->has_key) return fail(c, EDL_ERR_NOKEY, "encrypt_sk: no key");
     if (level < 0 || level > c->L) return fail(c, EDL_ERR_LEVEL, "encrypt_sk: level out of range");
     if (!out->data && n_vec > 0) return fail(c, EDL_ERR_ARG, "encrypt_sk: null output");
-    if (n_vec > 0) launch_encrypt_sk(c->dev(), poly, n_vec, level, enc_seed, obj0, c->d_s, out->data);
+    if (n_vec > 0)
+        launch_encrypt_sk(c->dev(), poly, n_vec, level, enc_seed, host::sk_error_key(c->sk_seed, enc_seed), obj0, c->d_s,
+                          out->data);
     set_meta(out, n_vec, level, scale, c->key_id);
     return cuda_check(c, "encrypt_sk");
 }
@@ -641,6 +675,7 @@ edl_status edl_decrypt_device(edl_ctx* c, const edl_cts* in, double* slots_out, 
         tab[2 * nl + i] = m64;
     }
     const uint64_t* dtab = upload(c, tab);
+    if (!dtab) return fail(c, EDL_ERR_CAPACITY, "CapacityError: constant table exceeds the staging ring");
     const size_t words = (size_t)in->count * nl * c->N;
     uint64_t* res = scratch(c, words + fft_scratch_bytes(in->count, c->logn) / 8);
     if (!res) return fail(c, EDL_ERR_CUDA, "decrypt_device: scratch");
@@ -674,6 +709,7 @@ edl_status edl_ct_pt_mul(edl_ctx* c, const edl_cts* a, const double* w, double p
     for (int64_t k = 0; k < a->count; k++) ints[k] = const_int(w[k], pt_scale);
     if (a->count > 0) {
         const ulonglong2* dw = upload(c, shoup_consts(c, ints, a->level));
+        if (!dw) return fail(c, EDL_ERR_CAPACITY, "CapacityError: constant table exceeds the staging ring");
         launch_mul_const(c->dev(), a->data, a->count, a->level, dw, out->data);
     }
     set_meta(out, a->count, a->level, a->scale * pt_scale, a->key_id);
@@ -688,6 +724,7 @@ edl_status edl_ct_pt_add(edl_ctx* c, const edl_cts* a, const double* cst, edl_ct
     for (int64_t k = 0; k < a->count; k++) ints[k] = const_int(cst[k], a->scale);
     if (a->count > 0) {
         const uint64_t* dk = upload(c, residues(c, ints, a->level + 1));
+        if (!dk) return fail(c, EDL_ERR_CAPACITY, "CapacityError: constant table exceeds the staging ring");
         launch_add_const(c->dev(), a->data, a->count, a->level, dk, out->data);
     }
     set_meta(out, a->count, a->level, a->scale, a->key_id);
@@ -780,11 +817,13 @@ edl_status edl_cross_correlate(edl_ctx* c, const edl_cts* x, int32_t H, int32_t 
     if (!acc) return fail(c, EDL_ERR_CUDA, "cross_correlate: scratch");
     uint64_t* r = acc + ct_words(c, cnt, l);
     const ulonglong2* dw = upload(c, residue_pairs(c, wi, l + 1));
+    if (!dw) return fail(c, EDL_ERR_CAPACITY, "CapacityError: constant table exceeds the staging ring");
     const uint64_t* db = nullptr;
     if (bias) {
         std::vector<int64_t> bi(cnt);
         for (int64_t o = 0; o < cnt; o++) bi[o] = const_int(bias[o / (Ho * Wo)], s_after);
         db = upload(c, residues(c, bi, l));
+        if (!db) return fail(c, EDL_ERR_CAPACITY, "CapacityError: constant table exceeds the staging ring");
     }
     Dev d = c->dev();
     launch_cc_mac(d, x->data, l, H, W, F, kh, kw, stride, dw, acc);
@@ -808,7 +847,7 @@ edl_status edl_dense(edl_ctx* c, const edl_cts* x, const double* Wt, const doubl
     std::vector<int64_t> wi((size_t)O * K);
     for (size_t t = 0; t < wi.size(); t++) wi[t] = const_int(Wt[t], pt_scale);
     const ulonglong2* dw = upload(c, residue_pairs(c, wi, l + 1));
-    if (!dw) return fail(c, EDL_ERR_ARG, "dense: weight table too large");
+    if (!dw) return fail(c, EDL_ERR_CAPACITY, "CapacityError: dense weight table exceeds the staging ring");
     Dev d = c->dev();
     const size_t part_words = (size_t)dense_split(d, K, O, l) * ct_words(c, O, l);
     if (defer_rescale) {
@@ -828,6 +867,7 @@ edl_status edl_dense(edl_ctx* c, const edl_cts* x, const double* Wt, const doubl
         std::vector<int64_t> bi(O);
         for (int o = 0; o < O; o++) bi[o] = const_int(b[o], s_after);
         db = upload(c, residues(c, bi, l));
+        if (!db) return fail(c, EDL_ERR_CAPACITY, "CapacityError: constant table exceeds the staging ring");
     }
     launch_dense_mac(d, x->data, K, O, l, dw, acc, part);
     launch_rescale_intt(d, acc, O, l, nullptr, r);
@@ -1087,6 +1127,7 @@ edl_status edl_dense_finish(edl_ctx* c, const edl_cts* acc, const double* b, edl
         std::vector<int64_t> bi(O);
         for (int64_t o = 0; o < O; o++) bi[o] = const_int(b[o], s_after);
         db = upload(c, residues(c, bi, l));
+        if (!db) return fail(c, EDL_ERR_CAPACITY, "CapacityError: constant table exceeds the staging ring");
     }
     Dev d = c->dev();
     launch_rescale_intt(d, acc->data, O, l, nullptr, r);
@@ -1123,7 +1164,9 @@ edl_status edl_poly_activation(edl_ctx* c, const edl_cts* x, const double* coeff
             if (!r) return fail(c, EDL_ERR_CUDA, "poly_activation: scratch");
             std::vector<int64_t> i1(cnt, const_int(coeffs[1], ql)), i0(cnt, const_int(coeffs[0], Su));
             const ulonglong2* w1 = upload(c, shoup_consts(c, i1, l));
+            if (!w1) return fail(c, EDL_ERR_CAPACITY, "CapacityError: constant table exceeds the staging ring");
             const uint64_t* k0 = upload(c, residues(c, i0, l));
+            if (!k0) return fail(c, EDL_ERR_CAPACITY, "CapacityError: constant table exceeds the staging ring");
             launch_rescale_intt(d, x->data, cnt, l, w1, r);
             launch_rescale_ntt(d, x->data, cnt, l, w1, r, k0, out->data);
         }
@@ -1153,8 +1196,11 @@ edl_status edl_poly_activation(edl_ctx* c, const edl_cts* x, const double* coeff
             uint64_t* rsc = r2 + (size_t)cnt * 2 * c->N;
             std::vector<int64_t> i2(cnt, const_int(c2, qlm1)), i1(cnt, const_int(c1, p1)), i0(cnt, const_int(c0, Sa));
             const ulonglong2* w2 = upload(c, shoup_consts(c, i2, l - 1));
+            if (!w2) return fail(c, EDL_ERR_CAPACITY, "CapacityError: constant table exceeds the staging ring");
             const ulonglong2* w1 = upload(c, shoup_consts(c, i1, l));
+            if (!w1) return fail(c, EDL_ERR_CAPACITY, "CapacityError: constant table exceeds the staging ring");
             const uint64_t* k0 = upload(c, residues(c, i0, l - 1));   // output level l-2: l-1 limbs
+            if (!k0) return fail(c, EDL_ERR_CAPACITY, "CapacityError: constant table exceeds the staging ring");
             relin_split(c, d, x->data, x->data, cnt, l, true, c->d_rlk, c->d_rlk_s, rsc, y2);
             launch_rescale_intt(d, y2, cnt, l - 1, w2, r);
             launch_rescale_ntt(d, y2, cnt, l - 1, w2, r, nullptr, av);
@@ -1189,8 +1235,11 @@ edl_status edl_poly_activation(edl_ctx* c, const edl_cts* x, const double* coeff
         uint64_t* rsc = r + (size_t)cnt * 2 * c->N;
         std::vector<int64_t> i3(cnt, const_int(c3, ql)), i1(cnt, const_int(c1, p1)), i0(cnt, const_int(c0, S3));
         const ulonglong2* w3 = upload(c, shoup_consts(c, i3, l));
+        if (!w3) return fail(c, EDL_ERR_CAPACITY, "CapacityError: constant table exceeds the staging ring");
         const ulonglong2* w1 = upload(c, shoup_consts(c, i1, l));
+        if (!w1) return fail(c, EDL_ERR_CAPACITY, "CapacityError: constant table exceeds the staging ring");
         const uint64_t* k0 = upload(c, residues(c, i0, l - 1));
+        if (!k0) return fail(c, EDL_ERR_CAPACITY, "CapacityError: constant table exceeds the staging ring");
         uint64_t* r2 = rsc + rs;   // second INTT output
         // 2.+4. (independent of 1.) run on the side stream, overlapping 1.'s tails and its
         // memory-light phases; 3. joins them

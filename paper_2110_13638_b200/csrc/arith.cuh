@@ -18,8 +18,8 @@ struct ModInfo {
     uint64_t r_hi;     // floor(2^128 / q), high word
     uint64_t two64;    // 2^64 mod q
     uint64_t two64_s;  // Shoup companion of two64
-    const ulonglong2* tw_fwd;   // [N] {psi^brv(k), shoup}
-    const ulonglong2* tw_inv;   // [N] {psi^-brv(k), shoup}
+    const ulonglong2* tw_fwd;   // [N] {psi^brv(k), shoup}; fp == 2: [N] binary64 psi^brv(k) (8 bytes each)
+    const ulonglong2* tw_inv;   // [N] {psi^-brv(k), shoup}; fp == 2: [N] binary64 (8 bytes each)
     uint64_t ninv, ninv_s;      // N^-1 mod q and Shoup companion
     uint64_t w1ninv, w1ninv_s;  // psi^-brv(1) * N^-1 (last INTT stage), Shoup companion
     uint64_t one_s;             // floor(2^64 / q): Shoup companion of 1 (64-bit reduction)
@@ -152,6 +152,19 @@ __device__ __forceinline__ double f64_mulc(double b, double w, double wq, double
     const double hi = __dmul_rn(b, w);
     const double lo = __fma_rn(b, w, -hi);
     const double qt = __dsub_rn(__fma_rn(b, wq, F64_RND), F64_RND);
+    return __dadd_rn(__fma_rn(-qt, q, hi), lo);
+}
+// Twiddle product without a companion (the NTT butterflies, round 2): b w mod q with the
+// quotient taken from the rounded product, qt = rint(RN(b w) RN(1/q)).  For q < 2^44,
+// w < q and |b| < 64 q: |RN(b w) - b w| <= 2^-53 |b w| <= 64 q^2 2^-53 and the quotient
+// estimate is off from b w / q by at most 64 q 2^-53 + |b w/q| 2^-53 < 0.13, so
+// |b w - qt q| <= 0.63 q; hi - qt q is an integer below 2^53 (exact in the FMA) and lo is
+// the exact product error.  Same 6 FP64 instructions as f64_mulc, but a twiddle is 8 bytes
+// (w only) instead of 16: half the twiddle traffic / shared memory.
+__device__ __forceinline__ double f64_mult(double b, double w, double q, double qinv) {
+    const double hi = __dmul_rn(b, w);
+    const double lo = __fma_rn(b, w, -hi);
+    const double qt = __dsub_rn(__fma_rn(hi, qinv, 6755399441055744.0), 6755399441055744.0);
     return __dadd_rn(__fma_rn(-qt, q, hi), lo);
 }
 // v mod q in [-0.51 q, 0.51 q] for |v| < 2^50 (qinv = RN(1/q))

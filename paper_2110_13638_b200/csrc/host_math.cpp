@@ -61,7 +61,7 @@ bool select_primes(const int* bits, int n_bits, int logn, uint64_t* out) {
     const uint64_t two_n = 2ull << logn;
     for (int k = 0; k < n_bits; k++) {
         const int b = bits[k];
-        if (b < 2 || b > 61) return false;
+        if (b < 2 || b > 60) return false;   // q < 2^60: MAC folds of 256 full products stay below 2^128
         const uint64_t top = (b == 64) ? ~0ull : ((1ull << b) - 1);
         uint64_t cand = top / two_n * two_n + 1;
         while (true) {
@@ -73,6 +73,92 @@ bool select_primes(const int* bits, int n_bits, int logn, uint64_t* out) {
         out[k] = cand;
     }
     return true;
+}
+
+// Philox4x32-10 (Salmon et al. 2011), host copy of the device generator (rng_kernels.cuh).
+void philox4x32_10(const uint32_t ctr[4], uint64_t key, uint32_t out[4]) {
+    uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+    uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
+    for (int r = 0; r < 10; r++) {
+        if (r > 0) {
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c0, p1 = (uint64_t)0xCD9E8D57u * c2;
+        const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0, n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+        c0 = n0;
+        c1 = (uint32_t)p1;
+        c2 = n2;
+        c3 = (uint32_t)p0;
+    }
+    out[0] = c0;
+    out[1] = c1;
+    out[2] = c2;
+    out[3] = c3;
+}
+
+uint64_t sk_error_key(uint64_t sk_seed, uint64_t enc_seed) {
+    const uint32_t ctr[4] = {(uint32_t)enc_seed, (uint32_t)(enc_seed >> 32), 0u, 13u};
+    uint32_t w[4];
+    philox4x32_10(ctr, sk_seed, w);
+    return (uint64_t)w[0] | ((uint64_t)w[1] << 32);
+}
+
+// SHA-256 (FIPS 180-4) of a short message, for key identifiers.
+static void sha256(const uint8_t* msg, size_t len, uint8_t out[32]) {
+    static const uint32_t K[64] = {
+        0x428a2f98, 0x71374491, 0xb5c0fbcf, 0xe9b5dba5, 0x3956c25b, 0x59f111f1, 0x923f82a4, 0xab1c5ed5, 0xd807aa98,
+        0x12835b01, 0x243185be, 0x550c7dc3, 0x72be5d74, 0x80deb1fe, 0x9bdc06a7, 0xc19bf174, 0xe49b69c1, 0xefbe4786,
+        0x0fc19dc6, 0x240ca1cc, 0x2de92c6f, 0x4a7484aa, 0x5cb0a9dc, 0x76f988da, 0x983e5152, 0xa831c66d, 0xb00327c8,
+        0xbf597fc7, 0xc6e00bf3, 0xd5a79147, 0x06ca6351, 0x14292967, 0x27b70a85, 0x2e1b2138, 0x4d2c6dfc, 0x53380d13,
+        0x650a7354, 0x766a0abb, 0x81c2c92e, 0x92722c85, 0xa2bfe8a1, 0xa81a664b, 0xc24b8b70, 0xc76c51a3, 0xd192e819,
+        0xd6990624, 0xf40e3585, 0x106aa070, 0x19a4c116, 0x1e376c08, 0x2748774c, 0x34b0bcb5, 0x391c0cb3, 0x4ed8aa4a,
+        0x5b9cca4f, 0x682e6ff3, 0x748f82ee, 0x78a5636f, 0x84c87814, 0x8cc70208, 0x90befffa, 0xa4506ceb, 0xbef9a3f7,
+        0xc67178f2};
+    uint32_t h[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a, 0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
+    std::vector<uint8_t> m(msg, msg + len);
+    m.push_back(0x80);
+    while (m.size() % 64 != 56) m.push_back(0);
+    const uint64_t bits = (uint64_t)len * 8;
+    for (int k = 7; k >= 0; k--) m.push_back((uint8_t)(bits >> (8 * k)));
+    auto rotr = [](uint32_t x, int n) { return (x >> n) | (x << (32 - n)); };
+    for (size_t blk = 0; blk < m.size(); blk += 64) {
+        uint32_t w[64];
+        for (int t = 0; t < 16; t++)
+            w[t] = ((uint32_t)m[blk + 4 * t] << 24) | ((uint32_t)m[blk + 4 * t + 1] << 16) |
+                   ((uint32_t)m[blk + 4 * t + 2] << 8) | m[blk + 4 * t + 3];
+        for (int t = 16; t < 64; t++) {
+            const uint32_t s0 = rotr(w[t - 15], 7) ^ rotr(w[t - 15], 18) ^ (w[t - 15] >> 3);
+            const uint32_t s1 = rotr(w[t - 2], 17) ^ rotr(w[t - 2], 19) ^ (w[t - 2] >> 10);
+            w[t] = w[t - 16] + s0 + w[t - 7] + s1;
+        }
+        uint32_t a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], hh = h[7];
+        for (int t = 0; t < 64; t++) {
+            const uint32_t t1 = hh + (rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25)) + ((e & f) ^ (~e & g)) + K[t] + w[t];
+            const uint32_t t2 = (rotr(a, 2) ^ rotr(a, 13) ^ rotr(a, 22)) + ((a & b) ^ (a & c) ^ (b & c));
+            hh = g;
+            g = f;
+            f = e;
+            e = d + t1;
+            d = c;
+            c = b;
+            b = a;
+            a = t1 + t2;
+        }
+        h[0] += a; h[1] += b; h[2] += c; h[3] += d; h[4] += e; h[5] += f; h[6] += g; h[7] += hh;
+    }
+    for (int k = 0; k < 8; k++)
+        for (int j = 0; j < 4; j++) out[4 * k + j] = (uint8_t)(h[k] >> (24 - 8 * j));
+}
+
+uint64_t key_identifier(uint64_t seed) {
+    uint8_t msg[16] = {'e', 'd', 'l', '-', 'k', 'e', 'y', '\0'};
+    for (int k = 0; k < 8; k++) msg[8 + k] = (uint8_t)(seed >> (8 * k));
+    uint8_t d[32];
+    sha256(msg, sizeof(msg), d);
+    uint64_t id = 0;
+    for (int k = 0; k < 8; k++) id |= (uint64_t)d[k] << (8 * k);
+    return id ? id : 1;
 }
 
 uint64_t minimal_psi(uint64_t q, int logn) {

@@ -17,6 +17,15 @@ bool is_prime(uint64_t n);
 uint64_t shoup_companion(uint64_t w, uint64_t q);
 // O2: largest unused primes p < 2^b, p = 1 mod 2N, in chain order
 bool select_primes(const int* bits, int n_bits, int logn, uint64_t* out);
+// Philox4x32-10 (the device generator's host copy): counter ctr[4], key (lo, hi) of `key`
+void philox4x32_10(const uint32_t ctr[4], uint64_t key, uint32_t out[4]);
+// Philox key of the secret-key encryption error: PRF(secret seed, enc_seed) =
+// words 0,1 of Philox_{sk_seed}(enc_seed lo, enc_seed hi, 0, 13).  The error thus depends
+// on key material the wire never carries (c1 is the only function of enc_seed alone).
+uint64_t sk_error_key(uint64_t sk_seed, uint64_t enc_seed);
+// Public key identifier: first 8 bytes (little-endian) of SHA-256("edl-key\0" || seed le64),
+// a one-way function of the key seed (never the seed itself); never 0.
+uint64_t key_identifier(uint64_t seed);
 // O3: minimal primitive 2N-th root of unity mod q
 uint64_t minimal_psi(uint64_t q, int logn);
 // Alg. 8: returns chain bits (c+2 entries) and log2 N

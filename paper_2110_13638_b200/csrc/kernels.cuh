@@ -59,6 +59,7 @@ struct Dev {
     int L;
     cudaStream_t st;
     Prof* prof;
+    bool ks_fused = false;      // key switch: fused modulus raise + key products (k_relin_ks, N = 2^14)
 };
 
 // Supported ring degrees: 2^10 .. 2^16 (N > 2^13 runs one limb per thread-block cluster).
@@ -86,13 +87,14 @@ void ensure_smem_attr(const void* kern, int bytes);
 // C::K (consecutive blocks form one limb's cluster), block = C::T threads, dynamic shared
 // memory C::SMEM_BYTES.
 template <class C, typename... KArgs, typename... Args>
-void launch_cfg(const Dev& d, const char* name, void (*kern)(KArgs...), dim3 grid, Args... args) {
-    ensure_smem_attr((const void*)kern, C::SMEM_BYTES);
+void launch_cfg_x(const Dev& d, const char* name, void (*kern)(KArgs...), dim3 grid, int extra_smem, Args... args) {
+    const int smem = C::SMEM_BYTES + extra_smem;
+    ensure_smem_attr((const void*)kern, smem);
     grid.x *= C::K;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(C::T, 1, 1);
-    cfg.dynamicSmemBytes = C::SMEM_BYTES;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = d.st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -101,6 +103,45 @@ void launch_cfg(const Dev& d, const char* name, void (*kern)(KArgs...), dim3 gri
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = C::K > 1 ? 1 : 0;
+    d.prof->begin(name, d.st);
+    cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+    d.prof->end(d.st);
+}
+template <class C, typename... KArgs, typename... Args>
+void launch_cfg(const Dev& d, const char* name, void (*kern)(KArgs...), dim3 grid, Args... args) {
+    launch_cfg_x<C>(d, name, kern, grid, 0, args...);
+}
+
+// Persistent cluster launch: as many clusters of C::K CTAs as can be co-resident (at most
+// one per work item), block = C::T threads, dynamic shared memory = the transform buffer
+// plus the rank's twiddle table (C::M entries of 16 bytes).
+template <class C, typename... KArgs, typename... Args>
+void launch_persist(const Dev& d, const char* name, void (*kern)(KArgs...), int64_t items, Args... args) {
+    const int smem = C::SMEM_BYTES + C::M * 16;
+    ensure_smem_attr((const void*)kern, smem);
+    static thread_local std::vector<std::pair<const void*, int>> occ;
+    int ncl = 0;
+    for (auto& e : occ)
+        if (e.first == (const void*)kern) ncl = e.second;
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(C::T, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = d.st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C::K;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (ncl == 0) {
+        cfg.gridDim = dim3(C::K * 1024, 1, 1);
+        if (cudaOccupancyMaxActiveClusters(&ncl, (void*)kern, &cfg) != cudaSuccess || ncl < 1) ncl = 1;
+        occ.emplace_back((const void*)kern, ncl);
+    }
+    const int64_t g = items < ncl ? items : ncl;
+    if (g <= 0) return;
+    cfg.gridDim = dim3((unsigned)(g * C::K), 1, 1);
     d.prof->begin(name, d.st);
     cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
     d.prof->end(d.st);
@@ -140,8 +181,8 @@ template <int LOGN>
 void launch_encrypt_n(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint64_t seed, uint32_t obj0,
                       const uint64_t* pk, uint64_t* out);
 template <int LOGN>
-void launch_encrypt_sk_n(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint64_t seed, uint32_t obj0,
-                         const uint64_t* s_hat, uint64_t* out);
+void launch_encrypt_sk_n(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint64_t seed, uint64_t eseed,
+                         uint32_t obj0, const uint64_t* s_hat, uint64_t* out);
 template <int LOGN>
 void launch_keygen_galois_n(const Dev& d, uint64_t seed, uint32_t g, const uint64_t* s_hat, uint64_t* gk, uint64_t* gk_c);
 template <int LOGN>
@@ -237,8 +278,8 @@ void launch_keygen(const Dev& d, uint64_t seed, uint64_t* s_hat /*[L+2][N]*/, ui
 void launch_encrypt(const Dev& d, const int64_t* msg /*[cnt][N]*/, int64_t cnt, int l, uint64_t seed, uint32_t obj0,
                     const uint64_t* pk, uint64_t* out);
 // secret-key encryption (reading Z16) and the server-side regeneration of its seeded c1
-void launch_encrypt_sk(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint64_t seed, uint32_t obj0,
-                       const uint64_t* s_hat, uint64_t* out);
+void launch_encrypt_sk(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint64_t seed, uint64_t eseed,
+                       uint32_t obj0, const uint64_t* s_hat, uint64_t* out);
 void launch_expand_sk_a(const Dev& d, uint64_t* ct, int64_t cnt, int l, uint64_t seed, uint32_t obj0);
 // m_hat = c0 + c1 s, INTT -> coefficient residues [cnt][l+1][N]
 void launch_decrypt(const Dev& d, const uint64_t* ct, int64_t cnt, int l, const uint64_t* s_hat, uint64_t* out);

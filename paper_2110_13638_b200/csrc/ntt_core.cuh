@@ -143,14 +143,27 @@ __device__ __forceinline__ void mbar_init_cluster(uint32_t mbar) {
 __device__ __forceinline__ void mbar_expect(uint32_t mbar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void mbar_wait0(uint32_t mbar) {   // phase 0 of a fresh mbarrier
+// Phase 0 of a fresh mbarrier.  The bytes it counts arrive by st.async into this CTA's own
+// shared memory, which the mbarrier's complete-tx makes visible at CTA scope: no
+// cluster-scope acquire, so ptxas emits no L1 invalidation (CCTL.IVALL) here -- the
+// round-2 ncu showed that invalidation at 2-4 % of stall samples, and it evicted the
+// L1-cached twiddles after every exchange.  (EDL_MBAR_CLUSTER_ACQUIRE restores it.)
+__device__ __forceinline__ void mbar_wait0(uint32_t mbar) {
     uint32_t done;
     do {
+#ifdef EDL_MBAR_CLUSTER_ACQUIRE
         asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], 0;\n\t"
                      "selp.u32 %0, 1, 0, p;\n\t}"
                      : "=r"(done)
                      : "r"(mbar)
                      : "memory");
+#else
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], 0;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(done)
+                     : "r"(mbar)
+                     : "memory");
+#endif
     } while (!done);
 }
 __device__ __forceinline__ void mbar_inval(uint32_t mbar) { asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(mbar) : "memory"); }
@@ -177,10 +190,10 @@ __device__ __forceinline__ uint64_t* cluster_smem(uint64_t* sm, int rank) {
 // butterflies/s register-only vs 1.26 T for the integer FP64-quotient path).
 template <bool FP>
 __device__ __forceinline__ void ct_bfly(uint64_t& X, uint64_t& Y, ulonglong2 w, uint64_t q, uint64_t two_q,
-                                        double qd = 0.0) {
-    if constexpr (FP) {
+                                        double qd = 0.0, double qinv = 0.0) {
+    if constexpr (FP) {   // twiddle = w only (f64_mult: no companion)
         const double x = f64_of(X);
-        const double t = f64_mulc(f64_of(Y), f64_of(w.x), f64_of(w.y), qd);
+        const double t = f64_mult(f64_of(Y), f64_of(w.x), qd, qinv);
         X = bits_of(__dadd_rn(x, t));
         Y = bits_of(__dsub_rn(x, t));
     } else {
@@ -198,12 +211,34 @@ __device__ __forceinline__ void gs_bfly(uint64_t& X, uint64_t& Y, uint64_t w, ui
     Y = shoup_lazy2(x - y + two_q, w, ws, q);
 }
 
+// Twiddle accessors: the global table (read-only path), or a CTA's shared-memory copy of
+// the entries its stages use (persistent kernels, ntt_persist.cuh).
+struct GlobTw {
+    const ulonglong2* __restrict__ t;
+    __device__ __forceinline__ ulonglong2 operator()(int i) const { return __ldg(t + i); }
+};
+struct SmemTw {
+    const ulonglong2* t;
+    __device__ __forceinline__ ulonglong2 operator()(int i) const { return t[i]; }
+};
+// F64-pipe primes (ModInfo::fp == 2) keep compact tables of 8-byte twiddles (binary64 w;
+// the f64_mult butterflies need no companion): half the twiddle bytes and L1 footprint.
+struct GlobTw8 {
+    const uint64_t* __restrict__ t;
+    __device__ __forceinline__ ulonglong2 operator()(int i) const { return make_ulonglong2(__ldg(t + i), 0); }
+};
+template <bool FP>
+__device__ __forceinline__ auto glob_tw(const ulonglong2* t) {
+    if constexpr (FP) return GlobTw8{reinterpret_cast<const uint64_t*>(t)};
+    else return GlobTw{t};
+}
+
 // NS forward stages on a group x[0..2^NS) held in registers; absolute stage SA + k uses
 // twiddle index 2^(SA+k) + (high << k) + (r >> (NS-k)), `high` = the group's index bits
 // above the stage window (SURVEY O3 stage twiddle psi^brv(m+i)).
-template <int SA, int NS, bool FP>
-__device__ __forceinline__ void fwd_pass_regs(uint64_t* x, int high, const ulonglong2* __restrict__ tw, uint64_t q,
-                                              uint64_t two_q, double qd) {
+template <int SA, int NS, bool FP, class TW>
+__device__ __forceinline__ void fwd_pass_regs_t(uint64_t* x, int high, TW tw, uint64_t q, uint64_t two_q, double qd,
+                                                double qinv) {
 #pragma unroll
     for (int k = 0; k < NS; k++) {
         const int half = 1 << (NS - 1 - k);
@@ -211,13 +246,18 @@ __device__ __forceinline__ void fwd_pass_regs(uint64_t* x, int high, const ulong
         for (int r = 0; r < (1 << NS); r++) {
             if (r & half) continue;
             const int tidx = (1 << (SA + k)) + (high << k) + (r >> (NS - k));
-            ulonglong2 w = __ldg(tw + tidx);
-            ct_bfly<FP>(x[r], x[r + half], w, q, two_q, qd);
+            ulonglong2 w = tw(tidx);
+            ct_bfly<FP>(x[r], x[r + half], w, q, two_q, qd, qinv);
         }
 #ifdef EDL_STAGE_FENCE
         asm volatile("" ::: "memory");
 #endif
     }
+}
+template <int SA, int NS, bool FP>
+__device__ __forceinline__ void fwd_pass_regs(uint64_t* x, int high, const ulonglong2* __restrict__ tw, uint64_t q,
+                                              uint64_t two_q, double qd, double qinv) {
+    fwd_pass_regs_t<SA, NS, FP>(x, high, glob_tw<FP>(tw), q, two_q, qd, qinv);
 }
 
 // NS inverse stages, last to first; with LAST the absolute stage 0 folds N^-1 into both
@@ -225,8 +265,8 @@ __device__ __forceinline__ void fwd_pass_regs(uint64_t* x, int high, const ulong
 // f64_mulc (|.| <= 0.625 q) and the sums of the pass's last stage are reduced, so every
 // pass starts from |x| < 2q (first pass: loads in [0, 2q)) and grows to at most
 // 2q 2^NS <= 64 q < 2^50 inside it.
-template <int SA, int NS, bool LAST, bool FP>
-__device__ __forceinline__ void inv_pass_regs(uint64_t* x, int high, const ModInfo& m, uint64_t two_q) {
+template <int SA, int NS, bool LAST, bool FP, class TW>
+__device__ __forceinline__ void inv_pass_regs_t(uint64_t* x, int high, const ModInfo& m, uint64_t two_q, TW tw) {
     double qd = 0.0;
     if constexpr (FP) qd = u52_to_double(m.q);
 #pragma unroll
@@ -242,11 +282,11 @@ __device__ __forceinline__ void inv_pass_regs(uint64_t* x, int high, const ModIn
                     x[r + half] = bits_of(f64_mulc(__dsub_rn(a, b), u52_to_double(m.w1ninv), f64_of(m.w1ninv_s), qd));
                 } else {
                     const int tidx = (1 << (SA + k)) + (high << k) + (r >> (NS - k));
-                    const ulonglong2 w = __ldg(m.tw_inv + tidx);
+                    const ulonglong2 w = tw(tidx);
                     double s = __dadd_rn(a, b);
                     if (k == 0) s = f64_reduce(s, qd, m.qinv_d);
                     x[r] = bits_of(s);
-                    x[r + half] = bits_of(f64_mulc(__dsub_rn(a, b), f64_of(w.x), f64_of(w.y), qd));
+                    x[r + half] = bits_of(f64_mult(__dsub_rn(a, b), f64_of(w.x), qd, m.qinv_d));
                 }
             } else if (LAST && SA + k == 0) {
                 uint64_t a = x[r], b = x[r + half];
@@ -256,7 +296,7 @@ __device__ __forceinline__ void inv_pass_regs(uint64_t* x, int high, const ModIn
                                    : shoup_lazy2(a - b + two_q, m.w1ninv, m.w1ninv_s, m.q);
             } else {
                 const int tidx = (1 << (SA + k)) + (high << k) + (r >> (NS - k));
-                ulonglong2 w = __ldg(m.tw_inv + tidx);
+                ulonglong2 w = tw(tidx);
                 gs_bfly(x[r], x[r + half], w.x, w.y, m.q, two_q);
             }
         }
@@ -264,6 +304,10 @@ __device__ __forceinline__ void inv_pass_regs(uint64_t* x, int high, const ModIn
         asm volatile("" ::: "memory");
 #endif
     }
+}
+template <int SA, int NS, bool LAST, bool FP>
+__device__ __forceinline__ void inv_pass_regs(uint64_t* x, int high, const ModInfo& m, uint64_t two_q) {
+    inv_pass_regs_t<SA, NS, LAST, FP>(x, high, m, two_q, glob_tw<FP>(m.tw_inv));
 }
 
 // A forward-transform epilogue may take the F64 path's outputs before canonicalisation:
@@ -309,7 +353,7 @@ __device__ __forceinline__ void pass_smem(uint64_t* sm, const ModInfo& m, uint64
         const int v = threadIdx.x + g * C::T;
         const int high = hc | (v >> PI::BLOW);
         if constexpr (INV) inv_pass_regs<PI::SA, PI::NS, false, FP>(x + g * (1 << PI::NS), high, m, two_q);
-        else fwd_pass_regs<PI::SA, PI::NS, FP>(x + g * (1 << PI::NS), high, m.tw_fwd, m.q, two_q, u52_to_double(m.q));
+        else fwd_pass_regs<PI::SA, PI::NS, FP>(x + g * (1 << PI::NS), high, m.tw_fwd, m.q, two_q, u52_to_double(m.q), m.qinv_d);
     }
 #pragma unroll
     for (int g = 0; g < PI::G; g++) {
@@ -380,7 +424,7 @@ __device__ __forceinline__ void ntt_fwd_impl(uint64_t* sm, const ModInfo& m, Loa
         for (int g = 0; g < C::E / C::K; g++) {
 #pragma unroll
             for (int t = 0; t < C::K; t++) x[g * C::K + t] = ld(j0 + g * C::T + t * C::M);
-            fwd_pass_regs<0, C::LOGK, FP>(x + g * C::K, 0, m.tw_fwd, q, two_q, qd);
+            fwd_pass_regs<0, C::LOGK, FP>(x + g * C::K, 0, m.tw_fwd, q, two_q, qd, m.qinv_d);
         }
 #ifndef EDL_FULL_CLUSTER_SYNC
         cluster_wait();       // every CTA is running and done with its shared memory
@@ -415,7 +459,7 @@ __device__ __forceinline__ void ntt_fwd_impl(uint64_t* sm, const ModInfo& m, Loa
 #pragma unroll
         for (int r = 0; r < C::E; r++) x[r] = sm[spad(tid + r * C::T)];
     }
-    fwd_pass_regs<C::LOGK, C::LOGE, FP>(x, C::crank(), m.tw_fwd, q, two_q, qd);
+    fwd_pass_regs<C::LOGK, C::LOGE, FP>(x, C::crank(), m.tw_fwd, q, two_q, qd, m.qinv_d);
 #pragma unroll
     for (int r = 0; r < C::E; r++) sm[spad(tid + r * C::T)] = x[r];
     __syncthreads();

@@ -6,6 +6,7 @@
 #include <type_traits>
 #include "kernels.cuh"
 #include "ntt_core.cuh"
+#include "ntt_persist.cuh"
 
 namespace edl {
 
@@ -25,6 +26,75 @@ k_ntt_limbs(uint64_t* __restrict__ data, int nl, const __grid_constant__ PrimeMa
     auto st = [&](int idx, uint64_t v) { p[idx] = v; };
     if constexpr (INV) ntt_inv<C>(sm, m, ld, st);
     else ntt_fwd<C>(sm, m, ld, st);
+}
+
+// Persistent variant (ntt_persist.cuh): items = (limb j, batch b), prime-major, item
+// cl + k * nclusters for cluster cl; the next item's residues are fetched into registers
+// before the current item's butterflies.
+template <class C, bool INV>
+__global__ void __launch_bounds__(C::T, C::MINB)
+k_ntt_limbs_p(uint64_t* __restrict__ data, int64_t batch, int nl, const __grid_constant__ PrimeMap pm,
+              const __grid_constant__ ModTable mods) {
+    extern __shared__ __align__(16) uint64_t sm[];
+    ulonglong2* tws = reinterpret_cast<ulonglong2*>(sm + C::SMEM_WORDS);
+    __shared__ alignas(8) uint64_t mbar;
+    const uint32_t mb = smem_u32(&mbar);
+    const int64_t nitems = batch * nl;
+    const int64_t ncl = gridDim.x >> C::LOGK;
+    const int tid = threadIdx.x;
+    auto fetch = [&](int64_t item, uint64_t* dst) {
+        const int limb = (int)(item / batch);
+        const int64_t b = item - (int64_t)limb * batch;
+        const uint64_t* p = data + (((size_t)b * nl + limb) << C::LOGN);
+        if constexpr (!INV) {
+            const int j0 = C::crank() * (C::M / C::K) + tid;
+#pragma unroll
+            for (int g = 0; g < C::E / C::K; g++)
+#pragma unroll
+                for (int t = 0; t < C::K; t++) dst[g * C::K + t] = p[j0 + g * C::T + t * C::M];
+        } else {
+#pragma unroll
+            for (int r = 0; r < C::E; r++) dst[r] = p[C::idx(r)];
+        }
+    };
+    uint64_t xn[C::E];
+    int cur = -1;
+    int64_t item = C::bx();
+    if (item < nitems) fetch(item, xn);
+    for (; item < nitems; item += ncl) {
+        const int limb = (int)(item / batch);
+        const int64_t b = item - (int64_t)limb * batch;
+        const int pi = pm.idx[limb];
+        const ModInfo& m = mods[pi];
+        uint64_t x[C::E];
+#pragma unroll
+        for (int r = 0; r < C::E; r++) x[r] = xn[r];
+        if (item + ncl < nitems) fetch(item + ncl, xn);
+        if (pi != cur) {   // uniform: the whole cluster works on one item
+            __syncthreads();
+            load_tw_smem<C>(tws, INV ? m.tw_inv : m.tw_fwd, m.fp == 2);
+            __syncthreads();
+            cur = pi;
+        }
+        uint64_t* p = data + (((size_t)b * nl + limb) << C::LOGN);
+        auto st = [&](int idx, uint64_t v) { p[idx] = v; };
+        if constexpr (!INV) item_open(mb);
+#ifndef EDL_P_ONLY_INT
+        if (m.fp == 2) {
+#else
+        if (false) {
+#endif
+#pragma unroll
+            for (int r = 0; r < C::E; r++) x[r] = f64_from_u(x[r]);
+            if constexpr (INV) pinv<C, true>(sm, m, tws, x, mb, st);
+            else pfwd<C, true>(sm, m, tws, x, mb, st);
+        } else {
+#ifndef EDL_P_ONLY_FP
+            if constexpr (INV) pinv<C, false>(sm, m, tws, x, mb, st);
+            else pfwd<C, false>(sm, m, tws, x, mb, st);
+#endif
+        }
+    }
 }
 
 // ------------------------------------------------------------------------------------
@@ -223,6 +293,133 @@ k_relin_modup(const uint64_t* __restrict__ acoef, int l, int L, uint64_t* __rest
     ntt_fwd<C>(sm, m, ld, st);
 }
 
+// M2 fused (round 2): modulus raise and key products in ONE pass, target-major.  CTA
+// (cluster) = (ciphertext c, target ti); for every digit j != ti it runs
+// x_{j,t} = NTT_t(acoef_j mod t) and accumulates x_{j,t} rlk_j[cc][t] (cc = 0, 1) in its
+// epilogue into accumulators the thread keeps in shared memory (its own E slots per
+// component, no synchronisation); the raised digits never reach HBM.  After the digits,
+// for data targets the t == j term d2_t rlk_t[cc][t] (d2 = a1 b1, NTT domain), the
+// tensor's d0 = a0 b0, d1 = a0 b1 + a1 b0 and the P^-1 fold give v_cc = d_cc + acc_cc P^-1;
+// for P the accumulators themselves are stored -- exactly k_relin_mac's output layout
+// [cnt][2][l+2][N], so the mod-down kernels are unchanged.
+// Arithmetic: F64 targets (q < 2^44) f64_mult products (no key companion) of the
+// transform's unreduced binary64 outputs, summed exactly in binary64 (<= l+2 terms of
+// |.| <= 0.63 q); other targets Shoup products with the key companion in [0, 2q) summed
+// lazily in uint64 ((l + 2) 2 q < 2^64 for q < 2^60, l <= 5) and reduced once.
+template <class C>
+__global__ void __launch_bounds__(C::T, C::MINB)
+k_relin_ks(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l, int L,
+           const uint64_t* __restrict__ acoef, const uint64_t* __restrict__ rlk, const uint64_t* __restrict__ rlk_c,
+           uint64_t* __restrict__ acc_out, const __grid_constant__ ModTable mods, const ChainConsts* __restrict__ cc) {
+    extern __shared__ __align__(16) uint64_t sm[];
+    uint64_t* accs = sm + C::SMEM_WORDS;   // [2][E][T]: slot of output C::idx(r) = r T + tid
+    const int ti = blockIdx.y;              // 0..l data targets, l+1 = P
+    const int t = (ti == l + 1) ? (L + 1) : ti;
+    const int64_t c = C::bx();
+    const ModInfo& m = mods[t];
+    const bool f64 = m.fp == 2;            // uniform per CTA
+    const int tid = threadIdx.x;
+    const size_t limb_n = (size_t)1 << C::LOGN;
+#pragma unroll
+    for (int r = 0; r < C::E; r++) {
+        accs[r * C::T + tid] = 0;   // binary64 +0 and integer 0 share the bit pattern
+        accs[(C::E + r) * C::T + tid] = 0;
+    }
+    const uint64_t qd_bits = bits_of(u52_to_double(m.q));
+    for (int j = 0; j <= l; j++) {
+        if (j == ti) continue;
+        const uint64_t* src = acoef + (((size_t)c * (l + 1) + j) << C::LOGN);
+        const uint64_t* k0 = rlk + ((((size_t)j * 2 + 0) * (L + 2) + t) << C::LOGN);
+        const uint64_t* k1 = rlk + ((((size_t)j * 2 + 1) * (L + 2) + t) << C::LOGN);
+        const uint64_t* k0c = rlk_c + ((((size_t)j * 2 + 0) * (L + 2) + t) << C::LOGN);
+        const uint64_t* k1c = rlk_c + ((((size_t)j * 2 + 1) * (L + 2) + t) << C::LOGN);
+        const bool need_red = mods[j].q > 4 * m.q;   // the forward NTT accepts [0, 4q)
+        auto ld = [&](int idx) {
+            uint64_t v = src[idx];
+            return need_red ? reduce64(v, m) : v;
+        };
+        struct Store {
+            uint64_t* accs;
+            const uint64_t *k0, *k1, *k0c, *k1c;
+            const ModInfo& m;
+            uint64_t qd_bits;
+            int base;
+            __device__ __forceinline__ int slot(int idx) const { return idx - base; }   // r T + tid
+            __device__ __forceinline__ void operator()(int idx, uint64_t x, int) const {   // Shoup targets
+                const int s = slot(idx);
+                const uint64_t p0 = shoup_lazy2(x, __ldg(k0 + idx), __ldg(k0c + idx), m.q);
+                const uint64_t p1 = shoup_lazy2(x, __ldg(k1 + idx), __ldg(k1c + idx), m.q);
+                accs[s] += p0;
+                accs[C::E * C::T + s] += p1;
+            }
+            __device__ __forceinline__ void f64(int idx, double x, int) const {   // F64 targets
+                const int s = slot(idx);
+                const double qd = f64_of(qd_bits);
+                const double p0 = f64_mult(x, u52_to_double(__ldg(k0 + idx)), qd, m.qinv_d);
+                const double p1 = f64_mult(x, u52_to_double(__ldg(k1 + idx)), qd, m.qinv_d);
+                accs[s] = bits_of(__dadd_rn(f64_of(accs[s]), p0));
+                accs[C::E * C::T + s] = bits_of(__dadd_rn(f64_of(accs[C::E * C::T + s]), p1));
+            }
+        };
+        ntt_fwd<C>(sm, m, ld, NoPre(), Store{accs, k0, k1, k0c, k1c, m, qd_bits, C::crank() * C::M});
+    }
+    // final: data targets add d2_t rlk_t (the j == t digit needs no transform) and fold the
+    // tensor's d0, d1 with P^-1; P stores the reduced accumulators
+    const double qd = u52_to_double(m.q);
+    const ulonglong2 pinv = (ti <= l) ? cc->qinv[L + 1][t] : make_ulonglong2(0, 0);
+    const bool single = (b == nullptr);
+    uint64_t* o0 = acc_out + ((((size_t)c * 2 + 0) * (l + 2) + ti) << C::LOGN);
+    uint64_t* o1 = acc_out + ((((size_t)c * 2 + 1) * (l + 2) + ti) << C::LOGN);
+    const uint64_t* a0 = a + limb_off(c, 0, ti <= l ? ti : 0, l + 1, C::LOGN);
+    const uint64_t* a1 = a + limb_off(c, 1, ti <= l ? ti : 0, l + 1, C::LOGN);
+    const uint64_t* b0 = single ? a0 : b + limb_off(c, 0, ti <= l ? ti : 0, l + 1, C::LOGN);
+    const uint64_t* b1 = single ? a1 : b + limb_off(c, 1, ti <= l ? ti : 0, l + 1, C::LOGN);
+    const uint64_t* kt0 = rlk + ((((size_t)(ti <= l ? ti : 0) * 2 + 0) * (L + 2) + t) << C::LOGN);
+    const uint64_t* kt1 = rlk + ((((size_t)(ti <= l ? ti : 0) * 2 + 1) * (L + 2) + t) << C::LOGN);
+    const uint64_t* kt0c = rlk_c + ((((size_t)(ti <= l ? ti : 0) * 2 + 0) * (L + 2) + t) << C::LOGN);
+    const uint64_t* kt1c = rlk_c + ((((size_t)(ti <= l ? ti : 0) * 2 + 1) * (L + 2) + t) << C::LOGN);
+    (void)limb_n;
+#pragma unroll 4
+    for (int r = 0; r < C::E; r++) {
+        const int idx = C::idx(r);
+        const uint64_t s0 = accs[r * C::T + tid], s1 = accs[(C::E + r) * C::T + tid];
+        uint64_t v0, v1;
+        if (ti > l) {   // P: reduced accumulators
+            if (f64) {
+                v0 = f64_to_canon(f64_reduce(f64_of(s0), qd, m.qinv_d), qd);
+                v1 = f64_to_canon(f64_reduce(f64_of(s1), qd, m.qinv_d), qd);
+            } else {
+                v0 = reduce64(s0, m);
+                v1 = reduce64(s1, m);
+            }
+        } else {
+            const uint64_t x0 = __ldg(a0 + idx), x1 = __ldg(a1 + idx);
+            const uint64_t y0 = single ? x0 : __ldg(b0 + idx), y1 = single ? x1 : __ldg(b1 + idx);
+            const uint64_t d2 = single ? x1 : mulmod(x1, y1, m);
+            uint64_t d0 = x0, d1 = 0;
+            if (!single) {
+                d0 = mulmod(x0, y0, m);
+                d1 = addmod(mulmod(x0, y1, m), mulmod(x1, y0, m), m.q);
+            }
+            uint64_t e0, e1;
+            if (f64) {
+                const double dd = u52_to_double(d2);
+                const double t0 = __dadd_rn(f64_of(s0), f64_mult(dd, u52_to_double(__ldg(kt0 + idx)), qd, m.qinv_d));
+                const double t1 = __dadd_rn(f64_of(s1), f64_mult(dd, u52_to_double(__ldg(kt1 + idx)), qd, m.qinv_d));
+                e0 = f64_to_canon(f64_reduce(t0, qd, m.qinv_d), qd);
+                e1 = f64_to_canon(f64_reduce(t1, qd, m.qinv_d), qd);
+            } else {
+                e0 = reduce64(s0 + shoup_lazy2(d2, __ldg(kt0 + idx), __ldg(kt0c + idx), m.q), m);
+                e1 = reduce64(s1 + shoup_lazy2(d2, __ldg(kt1 + idx), __ldg(kt1c + idx), m.q), m);
+            }
+            v0 = addmod(d0, mulc(e0, pinv, m), m.q);
+            v1 = addmod(d1, mulc(e1, pinv, m), m.q);
+        }
+        o0[idx] = v0;
+        o1[idx] = v1;
+    }
+}
+
 template <class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
 k_relin_moddown_intt(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l,
@@ -370,6 +567,14 @@ k_relin_moddown_ntt(const uint64_t* __restrict__ a, const uint64_t* __restrict__
 
 template <int LOGN>
 void launch_ntt_limbs_n(const Dev& d, uint64_t* data, int64_t batch, int nl, const PrimeMap& pm, bool inverse) {
+#ifdef EDL_NTT_PERSIST
+    if constexpr (LOGN == 14) {
+        using CP = NttCfg<14, 2, 4, 2>;
+        if (inverse) launch_persist<CP>(d, "k_ntt_limbs", k_ntt_limbs_p<CP, true>, batch * nl, data, batch, nl, pm, *d.mt);
+        else launch_persist<CP>(d, "k_ntt_limbs", k_ntt_limbs_p<CP, false>, batch * nl, data, batch, nl, pm, *d.mt);
+        return;
+    }
+#endif
     using C = CfgNttLimbs<LOGN>;   // (ntt_core.cuh: measured per degree)
     const dim3 grid((unsigned)batch, nl);
     if (inverse) launch_cfg<C>(d, "k_ntt_limbs", k_ntt_limbs<C, true>, grid, data, nl, pm, *d.mt);
@@ -401,9 +606,23 @@ void launch_relin_n(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t 
     using CP = CfgFused<LOGN>;
     const int rs = rescale ? 1 : 0;
     launch_cfg<C>(d, "k_relin_intt_d2", k_relin_intt_d2<C>, dim3((unsigned)cnt, l + 1), a, b, l, acoef, *d.mt);
-    launch_cfg<CP>(d, "k_relin_modup", k_relin_modup<CP>, dim3((unsigned)cnt, (l + 1) * (l + 1)), (const uint64_t*)acoef,
-                   l, d.L, xh, *d.mt);
-    launch_relin_mac(d, a, b, cnt, l, xh, rlk, rlk_c, acc);   // acc slots 0..l hold v
+#ifndef EDL_NO_KS_FUSED
+    if (LOGN == 14 && d.ks_fused) {
+        // fused modulus raise + key products (k_relin_ks): 2 CTAs per SM, accumulators in smem
+#ifndef EDL_KS_LOGE
+#define EDL_KS_LOGE 3
+#endif
+        using CK = NttCfg<14, 2, EDL_KS_LOGE, 2>;   // 4-CTA clusters, 2 CTAs/SM (smem accumulators)
+        launch_cfg_x<CK>(d, "k_relin_ks", k_relin_ks<CK>, dim3((unsigned)cnt, l + 2), 2 * CK::M * 8, a, b, l, d.L,
+                         (const uint64_t*)acoef, rlk, rlk_c, acc, *d.mt, d.cc);
+        (void)xh;
+    } else
+#endif
+    {
+        launch_cfg<CP>(d, "k_relin_modup", k_relin_modup<CP>, dim3((unsigned)cnt, (l + 1) * (l + 1)),
+                       (const uint64_t*)acoef, l, d.L, xh, *d.mt);
+        launch_relin_mac(d, a, b, cnt, l, xh, rlk, rlk_c, acc);   // acc slots 0..l hold v
+    }
     launch_cfg<C>(d, "k_relin_moddown_intt", k_relin_moddown_intt<C>, dim3((unsigned)cnt, 2), a, b, l, (const uint64_t*)acc,
                   d.L, rs, r, s, *d.mt, d.cc);
     launch_cfg<C>(d, "k_relin_moddown_ntt", k_relin_moddown_ntt<C>, dim3((unsigned)cnt, 2, rescale ? l : l + 1), a, b, l,

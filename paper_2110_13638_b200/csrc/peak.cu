@@ -38,12 +38,13 @@ __global__ void __launch_bounds__(256) k_bfly_peak(uint64_t q, const ulonglong2*
         if constexpr (FP) x[k] = f64_from_u(x[k]);
     }
 #pragma unroll
-    for (int k = 0; k < 8; k++) w[k] = tw[k];
+    for (int k = 0; k < 8; k++)   // F64 primes: compact binary64 table (8-byte entries)
+        w[k] = FP ? make_ulonglong2(reinterpret_cast<const uint64_t*>(tw)[k], 0) : tw[k];
     const uint64_t two_q = 2 * q;
     const double qd = u52_to_double(q);
     for (int it = 0; it < iters; it++) {
 #pragma unroll
-        for (int k = 0; k < 8; k++) ct_bfly<FP>(x[k], x[k + 8], w[k], q, two_q, qd);   // the NTT's own butterfly
+        for (int k = 0; k < 8; k++) ct_bfly<FP>(x[k], x[k + 8], w[k], q, two_q, qd, 1.0 / qd);   // the NTT's own butterfly
 #pragma unroll
         for (int k = 0; k < 8; k++) {   // pair different lanes next round
             const uint64_t tmp = x[k];

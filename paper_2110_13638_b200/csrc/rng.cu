@@ -24,9 +24,9 @@ void launch_encrypt(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint64
     EDL_DISPATCH_LOGN(d.logn, launch_encrypt_n<LOGN>(d, msg, cnt, l, seed, obj0, pk, out));
 }
 
-void launch_encrypt_sk(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint64_t seed, uint32_t obj0,
-                       const uint64_t* s_hat, uint64_t* out) {
-    EDL_DISPATCH_LOGN(d.logn, launch_encrypt_sk_n<LOGN>(d, msg, cnt, l, seed, obj0, s_hat, out));
+void launch_encrypt_sk(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint64_t seed, uint64_t eseed,
+                       uint32_t obj0, const uint64_t* s_hat, uint64_t* out) {
+    EDL_DISPATCH_LOGN(d.logn, launch_encrypt_sk_n<LOGN>(d, msg, cnt, l, seed, eseed, obj0, s_hat, out));
 }
 
 // Seeded public component of secret-key ciphertexts: c1[c][i][k] = uniform(seed, k, obj0 + c, i, TAG_SK_A).

@@ -218,11 +218,13 @@ k_encrypt(const int64_t* __restrict__ msg, int l, int L, uint64_t seed, uint32_t
 }
 
 // ---- secret-key encryption (DESIGN reading Z16): c1_i = a_i = uniform(seed, obj, i, TAG_SK_A)
-// drawn directly in the NTT domain, c0_i = NTT_i(m + e) - a_i s_i with e = CBD(TAG_SK_E).
+// drawn directly in the NTT domain, c0_i = NTT_i(m + e) - a_i s_i with e = CBD(eseed, obj,
+// TAG_SK_E), where eseed = PRF(secret seed, seed) (host::sk_error_key): only c1 is a public
+// function of the wire seed; the error needs the secret key's seed.
 template <class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
-k_encrypt_sk(const int64_t* __restrict__ msg, int l, uint64_t seed, uint32_t obj0, const uint64_t* __restrict__ s_hat,
-             uint64_t* __restrict__ out, const __grid_constant__ ModTable mods) {
+k_encrypt_sk(const int64_t* __restrict__ msg, int l, uint64_t seed, uint64_t eseed, uint32_t obj0,
+             const uint64_t* __restrict__ s_hat, uint64_t* __restrict__ out, const __grid_constant__ ModTable mods) {
     extern __shared__ uint64_t sm[];
     const int i = blockIdx.y;
     const int64_t c = C::bx();
@@ -233,7 +235,7 @@ k_encrypt_sk(const int64_t* __restrict__ msg, int l, uint64_t seed, uint32_t obj
     uint64_t* c1 = out + limb_off(c, 1, i, l + 1, C::LOGN);
     const uint64_t* s = s_hat + ((size_t)i << C::LOGN);
     auto ld = [&](int idx) {
-        return addmod(small_mod(cbd_of(draw(seed, idx, obj, 0, TAG_SK_E)), m.q), signed_mod(mm[idx], m), m.q);
+        return addmod(small_mod(cbd_of(draw(eseed, idx, obj, 0, TAG_SK_E)), m.q), signed_mod(mm[idx], m), m.q);
     };
     auto st = [&](int idx, uint64_t v) {
         const uint64_t a = uniform_of(draw(seed, idx, obj, i, TAG_SK_A), m);
@@ -278,10 +280,11 @@ void launch_encrypt_n(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint
 }
 
 template <int LOGN>
-void launch_encrypt_sk_n(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint64_t seed, uint32_t obj0,
-                         const uint64_t* s_hat, uint64_t* out) {
+void launch_encrypt_sk_n(const Dev& d, const int64_t* msg, int64_t cnt, int l, uint64_t seed, uint64_t eseed,
+                         uint32_t obj0, const uint64_t* s_hat, uint64_t* out) {
     using C = CfgFused<LOGN>;
-    launch_cfg<C>(d, "k_encrypt_sk", k_encrypt_sk<C>, dim3((unsigned)cnt, l + 1), msg, l, seed, obj0, s_hat, out, *d.mt);
+    launch_cfg<C>(d, "k_encrypt_sk", k_encrypt_sk<C>, dim3((unsigned)cnt, l + 1), msg, l, seed, eseed, obj0, s_hat, out,
+                  *d.mt);
 }
 
 template <int LOGN>
@@ -308,8 +311,8 @@ void launch_encode_pt_n(const Dev& d, const int64_t* msg, int64_t cnt, int l, ui
     template void launch_encrypt_n<LOGN>(const Dev&, const int64_t*, int64_t, int, uint64_t, uint32_t,          \
                                          const uint64_t*, uint64_t*);                                           \
     template void launch_decrypt_n<LOGN>(const Dev&, const uint64_t*, int64_t, int, const uint64_t*, uint64_t*);  \
-    template void launch_encrypt_sk_n<LOGN>(const Dev&, const int64_t*, int64_t, int, uint64_t, uint32_t,       \
-                                            const uint64_t*, uint64_t*);                                        \
+    template void launch_encrypt_sk_n<LOGN>(const Dev&, const int64_t*, int64_t, int, uint64_t, uint64_t,       \
+                                            uint32_t, const uint64_t*, uint64_t*);                              \
     template void launch_keygen_galois_n<LOGN>(const Dev&, uint64_t, uint32_t, const uint64_t*, uint64_t*, uint64_t*); \
     template void launch_encode_pt_n<LOGN>(const Dev&, const int64_t*, int64_t, int, uint64_t*);
 

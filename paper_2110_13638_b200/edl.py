@@ -109,6 +109,7 @@ _sigs = {
     "edl_ctx_set_stream": (_c.c_int32, [_c.c_void_p, _c.c_void_p]),
     "edl_last_error": (_c.c_char_p, [_c.c_void_p]),
     "edl_launch_count": (_c.c_int64, [_c.c_void_p]),
+    "edl_key_id": (_c.c_uint64, [_c.c_void_p]),
     "edl_profile": (_c.c_int32, [_c.c_void_p, _c.c_int32]),
     "edl_profile_read": (_c.c_int32, [_c.c_void_p, _c.c_char_p, _c.c_size_t, _c.c_void_p, _c.c_void_p, _c.c_int32]),
     "edl_keygen": (_c.c_int32, [_c.c_void_p, _c.c_uint64]),
@@ -293,7 +294,7 @@ class Context:
     # ---- keys / client side
     def keygen(self, seed: int):
         self._check(_lib.edl_keygen(self._h, seed), "keygen")
-        self.key_id = seed
+        self.key_id = int(_lib.edl_key_id(self._h))   # one-way in the seed (edl.h)
         return self
 
     def encode(self, slots: np.ndarray, scale: Optional[float] = None) -> np.ndarray:

@@ -80,6 +80,23 @@ def test_ntt_bit_exact(edl, logn):
     assert np.array_equal(t2.cpu().numpy().view(np.uint64).reshape(a.shape), oring.ntt_inv(a, mods, psis))
 
 
+def test_ntt_large_batch_sampled(edl):
+    """C2-sized batches (several work items per persistent cluster, ragged tail): sampled
+    polynomials of a 301-poly batch at N = 2^14 against the oracle, forward and inverse."""
+    bits = [60, 40, 40, 40, 40, 60]
+    g = edl.Context(edl.params_from_bits(14, bits))
+    po = make_params(1 << 14, bits)
+    lvl, n_polys = 4, 301
+    a = random_residues((n_polys, lvl + 1, 1 << 14), po.q[: lvl + 1] * n_polys, seed=77)
+    t = torch.from_numpy(a.view(np.int64).reshape(-1).copy()).cuda()
+    g.ntt_(t, n_polys, lvl, inverse=False)
+    got = t.cpu().numpy().view(np.uint64).reshape(a.shape)
+    for k in (0, 1, 150, 299, 300):
+        assert np.array_equal(got[k], oring.ntt_fwd(a[k], po.q[: lvl + 1], po.psi[: lvl + 1])), k
+    g.ntt_(t, n_polys, lvl, inverse=True)
+    assert np.array_equal(t.cpu().numpy().view(np.uint64).reshape(a.shape), a)
+
+
 @pytest.mark.parametrize("logn", [12, 14, 16])
 def test_ntt_prime_classes(edl, logn):
     """Every butterfly path of the NTT core against the oracle: q < 2^44 (FP64-pipe
@@ -131,6 +148,8 @@ def test_philox_words(edl, c0pair):
 @pytest.mark.parametrize("which", ["c0", "c1"])
 def test_keygen_bit_exact(which, c0pair, c1pair):
     g, o = c0pair if which == "c0" else c1pair
+    # public key identifier: SHA-256 of the seed on both sides (host C++ vs hashlib), never the seed
+    assert g.key_id == o.key_id != o.sk_seed
     assert np.array_equal(g.export_key(0), o.s_hat)
     assert np.array_equal(g.export_key(1), o.pk)
     assert np.array_equal(g.export_key(2), o.rlk)
@@ -203,6 +222,23 @@ def test_mul_relin_bit_exact(c1pair, lvl):
     got = g.mul_relin(_to_gpu(g, A.data, lvl, A.scale, o.key_id), _to_gpu(g, B.data, lvl, B.scale, o.key_id))
     want = o.mul_relin(A, B)
     assert got.scale == want.scale
+    assert np.array_equal(got.numpy(g.n), want.data)
+
+
+def test_fused_keyswitch_bit_exact(edl, monkeypatch):
+    """The fused target-major key switch (k_relin_ks, EDL_KS_FUSED=1) against the oracle:
+    mul_relin at every level of the C1 chain (16 ciphertexts: both stream halves), and the
+    sigma_a layer (two key switches, one with the fused output assembly)."""
+    monkeypatch.setenv("EDL_KS_FUSED", "1")
+    g, o = _pair(edl, depth=4)
+    for lvl in (1, 2, 3, 4):
+        A = ock.CtArray(_rand_ct(o, 16, lvl, 121 + lvl), lvl, 2.0 ** 40, o.key_id)
+        B = ock.CtArray(_rand_ct(o, 16, lvl, 131 + lvl), lvl, 2.0 ** 40, o.key_id)
+        got = g.mul_relin(_to_gpu(g, A.data, lvl, A.scale, o.key_id), _to_gpu(g, B.data, lvl, B.scale, o.key_id))
+        assert np.array_equal(got.numpy(g.n), o.mul_relin(A, B).data), lvl
+    X = ock.CtArray(_rand_ct(o, 3, 3, 141), 3, 2.0 ** 40, o.key_id)
+    got = g.poly_activation(_to_gpu(g, X.data, 3, X.scale, o.key_id), [0.5, 0.197, 0.0, -0.004])
+    want = olay.poly_activation(o, X, [0.5, 0.197, 0.0, -0.004])
     assert np.array_equal(got.numpy(g.n), want.data)
 
 
@@ -613,3 +649,13 @@ def test_device_round_trip_and_decrypt(c1pair):
     r = g.rescale(g.rescale(g.rescale(y)))                        # level 0: single-limb lift
     hd, dd = g.decrypt(r, 100), g.decrypt_device(r, 100).cpu().numpy()   # (scale ~1e-24: large values)
     assert np.max(np.abs(dd - hd) / np.maximum(1.0, np.abs(hd))) < 1e-9
+
+
+def test_keygen_drops_galois_keys(edl):
+    """a second keygen must not leave Galois keys of the old secret in place."""
+    g, o = _pair(edl, depth=2)
+    g.galois_keygen(5, [1])
+    g.keygen(3)
+    X = _rand_ct(o, 1, 2, 91)
+    with pytest.raises(edl.EdlError):
+        g.rotate(_to_gpu(g, X, 2, 2.0 ** 40, g.key_id), 1)

@@ -192,9 +192,14 @@ def test_encrypt_sk_error_identity(c0ctx):
     ct = c0ctx.encrypt_poly_sk(polys, enc_seed=9, obj0=4, scale=2.0 ** 40)
     assert ct.data.shape == (2, 2, c0ctx.L + 1, c0ctx.n)
     dec = c0ctx.decrypt_poly(ct)
+    k_e = ckks.sk_error_key(c0ctx.sk_seed, 9)
     for c in range(2):
-        e = smp.cbd(c0ctx.n, 9, 4 + c, smp.TAG_SK_E)
+        e = smp.cbd(c0ctx.n, k_e, 4 + c, smp.TAG_SK_E)
         assert dec[c] == [int(m) + int(x) for m, x in zip(polys[c], e)]
+        # the error is not the stream of the public wire seed (anyone holding c0
+        # and enc_seed could otherwise strip the noise)
+        e_pub = smp.cbd(c0ctx.n, 9, 4 + c, smp.TAG_SK_E)
+        assert not np.array_equal(e, e_pub)
         for i in range(c0ctx.L + 1):
             assert np.array_equal(ct.data[c, 1, i], smp.uniform(c0ctx.n, 9, 4 + c, i, smp.TAG_SK_A, c0ctx.q[i]))
 
@@ -209,3 +214,44 @@ def test_encrypt_sk_homomorphic(c0ctx):
     m = c0ctx.rescale(c0ctx.mul_relin(a, b))
     assert np.max(np.abs(c0ctx.decrypt(m, 4096) - z1 * z2)) < 1e-5
     assert np.max(np.abs(c0ctx.decrypt(a, 4096) - z1)) < 1e-6
+
+
+def _negacyclic_int(a, b):
+    """Exact negacyclic product of two small-integer polynomials (schoolbook via a linear
+    convolution, then X^N = -1 folding)."""
+    n = len(a)
+    full = np.convolve(np.asarray(a, dtype=np.int64), np.asarray(b, dtype=np.int64))
+    out = full[:n].copy()
+    out[: n - 1] -= full[n:]
+    return out
+
+
+def test_encrypt_pk_error_identity(c0ctx):
+    """O8 public-key encryption pinned exactly: with pk = (b, a),
+    b = -a s + e_pk, the ciphertext (v b + e0 + m, v a + e1) decrypts to
+    c0 + c1 s = m + v e_pk + e0 + e1 s, a negacyclic identity over the integers that is
+    checked coefficient by coefficient with the sampled v (ternary), e0, e1 (CBD), the
+    secret s and the key's error e_pk.  Dropping e0 or e1, drawing v from the CBD, or a
+    wrong sign anywhere breaks it."""
+    from oracle import sampling as smp
+    rng = np.random.default_rng(15)
+    polys = rng.integers(-2 ** 40, 2 ** 40, (2, c0ctx.n))
+    ct = c0ctx.encrypt_poly(polys, enc_seed=7, obj0=3, scale=2.0 ** 40)
+    dec = c0ctx.decrypt_poly(ct)
+    s = c0ctx.s_coef
+    for c in range(2):
+        v = smp.ternary(c0ctx.n, 7, 3 + c, smp.TAG_ENC_V)
+        e0 = smp.cbd(c0ctx.n, 7, 3 + c, smp.TAG_ENC_E0)
+        e1 = smp.cbd(c0ctx.n, 7, 3 + c, smp.TAG_ENC_E1)
+        assert set(np.unique(v)) <= {-1, 0, 1}
+        noise = _negacyclic_int(v, c0ctx.pk_e) + e0 + _negacyclic_int(e1, s)
+        assert dec[c] == [int(m) + int(x) for m, x in zip(polys[c], noise)]
+
+
+def test_key_identifier_is_not_the_seed(c0ctx):
+    """the public key_id is a one-way function of the secret seed."""
+    import hashlib
+    seed = c0ctx.sk_seed
+    assert c0ctx.key_id != seed
+    d = hashlib.sha256(b"edl-key\0" + seed.to_bytes(8, "little")).digest()
+    assert c0ctx.key_id == int.from_bytes(d[:8], "little")
