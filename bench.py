@@ -8,8 +8,10 @@ through the public API with the inputs copied from pinned host memory and the 10
 ciphertexts copied back inside the timed region.  N>1: each rank runs its own batch
 (weak scaling, independent batches -- the path needs no collective for them).
 
-`--impl reference` times the oracle (oracle/, the plain CPU implementation) on a bounded
-sample of the same workload on the host cores and prints the same JSON line.
+`--impl reference` times the oracle (oracle/, the plain CPU implementation) on the same
+workload on the host cores -- every step one full 8192-image batch, its 49 CC windows
+spread over one single-threaded process per core -- and prints the same JSON line (same
+metric, unit and config).
 """
 from __future__ import annotations
 
@@ -39,10 +41,40 @@ def _args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=12)
-    ap.add_argument("--cpu-windows", type=int, default=8, help="oracle sample size (windows of 49)")
+    ap.add_argument("--cpu-windows", type=int, default=8, help="single-core oracle sample (windows of 49)")
+    ap.add_argument("--cpu-procs", type=int, default=0, help="oracle processes (0: one per core, <= 49)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-c2", action="store_true", help="skip the C2 microbench sweep")
+    ap.add_argument("--no-c3", action="store_true", help="skip the C3 tabular net")
     return ap.parse_args()
+
+
+def c1_config(world: int) -> dict:
+    """The workload dict both arms print (same_config)."""
+    return {"workload": ("C1 Fashion-MNIST-shaped encrypted CNN, CKKS N=2^14 {60,40,40,40,40|60}, "
+                         "batch 8192 in slots (784 pixel ciphertexts), CC 5x4x4/4 -> sigma_a -> "
+                         "dense 245->10") if world == 1 else
+                        (f"C4 scale-out CNN: {world} batches of 8192 synthetic images (C1 "
+                         f"architecture and parameters), 49*{world} (window, batch) units over "
+                         f"{world} GPUs"), "global_batch": BATCH * world,
+            "parallelism": ("single GPU" if world == 1 else
+                            f"C4 (window, batch) units sharded x{world}, NCCL uint64 all-reduce of "
+                            f"dense partials"),
+            "l2": "inputs 1.03 GB per GPU > L2 (no flush)"}
+
+
+def cpu_info() -> dict:
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "numpy": np.__version__, "host_cores": len(os.sched_getaffinity(0))}
 
 
 # ----------------------------------------------------------------------------- oracle sample
@@ -85,26 +117,102 @@ def oracle_sample_seconds(windows: int, seed_data: int = 2110):
     return t
 
 
+def _oracle_shard(conn, windows, seed_data):
+    """One single-threaded host process: the oracle's C1 step restricted to `windows` (CC of
+    those windows for the 5 filters, sigma_a on their 5*len(windows) outputs, the dense
+    layer's un-rescaled partial sums over them).  Setup (keys, encryption) happens once;
+    every "go" runs the step and returns (t_start, t_end, partial accumulators)."""
+    from oracle import layers, networks
+    from oracle.ckks import CtArray
+    from synth import c1_images, c1_slots, c1_weights
+
+    K, kb, W, b = c1_weights()
+    ctx = networks.c1_context(1)
+    slots = c1_slots(c1_images(BATCH, seed_data))
+    pix = [(4 * (w // 7) + u) * 28 + 4 * (w % 7) + v for w in windows for u in range(4) for v in range(4)]
+    xs = [ctx.encrypt_poly(ctx.encode(slots[p])[None, :], 2, p, ctx.p.scale) for p in pix]   # object id = pixel
+    x = CtArray(np.concatenate([c.data for c in xs]), 4, xs[0].scale, xs[0].key_id)
+    cols = [f * WINDOWS + w for f in range(5) for w in windows]
+    ql = float(ctx.q[4])
+    conn.send("ready")
+    while conn.recv() == "go":
+        t0 = time.time()
+        parts = [layers.weighted_sum(ctx, x, range(16 * k, 16 * k + 16), K[f].reshape(-1), ql)
+                 for f in range(5) for k in range(len(windows))]
+        cc = ctx.add_scalar(ctx.rescale(CtArray(np.stack(parts), 4, x.scale * ql, x.key_id)),
+                            np.repeat(kb, len(windows)))
+        act = layers.poly_activation(ctx, cc, networks.SIGMA_A)
+        part = layers.dense_partial(ctx, act, W[:, cols])
+        conn.send((t0, time.time(), part.data, part.level, part.scale))
+
+
+class OracleFullBatch:
+    """The oracle on one full 8192-image C1 batch per step, its 49 windows split over P
+    single-threaded processes (one per host core, P <= 49); the per-process dense partials
+    are combined exactly as the multi-GPU path does (uint64 sum, mod q, rescale, bias:
+    oracle.layers.combine_partials / dense_finish).  Step time = last finish - first start
+    (host clock), setup excluded."""
+
+    def __init__(self, procs: int):
+        import multiprocessing as mp
+        os.environ.setdefault("OMP_NUM_THREADS", "1")
+        cores = len(os.sched_getaffinity(0))
+        self.P = max(1, min(WINDOWS, procs if procs > 0 else cores))
+        chunks = [list(range(WINDOWS))[k::self.P] for k in range(self.P)]
+        mpc = mp.get_context("spawn")
+        self.conns, self.procs = [], []
+        for ch in chunks:
+            a, b = mpc.Pipe()
+            p = mpc.Process(target=_oracle_shard, args=(b, ch, 2110), daemon=True)
+            p.start()
+            self.conns.append(a)
+            self.procs.append(p)
+        for c in self.conns:
+            assert c.recv() == "ready"
+
+    def step(self):
+        from oracle import layers, networks
+        from oracle.ckks import CtArray
+        from synth import c1_weights
+        for c in self.conns:
+            c.send("go")
+        res = [c.recv() for c in self.conns]
+        t = max(r[1] for r in res) - min(r[0] for r in res)
+        if not hasattr(self, "_fin"):
+            self._fin = networks.c1_context(1)
+        ctx = self._fin
+        parts = [CtArray(r[2], r[3], r[4], ctx.key_id) for r in res]
+        out = layers.dense_finish(ctx, layers.combine_partials(ctx, parts), c1_weights()[3])
+        assert out.count == 10 and out.level == 0
+        return t
+
+    def close(self):
+        for c in self.conns:
+            c.send("stop")
+        for p in self.procs:
+            p.join(timeout=10)
+
+
 def run_reference(a):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    per_step = []
-    for _ in range(a.warmup if a.warmup < 1 else 0):
-        pass
-    for _ in range(a.steps):
-        t = oracle_sample_seconds(a.cpu_windows)
-        per_step.append(t * WINDOWS / a.cpu_windows)
+    ob = OracleFullBatch(a.cpu_procs)
+    nb = max(a.gpus, 1)   # N > 1: the C4 step is N batches (global_batch 8192 N), run one after the other
+    for _ in range(max(a.warmup, 0)):
+        ob.step()
+    per_step = [sum(ob.step() for _ in range(nb)) for _ in range(a.steps)]
+    ob.close()
     t_full = float(np.mean(per_step))
-    value = BATCH / t_full
-    sample = f"{a.cpu_windows} of 49 CC windows per step (CC+sigma_a+dense partial over them), " \
-             f"extrapolated x{WINDOWS / a.cpu_windows:.3g} to one 8192-image batch"
+    value = nb * BATCH / t_full
+    sample = (f"every step {nb} full 8192-image C1 batch(es) (all 49 CC windows, sigma_a on 245 ciphertexts, "
+              f"dense 245->10 incl. rescale + bias), no extrapolation; {ob.P} single-threaded oracle processes")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": t_full * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "u64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": "C1 Fashion-MNIST-shaped encrypted CNN, CKKS N=2^14 {60,40,40,40,40|60}, "
-                                   "batch 8192 in slots", "global_batch": BATCH * a.gpus},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "config": c1_config(nb),
+            "cpu_baseline": dict({"value": value, "unit": UNIT, "cores": ob.P, "kind": "oracle", "sample": sample},
+                                 **cpu_info()),
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -164,20 +272,29 @@ C1_TRANSFORMS = {
     "k_rescale_ntt":        (490 + 490 + 490 + 20, 1470 + 980 + 490),
     "k_relin_intt_d2":      (245 + 245, 735 + 490),
     "k_relin_modup":        (245 * 7 + 245 * 5, 245 * 9 + 245 * 4),
+    "k_relin_ks":           (245 * 7 + 245 * 5, 245 * 9 + 245 * 4),   # fused variant (EDL_KS_FUSED=1)
     "k_relin_moddown_intt": (490 + 490, 490 + 490),
     "k_relin_moddown_ntt":  (490 + 490, 980 + 490),
 }
 
 
-# Algorithmic HBM bytes per launch (average over the step's launches) of the kernels that
-# can dominate: every operand limb read once, every output limb written once (N=2^14).
+# Algorithmic HBM bytes of one C1 step per kernel (all its launches in the step): every
+# operand limb read once, every output limb written once, 2^14 x 8 B per limb; keys and
+# constants (L2-resident) not counted.  Derivation per kernel in DESIGN.md §5.
 _LIMB = 8 << 14
-C1_ALG_BYTES = {
-    # modulus raise: reads (l+1) digit limbs, writes (l+1)^2 raised limbs; l = 3 and 2
-    "k_relin_modup": 245 * _LIMB * ((4 + 16) + (3 + 9)) / 2,
-    # rescale: reads last limb (2 polys) + kept limbs, writes kept limbs; 4 launches
-    "k_rescale_ntt": _LIMB * (245 * 2 * (2 + 4 + 4 + 4) + 245 * 2 * (3 + 3) + 245 * 2 * (2 + 2) + 10 * 2 * 2) / 4,
+C1_ALG_LIMBS = {
+    "k_cc_mac": 784 * 2 * 5 + 245 * 2 * 5,                          # 784 cts in @l=4, 245 out @l=4
+    "k_rescale_intt": (490 + 490) + (490 + 980) + (20 + 20),         # CC l=4; sigma u/w shared INTT (2 outs); dense
+    "k_rescale_ntt": (1960 + 490 + 1960) + (1470 + 490 + 1470) + (980 + 490 + 980) + (20 + 20 + 20),
+    "k_relin_intt_d2": (980 + 980) + (1470 + 735),                  # y*y (a == b) l=3; u*y2 l=2
+    "k_relin_modup": (980 + 3920) + (735 + 2205),                   # digits in, (l+1)^2 raised limbs out
+    "k_relin_mac": (3920 + 1960 + 2450) + (2205 + 2940 + 1960),     # raised digits + tensor operands in, acc out
+    "k_relin_ks": (980 + 1960 + 2450) + (735 + 2940 + 1960),        # fused: digits + tensor operands in, acc out
+    "k_relin_moddown_intt": 1960 + 1960,
+    "k_relin_moddown_ntt": (490 + 490 + 1470 + 1470) + (490 + 490 + 980 + 980 + 980),
+    "k_dense_mac": 980 + 40,
 }
+C1_ALG_BYTES = {k: v * _LIMB for k, v in C1_ALG_LIMBS.items()}
 
 
 def ntt_roofline(name, ms_total, steps, n, peak_int, peak_fp):
@@ -236,15 +353,26 @@ def run_ours(a):
         # (window, batch) units split over the ranks (49 each), dense partials combined by
         # one NCCL uint64 all-reduce, each rank finishing one batch
         sh = parallel.ShardedCNN(ctx, K, kb, W, b, world, rank, world)
-        full = []
+        # each rank encrypts only its own strip ciphertexts (16 per (window, batch) unit; object
+        # id = batch * 784 + pixel, as an unsharded encryption of that batch would use)
+        strips = []
         for bi in range(world):
-            polys = torch.from_numpy(ctx.encode(c1_slots(c1_images(BATCH, 2110 + bi)))).to(f"cuda:{local}")
-            full.append(ctx.encrypt_poly(polys, scale=float(2 ** 40), enc_seed=2, obj0=0))
+            px = sh.pixels(bi)
+            if not px:
+                continue
+            sl = c1_slots(c1_images(BATCH, 2110 + bi))[px]
+            polys = torch.from_numpy(ctx.encode(sl)).to(f"cuda:{local}")
+            for k, p in enumerate(px):
+                strips.append(ctx.encrypt_poly(polys[k:k + 1], scale=float(2 ** 40), enc_seed=2, obj0=784 * bi + p))
             del polys
-        x = parallel.rank_inputs(ctx, sh, full)
-        x_sk = None   # rank inputs are gathered ciphertexts: the e2e at N > 1 uses the public-key wire
-        del full
+        x = edl.CtArray(torch.cat([s_.tensor for s_ in strips]), len(strips), 4, strips[0].scale, strips[0].key_id)
+        x_sk = None   # rank inputs are strips: the e2e at N > 1 uses the public-key wire
+        del strips
         torch.cuda.empty_cache()
+        nccl_v = getattr(torch.cuda.nccl, "version", lambda: None)()
+        print(f"bench rank {rank}/{world}: backend {dist.get_backend()} NCCL {nccl_v} device cuda:{local} "
+              f"({torch.cuda.get_device_name(local)}), {sh.units} (window, batch) units, "
+              f"{x.count} input ciphertexts ({x.tensor.numel() * 8 / 2**30:.2f} GiB)", file=sys.stderr, flush=True)
         partials = torch.empty(sh.partials_words(), dtype=torch.int64, device=f"cuda:{local}")
 
         def all_reduce(t):
@@ -398,37 +526,68 @@ def run_ours(a):
         else:
             e2e = dict(e2e_pk, pipeline=pipeline, unpacked_bytes_per_step=int(x.tensor.numel() * 8))
 
-    # ---- roofline of the dominant kernel (largest share of the timed region)
+    # ---- roofline: every kernel against BOTH ceilings -- measured HBM (MEASURED_PEAKS.json)
+    # and, for the NTT family, the measured butterfly ceiling of its prime mix -- and the
+    # dominant kernel (largest share of the instrumented step) in the contract's keys
     n = ctx.n
     dom = max(prof.items(), key=lambda kv: kv[1][0]) if prof else ("none", (0.0, 0))
     peak_int = ctx.bfly_peak(0)          # q0 (60-bit): Shoup path
     peak_fp = ctx.bfly_peak(1)           # q1 (40-bit): FP64-pipe path
-    ntt_roofs = {}
-    for name in C1_TRANSFORMS:
-        if name in prof and world == 1:
-            ach, pk = ntt_roofline(name, prof[name][0], a.steps, n, peak_int, peak_fp)
-            ntt_roofs[name] = {"achieved_Gbfly_s": ach / 1e9, "peak_Gbfly_s": pk / 1e9, "frac": ach / pk,
-                               "share_of_step": prof[name][0] / ms_instr}
-    ntt_doms = [k for k in sorted(prof, key=lambda k: -prof[k][0]) if k in ntt_roofs]
+    dfma = ctx.pipe_peak(0)              # raw FP64 pipe: DFMA lane-ops/s
+    imadw = ctx.pipe_peak(1)             # raw integer multiply: IMAD.WIDE.U32 lane-ops/s
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    nominal_dp = sms * 64 * 1965e6       # 64 FP64 lanes / SM / clk at the max SM clock
+    hbm_peak = None
+    try:
+        hbm_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+        hbm_kind = "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        hbm_peak, hbm_kind = 6650.0, "fallback (B200_PROFILING.md)"
+    traffic_tab = {}
+    tf = os.path.join(ROOT, "profiles", "round2", "ncu_traffic.json")
+    if os.path.exists(tf):
+        traffic_tab = json.load(open(tf))
+    per_kernel = {}
+    if world == 1:
+        for name, (ms_tot, cnt) in prof.items():
+            ms_k = ms_tot / a.steps
+            e = {"ms_per_step": ms_k, "launches_per_step": cnt / a.steps, "share_of_step": ms_tot / ms_instr}
+            if name in C1_ALG_BYTES:
+                gbs = C1_ALG_BYTES[name] / (ms_k / 1e3) / 1e9
+                e.update({"alg_bytes_per_step": C1_ALG_BYTES[name], "hbm_GBps": gbs, "hbm_frac": gbs / hbm_peak})
+            if name in C1_TRANSFORMS:
+                ach, pk = ntt_roofline(name, ms_tot, a.steps, n, peak_int, peak_fp)
+                e.update({"achieved_Gbfly_s": ach / 1e9, "peak_Gbfly_s": pk / 1e9, "bfly_frac": ach / pk})
+            fr = {"hbm": e.get("hbm_frac", 0.0), "alu": e.get("bfly_frac", 0.0)}
+            e["bound"] = max(fr, key=fr.get) if any(fr.values()) else None
+            if name in traffic_tab:
+                e["dram_bytes_per_step_ncu"] = traffic_tab[name]["dram_bytes_per_step"]
+            per_kernel[name] = e
+    ntt_doms = [k for k in sorted(prof, key=lambda k: -prof[k][0]) if k in C1_TRANSFORMS]
     roof = None
-    if ntt_doms:
+    if ntt_doms and world == 1:
         k = ntt_doms[0]
-        r = ntt_roofs[k]
+        e = per_kernel[k]
+        launches_k = e["launches_per_step"]
         traffic = None
-        tf = os.path.join(ROOT, "profiles", "round1", "ncu_traffic.json")
-        if os.path.exists(tf):
-            tj = json.load(open(tf))
-            if k in tj:
-                traffic = tj[k]["dram_bytes_per_launch"]
-        roof = {"kernel": k, "bound": "alu", "unit": "Gbutterfly/s", "achieved": r["achieved_Gbfly_s"],
-                "peak": r["peak_Gbfly_s"], "frac": r["frac"], "traffic": traffic,
-                "traffic_unit": "DRAM bytes per launch (profiles/round1/ncu_traffic.json, ncu --set full)",
-                "algorithmic_bytes_per_launch": C1_ALG_BYTES.get(k),
+        if k in traffic_tab:   # DRAM bytes of the kernel's launches in one step (ncu --set full) / launches
+            traffic = traffic_tab[k]["dram_bytes_per_step"] / traffic_tab[k]["launches_per_step"]
+        roof = {"kernel": k, "bound": "alu", "unit": "Gbutterfly/s", "achieved": e["achieved_Gbfly_s"],
+                "peak": e["peak_Gbfly_s"], "frac": e["bfly_frac"], "traffic": traffic,
+                "traffic_unit": "DRAM bytes per launch (profiles/round2/ncu_traffic.json: ncu --set full of "
+                                "tools/prof_step.py, the bench step; bytes per step / launches per step)",
+                "algorithmic_bytes_per_launch": C1_ALG_BYTES.get(k, 0) / launches_k,
+                "hbm_frac": e.get("hbm_frac"), "hbm_peak_GBps": hbm_peak, "hbm_peak_kind": hbm_kind,
                 "peak_kind": "measured: register-only Harvey CT butterflies (edl_bfly_peak) through the "
                              "kernel's own arithmetic paths, weighted by its 60-bit/40-bit transform mix",
                 "peak_int_Gbfly_s": peak_int / 1e9, "peak_fp_Gbfly_s": peak_fp / 1e9,
-                "share_of_step": r["share_of_step"], "avg_launch_ms": prof[k][0] / prof[k][1],
-                "largest_kernel_overall": dom[0], "all_ntt_kernels": ntt_roofs}
+                "pipe_anchor": {"dfma_lane_ops_per_s": dfma, "imad_wide_lane_ops_per_s": imadw,
+                                "nominal_fp64_lane_ops_per_s": nominal_dp,
+                                "fp_bfly_vs_dfma": peak_fp * 8 / dfma,
+                                "note": "F64 butterfly = 8 FP64 instructions: peak_fp * 8 / dfma = the "
+                                        "butterfly kernel's FP64-pipe efficiency"},
+                "share_of_step": e["share_of_step"], "avg_launch_ms": prof[k][0] / prof[k][1],
+                "largest_kernel_overall": dom[0]}
     kernels = {k: {"ms_per_step": v[0] / a.steps, "launches_per_step": v[1] / a.steps} for k, v in prof.items()}
 
     # ---- second half of BASELINE's metric: NTT limb-transforms/s (C2 shape at N = 2^14:
@@ -474,6 +633,25 @@ def run_ours(a):
                    "config": f"{world} independent C1 batches (one per GPU), no communication"}
         del xr, net_r
 
+    # ---- the other BASELINE configs, rank 0 at N = 1 (outside the timed C1 region):
+    # C3 tabular net (configs[3]) and the C2 RNS microbench (configs[2]) at 3 and 24 limbs
+    c3 = c2 = None
+    if rank == 0 and world == 1:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        if not a.no_c3:
+            from c3_bench import run_c3
+            c3 = run_c3(5)
+            c3["config_index"] = 3
+        if not a.no_c2:
+            from c2_bench import point
+            c2 = {"config_index": 2, "batch": 256, "unit": "NTT/INTT: M limb-transforms/s; key-switch/s",
+                  "chains": "[60] + [40]*(L-2) + [60] data primes + one 60-bit special prime", "points": []}
+            for logn in (13, 14, 15, 16):
+                for L in (3, 24):
+                    r = point(logn, L, 256, 3)
+                    c2["points"].append({k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()})
+                    torch.cuda.empty_cache()
+
     props = torch.cuda.get_device_properties(local)
     device = {"name": props.name, "sms": props.multi_processor_count,
               "smem_per_sm_bytes": getattr(props, "shared_memory_per_multiprocessor", None),
@@ -481,32 +659,35 @@ def run_ours(a):
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        # all host cores: one full batch (no extrapolation), P single-threaded oracle processes
+        ob = OracleFullBatch(a.cpu_procs)
+        ob.step()                                   # warm-up
+        t_all = min(ob.step() for _ in range(2))
+        ob.close()
+        # one core: a sample of the same step, extrapolated linearly in the number of windows
         ts = oracle_sample_seconds(a.cpu_windows)
-        v = BATCH / (ts * WINDOWS / a.cpu_windows)
-        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"{a.cpu_windows} of 49 CC windows of one 8192-image batch, extrapolated x"
-                         f"{WINDOWS / a.cpu_windows:.3g}"}
+        t1 = ts * WINDOWS / a.cpu_windows
+        cpu = dict({"value": BATCH / t_all, "unit": UNIT, "cores": ob.P, "kind": "oracle",
+                    "sample": f"one full 8192-image batch (49 CC windows over {ob.P} single-threaded oracle "
+                              f"processes, dense partials combined), best of 2 after 1 warm-up, "
+                              f"{t_all:.2f} s; no extrapolation",
+                    "single_core": {"value": BATCH / t1, "unit": UNIT, "cores": 1,
+                                    "sampled_s": ts, "sample": f"{a.cpu_windows} of 49 CC windows (CC + sigma_a + "
+                                    f"dense partial over them) on one core",
+                                    "extrapolation": f"x{WINDOWS / a.cpu_windows:.4g} (linear in windows)",
+                                    "extrapolated_s_per_batch": t1}}, **cpu_info())
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
                 "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-                "config": {"workload": ("C1 Fashion-MNIST-shaped encrypted CNN, CKKS N=2^14 {60,40,40,40,40|60}, "
-                                        "batch 8192 in slots (784 pixel ciphertexts), CC 5x4x4/4 -> sigma_a -> "
-                                        "dense 245->10") if world == 1 else
-                                       (f"C4 scale-out CNN: {world} batches of 8192 synthetic images (C1 "
-                                        f"architecture and parameters), 49*{world} (window, batch) units over "
-                                        f"{world} GPUs"), "global_batch": BATCH * world,
-                           "parallelism": ("single GPU" if world == 1 else
-                                           f"C4 (window, batch) units sharded x{world}, NCCL uint64 all-reduce of "
-                                           f"dense partials"),
-                           "l2": "inputs 1.03 GB per GPU > L2 (no flush)"},
+                "config": c1_config(world),
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "clocks": clk, "dominant_kernel": dom[0], "kernels": kernels, "device": device,
+                "clocks": clk, "dominant_kernel": dom[0], "kernels": per_kernel or kernels, "device": device,
                 "kernel_timing": {"method": "CUDA event pair around every launch, on the library stream, over a "
                                             "second pass of the same K steps", "ms_per_step_instrumented":
                                   ms_instr / a.steps},
-                "replica_dp": replica,
+                "replica_dp": replica, "c2": c2, "c3": c3,
                 "ntt_limb_transforms_per_s": {"value": ntt_rate, "config": "N=2^14, C1 chain limbs q0..q4, 256 "
                                               "ciphertexts x 2 polys, forward NTT, device-timed (outside the "
                                               "timed C1 region)"}}

@@ -203,6 +203,14 @@ edl_status edl_dense_finish(edl_ctx* ctx, const edl_cts* acc, const double* b, e
 /* In-place forward (inverse != 0: inverse) NTT of n_polys * (level+1) limbs laid out
  * [n_polys][level+1][N] (device); limb j uses q_j (j == n_data means P). */
 edl_status edl_ntt(edl_ctx* ctx, uint64_t* limbs, int64_t n_polys, int32_t level, int32_t inverse);
+/* Key switch with the relinearisation key (C2 microbench; O11 on its own):
+ * for every ciphertext (d0, d2) of `d` (level l, NTT domain) -- d2 a polynomial under s^2 --
+ * out = (d0 + ks_0, ks_1) with (ks_0, ks_1) = ModDown(sum_j NTT_t([INTT_{q_j} d2_j] mod t)
+ * rlk_j), the same pipeline as edl_ct_ct_mul_relin without the tensor product, so
+ * decrypt(out) = d0 + d2 s^2 (+ key-switch noise).  out: caller-allocated (count, level),
+ * must not alias d; scale and key_id copied from d.  Errors: EDL_ERR_NOKEY, EDL_ERR_ARG.
+ * Asynchronous. */
+edl_status edl_keyswitch_bench(edl_ctx* ctx, const edl_cts* d, edl_cts* out);
 /* Raw Philox4x32-10 words for host counters ctr[n][4] with key (seed lo, seed hi). */
 edl_status edl_philox(edl_ctx* ctx, uint64_t seed, const uint32_t* ctr_host, int64_t n, uint32_t* out_host);
 /* ---- NEXT f1: the paper's one-image-per-ciphertext layout (kernel masquerading,
@@ -238,6 +246,15 @@ edl_status edl_encode_pt(edl_ctx* ctx, const double* slots, int64_t n_vec, int64
 edl_status edl_encode_pt_poly(edl_ctx* ctx, const int64_t* poly, int64_t n_vec, int32_t level, uint64_t* pt_out);
 edl_status edl_ct_pt_vec_mul(edl_ctx* ctx, const edl_cts* a, const uint64_t* pt, int64_t pt_count, int32_t pt_level,
                              double pt_scale, edl_cts* out);
+/* ct + plaintext vector (NEXT f1, the packed dense's per-block bias):
+ * out_c = (a_c0 + pt_c, a_c1) in the NTT domain; pt [pt_count][pt_level+1][N] device
+ * residues from edl_encode_pt(_poly) encoded at a's scale (the caller's choice: the
+ * scale is not checked), pt_count = 1 (broadcast) or a.count, pt_level >= a.level.
+ * out: caller-allocated (a's count and level), may alias a; scale = a.scale.
+ * Errors: EDL_ERR_SHAPE (pt_count), EDL_ERR_LEVEL (pt_level < a.level), EDL_ERR_ARG.
+ * Asynchronous. */
+edl_status edl_ct_pt_vec_add(edl_ctx* ctx, const edl_cts* a, const uint64_t* pt, int64_t pt_count, int32_t pt_level,
+                             edl_cts* out);
 /* Multi-plaintext MAC (NEXT f1, the tap-by-tap masked CC over hoisted rotations):
  * rots holds T blocks of n ciphertexts ([T][n][2][level+1][N], count = T n); pts holds
  * F x T NTT-domain plaintexts ([F][T][pt_level+1][N]); out[c F + f] = sum_t rots[t][c] (.)
@@ -303,6 +320,11 @@ edl_status edl_modmul_peak(edl_ctx* ctx, int32_t iters, double* modmul_per_s);
  * take for that modulus (FP64 quotient if q < 2^50, Shoup otherwise).  Writes butterflies
  * per second to *bfly_per_s.  Synchronises.  EDL_ERR_ARG on a bad index or iters <= 0. */
 edl_status edl_bfly_peak(edl_ctx* ctx, int32_t prime_index, int32_t iters, double* bfly_per_s);
+/* Raw pipe probes anchoring the butterfly ceilings: lane-operations per second of
+ * register-only chains of DFMA (which = 0, the FP64 pipe) or 32x32->64 IMAD.WIDE.U32
+ * (which = 1, the integer multiply the Shoup butterflies are built from) on every SM
+ * (8 CTAs of 256 threads per SM, 8 independent chains per thread).  Synchronises. */
+edl_status edl_pipe_peak(edl_ctx* ctx, int32_t which, int32_t iters, double* ops_per_s);
 /* Copy the secret key s_hat [L+2][N], public key [2][L+1][N] or rlk [L+1][2][L+2][N]
  * to host (which: 0, 1, 2).  For parity tests. */
 edl_status edl_export_key(edl_ctx* ctx, int32_t which, uint64_t* host_out, size_t words);

@@ -194,3 +194,157 @@ def masked_cc(ctx: Context, x: CtArray, K: np.ndarray, H: int, W: int, stride: i
         outs.append(y)
     data = np.stack([o.data for o in outs], axis=1).reshape((x.count * F,) + outs[0].data.shape[1:])
     return CtArray(data, outs[0].level, outs[0].scale, x.key_id)
+
+
+# ---------------------------------------------------------------------------------------
+# Hoisted tap-by-tap cross-correlation and the class-packed dense layer (NEXT f1 twins of
+# the GPU path's masquerade.masked_cc_hoisted / masked_dense_packed).
+# Paper: "kernel masquerading ... merging of weights and a respective zeros mask"
+# (PAPER.md:279), sums by "key rotation", the dense layer "summed across
+# the first axis".  Written from those passages and DESIGN.md §8b; every step
+# is an oracle primitive (rotate / rotate_hoisted / mul_plain / add / rescale / add_scalar).
+
+def add_plain(ctx: Context, ct: CtArray, pt_hat: np.ndarray) -> CtArray:
+    """ct + plaintext vector: c0 += pt (NTT domain), pt_hat [L'+1][N], L' >= ct.level."""
+    out = ct.data.copy()
+    for c in range(ct.count):
+        for i in range(ct.level + 1):
+            out[c, 0, i] = ring.add(ct.data[c, 0, i], pt_hat[i], ctx.q[i])
+    return CtArray(out, ct.level, ct.scale, ct.key_id)
+
+
+def anchor_slots(H: int, W: int, kh: int, kw: int, stride: int):
+    """Slot of window (r, c)'s top-left pixel (pixel p in slot p)."""
+    Ho, Wo = (H - kh) // stride + 1, (W - kw) // stride + 1
+    return [r * stride * W + c * stride for r in range(Ho) for c in range(Wo)]
+
+
+def masked_cc_hoisted(ctx: Context, x: CtArray, K: np.ndarray, H: int, W: int, stride: int, bias, gkeys,
+                      encode) -> CtArray:
+    """y_f = Rescale(sum_{u,v} rot(x, u W + v) (.) pt_{f,u,v}) + b_f, pt_{f,u,v} holding
+    K_f[u][v] at every window anchor (zeros elsewhere): the tap (u, v) of every window is
+    rotated onto the window's anchor, so window (r, c)'s value lands in its anchor slot.
+    Rotations share one modulus raise (rotate_hoisted); tap (0, 0) is x itself.
+    Output [count*F] image-major.  encode(z, scale) -> int64 poly."""
+    F, kh, kw = K.shape
+    l = x.level
+    ql = float(ctx.q[l])
+    n_slots = ctx.n // 2
+    anchors = anchor_slots(H, W, kh, kw, stride)
+    taps = [(u, v) for u in range(kh) for v in range(kw)]
+    rs = [u * W + v for (u, v) in taps]
+    rot = {0: x}
+    hoisted = rotate_hoisted(ctx, x, [r for r in rs if r != 0], gkeys)
+    for r, y in zip([r for r in rs if r != 0], hoisted):
+        rot[r] = y
+    idx = list(range(l + 1))
+    out = np.zeros((x.count * F, 2, l + 1, ctx.n), dtype=np.uint64)
+    for f in range(F):
+        acc = None
+        for (u, v), r in zip(taps, rs):
+            z = np.zeros(n_slots)
+            z[anchors] = K[f, u, v]
+            pt = ctx.signed_to_ntt(np.asarray(encode(z, ql), dtype=np.int64), idx)
+            y = mul_plain(ctx, rot[r], np.broadcast_to(pt, (x.count,) + pt.shape), ql)
+            acc = y if acc is None else ctx.add(acc, y)
+        out[f::F] = acc.data
+    y = ctx.rescale(CtArray(out, l, x.scale * ql, x.key_id))
+    if bias is not None:
+        y = ctx.add_scalar(y, [float(bias[f]) for _ in range(x.count) for f in range(F)])
+    return y
+
+
+def masked_dense_packed(ctx: Context, feats: CtArray, F: int, anchors, Wt: np.ndarray, b, span: int, fill, gkeys,
+                        encode) -> CtArray:
+    """Class-packed dense: blocks of blk = 2^ceil(log2 span) slots, nb = n_slots / blk
+    classes per product ciphertext, G = ceil(O / nb) of them per image.
+      1. feature f (slots outside the data region hold the constant fill[f]): subtract
+         fill[f] (constant add), then replicate block 0 into every block: r += rot(r, -s)
+         for s = blk, 2 blk, ... < n_slots (left rotation by n_slots - s);
+      2. product g: sum_f rep_f (.) pt_{g,f}, pt_{g,f}[k blk + anchors[w]] = W[g nb + k][f A + w];
+         rescale; block sums r += rot(r, s) for s = 1, 2, ... < blk;
+      3. bias: + pt_b with pt_b[k blk] = b_o + sum_f fill[f] sum_w W[o][f A + w] (o = g nb + k),
+         encoded at the accumulator's scale.
+    Logit o of image i sits in slot (o % nb) blk of ciphertext i G + o // nb."""
+    O = Wt.shape[0]
+    nimg = feats.count // F
+    l = feats.level
+    n_slots = ctx.n // 2
+    blk = 1
+    while blk < span:
+        blk *= 2
+    nb = n_slots // blk
+    G = (O + nb - 1) // nb
+    A = len(anchors)
+    ql = float(ctx.q[l])
+    idx = list(range(l + 1))
+    reps = []
+    for f in range(F):
+        r = feats.select(slice(f, None, F))
+        if fill is not None and fill[f] != 0.0:
+            r = ctx.add_scalar(r, [-float(fill[f])] * nimg)
+        s = blk
+        while s < n_slots:
+            r = ctx.add(r, rotate(ctx, r, n_slots - s, gkeys))
+            s *= 2
+        reps.append(r)
+    outs = []
+    for g in range(G):
+        acc = None
+        for f in range(F):
+            z = np.zeros(n_slots)
+            for k in range(nb):
+                o = g * nb + k
+                if o < O:
+                    for w in range(A):
+                        z[k * blk + anchors[w]] = Wt[o, f * A + w]
+            pt = ctx.signed_to_ntt(np.asarray(encode(z, ql), dtype=np.int64), idx)
+            y = mul_plain(ctx, reps[f], np.broadcast_to(pt, (nimg,) + pt.shape), ql)
+            acc = y if acc is None else ctx.add(acc, y)
+        acc = ctx.rescale(acc)
+        s = 1
+        while s < blk:
+            acc = ctx.add(acc, rotate(ctx, acc, s, gkeys))
+            s *= 2
+        if b is not None or fill is not None:
+            zb = np.zeros(n_slots)
+            for k in range(nb):
+                o = g * nb + k
+                if o < O:
+                    v = 0.0 if b is None else float(b[o])
+                    if fill is not None:
+                        v += sum(float(fill[f]) * float(np.sum(Wt[o, f * A:(f + 1) * A])) for f in range(F))
+                    zb[k * blk] = v
+            ptb = ctx.signed_to_ntt(np.asarray(encode(zb, acc.scale), dtype=np.int64), list(range(acc.level + 1)))
+            acc = add_plain(ctx, acc, ptb)
+        outs.append(acc)
+    data = np.stack([o.data for o in outs], axis=1).reshape((nimg * G,) + outs[0].data.shape[1:])
+    return CtArray(data, outs[0].level, outs[0].scale, feats.key_id)
+
+
+def packed_logits(ctx: Context, out: CtArray, O: int, span: int) -> np.ndarray:
+    """Decrypt masked_dense_packed outputs into [images][O] logits."""
+    n_slots = ctx.n // 2
+    blk = 1
+    while blk < span:
+        blk *= 2
+    nb = n_slots // blk
+    G = (O + nb - 1) // nb
+    z = ctx.decrypt(out, n_slots).reshape(out.count // G, G, n_slots)
+    return np.stack([z[:, o // nb, (o % nb) * blk] for o in range(O)], axis=1)
+
+
+def masked_cnn_packed(ctx: Context, x: CtArray, K, kb, Wt, b, H: int, W: int, stride: int, coeffs, gkeys,
+                      encode) -> CtArray:
+    """The paper-layout CNN: hoisted masked CC -> sigma -> class-packed dense, with the CC
+    bias' activation sigma(kb_f) (present in every slot outside the data region)
+    compensated inside the dense layer."""
+    from .layers import poly_activation
+    K = np.asarray(K, dtype=np.float64)
+    F, kh, kw = K.shape
+    cc = masked_cc_hoisted(ctx, x, K, H, W, stride, kb, gkeys, encode)
+    act = poly_activation(ctx, cc, coeffs)
+    kbv = np.zeros(F) if kb is None else np.asarray(kb, dtype=np.float64)
+    fill = [float(sum(c * v ** k for k, c in enumerate(coeffs))) for v in kbv]
+    return masked_dense_packed(ctx, act, F, anchor_slots(H, W, kh, kw, stride), np.asarray(Wt, dtype=np.float64), b,
+                               H * W, fill, gkeys, encode)

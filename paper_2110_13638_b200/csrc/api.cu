@@ -1088,6 +1088,35 @@ edl_status edl_ct_pt_vec_mul(edl_ctx* c, const edl_cts* a, const uint64_t* pt, i
     return cuda_check(c, "ct_pt_vec_mul");
 }
 
+edl_status edl_keyswitch_bench(edl_ctx* c, const edl_cts* d, edl_cts* out) {
+    if (!c || !out) return EDL_ERR_ARG;
+    if (!c->has_key) return fail(c, EDL_ERR_NOKEY, "keyswitch: no relinearisation key");
+    edl_status s = check_ct(c, d);
+    if (s != EDL_OK) return s;
+    if (d->count > 0 && (!out->data || out->data == d->data)) return fail(c, EDL_ERR_ARG, "keyswitch: bad output");
+    const int l = d->level;
+    if (d->count > 0) {
+        uint64_t* base = scratch(c, relin_scratch_words(d->count, l, c->logn));
+        if (!base) return fail(c, EDL_ERR_CUDA, "keyswitch: scratch");
+        relin_split(c, c->dev(), d->data, nullptr, d->count, l, false, c->d_rlk, c->d_rlk_s, base, out->data);
+    }
+    set_meta(out, d->count, l, d->scale, d->key_id);
+    return cuda_check(c, "keyswitch");
+}
+
+edl_status edl_ct_pt_vec_add(edl_ctx* c, const edl_cts* a, const uint64_t* pt, int64_t pt_count, int32_t pt_level,
+                             edl_cts* out) {
+    if (!c || !out) return EDL_ERR_ARG;
+    edl_status s = check_ct(c, a);
+    if (s != EDL_OK) return s;
+    if (a->count > 0 && (!pt || !out->data)) return fail(c, EDL_ERR_ARG, "ct_pt_vec_add: null buffer");
+    if (pt_count != 1 && pt_count != a->count) return fail(c, EDL_ERR_SHAPE, "ct_pt_vec_add: plaintext count");
+    if (pt_level < a->level) return fail(c, EDL_ERR_LEVEL, "ct_pt_vec_add: plaintext level below ciphertext level");
+    if (a->count > 0) launch_add_pt(c->dev(), a->data, a->count, a->level, pt, pt_count, pt_level, out->data);
+    set_meta(out, a->count, a->level, a->scale, a->key_id);
+    return cuda_check(c, "ct_pt_vec_add");
+}
+
 edl_status edl_ct_pt_mac_multi(edl_ctx* c, const edl_cts* rots, int32_t T, const uint64_t* pts, int32_t F,
                                int32_t pt_level, double pt_scale, edl_cts* out) {
     if (!c || !out || T < 1 || F < 1 || T > 64) return EDL_ERR_ARG;
@@ -1335,6 +1364,29 @@ edl_status edl_modmul_peak(edl_ctx* c, int32_t iters, double* modmul_per_s) {
     cudaEventDestroy(b);
     *modmul_per_s = (double)blocks * 256.0 * 8.0 * (double)iters / (ms * 1e-3);
     return cuda_check(c, "modmul_peak");
+}
+
+edl_status edl_pipe_peak(edl_ctx* c, int32_t which, int32_t iters, double* ops_per_s) {
+    if (!c || !ops_per_s || iters <= 0 || which < 0 || which > 1) return EDL_ERR_ARG;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    const int blocks = sms * 8;
+    uint64_t* sink = scratch(c, 1);
+    if (!sink) return fail(c, EDL_ERR_CUDA, "pipe_peak: scratch");
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    launch_pipe_probe(c->dev(), which, iters, blocks, sink);   // warm-up
+    cudaEventRecord(a, c->st);
+    launch_pipe_probe(c->dev(), which, iters, blocks, sink);
+    cudaEventRecord(b, c->st);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *ops_per_s = (double)blocks * 256.0 * 8.0 * (double)iters / (ms * 1e-3);
+    return cuda_check(c, "pipe_peak");
 }
 
 edl_status edl_export_galois_key(edl_ctx* c, int32_t steps, uint64_t* host_out, size_t words) {

@@ -256,6 +256,10 @@ void launch_automorphism(const Dev& d, const uint64_t* in, int64_t cnt, int l, u
 void launch_mul_pt(const Dev& d, const uint64_t* a, int64_t cnt, int l, const uint64_t* pt, int64_t pt_count,
                    int pt_level, uint64_t* out);
 
+// out = a + pt on polynomial 0 (pt as in launch_mul_pt)
+void launch_add_pt(const Dev& d, const uint64_t* a, int64_t cnt, int l, const uint64_t* pt, int64_t pt_count,
+                   int pt_level, uint64_t* out);
+
 // NEXT f3 (fft.cu): device canonical embedding; scratch fft_scratch_bytes(n_vec, logn)
 size_t fft_scratch_bytes(int64_t n_vec, int logn);
 void launch_encode_slots(const Dev& d, const double* z, int64_t n_vec, int64_t n_slots, double scale, int64_t* m,
@@ -287,6 +291,8 @@ void launch_philox_words(const Dev& d, uint64_t seed, const uint32_t* ctr /*[n][
 
 void launch_bfly_peak(const Dev& d, uint64_t q, bool fp, const ulonglong2* tw, int iters, int blocks, uint64_t* sink);
 void launch_modmul_peak(const Dev& d, uint64_t q, uint64_t w, uint64_t ws, int iters, int blocks, uint64_t* sink);
+// which = 0: DFMA chains, 1: IMAD.WIDE.U32 chains (8 per thread, 256 threads per CTA)
+void launch_pipe_probe(const Dev& d, int which, int iters, int blocks, uint64_t* sink);
 
 bool set_smem_attrs(int logn);
 

@@ -69,6 +69,46 @@ void launch_bfly_peak(const Dev& d, uint64_t q, bool fp, const ulonglong2* tw, i
     else EDL_LAUNCH(d, "k_bfly_peak", k_bfly_peak<false><<<blocks, 256, 0, d.st>>>(q, tw, iters, sink));
 }
 
+// Raw pipe probes anchoring the butterfly ceilings: 8 independent chains per
+// thread of (a) DFMA (FP64 pipe) or (b) 32x32->64 IMAD.WIDE.U32 (the fmaheavy integer
+// multiply the Shoup path is built from), 256 threads x 8 CTAs per SM, register-only.
+// Reports lane-operations per second (one DFMA or one IMAD.WIDE per lane).
+__global__ void __launch_bounds__(256) k_pipe_dfma(double a, double b, int iters, uint64_t* sink) {
+    double x[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) x[k] = (double)(threadIdx.x + k);
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int k = 0; k < 8; k++) x[k] = __fma_rn(x[k], a, b);
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) acc += x[k];
+    if (acc == 1.2345) sink[0] = 1;
+}
+__global__ void __launch_bounds__(256) k_pipe_imadw(uint32_t a, int iters, uint64_t* sink) {
+    uint64_t x[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) x[k] = threadIdx.x + k;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int k = 0; k < 8; k++) {   // IMAD.WIDE.U32: x = lo32(x) * a + x (64-bit addend)
+            uint64_t r;
+            asm volatile("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"((uint32_t)x[k]), "r"(a), "l"(x[k]));
+            x[k] = r;
+        }
+    }
+    uint64_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) acc ^= x[k];
+    if (acc == 0x123456789ull) sink[0] = acc;
+}
+
+void launch_pipe_probe(const Dev& d, int which, int iters, int blocks, uint64_t* sink) {
+    if (which == 0) EDL_LAUNCH(d, "k_pipe_dfma", k_pipe_dfma<<<blocks, 256, 0, d.st>>>(1.0000001, 1e-9, iters, sink));
+    else EDL_LAUNCH(d, "k_pipe_imadw", k_pipe_imadw<<<blocks, 256, 0, d.st>>>(0x9E3779B9u, iters, sink));
+}
+
 void launch_modmul_peak(const Dev& d, uint64_t q, uint64_t w, uint64_t ws, int iters, int blocks, uint64_t* sink) {
     EDL_LAUNCH(d, "k_modmul_peak", k_modmul_peak<<<blocks, 256, 0, d.st>>>(q, w, ws, iters, sink));
 }

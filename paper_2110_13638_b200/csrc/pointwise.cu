@@ -740,6 +740,32 @@ __global__ void k_mul_pt(const uint64_t* __restrict__ a, int64_t cnt, int l, con
     }
 }
 
+// out = a + pt on polynomial 0 (ct + plaintext vector, NTT domain; polynomial 1 copied)
+__global__ void k_add_pt(const uint64_t* __restrict__ a, int64_t cnt, int l, const uint64_t* __restrict__ pt,
+                         int64_t pt_count, int pt_level, uint64_t* __restrict__ out, const __grid_constant__ ModTable mods,
+                         int logn) {
+    const int64_t rows = cnt * 2 * (l + 1);
+    const int n2 = 1 << (logn - 1);
+    for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
+        const int i = (int)(row % (l + 1));
+        const int p = (int)((row / (l + 1)) % 2);
+        const int64_t c = row / (2 * (l + 1));
+        const uint64_t q = mods[i].q;
+        const uint64_t* pa = a + ((size_t)row << logn);
+        const uint64_t* pp = pt + ((((size_t)(pt_count == 1 ? 0 : c)) * (pt_level + 1) + i) << logn);
+        uint64_t* po = out + ((size_t)row << logn);
+        for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n2; k += gridDim.x * blockDim.x) {
+            const ulonglong2 x = v2(pa)[k];
+            if (p == 0) {
+                const ulonglong2 w = v2(pp)[k];
+                v2(po)[k] = make_ulonglong2(addmod(x.x, w.x, q), addmod(x.y, w.y, q));
+            } else {
+                v2(po)[k] = x;
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------- wire format (pack/unpack)
 // A ciphertext array travels host<->device with every residue of limb i stored in
 // bits_i = bit length of q_i (60 or 40 for the Alg. 8 chains) instead of 64: limb i of a
@@ -866,6 +892,12 @@ void launch_automorphism(const Dev& d, const uint64_t* in, int64_t cnt, int l, u
 void launch_mul_pt(const Dev& d, const uint64_t* a, int64_t cnt, int l, const uint64_t* pt, int64_t pt_count,
                    int pt_level, uint64_t* out) {
     EDL_LAUNCH(d, "k_mul_pt", k_mul_pt<<<rows_grid(d.logn, cnt * 2 * (l + 1)), PW_THREADS, 0, d.st>>>(
+                                  a, cnt, l, pt, pt_count, pt_level, out, *d.mt, d.logn));
+}
+
+void launch_add_pt(const Dev& d, const uint64_t* a, int64_t cnt, int l, const uint64_t* pt, int64_t pt_count,
+                   int pt_level, uint64_t* out) {
+    EDL_LAUNCH(d, "k_add_pt", k_add_pt<<<rows_grid(d.logn, cnt * 2 * (l + 1)), PW_THREADS, 0, d.st>>>(
                                   a, cnt, l, pt, pt_count, pt_level, out, *d.mt, d.logn));
 }
 

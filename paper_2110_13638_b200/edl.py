@@ -148,6 +148,9 @@ _sigs = {
     "edl_encode_pt": (_c.c_int32, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int64, _c.c_double, _c.c_int32,
                                    _c.c_void_p]),
     "edl_encode_pt_poly": (_c.c_int32, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int32, _c.c_void_p]),
+    "edl_keyswitch_bench": (_c.c_int32, [_c.c_void_p, _P(Cts), _P(Cts)]),
+    "edl_pipe_peak": (_c.c_int32, [_c.c_void_p, _c.c_int32, _c.c_int32, _c.c_void_p]),
+    "edl_ct_pt_vec_add": (_c.c_int32, [_c.c_void_p, _P(Cts), _c.c_void_p, _c.c_int64, _c.c_int32, _P(Cts)]),
     "edl_ct_pt_vec_mul": (_c.c_int32, [_c.c_void_p, _P(Cts), _c.c_void_p, _c.c_int64, _c.c_int32, _c.c_double,
                                        _P(Cts)]),
     "edl_export_galois_key": (_c.c_int32, [_c.c_void_p, _c.c_int32, _c.c_void_p, _c.c_size_t]),
@@ -505,6 +508,21 @@ class Context:
                                            pt_level, pt_scale, ctypes.byref(co)), "ct_pt_vec_mul")
         return o.update(co)
 
+    def keyswitch(self, d: CtArray) -> CtArray:
+        """(d0 + ks_0(d2), ks_1(d2)) for every (d0, d2) of d (edl_keyswitch_bench)."""
+        o = self.empty(d.count, d.level)
+        cd, co = d.cts(), o.cts()
+        self._check(_lib.edl_keyswitch_bench(self._h, ctypes.byref(cd), ctypes.byref(co)), "keyswitch")
+        return o.update(co)
+
+    def pt_vec_add(self, a: CtArray, pt, pt_count: int, pt_level: int, out: Optional[CtArray] = None) -> CtArray:
+        """a + pt on polynomial 0 (edl_ct_pt_vec_add); pt encoded at a's scale."""
+        o = out if out is not None else self.empty(a.count, a.level)
+        ca, co = a.cts(), o.cts()
+        self._check(_lib.edl_ct_pt_vec_add(self._h, ctypes.byref(ca), ctypes.c_void_p(pt.data_ptr()), pt_count,
+                                           pt_level, ctypes.byref(co)), "ct_pt_vec_add")
+        return o.update(co)
+
     def export_galois_key(self, steps: int) -> np.ndarray:
         L, nm, n = self.L, self.L + 2, self.n
         out = np.empty((L + 1, 2, nm, n), dtype=np.uint64)
@@ -575,6 +593,12 @@ class Context:
         out = np.empty_like(ctr)
         self._check(_lib.edl_philox(self._h, seed, _ptr(ctr), ctr.shape[0], _ptr(out)), "philox")
         return out
+
+    def pipe_peak(self, which: int, iters: int = 20000) -> float:
+        """Lane-ops/s of register-only DFMA (which=0) or IMAD.WIDE.U32 (which=1) chains."""
+        v = ctypes.c_double()
+        self._check(_lib.edl_pipe_peak(self._h, which, iters, ctypes.byref(v)), "pipe_peak")
+        return v.value
 
     def modmul_peak(self, iters: int = 20000) -> float:
         v = ctypes.c_double()

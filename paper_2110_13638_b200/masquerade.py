@@ -86,13 +86,14 @@ def tap_rotations(kh: int, kw: int, W: int) -> List[int]:
 
 
 def masked_cc_hoisted(ctx: Context, x: CtArray, K: np.ndarray, H: int, W: int, stride: int,
-                      bias: Optional[Sequence[float]] = None) -> CtArray:
+                      bias: Optional[Sequence[float]] = None, encode: Optional[Callable] = None) -> CtArray:
     """The masked CC computed tap by tap from hoisted rotations of the input (one modulus
     raise for all kh*kw - 1 rotations, `edl_rotate_hoisted`):
         y_f = sum_{u,v} rot(x, u W + v) (.) pt_{f,u,v},   pt_{f,u,v}[anchor] = K_f[u][v],
     so every window's value lands on its anchor slot and every other slot holds 0 (+ the
     bias).  Same output layout, level and scale as `masked_cc`; the 5 x 16 plaintexts are
-    encoded on the GPU (f3) in one batch.  Needs Galois keys for tap_rotations(kh, kw, W)."""
+    encoded on the GPU (f3) in one batch, or by `encode(z, scale) -> int64 poly` when given.
+    Needs Galois keys for tap_rotations(kh, kw, W)."""
     F, kh, kw = K.shape
     l = x.level
     ql = float(ctx.params.qs[l])
@@ -104,7 +105,8 @@ def masked_cc_hoisted(ctx: Context, x: CtArray, K: np.ndarray, H: int, W: int, s
         for k, (u, v) in enumerate((u, v) for u in range(kh) for v in range(kw)):
             z[f * len(taps) + k, anchors] = K[f, u, v]
     T = len(taps)
-    pts = ctx.encode_pt_poly(ctx.encode_device(z, ql), l)          # [F][T][l+1][N]
+    polys = ctx.encode_device(z, ql) if encode is None else np.stack([np.asarray(encode(v, ql)) for v in z])
+    pts = ctx.encode_pt_poly(polys, l)                              # [F][T][l+1][N]
     words = x.tensor.numel()
     big = ctx.torch.empty(T * words, dtype=ctx.torch.int64, device=x.tensor.device)
     views = [CtArray(big[k * words:(k + 1) * words], x.count, l, x.scale, x.key_id) for k in range(T)]
@@ -183,7 +185,8 @@ def packed_rotations(n_slots: int, span: int) -> List[int]:
 
 
 def masked_dense_packed(ctx: Context, feats: CtArray, F: int, anchors: Sequence[int], Wt: np.ndarray, b,
-                        span: int, fill: Optional[Sequence[float]] = None) -> CtArray:
+                        span: int, fill: Optional[Sequence[float]] = None,
+                        encode: Optional[Callable] = None) -> CtArray:
     """Dense layer with the classes packed into slot blocks (fewer rotations than
     `masked_dense`'s 10 per class): every feature ciphertext is replicated into the
     n_slots / blk blocks of blk = 2^ceil(log2 span) slots (log2(n_slots / blk) rotations,
@@ -197,7 +200,8 @@ def masked_dense_packed(ctx: Context, feats: CtArray, F: int, anchors: Sequence[
     (C1: sigma_a(kb_f), the activation of the CC bias that pt_add put in every slot); it is
     subtracted from every slot before the replication (no level used) so the other blocks'
     copies add exact zeros at the anchors, and sum_f fill[f] * sum_w W[o][f*A + w] is added
-    back through the bias.
+    back through the bias (a ct + plaintext-vector add, edl_ct_pt_vec_add).  Plaintexts come
+    from the library's host encoder, or from `encode(z, scale) -> int64 poly` when given.
     C1: 5 * 3 replication + 2 * 10 block-sum rotations = 35 per image instead of 100."""
     O = Wt.shape[0]
     nimg = feats.count // F
@@ -210,6 +214,12 @@ def masked_dense_packed(ctx: Context, feats: CtArray, F: int, anchors: Sequence[
     words = 2 * (l + 1) * ctx.n
     fv = feats.tensor.view(nimg, F, words)
     torch = ctx.torch
+
+    def enc_pt(z, scale, level):
+        if encode is None:
+            return ctx.encode_pt(z[None, :], scale, level)
+        return ctx.encode_pt_poly(np.asarray(encode(z, scale))[None, :], level)
+
     reps = []
     for f in range(F):
         r = CtArray(fv[:, f].contiguous().view(-1), nimg, l, feats.scale, feats.key_id)
@@ -229,7 +239,7 @@ def masked_dense_packed(ctx: Context, feats: CtArray, F: int, anchors: Sequence[
                 o = g * nb + k
                 if o < O:
                     z[k * blk + np.asarray(anchors)] = Wt[o, f * len(anchors):(f + 1) * len(anchors)]
-            pt = ctx.encode_pt(z[None, :], ql, l)
+            pt = enc_pt(z, ql, l)
             y = ctx.pt_vec_mul(reps[f], pt, 1, l, ql)
             acc = y if acc is None else ctx.add(acc, y)
         acc = ctx.rescale(acc)
@@ -244,10 +254,7 @@ def masked_dense_packed(ctx: Context, feats: CtArray, F: int, anchors: Sequence[
                     if fill is not None:
                         A = len(anchors)
                         zb[k * blk] += sum(float(fill[f]) * float(np.sum(Wt[o, f * A:(f + 1) * A])) for f in range(F))
-            ptb = ctx.encode_pt(zb[None, :], acc.scale, acc.level).view(acc.level + 1, ctx.n)
-            triv = torch.zeros((acc.count, 2, acc.level + 1, ctx.n), dtype=torch.int64, device=acc.tensor.device)
-            triv[:, 0] = ptb
-            acc = ctx.add(acc, CtArray(triv.view(-1), acc.count, acc.level, acc.scale, acc.key_id))
+            acc = ctx.pt_vec_add(acc, enc_pt(zb, acc.scale, acc.level), 1, acc.level)
         outs.append(acc)
     t = torch.stack([x.tensor.view(nimg, -1) for x in outs], dim=1).reshape(-1)
     return CtArray(t, nimg * G, outs[0].level, outs[0].scale, outs[0].key_id)
@@ -273,7 +280,7 @@ def masked_cnn(ctx: Context, x: CtArray, K, kb, Wt, b, H: int = 28, W: int = 28,
     `masked_cc_hoisted`."""
     F, kh, kw = np.asarray(K).shape
     if hoisted:
-        cc = masked_cc_hoisted(ctx, x, np.asarray(K, dtype=np.float64), H, W, stride, kb)
+        cc = masked_cc_hoisted(ctx, x, np.asarray(K, dtype=np.float64), H, W, stride, kb, encode=encode)
     else:
         cc = masked_cc(ctx, x, K, H, W, stride, kb, encode=encode)
     act = ctx.poly_activation(cc, coeffs)
@@ -281,5 +288,5 @@ def masked_cnn(ctx: Context, x: CtArray, K, kb, Wt, b, H: int = 28, W: int = 28,
         kbv = np.zeros(F) if kb is None else np.asarray(kb, dtype=np.float64)
         fill = [float(sum(c * v ** k for k, c in enumerate(coeffs))) for v in kbv]   # sigma(kb_f)
         return masked_dense_packed(ctx, act, F, anchor_slots(H, W, kh, kw, stride), np.asarray(Wt), b, H * W,
-                                   fill=fill)
+                                   fill=fill, encode=encode)
     return masked_dense(ctx, act, F, anchor_slots(H, W, kh, kw, stride), np.asarray(Wt), b, H * W, encode=encode)

@@ -136,3 +136,87 @@ def test_f1_masked_cnn_vs_float64(gpu):
     ctx.galois_keygen(9, [r for r in masquerade.tap_rotations(4, 4, 28) if r])
     outh = masquerade.masked_cnn(ctx, x, K, kb, W, b, packed=True, hoisted=True)
     assert np.max(np.abs(masquerade.packed_logits(ctx, outh, 10, 784) - ref)) < 1e-3
+
+
+@pytest.mark.timeout(1200)
+def test_c4_sharded_step_vs_oracle(gpu):
+    """C4 through ShardedCNN.step for R = 2 ranks and B = 2 batches:
+    each rank's step runs CC -> sigma_a -> dense partials on its own (window, batch) units,
+    the all-reduce is an in-process uint64 sum of both ranks' partials (the NCCL SUM's
+    arithmetic), and the batch each rank finishes equals the ORACLE's C1 output for that
+    batch on every residue (not only the GPU's unsharded network)."""
+    from oracle import networks as onet
+    from paper_2110_13638_b200 import parallel
+    from synth import c1_images, c1_slots, c1_weights
+
+    octx = onet.c1_context(1)
+    ctx = gpu.Context(gpu.params_from_depth(4)).keygen(1)
+    K, kb, W, b = c1_weights()
+    B, R = 2, 2
+    full, want = [], []
+    for bi in range(B):
+        polys = np.stack([octx.encode(z) for z in c1_slots(c1_images(8192, 2110 + bi))])
+        xo = octx.encrypt_poly(polys, 2, 784 * bi, octx.p.scale)          # distinct object ids per batch
+        full.append(ctx.encrypt_poly(polys, scale=octx.p.scale, enc_seed=2, obj0=784 * bi))
+        assert np.array_equal(full[bi].numpy(ctx.n), xo.data)
+        want.append(onet.c1_forward(octx, xo, K, kb, W, b)["out"])
+    shards = [parallel.ShardedCNN(ctx, K, kb, W, b, R, r, B) for r in range(R)]
+    xs = [parallel.rank_inputs(ctx, sh, full) for sh in shards]
+    # every rank's partials first (what the all-reduce would see), then each rank's step
+    parts = []
+    for sh, x in zip(shards, xs):
+        t = torch.empty(sh.partials_words(), dtype=torch.int64, device="cuda")
+        sh.partials(x, t)
+        parts.append(t)
+    got = {}
+    for r, (sh, x) in enumerate(zip(shards, xs)):
+        others = [parts[k] for k in range(R) if k != r]
+
+        def all_reduce(t, others=others):
+            for o in others:
+                t.add_(o)                                                   # int64 wrap == uint64 sum
+
+        pt = torch.empty(sh.partials_words(), dtype=torch.int64, device="cuda")
+        got.update(sh.step(x, pt, all_reduce))
+    assert sorted(got) == list(range(B))
+    for bi in range(B):
+        assert got[bi].level == want[bi].level == 0 and got[bi].scale == want[bi].scale
+        assert np.array_equal(got[bi].numpy(ctx.n), want[bi].data), bi
+
+
+@pytest.mark.timeout(900)
+def test_f1_packed_hoisted_bit_exact_vs_oracle(gpu):
+    """NEXT f1 in the paper's layout, bit-exact: the GPU's hoisted
+    masked CC -> sigma_a -> class-packed dense (with the sigma(kb) compensation and the
+    ct + plaintext-vector bias) equals the oracle twin (oracle/galois.py
+    masked_cnn_packed) on every residue, 2 images at N = 2^10 (16 x 16 images, 2 filters,
+    dense 32 -> 3), with the oracle's encoder feeding both sides' plaintexts (reading Z1)."""
+    from oracle import ckks as ock, galois, networks as onet
+    from oracle.params import make_params
+    from paper_2110_13638_b200 import masquerade
+
+    bits = [60, 40, 40, 40, 40, 60]
+    octx = ock.Context(make_params(1024, bits)).keygen(1)
+    ctx = gpu.Context(gpu.params_from_bits(10, bits)).keygen(1)
+    H = Wd = 16
+    rw = np.random.default_rng(41)
+    K = rw.normal(0.0, 0.1, (2, 4, 4))
+    kb = rw.normal(0.0, 0.1, 2)
+    Wt = rw.normal(0.0, 0.1, (3, 32))
+    b = rw.normal(0.0, 0.1, 3)
+    imgs = np.random.default_rng(42).integers(0, 256, (2, H, Wd)) / 255.0
+    rots = sorted(set([r for r in masquerade.tap_rotations(4, 4, Wd) if r] +
+                      masquerade.packed_rotations(ctx.n // 2, H * Wd)))
+    ctx.galois_keygen(7, rots)
+    gk = {galois.galois_element(r, octx.n): galois.galois_keygen(octx, 7, galois.galois_element(r, octx.n))
+          for r in rots}
+    polys = np.stack([octx.encode(z) for z in imgs.reshape(2, -1)])
+    xo = octx.encrypt_poly(polys, 2, 0, octx.p.scale)
+    xg = ctx.encrypt_poly(polys, scale=octx.p.scale, enc_seed=2)
+    want = galois.masked_cnn_packed(octx, xo, K, kb, Wt, b, H, Wd, 4, onet.SIGMA_A, gk, octx.encode)
+    got = masquerade.masked_cnn(ctx, xg, K, kb, Wt, b, H=H, W=Wd, stride=4, encode=octx.encode, packed=True,
+                                hoisted=True)
+    assert got.count == want.count == 4 and got.level == want.level == 0
+    assert np.array_equal(got.numpy(ctx.n), want.data)
+    ref = onet.c1_float64(imgs, K, kb, Wt, b)
+    assert np.max(np.abs(masquerade.packed_logits(ctx, got, 3, H * Wd) - ref)) < 1e-3

@@ -104,3 +104,61 @@ def test_masked_cc_matches_float64(small):
                 for cc in range(2):
                     got = dec[b, f, (rr * 4) * 8 + cc * 4]
                     assert abs(got - want[b, f * 4 + rr * 2 + cc]) < 1e-4
+
+
+# ------------------------------------------------------------------ packed paper-layout CNN
+F1_H, F1_W, F1_K, F1_F, F1_O = 16, 16, 4, 2, 3
+
+
+def _f1_small_net():
+    rw = np.random.default_rng(41)
+    K = rw.normal(0.0, 0.1, (F1_F, F1_K, F1_K))
+    kb = rw.normal(0.0, 0.1, F1_F)
+    A = (F1_H // F1_K) * (F1_W // F1_K)
+    Wt = rw.normal(0.0, 0.1, (F1_O, F1_F * A))
+    b = rw.normal(0.0, 0.1, F1_O)
+    imgs = np.random.default_rng(42).integers(0, 256, (2, F1_H, F1_W)) / 255.0
+    return K, kb, Wt, b, imgs
+
+
+def f1_rotations(n_slots):
+    """Tap rotations of the hoisted CC + replication and block-sum rotations of the packed dense."""
+    taps = [u * F1_W + v for u in range(F1_K) for v in range(F1_K) if u or v]
+    blk = 1
+    while blk < F1_H * F1_W:
+        blk *= 2
+    reps, s = [], blk
+    while s < n_slots:
+        reps.append(n_slots - s)
+        s *= 2
+    sums, s = [], 1
+    while s < blk:
+        sums.append(s)
+        s *= 2
+    return sorted(set(taps + reps + sums))
+
+
+@pytest.fixture(scope="module")
+def f1_small_oracle(small):
+    ctx = small
+    gk = {galois.galois_element(r, ctx.n): galois.galois_keygen(ctx, 7, galois.galois_element(r, ctx.n))
+          for r in f1_rotations(ctx.n // 2)}
+    K, kb, Wt, b, imgs = _f1_small_net()
+    x = ctx.encrypt(imgs.reshape(2, -1), 2)
+    out = galois.masked_cnn_packed(ctx, x, K, kb, Wt, b, F1_H, F1_W, F1_K, networks.SIGMA_A, gk, ctx.encode)
+    return out, gk
+
+
+def test_masked_cnn_packed_vs_float64(small, f1_small_oracle):
+    """the oracle twin of the GPU's hoisted masked CC + class-packed dense
+    (with the sigma(kb) compensation) decrypts to the float64 network within 1e-3
+    (N = 2^10, 16x16 images, 2 filters 4x4 stride 4, dense 32 -> 3; 2 product ciphertexts
+    per image because 2 classes fit in the 512 slots)."""
+    ctx = small
+    out, _ = f1_small_oracle
+    K, kb, Wt, b, imgs = _f1_small_net()
+    assert out.count == 2 * 2 and out.level == 0
+    got = galois.packed_logits(ctx, out, F1_O, F1_H * F1_W)
+    ref = networks.c1_float64(imgs, K, kb, Wt, b)
+    assert ref.shape == got.shape == (2, F1_O)
+    assert np.max(np.abs(got - ref)) < 1e-3
