@@ -62,6 +62,9 @@ struct edl_ctx {
     // k_relin_modup + k_relin_mac (default: measured faster on B200).
     // EDL_KS_FUSED=1 in the environment at context creation selects the fused kernel.
     bool ks_fused = false;
+    // Key switches of many ciphertexts in chunks of ks_chunk (EDL_KS_CHUNK, 0 = two halves)
+    // alternating over the two streams, so each chunk's raised digits stay in L2.
+    int64_t ks_chunk = 0;
 
     Dev dev() const {
         Dev d;
@@ -222,6 +225,24 @@ void relin_split(edl_ctx* c, const Dev& d, const uint64_t* a, const uint64_t* b,
     const size_t in_w = (size_t)2 * (l + 1) << c->logn, out_w = (size_t)2 * (rescale ? l : l + 1) << c->logn;
     Dev d2 = d;
     d2.st = c->st2;
+    if (c->ks_chunk > 0 && cnt > 2 * c->ks_chunk) {
+        // L2-sized chunks alternating over the two streams: a chunk's raised digits
+        // (chunk x (l+1)(l+2) limbs) stay in L2 between the modulus raise and the key products
+        const int64_t ch = c->ks_chunk;
+        cudaEventRecord(c->fork, c->st);
+        cudaStreamWaitEvent(c->st2, c->fork, 0);
+        const size_t sw = relin_scratch_words(ch, l, c->logn);
+        int k = 0;
+        for (int64_t s0 = 0; s0 < cnt; s0 += ch, k++) {
+            const int64_t n = (cnt - s0) < ch ? (cnt - s0) : ch;
+            const Dev& dd = (k & 1) ? d2 : d;
+            launch_relin(dd, a + s0 * in_w, b ? b + s0 * in_w : nullptr, n, l, rescale, rlk, rlk_s, scr + (k & 1) * sw,
+                         out + s0 * out_w, add_w ? add_w + s0 * out_w : nullptr, add_k ? add_k + s0 * nlo : nullptr);
+        }
+        cudaEventRecord(c->join, c->st2);
+        cudaStreamWaitEvent(c->st, c->join, 0);
+        return;
+    }
     // (measured: starting the second half only after the first half's d2 INTT, to pair
     // transforms with the key-product pass, is slower than the halves side by side)
     cudaEventRecord(c->fork, c->st);
@@ -346,6 +367,8 @@ edl_status edl_ctx_create(const edl_params* p, int32_t device, void* stream, edl
     {
         const char* e = std::getenv("EDL_KS_FUSED");
         c->ks_fused = e && e[0] == '1';
+        const char* k = std::getenv("EDL_KS_CHUNK");
+        c->ks_chunk = k ? std::atoll(k) : 0;
     }
     const int nm = c->L + 2;
     // twiddle tables: per modulus [fwd N][inv N] of {w, w'}

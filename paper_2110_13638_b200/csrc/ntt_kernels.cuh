@@ -11,6 +11,17 @@
 namespace edl {
 
 
+// Epilogue operand of a forward transform at the output indices (a limb laid out like the
+// output): at N = 2^14 it is copied into shared memory by cp.async at the kernel's start
+// (PreStaged, ntt_core.cuh: overlapped with the whole transform, no registers held), which
+// needs M extra words of shared memory per CTA and runs 3 CTAs per SM (CfgEpi); elsewhere
+// it is loaded for all E outputs before the first store (the round-1 form).
+template <class C>
+__device__ __forceinline__ auto epi_pre(const uint64_t* base, uint64_t* sm) {
+    if constexpr (C::STAGE_EPI) return PreStaged{base, sm + C::SMEM_WORDS};
+    else return PreLoad{base};
+}
+
 // ------------------------------------------------------------------------------------
 // K1/K2: plain batched NTT / INTT, in place, data [batch][nl][N], limb j uses pm.idx[j].
 template <class C, bool INV>
@@ -166,7 +177,7 @@ k_rescale_ntt(const uint64_t* __restrict__ in, int l, const ulonglong2* __restri
         pf_next_wave<C>([&](int64_t bx, int cr, int y, int) { pf_sub<C>(r + (((size_t)bx * 2 + y) << C::LOGN), cr, true); });
     }
     auto ld = [&](int idx) { return center_mod(rr[idx], ql, ql_mod, m); };
-    auto pre = [&](int idx) { return src[idx]; };
+    const auto pre = epi_pre<C>(src, sm);
     // out = (a w_i - x) q_l^-1 + b: integer path on canonical x, or (F64 limbs) on the
     // transform's unreduced binary64 output with exact FP64-pipe products
     struct Store {
@@ -516,9 +527,9 @@ k_relin_moddown_ntt(const uint64_t* __restrict__ a, const uint64_t* __restrict__
             }
         };
         const Load ld{rr, ss, P, pmod, ql, qlmod, pinv, m};
-        auto pre = [&](int idx) { return vi[idx]; };
         // (v - x) q_l^-1 (+ w + k: a fused ciphertext + constant addend, e.g. sigma's output
-        // assembly); F64 limbs: on the unreduced binary64 transform output
+        // assembly); F64 limbs: on the unreduced binary64 transform output.  Both epilogue
+        // operands (v and w) are fetched for all E outputs before the first store (pre).
         const uint64_t* wl = add_w ? add_w + limb_off(c, cp, i, nlo, C::LOGN) : nullptr;
         const uint64_t kk = (add_k && cp == 0) ? add_k[c * nlo + i] : 0;
         struct Store {
@@ -542,7 +553,7 @@ k_relin_moddown_ntt(const uint64_t* __restrict__ a, const uint64_t* __restrict__
                 dst[idx] = f64_to_canon(t, qd);
             }
         };
-        ntt_fwd<C>(sm, m, ld, pre, Store{dst, wl, kk, m, qlinv});
+        ntt_fwd<C>(sm, m, ld, epi_pre<C>(vi, sm), Store{dst, wl, kk, m, qlinv});
     } else {
         // out = d + (acc - NTT([r])) P^-1 = v - NTT([r] P^-1)  (Z_q-linear, exact)
         struct Load {   // [r] P^-1; F64 limbs: on the FP64 pipe, |.| <= 0.625 q
@@ -559,9 +570,8 @@ k_relin_moddown_ntt(const uint64_t* __restrict__ a, const uint64_t* __restrict__
             }
         };
         const Load ld{rr, P, pmod, pinv, m};
-        auto pre = [&](int idx) { return vi[idx]; };
         auto st = [&](int idx, uint64_t x, uint64_t v) { dst[idx] = submod(v, x, m.q); };
-        ntt_fwd<C>(sm, m, ld, pre, st);
+        ntt_fwd<C>(sm, m, ld, epi_pre<C>(vi, sm), st);
     }
 }
 
@@ -591,9 +601,9 @@ void launch_rescale_intt_n(const Dev& d, const uint64_t* in, int64_t cnt, int l,
 template <int LOGN>
 void launch_rescale_ntt_n(const Dev& d, const uint64_t* in, int64_t cnt, int l, const ulonglong2* w, const uint64_t* r,
                           const uint64_t* bias, uint64_t* out, int nlo) {
-    using C = CfgFused<LOGN>;
-    launch_cfg<C>(d, "k_rescale_ntt", k_rescale_ntt<C>, dim3((unsigned)cnt, 2, nlo), in, l, w, r, bias, out, nlo, *d.mt,
-                  d.cc);
+    using C = CfgEpi<LOGN>;
+    launch_cfg_x<C>(d, "k_rescale_ntt", k_rescale_ntt<C>, dim3((unsigned)cnt, 2, nlo), C::STAGE_EPI ? C::M * 8 : 0, in, l,
+                    w, r, bias, out, nlo, *d.mt, d.cc);
 }
 
 template <int LOGN>
@@ -625,8 +635,10 @@ void launch_relin_n(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t 
     }
     launch_cfg<C>(d, "k_relin_moddown_intt", k_relin_moddown_intt<C>, dim3((unsigned)cnt, 2), a, b, l, (const uint64_t*)acc,
                   d.L, rs, r, s, *d.mt, d.cc);
-    launch_cfg<C>(d, "k_relin_moddown_ntt", k_relin_moddown_ntt<C>, dim3((unsigned)cnt, 2, rescale ? l : l + 1), a, b, l,
-                  (const uint64_t*)acc, (const uint64_t*)r, (const uint64_t*)s, d.L, rs, out, add_w, add_k, *d.mt, d.cc);
+    using CE = CfgEpi<LOGN>;
+    launch_cfg_x<CE>(d, "k_relin_moddown_ntt", k_relin_moddown_ntt<CE>, dim3((unsigned)cnt, 2, rescale ? l : l + 1),
+                     CE::STAGE_EPI ? CE::M * 8 : 0, a, b, l, (const uint64_t*)acc, (const uint64_t*)r, (const uint64_t*)s,
+                     d.L, rs, out, add_w, add_k, *d.mt, d.cc);
 }
 
 // Hoisted rotations (several Galois elements of the same ciphertexts): the modulus raise of
@@ -650,8 +662,10 @@ void launch_relin_finish_n(const Dev& d, const uint64_t* a, int64_t cnt, int l, 
     launch_relin_mac(d, a, b, cnt, l, xh, rlk, rlk_c, acc);
     launch_cfg<C>(d, "k_relin_moddown_intt", k_relin_moddown_intt<C>, dim3((unsigned)cnt, 2), a, b, l, (const uint64_t*)acc,
                   d.L, 0, r, s, *d.mt, d.cc);
-    launch_cfg<C>(d, "k_relin_moddown_ntt", k_relin_moddown_ntt<C>, dim3((unsigned)cnt, 2, l + 1), a, b, l,
-                  (const uint64_t*)acc, (const uint64_t*)r, (const uint64_t*)s, d.L, 0, out, b, b, *d.mt, d.cc);
+    using CE = CfgEpi<LOGN>;
+    launch_cfg_x<CE>(d, "k_relin_moddown_ntt", k_relin_moddown_ntt<CE>, dim3((unsigned)cnt, 2, l + 1),
+                     CE::STAGE_EPI ? CE::M * 8 : 0, a, b, l, (const uint64_t*)acc, (const uint64_t*)r, (const uint64_t*)s,
+                     d.L, 0, out, b, b, *d.mt, d.cc);
 }
 
 #define EDL_INSTANTIATE_NTT(LOGN)                                                                                   \

@@ -322,6 +322,93 @@ k_cc_mac2(const uint64_t* __restrict__ x, int l, int W, int kw, int stride, int 
     }
 }
 
+// ---------------------------------------------------------------- cross-correlation MAC, round 2
+// One coefficient per thread (8-byte loads, 256 B per warp) and all FC <= 8 filters of a
+// filter chunk: accumulators take 2 (binary64) or 4 (128-bit) registers per filter instead
+// of twice that, so CTAs of CC3_T threads run more warps per SM than k_cc_mac2 (128
+// registers, 16 warps); tap loads run CC3_TB ahead of the MACs.  Measured on C1: 0.53 ms
+// against k_cc_mac2's 0.47 (the kernel is FP64-/IMAD-issue-bound, not occupancy-bound), so
+// it is compiled only with EDL_CC_MAC3.
+constexpr int CC3_T = 128;
+constexpr int CC3_TB = 8;
+
+template <int FC>
+__global__ void __launch_bounds__(CC3_T, 8)
+k_cc_mac3(const uint64_t* __restrict__ x, int l, int W, int kw, int stride, int Wo, int taps, int f0, int F,
+          int n_out_per_f, const ulonglong2* __restrict__ wk, uint64_t* __restrict__ out,
+          const __grid_constant__ ModTable mods, int logn) {
+    __shared__ ulonglong2 wsm[FC * CC2_MAXTAPS];   // [f][tap] {residue (binary64 on F64 limbs), companion}
+    __shared__ int tpix[CC2_MAXTAPS];
+    const int nl = l + 1;
+    const int p = blockIdx.y / nl, i = blockIdx.y % nl;
+    const int win = blockIdx.z;
+    const int wr = win / Wo, wc = win % Wo;
+    const ModInfo& m = mods[i];
+    const bool f64 = m.fp == 2, fp = m.fp != 0;   // uniform per CTA
+    for (int t = threadIdx.x; t < FC * taps; t += CC3_T) {
+        const int f = t / taps, tt = t % taps;
+        ulonglong2 w = (f0 + f < F) ? wk[((size_t)(f0 + f) * taps + tt) * nl + i] : make_ulonglong2(0, 0);
+        if (f64) w.x = f64_from_u(w.x);
+        wsm[t] = w;
+    }
+    for (int t = threadIdx.x; t < taps; t += CC3_T) tpix[t] = (wr * stride + t / kw) * W + (wc * stride + t % kw);
+    __syncthreads();
+    const int n = blockIdx.x * CC3_T + threadIdx.x;
+    if (n >= (1 << logn)) return;
+    const size_t ct_words = (size_t)2 * nl << logn;
+    const uint64_t* xb = x + limb_off(0, p, i, nl, logn) + n;
+    const double qd = u52_to_double(m.q);
+    if (f64) {
+        double acc[FC];
+#pragma unroll
+        for (int f = 0; f < FC; f++) acc[f] = 0.0;
+        for (int t0 = 0; t0 < taps; t0 += CC3_TB) {
+            uint64_t xv[CC3_TB];
+#pragma unroll
+            for (int u = 0; u < CC3_TB; u++) xv[u] = (t0 + u < taps) ? __ldg(xb + tpix[t0 + u] * ct_words) : 0;
+#pragma unroll
+            for (int u = 0; u < CC3_TB; u++) {
+                if (t0 + u >= taps) break;
+                const double xd = u52_to_double(xv[u]);
+#pragma unroll
+                for (int f = 0; f < FC; f++) {
+                    const ulonglong2 w = wsm[f * taps + t0 + u];
+                    acc[f] = __dadd_rn(acc[f], f64_mulc(xd, f64_of(w.x), f64_of(w.y), qd));
+                }
+            }
+        }
+#pragma unroll
+        for (int f = 0; f < FC; f++)
+            if (f0 + f < F)
+                out[limb_off((int64_t)(f0 + f) * n_out_per_f + win, p, i, nl, logn) + n] =
+                    f64_to_canon(f64_reduce(acc[f], qd, m.qinv_d), qd);
+    } else {
+        U128 acc[FC];
+#pragma unroll
+        for (int f = 0; f < FC; f++) acc[f].lo = acc[f].hi = 0;
+        for (int t0 = 0; t0 < taps; t0 += CC3_TB) {
+            uint64_t xv[CC3_TB];
+#pragma unroll
+            for (int u = 0; u < CC3_TB; u++) xv[u] = (t0 + u < taps) ? __ldg(xb + tpix[t0 + u] * ct_words) : 0;
+#pragma unroll
+            for (int u = 0; u < CC3_TB; u++) {
+                if (t0 + u >= taps) break;
+#pragma unroll
+                for (int f = 0; f < FC; f++) {
+                    const ulonglong2 w = wsm[f * taps + t0 + u];
+                    if (fp) acc[f].lo += tw_mul_fp(xv[u], w.x, w.y, m.q);   // [0, 2q): taps * 2q < 2^53
+                    else mac128(acc[f], xv[u], w.x);
+                }
+            }
+        }
+#pragma unroll
+        for (int f = 0; f < FC; f++)
+            if (f0 + f < F)
+                out[limb_off((int64_t)(f0 + f) * n_out_per_f + win, p, i, nl, logn) + n] =
+                    fp ? reduce64(acc[f].lo, m) : barrett128(acc[f], m);
+    }
+}
+
 // ---------------------------------------------------------------- dense MAC
 // grid: x = coefficient blocks, y = poly*(l+1) + limb, z = output chunk of DN_OC x K split.
 // Split-K (round 2): the K inputs are cut into ks slices so a small layer (C1: 245 -> 10
@@ -408,6 +495,89 @@ k_dense_mac(const uint64_t* __restrict__ x, int64_t K, int64_t O, int l, int ks,
             }
         }
         first = false;
+    }
+}
+
+// ---------------------------------------------------------------- dense MAC, round 2
+// grid: x = coefficient blocks (one coefficient per thread), y = poly * (l+1) + limb,
+// z = K slice.  A CTA stages only its slice's weights [kc][OC] in shared memory (round 1
+// staged a [12][256] block per CTA: 48 KB of mostly padding per CTA, ~50 MB of L2 reads
+// per layer) and every thread keeps all OC <= 16 outputs' accumulators in registers, so
+// each input residue is read once and feeds O products.  Input loads run DN3_U ahead.
+// F64 limbs: exact binary64 products (f64_mulc) summed exactly (kc <= 256 terms); others
+// full 128-bit products summed lazily; one reduction per output (O4).
+constexpr int DN3_T = 128;
+constexpr int DN3_U = 4;
+
+template <int OC>
+__global__ void __launch_bounds__(DN3_T)
+k_dense_mac3(const uint64_t* __restrict__ x, int64_t K, int O, int l, int kper, const ulonglong2* __restrict__ wd,
+             uint64_t* __restrict__ out, const __grid_constant__ ModTable mods, int logn) {
+    extern __shared__ ulonglong2 wsm3[];   // [kper][OC] {residue (binary64 on F64 limbs), companion}
+    const int nl = l + 1;
+    const int p = blockIdx.y / nl, i = blockIdx.y % nl;
+    const int sl = blockIdx.z;
+    const int64_t k0 = (int64_t)sl * kper;
+    const int kc = (int)((K - k0) < kper ? (K - k0) : kper);
+    const ModInfo& m = mods[i];
+    const bool f64 = m.fp == 2, fp = m.fp != 0;
+    for (int t = threadIdx.x; t < kc * OC; t += DN3_T) {
+        const int kk = t / OC, o = t % OC;
+        ulonglong2 w = (o < O) ? wd[((size_t)o * K + (k0 + kk)) * nl + i] : make_ulonglong2(0, 0);
+        if (f64) w.x = f64_from_u(w.x);
+        wsm3[t] = w;
+    }
+    __syncthreads();
+    const int n = blockIdx.x * DN3_T + threadIdx.x;
+    if (n >= (1 << logn)) return;
+    const size_t kstride = (size_t)2 * nl << logn;
+    const uint64_t* xp = x + limb_off(k0, p, i, nl, logn) + n;
+    uint64_t* outp = out + (size_t)sl * ((size_t)O * 2 * nl << logn);
+    const double qd = u52_to_double(m.q);
+    if (f64) {
+        double acc[OC];
+#pragma unroll
+        for (int o = 0; o < OC; o++) acc[o] = 0.0;
+        for (int kk = 0; kk < kc; kk += DN3_U) {
+            uint64_t xv[DN3_U];
+#pragma unroll
+            for (int u = 0; u < DN3_U; u++) xv[u] = (kk + u < kc) ? __ldg(xp + (size_t)(kk + u) * kstride) : 0;
+#pragma unroll
+            for (int u = 0; u < DN3_U; u++) {
+                if (kk + u >= kc) break;
+                const double xd = u52_to_double(xv[u]);
+#pragma unroll
+                for (int o = 0; o < OC; o++) {
+                    const ulonglong2 w = wsm3[(kk + u) * OC + o];
+                    acc[o] = __dadd_rn(acc[o], f64_mulc(xd, f64_of(w.x), f64_of(w.y), qd));
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 0; o < OC; o++)
+            if (o < O) outp[limb_off(o, p, i, nl, logn) + n] = f64_to_canon(f64_reduce(acc[o], qd, m.qinv_d), qd);
+    } else {
+        U128 acc[OC];
+#pragma unroll
+        for (int o = 0; o < OC; o++) acc[o].lo = acc[o].hi = 0;
+        for (int kk = 0; kk < kc; kk += DN3_U) {
+            uint64_t xv[DN3_U];
+#pragma unroll
+            for (int u = 0; u < DN3_U; u++) xv[u] = (kk + u < kc) ? __ldg(xp + (size_t)(kk + u) * kstride) : 0;
+#pragma unroll
+            for (int u = 0; u < DN3_U; u++) {
+                if (kk + u >= kc) break;
+#pragma unroll
+                for (int o = 0; o < OC; o++) {
+                    const ulonglong2 w = wsm3[(kk + u) * OC + o];
+                    if (fp) acc[o].lo += tw_mul_fp(xv[u], w.x, w.y, m.q);   // [0, 2q) lazy, kc * 2q < 2^55
+                    else mac128(acc[o], xv[u], w.x);
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 0; o < OC; o++)
+            if (o < O) outp[limb_off(o, p, i, nl, logn) + n] = fp ? reduce64(acc[o].lo, m) : barrett128(acc[o], m);
     }
 }
 
@@ -703,6 +873,157 @@ k_relin_mac2(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int
     }
 }
 
+// ---------------------------------------------------------------- key inner product, round 2
+// One coefficient per thread (8-byte accesses), the thread's key entries for its target
+// (ND digits x 2 components) held in registers for all MAC3_CTS ciphertexts of its CTA,
+// and the next ciphertext's loads (l digit limbs + the tensor operands) issued before the
+// current one's arithmetic (software pipelining across ciphertexts): 256-thread CTAs at
+// <= 80 registers, 3 per SM, instead of k_relin_mac2's 128-register 128-thread CTAs.
+// F64 targets: f64_mult products (no key companion) summed exactly; 60-bit targets: full
+// 128-bit products summed lazily, Barrett once; MODE 1 (2^44 <= q < 2^46) keeps the
+// FP64-quotient lazy products with companions.  Same output as k_relin_mac2.
+constexpr int MAC3_T = 256;
+#ifndef EDL_MAC3_CTS
+#define EDL_MAC3_CTS 8
+#endif
+constexpr int MAC3_CTS = EDL_MAC3_CTS;
+
+template <int MODE, int ND>
+__global__ void __launch_bounds__(MAC3_T, 3)
+k_relin_mac3(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l, int L, int64_t cnt,
+             const uint64_t* __restrict__ xh, const uint64_t* __restrict__ rlk, const uint64_t* __restrict__ rlk_c,
+             uint64_t* __restrict__ acc, const __grid_constant__ TargetList tl, const __grid_constant__ ModTable mods,
+             const ChainConsts* __restrict__ chain, int logn) {
+    constexpr bool F64 = MODE == 2;
+    const int ti = tl.slot[blockIdx.y];
+    const int t = (ti == l + 1) ? (L + 1) : ti;
+    const ModInfo& m = mods[t];
+    const int k = blockIdx.x * MAC3_T + threadIdx.x;
+    if (k >= (1 << logn)) return;
+    const double qd = u52_to_double(m.q);
+    // key entries of this coefficient: kv[j][cc] (binary64 on F64 targets), companions for MODE 1
+    uint64_t kv[ND][2], kc[ND][2];
+#pragma unroll
+    for (int j = 0; j < ND; j++)
+#pragma unroll
+        for (int cc = 0; cc < 2; cc++) {
+            const size_t o = ((((size_t)j * 2 + cc) * (L + 2) + t) << logn) + k;
+            kv[j][cc] = F64 ? bits_of(u52_to_double(__ldg(rlk + o))) : __ldg(rlk + o);
+            kc[j][cc] = (MODE == 1) ? __ldg(rlk_c + o) : 0;
+        }
+    const bool data = ti <= l;
+    const bool single = (b == nullptr);
+    const ulonglong2 pinv = data ? chain->qinv[L + 1][t] : make_ulonglong2(0, 0);
+    const double pinv_d = u52_to_double(pinv.x);
+    const size_t limb = (size_t)1 << logn;
+    const size_t cs = (size_t)2 * (l + 1) << logn;                       // one ciphertext
+    const size_t xs_c = (size_t)(l + 1) * (l + 2) << logn;               // raised digits of one ciphertext
+    const uint64_t* xb = xh + ((size_t)ti << logn) + k;                  // digit j at + j (l+2) N
+    const uint64_t* a0b = a + ((size_t)(data ? ti : 0) << logn) + k;
+    const uint64_t* a1b = a0b + (size_t)(l + 1) * limb;
+    const uint64_t* b0b = single ? a0b : b + ((size_t)(data ? ti : 0) << logn) + k;
+    const uint64_t* b1b = b0b + (size_t)(l + 1) * limb;
+    (void)limb;
+    const int64_t c_beg = (int64_t)blockIdx.z * MAC3_CTS;
+    const int64_t c_end = c_beg + MAC3_CTS < cnt ? c_beg + MAC3_CTS : cnt;
+    // per-ciphertext operands: x[j] (j != ti), a0, a1, b0, b1
+    struct Ops {
+        uint64_t x[ND], a0, a1, b0, b1;
+    };
+    auto fetch = [&](int64_t c, Ops& o) {
+#pragma unroll
+        for (int j = 0; j < ND; j++) o.x[j] = (j != ti) ? xb[(size_t)c * xs_c + (size_t)j * (l + 2) * limb] : 0;
+        if (data) {
+            o.a0 = a0b[(size_t)c * cs];
+            o.a1 = a1b[(size_t)c * cs];
+            o.b0 = single ? o.a0 : b0b[(size_t)c * cs];
+            o.b1 = single ? o.a1 : b1b[(size_t)c * cs];
+        } else if (ti < ND) {
+            o.a0 = o.a1 = o.b0 = o.b1 = 0;
+        } else {
+            o.a0 = o.a1 = o.b0 = o.b1 = 0;
+        }
+    };
+    Ops nx;
+    if (c_beg < c_end) fetch(c_beg, nx);
+    for (int64_t c = c_beg; c < c_end; c++) {
+        const Ops cur = nx;
+        if (c + 1 < c_end) fetch(c + 1, nx);
+        uint64_t v0, v1;
+        if constexpr (F64) {
+            double s0 = 0.0, s1 = 0.0;
+            double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+            for (int j = 0; j < ND; j++) {
+                double xd;
+                if (j == ti) {   // d2 = a1 b1 (rotation: a1), exact product reduced on the FP64 pipe
+                    const double x1 = u52_to_double(cur.a1);
+                    xd = single ? x1 : f64_mult(x1, u52_to_double(cur.b1), qd, m.qinv_d);
+                } else {
+                    xd = u52_to_double(cur.x[j]);
+                }
+                s0 = __dadd_rn(s0, f64_mult(xd, f64_of(kv[j][0]), qd, m.qinv_d));
+                s1 = __dadd_rn(s1, f64_mult(xd, f64_of(kv[j][1]), qd, m.qinv_d));
+            }
+            if (data) {   // v = d + acc P^-1, d0 = a0 b0, d1 = a0 b1 + a1 b0 (rotation: d = (a0, 0))
+                const double x0 = u52_to_double(cur.a0);
+                if (single) {
+                    d0 = x0;
+                } else {
+                    const double y0 = u52_to_double(cur.b0), y1 = u52_to_double(cur.b1), x1 = u52_to_double(cur.a1);
+                    d0 = f64_mult(x0, y0, qd, m.qinv_d);
+                    d1 = __dadd_rn(f64_mult(x0, y1, qd, m.qinv_d), f64_mult(x1, y0, qd, m.qinv_d));
+                }
+                s0 = __dadd_rn(d0, f64_mult(s0, pinv_d, qd, m.qinv_d));
+                s1 = __dadd_rn(d1, f64_mult(s1, pinv_d, qd, m.qinv_d));
+            }
+            v0 = f64_to_canon(f64_reduce(s0, qd, m.qinv_d), qd);
+            v1 = f64_to_canon(f64_reduce(s1, qd, m.qinv_d), qd);
+        } else if constexpr (MODE == 1) {
+            uint64_t s0 = 0, s1 = 0;
+#pragma unroll
+            for (int j = 0; j < ND; j++) {
+                const uint64_t x = (j == ti) ? (single ? cur.a1 : mulmod_fp(cur.a1, cur.b1, m)) : cur.x[j];
+                s0 += tw_mul_fp(x, kv[j][0], kc[j][0], m.q);
+                s1 += tw_mul_fp(x, kv[j][1], kc[j][1], m.q);
+            }
+            v0 = reduce64(s0, m);
+            v1 = reduce64(s1, m);
+            if (data) {
+                uint64_t d0 = cur.a0, d1 = 0;
+                if (!single) {
+                    d0 = mulmod_fp(cur.a0, cur.b0, m);
+                    d1 = addmod(mulmod_fp(cur.a0, cur.b1, m), mulmod_fp(cur.a1, cur.b0, m), m.q);
+                }
+                v0 = addmod(d0, mulc(v0, pinv, m), m.q);
+                v1 = addmod(d1, mulc(v1, pinv, m), m.q);
+            }
+        } else {
+            U128 s0, s1;
+            s0.lo = s0.hi = s1.lo = s1.hi = 0;
+#pragma unroll
+            for (int j = 0; j < ND; j++) {
+                const uint64_t x = (j == ti) ? (single ? cur.a1 : mulmod_barrett(cur.a1, cur.b1, m)) : cur.x[j];
+                mac128(s0, x, kv[j][0]);
+                mac128(s1, x, kv[j][1]);
+            }
+            v0 = barrett128(s0, m);
+            v1 = barrett128(s1, m);
+            if (data) {
+                uint64_t d0 = cur.a0, d1 = 0;
+                if (!single) {
+                    d0 = mulmod_barrett(cur.a0, cur.b0, m);
+                    d1 = addmod(mulmod_barrett(cur.a0, cur.b1, m), mulmod_barrett(cur.a1, cur.b0, m), m.q);
+                }
+                v0 = addmod(d0, mulc(v0, pinv, m), m.q);
+                v1 = addmod(d1, mulc(v1, pinv, m), m.q);
+            }
+        }
+        acc[((((size_t)c * 2 + 0) * (l + 2) + ti) << logn) + k] = v0;
+        acc[((((size_t)c * 2 + 1) * (l + 2) + ti) << logn) + k] = v1;
+    }
+}
+
 // ---------------------------------------------------------------- NEXT f1: automorphism, ct (.) pt
 // sigma_g in the NTT domain is a permutation of the evaluation points (same for every limb):
 // out[k] = in[src_g(k)], (2 brv(src) + 1) = (2 brv(k) + 1) g mod 2N.
@@ -949,6 +1270,31 @@ void launch_relin_mac(const Dev& d, const uint64_t* a, const uint64_t* b, int64_
         else if (d.hmods[t].fp) tf.slot[nf++] = (int8_t)s;
         else ti.slot[ni++] = (int8_t)s;
     }
+#ifndef EDL_MAC2
+    if (l + 1 <= 6 && d.logn >= 8) {   // round 2: k_relin_mac3
+        const unsigned gx3 = (unsigned)((1 << d.logn) / MAC3_T), gz3 = (unsigned)((cnt + MAC3_CTS - 1) / MAC3_CTS);
+#define EDL_MAC3(FPV, ND, LIST, NT)                                                                   \
+    EDL_LAUNCH(d, "k_relin_mac", (k_relin_mac3<FPV, ND><<<dim3(gx3, NT, gz3), MAC3_T, 0, d.st>>>( \
+                                     a, b, l, d.L, cnt, xh, rlk, rlk_c, acc, LIST, *d.mt, d.cc, d.logn)))
+#define EDL_MAC3_ND(ND)                                  \
+    case ND:                                             \
+        if (n6) EDL_MAC3(2, ND, t6, n6);                 \
+        if (nf) EDL_MAC3(1, ND, tf, nf);                 \
+        if (ni) EDL_MAC3(0, ND, ti, ni);                 \
+        break;
+        switch (l + 1) {
+            EDL_MAC3_ND(1)
+            EDL_MAC3_ND(2)
+            EDL_MAC3_ND(3)
+            EDL_MAC3_ND(4)
+            EDL_MAC3_ND(5)
+            EDL_MAC3_ND(6)
+        }
+#undef EDL_MAC3_ND
+#undef EDL_MAC3
+        return;
+    }
+#endif
 #ifdef EDL_NO_MAC2
     if (false) {
 #else
@@ -1015,6 +1361,27 @@ void launch_cc_mac(const Dev& d, const uint64_t* x, int l, int H, int W, int F, 
                    const ulonglong2* wk, uint64_t* out) {
     const int Ho = (H - kh) / stride + 1, Wo = (W - kw) / stride + 1;
     const int taps = kh * kw;
+#ifdef EDL_CC_MAC3   // measured slower on C1 (0.53 vs 0.47 ms): kept for reference
+    if (taps <= CC2_MAXTAPS && d.logn >= 8) {
+        dim3 grid((unsigned)((1 << d.logn) / CC3_T), (unsigned)(2 * (l + 1)), (unsigned)(Ho * Wo));
+        for (int f0 = 0; f0 < F; f0 += 8) {
+            const int fc = (F - f0) < 8 ? (F - f0) : 8;
+#define EDL_CC3(FCV) EDL_LAUNCH(d, "k_cc_mac", (k_cc_mac3<FCV><<<grid, CC3_T, 0, d.st>>>(x, l, W, kw, stride, Wo, taps, f0, F, Ho * Wo, wk, out, *d.mt, d.logn)))
+            switch (fc) {
+                case 1: EDL_CC3(1); break;
+                case 2: EDL_CC3(2); break;
+                case 3: EDL_CC3(3); break;
+                case 4: EDL_CC3(4); break;
+                case 5: EDL_CC3(5); break;
+                case 6: EDL_CC3(6); break;
+                case 7: EDL_CC3(7); break;
+                default: EDL_CC3(8); break;
+            }
+#undef EDL_CC3
+        }
+        return;
+    }
+#endif
     if (taps <= CC2_MAXTAPS && d.logn >= 9) {
         dim3 grid((unsigned)((1 << d.logn) / (2 * CC2_THREADS)), (unsigned)(2 * (l + 1)), (unsigned)(Ho * Wo));
         for (int f0 = 0; f0 < F; f0 += 8) {
@@ -1040,6 +1407,13 @@ void launch_cc_mac(const Dev& d, const uint64_t* x, int l, int H, int W, int F, 
 }
 
 int dense_split(const Dev& d, int64_t K, int64_t O, int l) {
+    if (O <= 16 && d.logn >= 7) {   // k_dense_mac3: ~8 CTAs of 128 threads per SM, K slices of >= 8 inputs
+        const int64_t base = (int64_t)((1 << d.logn) / DN3_T) * 2 * (l + 1);
+        int64_t ks = (8 * 148 + base - 1) / base;
+        if (ks > K / 8) ks = K / 8;
+        if (ks > 32) ks = 32;
+        return ks < 1 ? 1 : (int)ks;
+    }
     const int64_t ctas = (int64_t)((1 << d.logn) / PW_THREADS) * 2 * (l + 1) * ((O + DN_OC - 1) / DN_OC);
     int ks = 1;
     while (ks < 16 && ctas * ks < 4 * 148 && K / (ks * 2) >= 16) ks *= 2;
@@ -1049,6 +1423,27 @@ int dense_split(const Dev& d, int64_t K, int64_t O, int l) {
 void launch_dense_mac(const Dev& d, const uint64_t* x, int64_t K, int64_t O, int l, const ulonglong2* wd, uint64_t* out,
                       uint64_t* part) {
     const int ks = part ? dense_split(d, K, O, l) : 1;
+    if (O <= 16 && d.logn >= 7) {
+        const int kper = (int)((K + ks - 1) / ks);
+        if (kper <= 256) {   // exact binary64 / 128-bit sums bounded for <= 256 terms
+            const int oc = O <= 4 ? 4 : (O <= 8 ? 8 : (O <= 12 ? 12 : 16));
+            dim3 grid((unsigned)((1 << d.logn) / DN3_T), (unsigned)(2 * (l + 1)), (unsigned)ks);
+            const size_t smem = (size_t)kper * oc * sizeof(ulonglong2);
+            uint64_t* dst = ks > 1 ? part : out;
+#define EDL_DN3(OCV) EDL_LAUNCH(d, "k_dense_mac", (k_dense_mac3<OCV><<<grid, DN3_T, smem, d.st>>>(x, K, (int)O, l, kper, wd, dst, *d.mt, d.logn)))
+            switch (oc) {
+                case 4: EDL_DN3(4); break;
+                case 8: EDL_DN3(8); break;
+                case 12: EDL_DN3(12); break;
+                default: EDL_DN3(16); break;
+            }
+#undef EDL_DN3
+            if (ks > 1)
+                EDL_LAUNCH(d, "k_dense_combine", k_dense_combine<<<rows_grid(d.logn, O * 2 * (l + 1)), PW_THREADS, 0, d.st>>>(
+                                                     part, ks, O, l, out, *d.mt, d.logn));
+            return;
+        }
+    }
     dim3 grid((unsigned)(((1 << d.logn) + PW_THREADS - 1) / PW_THREADS), (unsigned)(2 * (l + 1)),
               (unsigned)(((O + DN_OC - 1) / DN_OC) * ks));
     size_t smem = (size_t)DN_OC * DN_KC * sizeof(ulonglong2);

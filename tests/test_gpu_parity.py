@@ -659,3 +659,19 @@ def test_keygen_drops_galois_keys(edl):
     X = _rand_ct(o, 1, 2, 91)
     with pytest.raises(edl.EdlError):
         g.rotate(_to_gpu(g, X, 2, 2.0 ** 40, g.key_id), 1)
+
+
+def test_chunked_keyswitch_bit_exact(edl, monkeypatch):
+    """Key switches in L2-sized chunks over the two streams (EDL_KS_CHUNK): 37 ciphertexts
+    (ragged last chunk) at every level of the C0 chain, and the sigma_a-shaped x^2 layer,
+    against the oracle."""
+    monkeypatch.setenv("EDL_KS_CHUNK", "8")
+    g, o = _pair(edl, depth=2)
+    for lvl in (1, 2):
+        A = ock.CtArray(_rand_ct(o, 37, lvl, 151 + lvl), lvl, 2.0 ** 40, o.key_id)
+        B = ock.CtArray(_rand_ct(o, 37, lvl, 161 + lvl), lvl, 2.0 ** 40, o.key_id)
+        got = g.mul_relin(_to_gpu(g, A.data, lvl, A.scale, o.key_id), _to_gpu(g, B.data, lvl, B.scale, o.key_id))
+        assert np.array_equal(got.numpy(g.n), o.mul_relin(A, B).data), lvl
+    X = ock.CtArray(_rand_ct(o, 37, 2, 171), 2, 2.0 ** 40, o.key_id)
+    got = g.poly_activation(_to_gpu(g, X.data, 2, X.scale, o.key_id), [0.0, 0.0, 1.0])
+    assert np.array_equal(got.numpy(g.n), olay.poly_activation(o, X, [0.0, 0.0, 1.0]).data)

@@ -50,6 +50,15 @@ def main():
     x = ctx.encrypt_poly(polys, scale=2.0 ** 40, enc_seed=2)
     net = C1Net(ctx, K, kb, W, b)
     res["c1_step_ms"] = time_ms(lambda: net.forward(x), reps=3)
+    for ch in os.environ.get("EDL_BENCH_CHUNKS", "").split(","):
+        if ch:   # the same C1 step with key switches in chunks (EDL_KS_CHUNK, read at context creation)
+            os.environ["EDL_KS_CHUNK"] = ch
+            cx = edl.Context(edl.params_from_depth(4)).keygen(1)
+            xc = cx.encrypt_poly(polys, scale=2.0 ** 40, enc_seed=2)
+            nc = C1Net(cx, K, kb, W, b)
+            res[f"c1_step_ms_chunk{ch}"] = time_ms(lambda: nc.forward(xc), reps=3)
+            del nc, xc, cx
+            os.environ.pop("EDL_KS_CHUNK")
     ctx.profile(True)
     net.forward(x)
     res["c1_kernels_ms"] = {k: round(v[0], 3) for k, v in ctx.profile_read().items()}
