@@ -39,6 +39,8 @@ struct edl_ctx {
     uint64_t* d_pk = nullptr;
     uint64_t* d_rlk = nullptr;
     uint64_t* d_rlk_s = nullptr;
+    uint64_t* d_rlk_pf = nullptr;     // rlk with P^-1 folded into the data limbs (+ companions)
+    uint64_t* d_rlk_pf_c = nullptr;
     std::map<uint32_t, std::pair<uint64_t*, uint64_t*>> gkeys;   // Galois element -> (key, companions)
     bool has_key = false;
     uint64_t key_id = 0;       // host::key_identifier(seed): public, one-way in the seed
@@ -77,6 +79,9 @@ struct edl_ctx {
         d.st = st;
         d.prof = &prof;
         d.ks_fused = ks_fused;
+        d.rlk = d_rlk;
+        d.rlk_pf = ks_fused ? nullptr : d_rlk_pf;   // the fused kernel applies P^-1 itself
+        d.rlk_pf_c = d_rlk_pf_c;
         return d;
     }
     uint64_t modulus(int idx) const { return idx <= L ? prm.q[idx] : prm.p_special; }
@@ -485,6 +490,8 @@ void edl_ctx_destroy(edl_ctx* c) {
     cudaFree(c->d_pk);
     cudaFree(c->d_rlk);
     cudaFree(c->d_rlk_s);
+    cudaFree(c->d_rlk_pf);
+    cudaFree(c->d_rlk_pf_c);
     for (auto& kv : c->gkeys) {
         cudaFree(kv.second.first);
         cudaFree(kv.second.second);
@@ -560,7 +567,9 @@ edl_status edl_keygen(edl_ctx* c, uint64_t seed) {
         if (cudaMalloc(&c->d_s, nm * N * 8) != cudaSuccess ||
             cudaMalloc(&c->d_pk, 2 * (size_t)(c->L + 1) * N * 8) != cudaSuccess ||
             cudaMalloc(&c->d_rlk, (size_t)(c->L + 1) * 2 * nm * N * 8) != cudaSuccess ||
-            cudaMalloc(&c->d_rlk_s, (size_t)(c->L + 1) * 2 * nm * N * 8) != cudaSuccess)
+            cudaMalloc(&c->d_rlk_s, (size_t)(c->L + 1) * 2 * nm * N * 8) != cudaSuccess ||
+            cudaMalloc(&c->d_rlk_pf, (size_t)(c->L + 1) * 2 * nm * N * 8) != cudaSuccess ||
+            cudaMalloc(&c->d_rlk_pf_c, (size_t)(c->L + 1) * 2 * nm * N * 8) != cudaSuccess)
             return fail(c, EDL_ERR_CUDA, "keygen: out of device memory");
     }
     // Galois keys belong to the previous secret: drop them (edl_galois_keygen regenerates)
@@ -571,6 +580,7 @@ edl_status edl_keygen(edl_ctx* c, uint64_t seed) {
     }
     c->gkeys.clear();
     launch_keygen(c->dev(), seed, c->d_s, c->d_pk, c->d_rlk, c->d_rlk_s, nullptr);
+    launch_fold_pinv(c->dev(), c->d_rlk, c->d_rlk_pf, c->d_rlk_pf_c);
     if (cudaStreamSynchronize(c->st) != cudaSuccess) return cuda_check(c, "keygen");
     c->has_key = true;
     c->key_id = host::key_identifier(seed);

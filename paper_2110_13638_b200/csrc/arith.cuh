@@ -80,6 +80,28 @@ __device__ __forceinline__ uint64_t shoup_lazy4(uint64_t y, uint64_t w, uint64_t
     return y * w - qt * q;
 }
 
+// Shoup with a 3-product quotient (round 2): qt' = floor((y1 s1 2^64 + y1 s0 2^32 + y0 s1 2^32)
+// / 2^64) computed as hi(y1 s1 + hi(y0 s1) + hi(y1 s0 + lo(y0 s1))) -- three IMAD.WIDE
+// instead of __umul64hi's four -- drops y0 s0 / 2^64 < 1 and one fractional carry, so
+// qt' is qt or qt - 1 and y w - qt' q lies in [0, 3q) (any y < 2^64).
+__device__ __forceinline__ uint64_t shoup_lazy3(uint64_t y, uint64_t w, uint64_t ws, uint64_t q) {
+    const uint32_t y0 = (uint32_t)y, y1 = (uint32_t)(y >> 32);
+    const uint32_t s0 = (uint32_t)ws, s1 = (uint32_t)(ws >> 32);
+    const uint64_t a = (uint64_t)y0 * s1;
+    const uint64_t b = (uint64_t)y1 * s0 + (a & 0xFFFFFFFFull);
+    const uint64_t qt = (uint64_t)y1 * s1 + (a >> 32) + (b >> 32);
+    return y * w - qt * q;
+}
+
+// Lazy bound of the Shoup butterflies (ntt_core.cuh): with the 3-product quotient the
+// forward keeps values in [0, 8q) and the inverse in [0, 4q) (8q < 2^63 for q < 2^60), the
+// same number of conditional subtractions as the exact quotient's [0, 4q) / [0, 2q).
+// Measured (C1, B200): the 3-product quotient is slower in the fused kernels (4.54 vs 4.41
+// ms per step) although the plain NTT gains 3 %, so it is opt-in (EDL_SHOUP3).
+#ifdef EDL_SHOUP3_ON
+#define EDL_SHOUP3 1
+#endif
+
 // [0, 2q) result for the butterflies.
 __device__ __forceinline__ uint64_t shoup_lazy2(uint64_t y, uint64_t w, uint64_t ws, uint64_t q) {
 #ifndef EDL_APPROX_SHOUP

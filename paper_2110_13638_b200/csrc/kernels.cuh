@@ -60,6 +60,11 @@ struct Dev {
     cudaStream_t st;
     Prof* prof;
     bool ks_fused = false;      // key switch: fused modulus raise + key products (k_relin_ks, N = 2^14)
+    // relinearisation key and its copy with P^-1 folded into the data limbs (keygen):
+    // the key-product pass uses the copy when it is handed `rlk`
+    const uint64_t* rlk = nullptr;
+    const uint64_t* rlk_pf = nullptr;
+    const uint64_t* rlk_pf_c = nullptr;
 };
 
 // Supported ring degrees: 2^10 .. 2^16 (N > 2^13 runs one limb per thread-block cluster).
@@ -279,6 +284,9 @@ void launch_fetch_mapped(const Dev& d, const uint64_t* src, uint64_t* dst, int64
 // ---- randomness / keys / encryption (rng.cu) ----
 void launch_keygen(const Dev& d, uint64_t seed, uint64_t* s_hat /*[L+2][N]*/, uint64_t* pk /*[2][L+1][N]*/,
                    uint64_t* rlk /*[L+1][2][L+2][N]*/, uint64_t* rlk_s, uint64_t* scratch);
+// rlk_pf[j][c][t] = rlk[j][c][t] P^-1 mod q_t for data limbs t <= L (rlk for t = P), with
+// mulc() companions (the key-product pass's P^-1 fold moved into the key)
+void launch_fold_pinv(const Dev& d, const uint64_t* rlk, uint64_t* rlk_pf, uint64_t* rlk_pf_c);
 void launch_encrypt(const Dev& d, const int64_t* msg /*[cnt][N]*/, int64_t cnt, int l, uint64_t seed, uint32_t obj0,
                     const uint64_t* pk, uint64_t* out);
 // secret-key encryption (reading Z16) and the server-side regeneration of its seeded c1

@@ -198,18 +198,53 @@ __device__ __forceinline__ void ct_bfly(uint64_t& X, uint64_t& Y, ulonglong2 w, 
         X = bits_of(__dadd_rn(x, t));
         Y = bits_of(__dsub_rn(x, t));
     } else {
+#ifdef EDL_SHOUP3   // X, Y in [0, 8q): x in [0, 4q), t in [0, 3q) -> [0, 7q), (q, 8q)
+        const uint64_t four_q = 2 * two_q;
+        uint64_t x = csub(X, four_q);
+        uint64_t t = shoup_lazy3(Y, w.x, w.y, q);
+        X = x + t;
+        Y = x - t + four_q;
+#else
         uint64_t x = csub(X, two_q);
         uint64_t t = shoup_lazy2(Y, w.x, w.y, q);
         X = x + t;
         Y = x - t + two_q;
+#endif
     }
 }
 
 // ---- inverse GS butterfly (Harvey): X, Y in [0,2q) -> [0,2q)
 __device__ __forceinline__ void gs_bfly(uint64_t& X, uint64_t& Y, uint64_t w, uint64_t ws, uint64_t q, uint64_t two_q) {
     uint64_t x = X, y = Y;
+#ifdef EDL_SHOUP3   // X, Y in [0, 4q) -> [0, 4q), [0, 3q)
+    X = csub(x + y, 2 * two_q);
+    Y = shoup_lazy3(x - y + 2 * two_q, w, ws, q);
+#else
     X = csub(x + y, two_q);
     Y = shoup_lazy2(x - y + two_q, w, ws, q);
+#endif
+}
+// Lazy bound added before a difference in the inverse (x - y + LB >= 0): 4q or 2q.
+__device__ __forceinline__ uint64_t inv_lb(uint64_t two_q) {
+#ifdef EDL_SHOUP3
+    return 2 * two_q;
+#else
+    return two_q;
+#endif
+}
+// Canonical residue of the integer path's outputs: forward [0, 8q) (or [0, 4q)), inverse
+// [0, 3q) (or [0, 2q)).
+__device__ __forceinline__ uint64_t canon_fwd(uint64_t v, uint64_t q) {
+#ifdef EDL_SHOUP3
+    v = csub(v, 4 * q);
+#endif
+    return csub(csub(v, 2 * q), q);
+}
+__device__ __forceinline__ uint64_t canon_inv(uint64_t v, uint64_t q) {
+#ifdef EDL_SHOUP3
+    v = csub(v, 2 * q);
+#endif
+    return csub(v, q);
 }
 
 // Twiddle accessors: the global table (read-only path), or a CTA's shared-memory copy of
@@ -293,8 +328,8 @@ __device__ __forceinline__ void inv_pass_regs_t(uint64_t* x, int high, const Mod
                 uint64_t a = x[r], b = x[r + half];
                 // fp == 1 primes (2^44 <= q < 2^46) take this path with RD(w/q) companions
                 x[r] = m.fp ? tw_mul_fp(a + b, m.ninv, m.ninv_s, m.q) : shoup_lazy2(a + b, m.ninv, m.ninv_s, m.q);
-                x[r + half] = m.fp ? tw_mul_fp(a - b + two_q, m.w1ninv, m.w1ninv_s, m.q)
-                                   : shoup_lazy2(a - b + two_q, m.w1ninv, m.w1ninv_s, m.q);
+                x[r + half] = m.fp ? tw_mul_fp(a - b + inv_lb(two_q), m.w1ninv, m.w1ninv_s, m.q)
+                                   : shoup_lazy2(a - b + inv_lb(two_q), m.w1ninv, m.w1ninv_s, m.q);
             } else {
                 const int tidx = (1 << (SA + k)) + (high << k) + (r >> (NS - k));
                 ulonglong2 w = tw(tidx);
@@ -504,7 +539,7 @@ __device__ __forceinline__ void ntt_fwd_impl(uint64_t* sm, const ModInfo& m, Loa
             store.f64(C::idx(r), f64_of(v), pv[r]);
         } else {
             if constexpr (FP) v = f64_to_canon(f64_reduce(f64_of(v), qd, m.qinv_d), qd);
-            else v = csub(csub(v, two_q), q);
+            else v = canon_fwd(v, q);
             store(C::idx(r), v, pv[r]);
         }
     }
@@ -527,7 +562,7 @@ __device__ __forceinline__ void ntt_inv_impl(uint64_t* sm, const ModInfo& m, Loa
     // F64 path: residues (< 2q) in as exact binary64 integers, canonical uint64 out
     auto canon = [&](uint64_t v) {
         if constexpr (FP) return f64_to_canon(f64_of(v), qd);
-        else return csub(v, q);
+        else return canon_inv(v, q);
     };
     // outputs: canonical uint64, or (F64 path, Store with f64()) the binary64 value, |.| <= 0.625 q
     auto put = [&](int idx, uint64_t v, auto pvv) {

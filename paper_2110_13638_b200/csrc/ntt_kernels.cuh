@@ -11,6 +11,39 @@
 namespace edl {
 
 
+// Grid order of the per-(ciphertext, polynomial, output limb) forward transforms whose
+// prologue reads a per-(ciphertext, polynomial) limb once per output limb (rescale's r,
+// mod-down's r and s): launch order walks groups of EDL_L2_GROUP ciphertexts, and inside a
+// group output limb -> polynomial -> ciphertext, so a group's r / s limbs (G x 2 x 128 KB
+// at 2^14) are re-read from L2 for every output limb instead of from HBM; co-resident
+// clusters still share one output limb (one prime) at a time.  EDL_L2_GROUP = 0 restores
+// the plain (ct fastest, limb slowest) order.
+// Measured (C1, B200): the mod-down's two re-read limbs gain (0.62 -> 0.58 ms at G = 32),
+// rescale's single one loses (0.84 -> 0.86), so only k_relin_moddown_ntt uses it.
+#ifndef EDL_L2_GROUP
+#define EDL_L2_GROUP 32
+#endif
+template <class C, int G = EDL_L2_GROUP>
+__device__ __forceinline__ void grid_ct_p_i(int64_t& c, int& p, int& i) {
+    const int64_t cnt = gridDim.x >> C::LOGK;
+    if (G <= 0 || cnt <= G) {
+        c = C::bx();
+        p = blockIdx.y;
+        i = blockIdx.z;
+        return;
+    }
+    const int P2 = gridDim.y, NL = gridDim.z;
+    const int64_t lin = (int64_t)C::bx() + cnt * (blockIdx.y + (int64_t)P2 * blockIdx.z);
+    const int64_t per = (int64_t)G * P2 * NL;
+    const int64_t g = lin / per;
+    const int64_t rem = lin - g * per;
+    const int64_t gg = (cnt - g * G) < G ? (cnt - g * G) : G;
+    i = (int)(rem / (gg * P2));
+    const int64_t r2 = rem - (int64_t)i * gg * P2;
+    p = (int)(r2 / gg);
+    c = g * G + (r2 - (int64_t)p * gg);
+}
+
 // Epilogue operand of a forward transform at the output indices (a limb laid out like the
 // output): at N = 2^14 it is copied into shared memory by cp.async at the kernel's start
 // (PreStaged, ntt_core.cuh: overlapped with the whole transform, no registers held), which
@@ -160,8 +193,9 @@ k_rescale_ntt(const uint64_t* __restrict__ in, int l, const ulonglong2* __restri
               const uint64_t* __restrict__ r, const uint64_t* __restrict__ bias, uint64_t* __restrict__ out, int nlo,
               const __grid_constant__ ModTable mods, const ChainConsts* __restrict__ cc) {
     extern __shared__ uint64_t sm[];
-    const int i = blockIdx.z, p = blockIdx.y;
-    const int64_t c = C::bx();
+    int64_t c;
+    int p, i;
+    grid_ct_p_i<C, 0>(c, p, i);
     const ModInfo& m = mods[i];
     const uint64_t ql = mods[l].q;
     const uint64_t ql_mod = cc->qmod[l][i];
@@ -488,8 +522,9 @@ k_relin_moddown_ntt(const uint64_t* __restrict__ a, const uint64_t* __restrict__
                     const uint64_t* __restrict__ add_w, const uint64_t* __restrict__ add_k,
                     const __grid_constant__ ModTable mods, const ChainConsts* __restrict__ cc) {
     extern __shared__ uint64_t sm[];
-    const int i = blockIdx.z, cp = blockIdx.y;
-    const int64_t c = C::bx();
+    int64_t c;
+    int cp, i;
+    grid_ct_p_i<C>(c, cp, i);
     const ModInfo& m = mods[i];
     const uint64_t P = mods[L + 1].q;
     const uint64_t pmod = cc->qmod[L + 1][i];

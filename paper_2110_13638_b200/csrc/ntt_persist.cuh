@@ -149,7 +149,7 @@ __device__ __forceinline__ void pfwd(uint64_t* sm, const ModInfo& m, const ulong
     for (int r = 0; r < C::E; r++) {
         uint64_t v = sm[spad(tid + r * C::T)];
         if constexpr (FP) v = f64_to_canon(f64_reduce(f64_of(v), qd, m.qinv_d), qd);
-        else v = csub(csub(v, two_q), q);
+        else v = canon_fwd(v, q);
         store(C::idx(r), v);
     }
     __syncthreads();
@@ -201,7 +201,7 @@ __device__ __forceinline__ void pinv(uint64_t* sm, const ModInfo& m, const ulong
         for (int t = 0; t < C::K; t++) {
             uint64_t v = x[g * C::K + t];
             if constexpr (FP) v = f64_to_canon(f64_of(v), qd);
-            else v = csub(v, q);
+            else v = canon_inv(v, q);
             store(j0 + g * C::T + t * C::M, v);
         }
     }

@@ -888,18 +888,15 @@ constexpr int MAC3_T = 256;
 #endif
 constexpr int MAC3_CTS = EDL_MAC3_CTS;
 
+// pfold: the data targets' key entries already carry the factor P^-1 (the context's
+// P^-1-folded copy of rlk, keygen), so v = d + acc directly.
 template <int MODE, int ND>
-__global__ void __launch_bounds__(MAC3_T, 3)
-k_relin_mac3(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l, int L, int64_t cnt,
-             const uint64_t* __restrict__ xh, const uint64_t* __restrict__ rlk, const uint64_t* __restrict__ rlk_c,
-             uint64_t* __restrict__ acc, const __grid_constant__ TargetList tl, const __grid_constant__ ModTable mods,
-             const ChainConsts* __restrict__ chain, int logn) {
+__device__ __forceinline__ void mac3_body(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l, int L,
+                                          int64_t cnt, const uint64_t* __restrict__ xh, const uint64_t* __restrict__ rlk,
+                                          const uint64_t* __restrict__ rlk_c, uint64_t* __restrict__ acc, int ti, int t,
+                                          const ModInfo& m, const ChainConsts* __restrict__ chain, int logn, bool pfold,
+                                          int k) {
     constexpr bool F64 = MODE == 2;
-    const int ti = tl.slot[blockIdx.y];
-    const int t = (ti == l + 1) ? (L + 1) : ti;
-    const ModInfo& m = mods[t];
-    const int k = blockIdx.x * MAC3_T + threadIdx.x;
-    if (k >= (1 << logn)) return;
     const double qd = u52_to_double(m.q);
     // key entries of this coefficient: kv[j][cc] (binary64 on F64 targets), companions for MODE 1
     uint64_t kv[ND][2], kc[ND][2];
@@ -913,6 +910,7 @@ k_relin_mac3(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int
         }
     const bool data = ti <= l;
     const bool single = (b == nullptr);
+    const bool fold = data && !pfold;   // multiply the key sum by P^-1 here
     const ulonglong2 pinv = data ? chain->qinv[L + 1][t] : make_ulonglong2(0, 0);
     const double pinv_d = u52_to_double(pinv.x);
     const size_t limb = (size_t)1 << logn;
@@ -974,8 +972,8 @@ k_relin_mac3(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int
                     d0 = f64_mult(x0, y0, qd, m.qinv_d);
                     d1 = __dadd_rn(f64_mult(x0, y1, qd, m.qinv_d), f64_mult(x1, y0, qd, m.qinv_d));
                 }
-                s0 = __dadd_rn(d0, f64_mult(s0, pinv_d, qd, m.qinv_d));
-                s1 = __dadd_rn(d1, f64_mult(s1, pinv_d, qd, m.qinv_d));
+                s0 = __dadd_rn(d0, fold ? f64_mult(s0, pinv_d, qd, m.qinv_d) : f64_reduce(s0, qd, m.qinv_d));
+                s1 = __dadd_rn(d1, fold ? f64_mult(s1, pinv_d, qd, m.qinv_d) : f64_reduce(s1, qd, m.qinv_d));
             }
             v0 = f64_to_canon(f64_reduce(s0, qd, m.qinv_d), qd);
             v1 = f64_to_canon(f64_reduce(s1, qd, m.qinv_d), qd);
@@ -995,8 +993,8 @@ k_relin_mac3(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int
                     d0 = mulmod_fp(cur.a0, cur.b0, m);
                     d1 = addmod(mulmod_fp(cur.a0, cur.b1, m), mulmod_fp(cur.a1, cur.b0, m), m.q);
                 }
-                v0 = addmod(d0, mulc(v0, pinv, m), m.q);
-                v1 = addmod(d1, mulc(v1, pinv, m), m.q);
+                v0 = addmod(d0, fold ? mulc(v0, pinv, m) : v0, m.q);
+                v1 = addmod(d1, fold ? mulc(v1, pinv, m) : v1, m.q);
             }
         } else {
             U128 s0, s1;
@@ -1015,12 +1013,35 @@ k_relin_mac3(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int
                     d0 = mulmod_barrett(cur.a0, cur.b0, m);
                     d1 = addmod(mulmod_barrett(cur.a0, cur.b1, m), mulmod_barrett(cur.a1, cur.b0, m), m.q);
                 }
-                v0 = addmod(d0, mulc(v0, pinv, m), m.q);
-                v1 = addmod(d1, mulc(v1, pinv, m), m.q);
+                v0 = addmod(d0, fold ? mulc(v0, pinv, m) : v0, m.q);
+                v1 = addmod(d1, fold ? mulc(v1, pinv, m) : v1, m.q);
             }
         }
         acc[((((size_t)c * 2 + 0) * (l + 2) + ti) << logn) + k] = v0;
         acc[((((size_t)c * 2 + 1) * (l + 2) + ti) << logn) + k] = v1;
+    }
+}
+
+// MODE >= 0: one arithmetic path for every target of the launch; MODE = -1: the targets of
+// all paths in ONE launch (per-CTA branch on the target's mode), so the memory-latency-bound
+// F64 targets and the IMAD-bound 60-bit targets share the SMs instead of running back to back.
+template <int MODE, int ND>
+__global__ void __launch_bounds__(MAC3_T, 3)
+k_relin_mac3(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l, int L, int64_t cnt,
+             const uint64_t* __restrict__ xh, const uint64_t* __restrict__ rlk, const uint64_t* __restrict__ rlk_c,
+             uint64_t* __restrict__ acc, const __grid_constant__ TargetList tl, const __grid_constant__ ModTable mods,
+             const ChainConsts* __restrict__ chain, int logn, int pfold) {
+    const int ti = tl.slot[blockIdx.y];
+    const int t = (ti == l + 1) ? (L + 1) : ti;
+    const ModInfo& m = mods[t];
+    const int k = blockIdx.x * MAC3_T + threadIdx.x;
+    if (k >= (1 << logn)) return;
+    if constexpr (MODE >= 0) {
+        mac3_body<MODE, ND>(a, b, l, L, cnt, xh, rlk, rlk_c, acc, ti, t, m, chain, logn, pfold != 0, k);
+    } else {
+        // (the launcher sends MODE-1 targets, 2^44 <= q < 2^46, to their own launch)
+        if (m.fp == 2) mac3_body<2, ND>(a, b, l, L, cnt, xh, rlk, rlk_c, acc, ti, t, m, chain, logn, pfold != 0, k);
+        else mac3_body<0, ND>(a, b, l, L, cnt, xh, rlk, rlk_c, acc, ti, t, m, chain, logn, pfold != 0, k);
     }
 }
 
@@ -1273,15 +1294,35 @@ void launch_relin_mac(const Dev& d, const uint64_t* a, const uint64_t* b, int64_
 #ifndef EDL_MAC2
     if (l + 1 <= 6 && d.logn >= 8) {   // round 2: k_relin_mac3
         const unsigned gx3 = (unsigned)((1 << d.logn) / MAC3_T), gz3 = (unsigned)((cnt + MAC3_CTS - 1) / MAC3_CTS);
+        // the relinearisation key's P^-1-folded copy (data targets), when these are its keys
+        const int pfold = (rlk == d.rlk && d.rlk_pf != nullptr) ? 1 : 0;
+        const uint64_t* kk = pfold ? d.rlk_pf : rlk;
+        const uint64_t* kkc = pfold ? d.rlk_pf_c : rlk_c;
+        TargetList all;
+        int na = 0;
+        for (int k = 0; k < n6; k++) all.slot[na++] = t6.slot[k];
+        for (int k = 0; k < ni; k++) all.slot[na++] = ti.slot[k];
+#ifndef EDL_MAC3_SPLIT
+#define EDL_MAC3_ND(ND)                                                                                            \
+    case ND:                                                                                                       \
+        if (na)                                                                                                    \
+            EDL_LAUNCH(d, "k_relin_mac", (k_relin_mac3<-1, ND><<<dim3(gx3, na, gz3), MAC3_T, 0, d.st>>>(          \
+                                             a, b, l, d.L, cnt, xh, kk, kkc, acc, all, *d.mt, d.cc, d.logn, pfold))); \
+        if (nf)                                                                                                    \
+            EDL_LAUNCH(d, "k_relin_mac", (k_relin_mac3<1, ND><<<dim3(gx3, nf, gz3), MAC3_T, 0, d.st>>>(           \
+                                             a, b, l, d.L, cnt, xh, kk, kkc, acc, tf, *d.mt, d.cc, d.logn, pfold))); \
+        break;
+#else
 #define EDL_MAC3(FPV, ND, LIST, NT)                                                                   \
     EDL_LAUNCH(d, "k_relin_mac", (k_relin_mac3<FPV, ND><<<dim3(gx3, NT, gz3), MAC3_T, 0, d.st>>>( \
-                                     a, b, l, d.L, cnt, xh, rlk, rlk_c, acc, LIST, *d.mt, d.cc, d.logn)))
+                                     a, b, l, d.L, cnt, xh, kk, kkc, acc, LIST, *d.mt, d.cc, d.logn, pfold)))
 #define EDL_MAC3_ND(ND)                                  \
     case ND:                                             \
         if (n6) EDL_MAC3(2, ND, t6, n6);                 \
         if (nf) EDL_MAC3(1, ND, tf, nf);                 \
         if (ni) EDL_MAC3(0, ND, ti, ni);                 \
         break;
+#endif
         switch (l + 1) {
             EDL_MAC3_ND(1)
             EDL_MAC3_ND(2)
@@ -1291,7 +1332,9 @@ void launch_relin_mac(const Dev& d, const uint64_t* a, const uint64_t* b, int64_
             EDL_MAC3_ND(6)
         }
 #undef EDL_MAC3_ND
+#ifdef EDL_MAC3
 #undef EDL_MAC3
+#endif
         return;
     }
 #endif
@@ -1406,10 +1449,13 @@ void launch_cc_mac(const Dev& d, const uint64_t* x, int l, int H, int W, int F, 
     EDL_LAUNCH(d, "k_cc_mac", k_cc_mac<<<grid, PW_THREADS, smem, d.st>>>(x, l, H, W, F, kh, kw, stride, wk, out, *d.mt, d.logn));
 }
 
+#ifndef EDL_DN3_CTAS_PER_SM
+#define EDL_DN3_CTAS_PER_SM 28   // several waves of short CTAs (1.5 waves of long ones left a tail)
+#endif
 int dense_split(const Dev& d, int64_t K, int64_t O, int l) {
-    if (O <= 16 && d.logn >= 7) {   // k_dense_mac3: ~8 CTAs of 128 threads per SM, K slices of >= 8 inputs
+    if (O <= 16 && d.logn >= 7) {   // k_dense_mac3: K slices of >= 8 inputs
         const int64_t base = (int64_t)((1 << d.logn) / DN3_T) * 2 * (l + 1);
-        int64_t ks = (8 * 148 + base - 1) / base;
+        int64_t ks = (EDL_DN3_CTAS_PER_SM * 148 + base - 1) / base;
         if (ks > K / 8) ks = K / 8;
         if (ks > 32) ks = 32;
         return ks < 1 ? 1 : (int)ks;
@@ -1426,7 +1472,7 @@ void launch_dense_mac(const Dev& d, const uint64_t* x, int64_t K, int64_t O, int
     if (O <= 16 && d.logn >= 7) {
         const int kper = (int)((K + ks - 1) / ks);
         if (kper <= 256) {   // exact binary64 / 128-bit sums bounded for <= 256 terms
-            const int oc = O <= 4 ? 4 : (O <= 8 ? 8 : (O <= 12 ? 12 : 16));
+            const int oc = O <= 4 ? 4 : (O <= 8 ? 8 : (O == 10 ? 10 : (O <= 12 ? 12 : 16)));
             dim3 grid((unsigned)((1 << d.logn) / DN3_T), (unsigned)(2 * (l + 1)), (unsigned)ks);
             const size_t smem = (size_t)kper * oc * sizeof(ulonglong2);
             uint64_t* dst = ks > 1 ? part : out;
@@ -1434,6 +1480,7 @@ void launch_dense_mac(const Dev& d, const uint64_t* x, int64_t K, int64_t O, int
             switch (oc) {
                 case 4: EDL_DN3(4); break;
                 case 8: EDL_DN3(8); break;
+                case 10: EDL_DN3(10); break;   // C1's 245 -> 10
                 case 12: EDL_DN3(12); break;
                 default: EDL_DN3(16); break;
             }

@@ -50,6 +50,29 @@ void launch_expand_sk_a(const Dev& d, uint64_t* ct, int64_t cnt, int l, uint64_t
     EDL_LAUNCH(d, "k_expand_sk_a", k_expand_sk_a<<<grid, 256, 0, d.st>>>(ct, cnt, l, seed, obj0, *d.mt, d.logn));
 }
 
+__global__ void k_fold_pinv(const uint64_t* __restrict__ rlk, uint64_t* __restrict__ pf, uint64_t* __restrict__ pfc,
+                            int L, const __grid_constant__ ModTable mods, const ChainConsts* __restrict__ cc, int logn) {
+    const int64_t rows = (int64_t)(L + 1) * 2 * (L + 2);
+    const int n = 1 << logn;
+    for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
+        const int t = (int)(row % (L + 2));
+        const ModInfo& m = mods[t];
+        const ulonglong2 pinv = (t <= L) ? cc->qinv[L + 1][t] : make_ulonglong2(1, 0);
+        const uint64_t* src = rlk + ((size_t)row << logn);
+        for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+            const uint64_t v = (t <= L) ? mulc(src[k], pinv, m) : src[k];
+            pf[((size_t)row << logn) + k] = v;
+            pfc[((size_t)row << logn) + k] = key_companion(v, m);
+        }
+    }
+}
+
+void launch_fold_pinv(const Dev& d, const uint64_t* rlk, uint64_t* rlk_pf, uint64_t* rlk_pf_c) {
+    const int64_t rows = (int64_t)(d.L + 1) * 2 * (d.L + 2);
+    const dim3 grid((unsigned)((1 << d.logn) / 256), (unsigned)(rows < 65535 ? rows : 65535));
+    EDL_LAUNCH(d, "k_fold_pinv", k_fold_pinv<<<grid, 256, 0, d.st>>>(rlk, rlk_pf, rlk_pf_c, d.L, *d.mt, d.cc, d.logn));
+}
+
 void launch_keygen_galois(const Dev& d, uint64_t seed, uint32_t g, const uint64_t* s_hat, uint64_t* gk, uint64_t* gk_c) {
     EDL_DISPATCH_LOGN(d.logn, launch_keygen_galois_n<LOGN>(d, seed, g, s_hat, gk, gk_c));
 }
