@@ -296,6 +296,17 @@ C1_ALG_LIMBS = {
 }
 C1_ALG_BYTES = {k: v * _LIMB for k, v in C1_ALG_LIMBS.items()}
 
+# Modular MACs of one C1 step per MAC kernel, (F64-path 40-bit limbs, 60-bit limbs): CC
+# 245 outputs x 16 taps x 2 polys x N on q1..q4 | q0; dense 245 x 10 x 2 x N on q1 | q0; key
+# products per (ciphertext, target, coefficient): 2 (l+1) key MACs + the tensor's 4 products
+# on data targets (q0 and P are the 60-bit targets), l = 3 and l = 2.
+_N14 = 1 << 14
+C1_MACS = {
+    "k_cc_mac": (245 * 16 * 2 * 4 * _N14, 245 * 16 * 2 * 1 * _N14),
+    "k_dense_mac": (245 * 10 * 2 * _N14, 245 * 10 * 2 * _N14),
+    "k_relin_mac": (245 * _N14 * (3 * 12 + 2 * 10), 245 * _N14 * ((12 + 8) + (10 + 6))),
+}
+
 
 def ntt_roofline(name, ms_total, steps, n, peak_int, peak_fp):
     """Achieved algorithmic butterflies/s of one NTT-family kernel over the timed region
@@ -535,6 +546,8 @@ def run_ours(a):
     peak_fp = ctx.bfly_peak(1)           # q1 (40-bit): FP64-pipe path
     dfma = ctx.pipe_peak(0)              # raw FP64 pipe: DFMA lane-ops/s
     imadw = ctx.pipe_peak(1)             # raw integer multiply: IMAD.WIDE.U32 lane-ops/s
+    fmac = ctx.pipe_peak(2)              # F64 modular MAC (40-bit limbs of the MAC layers) / s
+    imac = ctx.pipe_peak(3)              # 128-bit lazy MAC (60-bit limbs) / s
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     nominal_dp = sms * 64 * 1965e6       # 64 FP64 lanes / SM / clk at the max SM clock
     hbm_peak = None
@@ -558,7 +571,11 @@ def run_ours(a):
             if name in C1_TRANSFORMS:
                 ach, pk = ntt_roofline(name, ms_tot, a.steps, n, peak_int, peak_fp)
                 e.update({"achieved_Gbfly_s": ach / 1e9, "peak_Gbfly_s": pk / 1e9, "bfly_frac": ach / pk})
-            fr = {"hbm": e.get("hbm_frac", 0.0), "alu": e.get("bfly_frac", 0.0)}
+            if name in C1_MACS:   # MAC layers: time at the measured MAC ceilings / measured time
+                nf, ni = C1_MACS[name]
+                t_peak = nf / fmac + ni / imac
+                e.update({"macs_per_step": nf + ni, "mac_alu_frac": t_peak / (ms_k / 1e3)})
+            fr = {"hbm": e.get("hbm_frac", 0.0), "alu": e.get("bfly_frac", e.get("mac_alu_frac", 0.0))}
             e["bound"] = max(fr, key=fr.get) if any(fr.values()) else None
             if name in traffic_tab:
                 e["dram_bytes_per_step_ncu"] = traffic_tab[name]["dram_bytes_per_step"]
@@ -582,6 +599,7 @@ def run_ours(a):
                              "kernel's own arithmetic paths, weighted by its 60-bit/40-bit transform mix",
                 "peak_int_Gbfly_s": peak_int / 1e9, "peak_fp_Gbfly_s": peak_fp / 1e9,
                 "pipe_anchor": {"dfma_lane_ops_per_s": dfma, "imad_wide_lane_ops_per_s": imadw,
+                                "f64_mac_per_s": fmac, "mac128_per_s": imac,
                                 "nominal_fp64_lane_ops_per_s": nominal_dp,
                                 "fp_bfly_vs_dfma": peak_fp * 8 / dfma,
                                 "note": "F64 butterfly = 8 FP64 instructions: peak_fp * 8 / dfma = the "

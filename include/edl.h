@@ -320,10 +320,12 @@ edl_status edl_modmul_peak(edl_ctx* ctx, int32_t iters, double* modmul_per_s);
  * take for that modulus (FP64 quotient if q < 2^50, Shoup otherwise).  Writes butterflies
  * per second to *bfly_per_s.  Synchronises.  EDL_ERR_ARG on a bad index or iters <= 0. */
 edl_status edl_bfly_peak(edl_ctx* ctx, int32_t prime_index, int32_t iters, double* bfly_per_s);
-/* Raw pipe probes anchoring the butterfly ceilings: lane-operations per second of
- * register-only chains of DFMA (which = 0, the FP64 pipe) or 32x32->64 IMAD.WIDE.U32
- * (which = 1, the integer multiply the Shoup butterflies are built from) on every SM
- * (8 CTAs of 256 threads per SM, 8 independent chains per thread).  Synchronises. */
+/* Raw pipe probes anchoring the butterfly and MAC ceilings: lane-operations per second of
+ * register-only chains of DFMA (which = 0, the FP64 pipe), 32x32->64 IMAD.WIDE.U32
+ * (which = 1, the integer multiply the Shoup butterflies are built from), the F64 modular
+ * MAC acc += x w mod q (which = 2, the MAC layers' 40-bit path) or the 128-bit lazy MAC
+ * acc += x w (which = 3, their 60-bit path), on every SM (8 CTAs of 256 threads per SM,
+ * 8 independent chains per thread).  EDL_ERR_ARG for another `which`.  Synchronises. */
 edl_status edl_pipe_peak(edl_ctx* ctx, int32_t which, int32_t iters, double* ops_per_s);
 /* Copy the secret key s_hat [L+2][N], public key [2][L+1][N] or rlk [L+1][2][L+2][N]
  * to host (which: 0, 1, 2).  For parity tests. */

@@ -1400,7 +1400,7 @@ edl_status edl_modmul_peak(edl_ctx* c, int32_t iters, double* modmul_per_s) {
 }
 
 edl_status edl_pipe_peak(edl_ctx* c, int32_t which, int32_t iters, double* ops_per_s) {
-    if (!c || !ops_per_s || iters <= 0 || which < 0 || which > 1) return EDL_ERR_ARG;
+    if (!c || !ops_per_s || iters <= 0 || which < 0 || which > 3) return EDL_ERR_ARG;
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
     const int blocks = sms * 8;

@@ -104,9 +104,61 @@ __global__ void __launch_bounds__(256) k_pipe_imadw(uint32_t a, int iters, uint6
     if (acc == 0x123456789ull) sink[0] = acc;
 }
 
+// Modular multiply-accumulate ceilings of the MAC layers (register-only, 8 independent
+// accumulators per thread): (2) the F64 path acc += f64_mulc(x, w, RD(w/q), q) for a 40-bit
+// prime, (3) the 60-bit path's lazy 128-bit acc += x w (mac128).  One MAC per lane-op.
+__global__ void __launch_bounds__(256) k_pipe_fmac(double q, double w, double wq, int iters, uint64_t* sink) {
+    double acc[8], x[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        acc[k] = 0.0;
+        x[k] = (double)(threadIdx.x * 8 + k + 1);
+    }
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int k = 0; k < 8; k++) acc[k] = __dadd_rn(acc[k], f64_mulc(x[k], w, wq, q));
+#pragma unroll
+        for (int k = 0; k < 8; k++) x[k] = __dadd_rn(x[k], 1.0);   // fresh operands (exact, small)
+        if ((it & 255) == 255) {
+#pragma unroll
+            for (int k = 0; k < 8; k++) acc[k] = f64_reduce(acc[k], q, 1.0 / q);
+        }
+    }
+    double a = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) a += acc[k];
+    if (a == 1.5) sink[0] = 1;
+}
+__global__ void __launch_bounds__(256) k_pipe_imac(uint64_t w, int iters, uint64_t* sink) {
+    U128 acc[8];
+    uint64_t x[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        acc[k].lo = acc[k].hi = 0;
+        x[k] = threadIdx.x * 8 + k + 1;
+    }
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int k = 0; k < 8; k++) mac128(acc[k], x[k], w);
+#pragma unroll
+        for (int k = 0; k < 8; k++) x[k] += 0x9E3779B97F4A7C15ull;
+    }
+    uint64_t a = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) a ^= acc[k].lo ^ acc[k].hi;
+    if (a == 0x123456789ull) sink[0] = a;
+}
+
 void launch_pipe_probe(const Dev& d, int which, int iters, int blocks, uint64_t* sink) {
     if (which == 0) EDL_LAUNCH(d, "k_pipe_dfma", k_pipe_dfma<<<blocks, 256, 0, d.st>>>(1.0000001, 1e-9, iters, sink));
-    else EDL_LAUNCH(d, "k_pipe_imadw", k_pipe_imadw<<<blocks, 256, 0, d.st>>>(0x9E3779B9u, iters, sink));
+    else if (which == 1) EDL_LAUNCH(d, "k_pipe_imadw", k_pipe_imadw<<<blocks, 256, 0, d.st>>>(0x9E3779B9u, iters, sink));
+    else if (which == 2) {
+        const double q = 1099511627689.0, w = 777777777777.0;   // a 40-bit odd modulus, w < q
+        EDL_LAUNCH(d, "k_pipe_fmac", k_pipe_fmac<<<blocks, 256, 0, d.st>>>(q, w, __builtin_floor(w / q * 1e15) / 1e15, iters,
+                                                                           sink));
+    } else {
+        EDL_LAUNCH(d, "k_pipe_imac", k_pipe_imac<<<blocks, 256, 0, d.st>>>(0xFEDCBA987654321ull, iters, sink));
+    }
 }
 
 void launch_modmul_peak(const Dev& d, uint64_t q, uint64_t w, uint64_t ws, int iters, int blocks, uint64_t* sink) {
