@@ -67,6 +67,8 @@ struct edl_ctx {
     // Key switches of many ciphertexts in chunks of ks_chunk (EDL_KS_CHUNK, 0 = two halves)
     // alternating over the two streams, so each chunk's raised digits stay in L2.
     int64_t ks_chunk = 0;
+    // d2 INTT + modulus raise in one kernel (EDL_RAISE_FUSED=1, N = 2^14)
+    bool raise_fused = false;
 
     Dev dev() const {
         Dev d;
@@ -79,6 +81,7 @@ struct edl_ctx {
         d.st = st;
         d.prof = &prof;
         d.ks_fused = ks_fused;
+        d.raise_fused = raise_fused;
         d.rlk = d_rlk;
         d.rlk_pf = ks_fused ? nullptr : d_rlk_pf;   // the fused kernel applies P^-1 itself
         d.rlk_pf_c = d_rlk_pf_c;
@@ -372,6 +375,8 @@ edl_status edl_ctx_create(const edl_params* p, int32_t device, void* stream, edl
     {
         const char* e = std::getenv("EDL_KS_FUSED");
         c->ks_fused = e && e[0] == '1';
+        const char* rf = std::getenv("EDL_RAISE_FUSED");
+        c->raise_fused = rf && rf[0] == '1';
         const char* k = std::getenv("EDL_KS_CHUNK");
         c->ks_chunk = k ? std::atoll(k) : 0;
     }

@@ -60,6 +60,7 @@ struct Dev {
     cudaStream_t st;
     Prof* prof;
     bool ks_fused = false;      // key switch: fused modulus raise + key products (k_relin_ks, N = 2^14)
+    bool raise_fused = false;   // key switch: fused d2 INTT + modulus raise (k_relin_raise, N = 2^14)
     // relinearisation key and its copy with P^-1 folded into the data limbs (keygen):
     // the key-product pass uses the copy when it is handed `rlk`
     const uint64_t* rlk = nullptr;

@@ -465,6 +465,70 @@ k_relin_ks(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l
     }
 }
 
+// M1 + M2a fused (round 2, EDL_RAISE_FUSED=1): CTA (cluster) = (ciphertext c, digit j).
+// a_j = INTT_{q_j}(a1_j b1_j), kept in a shared-memory copy (thread-private slots: the
+// inverse's output indices of a thread are exactly the forward transform's phase-A input
+// indices of the same thread), then x_{j,t} = NTT_t(a_j mod t) for every target t != j
+// (t = q_0..q_l, P): the digit never round-trips through HBM and no transform waits on a
+// global load of it.
+template <class C>
+__device__ __forceinline__ int raise_slot(int idx) {   // register slot (g K + t) of coefficient idx
+    const int t = idx >> C::LOGM;
+    const int g = ((idx & (C::M - 1)) - (C::crank() * (C::M / C::K) + (int)threadIdx.x)) / C::T;
+    return g * C::K + t;
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::T, C::MINB)
+k_relin_raise(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l, int L, uint64_t* __restrict__ xh,
+              const __grid_constant__ ModTable mods) {
+    static_assert(C::K > 1, "cluster configuration");
+    extern __shared__ __align__(16) uint64_t sm[];
+    uint64_t* dig = sm + C::SMEM_WORDS;   // [E][T]
+    const int j = blockIdx.y;
+    const int64_t c = C::bx();
+    const int tid = threadIdx.x;
+    {
+        const ModInfo& m = mods[j];
+        const uint64_t* a1 = a + limb_off(c, 1, j, l + 1, C::LOGN);
+        const uint64_t* b1 = b ? b + limb_off(c, 1, j, l + 1, C::LOGN) : a1;
+        const bool single = (b == nullptr);
+        struct Load {   // d2 = a1 b1 (or a1); F64 limbs: the exact product on the FP64 pipe
+            const uint64_t *a1, *b1;
+            bool single;
+            const ModInfo& m;
+            __device__ __forceinline__ uint64_t operator()(int idx) const {
+                return single ? a1[idx] : mulmod(a1[idx], b1[idx], m);
+            }
+            __device__ __forceinline__ double f64(int idx) const {
+                const double x = u52_to_double(a1[idx]);
+                if (single) return x;
+                const double y = u52_to_double(b1[idx]), qd = u52_to_double(m.q);
+                const double hi = __dmul_rn(x, y);
+                const double lo = __fma_rn(x, y, -hi);
+                const double qt = __dsub_rn(__fma_rn(hi, m.qinv_d, F64_RND), F64_RND);
+                return __dadd_rn(__fma_rn(-qt, qd, hi), lo);
+            }
+        };
+        auto st = [&](int idx, uint64_t v) { dig[raise_slot<C>(idx) * C::T + tid] = v; };
+        ntt_inv<C>(sm, m, Load{a1, b1, single, m}, st);
+    }
+    const uint64_t qj = mods[j].q;
+    for (int ti = 0; ti <= l + 1; ti++) {
+        if (ti == j) continue;
+        const int t = (ti == l + 1) ? (L + 1) : ti;
+        const ModInfo& m = mods[t];
+        const bool need_red = qj > 4 * m.q;   // the forward NTT accepts [0, 4q)
+        uint64_t* dst = xh + ((((size_t)c * (l + 1) + j) * (l + 2) + ti) << C::LOGN);
+        auto ld = [&](int idx) {
+            const uint64_t v = dig[raise_slot<C>(idx) * C::T + tid];
+            return need_red ? reduce64(v, m) : v;
+        };
+        auto st = [&](int idx, uint64_t v) { dst[idx] = v; };
+        ntt_fwd<C>(sm, m, ld, st);
+    }
+}
+
 template <class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
 k_relin_moddown_intt(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l,
@@ -650,6 +714,19 @@ void launch_relin_n(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t 
     // (2-CTA clusters of 512 threads, 2 CTAs/SM at 2^14): 1.22 vs 1.32 ms per C1 step
     using CP = CfgFused<LOGN>;
     const int rs = rescale ? 1 : 0;
+    if (LOGN == 14 && d.raise_fused && !d.ks_fused) {
+        using CR = NttCfg<14, 2, 4, 3>;   // 3 CTAs per SM: transform buffer + digit copy
+        launch_cfg_x<CR>(d, "k_relin_raise", k_relin_raise<CR>, dim3((unsigned)cnt, l + 1), CR::M * 8, a, b, l, d.L, xh,
+                         *d.mt);
+        launch_relin_mac(d, a, b, cnt, l, xh, rlk, rlk_c, acc);
+        launch_cfg<C>(d, "k_relin_moddown_intt", k_relin_moddown_intt<C>, dim3((unsigned)cnt, 2), a, b, l,
+                      (const uint64_t*)acc, d.L, rs, r, s, *d.mt, d.cc);
+        launch_cfg<C>(d, "k_relin_moddown_ntt", k_relin_moddown_ntt<C>, dim3((unsigned)cnt, 2, rescale ? l : l + 1), a, b,
+                      l, (const uint64_t*)acc, (const uint64_t*)r, (const uint64_t*)s, d.L, rs, out, add_w, add_k, *d.mt,
+                      d.cc);
+        (void)acoef;
+        return;
+    }
     launch_cfg<C>(d, "k_relin_intt_d2", k_relin_intt_d2<C>, dim3((unsigned)cnt, l + 1), a, b, l, acoef, *d.mt);
 #ifndef EDL_NO_KS_FUSED
     if (LOGN == 14 && d.ks_fused) {

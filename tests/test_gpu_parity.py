@@ -675,3 +675,19 @@ def test_chunked_keyswitch_bit_exact(edl, monkeypatch):
     X = ock.CtArray(_rand_ct(o, 37, 2, 171), 2, 2.0 ** 40, o.key_id)
     got = g.poly_activation(_to_gpu(g, X.data, 2, X.scale, o.key_id), [0.0, 0.0, 1.0])
     assert np.array_equal(got.numpy(g.n), olay.poly_activation(o, X, [0.0, 0.0, 1.0]).data)
+
+
+def test_fused_raise_bit_exact(edl, monkeypatch):
+    """The fused d2 INTT + modulus raise (k_relin_raise, EDL_RAISE_FUSED=1) against the
+    oracle: mul_relin at every level of the C1 chain (16 ciphertexts: both stream halves)
+    and the sigma_a layer."""
+    monkeypatch.setenv("EDL_RAISE_FUSED", "1")
+    g, o = _pair(edl, depth=4)
+    for lvl in (1, 2, 3, 4):
+        A = ock.CtArray(_rand_ct(o, 16, lvl, 181 + lvl), lvl, 2.0 ** 40, o.key_id)
+        B = ock.CtArray(_rand_ct(o, 16, lvl, 191 + lvl), lvl, 2.0 ** 40, o.key_id)
+        got = g.mul_relin(_to_gpu(g, A.data, lvl, A.scale, o.key_id), _to_gpu(g, B.data, lvl, B.scale, o.key_id))
+        assert np.array_equal(got.numpy(g.n), o.mul_relin(A, B).data), lvl
+    X = ock.CtArray(_rand_ct(o, 3, 3, 199), 3, 2.0 ** 40, o.key_id)
+    got = g.poly_activation(_to_gpu(g, X.data, 3, X.scale, o.key_id), [0.5, 0.197, 0.0, -0.004])
+    assert np.array_equal(got.numpy(g.n), olay.poly_activation(o, X, [0.5, 0.197, 0.0, -0.004]).data)

@@ -50,6 +50,20 @@ def main():
     x = ctx.encrypt_poly(polys, scale=2.0 ** 40, enc_seed=2)
     net = C1Net(ctx, K, kb, W, b)
     res["c1_step_ms"] = time_ms(lambda: net.forward(x), reps=3)
+    for ev in os.environ.get("EDL_BENCH_ENVS", "").split(";"):
+        if ev:   # the same C1 step under a context-creation switch, e.g. EDL_RAISE_FUSED=1
+            k_, v_ = ev.split("=")
+            os.environ[k_] = v_
+            cx = edl.Context(edl.params_from_depth(4)).keygen(1)
+            xc = cx.encrypt_poly(polys, scale=2.0 ** 40, enc_seed=2)
+            nc = C1Net(cx, K, kb, W, b)
+            res[f"c1_step_ms[{ev}]"] = time_ms(lambda: nc.forward(xc), reps=3)
+            cx.profile(True)
+            nc.forward(xc)
+            res[f"c1_kernels_ms[{ev}]"] = {k: round(v[0], 3) for k, v in cx.profile_read().items()}
+            cx.profile(False)
+            del nc, xc, cx
+            os.environ.pop(k_)
     for ch in os.environ.get("EDL_BENCH_CHUNKS", "").split(","):
         if ch:   # the same C1 step with key switches in chunks (EDL_KS_CHUNK, read at context creation)
             os.environ["EDL_KS_CHUNK"] = ch
