@@ -529,10 +529,12 @@ k_relin_raise(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, in
     }
 }
 
-template <class C>
+// RESCALE is a template parameter (round 2): each instantiation compiles only its own
+// transforms and epilogues, which halves the mod-down kernels' spills at 64 registers.
+template <class C, bool RESCALE>
 __global__ void __launch_bounds__(C::T, C::MINB)
 k_relin_moddown_intt(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l,
-                     const uint64_t* __restrict__ acc, int L, int rescale, uint64_t* __restrict__ r_out,
+                     const uint64_t* __restrict__ acc, int L, int rescale_unused, uint64_t* __restrict__ r_out,
                      uint64_t* __restrict__ s_out, const __grid_constant__ ModTable mods,
                      const ChainConsts* __restrict__ cc) {
     extern __shared__ uint64_t sm[];
@@ -541,6 +543,8 @@ k_relin_moddown_intt(const uint64_t* __restrict__ a, const uint64_t* __restrict_
     const ModInfo& mp = mods[L + 1];
     const uint64_t* accP = acc + ((((size_t)c * 2 + cp) * (l + 2) + (l + 1)) << C::LOGN);
     uint64_t* rdst = r_out + (((size_t)c * 2 + cp) << C::LOGN);
+    constexpr bool rescale = RESCALE;
+    (void)rescale_unused;
     if (threadIdx.x == 0) {
         if (rescale) pf_own<C>(acc + ((((size_t)c * 2 + cp) * (l + 2) + l) << C::LOGN));
         pf_next_wave<C>([&](int64_t bx, int cr, int y, int) {
@@ -552,7 +556,7 @@ k_relin_moddown_intt(const uint64_t* __restrict__ a, const uint64_t* __restrict_
         auto st = [&](int idx, uint64_t v) { rdst[idx] = v; };
         ntt_inv<C>(sm, mp, ld, st);
     }
-    if (!rescale) return;
+    if constexpr (!RESCALE) return;
     const ModInfo& ml = mods[l];
     const ulonglong2 pinv = cc->qinv[L + 1][l];
     const uint64_t pmod = cc->qmod[L + 1][l];
@@ -578,11 +582,11 @@ k_relin_moddown_intt(const uint64_t* __restrict__ a, const uint64_t* __restrict_
     ntt_inv<C>(sm, ml, ld, pre, Store{sdst, mp.q, pmod, pinv, ml});
 }
 
-template <class C>
+template <class C, bool RESCALE>
 __global__ void __launch_bounds__(C::T, C::MINB)
 k_relin_moddown_ntt(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l,
                     const uint64_t* __restrict__ acc, const uint64_t* __restrict__ r,
-                    const uint64_t* __restrict__ s, int L, int rescale, uint64_t* __restrict__ out,
+                    const uint64_t* __restrict__ s, int L, int rescale_unused, uint64_t* __restrict__ out,
                     const uint64_t* __restrict__ add_w, const uint64_t* __restrict__ add_k,
                     const __grid_constant__ ModTable mods, const ChainConsts* __restrict__ cc) {
     extern __shared__ uint64_t sm[];
@@ -596,6 +600,8 @@ k_relin_moddown_ntt(const uint64_t* __restrict__ a, const uint64_t* __restrict__
     const uint64_t* rr = r + (((size_t)c * 2 + cp) << C::LOGN);
     const uint64_t* ss = s + (((size_t)c * 2 + cp) << C::LOGN);
     const uint64_t* vi = acc + ((((size_t)c * 2 + cp) * (l + 2) + i) << C::LOGN);   // d_i + acc_i P^-1 (M2b)
+    constexpr bool rescale = RESCALE;
+    (void)rescale_unused;
     const int nlo = rescale ? l : l + 1;
     uint64_t* dst = out + limb_off(c, cp, i, nlo, C::LOGN);
     if (threadIdx.x == 0) {   // epilogue operand of this CTA, prologue inputs of the next wave
@@ -605,7 +611,7 @@ k_relin_moddown_ntt(const uint64_t* __restrict__ a, const uint64_t* __restrict__
             if (rescale) pf_sub<C>(s + (((size_t)bx * 2 + y) << C::LOGN), cr, true);
         });
     }
-    if (rescale) {
+    if constexpr (RESCALE) {
         const uint64_t ql = mods[l].q;
         const uint64_t qlmod = cc->qmod[l][i];
         const ulonglong2 qlinv = cc->qinv[l][i];
@@ -719,9 +725,9 @@ void launch_relin_n(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t 
         launch_cfg_x<CR>(d, "k_relin_raise", k_relin_raise<CR>, dim3((unsigned)cnt, l + 1), CR::M * 8, a, b, l, d.L, xh,
                          *d.mt);
         launch_relin_mac(d, a, b, cnt, l, xh, rlk, rlk_c, acc);
-        launch_cfg<C>(d, "k_relin_moddown_intt", k_relin_moddown_intt<C>, dim3((unsigned)cnt, 2), a, b, l,
+        launch_cfg<C>(d, "k_relin_moddown_intt", (rescale ? k_relin_moddown_intt<C, true> : k_relin_moddown_intt<C, false>), dim3((unsigned)cnt, 2), a, b, l,
                       (const uint64_t*)acc, d.L, rs, r, s, *d.mt, d.cc);
-        launch_cfg<C>(d, "k_relin_moddown_ntt", k_relin_moddown_ntt<C>, dim3((unsigned)cnt, 2, rescale ? l : l + 1), a, b,
+        launch_cfg<C>(d, "k_relin_moddown_ntt", (rescale ? k_relin_moddown_ntt<C, true> : k_relin_moddown_ntt<C, false>), dim3((unsigned)cnt, 2, rescale ? l : l + 1), a, b,
                       l, (const uint64_t*)acc, (const uint64_t*)r, (const uint64_t*)s, d.L, rs, out, add_w, add_k, *d.mt,
                       d.cc);
         (void)acoef;
@@ -745,10 +751,11 @@ void launch_relin_n(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t 
                        (const uint64_t*)acoef, l, d.L, xh, *d.mt);
         launch_relin_mac(d, a, b, cnt, l, xh, rlk, rlk_c, acc);   // acc slots 0..l hold v
     }
-    launch_cfg<C>(d, "k_relin_moddown_intt", k_relin_moddown_intt<C>, dim3((unsigned)cnt, 2), a, b, l, (const uint64_t*)acc,
-                  d.L, rs, r, s, *d.mt, d.cc);
+    launch_cfg<C>(d, "k_relin_moddown_intt", (rescale ? k_relin_moddown_intt<C, true> : k_relin_moddown_intt<C, false>),
+                  dim3((unsigned)cnt, 2), a, b, l, (const uint64_t*)acc, d.L, rs, r, s, *d.mt, d.cc);
     using CE = CfgEpi<LOGN>;
-    launch_cfg_x<CE>(d, "k_relin_moddown_ntt", k_relin_moddown_ntt<CE>, dim3((unsigned)cnt, 2, rescale ? l : l + 1),
+    launch_cfg_x<CE>(d, "k_relin_moddown_ntt", (rescale ? k_relin_moddown_ntt<CE, true> : k_relin_moddown_ntt<CE, false>),
+                     dim3((unsigned)cnt, 2, rescale ? l : l + 1),
                      CE::STAGE_EPI ? CE::M * 8 : 0, a, b, l, (const uint64_t*)acc, (const uint64_t*)r, (const uint64_t*)s,
                      d.L, rs, out, add_w, add_k, *d.mt, d.cc);
 }
@@ -772,10 +779,10 @@ void launch_relin_finish_n(const Dev& d, const uint64_t* a, int64_t cnt, int l, 
     using C = CfgFused<LOGN>;
     const uint64_t* b = nullptr;
     launch_relin_mac(d, a, b, cnt, l, xh, rlk, rlk_c, acc);
-    launch_cfg<C>(d, "k_relin_moddown_intt", k_relin_moddown_intt<C>, dim3((unsigned)cnt, 2), a, b, l, (const uint64_t*)acc,
-                  d.L, 0, r, s, *d.mt, d.cc);
+    launch_cfg<C>(d, "k_relin_moddown_intt", k_relin_moddown_intt<C, false>, dim3((unsigned)cnt, 2), a, b, l,
+                  (const uint64_t*)acc, d.L, 0, r, s, *d.mt, d.cc);
     using CE = CfgEpi<LOGN>;
-    launch_cfg_x<CE>(d, "k_relin_moddown_ntt", k_relin_moddown_ntt<CE>, dim3((unsigned)cnt, 2, l + 1),
+    launch_cfg_x<CE>(d, "k_relin_moddown_ntt", k_relin_moddown_ntt<CE, false>, dim3((unsigned)cnt, 2, l + 1),
                      CE::STAGE_EPI ? CE::M * 8 : 0, a, b, l, (const uint64_t*)acc, (const uint64_t*)r, (const uint64_t*)s,
                      d.L, 0, out, b, b, *d.mt, d.cc);
 }

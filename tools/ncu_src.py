@@ -49,6 +49,20 @@ def main():
     for op, n in by_op.most_common(15):
         rs = by_op_reason[op].most_common(3)
         print(f"  {op:10s} {n / total:6.1%}   " + ", ".join(f"{k[6:]} {v / total:.1%}" for k, v in rs))
+    ex = collections.Counter()
+    for r in body:
+        src = r[H["Source"]].strip()
+        op = src.split()[0] if src else "?"
+        if op.startswith("@"):
+            op = src.split()[1]
+        try:
+            ex[op] += int(r[H["Instructions Executed"]] or 0)
+        except (KeyError, ValueError):
+            pass
+    te = sum(ex.values())
+    if te:
+        print("executed warp-instructions %d; by opcode:" % te)
+        print("  " + ", ".join("%s %.1f%%" % (k, 100.0 * v / te) for k, v in ex.most_common(22)))
     print("hottest instructions:")
     for n, a, src, st in sorted(insts, key=lambda x: -x[0])[:top]:
         rs = sorted(st.items(), key=lambda kv: -kv[1])[:2]
