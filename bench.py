@@ -588,7 +588,7 @@ def run_ours(a):
         launches_k = e["launches_per_step"]
         traffic = None
         if k in traffic_tab:   # DRAM bytes of the kernel's launches in one step (ncu --set full) / launches
-            traffic = traffic_tab[k]["dram_bytes_per_step"] / traffic_tab[k]["launches_per_step"]
+            traffic = traffic_tab[k]["dram_bytes_per_step"] / launches_k   # same divisor as the algorithmic bytes
         roof = {"kernel": k, "bound": "alu", "unit": "Gbutterfly/s", "achieved": e["achieved_Gbfly_s"],
                 "peak": e["peak_Gbfly_s"], "frac": e["bfly_frac"], "traffic": traffic,
                 "traffic_unit": "DRAM bytes per launch (profiles/round2/ncu_traffic.json: ncu --set full of "

@@ -230,10 +230,17 @@ k_cc_mac2(const uint64_t* __restrict__ x, int l, int W, int kw, int stride, int 
     const int win = blockIdx.z;
     const int wr = win / Wo, wc = win % Wo;
     const bool f64 = mods[i].fp == 2;   // uniform per CTA (limb i)
+#ifdef EDL_CC2_SPLIT
+    // split products (see k_cc_mac3): 4 DFMA per MAC, three exact sums per output
+    const bool split = f64 && taps <= 16;
+#else
+    const bool split = false;
+#endif
     for (int t = threadIdx.x; t < FC * taps; t += blockDim.x) {
         const int f = t / taps, tt = t % taps;
         ulonglong2 w = (f0 + f < F) ? wk[((size_t)(f0 + f) * taps + tt) * nl + i] : make_ulonglong2(0, 0);
-        if (f64) w.x = f64_from_u(w.x);   // {binary64 w, RD(w/q)} for the FP64-pipe products
+        if (split) w = make_ulonglong2(f64_from_u(w.x & 0x3FFFFFull), f64_from_u(w.x >> 22));
+        else if (f64) w.x = f64_from_u(w.x);   // {binary64 w, RD(w/q)} for the FP64-pipe products
         wsm[t] = w;
     }
     for (int t = threadIdx.x; t < taps; t += blockDim.x)
@@ -250,6 +257,11 @@ k_cc_mac2(const uint64_t* __restrict__ x, int l, int W, int kw, int stride, int 
     U128 acc[FC][2];
 #pragma unroll
     for (int f = 0; f < FC; f++) acc[f][0].lo = acc[f][0].hi = acc[f][1].lo = acc[f][1].hi = 0;
+#ifdef EDL_CC2_SPLIT
+    double s2[FC][2];
+#pragma unroll
+    for (int f = 0; f < FC; f++) s2[f][0] = s2[f][1] = 0.0;
+#endif
     ulonglong2 cur[CC2_TB], nxt[CC2_TB];
 #pragma unroll
     for (int u = 0; u < CC2_TB; u++)
@@ -261,6 +273,27 @@ k_cc_mac2(const uint64_t* __restrict__ x, int l, int W, int kw, int stride, int 
             nxt[u] = (tt < taps) ? __ldg(reinterpret_cast<const ulonglong2*>(xb + tpix[tt] * ct_words))
                                  : make_ulonglong2(0, 0);
         }
+#ifdef EDL_CC2_SPLIT
+        if (split) {   // acc[f][h].lo / .hi / s2[f][h]: the three split sums of coefficient h
+#pragma unroll
+            for (int u = 0; u < CC2_TB; u++) {
+                const int tt = t0 + u < taps ? t0 + u : 0;   // out-of-range taps carry x = 0
+                const double xl0 = u52_to_double(cur[u].x & 0x3FFFFFull), xh0 = u52_to_double(cur[u].x >> 22);
+                const double xl1 = u52_to_double(cur[u].y & 0x3FFFFFull), xh1 = u52_to_double(cur[u].y >> 22);
+#pragma unroll
+                for (int f = 0; f < FC; f++) {
+                    const ulonglong2 w = wsm[f * taps + tt];
+                    const double wl = f64_of(w.x), wh = f64_of(w.y);
+                    acc[f][0].lo = bits_of(__fma_rn(xl0, wl, f64_of(acc[f][0].lo)));
+                    acc[f][0].hi = bits_of(__fma_rn(xl0, wh, __fma_rn(xh0, wl, f64_of(acc[f][0].hi))));
+                    s2[f][0] = __fma_rn(xh0, wh, s2[f][0]);
+                    acc[f][1].lo = bits_of(__fma_rn(xl1, wl, f64_of(acc[f][1].lo)));
+                    acc[f][1].hi = bits_of(__fma_rn(xl1, wh, __fma_rn(xh1, wl, f64_of(acc[f][1].hi))));
+                    s2[f][1] = __fma_rn(xh1, wh, s2[f][1]);
+                }
+            }
+        } else
+#endif
         if (f64) {
             // exact binary64 products t = x w mod q in [-0.625q, 0.625q] summed exactly
             // (taps * 0.625 q < 2^51), reduced once at the end; accumulators hold doubles
@@ -309,6 +342,22 @@ k_cc_mac2(const uint64_t* __restrict__ x, int l, int W, int kw, int stride, int 
             const int64_t o = (int64_t)(f0 + f) * n_out_per_f + win;
             uint64_t* dst = out + limb_off(o, p, i, nl, logn) + 2 * (size_t)n2;
             ulonglong2 v;
+#ifdef EDL_CC2_SPLIT
+            if (split) {   // v = s2 (2^44 mod q) + s1 2^22 + s0 mod q
+                const double qd = u52_to_double(m.q);
+                const double c44d = u52_to_double((1ull << 44) % m.q), c44q = __ddiv_rd(c44d, qd);
+                const double c22q = __ddiv_rd(4194304.0, qd);
+                uint64_t o[2];
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    const double t = __dadd_rn(f64_reduce(f64_of(acc[f][h].lo), qd, m.qinv_d),
+                                               __dadd_rn(f64_mulc(f64_of(acc[f][h].hi), 4194304.0, c22q, qd),
+                                                         f64_mulc(s2[f][h], c44d, c44q, qd)));
+                    o[h] = f64_to_canon(f64_reduce(t, qd, m.qinv_d), qd);
+                }
+                v = make_ulonglong2(o[0], o[1]);
+            } else
+#endif
             if (f64) {
                 const double qd = u52_to_double(m.q);
                 v = make_ulonglong2(f64_to_canon(f64_reduce(f64_of(acc[f][0].lo), qd, m.qinv_d), qd),
@@ -345,10 +394,16 @@ k_cc_mac3(const uint64_t* __restrict__ x, int l, int W, int kw, int stride, int 
     const int wr = win / Wo, wc = win % Wo;
     const ModInfo& m = mods[i];
     const bool f64 = m.fp == 2, fp = m.fp != 0;   // uniform per CTA
+    // F64 limbs with <= 16 taps: split products (x = xh 2^22 + xl, w = wh 2^22 + wl, every
+    // piece < 2^22): x w = xh wh 2^44 + (xh wl + xl wh) 2^22 + xl wl with three exact binary64
+    // sums (S1 < 2 taps 2^44 <= 2^49), 4 DFMA per MAC instead of f64_mulc's 6 + 1; reduced
+    // once per output.  wsm then holds {wl, wh} as binary64.
+    const bool split = f64 && taps <= 16;
     for (int t = threadIdx.x; t < FC * taps; t += CC3_T) {
         const int f = t / taps, tt = t % taps;
         ulonglong2 w = (f0 + f < F) ? wk[((size_t)(f0 + f) * taps + tt) * nl + i] : make_ulonglong2(0, 0);
-        if (f64) w.x = f64_from_u(w.x);
+        if (split) w = make_ulonglong2(f64_from_u(w.x & 0x3FFFFFull), f64_from_u(w.x >> 22));
+        else if (f64) w.x = f64_from_u(w.x);
         wsm[t] = w;
     }
     for (int t = threadIdx.x; t < taps; t += CC3_T) tpix[t] = (wr * stride + t / kw) * W + (wc * stride + t % kw);
@@ -358,7 +413,42 @@ k_cc_mac3(const uint64_t* __restrict__ x, int l, int W, int kw, int stride, int 
     const size_t ct_words = (size_t)2 * nl << logn;
     const uint64_t* xb = x + limb_off(0, p, i, nl, logn) + n;
     const double qd = u52_to_double(m.q);
-    if (f64) {
+    if (split) {
+        double s0[FC], s1[FC], s2[FC];
+#pragma unroll
+        for (int f = 0; f < FC; f++) s0[f] = s1[f] = s2[f] = 0.0;
+        for (int t0 = 0; t0 < taps; t0 += CC3_TB) {
+            uint64_t xv[CC3_TB];
+#pragma unroll
+            for (int u = 0; u < CC3_TB; u++) xv[u] = (t0 + u < taps) ? __ldg(xb + tpix[t0 + u] * ct_words) : 0;
+#pragma unroll
+            for (int u = 0; u < CC3_TB; u++) {
+                if (t0 + u >= taps) break;
+                const double xl = u52_to_double(xv[u] & 0x3FFFFFull), xh = u52_to_double(xv[u] >> 22);
+#pragma unroll
+                for (int f = 0; f < FC; f++) {
+                    const ulonglong2 w = wsm[f * taps + t0 + u];
+                    const double wl = f64_of(w.x), wh = f64_of(w.y);
+                    s0[f] = __fma_rn(xl, wl, s0[f]);
+                    s1[f] = __fma_rn(xh, wl, s1[f]);
+                    s1[f] = __fma_rn(xl, wh, s1[f]);
+                    s2[f] = __fma_rn(xh, wh, s2[f]);
+                }
+            }
+        }
+        // v = s2 (2^44 mod q) + s1 2^22 + s0 mod q (2^22 < q: c22 = 2^22)
+        const uint64_t c44 = (1ull << 44) % m.q;
+        const double c44d = u52_to_double(c44), c44q = __ddiv_rd(c44d, qd);
+        const double c22d = 4194304.0, c22q = __ddiv_rd(c22d, qd);
+#pragma unroll
+        for (int f = 0; f < FC; f++)
+            if (f0 + f < F) {
+                double v = __dadd_rn(f64_reduce(s0[f], qd, m.qinv_d),
+                                     __dadd_rn(f64_mulc(s1[f], c22d, c22q, qd), f64_mulc(s2[f], c44d, c44q, qd)));
+                out[limb_off((int64_t)(f0 + f) * n_out_per_f + win, p, i, nl, logn) + n] =
+                    f64_to_canon(f64_reduce(v, qd, m.qinv_d), qd);
+            }
+    } else if (f64) {
         double acc[FC];
 #pragma unroll
         for (int f = 0; f < FC; f++) acc[f] = 0.0;
@@ -1005,9 +1095,26 @@ __device__ __forceinline__ void mac3_body(const uint64_t* __restrict__ a, const 
                 mac128(s0, x, kv[j][0]);
                 mac128(s1, x, kv[j][1]);
             }
-            v0 = barrett128(s0, m);
-            v1 = barrett128(s1, m);
-            if (data) {
+            if (data && pfold) {
+                // keys carry P^-1: the tensor's d0 = a0 b0 and d1 = a0 b1 + a1 b0 join the same
+                // lazy 128-bit sums (<= l + 3 terms below 2^120), one Barrett per output
+                if (single) {
+                    U128 t;
+                    t.lo = cur.a0;
+                    t.hi = 0;
+                    add128(s0, t);
+                } else {
+                    mac128(s0, cur.a0, cur.b0);
+                    mac128(s1, cur.a0, cur.b1);
+                    mac128(s1, cur.a1, cur.b0);
+                }
+                v0 = barrett128(s0, m);
+                v1 = barrett128(s1, m);
+            } else {
+                v0 = barrett128(s0, m);
+                v1 = barrett128(s1, m);
+            }
+            if (data && !pfold) {
                 uint64_t d0 = cur.a0, d1 = 0;
                 if (!single) {
                     d0 = mulmod_barrett(cur.a0, cur.b0, m);
