@@ -33,9 +33,10 @@
 
 namespace edl {
 
-template <int LOGN_, int LOGK_, int LOGE_, int MINB_, bool STAGE_ = false>
+template <int LOGN_, int LOGK_, int LOGE_, int MINB_, bool STAGE_ = false, bool TWPF_ = false>
 struct NttCfg {
     static constexpr bool STAGE_EPI = STAGE_;   // epilogue operand staged in smem by cp.async (epi_pre)
+    static constexpr bool TW_PF_FWD = TWPF_;    // F64 forward: next-pass twiddles prefetched across barriers
     static constexpr int LOGN = LOGN_;
     static constexpr int LOGK = LOGK_;
     static constexpr int LOGM = LOGN_ - LOGK_;
@@ -408,6 +409,115 @@ __device__ __forceinline__ void pass_smem(uint64_t* sm, const ModInfo& m, uint64
     __syncthreads();
 }
 
+// ---- F64 path: twiddles of the next pass prefetched across the barrier ------------------
+// ncu (round 2, plain 2^14 NTT on 40-bit primes): the DMUL of a butterfly waiting on its
+// twiddle's global load (L2: the twiddle tables do not stay in L1) was the largest single
+// stall (11-14 % of samples).  A pass with one group per thread (G == 1) uses 2^NS - 1
+// distinct twiddles per thread -- stage k, group position r -> entry (2^k - 1) + (r >> (NS-k))
+// -- and they do not depend on the data, so they are loaded right after the previous pass's
+// shared-memory stores (its residues are dead then: the registers are free) and arrive
+// while the CTA waits at the barrier.
+// Measured (B200, round 2): inverse 40-bit transforms +9 %; forward: plain transforms and the
+// modulus raise -1..4 %, the kernels with an epilogue operand (rescale, mod-down: CfgEpi) gain
+// (mod-down NTT 0.565 -> 0.538 ms per C1 step; ptxas: its spills 224 -> 28 bytes), so the
+// forward prefetch is a per-configuration choice (NttCfg::TW_PF_FWD).
+#ifndef EDL_NO_TW_PREFETCH
+#define EDL_TW_PREFETCH_INV 1
+#endif
+#ifndef EDL_TW_PREFETCH_FWD
+#define EDL_TW_PREFETCH_FWD 0   // 1: every forward transform; else per configuration (NttCfg::TW_PF_FWD)
+#endif
+template <class C, int P>
+struct TwPre {
+    static constexpr bool OK = (P >= 1 && P < C::NPASS && PassInfo<C, P>::G == 1);
+    static constexpr int NW = (1 << C::LOGE) - 1;   // any pass's count (one buffer serves every pass)
+};
+template <class C, int P, bool INV>
+__device__ __forceinline__ void tw_prefetch(double* w, const ModInfo& m) {
+    using PI = PassInfo<C, P>;
+    const int high = (C::crank() << PI::SL) | ((int)threadIdx.x >> PI::BLOW);
+    const uint64_t* __restrict__ t = reinterpret_cast<const uint64_t*>(INV ? m.tw_inv : m.tw_fwd);
+#pragma unroll
+    for (int k = 0; k < PI::NS; k++)
+#pragma unroll
+        for (int j = 0; j < (1 << k); j++) w[(1 << k) - 1 + j] = f64_of(__ldg(t + (1 << (PI::SA + k)) + (high << k) + j));
+}
+// One G == 1 pass on the F64 path with its twiddles in w; on return w holds pass PN's
+// twiddles when TwPre<C, PN>::OK (prefetched between the stores and the closing barrier).
+template <class C, int P, bool INV, int PN>
+__device__ __forceinline__ void pass_smem_pre(uint64_t* sm, const ModInfo& m, double* w) {
+    using PI = PassInfo<C, P>;
+    static_assert(PI::G == 1, "one group per thread");
+    constexpr int NS = PI::NS;
+    const double qd = u52_to_double(m.q), qinv = m.qinv_d;
+    uint64_t x[1 << NS];
+    const int base = ((threadIdx.x >> PI::BLOW) << (PI::BTOP + 1)) | (threadIdx.x & ((1 << PI::BLOW) - 1));
+#pragma unroll
+    for (int r = 0; r < (1 << NS); r++) x[r] = sm[spad(base) + spad(r << PI::BLOW)];
+    __syncthreads();
+    if constexpr (!INV) {
+#pragma unroll
+        for (int k = 0; k < NS; k++) {
+            const int half = 1 << (NS - 1 - k);
+#pragma unroll
+            for (int r = 0; r < (1 << NS); r++) {
+                if (r & half) continue;
+                const double wv = w[(1 << k) - 1 + (r >> (NS - k))];
+                const double a = f64_of(x[r]);
+                const double t = f64_mult(f64_of(x[r + half]), wv, qd, qinv);
+                x[r] = bits_of(__dadd_rn(a, t));
+                x[r + half] = bits_of(__dsub_rn(a, t));
+            }
+        }
+    } else {
+#pragma unroll
+        for (int k = NS - 1; k >= 0; k--) {
+            const int half = 1 << (NS - 1 - k);
+#pragma unroll
+            for (int r = 0; r < (1 << NS); r++) {
+                if (r & half) continue;
+                const double wv = w[(1 << k) - 1 + (r >> (NS - k))];
+                const double a = f64_of(x[r]), b = f64_of(x[r + half]);
+                double sum = __dadd_rn(a, b);
+                if (k == 0) sum = f64_reduce(sum, qd, qinv);
+                x[r] = bits_of(sum);
+                x[r + half] = bits_of(f64_mult(__dsub_rn(a, b), wv, qd, qinv));
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < (1 << NS); r++) sm[spad(base) + spad(r << PI::BLOW)] = x[r];
+    if constexpr (TwPre<C, PN>::OK) tw_prefetch<C, PN, INV>(w, m);
+    __syncthreads();
+}
+// F64 forward passes P.. with prefetched twiddles (w holds pass P's when HAVE).
+template <class C, int P, bool HAVE>
+__device__ __forceinline__ void fwd_middle_pre(uint64_t* sm, const ModInfo& m, double* w) {
+    if constexpr (P < C::NPASS) {
+        if constexpr (TwPre<C, P>::OK) {
+            if constexpr (!HAVE) tw_prefetch<C, P, false>(w, m);
+            pass_smem_pre<C, P, false, P + 1>(sm, m, w);
+            fwd_middle_pre<C, P + 1, TwPre<C, P + 1>::OK>(sm, m, w);
+        } else {
+            pass_smem<C, P, false, true>(sm, m, 2 * m.q);
+            fwd_middle_pre<C, P + 1, false>(sm, m, w);
+        }
+    }
+}
+template <class C, int P, bool HAVE>
+__device__ __forceinline__ void inv_middle_pre(uint64_t* sm, const ModInfo& m, double* w) {
+    if constexpr (P > 0) {
+        if constexpr (TwPre<C, P>::OK) {
+            if constexpr (!HAVE) tw_prefetch<C, P, true>(w, m);
+            pass_smem_pre<C, P, true, P - 1>(sm, m, w);
+            inv_middle_pre<C, P - 1, TwPre<C, P - 1>::OK>(sm, m, w);
+        } else {
+            pass_smem<C, P, true, true>(sm, m, 2 * m.q);
+            inv_middle_pre<C, P - 1, false>(sm, m, w);
+        }
+    }
+}
+
 template <class C, int P, bool FP>
 __device__ __forceinline__ void fwd_middle(uint64_t* sm, const ModInfo& m, uint64_t two_q) {
     if constexpr (P < C::NPASS) {
@@ -525,8 +635,18 @@ __device__ __forceinline__ void ntt_fwd_impl(uint64_t* sm, const ModInfo& m, Loa
     fwd_pass_regs<C::LOGK, C::LOGE, FP>(x, C::crank(), m.tw_fwd, q, two_q, qd, m.qinv_d);
 #pragma unroll
     for (int r = 0; r < C::E; r++) sm[spad(tid) + spad(r * C::T)] = x[r];
-    __syncthreads();
-    fwd_middle<C, 1, FP>(sm, m, two_q);
+#ifdef EDL_TW_PREFETCH_INV
+    if constexpr (FP && (C::TW_PF_FWD || EDL_TW_PREFETCH_FWD)) {
+        double w[TwPre<C, 1>::NW];
+        if constexpr (TwPre<C, 1>::OK) tw_prefetch<C, 1, false>(w, m);
+        __syncthreads();
+        fwd_middle_pre<C, 1, TwPre<C, 1>::OK>(sm, m, w);
+    } else
+#endif
+    {
+        __syncthreads();
+        fwd_middle<C, 1, FP>(sm, m, two_q);
+    }
     // epilogue operands first (all E loads in flight, or the staged copies), then the outputs
     using PT = decltype(pre(0));
     PT pv[C::E];
@@ -590,8 +710,19 @@ __device__ __forceinline__ void ntt_inv_impl(uint64_t* sm, const ModInfo& m, Loa
             else sm[spad(tid) + spad(r * C::T)] = t[r];
         }
     }
-    __syncthreads();
-    inv_middle<C, C::NPASS - 1, FP>(sm, m, two_q);
+#ifdef EDL_TW_PREFETCH_INV
+    if constexpr (FP) {
+        constexpr int P1 = C::NPASS - 1;
+        double w[TwPre<C, P1>::NW];
+        if constexpr (TwPre<C, P1>::OK) tw_prefetch<C, P1, true>(w, m);
+        __syncthreads();
+        inv_middle_pre<C, P1, TwPre<C, P1>::OK>(sm, m, w);
+    } else
+#endif
+    {
+        __syncthreads();
+        inv_middle<C, C::NPASS - 1, FP>(sm, m, two_q);
+    }
     uint64_t x[C::E];
 #pragma unroll
     for (int r = 0; r < C::E; r++) x[r] = sm[spad(tid) + spad(r * C::T)];
@@ -765,13 +896,18 @@ template <int LOGN>   // key-switch MAC kernel (largest epilogue)
 using CfgKs = CfgFusedE<LOGN, cfg_logm(LOGN, false) == 14 ? EDL_LOGE_KS14 : cfg_loge(LOGN, false)>;
 template <int LOGN>
 using CfgPlain = CfgOf<LOGN, true>;
-// Batched plain transforms (k_ntt_limbs): at 2^14 a 2-CTA cluster of 512 threads x 16
-// residues, 2 CTAs/SM (7.6 M limb-transforms/s forward vs 7.2 with the fused kernels'
-// 4-CTA clusters, whose 12 local stages avoid the 1-stage pass that 13 local stages need
-// and win inside the fused kernels: C1 4.77 vs 4.85 ms); below 2^14 the fused config.
+// Batched plain transforms (k_ntt_limbs): at 2^14 the fused kernels' 4-CTA clusters of
+// 256 threads x 16 residues, 4 CTAs/SM (round 2, after the st.async exchange and the inverse
+// twiddle prefetch: 8.65 / 8.18 M limb-transforms/s forward / inverse on the C1 chain against
+// 8.50 / 7.50 for round 1's 2-CTA clusters of 512 x 16; 48 registers and 5 CTAs/SM: equal
+// forward, slower integer inverse); below 2^14 the fused config.
+#ifndef EDL_PLAIN14_MINB
+#define EDL_PLAIN14_MINB 4
+#endif
 template <int LOGN>
 using CfgNttLimbs = typename std::conditional<
-    (LOGN == 14), NttCfg<14, 1, 4, 2>, typename std::conditional<(LOGN < 14), CfgOf<LOGN, false>, CfgOf<LOGN, true>>::type>::type;
+    (LOGN == 14), NttCfg<14, 2, 4, EDL_PLAIN14_MINB>,
+    typename std::conditional<(LOGN < 14), CfgOf<LOGN, false>, CfgOf<LOGN, true>>::type>::type;
 template <int LOGN>
 using CfgFused = CfgOf<LOGN, false>;
 // Forward transforms with an epilogue operand: optionally (EDL_STAGE_EPI) at 2^14 the fused
@@ -783,8 +919,10 @@ template <int LOGN>
 using CfgEpi = typename std::conditional<(LOGN == 14 && cfg_logk(14, false) == 2), NttCfg<14, 2, 4, 3, true>,
                                          CfgFused<LOGN>>::type;
 #else
+template <class C>
+using WithTwPf = NttCfg<C::LOGN, C::LOGK, C::LOGE, C::MINB, C::STAGE_EPI, true>;
 template <int LOGN>
-using CfgEpi = CfgFused<LOGN>;
+using CfgEpi = WithTwPf<CfgFused<LOGN>>;
 #endif
 
 }  // namespace edl
