@@ -854,7 +854,8 @@ edl_status edl_cross_correlate(edl_ctx* c, const edl_cts* x, int32_t H, int32_t 
     uint64_t* acc = scratch(c, ct_words(c, cnt, l) + (size_t)cnt * 2 * c->N);
     if (!acc) return fail(c, EDL_ERR_CUDA, "cross_correlate: scratch");
     uint64_t* r = acc + ct_words(c, cnt, l);
-    const ulonglong2* dw = upload(c, residue_pairs(c, wi, l + 1));
+    const std::vector<ulonglong2> hw = residue_pairs(c, wi, l + 1);
+    const ulonglong2* dw = upload(c, hw);
     if (!dw) return fail(c, EDL_ERR_CAPACITY, "CapacityError: constant table exceeds the staging ring");
     const uint64_t* db = nullptr;
     if (bias) {
@@ -864,7 +865,7 @@ edl_status edl_cross_correlate(edl_ctx* c, const edl_cts* x, int32_t H, int32_t 
         if (!db) return fail(c, EDL_ERR_CAPACITY, "CapacityError: constant table exceeds the staging ring");
     }
     Dev d = c->dev();
-    launch_cc_mac(d, x->data, l, H, W, F, kh, kw, stride, dw, acc);
+    launch_cc_mac(d, x->data, l, H, W, F, kh, kw, stride, dw, acc, hw.data());
     launch_rescale_intt(d, acc, cnt, l, nullptr, r);
     launch_rescale_ntt(d, acc, cnt, l, nullptr, r, db, out->data);
     set_meta(out, cnt, l - 1, s_after, x->key_id);

@@ -246,7 +246,8 @@ void launch_add_add_const(const Dev& d, const uint64_t* v, const uint64_t* w, in
                           const uint64_t* k, uint64_t* out);
 // cross-correlation MAC: out[f*Ho*Wo + r*Wo + c] = sum_{u,v} x[(r*st+u)*W + c*st+v] * wk[f][u*kw+v][i]
 void launch_cc_mac(const Dev& d, const uint64_t* x, int l, int H, int W, int F, int kh, int kw, int stride,
-                   const ulonglong2* wk /*[F][kh*kw][l+1] {residue, companion}*/, uint64_t* out);
+                   const ulonglong2* wk /*[F][kh*kw][l+1] {residue, companion}*/, uint64_t* out,
+                   const ulonglong2* hw = nullptr /*host copy of wk: 4x4 taps go to k_cc_mac4*/);
 // dense MAC: out[o] = sum_k x[k] * wd[o][k][i]  (x: K cts, out: O cts, level l)
 // part: scratch for split-K partial sums (dense_split(...) * O * 2 * (l+1) * N words) or null
 void launch_dense_mac(const Dev& d, const uint64_t* x, int64_t K, int64_t O, int l, const ulonglong2* wd, uint64_t* out,

@@ -9,6 +9,7 @@
 #include <algorithm>
 
 #include "kernels.cuh"
+#include "host_math.h"
 
 namespace edl {
 
@@ -368,6 +369,115 @@ k_cc_mac2(const uint64_t* __restrict__ x, int l, int W, int kw, int stride, int 
             }
             *reinterpret_cast<ulonglong2*>(dst) = v;
         }
+    }
+}
+
+// ---------------------------------------------------------------- cross-correlation MAC, round 2b
+// k_cc_mac4: the C1 geometry (KH x KW = 4 x 4 taps, <= 8 filters, <= 6 limbs) with the
+// filter weights in the kernel's parameter space (constant bank: uniform loads, no shared-
+// memory staging or barrier per CTA) and F64 limbs as split products: x = xh 2^22 + xl and
+// w = wh 2^22 + wl (every piece < 2^22 for q < 2^44) give x w = xh wh 2^44 +
+// (xh wl + xl wh) 2^22 + xl wl, three exact binary64 FMA sums (S0, S2 < 16 2^44 = 2^48,
+// S1 < 2^49 for 16 taps) -- 4 DFMA per MAC instead of f64_mulc's 6 plus the add -- reduced
+// once per output: S0 mod q + S1 2^22 + S2 (2^44 mod q).  60-bit limbs: full 128-bit products
+// summed lazily, one Barrett per output (O4).  One coefficient per thread, a CTA walks
+// CC4_WPB windows (tap loads of a window all issued before its MACs).
+constexpr int CC4_T = 128;
+constexpr int CC4_MAXL = 6, CC4_MAXF = 8, CC4_TAPS = 16;
+#ifndef EDL_CC4_WPB
+#define EDL_CC4_WPB 4
+#endif
+#ifndef EDL_CC4_MINB
+#define EDL_CC4_MINB 6
+#endif
+struct CCW4 {   // [limb][filter][tap] {wl, wh} as binary64 (F64 limbs), {w, companion} (others)
+    uint64_t w[CC4_MAXL][CC4_MAXF][CC4_TAPS][2];
+    double c44[CC4_MAXL][3];   // F64 limbs: 2^44 mod q, RD((2^44 mod q) / q), RD(2^22 / q) (host-made)
+};
+
+template <int FC, int KH, int KW>
+__global__ void __launch_bounds__(CC4_T, EDL_CC4_MINB)
+k_cc_mac4(const uint64_t* __restrict__ x, int l, int W, int stride, int Wo, int nwin, int f0, int F, int n_out_per_f,
+          uint64_t* __restrict__ out, const __grid_constant__ CCW4 wt, const __grid_constant__ ModTable mods, int logn) {
+    constexpr int TAPS = KH * KW;
+    static_assert(TAPS <= CC4_TAPS && FC <= CC4_MAXF, "k_cc_mac4 geometry");
+    const int nl = l + 1;
+    const int p = blockIdx.y / nl, i = blockIdx.y % nl;
+    const int n = blockIdx.x * CC4_T + threadIdx.x;
+    const ModInfo& m = mods[i];
+    const int mode = (int)m.fp;   // uniform per CTA (limb i)
+    static_assert(CC4_T >= 1, "");
+    const size_t ct_words = (size_t)2 * nl << logn;
+    const uint64_t* xb = x + limb_off(0, p, i, nl, logn) + n;
+    const double qd = u52_to_double(m.q);
+    // this limb's weights -> shared memory once per CTA (LDS.128 broadcasts in the MAC loop:
+    // constant-bank loads with the runtime limb index stalled every DFMA on LDC, ncu round 2)
+    __shared__ ulonglong2 ws[FC][TAPS];
+    for (int e = threadIdx.x; e < FC * TAPS; e += CC4_T)
+        ws[e / TAPS][e % TAPS] = make_ulonglong2(wt.w[i][e / TAPS][e % TAPS][0], wt.w[i][e / TAPS][e % TAPS][1]);
+    __syncthreads();
+    const double c44d = wt.c44[i][0], c44q = wt.c44[i][1], c22q = wt.c44[i][2];
+    const int w_end = min(nwin, (int)(blockIdx.z + 1) * EDL_CC4_WPB);
+    auto fetch = [&](int win, uint64_t* xv) {
+        const int wr = win / Wo, wc = win - (win / Wo) * Wo;
+        const uint64_t* xw = xb + (size_t)((wr * stride) * W + wc * stride) * ct_words;
+#pragma unroll
+        for (int t = 0; t < TAPS; t++) xv[t] = __ldg(xw + (size_t)((t / KW) * W + (t % KW)) * ct_words);
+    };
+    // (measured: prefetching the next window's taps during this window's MACs, 128 registers,
+    //  4 CTAs/SM: 0.46 ms vs 0.44 without)
+    for (int win = blockIdx.z * EDL_CC4_WPB; win < w_end; win++) {
+        uint64_t xv[TAPS];
+        fetch(win, xv);
+        uint64_t res[FC];
+        if (mode == 2) {
+            double s0[FC], s1[FC], s2[FC];
+#pragma unroll
+            for (int f = 0; f < FC; f++) s0[f] = s1[f] = s2[f] = 0.0;
+#pragma unroll
+            for (int t = 0; t < TAPS; t++) {
+                const double xl = __hiloint2double(0x43300000, (int)((uint32_t)xv[t] & 0x3FFFFFu)) - F64_TWO52;
+                const double xh = __hiloint2double(0x43300000, (int)(uint32_t)(xv[t] >> 22)) - F64_TWO52;
+#pragma unroll
+                for (int f = 0; f < FC; f++) {
+                    const ulonglong2 wv = ws[f][t];
+                    const double wl = f64_of(wv.x), wh = f64_of(wv.y);
+                    s0[f] = __fma_rn(xl, wl, s0[f]);
+                    s1[f] = __fma_rn(xh, wl, s1[f]);
+                    s1[f] = __fma_rn(xl, wh, s1[f]);
+                    s2[f] = __fma_rn(xh, wh, s2[f]);
+                }
+            }
+#pragma unroll
+            for (int f = 0; f < FC; f++) {
+                const double tt = __dadd_rn(f64_reduce(s0[f], qd, m.qinv_d),
+                                            __dadd_rn(f64_mulc(s1[f], 4194304.0, c22q, qd), f64_mulc(s2[f], c44d, c44q, qd)));
+                res[f] = f64_to_canon(f64_reduce(tt, qd, m.qinv_d), qd);
+            }
+        } else if (mode == 1) {   // lazy [0, 2q) products summed in 64 bits (16 x 2q < 2^51)
+            uint64_t acc[FC];
+#pragma unroll
+            for (int f = 0; f < FC; f++) acc[f] = 0;
+#pragma unroll
+            for (int t = 0; t < TAPS; t++)
+#pragma unroll
+                for (int f = 0; f < FC; f++) acc[f] += tw_mul_fp(xv[t], ws[f][t].x, ws[f][t].y, m.q);
+#pragma unroll
+            for (int f = 0; f < FC; f++) res[f] = reduce64(acc[f], m);
+        } else {
+            U128 acc[FC];
+#pragma unroll
+            for (int f = 0; f < FC; f++) acc[f].lo = acc[f].hi = 0;
+#pragma unroll
+            for (int t = 0; t < TAPS; t++)
+#pragma unroll
+                for (int f = 0; f < FC; f++) mac128(acc[f], xv[t], ws[f][t].x);
+#pragma unroll
+            for (int f = 0; f < FC; f++) res[f] = barrett128(acc[f], m);
+        }
+#pragma unroll
+        for (int f = 0; f < FC; f++)
+            if (f0 + f < F) out[limb_off((int64_t)(f0 + f) * n_out_per_f + win, p, i, nl, logn) + n] = res[f];
     }
 }
 
@@ -1508,9 +1618,54 @@ void launch_add_add_const(const Dev& d, const uint64_t* v, const uint64_t* w, in
 }
 
 void launch_cc_mac(const Dev& d, const uint64_t* x, int l, int H, int W, int F, int kh, int kw, int stride,
-                   const ulonglong2* wk, uint64_t* out) {
+                   const ulonglong2* wk, uint64_t* out, const ulonglong2* hw) {
     const int Ho = (H - kh) / stride + 1, Wo = (W - kw) / stride + 1;
     const int taps = kh * kw;
+#ifndef EDL_NO_CC4
+    if (hw && kh == 4 && kw == 4 && l + 1 <= CC4_MAXL && d.logn >= 7) {
+        const int nl = l + 1, nwin = Ho * Wo;
+        const dim3 grid((unsigned)((1 << d.logn) / CC4_T), (unsigned)(2 * nl), (unsigned)((nwin + EDL_CC4_WPB - 1) / EDL_CC4_WPB));
+        for (int f0 = 0; f0 < F; f0 += CC4_MAXF) {
+            const int fc = (F - f0) < CC4_MAXF ? (F - f0) : CC4_MAXF;
+            CCW4 wt;
+            memset(&wt, 0, sizeof(wt));
+            for (int i = 0; i < nl; i++)
+                for (int f = 0; f < fc; f++)
+                    for (int t = 0; t < taps; t++) {
+                        const ulonglong2 v = hw[((size_t)(f0 + f) * taps + t) * nl + i];
+                        if (d.hmods[i].fp == 2) {   // split residue pieces as binary64
+                            const double lo = (double)(v.x & 0x3FFFFFull), hi = (double)(v.x >> 22);
+                            memcpy(&wt.w[i][f][t][0], &lo, 8);
+                            memcpy(&wt.w[i][f][t][1], &hi, 8);
+                        } else {
+                            wt.w[i][f][t][0] = v.x;
+                            wt.w[i][f][t][1] = v.y;
+                        }
+                    }
+            for (int i = 0; i < nl; i++)
+                if (d.hmods[i].fp == 2) {
+                    const uint64_t q = d.hmods[i].q, c44 = (1ull << 44) % q;
+                    const uint64_t b44 = host::mul_companion(c44, q), b22 = host::mul_companion(1ull << 22, q);
+                    wt.c44[i][0] = (double)c44;   // exact: < 2^44
+                    memcpy(&wt.c44[i][1], &b44, 8);
+                    memcpy(&wt.c44[i][2], &b22, 8);
+                }
+#define EDL_CC4(FCV) EDL_LAUNCH(d, "k_cc_mac", (k_cc_mac4<FCV, 4, 4><<<grid, CC4_T, 0, d.st>>>(x, l, W, stride, Wo, nwin, f0, F, nwin, out, wt, *d.mt, d.logn)))
+            switch (fc) {
+                case 1: EDL_CC4(1); break;
+                case 2: EDL_CC4(2); break;
+                case 3: EDL_CC4(3); break;
+                case 4: EDL_CC4(4); break;
+                case 5: EDL_CC4(5); break;
+                case 6: EDL_CC4(6); break;
+                case 7: EDL_CC4(7); break;
+                default: EDL_CC4(8); break;
+            }
+#undef EDL_CC4
+        }
+        return;
+    }
+#endif
 #ifdef EDL_CC_MAC3   // measured slower on C1 (0.53 vs 0.47 ms): kept for reference
     if (taps <= CC2_MAXTAPS && d.logn >= 8) {
         dim3 grid((unsigned)((1 << d.logn) / CC3_T), (unsigned)(2 * (l + 1)), (unsigned)(Ho * Wo));

@@ -405,6 +405,23 @@ def test_mac_layers_extreme_residues(c1pair):
     assert np.array_equal(g.rescale(m_g).numpy(g.n), o.rescale(m_o).data)
 
 
+@pytest.mark.parametrize("H,F,kh,stride", [(10, 11, 4, 2), (12, 3, 4, 4), (9, 4, 3, 3)])
+def test_cc_geometries(c1pair, H, F, kh, stride):
+    """Cross-correlation beyond C1's geometry, GPU == oracle on every residue: more filters
+    than one launch chunk (11 = 8 + 3), overlapping windows (stride 2 < 4), and a 3x3 kernel
+    (k_cc_mac2 path; 4x4 kernels take k_cc_mac4)."""
+    g, o = c1pair
+    lvl = o.L
+    rng = np.random.default_rng(100 + H)
+    data = _rand_ct(o, H * H, lvl, 101 + H)
+    xo = ock.CtArray(data, lvl, 2.0 ** 40, o.key_id)
+    xg = _to_gpu(g, data, lvl, 2.0 ** 40, o.key_id)
+    K, kb = rng.normal(0, 0.3, (F, kh, kh)), rng.normal(0, 0.1, F)
+    cc_o = olay.cross_correlate(o, xo, H, H, K, stride, kb)
+    cc_g = g.cross_correlate(xg, H, H, K, stride, kb)
+    assert cc_g.count == cc_o.count and np.array_equal(cc_g.numpy(g.n), cc_o.data)
+
+
 def test_dense_ragged_and_deferred(c1pair):
     """Dense with K > 256 (accumulator folding), O > 16 (several output chunks), and the
     C4 deferred-rescale + uint64 combine + mod_reduce path (O15)."""
