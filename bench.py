@@ -306,6 +306,11 @@ C1_MACS = {
     "k_dense_mac": (245 * 10 * 2 * _N14, 245 * 10 * 2 * _N14),
     "k_relin_mac": (245 * _N14 * (3 * 12 + 2 * 10), 245 * _N14 * ((12 + 8) + (10 + 6))),
 }
+# k_cc_mac4 (round 2b) runs its F64-limb MACs as exact 22-bit split products: 4 DFMA per MAC,
+# + 2 DADD per tap for the split of x shared by 5 filters (0.4), + ~21 FP64 instructions per
+# output to fold the three sums (S0 mod q + S1 2^22 + S2 2^44) over 16 taps (1.3): its F64
+# ceiling is the measured DFMA rate / 5.7 instead of the f64_mulc-MAC probe.
+C1_F64_DP_PER_MAC = {"k_cc_mac": 4.0 + 2.0 / 5 + 21.0 / 16}
 
 
 def ntt_roofline(name, ms_total, steps, n, peak_int, peak_fp):
@@ -573,7 +578,8 @@ def run_ours(a):
                 e.update({"achieved_Gbfly_s": ach / 1e9, "peak_Gbfly_s": pk / 1e9, "bfly_frac": ach / pk})
             if name in C1_MACS:   # MAC layers: time at the measured MAC ceilings / measured time
                 nf, ni = C1_MACS[name]
-                t_peak = nf / fmac + ni / imac
+                fceil = dfma / C1_F64_DP_PER_MAC[name] if name in C1_F64_DP_PER_MAC else fmac
+                t_peak = nf / fceil + ni / imac
                 e.update({"macs_per_step": nf + ni, "mac_alu_frac": t_peak / (ms_k / 1e3)})
             fr = {"hbm": e.get("hbm_frac", 0.0), "alu": e.get("bfly_frac", e.get("mac_alu_frac", 0.0))}
             e["bound"] = max(fr, key=fr.get) if any(fr.values()) else None

@@ -375,9 +375,59 @@ struct PassInfo {
     static constexpr int G = C::E >> NS;              // groups per thread
 };
 
+// ---- barriers between in-CTA passes (round 2b) ------------------------------------------
+// A pass reads and writes back exactly the same shared-memory words in every thread (each
+// word belongs to one thread's group), so no barrier is needed between a pass's loads and
+// its stores; only the next pass (or the epilogue / pass 0 layout, index tid + r T) reading
+// words another thread wrote needs one -- and when every word a warp reads next was written
+// by that same warp, __syncwarp suffices.  pass_warp_local<C, P, Q>() checks this for
+// pass P followed by pass Q (Q = 0: the tid + r T layout) over all M words at compile time.
+template <class C, int P>
+__host__ __device__ constexpr int pass_word(int tid, int g, int r) {
+    using PI = PassInfo<C, P>;
+    const int v = tid + g * C::T;
+    const int low = v & ((1 << PI::BLOW) - 1);
+    const int high = v >> PI::BLOW;
+    return ((high << (PI::BTOP + 1)) | low) + (r << PI::BLOW);
+}
+template <class C, int P, int Q>
+__host__ __device__ constexpr bool pass_warp_local() {
+    using PP = PassInfo<C, P>;
+    using PQ = PassInfo<C, Q>;
+    short owner[C::M] = {};
+    for (int tid = 0; tid < C::T; tid++)
+        for (int g = 0; g < PP::G; g++)
+            for (int r = 0; r < (1 << PP::NS); r++) owner[pass_word<C, P>(tid, g, r)] = (short)(tid >> 5);
+    for (int tid = 0; tid < C::T; tid++)
+        for (int g = 0; g < PQ::G; g++)
+            for (int r = 0; r < (1 << PQ::NS); r++)
+                if (owner[pass_word<C, Q>(tid, g, r)] != (short)(tid >> 5)) return false;
+    return true;
+}
+#ifndef EDL_PASS_SYNC_FULL
+#define EDL_PASS_SYNC_LEAN 1
+#endif
+// barrier after pass P's stores, before pass Q's loads
+template <class C, int P, int Q>
+__device__ __forceinline__ void pass_barrier() {
+#ifdef EDL_PASS_SYNC_LEAN
+    if constexpr (pass_warp_local<C, P, Q>()) __syncwarp();
+    else __syncthreads();
+#else
+    __syncthreads();
+#endif
+}
+// barrier between a pass's loads and its stores (same words per thread: not needed)
+__device__ __forceinline__ void pass_inner_barrier() {
+#ifndef EDL_PASS_SYNC_LEAN
+    __syncthreads();
+#endif
+}
+
 template <class C, int P, bool INV, bool FP>
 __device__ __forceinline__ void pass_smem(uint64_t* sm, const ModInfo& m, uint64_t two_q) {
     using PI = PassInfo<C, P>;
+    constexpr int QN = INV ? (P > 1 ? P - 1 : 0) : (P + 1 < C::NPASS ? P + 1 : 0);   // next reader layout
     uint64_t x[C::E];
 #pragma unroll
     for (int g = 0; g < PI::G; g++) {
@@ -388,7 +438,7 @@ __device__ __forceinline__ void pass_smem(uint64_t* sm, const ModInfo& m, uint64
 #pragma unroll
         for (int r = 0; r < (1 << PI::NS); r++) x[g * (1 << PI::NS) + r] = sm[spad(base) + spad(r << PI::BLOW)];
     }
-    __syncthreads();
+    pass_inner_barrier();
     const int hc = C::crank() << PI::SL;
 #pragma unroll
     for (int g = 0; g < PI::G; g++) {
@@ -406,7 +456,7 @@ __device__ __forceinline__ void pass_smem(uint64_t* sm, const ModInfo& m, uint64
 #pragma unroll
         for (int r = 0; r < (1 << PI::NS); r++) sm[spad(base) + spad(r << PI::BLOW)] = x[g * (1 << PI::NS) + r];
     }
-    __syncthreads();
+    pass_barrier<C, P, QN>();
 }
 
 // ---- F64 path: twiddles of the next pass prefetched across the barrier ------------------
@@ -454,7 +504,7 @@ __device__ __forceinline__ void pass_smem_pre(uint64_t* sm, const ModInfo& m, do
     const int base = ((threadIdx.x >> PI::BLOW) << (PI::BTOP + 1)) | (threadIdx.x & ((1 << PI::BLOW) - 1));
 #pragma unroll
     for (int r = 0; r < (1 << NS); r++) x[r] = sm[spad(base) + spad(r << PI::BLOW)];
-    __syncthreads();
+    pass_inner_barrier();
     if constexpr (!INV) {
 #pragma unroll
         for (int k = 0; k < NS; k++) {
@@ -488,7 +538,8 @@ __device__ __forceinline__ void pass_smem_pre(uint64_t* sm, const ModInfo& m, do
 #pragma unroll
     for (int r = 0; r < (1 << NS); r++) sm[spad(base) + spad(r << PI::BLOW)] = x[r];
     if constexpr (TwPre<C, PN>::OK) tw_prefetch<C, PN, INV>(w, m);
-    __syncthreads();
+    constexpr int QN = (PN >= 1 && PN < C::NPASS) ? PN : 0;   // next reader layout (0: tid + r T)
+    pass_barrier<C, P, QN>();
 }
 // F64 forward passes P.. with prefetched twiddles (w holds pass P's when HAVE).
 template <class C, int P, bool HAVE>

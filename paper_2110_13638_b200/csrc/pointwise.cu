@@ -1243,7 +1243,10 @@ __device__ __forceinline__ void mac3_body(const uint64_t* __restrict__ a, const 
 // all paths in ONE launch (per-CTA branch on the target's mode), so the memory-latency-bound
 // F64 targets and the IMAD-bound 60-bit targets share the SMs instead of running back to back.
 template <int MODE, int ND>
-__global__ void __launch_bounds__(MAC3_T, 3)
+#ifndef EDL_MAC3_MINB
+#define EDL_MAC3_MINB 3
+#endif
+__global__ void __launch_bounds__(MAC3_T, EDL_MAC3_MINB)
 k_relin_mac3(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l, int L, int64_t cnt,
              const uint64_t* __restrict__ xh, const uint64_t* __restrict__ rlk, const uint64_t* __restrict__ rlk_c,
              uint64_t* __restrict__ acc, const __grid_constant__ TargetList tl, const __grid_constant__ ModTable mods,

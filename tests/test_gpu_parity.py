@@ -405,18 +405,19 @@ def test_mac_layers_extreme_residues(c1pair):
     assert np.array_equal(g.rescale(m_g).numpy(g.n), o.rescale(m_o).data)
 
 
-@pytest.mark.parametrize("H,F,kh,stride", [(10, 11, 4, 2), (12, 3, 4, 4), (9, 4, 3, 3)])
-def test_cc_geometries(c1pair, H, F, kh, stride):
+@pytest.mark.parametrize("H,F,kh,stride,ksd", [(10, 11, 4, 2, 0.3), (12, 3, 4, 4, 3.0), (9, 4, 3, 3, 0.3)])
+def test_cc_geometries(c1pair, H, F, kh, stride, ksd):
     """Cross-correlation beyond C1's geometry, GPU == oracle on every residue: more filters
-    than one launch chunk (11 = 8 + 3), overlapping windows (stride 2 < 4), and a 3x3 kernel
-    (k_cc_mac2 path; 4x4 kernels take k_cc_mac4)."""
+    than one launch chunk (11 = 8 + 3), overlapping windows (stride 2 < 4), a 3x3 kernel
+    (k_cc_mac2 path; 4x4 kernels take k_cc_mac4), and weights ~N(0, 3) (integer encodings
+    past 2^40: large 128-bit sums on q0)."""
     g, o = c1pair
     lvl = o.L
     rng = np.random.default_rng(100 + H)
     data = _rand_ct(o, H * H, lvl, 101 + H)
     xo = ock.CtArray(data, lvl, 2.0 ** 40, o.key_id)
     xg = _to_gpu(g, data, lvl, 2.0 ** 40, o.key_id)
-    K, kb = rng.normal(0, 0.3, (F, kh, kh)), rng.normal(0, 0.1, F)
+    K, kb = rng.normal(0, ksd, (F, kh, kh)), rng.normal(0, 0.1, F)
     cc_o = olay.cross_correlate(o, xo, H, H, K, stride, kb)
     cc_g = g.cross_correlate(xg, H, H, K, stride, kb)
     assert cc_g.count == cc_o.count and np.array_equal(cc_g.numpy(g.n), cc_o.data)

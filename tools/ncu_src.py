@@ -21,6 +21,14 @@ def main():
             continue
         if hdr and len(r) == len(hdr):
             body.append(r)
+    # ncu repeats the whole table for some captures (same rows twice): count each row once
+    seen, uniq = set(), []
+    for r in body:
+        k = tuple(r)
+        if k not in seen:
+            seen.add(k)
+            uniq.append(r)
+    body = uniq
     if not hdr:
         print("no source page"); return
     H = {h: i for i, h in enumerate(hdr)}

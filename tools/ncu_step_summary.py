@@ -28,6 +28,7 @@ def main(rep, out_dir):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, data = rows[0], rows[1], rows[2:]
+    os.makedirs(out_dir, exist_ok=True)
     H = {h: i for i, h in enumerate(hdr)}
 
     def val(d, k, unit_to=None):
@@ -36,6 +37,19 @@ def main(rep, out_dir):
         v = float(d[H[k]].replace(",", ""))
         return v * SCALE.get(units[H[k]], 1.0)
 
+    def first(d, keys):   # the integer-multiply pipe metric's name differs between ncu versions
+        for k in keys:
+            v = val(d, k)
+            if v is not None:
+                return v
+        return None
+
+    FMA_KEYS = [k for k in ("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active",
+                            "sm__inst_executed_pipe_fmaheavy.avg.pct_of_peak_sustained_active",
+                            "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+                            "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active") if k in H]
+    with open(os.path.join(out_dir, "ncu_pipe_metric_names.txt"), "w") as f:   # what this ncu reports
+        f.write("\n".join(h for h in hdr if "pipe" in h) + "\n")
     stall_keys = [h for h in hdr if h.startswith("smsp__average_warps_issue_stalled_") and h.endswith("_per_issue_active.ratio")]
     lines, agg = [], collections.OrderedDict()
     for d in data:
@@ -47,7 +61,7 @@ def main(rep, out_dir):
         e = {"kernel": name, "ms": ms, "dram_MB": dram / 1e6,
              "issue_active_pct": val(d, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
              "fp64_pipe_pct": val(d, "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
-             "fmaheavy_pipe_pct": val(d, "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active"),
+             "fmaheavy_pipe_pct": first(d, FMA_KEYS),
              "alu_pipe_pct": val(d, "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
              "warps_active_pct": val(d, "sm__warps_active.avg.pct_of_peak_sustained_active"),
              "registers": val(d, "launch__registers_per_thread"),
@@ -57,7 +71,6 @@ def main(rep, out_dir):
         a["launches_per_step"] += 1
         a["dram_bytes_per_step"] += dram
         a["ncu_ms_per_step"] += ms or 0.0
-    os.makedirs(out_dir, exist_ok=True)
     for a in agg.values():
         a["source"] = "ncu --set full --clock-control none, one C1 step (tools/prof_step.py --step-only), cold/serialised"
     json.dump(agg, open(os.path.join(out_dir, "ncu_traffic.json"), "w"), indent=1)

@@ -15,7 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CSRC = os.path.join(ROOT, "paper_2110_13638_b200", "csrc")
 LIB = os.path.join(ROOT, "paper_2110_13638_b200", "libedl.so")
 HOT = ["k_relin_modup", "k_rescale_ntt", "k_relin_moddown_ntt", "k_relin_moddown_intt", "k_relin_intt_d2",
-       "k_rescale_intt", "k_relin_mac3", "k_cc_mac2", "k_dense_mac3", "k_relin_ks", "k_ntt_limbs"]
+       "k_rescale_intt", "k_relin_mac3", "k_cc_mac4", "k_cc_mac2", "k_dense_mac3", "k_relin_ks", "k_ntt_limbs"]
 
 
 def demangle(sym):
@@ -58,7 +58,7 @@ def sass(out_dir):
                 hist[cur] = cnt
             name = demangle(m.group(1))
             keep = any(h in name for h in HOT) and ("NttCfg<14" in name or
-                                                     any(h in name for h in ("k_relin_mac3", "k_cc_mac2", "k_dense_mac3")))
+                                                     any(h in name for h in ("k_relin_mac3", "k_cc_mac4", "k_cc_mac2", "k_dense_mac3")))
             cur = name if keep else None
             cnt = collections.Counter() if keep else None
             continue
