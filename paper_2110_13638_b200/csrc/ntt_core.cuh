@@ -656,6 +656,18 @@ __device__ __forceinline__ void ntt_fwd_impl(uint64_t* sm, const ModInfo& m, Loa
         cluster_sync_all();
 #endif
 #ifdef EDL_XCHG_ASYNC
+#ifdef EDL_XCHG_SELF
+        // the CTA's own chunk also travels by st.async, so the mbarrier counts every word of
+        // the sub-block and no CTA barrier is needed before reading it
+        if (tid == 0) mbar_expect(mb, (uint32_t)(C::M * 8));
+#pragma unroll
+        for (int t = 0; t < C::K; t++) {
+            const uint32_t rb = mapa_u32(mb, t);
+            const uint32_t rs = mapa_u32(smem_u32(sm), t);
+#pragma unroll
+            for (int g = 0; g < C::E / C::K; g++) st_async_b64(rs + 8u * (spad(j0) + spad(g * C::T)), x[g * C::K + t], rb);
+        }
+#else
         if (tid == 0) mbar_expect(mb, (uint32_t)((C::K - 1) * (C::M / C::K) * 8));
 #pragma unroll
         for (int t = 0; t < C::K; t++) {
@@ -670,6 +682,7 @@ __device__ __forceinline__ void ntt_fwd_impl(uint64_t* sm, const ModInfo& m, Loa
             }
         }
         __syncthreads();
+#endif
         mbar_wait0(mb);
 #else
 #pragma unroll
@@ -789,7 +802,13 @@ __device__ __forceinline__ void ntt_inv_impl(uint64_t* sm, const ModInfo& m, Loa
     } else {
         constexpr int MK = C::M / C::K;
 #if defined(EDL_INV_RELAXED) || defined(EDL_XCHG_ASYNC)
+#ifndef EDL_INV_NOSYNC_ARRIVE
         __syncthreads();      // this CTA's reads of its sub-block are performed
+#endif
+        // (EDL_INV_NOSYNC_ARRIVE: every thread arrives after its own reads -- the cluster
+        //  barrier completes only when all threads of all CTAs have arrived; EDL_XCHG_SELF: the
+        //  own chunk by st.async too, no CTA barrier before reading: both measured slower on
+        //  B200, round 2b: 40-bit INTT 1085 -> 950 Gbfly/s together)
 #ifdef EDL_XCHG_ASYNC
         if (tid == 0) mbar_init_cluster(mb);
 #endif
@@ -799,17 +818,27 @@ __device__ __forceinline__ void ntt_inv_impl(uint64_t* sm, const ModInfo& m, Loa
         cluster_sync_all();   // every CTA has read its sub-block out of shared memory
 #endif
 #ifdef EDL_XCHG_ASYNC
+#ifdef EDL_XCHG_SELF
+        if (tid == 0) mbar_expect(mb, (uint32_t)(C::K * MK * 8));   // own chunk by st.async too
+#else
         if (tid == 0) mbar_expect(mb, (uint32_t)((C::K - 1) * MK * 8));
+#endif
         const uint32_t rs0 = smem_u32(sm);
 #pragma unroll
         for (int r = 0; r < C::E; r++) {
             const int j = tid + r * C::T;
             const int t = r / (C::E / C::K);   // == j / MK (T divides MK)
             const int w = spad(C::crank() * MK) + spad(tid) + spad((r * C::T) & (MK - 1));   // disjoint parts of crank MK + (j mod MK)
+#ifdef EDL_XCHG_SELF
+            st_async_b64(mapa_u32(rs0, t) + 8u * w, x[r], mapa_u32(mb, t));
+#else
             if (t == C::crank()) sm[w] = x[r];
             else st_async_b64(mapa_u32(rs0, t) + 8u * w, x[r], mapa_u32(mb, t));
+#endif
         }
+#ifndef EDL_XCHG_SELF
         __syncthreads();
+#endif
         mbar_wait0(mb);
 #else
 #pragma unroll

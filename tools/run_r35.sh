@@ -1,4 +1,4 @@
-O=gpurun_out/r35; mkdir -p $O
+O=gpurun_out/${RUNDIR:-r35}; mkdir -p $O
 timeout 2400 python -m pytest tests -q -m gpu > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/summary.log
 timeout 900 python bench.py --steps 10 --warmup 3 > $O/bench.json 2> $O/bench.err; echo "bench rc=$?" >> $O/summary.log
 timeout 600 python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-c2 --no-c3 > $O/b_plain.log 2>&1 && \
