@@ -583,8 +583,9 @@ def run_ours(a):
                 e.update({"macs_per_step": nf + ni, "mac_alu_frac": t_peak / (ms_k / 1e3)})
             fr = {"hbm": e.get("hbm_frac", 0.0), "alu": e.get("bfly_frac", e.get("mac_alu_frac", 0.0))}
             e["bound"] = max(fr, key=fr.get) if any(fr.values()) else None
-            if name in traffic_tab:
-                e["dram_bytes_per_step_ncu"] = traffic_tab[name]["dram_bytes_per_step"]
+            tk = name if name in traffic_tab else next((k for k in traffic_tab if k.startswith(name)), None)
+            if tk is not None:   # ncu names the template (k_cc_mac4), the library the launch (k_cc_mac)
+                e["dram_bytes_per_step_ncu"] = traffic_tab[tk]["dram_bytes_per_step"]
             per_kernel[name] = e
     ntt_doms = [k for k in sorted(prof, key=lambda k: -prof[k][0]) if k in C1_TRANSFORMS]
     roof = None

@@ -75,7 +75,7 @@ def main(rep, out_dir):
         a["source"] = "ncu --set full --clock-control none, one C1 step (tools/prof_step.py --step-only), cold/serialised"
     json.dump(agg, open(os.path.join(out_dir, "ncu_traffic.json"), "w"), indent=1)
     with open(os.path.join(out_dir, "ncu_step_summary.txt"), "w") as f:
-        f.write("kernel                    ms      DRAM_MB  issue%  fp64%  fmaheavy%  alu%  warps%  regs  top stalls/issue\n")
+        f.write("kernel                    ms      DRAM_MB  issue%  fp64%  fma%       alu%  warps%  regs  top stalls/issue\n")
         for e in lines:
             f.write("%-24s %7.4f %9.1f %6.1f %6.1f %9.1f %6.1f %6.1f %5.0f  %s\n" % (
                 e["kernel"][:24], e["ms"] or 0, e["dram_MB"], e["issue_active_pct"] or 0, e["fp64_pipe_pct"] or 0,
