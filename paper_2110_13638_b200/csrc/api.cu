@@ -91,12 +91,18 @@ struct edl_ctx {
 };
 
 namespace edl {
-void ensure_smem_attr(const void* kern, int bytes) {
-    static std::vector<const void*> done;
-    for (const void* k : done)
-        if (k == kern) return;
+void ensure_smem_attr(const void* kern, int bytes) {   // raise (never lower) a kernel's dynamic smem limit
+    static std::vector<std::pair<const void*, int>> done;
+    for (auto& e : done)
+        if (e.first == kern) {
+            if (bytes > e.second) {
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+                e.second = bytes;
+            }
+            return;
+        }
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    done.push_back(kern);
+    done.emplace_back(kern, bytes);
 }
 
 cudaEvent_t Prof::ev() {

@@ -426,9 +426,38 @@ k_cc_mac4(const uint64_t* __restrict__ x, int l, int W, int stride, int Wo, int 
     };
     // (measured: prefetching the next window's taps during this window's MACs, 128 registers,
     //  4 CTAs/SM: 0.46 ms vs 0.44 without)
+#ifdef EDL_CC4_ASYNC
+    // the next window's taps copied by cp.async into this thread's slots of a 2-stage
+    // shared-memory ring while this window computes (no registers held)
+    extern __shared__ uint64_t cc_ring[];   // [2][TAPS][CC4_T]
+    auto afetch = [&](int win, int st) {
+        const int wr = win / Wo, wc = win - (win / Wo) * Wo;
+        const uint64_t* xw = xb + (size_t)((wr * stride) * W + wc * stride) * ct_words;
+#pragma unroll
+        for (int t = 0; t < TAPS; t++)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(
+                             cc_ring + ((size_t)st * TAPS + t) * CC4_T + threadIdx.x)),
+                         "l"(xw + (size_t)((t / KW) * W + (t % KW)) * ct_words)
+                         : "memory");
+    };
+    const int w_beg = blockIdx.z * EDL_CC4_WPB;
+    if (w_beg < w_end) afetch(w_beg, 0);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+#endif
     for (int win = blockIdx.z * EDL_CC4_WPB; win < w_end; win++) {
         uint64_t xv[TAPS];
+#ifdef EDL_CC4_ASYNC
+        {
+            const int u = win - w_beg;
+            if (win + 1 < w_end) afetch(win + 1, (u + 1) & 1);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+#pragma unroll
+            for (int t = 0; t < TAPS; t++) xv[t] = cc_ring[((size_t)(u & 1) * TAPS + t) * CC4_T + threadIdx.x];
+        }
+#else
         fetch(win, xv);
+#endif
         uint64_t res[FC];
         if (mode == 2) {
             double s0[FC], s1[FC], s2[FC];
@@ -709,6 +738,41 @@ k_dense_mac(const uint64_t* __restrict__ x, int64_t K, int64_t O, int l, int ks,
 constexpr int DN3_T = 128;
 constexpr int DN3_U = 4;
 
+// EDL_DN3_ASYNC: the next DN3_U inputs copied by cp.async into this thread's slots of a
+// 2-stage shared-memory ring (behind the weight slice) while the current ones compute
+// (C1 dense 0.146-0.150 -> 0.140 ms; EDL_DN3_ASYNC=0 restores register loads).
+#ifndef EDL_DN3_ASYNC
+#define EDL_DN3_ASYNC 1
+#endif
+#if EDL_DN3_ASYNC == 0
+#undef EDL_DN3_ASYNC
+#endif
+#ifdef EDL_DN3_ASYNC
+#define DN3_RING_PROLOGUE                                                                                      \
+    uint64_t* ring = reinterpret_cast<uint64_t*>(wsm3 + kc * OC);                                             \
+    auto afetch = [&](int k0_, int st) {                                                                       \
+        _Pragma("unroll") for (int u = 0; u < DN3_U; u++) if (k0_ + u < kc) asm volatile(                    \
+            "cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(              \
+                ring + ((size_t)st * DN3_U + u) * DN3_T + threadIdx.x)), "l"(xp + (size_t)(k0_ + u) * kstride) \
+            : "memory");                                                                                       \
+    };                                                                                                         \
+    afetch(0, 0);                                                                                              \
+    asm volatile("cp.async.commit_group;" ::: "memory");
+#define DN3_FETCH(xv)                                                                                          \
+    {                                                                                                          \
+        const int it = kk / DN3_U;                                                                             \
+        if (kk + DN3_U < kc) afetch(kk + DN3_U, (it + 1) & 1);                                                 \
+        asm volatile("cp.async.commit_group;" ::: "memory");                                                   \
+        asm volatile("cp.async.wait_group 1;" ::: "memory");                                                   \
+        _Pragma("unroll") for (int u = 0; u < DN3_U; u++) xv[u] =                                             \
+            (kk + u < kc) ? ring[((size_t)(it & 1) * DN3_U + u) * DN3_T + threadIdx.x] : 0;                   \
+    }
+#else
+#define DN3_RING_PROLOGUE
+#define DN3_FETCH(xv)                                                                                          \
+    _Pragma("unroll") for (int u = 0; u < DN3_U; u++) xv[u] = (kk + u < kc) ? __ldg(xp + (size_t)(kk + u) * kstride) : 0;
+#endif
+
 template <int OC>
 __global__ void __launch_bounds__(DN3_T)
 k_dense_mac3(const uint64_t* __restrict__ x, int64_t K, int O, int l, int kper, const ulonglong2* __restrict__ wd,
@@ -738,10 +802,10 @@ k_dense_mac3(const uint64_t* __restrict__ x, int64_t K, int O, int l, int kper, 
         double acc[OC];
 #pragma unroll
         for (int o = 0; o < OC; o++) acc[o] = 0.0;
+        DN3_RING_PROLOGUE
         for (int kk = 0; kk < kc; kk += DN3_U) {
             uint64_t xv[DN3_U];
-#pragma unroll
-            for (int u = 0; u < DN3_U; u++) xv[u] = (kk + u < kc) ? __ldg(xp + (size_t)(kk + u) * kstride) : 0;
+            DN3_FETCH(xv)
 #pragma unroll
             for (int u = 0; u < DN3_U; u++) {
                 if (kk + u >= kc) break;
@@ -760,10 +824,10 @@ k_dense_mac3(const uint64_t* __restrict__ x, int64_t K, int O, int l, int kper, 
         U128 acc[OC];
 #pragma unroll
         for (int o = 0; o < OC; o++) acc[o].lo = acc[o].hi = 0;
+        DN3_RING_PROLOGUE
         for (int kk = 0; kk < kc; kk += DN3_U) {
             uint64_t xv[DN3_U];
-#pragma unroll
-            for (int u = 0; u < DN3_U; u++) xv[u] = (kk + u < kc) ? __ldg(xp + (size_t)(kk + u) * kstride) : 0;
+            DN3_FETCH(xv)
 #pragma unroll
             for (int u = 0; u < DN3_U; u++) {
                 if (kk + u >= kc) break;
@@ -1087,6 +1151,14 @@ constexpr int MAC3_T = 256;
 #define EDL_MAC3_CTS 8
 #endif
 constexpr int MAC3_CTS = EDL_MAC3_CTS;
+// operand ring depth (cp.async, shared memory): measured on C1 (round 2b) 2 stages 0.552 ms,
+// 3 stages 0.564, 4 stages 0.557, register prefetch (0 = off) 0.599; 4 CTAs/SM 0.559
+#ifndef EDL_MAC3_ASYNC
+#define EDL_MAC3_ASYNC 2
+#endif
+#if EDL_MAC3_ASYNC == 0
+#undef EDL_MAC3_ASYNC
+#endif
 
 // pfold: the data targets' key entries already carry the factor P^-1 (the context's
 // P^-1-folded copy of rlk, keygen), so v = d + acc directly.
@@ -1142,11 +1214,59 @@ __device__ __forceinline__ void mac3_body(const uint64_t* __restrict__ a, const 
             o.a0 = o.a1 = o.b0 = o.b1 = 0;
         }
     };
+#ifdef EDL_MAC3_ASYNC
+    // operands of ciphertext c + S - 1 copied into this thread's slots of a shared-memory
+    // ring by cp.async while ciphertext c computes (S - 1 ciphertexts in flight, no registers
+    // held); each thread reads back only words it copied itself, so no barrier
+    extern __shared__ uint64_t mac_ring[];   // [S][ND + 4][MAC3_T]
+    constexpr int S = EDL_MAC3_ASYNC, NO = ND + 4;
+    const int tid = threadIdx.x;
+    auto slot = [&](int st, int o) { return mac_ring + ((size_t)st * NO + o) * MAC3_T + tid; };
+    auto cpa = [&](uint64_t* dst, const uint64_t* src) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+                     : "memory");
+    };
+    auto afetch = [&](int64_t c, int st) {
+#pragma unroll
+        for (int j = 0; j < ND; j++)
+            if (j != ti) cpa(slot(st, j), xb + (size_t)c * xs_c + (size_t)j * (l + 2) * limb);
+        if (data) {
+            cpa(slot(st, ND + 0), a0b + (size_t)c * cs);
+            cpa(slot(st, ND + 1), a1b + (size_t)c * cs);
+            if (!single) {
+                cpa(slot(st, ND + 2), b0b + (size_t)c * cs);
+                cpa(slot(st, ND + 3), b1b + (size_t)c * cs);
+            }
+        }
+    };
+#pragma unroll
+    for (int u = 0; u < S - 1; u++) {
+        if (c_beg + u < c_end) afetch(c_beg + u, u);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    for (int64_t c = c_beg; c < c_end; c++) {
+        const int u = (int)(c - c_beg);
+        if (c + S - 1 < c_end) afetch(c + S - 1, (u + S - 1) % S);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group %0;" ::"n"(S - 1) : "memory");
+        const int st = u % S;
+        Ops cur;
+#pragma unroll
+        for (int j = 0; j < ND; j++) cur.x[j] = (j != ti) ? *slot(st, j) : 0;
+        cur.a0 = cur.a1 = cur.b0 = cur.b1 = 0;
+        if (data) {
+            cur.a0 = *slot(st, ND + 0);
+            cur.a1 = *slot(st, ND + 1);
+            cur.b0 = single ? cur.a0 : *slot(st, ND + 2);
+            cur.b1 = single ? cur.a1 : *slot(st, ND + 3);
+        }
+#else
     Ops nx;
     if (c_beg < c_end) fetch(c_beg, nx);
     for (int64_t c = c_beg; c < c_end; c++) {
         const Ops cur = nx;
         if (c + 1 < c_end) fetch(c + 1, nx);
+#endif
         uint64_t v0, v1;
         if constexpr (F64) {
             double s0 = 0.0, s1 = 0.0;
@@ -1500,6 +1620,19 @@ void launch_pack(const Dev& d, const uint64_t* in, int64_t polys, int nl, const 
                                                                                                  d.logn, stride));
 }
 
+// dynamic shared memory of k_relin_mac3 (the cp.async operand ring, EDL_MAC3_ASYNC stages)
+static int mac3_smem(int nd, const void* kern) {
+#ifdef EDL_MAC3_ASYNC
+    const int bytes = EDL_MAC3_ASYNC * (nd + 4) * MAC3_T * 8;
+    ensure_smem_attr(kern, bytes);
+    return bytes;
+#else
+    (void)nd;
+    (void)kern;
+    return 0;
+#endif
+}
+
 void launch_relin_mac(const Dev& d, const uint64_t* a, const uint64_t* b, int64_t cnt, int l, const uint64_t* xh,
                       const uint64_t* rlk, const uint64_t* rlk_c, uint64_t* acc) {
     // one launch per arithmetic path (targets grouped by their modulus' mode)
@@ -1526,10 +1659,10 @@ void launch_relin_mac(const Dev& d, const uint64_t* a, const uint64_t* b, int64_
 #define EDL_MAC3_ND(ND)                                                                                            \
     case ND:                                                                                                       \
         if (na)                                                                                                    \
-            EDL_LAUNCH(d, "k_relin_mac", (k_relin_mac3<-1, ND><<<dim3(gx3, na, gz3), MAC3_T, 0, d.st>>>(          \
+            EDL_LAUNCH(d, "k_relin_mac", (k_relin_mac3<-1, ND><<<dim3(gx3, na, gz3), MAC3_T, mac3_smem(ND, (const void*)k_relin_mac3<-1, ND>), d.st>>>( \
                                              a, b, l, d.L, cnt, xh, kk, kkc, acc, all, *d.mt, d.cc, d.logn, pfold))); \
         if (nf)                                                                                                    \
-            EDL_LAUNCH(d, "k_relin_mac", (k_relin_mac3<1, ND><<<dim3(gx3, nf, gz3), MAC3_T, 0, d.st>>>(           \
+            EDL_LAUNCH(d, "k_relin_mac", (k_relin_mac3<1, ND><<<dim3(gx3, nf, gz3), MAC3_T, mac3_smem(ND, (const void*)k_relin_mac3<1, ND>), d.st>>>( \
                                              a, b, l, d.L, cnt, xh, kk, kkc, acc, tf, *d.mt, d.cc, d.logn, pfold))); \
         break;
 #else
@@ -1653,7 +1786,16 @@ void launch_cc_mac(const Dev& d, const uint64_t* x, int l, int H, int W, int F, 
                     memcpy(&wt.c44[i][1], &b44, 8);
                     memcpy(&wt.c44[i][2], &b22, 8);
                 }
+#ifdef EDL_CC4_ASYNC
+#define EDL_CC4(FCV)                                                                                         \
+    {                                                                                                        \
+        const int sm4 = 2 * 16 * CC4_T * 8;                                                                  \
+        ensure_smem_attr((const void*)k_cc_mac4<FCV, 4, 4>, sm4);                                            \
+        EDL_LAUNCH(d, "k_cc_mac", (k_cc_mac4<FCV, 4, 4><<<grid, CC4_T, sm4, d.st>>>(x, l, W, stride, Wo, nwin, f0, F, nwin, out, wt, *d.mt, d.logn))); \
+    }
+#else
 #define EDL_CC4(FCV) EDL_LAUNCH(d, "k_cc_mac", (k_cc_mac4<FCV, 4, 4><<<grid, CC4_T, 0, d.st>>>(x, l, W, stride, Wo, nwin, f0, F, nwin, out, wt, *d.mt, d.logn)))
+#endif
             switch (fc) {
                 case 1: EDL_CC4(1); break;
                 case 2: EDL_CC4(2); break;
@@ -1739,9 +1881,16 @@ void launch_dense_mac(const Dev& d, const uint64_t* x, int64_t K, int64_t O, int
         if (kper <= 256) {   // exact binary64 / 128-bit sums bounded for <= 256 terms
             const int oc = O <= 4 ? 4 : (O <= 8 ? 8 : (O == 10 ? 10 : (O <= 12 ? 12 : 16)));
             dim3 grid((unsigned)((1 << d.logn) / DN3_T), (unsigned)(2 * (l + 1)), (unsigned)ks);
-            const size_t smem = (size_t)kper * oc * sizeof(ulonglong2);
+            size_t smem = (size_t)kper * oc * sizeof(ulonglong2);
+#ifdef EDL_DN3_ASYNC
+            smem += (size_t)2 * DN3_U * DN3_T * 8;   // cp.async input ring
+#endif
             uint64_t* dst = ks > 1 ? part : out;
-#define EDL_DN3(OCV) EDL_LAUNCH(d, "k_dense_mac", (k_dense_mac3<OCV><<<grid, DN3_T, smem, d.st>>>(x, K, (int)O, l, kper, wd, dst, *d.mt, d.logn)))
+#define EDL_DN3(OCV)                                                                                \
+    {                                                                                               \
+        ensure_smem_attr((const void*)k_dense_mac3<OCV>, (int)smem); /* kper x 16 x 16 B can pass 48 KB */ \
+        EDL_LAUNCH(d, "k_dense_mac", (k_dense_mac3<OCV><<<grid, DN3_T, smem, d.st>>>(x, K, (int)O, l, kper, wd, dst, *d.mt, d.logn))); \
+    }
             switch (oc) {
                 case 4: EDL_DN3(4); break;
                 case 8: EDL_DN3(8); break;
