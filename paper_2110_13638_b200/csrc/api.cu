@@ -91,6 +91,13 @@ struct edl_ctx {
 };
 
 namespace edl {
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("EDL_PDL");   // default on; EDL_PDL=0 turns it off
+        return e == nullptr || e[0] != '0';
+    }();
+    return on;
+}
 void ensure_smem_attr(const void* kern, int bytes) {   // raise (never lower) a kernel's dynamic smem limit
     static std::vector<std::pair<const void*, int>> done;
     for (auto& e : done)

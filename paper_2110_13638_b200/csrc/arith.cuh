@@ -10,6 +10,24 @@
 #pragma once
 #include <cstdint>
 
+// ---- programmatic dependent launch (round 2c) -----------------------------------------
+// Every kernel of the library starts with EDL_PDL_ENTRY(): griddepcontrol.wait blocks until
+// the preceding kernel of the stream has completed and its memory is visible, so a kernel
+// launched with the programmatic-serialization attribute (EDL_PDL, kernels.cuh) may be
+// scheduled while its predecessor's last wave still runs without reading or overwriting
+// anything early; launched without the attribute both instructions are no-ops.  With
+// EDL_PDL_TRIGGER each CTA also signals at entry that the dependent grid may launch (it can
+// then become resident as soon as this grid's last CTAs are running).
+#ifdef EDL_PDL_TRIGGER
+#define EDL_PDL_ENTRY()                                                  \
+    do {                                                                 \
+        asm volatile("griddepcontrol.wait;" ::: "memory");               \
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
+    } while (0)
+#else
+#define EDL_PDL_ENTRY() asm volatile("griddepcontrol.wait;" ::: "memory")
+#endif
+
 namespace edl {
 
 struct ModInfo {

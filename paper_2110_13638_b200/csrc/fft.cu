@@ -35,6 +35,7 @@ __device__ __forceinline__ uint32_t pow5(uint32_t j, uint32_t two_n) {
 
 __global__ void k_encode_prep(const double* __restrict__ z, int64_t n_vec, int64_t n_slots, int logn,
                               double2* __restrict__ v) {
+    EDL_PDL_ENTRY();
     const int64_t n = 1LL << logn;
     const int64_t b = blockIdx.y;
     double2* vb = v + b * n;
@@ -77,6 +78,7 @@ __device__ void fft_smem(double2* a, const double2* root, int L, int logL) {
 // stage 1: for vector b, column c < n2: X1[k1][c] = twist^(k1 c) sum_r x[r n2 + c] w128^(r k1)
 __global__ void __launch_bounds__(FFT_N1) k_fft_cols(const double2* __restrict__ in, double2* __restrict__ out, int logn,
                                                      int sign) {
+    EDL_PDL_ENTRY();
     __shared__ double2 col[FFT_N1];
     __shared__ double2 root[FFT_N1 / 2];
     const int64_t n = 1LL << logn;
@@ -98,6 +100,7 @@ __global__ void __launch_bounds__(FFT_N1) k_fft_cols(const double2* __restrict__
 
 // stage 2: for vector b, row k1: X[k1 + 128 k2] = sum_c X1[k1][c] w_{n2}^(c k2)
 __global__ void k_fft_rows(const double2* __restrict__ in, double2* __restrict__ out, int logn, int sign) {
+    EDL_PDL_ENTRY();
     extern __shared__ double2 sh[];   // row [n2] then roots [n2 / 2]
     const int64_t n = 1LL << logn;
     const int n2 = (int)(n / FFT_N1);
@@ -121,6 +124,7 @@ __global__ void k_fft_rows(const double2* __restrict__ in, double2* __restrict__
 
 __global__ void k_encode_finish(const double2* __restrict__ w, int64_t n_vec, int logn, double scale,
                                 int64_t* __restrict__ m) {
+    EDL_PDL_ENTRY();
     const int64_t n = 1LL << logn;
     const int64_t b = blockIdx.y;
     for (int64_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
@@ -136,6 +140,7 @@ __global__ void k_encode_finish(const double2* __restrict__ w, int64_t n_vec, in
 __global__ void k_decode_prep(const uint64_t* __restrict__ r, int64_t n_vec, int nl, const uint64_t* __restrict__ q,
                               const uint64_t* __restrict__ qhat_inv, const uint64_t* __restrict__ qhat64,
                               uint64_t Q64, int logn, double2* __restrict__ v) {
+    EDL_PDL_ENTRY();
     const int64_t n = 1LL << logn;
     const int64_t b = blockIdx.y;
     for (int64_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
@@ -164,6 +169,7 @@ __global__ void k_decode_prep(const uint64_t* __restrict__ r, int64_t n_vec, int
 
 __global__ void k_decode_finish(const double2* __restrict__ v, int64_t n_vec, int64_t n_slots, int logn, double scale,
                                 double* __restrict__ z) {
+    EDL_PDL_ENTRY();
     const int64_t n = 1LL << logn;
     const int64_t b = blockIdx.y;
     for (int64_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n_slots; j += gridDim.x * blockDim.x) {

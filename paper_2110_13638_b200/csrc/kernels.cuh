@@ -89,6 +89,35 @@ struct Dev {
 
 void ensure_smem_attr(const void* kern, int bytes);
 
+// Programmatic dependent launch (arith.cuh EDL_PDL_ENTRY; on unless EDL_PDL=0 in the
+// environment, read once): the launch may overlap the tail of the stream's previous kernel.
+// Off while per-launch profiling brackets every launch with events (they serialise anyway).
+// Measured (C1, B200, round 2c): 4.024 -> 4.002 ms per step; with an early trigger
+// (griddepcontrol.launch_dependents at CTA entry, EDL_PDL_TRIGGER) 4.03: the waiting
+// dependent CTAs take SM slots the other stream's kernels would use.
+bool pdl_enabled();
+inline int pdl_attr(const Dev& d, cudaLaunchAttribute* at) {
+    if (!pdl_enabled() || d.prof->on) return 0;
+    at->id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at->val.programmaticStreamSerializationAllowed = 1;
+    return 1;
+}
+// A plain (non-cluster) launch with the PDL attribute: the <<<>>> form of the hot kernels.
+template <typename... KArgs, typename... Args>
+void launch_k(const Dev& d, const char* name, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = d.st;
+    cudaLaunchAttribute at[1];
+    cfg.numAttrs = pdl_attr(d, at);
+    cfg.attrs = at;
+    d.prof->begin(name, d.st);
+    cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+    d.prof->end(d.st);
+}
+
 // Launch an NTT-family kernel with config C: grid.x is multiplied by the cluster size
 // C::K (consecutive blocks form one limb's cluster), block = C::T threads, dynamic shared
 // memory C::SMEM_BYTES.
@@ -102,13 +131,18 @@ void launch_cfg_x(const Dev& d, const char* name, void (*kern)(KArgs...), dim3 g
     cfg.blockDim = dim3(C::T, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = d.st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = C::K;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (C::K > 1) {
+        at[na].id = cudaLaunchAttributeClusterDimension;
+        at[na].val.clusterDim.x = C::K;
+        at[na].val.clusterDim.y = 1;
+        at[na].val.clusterDim.z = 1;
+        na++;
+    }
+    na += pdl_attr(d, at + na);
     cfg.attrs = at;
-    cfg.numAttrs = C::K > 1 ? 1 : 0;
+    cfg.numAttrs = na;
     d.prof->begin(name, d.st);
     cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
     d.prof->end(d.st);

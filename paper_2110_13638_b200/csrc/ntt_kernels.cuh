@@ -60,6 +60,7 @@ __device__ __forceinline__ auto epi_pre(const uint64_t* base, uint64_t* sm) {
 template <class C, bool INV>
 __global__ void __launch_bounds__(C::T, C::MINB)
 k_ntt_limbs(uint64_t* __restrict__ data, int nl, const __grid_constant__ PrimeMap pm, const __grid_constant__ ModTable mods) {
+    EDL_PDL_ENTRY();
     extern __shared__ uint64_t sm[];
     const int limb = blockIdx.y;    // limb-major grid: co-resident CTAs share a prime (code path, twiddles)
     uint64_t* p = data + (((size_t)C::bx() * nl + limb) << C::LOGN);
@@ -79,6 +80,7 @@ template <class C, bool INV>
 __global__ void __launch_bounds__(C::T, C::MINB)
 k_ntt_limbs_p(uint64_t* __restrict__ data, int64_t batch, int nl, const __grid_constant__ PrimeMap pm,
               const __grid_constant__ ModTable mods) {
+    EDL_PDL_ENTRY();
     extern __shared__ __align__(16) uint64_t sm[];
     ulonglong2* tws = reinterpret_cast<ulonglong2*>(sm + C::SMEM_WORDS);
     __shared__ alignas(8) uint64_t mbar;
@@ -150,6 +152,7 @@ __global__ void __launch_bounds__(C::T, C::MINB)
 k_rescale_intt(const uint64_t* __restrict__ in, int l, const ulonglong2* __restrict__ w,
                uint64_t* __restrict__ r_out, const ulonglong2* __restrict__ w2, uint64_t* __restrict__ r_out2,
                const __grid_constant__ ModTable mods) {
+    EDL_PDL_ENTRY();
     extern __shared__ uint64_t sm[];
     const int p = blockIdx.y;
     const int64_t c = C::bx();
@@ -192,6 +195,7 @@ __global__ void __launch_bounds__(C::T, C::MINB)
 k_rescale_ntt(const uint64_t* __restrict__ in, int l, const ulonglong2* __restrict__ w,
               const uint64_t* __restrict__ r, const uint64_t* __restrict__ bias, uint64_t* __restrict__ out, int nlo,
               const __grid_constant__ ModTable mods, const ChainConsts* __restrict__ cc) {
+    EDL_PDL_ENTRY();
     extern __shared__ uint64_t sm[];
     int64_t c;
     int p, i;
@@ -254,6 +258,7 @@ template <class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
 k_relin_intt_d2(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l,
                 uint64_t* __restrict__ acoef, const __grid_constant__ ModTable mods) {
+    EDL_PDL_ENTRY();
     extern __shared__ uint64_t sm[];
     const int j = blockIdx.y;
     const int64_t c = C::bx();
@@ -296,6 +301,7 @@ template <class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
 k_relin_modup(const uint64_t* __restrict__ acoef, int l, int L, uint64_t* __restrict__ xh,
               const __grid_constant__ ModTable mods) {
+    EDL_PDL_ENTRY();
     extern __shared__ uint64_t sm[];
     // y enumerates (target, digit) target-major: data targets ti = 0..l with the l digits
     // j != ti, then P (ti = l+1) with all l+1 digits, so co-resident CTAs (limb-major
@@ -356,6 +362,7 @@ __global__ void __launch_bounds__(C::T, C::MINB)
 k_relin_ks(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l, int L,
            const uint64_t* __restrict__ acoef, const uint64_t* __restrict__ rlk, const uint64_t* __restrict__ rlk_c,
            uint64_t* __restrict__ acc_out, const __grid_constant__ ModTable mods, const ChainConsts* __restrict__ cc) {
+    EDL_PDL_ENTRY();
     extern __shared__ __align__(16) uint64_t sm[];
     uint64_t* accs = sm + C::SMEM_WORDS;   // [2][E][T]: slot of output C::idx(r) = r T + tid
     const int ti = blockIdx.y;              // 0..l data targets, l+1 = P
@@ -482,6 +489,7 @@ template <class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
 k_relin_raise(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int l, int L, uint64_t* __restrict__ xh,
               const __grid_constant__ ModTable mods) {
+    EDL_PDL_ENTRY();
     static_assert(C::K > 1, "cluster configuration");
     extern __shared__ __align__(16) uint64_t sm[];
     uint64_t* dig = sm + C::SMEM_WORDS;   // [E][T]
@@ -537,6 +545,7 @@ k_relin_moddown_intt(const uint64_t* __restrict__ a, const uint64_t* __restrict_
                      const uint64_t* __restrict__ acc, int L, int rescale_unused, uint64_t* __restrict__ r_out,
                      uint64_t* __restrict__ s_out, const __grid_constant__ ModTable mods,
                      const ChainConsts* __restrict__ cc) {
+    EDL_PDL_ENTRY();
     extern __shared__ uint64_t sm[];
     const int cp = blockIdx.y;
     const int64_t c = C::bx();
@@ -589,6 +598,7 @@ k_relin_moddown_ntt(const uint64_t* __restrict__ a, const uint64_t* __restrict__
                     const uint64_t* __restrict__ s, int L, int rescale_unused, uint64_t* __restrict__ out,
                     const uint64_t* __restrict__ add_w, const uint64_t* __restrict__ add_k,
                     const __grid_constant__ ModTable mods, const ChainConsts* __restrict__ cc) {
+    EDL_PDL_ENTRY();
     extern __shared__ uint64_t sm[];
     int64_t c;
     int cp, i;

@@ -9,6 +9,7 @@
 namespace edl {
 
 __global__ void __launch_bounds__(256) k_modmul_peak(uint64_t q, uint64_t w, uint64_t ws, int iters, uint64_t* sink) {
+    EDL_PDL_ENTRY();
     uint64_t x[8];
 #pragma unroll
     for (int k = 0; k < 8; k++) x[k] = (threadIdx.x * 8 + k + 1) % q;
@@ -30,6 +31,7 @@ __global__ void __launch_bounds__(256) k_modmul_peak(uint64_t q, uint64_t w, uin
 template <bool FP>
 __global__ void __launch_bounds__(256) k_bfly_peak(uint64_t q, const ulonglong2* __restrict__ tw, int iters,
                                                    uint64_t* sink) {
+    EDL_PDL_ENTRY();
     uint64_t x[16];
     ulonglong2 w[8];
 #pragma unroll
@@ -74,6 +76,7 @@ void launch_bfly_peak(const Dev& d, uint64_t q, bool fp, const ulonglong2* tw, i
 // multiply the Shoup path is built from), 256 threads x 8 CTAs per SM, register-only.
 // Reports lane-operations per second (one DFMA or one IMAD.WIDE per lane).
 __global__ void __launch_bounds__(256) k_pipe_dfma(double a, double b, int iters, uint64_t* sink) {
+    EDL_PDL_ENTRY();
     double x[8];
 #pragma unroll
     for (int k = 0; k < 8; k++) x[k] = (double)(threadIdx.x + k);
@@ -87,6 +90,7 @@ __global__ void __launch_bounds__(256) k_pipe_dfma(double a, double b, int iters
     if (acc == 1.2345) sink[0] = 1;
 }
 __global__ void __launch_bounds__(256) k_pipe_imadw(uint32_t a, int iters, uint64_t* sink) {
+    EDL_PDL_ENTRY();
     uint64_t x[8];
 #pragma unroll
     for (int k = 0; k < 8; k++) x[k] = threadIdx.x + k;
@@ -108,6 +112,7 @@ __global__ void __launch_bounds__(256) k_pipe_imadw(uint32_t a, int iters, uint6
 // accumulators per thread): (2) the F64 path acc += f64_mulc(x, w, RD(w/q), q) for a 40-bit
 // prime, (3) the 60-bit path's lazy 128-bit acc += x w (mac128).  One MAC per lane-op.
 __global__ void __launch_bounds__(256) k_pipe_fmac(double q, double w, double wq, int iters, uint64_t* sink) {
+    EDL_PDL_ENTRY();
     double acc[8], x[8];
 #pragma unroll
     for (int k = 0; k < 8; k++) {
@@ -130,6 +135,7 @@ __global__ void __launch_bounds__(256) k_pipe_fmac(double q, double w, double wq
     if (a == 1.5) sink[0] = 1;
 }
 __global__ void __launch_bounds__(256) k_pipe_imac(uint64_t w, int iters, uint64_t* sink) {
+    EDL_PDL_ENTRY();
     U128 acc[8];
     uint64_t x[8];
 #pragma unroll

@@ -30,6 +30,7 @@ dim3 rows_grid(int logn, int64_t rows) {
 // ---------------------------------------------------------------- add
 __global__ void k_add(const uint64_t* __restrict__ a, int la, const uint64_t* __restrict__ b, int lb, int64_t cnt,
                       int lo, uint64_t* __restrict__ out, const __grid_constant__ ModTable mods, int logn) {
+    EDL_PDL_ENTRY();
     const int64_t rows = cnt * 2 * (lo + 1);
     const int n2 = 1 << (logn - 1);
     for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
@@ -49,6 +50,7 @@ __global__ void k_add(const uint64_t* __restrict__ a, int la, const uint64_t* __
 // ---------------------------------------------------------------- scalar const multiply
 __global__ void k_mul_const(const uint64_t* __restrict__ a, int64_t cnt, int l, const ulonglong2* __restrict__ w,
                             uint64_t* __restrict__ out, const __grid_constant__ ModTable mods, int logn) {
+    EDL_PDL_ENTRY();
     const int64_t rows = cnt * 2 * (l + 1);
     const int n2 = 1 << (logn - 1);
     for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
@@ -68,6 +70,7 @@ __global__ void k_mul_const(const uint64_t* __restrict__ a, int64_t cnt, int l, 
 // ---------------------------------------------------------------- add constant (poly 0 only)
 __global__ void k_add_const(const uint64_t* __restrict__ a, int64_t cnt, int l, const uint64_t* __restrict__ kc,
                             uint64_t* __restrict__ out, const __grid_constant__ ModTable mods, int logn) {
+    EDL_PDL_ENTRY();
     const int64_t rows = cnt * 2 * (l + 1);
     const int n2 = 1 << (logn - 1);
     for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
@@ -88,6 +91,7 @@ __global__ void k_add_const(const uint64_t* __restrict__ a, int64_t cnt, int l, 
 // ---------------------------------------------------------------- mod drop (copy limbs 0..lo)
 __global__ void k_mod_drop(const uint64_t* __restrict__ a, int64_t cnt, int la, int lo, uint64_t* __restrict__ out,
                            int logn) {
+    EDL_PDL_ENTRY();
     const int64_t rows = cnt * 2 * (lo + 1);
     const int n2 = 1 << (logn - 1);
     for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
@@ -102,6 +106,7 @@ __global__ void k_mod_drop(const uint64_t* __restrict__ a, int64_t cnt, int la, 
 // ---------------------------------------------------------------- in-place x mod q (after NCCL uint64 sum)
 __global__ void k_mod_reduce(uint64_t* __restrict__ x, int64_t cnt, int l, const __grid_constant__ ModTable mods,
                              int logn) {
+    EDL_PDL_ENTRY();
     const int64_t rows = cnt * 2 * (l + 1);
     const int n2 = 1 << (logn - 1);
     for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
@@ -118,6 +123,7 @@ __global__ void k_mod_reduce(uint64_t* __restrict__ x, int64_t cnt, int l, const
 __global__ void k_add_add_const(const uint64_t* __restrict__ v, const uint64_t* __restrict__ w, int lw, int64_t cnt,
                                 int lo, const uint64_t* __restrict__ kc, uint64_t* __restrict__ out,
                                 const __grid_constant__ ModTable mods, int logn) {
+    EDL_PDL_ENTRY();
     const int64_t rows = cnt * 2 * (lo + 1);
     const int n2 = 1 << (logn - 1);
     for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
@@ -149,6 +155,7 @@ constexpr int CC_TAPS = 16;
 __global__ void __launch_bounds__(PW_THREADS, 2)
 k_cc_mac(const uint64_t* __restrict__ x, int l, int H, int W, int F, int kh, int kw, int stride,
          const ulonglong2* __restrict__ wk, uint64_t* __restrict__ out, const __grid_constant__ ModTable mods, int logn) {
+    EDL_PDL_ENTRY();
     extern __shared__ uint64_t wsm[];   // [F][taps] residues for this limb
     const int nl = l + 1;
     const int p = blockIdx.y / nl, i = blockIdx.y % nl;
@@ -224,6 +231,7 @@ __global__ void __launch_bounds__(CC2_THREADS, EDL_CC2_MINB)
 k_cc_mac2(const uint64_t* __restrict__ x, int l, int W, int kw, int stride, int Wo, int taps, int f0, int F,
           int n_out_per_f, const ulonglong2* __restrict__ wk, uint64_t* __restrict__ out,
           const __grid_constant__ ModTable mods, int logn) {
+    EDL_PDL_ENTRY();
     __shared__ ulonglong2 wsm[FC * CC2_MAXTAPS];  // [f][tap] {residue, companion} of this limb
     __shared__ int tpix[CC2_MAXTAPS];            // pixel (ciphertext) index of each tap
     const int nl = l + 1;
@@ -399,6 +407,7 @@ template <int FC, int KH, int KW>
 __global__ void __launch_bounds__(CC4_T, EDL_CC4_MINB)
 k_cc_mac4(const uint64_t* __restrict__ x, int l, int W, int stride, int Wo, int nwin, int f0, int F, int n_out_per_f,
           uint64_t* __restrict__ out, const __grid_constant__ CCW4 wt, const __grid_constant__ ModTable mods, int logn) {
+    EDL_PDL_ENTRY();
     constexpr int TAPS = KH * KW;
     static_assert(TAPS <= CC4_TAPS && FC <= CC4_MAXF, "k_cc_mac4 geometry");
     const int nl = l + 1;
@@ -525,6 +534,7 @@ __global__ void __launch_bounds__(CC3_T, 8)
 k_cc_mac3(const uint64_t* __restrict__ x, int l, int W, int kw, int stride, int Wo, int taps, int f0, int F,
           int n_out_per_f, const ulonglong2* __restrict__ wk, uint64_t* __restrict__ out,
           const __grid_constant__ ModTable mods, int logn) {
+    EDL_PDL_ENTRY();
     __shared__ ulonglong2 wsm[FC * CC2_MAXTAPS];   // [f][tap] {residue (binary64 on F64 limbs), companion}
     __shared__ int tpix[CC2_MAXTAPS];
     const int nl = l + 1;
@@ -651,6 +661,7 @@ constexpr int DN_U = 4;
 __global__ void __launch_bounds__(PW_THREADS, 2)
 k_dense_mac(const uint64_t* __restrict__ x, int64_t K, int64_t O, int l, int ks, const ulonglong2* __restrict__ wd,
             uint64_t* __restrict__ out, const __grid_constant__ ModTable mods, int logn) {
+    EDL_PDL_ENTRY();
     extern __shared__ ulonglong2 wsm2[];   // [DN_OC][DN_KC] {residue, companion}
     const int nl = l + 1;
     const int p = blockIdx.y / nl, i = blockIdx.y % nl;
@@ -777,6 +788,7 @@ template <int OC>
 __global__ void __launch_bounds__(DN3_T)
 k_dense_mac3(const uint64_t* __restrict__ x, int64_t K, int O, int l, int kper, const ulonglong2* __restrict__ wd,
              uint64_t* __restrict__ out, const __grid_constant__ ModTable mods, int logn) {
+    EDL_PDL_ENTRY();
     extern __shared__ ulonglong2 wsm3[];   // [kper][OC] {residue (binary64 on F64 limbs), companion}
     const int nl = l + 1;
     const int p = blockIdx.y / nl, i = blockIdx.y % nl;
@@ -848,6 +860,7 @@ k_dense_mac3(const uint64_t* __restrict__ x, int64_t K, int O, int l, int kper, 
 // out[r][k] = sum_s part[s][r][k] mod q over ks slices (rows = O * 2 * nl limbs).
 __global__ void k_dense_combine(const uint64_t* __restrict__ part, int ks, int64_t O, int l, uint64_t* __restrict__ out,
                                 const __grid_constant__ ModTable mods, int logn) {
+    EDL_PDL_ENTRY();
     const int64_t rows = O * 2 * (l + 1);
     const int n2 = 1 << (logn - 1);
     const size_t slice = (size_t)rows << logn;
@@ -885,6 +898,7 @@ k_relin_mac(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int 
             const uint64_t* __restrict__ xh, const uint64_t* __restrict__ rlk, const uint64_t* __restrict__ rlk_c,
             uint64_t* __restrict__ acc, const __grid_constant__ TargetList tl, const __grid_constant__ ModTable mods,
             const ChainConsts* __restrict__ chain, int logn) {
+    EDL_PDL_ENTRY();
     const int ti = tl.slot[blockIdx.y];        // 0..l data targets, l+1 = P
     const int64_t c0 = (int64_t)blockIdx.z * MAC_CB;
     const int t = (ti == l + 1) ? (L + 1) : ti;
@@ -1022,6 +1036,7 @@ k_relin_mac2(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int
              const uint64_t* __restrict__ xh, const uint64_t* __restrict__ rlk, const uint64_t* __restrict__ rlk_c,
              uint64_t* __restrict__ acc, const __grid_constant__ TargetList tl, const __grid_constant__ ModTable mods,
              const ChainConsts* __restrict__ chain, int logn) {
+    EDL_PDL_ENTRY();
     // [digit][comp][thread] {key pair, companion pair}
     extern __shared__ ulonglong2 ks[];
     constexpr bool FP = MODE != 0;
@@ -1371,6 +1386,7 @@ k_relin_mac3(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int
              const uint64_t* __restrict__ xh, const uint64_t* __restrict__ rlk, const uint64_t* __restrict__ rlk_c,
              uint64_t* __restrict__ acc, const __grid_constant__ TargetList tl, const __grid_constant__ ModTable mods,
              const ChainConsts* __restrict__ chain, int logn, int pfold) {
+    EDL_PDL_ENTRY();
     const int ti = tl.slot[blockIdx.y];
     const int t = (ti == l + 1) ? (L + 1) : ti;
     const ModInfo& m = mods[t];
@@ -1390,6 +1406,7 @@ k_relin_mac3(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int
 // out[k] = in[src_g(k)], (2 brv(src) + 1) = (2 brv(k) + 1) g mod 2N.
 __global__ void k_automorphism(const uint64_t* __restrict__ in, int64_t rows, uint32_t g, uint64_t* __restrict__ out,
                                int logn) {
+    EDL_PDL_ENTRY();
     const int n = 1 << logn;
     const uint32_t two_n = 2u << logn;
     for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
@@ -1406,6 +1423,7 @@ __global__ void k_automorphism(const uint64_t* __restrict__ in, int64_t rows, ui
 __global__ void k_mul_pt(const uint64_t* __restrict__ a, int64_t cnt, int l, const uint64_t* __restrict__ pt,
                          int64_t pt_count, int pt_level, uint64_t* __restrict__ out,
                          const __grid_constant__ ModTable mods, int logn) {
+    EDL_PDL_ENTRY();
     const int64_t rows = cnt * 2 * (l + 1);
     const int n2 = 1 << (logn - 1);
     for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
@@ -1426,6 +1444,7 @@ __global__ void k_mul_pt(const uint64_t* __restrict__ a, int64_t cnt, int l, con
 __global__ void k_add_pt(const uint64_t* __restrict__ a, int64_t cnt, int l, const uint64_t* __restrict__ pt,
                          int64_t pt_count, int pt_level, uint64_t* __restrict__ out, const __grid_constant__ ModTable mods,
                          int logn) {
+    EDL_PDL_ENTRY();
     const int64_t rows = cnt * 2 * (l + 1);
     const int n2 = 1 << (logn - 1);
     for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
@@ -1463,6 +1482,7 @@ struct PackInfo {
 // secret-key ciphertext): wire polynomial p <-> array polynomial stride * p.
 __global__ void k_unpack(const uint64_t* __restrict__ in, int64_t polys, int nl, int64_t pw,
                          const __grid_constant__ PackInfo pi, uint64_t* __restrict__ out, int logn, int stride) {
+    EDL_PDL_ENTRY();
     const int64_t rows = polys * nl;
     const int n = 1 << logn;
     for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
@@ -1485,6 +1505,7 @@ __global__ void k_unpack(const uint64_t* __restrict__ in, int64_t polys, int nl,
 
 __global__ void k_pack(const uint64_t* __restrict__ in, int64_t polys, int nl, int64_t pw,
                        const __grid_constant__ PackInfo pi, uint64_t* __restrict__ out, int logn, int stride) {
+    EDL_PDL_ENTRY();
     const int64_t rows = polys * nl;
     const int n = 1 << logn;
     for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
@@ -1518,6 +1539,7 @@ __global__ void k_pack(const uint64_t* __restrict__ in, int64_t polys, int nl, i
 __global__ void k_pt_mac_multi(const uint64_t* __restrict__ rots, int T, int64_t n, int l,
                                const uint64_t* __restrict__ pts, int F, int ptl, uint64_t* __restrict__ out,
                                const __grid_constant__ ModTable mods, int logn) {
+    EDL_PDL_ENTRY();
     const int nl = l + 1;
     const int64_t row = blockIdx.y;                 // (c, p, i)
     const int i = (int)(row % nl);
@@ -1603,6 +1625,7 @@ void launch_unpack(const Dev& d, const uint64_t* in, int64_t polys, int nl, cons
 }
 
 __global__ void k_fetch_mapped(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst, int64_t words) {
+    EDL_PDL_ENTRY();
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < words; k += (int64_t)gridDim.x * blockDim.x)
         dst[k] = src[k];
 }
@@ -1659,11 +1682,11 @@ void launch_relin_mac(const Dev& d, const uint64_t* a, const uint64_t* b, int64_
 #define EDL_MAC3_ND(ND)                                                                                            \
     case ND:                                                                                                       \
         if (na)                                                                                                    \
-            EDL_LAUNCH(d, "k_relin_mac", (k_relin_mac3<-1, ND><<<dim3(gx3, na, gz3), MAC3_T, mac3_smem(ND, (const void*)k_relin_mac3<-1, ND>), d.st>>>( \
-                                             a, b, l, d.L, cnt, xh, kk, kkc, acc, all, *d.mt, d.cc, d.logn, pfold))); \
+            launch_k(d, "k_relin_mac", k_relin_mac3<-1, ND>, dim3(gx3, na, gz3), dim3(MAC3_T), mac3_smem(ND, (const void*)k_relin_mac3<-1, ND>), \
+                     a, b, l, d.L, cnt, xh, kk, kkc, acc, all, *d.mt, d.cc, d.logn, pfold); \
         if (nf)                                                                                                    \
-            EDL_LAUNCH(d, "k_relin_mac", (k_relin_mac3<1, ND><<<dim3(gx3, nf, gz3), MAC3_T, mac3_smem(ND, (const void*)k_relin_mac3<1, ND>), d.st>>>( \
-                                             a, b, l, d.L, cnt, xh, kk, kkc, acc, tf, *d.mt, d.cc, d.logn, pfold))); \
+            launch_k(d, "k_relin_mac", k_relin_mac3<1, ND>, dim3(gx3, nf, gz3), dim3(MAC3_T), mac3_smem(ND, (const void*)k_relin_mac3<1, ND>), \
+                     a, b, l, d.L, cnt, xh, kk, kkc, acc, tf, *d.mt, d.cc, d.logn, pfold); \
         break;
 #else
 #define EDL_MAC3(FPV, ND, LIST, NT)                                                                   \
@@ -1794,7 +1817,7 @@ void launch_cc_mac(const Dev& d, const uint64_t* x, int l, int H, int W, int F, 
         EDL_LAUNCH(d, "k_cc_mac", (k_cc_mac4<FCV, 4, 4><<<grid, CC4_T, sm4, d.st>>>(x, l, W, stride, Wo, nwin, f0, F, nwin, out, wt, *d.mt, d.logn))); \
     }
 #else
-#define EDL_CC4(FCV) EDL_LAUNCH(d, "k_cc_mac", (k_cc_mac4<FCV, 4, 4><<<grid, CC4_T, 0, d.st>>>(x, l, W, stride, Wo, nwin, f0, F, nwin, out, wt, *d.mt, d.logn)))
+#define EDL_CC4(FCV) launch_k(d, "k_cc_mac", k_cc_mac4<FCV, 4, 4>, grid, dim3(CC4_T), 0, x, l, W, stride, Wo, nwin, f0, F, nwin, out, wt, *d.mt, d.logn)
 #endif
             switch (fc) {
                 case 1: EDL_CC4(1); break;
@@ -1889,7 +1912,7 @@ void launch_dense_mac(const Dev& d, const uint64_t* x, int64_t K, int64_t O, int
 #define EDL_DN3(OCV)                                                                                \
     {                                                                                               \
         ensure_smem_attr((const void*)k_dense_mac3<OCV>, (int)smem); /* kper x 16 x 16 B can pass 48 KB */ \
-        EDL_LAUNCH(d, "k_dense_mac", (k_dense_mac3<OCV><<<grid, DN3_T, smem, d.st>>>(x, K, (int)O, l, kper, wd, dst, *d.mt, d.logn))); \
+        launch_k(d, "k_dense_mac", k_dense_mac3<OCV>, grid, dim3(DN3_T), smem, x, K, (int)O, l, kper, wd, dst, *d.mt, d.logn); \
     }
             switch (oc) {
                 case 4: EDL_DN3(4); break;
@@ -1900,8 +1923,8 @@ void launch_dense_mac(const Dev& d, const uint64_t* x, int64_t K, int64_t O, int
             }
 #undef EDL_DN3
             if (ks > 1)
-                EDL_LAUNCH(d, "k_dense_combine", k_dense_combine<<<rows_grid(d.logn, O * 2 * (l + 1)), PW_THREADS, 0, d.st>>>(
-                                                     part, ks, O, l, out, *d.mt, d.logn));
+                launch_k(d, "k_dense_combine", k_dense_combine, rows_grid(d.logn, O * 2 * (l + 1)), dim3(PW_THREADS), 0, part, ks, O,
+                         l, out, *d.mt, d.logn);
             return;
         }
     }

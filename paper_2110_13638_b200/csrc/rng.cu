@@ -5,6 +5,7 @@
 namespace edl {
 
 __global__ void k_philox_words(uint64_t seed, const uint32_t* __restrict__ ctr, int64_t n, uint32_t* __restrict__ out) {
+    EDL_PDL_ENTRY();
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n) return;
     uint4 r = draw(seed, ctr[4 * t], ctr[4 * t + 1], ctr[4 * t + 2], ctr[4 * t + 3]);
@@ -32,6 +33,7 @@ void launch_encrypt_sk(const Dev& d, const int64_t* msg, int64_t cnt, int l, uin
 // Seeded public component of secret-key ciphertexts: c1[c][i][k] = uniform(seed, k, obj0 + c, i, TAG_SK_A).
 __global__ void k_expand_sk_a(uint64_t* __restrict__ ct, int64_t cnt, int l, uint64_t seed, uint32_t obj0,
                               const __grid_constant__ ModTable mods, int logn) {
+    EDL_PDL_ENTRY();
     const int64_t rows = cnt * (l + 1);
     const int n = 1 << logn;
     for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
@@ -52,6 +54,7 @@ void launch_expand_sk_a(const Dev& d, uint64_t* ct, int64_t cnt, int l, uint64_t
 
 __global__ void k_fold_pinv(const uint64_t* __restrict__ rlk, uint64_t* __restrict__ pf, uint64_t* __restrict__ pfc,
                             int L, const __grid_constant__ ModTable mods, const ChainConsts* __restrict__ cc, int logn) {
+    EDL_PDL_ENTRY();
     const int64_t rows = (int64_t)(L + 1) * 2 * (L + 2);
     const int n = 1 << logn;
     for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {

@@ -83,6 +83,7 @@ __device__ __forceinline__ uint64_t key_companion(uint64_t v, const ModInfo& m) 
 template <class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
 k_keygen_s(uint64_t seed, uint64_t* __restrict__ s_hat, const __grid_constant__ ModTable mods) {
+    EDL_PDL_ENTRY();
     extern __shared__ uint64_t sm[];
     const int i = C::bx();
     const ModInfo& m = mods[i];
@@ -96,6 +97,7 @@ template <class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
 k_keygen_pk(uint64_t seed, int L, const uint64_t* __restrict__ s_hat, uint64_t* __restrict__ pk,
             const __grid_constant__ ModTable mods) {
+    EDL_PDL_ENTRY();
     extern __shared__ uint64_t sm[];
     const int i = C::bx();
     const ModInfo& m = mods[i];
@@ -115,6 +117,7 @@ template <class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
 k_keygen_rlk(uint64_t seed, int L, const uint64_t* __restrict__ s_hat, uint64_t* __restrict__ rlk,
              uint64_t* __restrict__ rlk_s, const __grid_constant__ ModTable mods, const ChainConsts* __restrict__ cc) {
+    EDL_PDL_ENTRY();
     extern __shared__ uint64_t sm[];
     const int i = C::bx();   // limb 0..L+1 (L+1 = P)
     const int j = blockIdx.y;   // digit 0..L
@@ -143,6 +146,7 @@ template <class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
 k_keygen_galois(uint64_t seed, int L, uint32_t g, const uint64_t* __restrict__ s_hat, uint64_t* __restrict__ gk,
                 uint64_t* __restrict__ gk_c, const __grid_constant__ ModTable mods, const ChainConsts* __restrict__ cc) {
+    EDL_PDL_ENTRY();
     extern __shared__ uint64_t sm[];
     const int i = C::bx();      // limb 0..L+1 (L+1 = P)
     const int j = blockIdx.y;   // digit 0..L
@@ -169,6 +173,7 @@ k_keygen_galois(uint64_t seed, int L, uint32_t g, const uint64_t* __restrict__ s
 template <class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
 k_encode_pt(const int64_t* __restrict__ msg, int l, uint64_t* __restrict__ out, const __grid_constant__ ModTable mods) {
+    EDL_PDL_ENTRY();
     extern __shared__ uint64_t sm[];
     const int i = blockIdx.y;
     const int64_t c = C::bx();
@@ -185,6 +190,7 @@ template <class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
 k_encrypt(const int64_t* __restrict__ msg, int l, int L, uint64_t seed, uint32_t obj0, const uint64_t* __restrict__ pk,
           uint64_t* __restrict__ out, const __grid_constant__ ModTable mods) {
+    EDL_PDL_ENTRY();
     extern __shared__ uint64_t sm[];
     const int i = blockIdx.y;
     const int64_t c = C::bx();
@@ -225,6 +231,7 @@ template <class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
 k_encrypt_sk(const int64_t* __restrict__ msg, int l, uint64_t seed, uint64_t eseed, uint32_t obj0,
              const uint64_t* __restrict__ s_hat, uint64_t* __restrict__ out, const __grid_constant__ ModTable mods) {
+    EDL_PDL_ENTRY();
     extern __shared__ uint64_t sm[];
     const int i = blockIdx.y;
     const int64_t c = C::bx();
@@ -250,6 +257,7 @@ template <class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
 k_decrypt(const uint64_t* __restrict__ ct, int l, const uint64_t* __restrict__ s_hat, uint64_t* __restrict__ out,
           const __grid_constant__ ModTable mods) {
+    EDL_PDL_ENTRY();
     extern __shared__ uint64_t sm[];
     const int i = blockIdx.y;
     const int64_t c = C::bx();
