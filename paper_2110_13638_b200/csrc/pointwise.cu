@@ -398,6 +398,13 @@ constexpr int CC4_MAXL = 6, CC4_MAXF = 8, CC4_TAPS = 16;
 #ifndef EDL_CC4_MINB
 #define EDL_CC4_MINB 6
 #endif
+// F64 limbs: Karatsuba split products (3 DFMA per MAC instead of 4; EDL_CC4_KARATSUBA=0: 4)
+#ifndef EDL_CC4_KARATSUBA
+#define EDL_CC4_KARATSUBA 1
+#endif
+#if EDL_CC4_KARATSUBA == 0
+#undef EDL_CC4_KARATSUBA
+#endif
 struct CCW4 {   // [limb][filter][tap] {wl, wh} as binary64 (F64 limbs), {w, companion} (others)
     uint64_t w[CC4_MAXL][CC4_MAXF][CC4_TAPS][2];
     double c44[CC4_MAXL][3];   // F64 limbs: 2^44 mod q, RD((2^44 mod q) / q), RD(2^22 / q) (host-made)
@@ -422,8 +429,16 @@ k_cc_mac4(const uint64_t* __restrict__ x, int l, int W, int stride, int Wo, int 
     // this limb's weights -> shared memory once per CTA (LDS.128 broadcasts in the MAC loop:
     // constant-bank loads with the runtime limb index stalled every DFMA on LDC, ncu round 2)
     __shared__ ulonglong2 ws[FC][TAPS];
-    for (int e = threadIdx.x; e < FC * TAPS; e += CC4_T)
+#ifdef EDL_CC4_KARATSUBA
+    __shared__ double wsum[FC][TAPS];   // F64 limbs: wl + wh (< 2^23, exact)
+#endif
+    for (int e = threadIdx.x; e < FC * TAPS; e += CC4_T) {
         ws[e / TAPS][e % TAPS] = make_ulonglong2(wt.w[i][e / TAPS][e % TAPS][0], wt.w[i][e / TAPS][e % TAPS][1]);
+#ifdef EDL_CC4_KARATSUBA
+        if (mode == 2)
+            wsum[e / TAPS][e % TAPS] = __dadd_rn(f64_of(wt.w[i][e / TAPS][e % TAPS][0]), f64_of(wt.w[i][e / TAPS][e % TAPS][1]));
+#endif
+    }
     __syncthreads();
     const double c44d = wt.c44[i][0], c44q = wt.c44[i][1], c22q = wt.c44[i][2];
     const int w_end = min(nwin, (int)(blockIdx.z + 1) * EDL_CC4_WPB);
@@ -476,16 +491,29 @@ k_cc_mac4(const uint64_t* __restrict__ x, int l, int W, int stride, int Wo, int 
             for (int t = 0; t < TAPS; t++) {
                 const double xl = __hiloint2double(0x43300000, (int)((uint32_t)xv[t] & 0x3FFFFFu)) - F64_TWO52;
                 const double xh = __hiloint2double(0x43300000, (int)(uint32_t)(xv[t] >> 22)) - F64_TWO52;
+#ifdef EDL_CC4_KARATSUBA
+                // 3 DFMA per MAC: S1 = sum (xl + xh)(wl + wh) - S0 - S2 after the taps; every
+                // product < 2^46 and every sum < 16 2^46 = 2^50, so all of it is exact
+                const double xs = __dadd_rn(xl, xh);
+#endif
 #pragma unroll
                 for (int f = 0; f < FC; f++) {
                     const ulonglong2 wv = ws[f][t];
                     const double wl = f64_of(wv.x), wh = f64_of(wv.y);
                     s0[f] = __fma_rn(xl, wl, s0[f]);
+#ifdef EDL_CC4_KARATSUBA
+                    s1[f] = __fma_rn(xs, wsum[f][t], s1[f]);
+#else
                     s1[f] = __fma_rn(xh, wl, s1[f]);
                     s1[f] = __fma_rn(xl, wh, s1[f]);
+#endif
                     s2[f] = __fma_rn(xh, wh, s2[f]);
                 }
             }
+#ifdef EDL_CC4_KARATSUBA
+#pragma unroll
+            for (int f = 0; f < FC; f++) s1[f] = __dsub_rn(__dsub_rn(s1[f], s0[f]), s2[f]);
+#endif
 #pragma unroll
             for (int f = 0; f < FC; f++) {
                 const double tt = __dadd_rn(f64_reduce(s0[f], qd, m.qinv_d),
