@@ -408,6 +408,9 @@ constexpr int CC4_MAXL = 6, CC4_MAXF = 8, CC4_TAPS = 16;
 struct CCW4 {   // [limb][filter][tap] {wl, wh} as binary64 (F64 limbs), {w, companion} (others)
     uint64_t w[CC4_MAXL][CC4_MAXF][CC4_TAPS][2];
     double c44[CC4_MAXL][3];   // F64 limbs: 2^44 mod q, RD((2^44 mod q) / q), RD(2^22 / q) (host-made)
+#ifdef EDL_CC4_CBANK
+    double ws[CC4_MAXL][CC4_MAXF][CC4_TAPS];   // F64 limbs: wl + wh (< 2^23, exact)
+#endif
 };
 
 template <int FC, int KH, int KW>
@@ -546,6 +549,111 @@ k_cc_mac4(const uint64_t* __restrict__ x, int l, int W, int stride, int Wo, int 
             if (f0 + f < F) out[limb_off((int64_t)(f0 + f) * n_out_per_f + win, p, i, nl, logn) + n] = res[f];
     }
 }
+
+#ifdef EDL_CC4_CBANK
+// k_cc_mac5: k_cc_mac4's arithmetic with the weights read as constant-bank operands of the
+// DFMA / IMAD.WIDE instructions themselves: the limb index is made a compile-time constant
+// by a switch over per-limb instantiations of the body (the first attempt indexed the
+// parameter table with the runtime limb and paid an LDC per operand), so the MAC loop has no
+// shared-memory weight loads (k_cc_mac4: one LDS.128 + one LDS.64 per 3 DFMA) and no staging
+// barrier.  Grid: z = poly * (l+1) + limb is the slowest index, so the CTAs running at one
+// time work on one limb (one body's code and one limb's 2 KB of weights in the caches).
+// Measured on B200 (C1): 0.68 ms against k_cc_mac4's 0.42 (ptxas feeds the constants through
+// LDCU + uniform registers, one load per DFMA and window, and spills ~200 B per thread at 80
+// registers; 96 registers: 0.77 ms), so it is compiled only with -DEDL_CC4_CBANK; bit-exact.
+template <int FC, int KH, int KW, int I, int MODE>
+__device__ __forceinline__ void cc5_body(const uint64_t* __restrict__ xb, size_t ct_words, int W, int stride, int Wo,
+                                         int w_beg, int w_end, int f0, int F, int n_out_per_f, uint64_t* __restrict__ out,
+                                         const CCW4& wt, const ModInfo& m, int p, int nl, int logn, int n) {
+    constexpr int TAPS = KH * KW;
+    const double qd = u52_to_double(m.q);
+    for (int win = w_beg; win < w_end; win++) {
+        uint64_t xv[TAPS];
+        {
+            const int wr = win / Wo, wc = win - (win / Wo) * Wo;
+            const uint64_t* xw = xb + (size_t)((wr * stride) * W + wc * stride) * ct_words;
+#pragma unroll
+            for (int t = 0; t < TAPS; t++) xv[t] = __ldg(xw + (size_t)((t / KW) * W + (t % KW)) * ct_words);
+        }
+        uint64_t res[FC];
+        if constexpr (MODE == 2) {
+            double s0[FC], s1[FC], s2[FC];
+#pragma unroll
+            for (int f = 0; f < FC; f++) s0[f] = s1[f] = s2[f] = 0.0;
+#pragma unroll
+            for (int t = 0; t < TAPS; t++) {
+                const double xl = __hiloint2double(0x43300000, (int)((uint32_t)xv[t] & 0x3FFFFFu)) - F64_TWO52;
+                const double xh = __hiloint2double(0x43300000, (int)(uint32_t)(xv[t] >> 22)) - F64_TWO52;
+                const double xs = __dadd_rn(xl, xh);
+#pragma unroll
+                for (int f = 0; f < FC; f++) {
+                    s0[f] = __fma_rn(xl, f64_of(wt.w[I][f][t][0]), s0[f]);
+                    s1[f] = __fma_rn(xs, wt.ws[I][f][t], s1[f]);
+                    s2[f] = __fma_rn(xh, f64_of(wt.w[I][f][t][1]), s2[f]);
+                }
+            }
+            const double c44d = wt.c44[I][0], c44q = wt.c44[I][1], c22q = wt.c44[I][2];
+#pragma unroll
+            for (int f = 0; f < FC; f++) {
+                const double s1f = __dsub_rn(__dsub_rn(s1[f], s0[f]), s2[f]);
+                const double tt = __dadd_rn(f64_reduce(s0[f], qd, m.qinv_d),
+                                            __dadd_rn(f64_mulc(s1f, 4194304.0, c22q, qd), f64_mulc(s2[f], c44d, c44q, qd)));
+                res[f] = f64_to_canon(f64_reduce(tt, qd, m.qinv_d), qd);
+            }
+        } else if constexpr (MODE == 1) {
+            uint64_t acc[FC];
+#pragma unroll
+            for (int f = 0; f < FC; f++) acc[f] = 0;
+#pragma unroll
+            for (int t = 0; t < TAPS; t++)
+#pragma unroll
+                for (int f = 0; f < FC; f++) acc[f] += tw_mul_fp(xv[t], wt.w[I][f][t][0], wt.w[I][f][t][1], m.q);
+#pragma unroll
+            for (int f = 0; f < FC; f++) res[f] = reduce64(acc[f], m);
+        } else {
+            U128 acc[FC];
+#pragma unroll
+            for (int f = 0; f < FC; f++) acc[f].lo = acc[f].hi = 0;
+#pragma unroll
+            for (int t = 0; t < TAPS; t++)
+#pragma unroll
+                for (int f = 0; f < FC; f++) mac128(acc[f], xv[t], wt.w[I][f][t][0]);
+#pragma unroll
+            for (int f = 0; f < FC; f++) res[f] = barrett128(acc[f], m);
+        }
+#pragma unroll
+        for (int f = 0; f < FC; f++)
+            if (f0 + f < F) out[limb_off((int64_t)(f0 + f) * n_out_per_f + win, p, I, nl, logn) + n] = res[f];
+    }
+}
+
+template <int FC, int KH, int KW>
+__global__ void __launch_bounds__(CC4_T, EDL_CC4_MINB)
+k_cc_mac5(const uint64_t* __restrict__ x, int l, int W, int stride, int Wo, int nwin, int f0, int F, int n_out_per_f,
+          uint64_t* __restrict__ out, const __grid_constant__ CCW4 wt, const __grid_constant__ ModTable mods, int logn) {
+    EDL_PDL_ENTRY();
+    const int nl = l + 1;
+    const int p = blockIdx.z / nl, i = blockIdx.z % nl;
+    const int n = blockIdx.x * CC4_T + threadIdx.x;
+    const ModInfo& m = mods[i];
+    const int mode = (int)m.fp;   // uniform per CTA (limb i)
+    const size_t ct_words = (size_t)2 * nl << logn;
+    const uint64_t* xb = x + limb_off(0, p, i, nl, logn) + n;
+    const int w_beg = blockIdx.y * EDL_CC4_WPB, w_end = min(nwin, (int)(blockIdx.y + 1) * EDL_CC4_WPB);
+#define CC5_ARGS xb, ct_words, W, stride, Wo, w_beg, w_end, f0, F, n_out_per_f, out, wt, m, p, nl, logn, n
+#define CC5_CASE(II)                                                      \
+    case II:                                                              \
+        if (mode == 2) cc5_body<FC, KH, KW, II, 2>(CC5_ARGS);             \
+        else if (mode == 1) cc5_body<FC, KH, KW, II, 1>(CC5_ARGS);        \
+        else cc5_body<FC, KH, KW, II, 0>(CC5_ARGS);                       \
+        break;
+    switch (i) {
+        CC5_CASE(0) CC5_CASE(1) CC5_CASE(2) CC5_CASE(3) CC5_CASE(4) CC5_CASE(5)
+    }
+#undef CC5_CASE
+#undef CC5_ARGS
+}
+#endif
 
 // ---------------------------------------------------------------- cross-correlation MAC, round 2
 // One coefficient per thread (8-byte loads, 256 B per warp) and all FC <= 8 filters of a
@@ -787,6 +895,7 @@ constexpr int DN3_U = 4;
 #undef EDL_DN3_ASYNC
 #endif
 #ifdef EDL_DN3_ASYNC
+constexpr int DN3_RING_WORDS = 2 * DN3_U * DN3_T;
 #define DN3_RING_PROLOGUE                                                                                      \
     uint64_t* ring = reinterpret_cast<uint64_t*>(wsm3 + kc * OC);                                             \
     auto afetch = [&](int k0_, int st) {                                                                       \
@@ -807,17 +916,34 @@ constexpr int DN3_U = 4;
             (kk + u < kc) ? ring[((size_t)(it & 1) * DN3_U + u) * DN3_T + threadIdx.x] : 0;                   \
     }
 #else
+constexpr int DN3_RING_WORDS = 0;
 #define DN3_RING_PROLOGUE
 #define DN3_FETCH(xv)                                                                                          \
     _Pragma("unroll") for (int u = 0; u < DN3_U; u++) xv[u] = (kk + u < kc) ? __ldg(xp + (size_t)(kk + u) * kstride) : 0;
 #endif
 
-template <int OC>
+// KARA (kper <= DN3_KARA_MAX): F64 limbs as Karatsuba split products like k_cc_mac4 -- x =
+// xh 2^22 + xl, w = wh 2^22 + wl, S0 = sum xl wl, S2 = sum xh wh, S = sum (xl + xh)(wl + wh)
+// (every product < 2^46, so sums of <= 128 terms stay below 2^53: exact), S1 = S - S0 - S2;
+// 3 DFMA per MAC instead of f64_mulc + add = 7.  Each sum is reduced (f64_reduce is exact for
+// any integer |v| < 2^53: the quotient estimate is off by < 2^-38) before the two constant
+// products S1 2^22 + S2 (2^44 mod q), whose operands are then below q.
+// Measured on B200 (C1 dense 245 -> 10): 0.148 ms against 0.140 for the f64_mulc form -- the
+// three sums per output take 94 registers (5 CTAs per SM instead of 7) and the dense MAC is
+// latency-, not FP64-bound -- so it is opt-in (-DEDL_DN3_KARATSUBA=1); bit-exact either way.
+constexpr int DN3_KARA_MAX = 128;
+#ifndef EDL_DN3_KARATSUBA
+#define EDL_DN3_KARATSUBA 0
+#endif
+template <int OC, bool KARA>
 __global__ void __launch_bounds__(DN3_T)
 k_dense_mac3(const uint64_t* __restrict__ x, int64_t K, int O, int l, int kper, const ulonglong2* __restrict__ wd,
              uint64_t* __restrict__ out, const __grid_constant__ ModTable mods, int logn) {
     EDL_PDL_ENTRY();
-    extern __shared__ ulonglong2 wsm3[];   // [kper][OC] {residue (binary64 on F64 limbs), companion}
+    // [kper][OC] {residue (binary64 on F64 limbs), companion}; KARA F64 limbs: {wl, wh} as
+    // binary64, then [kper][OC] wl + wh behind the input ring
+    extern __shared__ ulonglong2 wsm3[];
+    __shared__ double kc3[3];   // KARA: 2^44 mod q, RD((2^44 mod q) / q), RD(2^22 / q)
     const int nl = l + 1;
     const int p = blockIdx.y / nl, i = blockIdx.y % nl;
     const int sl = blockIdx.z;
@@ -825,11 +951,25 @@ k_dense_mac3(const uint64_t* __restrict__ x, int64_t K, int O, int l, int kper, 
     const int kc = (int)((K - k0) < kper ? (K - k0) : kper);
     const ModInfo& m = mods[i];
     const bool f64 = m.fp == 2, fp = m.fp != 0;
+    double* wsum = reinterpret_cast<double*>(wsm3 + kc * OC) + DN3_RING_WORDS;
     for (int t = threadIdx.x; t < kc * OC; t += DN3_T) {
         const int kk = t / OC, o = t % OC;
         ulonglong2 w = (o < O) ? wd[((size_t)o * K + (k0 + kk)) * nl + i] : make_ulonglong2(0, 0);
-        if (f64) w.x = f64_from_u(w.x);
+        if (KARA && f64) {
+            const uint64_t wl = w.x & 0x3FFFFFu, wh = w.x >> 22;
+            w.x = f64_from_u(wl);
+            w.y = f64_from_u(wh);
+            wsum[t] = u52_to_double(wl + wh);
+        } else if (f64) {
+            w.x = f64_from_u(w.x);
+        }
         wsm3[t] = w;
+    }
+    if (KARA && f64 && threadIdx.x == 0) {
+        const double qd0 = u52_to_double(m.q), c44 = u52_to_double((1ull << 44) % m.q);
+        kc3[0] = c44;
+        kc3[1] = __ddiv_rd(c44, qd0);
+        kc3[2] = __ddiv_rd(4194304.0, qd0);
     }
     __syncthreads();
     const int n = blockIdx.x * DN3_T + threadIdx.x;
@@ -838,7 +978,39 @@ k_dense_mac3(const uint64_t* __restrict__ x, int64_t K, int O, int l, int kper, 
     const uint64_t* xp = x + limb_off(k0, p, i, nl, logn) + n;
     uint64_t* outp = out + (size_t)sl * ((size_t)O * 2 * nl << logn);
     const double qd = u52_to_double(m.q);
-    if (f64) {
+    if (KARA && f64) {
+        double s0[OC], s1[OC], s2[OC];
+#pragma unroll
+        for (int o = 0; o < OC; o++) s0[o] = s1[o] = s2[o] = 0.0;
+        DN3_RING_PROLOGUE
+        for (int kk = 0; kk < kc; kk += DN3_U) {
+            uint64_t xv[DN3_U];
+            DN3_FETCH(xv)
+#pragma unroll
+            for (int u = 0; u < DN3_U; u++) {
+                if (kk + u >= kc) break;
+                const double xl = __hiloint2double(0x43300000, (int)((uint32_t)xv[u] & 0x3FFFFFu)) - F64_TWO52;
+                const double xh = __hiloint2double(0x43300000, (int)(uint32_t)(xv[u] >> 22)) - F64_TWO52;
+                const double xs = __dadd_rn(xl, xh);
+#pragma unroll
+                for (int o = 0; o < OC; o++) {
+                    const ulonglong2 w = wsm3[(kk + u) * OC + o];
+                    s0[o] = __fma_rn(xl, f64_of(w.x), s0[o]);
+                    s1[o] = __fma_rn(xs, wsum[(kk + u) * OC + o], s1[o]);
+                    s2[o] = __fma_rn(xh, f64_of(w.y), s2[o]);
+                }
+            }
+        }
+        const double c44d = kc3[0], c44q = kc3[1], c22q = kc3[2];
+#pragma unroll
+        for (int o = 0; o < OC; o++)
+            if (o < O) {
+                const double r0 = f64_reduce(s0[o], qd, m.qinv_d), r2 = f64_reduce(s2[o], qd, m.qinv_d);
+                const double r1 = f64_reduce(__dsub_rn(__dsub_rn(s1[o], s0[o]), s2[o]), qd, m.qinv_d);
+                const double tt = __dadd_rn(r0, __dadd_rn(f64_mulc(r1, 4194304.0, c22q, qd), f64_mulc(r2, c44d, c44q, qd)));
+                outp[limb_off(o, p, i, nl, logn) + n] = f64_to_canon(f64_reduce(tt, qd, m.qinv_d), qd);
+            }
+    } else if (f64) {
         double acc[OC];
 #pragma unroll
         for (int o = 0; o < OC; o++) acc[o] = 0.0;
@@ -1824,6 +1996,9 @@ void launch_cc_mac(const Dev& d, const uint64_t* x, int l, int H, int W, int F, 
                             const double lo = (double)(v.x & 0x3FFFFFull), hi = (double)(v.x >> 22);
                             memcpy(&wt.w[i][f][t][0], &lo, 8);
                             memcpy(&wt.w[i][f][t][1], &hi, 8);
+#ifdef EDL_CC4_CBANK
+                            wt.ws[i][f][t] = lo + hi;
+#endif
                         } else {
                             wt.w[i][f][t][0] = v.x;
                             wt.w[i][f][t][1] = v.y;
@@ -1844,6 +2019,9 @@ void launch_cc_mac(const Dev& d, const uint64_t* x, int l, int H, int W, int F, 
         ensure_smem_attr((const void*)k_cc_mac4<FCV, 4, 4>, sm4);                                            \
         EDL_LAUNCH(d, "k_cc_mac", (k_cc_mac4<FCV, 4, 4><<<grid, CC4_T, sm4, d.st>>>(x, l, W, stride, Wo, nwin, f0, F, nwin, out, wt, *d.mt, d.logn))); \
     }
+#elif defined(EDL_CC4_CBANK)
+            const dim3 grid5(grid.x, grid.z, grid.y);   // limb slowest
+#define EDL_CC4(FCV) launch_k(d, "k_cc_mac", k_cc_mac5<FCV, 4, 4>, grid5, dim3(CC4_T), 0, x, l, W, stride, Wo, nwin, f0, F, nwin, out, wt, *d.mt, d.logn)
 #else
 #define EDL_CC4(FCV) launch_k(d, "k_cc_mac", k_cc_mac4<FCV, 4, 4>, grid, dim3(CC4_T), 0, x, l, W, stride, Wo, nwin, f0, F, nwin, out, wt, *d.mt, d.logn)
 #endif
@@ -1937,10 +2115,15 @@ void launch_dense_mac(const Dev& d, const uint64_t* x, int64_t K, int64_t O, int
             smem += (size_t)2 * DN3_U * DN3_T * 8;   // cp.async input ring
 #endif
             uint64_t* dst = ks > 1 ? part : out;
+            const bool kara = EDL_DN3_KARATSUBA && kper <= DN3_KARA_MAX;
+            if (kara) smem += (size_t)kper * oc * sizeof(double);   // wl + wh
 #define EDL_DN3(OCV)                                                                                \
-    {                                                                                               \
-        ensure_smem_attr((const void*)k_dense_mac3<OCV>, (int)smem); /* kper x 16 x 16 B can pass 48 KB */ \
-        launch_k(d, "k_dense_mac", k_dense_mac3<OCV>, grid, dim3(DN3_T), smem, x, K, (int)O, l, kper, wd, dst, *d.mt, d.logn); \
+    if (kara) {                                                                                     \
+        ensure_smem_attr((const void*)k_dense_mac3<OCV, true>, (int)smem);                          \
+        launch_k(d, "k_dense_mac", k_dense_mac3<OCV, true>, grid, dim3(DN3_T), smem, x, K, (int)O, l, kper, wd, dst, *d.mt, d.logn); \
+    } else {                                                                                        \
+        ensure_smem_attr((const void*)k_dense_mac3<OCV, false>, (int)smem); /* kper x 16 x 16 B can pass 48 KB */ \
+        launch_k(d, "k_dense_mac", k_dense_mac3<OCV, false>, grid, dim3(DN3_T), smem, x, K, (int)O, l, kper, wd, dst, *d.mt, d.logn); \
     }
             switch (oc) {
                 case 4: EDL_DN3(4); break;
