@@ -120,9 +120,40 @@ __device__ __forceinline__ uint64_t shoup_lazy3(uint64_t y, uint64_t w, uint64_t
 #define EDL_SHOUP3 1
 #endif
 
+// Shoup with the quotient's cross products on the FP64 pipe (round 2c experiment,
+// EDL_SHOUP_FQ): with y = yh 2^32 + yl and ws = sh 2^32 + sl,
+//   y ws / 2^64 = yh sh + (yh sl + yl sh + yl sl 2^-32) 2^-32,
+// yh sh is one exact IMAD.WIDE and the bracket S < 2^65 is summed in binary64 with every
+// operation rounded down (s <= S, S - s < 2^13), so E = yh sh + floor(s 2^-32) satisfies
+// y ws / 2^64 - 1 - 2^-19 < E <= y ws / 2^64 <= y w / q and, with Shoup's own y / 2^64 < 1/2
+// (y < 2^63), y w - E q lies in [0, 1.51 q): the same [0, 2q) contract as shoup_lazy with
+// 3 IMAD.WIDE + 4 IMAD on the fmaheavy pipe instead of 6 + 4.  The 32-bit halves become
+// binary64 exactly by the 2^52 exponent trick (2^20 exponent: sl 2^-32).
+// Measured on B200: register-only butterfly ceiling 774 -> 702 Gbfly/s, C1 3.97 -> 4.45 ms
+// (DFMA and IMAD.WIDE do not overlap), so it stays an opt-in switch; bit-exact.
+__device__ __forceinline__ uint64_t shoup_lazy_fq(uint64_t y, uint64_t w, uint64_t ws, uint64_t q) {
+    const uint32_t yl = (uint32_t)y, yh = (uint32_t)(y >> 32);
+    const uint32_t sl = (uint32_t)ws, sh = (uint32_t)(ws >> 32);
+    const double m52 = 4503599627370496.0, m20 = 1048576.0;
+    const double dyh = __hiloint2double(0x43300000, (int)yh) - m52;
+    const double dyl = __hiloint2double(0x43300000, (int)yl) - m52;
+    const double dsh = __hiloint2double(0x43300000, (int)sh) - m52;
+    const double dsl = __hiloint2double(0x43300000, (int)sl) - m52;
+    const double dsl32 = __hiloint2double(0x41300000, (int)sl) - m20;   // sl 2^-32
+    double s = __dmul_rd(dyl, dsh);
+    s = __fma_rd(dyh, dsl, s);
+    s = __fma_rd(dyl, dsl32, s);
+    const double t = __fma_rd(s, 2.3283064365386963e-10, m52);   // 2^52 + floor(s 2^-32)
+    const uint64_t ti = (uint64_t)__double_as_longlong(t) & 0xFFFFFFFFFFFFFull;
+    const uint64_t qt = (uint64_t)yh * sh + ti;
+    return y * w - qt * q;
+}
+
 // [0, 2q) result for the butterflies.
 __device__ __forceinline__ uint64_t shoup_lazy2(uint64_t y, uint64_t w, uint64_t ws, uint64_t q) {
-#ifndef EDL_APPROX_SHOUP
+#ifdef EDL_SHOUP_FQ
+    return shoup_lazy_fq(y, w, ws, q);
+#elif !defined(EDL_APPROX_SHOUP)
     return shoup_lazy(y, w, ws, q);
 #else
     return csub(shoup_lazy4(y, w, ws, q), 2 * q);
