@@ -1,5 +1,5 @@
 O=gpurun_out/${RUNDIR:-r62}; mkdir -p $O
-for v in base fq; do
+for v in ${VARS:-base fq}; do
   L=variants/lib_$v.so
   EDL_LIB=$L timeout 900 python -m pytest tests -q -m gpu -x -k "ntt or relin or c1_full or rescale or keygen" > $O/pytest_$v.log 2>&1; echo "$v pytest rc=$?" >> $O/summary.log
   EDL_LIB=$L timeout 300 python tools/path_rates.py > $O/path_$v.log 2>&1; echo "$v path rc=$?" >> $O/summary.log
