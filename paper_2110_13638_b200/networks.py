@@ -85,3 +85,18 @@ class C3Net:
         return _run_chain([("dense1", lambda s: c.dense(s, self.W1, self.b1), 1),
                            ("act", lambda s: c.poly_activation(s, SIGMA_A), 2),
                            ("dense2", lambda s: c.dense(s, self.W2, self.b2), 1)], x, keep)
+
+    def forward_many(self, xs):
+        """Several slot-batches in one pass: dense1 per batch into one array, sigma_a ONCE over
+        all batches' hidden ciphertexts (the activation is per ciphertext, so the key switches
+        run as one full-size launch sequence instead of one small one per batch), dense2 per
+        batch.  Every output residue equals forward()'s (tests/test_gpu_full_configs.py)."""
+        from .parallel import ct_slice
+        c, n = self.ctx, self.ctx.n
+        O1 = self.W1.shape[0]
+        h = c.empty(O1 * len(xs), max(xs[0].level - 1, 0))
+        for b, x in enumerate(xs):
+            r = c.dense(x, self.W1, self.b1, out=ct_slice(h, O1 * b, O1 * (b + 1), n))
+            h.level, h.scale, h.key_id = r.level, r.scale, r.key_id
+        a = c.poly_activation(h, SIGMA_A)
+        return [c.dense(ct_slice(a, O1 * b, O1 * (b + 1), n), self.W2, self.b2) for b in range(len(xs))]

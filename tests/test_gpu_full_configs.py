@@ -59,7 +59,7 @@ def test_c3_full_bit_exact(gpu):
     octx = onet.c3_context(1)
     ctx = gpu.Context(gpu.params_from_depth(4)).keygen(1)
     net = C3Net(ctx, inp.W1, inp.b1, inp.W2, inp.b2)
-    preds = []
+    preds, xgs, outs_o = [], [], []
     for bidx in range(2):                                    # reading Z12: 2 slot-batches
         Xb = inp.X[bidx * 8192:(bidx + 1) * 8192]
         polys = np.stack([octx.encode(z) for z in Xb.T])
@@ -70,6 +70,11 @@ def test_c3_full_bit_exact(gpu):
         for k in ("dense1", "act", "out"):
             assert np.array_equal(rg[k].numpy(ctx.n), ro[k].data), k
         preds.append(ctx.decrypt(rg["out"], 8192)[0])
+        xgs.append(xg)
+        outs_o.append(ro["out"].data)
+    # both slot-batches in one pass (sigma_a once over all hidden ciphertexts): same residues
+    for og, oo in zip(net.forward_many(xgs), outs_o):
+        assert np.array_equal(og.numpy(ctx.n), oo), "forward_many"
     pred = np.concatenate(preds)
     ref = onet.c3_float64(inp.X, inp.W1, inp.b1, inp.W2, inp.b2)[:, 0]
     assert np.max(np.abs(pred - ref)) < 1e-3

@@ -31,11 +31,20 @@ def run_c3(reps: int = 5) -> dict:
     st = ctx.stream
     for x in xs:
         net.forward(x)
+    net.forward_many(xs)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
     for _ in range(reps):
         outs = [net.forward(x)["out"] for x in xs]
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms_per_batch_calls = e0.elapsed_time(e1) / reps
+    # both slot-batches in one pass (dense per batch, sigma_a once over the 128 hidden
+    # ciphertexts): the same residues, full-size key-switch launches
+    e0.record(st)
+    for _ in range(reps):
+        outs = net.forward_many(xs)
     e1.record(st)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
@@ -48,6 +57,7 @@ def run_c3(reps: int = 5) -> dict:
     return {"config": "C3 tabular: 16384 samples x 32 features, dense 32->64, sigma_a, dense 64->1, "
                       "N=2^14 {60,40,40,40,40|60}, 2 slot-batches of 8192, inputs resident, device-timed",
             "ms_per_pass": ms, "samples_per_s": 16384 / (ms / 1e3), "unit": "samples/s",
+            "ms_per_pass_one_call_per_batch": ms_per_batch_calls,
             "mse_vs_float64": float(np.mean(err ** 2)), "max_abs_err": float(np.max(np.abs(err)))}
 
 
