@@ -47,6 +47,9 @@ def _args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-c2", action="store_true", help="skip the C2 microbench sweep")
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 tabular net")
+    ap.add_argument("--inflight", type=int, default=2,
+                    help="N=1: batches in flight (consecutive steps alternate over this many contexts, each "
+                         "with its own stream pair and scratch); 1 = one batch at a time")
     return ap.parse_args()
 
 
@@ -364,6 +367,27 @@ def run_ours(a):
 
         def step(inp):
             return net.forward(inp)["out"]
+
+        # Batches in flight (serving pipeline): consecutive steps alternate over `inflight`
+        # contexts -- same keys (same seed), own stream pair and scratch, own resident batch of
+        # images -- so the head of batch k+1 (CC, rescale) fills the SMs that the tail of batch k
+        # (last key-switch waves, dense MAC, 10-ciphertext rescale) leaves idle.  Every step is
+        # still one full 8192-image batch through the whole path.
+        pipe = [(ctx, net, x, stream)]
+        for i in range(1, max(1, a.inflight)):
+            st_i = torch.cuda.Stream(device=local)
+            with torch.cuda.stream(st_i):
+                ctx_i = edl.Context(edl.params_from_depth(4), device=local, stream=st_i).keygen(1)
+                polys_i = torch.from_numpy(ctx_i.encode(c1_slots(c1_images(BATCH, 2110 + i)))).to(f"cuda:{local}")
+                x_i = ctx_i.encrypt_poly(polys_i, scale=float(2 ** 40), enc_seed=2, obj0=784 * i)
+                del polys_i
+            st_i.synchronize()
+            pipe.append((ctx_i, C1Net(ctx_i, K, kb, W, b), x_i, st_i))
+
+        def step_pipe(k):
+            c_k, net_k, x_k, st_k = pipe[k % len(pipe)]
+            with torch.cuda.stream(st_k):   # torch allocations of this step on the step's stream
+                return net_k.forward(x_k)["out"]
     else:
         # C4 (configs[4]) at weak scale: `world` batches of 8192 images, their 49*world
         # (window, batch) units split over the ranks (49 each), dense partials combined by
@@ -402,25 +426,49 @@ def run_ours(a):
         if world > 1:
             dist.barrier()
 
+    piped = world == 1 and len(pipe) > 1
     for _ in range(max(a.warmup, 0)):
         step(x)
-    stream.synchronize()
+        if piped:
+            for j in range(1, len(pipe)):
+                step_pipe(j)
+    torch.cuda.synchronize(local)
     barrier()
 
     clocks = ClockSampler(local)
     clocks.start()
-    l0 = ctx.launches
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    stream.synchronize()
+    ms_one = None
+    if piped:
+        # one batch at a time first (the latency of a batch, reported beside the pipelined rate)
+        e0.record(stream)
+        for _ in range(a.steps):
+            out = step(x)
+        e1.record(stream)
+        stream.synchronize()
+        ms_one = e0.elapsed_time(e1) / a.steps
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = sum(p_[0].launches for p_ in pipe) if world == 1 else ctx.launches
+    torch.cuda.synchronize(local)
     barrier()
     e0.record(stream)
-    for _ in range(a.steps):
-        out = step(x)
+    if piped:
+        for p_ in pipe[1:]:
+            p_[3].wait_event(e0)
+        for k in range(a.steps):
+            out = step_pipe(k)
+        for p_ in pipe[1:]:
+            j_ = torch.cuda.Event()
+            j_.record(p_[3])
+            stream.wait_event(j_)
+    else:
+        for _ in range(a.steps):
+            out = step(x)
     e1.record(stream)
-    stream.synchronize()
+    torch.cuda.synchronize(local)
     barrier()
     ms = e0.elapsed_time(e1)
-    launches = ctx.launches - l0
+    launches = (sum(p_[0].launches for p_ in pipe) if world == 1 else ctx.launches) - l0
     clk = clocks.stop()
     # per-kernel durations (roofline, kernel split): the same K steps again with a CUDA event
     # pair around every launch on the library's stream; the events' own gaps would inflate the
@@ -712,6 +760,10 @@ def run_ours(a):
                 "kernel_timing": {"method": "CUDA event pair around every launch, on the library stream, over a "
                                             "second pass of the same K steps", "ms_per_step_instrumented":
                                   ms_instr / a.steps},
+                "pipeline": ({"batches_in_flight": len(pipe), "ms_per_batch_one_at_a_time": ms_one,
+                              "note": "consecutive steps alternate over contexts with their own stream pair, "
+                                      "scratch and resident input batch; every step is one full batch; "
+                                      "--inflight 1 times one batch at a time"} if world == 1 else None),
                 "replica_dp": replica, "c2": c2, "c3": c3,
                 "ntt_limb_transforms_per_s": {"value": ntt_rate, "config": "N=2^14, C1 chain limbs q0..q4, 256 "
                                               "ciphertexts x 2 polys, forward NTT, device-timed (outside the "

@@ -225,3 +225,37 @@ def test_f1_packed_hoisted_bit_exact_vs_oracle(gpu):
     assert np.array_equal(got.numpy(ctx.n), want.data)
     ref = onet.c1_float64(imgs, K, kb, Wt, b)
     assert np.max(np.abs(masquerade.packed_logits(ctx, got, 3, H * Wd) - ref)) < 1e-3
+
+
+def test_two_contexts_in_flight_bit_exact(gpu):
+    """bench.py's batches-in-flight pipeline: two contexts (same key seed, own stream pair and
+    scratch) fed alternately without synchronisation give the residues of one context run
+    alone (C3 net, 32 -> 64 -> 1, as the workload: every layer kind of the path but the CC)."""
+    import torch
+    from paper_2110_13638_b200.networks import C3Net
+    from synth import c3_inputs
+
+    inp = c3_inputs()
+    pipe = []
+    for i in range(2):
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            ctx = gpu.Context(gpu.params_from_depth(4), stream=st).keygen(1)
+            x = ctx.encrypt(inp.X[i * 8192:(i + 1) * 8192].T, enc_seed=2, obj0=32 * i)
+        st.synchronize()
+        pipe.append((ctx, C3Net(ctx, inp.W1, inp.b1, inp.W2, inp.b2), x, st))
+    alone = []
+    for ctx, net, x, st in pipe:
+        with torch.cuda.stream(st):
+            alone.append(net.forward(x)["out"].numpy(ctx.n))
+    outs = []
+    for k in range(6):                       # 3 rounds, alternating, nothing waits in between
+        ctx, net, x, st = pipe[k % 2]
+        with torch.cuda.stream(st):
+            outs.append(net.forward(x)["out"])
+    torch.cuda.synchronize()
+    for k, o in enumerate(outs):
+        assert np.array_equal(o.numpy(pipe[k % 2][0].n), alone[k % 2]), k
+    assert pipe[0][0].key_id == pipe[1][0].key_id
+    for ctx, *_ in pipe:
+        ctx.close()
