@@ -69,6 +69,9 @@ struct edl_ctx {
     int64_t ks_chunk = 0;
     // d2 INTT + modulus raise in one kernel (EDL_RAISE_FUSED=1, N = 2^14)
     bool raise_fused = false;
+    // EDL_KS_SPLIT=0: key switches as one launch sequence on the main stream instead of two
+    // halves on the two streams (experiments with several contexts in flight)
+    bool ks_split = true;
 
     Dev dev() const {
         Dev d;
@@ -238,7 +241,7 @@ void relin_split(edl_ctx* c, const Dev& d, const uint64_t* a, const uint64_t* b,
                  const uint64_t* rlk, const uint64_t* rlk_s, uint64_t* scr, uint64_t* out,
                  const uint64_t* add_w = nullptr, const uint64_t* add_k = nullptr) {
     const int64_t c0 = cnt / 2;
-    if (c->prof.on || c0 < 8) {
+    if (c->prof.on || c0 < 8 || !c->ks_split) {
         launch_relin(d, a, b, cnt, l, rescale, rlk, rlk_s, scr, out, add_w, add_k);
         return;
     }
@@ -392,6 +395,8 @@ edl_status edl_ctx_create(const edl_params* p, int32_t device, void* stream, edl
         c->raise_fused = rf && rf[0] == '1';
         const char* k = std::getenv("EDL_KS_CHUNK");
         c->ks_chunk = k ? std::atoll(k) : 0;
+        const char* sp = std::getenv("EDL_KS_SPLIT");
+        c->ks_split = !(sp && sp[0] == '0');
     }
     const int nm = c->L + 2;
     // twiddle tables: per modulus [fwd N][inv N] of {w, w'}
