@@ -502,62 +502,33 @@ def run_ours(a):
         out_words = out.tensor.numel()
         host_out = [torch.empty(out_words, dtype=torch.int64, pin_memory=True) for _ in range(2)]
         dev_in = [edl.CtArray(torch.empty_like(x.tensor), x.count, x.level, x.scale, x.key_id) for _ in range(2)]
-        copy_stream = torch.cuda.Stream(device=local)
-        copied = [torch.cuda.Event() for _ in range(2)]
-        used = [torch.cuda.Event() for _ in range(2)]
-        trace = [] if os.environ.get("EDL_E2E_TRACE") else None
 
-        def measure_e2e(host_in, unpack_into):
-            wire = [torch.empty(host_in.numel(), dtype=torch.int64, device=f"cuda:{local}") for _ in range(2)]
-
+        def measure_e2e(host_in, unpack_host):
+            """Every step through the C-ABI's host-buffer calls: edl_wire_upload (pinned host bytes ->
+            the context's staging slot, on the context's copy stream), edl_cts_unpack*_host (the
+            compute stream waits for the slot, unpacks), the step, edl_cts_download (outputs ->
+            pinned host memory).  The upload of step k+1 is queued while step k computes."""
             def run_pipeline(nsteps, first_event=None):
                 for k in range(nsteps):
                     buf = k % 2
-                    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if trace is not None else None
-                    with torch.cuda.stream(copy_stream):
-                        if k >= 2:
-                            copy_stream.wait_event(used[buf])      # step k-2 is done with this buffer
-                        if k == 0 and first_event is not None:
-                            first_event.record(copy_stream)
-                        if ev:
-                            ev[0].record(copy_stream)
-                        wire[buf].copy_(host_in, non_blocking=True)
-                        copied[buf].record(copy_stream)
-                        if ev:
-                            ev[1].record(copy_stream)
-                    stream.wait_event(copied[buf])
-                    if ev:
-                        ev[2].record(stream)
-                    unpack_into(wire[buf], dev_in[buf])
+                    if k == 0 and first_event is not None:
+                        first_event.record(stream)
+                    ctx.wire_upload(buf, host_in)
+                    unpack_host(buf, dev_in[buf])
                     res = step(dev_in[buf])
-                    host_out[buf].copy_(res.tensor, non_blocking=True)
-                    used[buf].record(stream)
-                    if ev:
-                        ev[3].record(stream)
-                        trace.append(ev)
+                    ctx.download(res, host_out[buf])
 
             run_pipeline(2)
-            stream.synchronize()
-            copy_stream.synchronize()
+            ctx.sync()
             barrier()
             f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            if trace is not None:
-                trace.clear()
             run_pipeline(a.e2e_steps, first_event=f0)
             f1.record(stream)
-            stream.synchronize()
-            copy_stream.synchronize()
+            ctx.sync()
             barrier()
-            if trace:
-                t0 = trace[0][0]
-                for k, ev in enumerate(trace):
-                    print("e2e trace step %d: h2d %.2f-%.2f  compute %.2f-%.2f ms" % (
-                        k, t0.elapsed_time(ev[0]), t0.elapsed_time(ev[1]), t0.elapsed_time(ev[2]),
-                        t0.elapsed_time(ev[3])), file=sys.stderr)
             te = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=f"cuda:{local}")
             if world > 1:
                 dist.all_reduce(te, op=dist.ReduceOp.MAX)
-            del wire
             return world * BATCH * a.e2e_steps / (float(te.item()) / 1e3)
 
         def pinned(t):
@@ -567,19 +538,20 @@ def run_ours(a):
 
         # public-key ciphertexts in the packed wire format (edl.h: residues in bit-length-of-q bits)
         host_pk = pinned(ctx.pack(x))
-        v_pk = measure_e2e(host_pk, lambda w, o: ctx.unpack(w, x.count, x.level, x.scale, x.key_id, out=o))
+        v_pk = measure_e2e(host_pk, lambda sl, o: ctx.unpack_host(sl, x.count, x.level, x.scale, x.key_id, out=o))
         e2e_pk = {"value": v_pk, "unit": UNIT, "h2d_bytes_per_step": int(host_pk.numel() * 8),
                   "d2h_bytes_per_step": int(out_words * 8),
                   "inputs": "public-key ciphertexts, packed wire format (edl_cts_pack/unpack)"}
         del host_pk
-        pipeline = ("H2D of step k+1 on a copy stream overlaps step k (2 device input buffers); unpack and "
-                    "the step's kernels inside the timed region; 10 output ciphertexts read back every step")
+        pipeline = ("C-ABI host-buffer calls: edl_wire_upload of step k+1 (pinned host memory -> the context's "
+                    "staging slot on its copy stream) overlaps step k; edl_cts_unpack*_host, the step's kernels and "
+                    "edl_cts_download of the 10 output ciphertexts to pinned host memory inside the timed region")
         if x_sk is not None:
             # secret-key ciphertexts of the same images (reading Z16): c0 packed, c1 regenerated on the
             # device from (enc_seed, object id) by edl_cts_unpack_seeded inside each step
             host_sk = pinned(ctx.pack_c0(x_sk))
-            v_sk = measure_e2e(host_sk, lambda w, o: ctx.unpack_seeded(w, x_sk.count, x_sk.level, x_sk.scale,
-                                                                        x_sk.key_id, enc_seed=3, obj0=0, out=o))
+            v_sk = measure_e2e(host_sk, lambda sl, o: ctx.unpack_seeded_host(sl, x_sk.count, x_sk.level, x_sk.scale,
+                                                                              x_sk.key_id, enc_seed=3, obj0=0, out=o))
             e2e = {"value": v_sk, "unit": UNIT, "h2d_bytes_per_step": int(host_sk.numel() * 8),
                    "d2h_bytes_per_step": int(out_words * 8),
                    "inputs": "secret-key ciphertexts of the same 8192 images (DESIGN reading Z16): c0 in the "

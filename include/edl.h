@@ -310,6 +310,33 @@ edl_status edl_cts_pack_c0(edl_ctx* ctx, const edl_cts* in, void* packed);
 edl_status edl_cts_unpack_seeded(edl_ctx* ctx, const void* packed, int64_t count, int32_t level, double scale,
                                  uint64_t key_id, uint64_t enc_seed, uint32_t obj0, edl_cts* out);
 
+/* Host wire path (the EDLaaS server's receive / reply side, PAPER.md:85 client-server split;
+ * DESIGN.md §7b): ciphertexts arrive in HOST memory in a wire format and results return to
+ * HOST memory; the context owns two device staging slots and a copy stream, so the transfer
+ * of batch k+1 overlaps the compute of batch k.
+ * edl_wire_upload: enqueue the copy of `bytes` (a multiple of 8) of host memory `host`
+ *   (pinned memory for an asynchronous copy; it must stay valid until the slot's unpack has
+ *   run) into staging slot `slot` (0 or 1) on the copy stream, after the last unpack that
+ *   read the slot; returns at once.  The slot's device buffer is (re)allocated when `bytes`
+ *   exceeds its capacity (this synchronises).
+ * edl_cts_unpack_host / edl_cts_unpack_seeded_host: edl_cts_unpack / edl_cts_unpack_seeded
+ *   reading staging slot `slot`: the context's stream waits for the slot's copy, unpacks into
+ *   the device array `out`, and frees the slot for the next upload.  Asynchronous.
+ * edl_cts_download: enqueue the device -> host copy of a ciphertext array (64-bit layout,
+ *   edl_cts_bytes) into `host_out` on the context's stream; the bytes are valid after
+ *   edl_ctx_sync.
+ * Errors: EDL_ERR_ARG on a bad slot, null buffers, a size that is not a multiple of 8, or a
+ *   slot holding fewer bytes than the array needs; EDL_ERR_CUDA when the copy cannot be queued. */
+edl_status edl_wire_upload(edl_ctx* ctx, int32_t slot, const void* host, size_t bytes);
+edl_status edl_cts_unpack_host(edl_ctx* ctx, int32_t slot, int64_t count, int32_t level, double scale, uint64_t key_id,
+                               edl_cts* out);
+edl_status edl_cts_unpack_seeded_host(edl_ctx* ctx, int32_t slot, int64_t count, int32_t level, double scale,
+                                      uint64_t key_id, uint64_t enc_seed, uint32_t obj0, edl_cts* out);
+edl_status edl_cts_download(edl_ctx* ctx, const edl_cts* x, void* host_out);
+/* Block the calling host thread until everything queued on the context's streams (compute,
+ * side and copy stream) has completed; reports a pending CUDA error as EDL_ERR_CUDA. */
+edl_status edl_ctx_sync(edl_ctx* ctx);
+
 /* Integer-pipe ceiling: lazy Shoup 64-bit modular multiplications per second measured
  * by a register-only kernel on all SMs (the "alu" roofline peak). */
 edl_status edl_modmul_peak(edl_ctx* ctx, int32_t iters, double* modmul_per_s);

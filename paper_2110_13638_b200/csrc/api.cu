@@ -29,6 +29,14 @@ struct edl_ctx {
     cudaStream_t st = nullptr;
     cudaStream_t st2 = nullptr;              // side stream for independent branches of a schedule
     cudaEvent_t fork = nullptr, join = nullptr;
+    // host wire path (edl_wire_upload / edl_cts_unpack*_host): two device staging buffers
+    // filled on the context's own copy stream
+    cudaStream_t cst = nullptr;
+    void* wire[2] = {nullptr, nullptr};
+    size_t wire_cap[2] = {0, 0};
+    size_t wire_len[2] = {0, 0};
+    cudaEvent_t wire_copied[2] = {nullptr, nullptr}, wire_used[2] = {nullptr, nullptr};
+    bool wire_busy[2] = {false, false};   // an unpack has been queued on the slot since its last upload
     std::vector<ModInfo> h_mods;
     ModInfo* d_mods = nullptr;
     ModTable h_mt;
@@ -521,6 +529,12 @@ void edl_ctx_destroy(edl_ctx* c) {
     }
     cudaFree(c->d_scratch);
     cudaFree(c->d_const);
+    for (int k = 0; k < 2; k++) {
+        cudaFree(c->wire[k]);
+        if (c->wire_copied[k]) cudaEventDestroy(c->wire_copied[k]);
+        if (c->wire_used[k]) cudaEventDestroy(c->wire_used[k]);
+    }
+    if (c->cst) cudaStreamDestroy(c->cst);
     if (c->st2) cudaStreamDestroy(c->st2);
     if (c->fork) cudaEventDestroy(c->fork);
     if (c->join) cudaEventDestroy(c->join);
@@ -1008,6 +1022,93 @@ edl_status edl_cts_unpack_seeded(edl_ctx* c, const void* packed, int64_t count, 
     }
     set_meta(out, count, level, scale, key_id);
     return cuda_check(c, "cts_unpack_seeded");
+}
+
+// ---- host wire path: ciphertexts arrive in host memory, results return to host memory ----
+edl_status edl_wire_upload(edl_ctx* c, int32_t slot, const void* host, size_t bytes) {
+    if (!c || slot < 0 || slot > 1) return EDL_ERR_ARG;
+    if (bytes > 0 && !host) return fail(c, EDL_ERR_ARG, "wire_upload: null host buffer");
+    if (bytes % 8) return fail(c, EDL_ERR_ARG, "wire_upload: size must be a multiple of 8 bytes");
+    cudaSetDevice(c->device);
+    if (!c->cst && cudaStreamCreateWithFlags(&c->cst, cudaStreamNonBlocking) != cudaSuccess)
+        return fail(c, EDL_ERR_CUDA, "wire_upload: copy stream");
+    if (!c->wire_copied[slot]) {
+        if (cudaEventCreateWithFlags(&c->wire_copied[slot], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->wire_used[slot], cudaEventDisableTiming) != cudaSuccess)
+            return fail(c, EDL_ERR_CUDA, "wire_upload: events");
+    }
+    if (bytes > c->wire_cap[slot]) {   // first use (or a larger batch): the old buffer may still be read
+        cudaStreamSynchronize(c->st);
+        cudaStreamSynchronize(c->cst);
+        cudaFree(c->wire[slot]);
+        c->wire[slot] = nullptr;
+        c->wire_cap[slot] = 0;
+        if (cudaMalloc(&c->wire[slot], bytes) != cudaSuccess) return fail(c, EDL_ERR_CUDA, "wire_upload: device staging buffer");
+        c->wire_cap[slot] = bytes;
+        c->wire_busy[slot] = false;
+    }
+    if (c->wire_busy[slot]) cudaStreamWaitEvent(c->cst, c->wire_used[slot], 0);   // the last unpack of this slot
+    if (bytes > 0 && cudaMemcpyAsync(c->wire[slot], host, bytes, cudaMemcpyHostToDevice, c->cst) != cudaSuccess)
+        return fail(c, EDL_ERR_CUDA, "wire_upload: cudaMemcpyAsync");
+    cudaEventRecord(c->wire_copied[slot], c->cst);
+    c->wire_len[slot] = bytes;
+    c->wire_busy[slot] = false;
+    return EDL_OK;
+}
+
+static edl_status wire_ready(edl_ctx* c, int32_t slot, size_t need, const char* what) {
+    if (slot < 0 || slot > 1) return EDL_ERR_ARG;
+    if (!c->wire_copied[slot] || c->wire_len[slot] < need) return fail(c, EDL_ERR_ARG, what);
+    cudaStreamWaitEvent(c->st, c->wire_copied[slot], 0);
+    return EDL_OK;
+}
+static void wire_release(edl_ctx* c, int32_t slot) {
+    cudaEventRecord(c->wire_used[slot], c->st);
+    c->wire_busy[slot] = true;
+}
+
+edl_status edl_cts_unpack_host(edl_ctx* c, int32_t slot, int64_t count, int32_t level, double scale, uint64_t key_id,
+                               edl_cts* out) {
+    if (!c || !out || count < 0) return EDL_ERR_ARG;
+    if (level < 0 || level > c->L) return fail(c, EDL_ERR_ARG, "cts_unpack_host: level out of range");
+    edl_status s = wire_ready(c, slot, edl_cts_packed_bytes(c, count, level), "cts_unpack_host: slot holds fewer bytes than the array");
+    if (s != EDL_OK) return s;
+    s = edl_cts_unpack(c, c->wire[slot], count, level, scale, key_id, out);
+    wire_release(c, slot);
+    return s;
+}
+
+edl_status edl_cts_unpack_seeded_host(edl_ctx* c, int32_t slot, int64_t count, int32_t level, double scale,
+                                      uint64_t key_id, uint64_t enc_seed, uint32_t obj0, edl_cts* out) {
+    if (!c || !out || count < 0) return EDL_ERR_ARG;
+    if (level < 0 || level > c->L) return fail(c, EDL_ERR_ARG, "cts_unpack_seeded_host: level out of range");
+    edl_status s = wire_ready(c, slot, edl_cts_seeded_bytes(c, count, level),
+                              "cts_unpack_seeded_host: slot holds fewer bytes than the array");
+    if (s != EDL_OK) return s;
+    s = edl_cts_unpack_seeded(c, c->wire[slot], count, level, scale, key_id, enc_seed, obj0, out);
+    wire_release(c, slot);
+    return s;
+}
+
+edl_status edl_cts_download(edl_ctx* c, const edl_cts* x, void* host_out) {
+    if (!c) return EDL_ERR_ARG;
+    edl_status s = check_ct(c, x);
+    if (s != EDL_OK) return s;
+    if (x->count > 0 && !host_out) return fail(c, EDL_ERR_ARG, "cts_download: null host buffer");
+    if (x->count > 0 && cudaMemcpyAsync(host_out, x->data, edl_cts_bytes(x->count, x->level, c->logn), cudaMemcpyDeviceToHost,
+                                        c->st) != cudaSuccess)
+        return fail(c, EDL_ERR_CUDA, "cts_download: cudaMemcpyAsync");
+    return EDL_OK;
+}
+
+edl_status edl_ctx_sync(edl_ctx* c) {
+    if (!c) return EDL_ERR_ARG;
+    cudaSetDevice(c->device);
+    cudaError_t e = cudaStreamSynchronize(c->st);
+    if (e == cudaSuccess && c->st2) e = cudaStreamSynchronize(c->st2);
+    if (e == cudaSuccess && c->cst) e = cudaStreamSynchronize(c->cst);
+    if (e != cudaSuccess) return fail(c, EDL_ERR_CUDA, cudaGetErrorString(e));
+    return cuda_check(c, "ctx_sync");
 }
 
 // ---- NEXT f1: Galois rotations and plaintext vectors ----

@@ -124,6 +124,13 @@ _sigs = {
     "edl_cts_pack_c0": (_c.c_int32, [_c.c_void_p, _P(Cts), _c.c_void_p]),
     "edl_cts_unpack_seeded": (_c.c_int32, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int32, _c.c_double,
                                            _c.c_uint64, _c.c_uint64, _c.c_uint32, _P(Cts)]),
+    "edl_wire_upload": (_c.c_int32, [_c.c_void_p, _c.c_int32, _c.c_void_p, _c.c_size_t]),
+    "edl_cts_unpack_host": (_c.c_int32, [_c.c_void_p, _c.c_int32, _c.c_int64, _c.c_int32, _c.c_double, _c.c_uint64,
+                                         _P(Cts)]),
+    "edl_cts_unpack_seeded_host": (_c.c_int32, [_c.c_void_p, _c.c_int32, _c.c_int64, _c.c_int32, _c.c_double,
+                                                _c.c_uint64, _c.c_uint64, _c.c_uint32, _P(Cts)]),
+    "edl_cts_download": (_c.c_int32, [_c.c_void_p, _P(Cts), _c.c_void_p]),
+    "edl_ctx_sync": (_c.c_int32, [_c.c_void_p]),
     "edl_decrypt_poly": (_c.c_int32, [_c.c_void_p, _P(Cts), _c.c_void_p]),
     "edl_decrypt": (_c.c_int32, [_c.c_void_p, _P(Cts), _c.c_void_p, _c.c_int64]),
     "edl_ct_add": (_c.c_int32, [_c.c_void_p, _P(Cts), _P(Cts), _P(Cts)]),
@@ -568,6 +575,42 @@ class Context:
         self._check(_lib.edl_cts_unpack_seeded(self._h, ctypes.c_void_p(packed.data_ptr()), count, level, scale,
                                                key_id, enc_seed, obj0, ctypes.byref(co)), "cts_unpack_seeded")
         return o.update(co)
+
+    # ---- host wire path (host buffers in, host buffers out)
+    def wire_upload(self, slot: int, host) -> None:
+        """Queue the copy of a host buffer (pinned torch tensor or numpy array of 8-byte words)
+        into staging slot `slot` on the context's copy stream."""
+        if isinstance(host, np.ndarray):
+            ptr, nbytes = host.ctypes.data, host.nbytes
+        else:
+            ptr, nbytes = host.data_ptr(), host.numel() * host.element_size()
+        self._check(_lib.edl_wire_upload(self._h, slot, ctypes.c_void_p(ptr), nbytes), "wire_upload")
+
+    def unpack_host(self, slot: int, count: int, level: int, scale: float, key_id: int,
+                    out: Optional[CtArray] = None) -> CtArray:
+        o = out if out is not None else self.empty(count, level)
+        co = o.cts()
+        self._check(_lib.edl_cts_unpack_host(self._h, slot, count, level, scale, key_id, ctypes.byref(co)),
+                    "cts_unpack_host")
+        return o.update(co)
+
+    def unpack_seeded_host(self, slot: int, count: int, level: int, scale: float, key_id: int, enc_seed: int,
+                           obj0: int = 0, out: Optional[CtArray] = None) -> CtArray:
+        o = out if out is not None else self.empty(count, level)
+        co = o.cts()
+        self._check(_lib.edl_cts_unpack_seeded_host(self._h, slot, count, level, scale, key_id, enc_seed, obj0,
+                                                    ctypes.byref(co)), "cts_unpack_seeded_host")
+        return o.update(co)
+
+    def download(self, x: CtArray, host) -> None:
+        """Queue the device -> host copy of a ciphertext array into `host` (pinned tensor / numpy
+        array of at least count * 2 * (level + 1) * N words); valid after sync()."""
+        ptr = host.ctypes.data if isinstance(host, np.ndarray) else host.data_ptr()
+        c = x.cts()
+        self._check(_lib.edl_cts_download(self._h, ctypes.byref(c), ctypes.c_void_p(ptr)), "cts_download")
+
+    def sync(self) -> None:
+        self._check(_lib.edl_ctx_sync(self._h), "ctx_sync")
 
     def mod_reduce(self, x: CtArray) -> CtArray:
         c = x.cts()

@@ -563,6 +563,49 @@ def test_wire_format_pack_unpack(c1pair, level):
     assert np.array_equal(y.numpy(g.n), A)
 
 
+def test_host_wire_path(c1pair):
+    """C-ABI host-buffer path (edl_wire_upload / edl_cts_unpack_host / edl_cts_unpack_seeded_host /
+    edl_cts_download / edl_ctx_sync): wire bytes in pinned HOST memory -> device array ==
+    the oracle's residues, for both slots, slot reuse without synchronisation in between,
+    public-key and seeded secret-key formats; downloaded bytes == the device array; errors."""
+    import torch
+    g, o = c1pair
+    lvl = 3
+    A = [_rand_ct(o, 3, lvl, 170 + k) for k in range(3)]
+    hosts = []
+    for a_ in A:
+        dev = g.pack(_to_gpu(g, a_, lvl, 2.0 ** 40, o.key_id))
+        h = torch.empty(dev.numel(), dtype=torch.int64, pin_memory=True)
+        h.copy_(dev.cpu())
+        hosts.append(h)
+    outs = []
+    for k, h in enumerate(hosts):               # slots 0, 1, 0: the third upload reuses slot 0
+        g.wire_upload(k % 2, h)
+        outs.append(g.unpack_host(k % 2, 3, lvl, 2.0 ** 40, o.key_id))
+    back = torch.empty(outs[2].tensor.numel(), dtype=torch.int64, pin_memory=True)
+    g.download(outs[2], back)
+    g.sync()
+    for a_, y in zip(A, outs):
+        assert y.count == 3 and y.level == lvl and np.array_equal(y.numpy(g.n), a_)
+    assert np.array_equal(back.numpy().view(np.uint64).reshape(A[2].shape), A[2])
+    # seeded secret-key wire: c0 from the host, c1 regenerated on the device
+    polys = np.random.default_rng(23).integers(-2 ** 40, 2 ** 40, (2, o.n))
+    xs = g.encrypt_poly_sk(polys, scale=2.0 ** 40, enc_seed=9, obj0=4)
+    c0 = g.pack_c0(xs)
+    hc = torch.empty(c0.numel(), dtype=torch.int64, pin_memory=True)
+    hc.copy_(c0.cpu())
+    g.wire_upload(1, hc)
+    ys = g.unpack_seeded_host(1, 2, xs.level, xs.scale, xs.key_id, enc_seed=9, obj0=4)
+    g.sync()
+    assert np.array_equal(ys.numpy(g.n), o.encrypt_poly_sk(polys, enc_seed=9, obj0=4, scale=2.0 ** 40).data)
+    # a slot holding fewer bytes than the array needs, and a bad slot
+    g.wire_upload(0, hc)
+    with pytest.raises(Exception):
+        g.unpack_host(0, 3, lvl, 2.0 ** 40, o.key_id)
+    with pytest.raises(Exception):
+        g.wire_upload(2, hc)
+
+
 # ---------------------------------------------------------------- NEXT f1: rotations, plaintext vectors
 @pytest.fixture(scope="module")
 def f1pair(c1pair):
