@@ -47,7 +47,7 @@ def _args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-c2", action="store_true", help="skip the C2 microbench sweep")
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 tabular net")
-    ap.add_argument("--inflight", type=int, default=2,
+    ap.add_argument("--inflight", type=int, default=4,
                     help="N=1: batches in flight (consecutive steps alternate over this many contexts, each "
                          "with its own stream pair and scratch); 1 = one batch at a time")
     return ap.parse_args()
