@@ -685,7 +685,7 @@ def run_ours(a):
         sys.path.insert(0, os.path.join(ROOT, "tools"))
         if not a.no_c3:
             from c3_bench import run_c3
-            c3 = run_c3(5)
+            c3 = run_c3(5, max(1, a.inflight))
             c3["config_index"] = 3
         if not a.no_c2:
             from c2_bench import point
