@@ -91,6 +91,11 @@ edl_status edl_params_from_bits(int32_t log_n, const int32_t* bits, int32_t n_bi
 /* Bytes of a ciphertext array: 2 * (level+1) * 2^log_n * 8 * count. */
 size_t edl_cts_bytes(int64_t count, int32_t level, int32_t log_n);
 
+/* Environment switches read at context creation (diagnostics; results never change):
+ * EDL_NVTX=1 wraps every layer-level call in an NVTX range named after the call; EDL_PDL=0
+ * turns programmatic dependent launch off; EDL_KS_SPLIT=0 keeps key switches on one stream;
+ * EDL_KS_FUSED=1 / EDL_RAISE_FUSED=1 / EDL_KS_CHUNK=<n> select measured-and-rejected key-switch
+ * variants. */
 /* Create a context on CUDA `device`, enqueueing on `cuda_stream` (a cudaStream_t; NULL =
  * legacy default stream).  Uploads twiddle tables.  log_n must be in [10, 16] (N > 2^13
  * runs one limb per thread-block cluster) and compiled into the build (EDL_LOGNS_MASK);

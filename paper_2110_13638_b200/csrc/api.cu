@@ -3,6 +3,7 @@
 // orchestration on the context's stream.  No arithmetic on ciphertexts happens here:
 // every residue is produced by the sm_100a kernels in *.cu.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>   // header-only; ranges are emitted only with EDL_NVTX=1
 
 #include <cfenv>
 #include <cstdlib>
@@ -77,6 +78,8 @@ struct edl_ctx {
     int64_t ks_chunk = 0;
     // d2 INTT + modulus raise in one kernel (EDL_RAISE_FUSED=1, N = 2^14)
     bool raise_fused = false;
+    // EDL_NVTX=1: an NVTX range around every layer-level C-ABI call (ncu --nvtx filters, timelines)
+    bool nvtx = false;
     // EDL_KS_SPLIT=0: key switches as one launch sequence on the main stream instead of two
     // halves on the two streams (experiments with several contexts in flight)
     bool ks_split = true;
@@ -287,6 +290,19 @@ void relin_split(edl_ctx* c, const Dev& d, const uint64_t* a, const uint64_t* b,
     cudaStreamWaitEvent(c->st, c->join, 0);
 }
 
+// NVTX range over one C-ABI call (host side: the kernels it launches fall inside it on a timeline
+// and under `ncu --nvtx --nvtx-include <name>/`); a no-op unless the context was created with
+// EDL_NVTX=1.
+struct NvtxRange {
+    bool on;
+    NvtxRange(const edl_ctx* c, const char* name) : on(c && c->nvtx) {
+        if (on) nvtxRangePushA(name);
+    }
+    ~NvtxRange() {
+        if (on) nvtxRangePop();
+    }
+};
+
 bool scales_match(double a, double b) { return std::fabs(a - b) <= std::ldexp(1.0, -30) * std::fmax(a, b); }
 
 // O10: a constant encodes to rint(value * scale) (one IEEE multiply, round-half-even).
@@ -403,6 +419,8 @@ edl_status edl_ctx_create(const edl_params* p, int32_t device, void* stream, edl
         c->raise_fused = rf && rf[0] == '1';
         const char* k = std::getenv("EDL_KS_CHUNK");
         c->ks_chunk = k ? std::atoll(k) : 0;
+        const char* nv = std::getenv("EDL_NVTX");
+        c->nvtx = nv && nv[0] == '1';
         const char* sp = std::getenv("EDL_KS_SPLIT");
         c->ks_split = !(sp && sp[0] == '0');
     }
@@ -636,6 +654,7 @@ edl_status edl_encode(edl_ctx* c, const double* slots, int64_t n_vec, int64_t n_
 
 edl_status edl_encrypt_poly(edl_ctx* c, const int64_t* poly, int64_t n_vec, int32_t level, double scale,
                             uint64_t enc_seed, uint32_t obj0, edl_cts* out) {
+    NvtxRange nvtx_(c, "edl_encrypt_poly");
     if (!c || !out || (!poly && n_vec > 0) || n_vec < 0) return fail(c, EDL_ERR_ARG, "encrypt: bad arguments");
     if (!c->has_key) return fail(c, EDL_ERR_NOKEY, "encrypt: no key");
     if (level < 0 || level > c->L) return fail(c, EDL_ERR_LEVEL, "encrypt: level out of range");
@@ -649,6 +668,7 @@ edl_status edl_encrypt_poly(edl_ctx* c, const int64_t* poly, int64_t n_vec, int3
 
 edl_status edl_encrypt_poly_sk(edl_ctx* c, const int64_t* poly, int64_t n_vec, int32_t level, double scale,
                                uint64_t enc_seed, uint32_t obj0, edl_cts* out) {
+    NvtxRange nvtx_(c, "edl_encrypt_poly_sk");
     if (!c || !out || (!poly && n_vec > 0) || n_vec < 0) return fail(c, EDL_ERR_ARG, "encrypt_sk: bad arguments");
     if (!c->has_key) return fail(c, EDL_ERR_NOKEY, "encrypt_sk: no key");
     if (level < 0 || level > c->L) return fail(c, EDL_ERR_LEVEL, "encrypt_sk: level out of range");
@@ -815,6 +835,7 @@ edl_status edl_mod_drop(edl_ctx* c, const edl_cts* in, int32_t level, edl_cts* o
 }
 
 edl_status edl_rescale(edl_ctx* c, const edl_cts* in, edl_cts* out) {
+    NvtxRange nvtx_(c, "edl_rescale");
     if (!c || !out) return EDL_ERR_ARG;
     edl_status s = check_ct(c, in);
     if (s != EDL_OK) return s;
@@ -832,6 +853,7 @@ edl_status edl_rescale(edl_ctx* c, const edl_cts* in, edl_cts* out) {
 }
 
 edl_status edl_ct_ct_mul_relin(edl_ctx* c, const edl_cts* a, const edl_cts* b, edl_cts* out) {
+    NvtxRange nvtx_(c, "edl_ct_ct_mul_relin");
     if (!c || !out) return EDL_ERR_ARG;
     if (!c->has_key) return fail(c, EDL_ERR_NOKEY, "mul_relin: no relinearisation key");
     edl_status s;
@@ -867,6 +889,7 @@ edl_status edl_ct_ct_mul_relin(edl_ctx* c, const edl_cts* a, const edl_cts* b, e
 
 edl_status edl_cross_correlate(edl_ctx* c, const edl_cts* x, int32_t H, int32_t W, const double* k, int32_t F,
                                int32_t kh, int32_t kw, int32_t stride, const double* bias, edl_cts* out) {
+    NvtxRange nvtx_(c, "edl_cross_correlate");
     if (!c || !out || !k) return EDL_ERR_ARG;
     edl_status s = check_ct(c, x);
     if (s != EDL_OK) return s;
@@ -906,6 +929,7 @@ edl_status edl_cross_correlate(edl_ctx* c, const edl_cts* x, int32_t H, int32_t 
 
 edl_status edl_dense(edl_ctx* c, const edl_cts* x, const double* Wt, const double* b, int32_t O,
                      int32_t defer_rescale, edl_cts* out) {
+    NvtxRange nvtx_(c, "edl_dense");
     if (!c || !out || !Wt || O <= 0) return EDL_ERR_ARG;
     edl_status s = check_ct(c, x);
     if (s != EDL_OK) return s;
@@ -980,6 +1004,7 @@ edl_status edl_cts_pack(edl_ctx* c, const edl_cts* in, void* packed) {
 
 edl_status edl_cts_unpack(edl_ctx* c, const void* packed, int64_t count, int32_t level, double scale, uint64_t key_id,
                           edl_cts* out) {
+    NvtxRange nvtx_(c, "edl_cts_unpack");
     if (!c || !out || count < 0) return EDL_ERR_ARG;
     if (level < 0 || level > c->L) return fail(c, EDL_ERR_ARG, "cts_unpack: level out of range");
     if (count > 0 && (!packed || !out->data)) return fail(c, EDL_ERR_ARG, "cts_unpack: null buffer");
@@ -1011,6 +1036,7 @@ edl_status edl_cts_pack_c0(edl_ctx* c, const edl_cts* in, void* packed) {
 
 edl_status edl_cts_unpack_seeded(edl_ctx* c, const void* packed, int64_t count, int32_t level, double scale,
                                  uint64_t key_id, uint64_t enc_seed, uint32_t obj0, edl_cts* out) {
+    NvtxRange nvtx_(c, "edl_cts_unpack_seeded");
     if (!c || !out || count < 0) return EDL_ERR_ARG;
     if (level < 0 || level > c->L) return fail(c, EDL_ERR_ARG, "cts_unpack_seeded: level out of range");
     if (count > 0 && (!packed || !out->data)) return fail(c, EDL_ERR_ARG, "cts_unpack_seeded: null buffer");
@@ -1144,6 +1170,7 @@ edl_status edl_galois_keygen(edl_ctx* c, uint64_t seed, const int32_t* steps, in
 }
 
 edl_status edl_rotate(edl_ctx* c, const edl_cts* in, int32_t steps, edl_cts* out) {
+    NvtxRange nvtx_(c, "edl_rotate");
     if (!c || !out) return EDL_ERR_ARG;
     edl_status s = check_ct(c, in);
     if (s != EDL_OK) return s;
@@ -1170,6 +1197,7 @@ edl_status edl_rotate(edl_ctx* c, const edl_cts* in, int32_t steps, edl_cts* out
 }
 
 edl_status edl_rotate_hoisted(edl_ctx* c, const edl_cts* in, const int32_t* steps, int32_t n_steps, edl_cts* outs) {
+    NvtxRange nvtx_(c, "edl_rotate_hoisted");
     if (!c || n_steps < 0 || (n_steps > 0 && (!steps || !outs))) return EDL_ERR_ARG;
     edl_status s = check_ct(c, in);
     if (s != EDL_OK) return s;
@@ -1300,6 +1328,7 @@ edl_status edl_mod_reduce(edl_ctx* c, edl_cts* x) {
 }
 
 edl_status edl_dense_finish(edl_ctx* c, const edl_cts* acc, const double* b, edl_cts* out) {
+    NvtxRange nvtx_(c, "edl_dense_finish");
     if (!c || !out) return EDL_ERR_ARG;
     edl_status s = check_ct(c, acc);
     if (s != EDL_OK) return s;
@@ -1324,6 +1353,7 @@ edl_status edl_dense_finish(edl_ctx* c, const edl_cts* acc, const double* b, edl
 }
 
 edl_status edl_poly_activation(edl_ctx* c, const edl_cts* x, const double* coeffs, int32_t degree, edl_cts* out) {
+    NvtxRange nvtx_(c, "edl_poly_activation");
     if (!c || !out || !coeffs) return EDL_ERR_ARG;
     if (!c->has_key) return fail(c, EDL_ERR_NOKEY, "poly_activation: no relinearisation key");
     edl_status s = check_ct(c, x);
